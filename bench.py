@@ -1,0 +1,522 @@
+#!/usr/bin/env python
+"""MoE-layer tokens/s under predicted-expert residency (BASELINE.json metric).
+
+Default workload = BASELINE config 2: Mixtral-8x7B-shaped MoE layer, bf16,
+8 experts top-2, 4 resident experts (predicted), batch 32 x 2048 tokens on one
+B200.  One step = one pass of the hot path over that batch:
+    gate + top-k + residency remap (K1) -> scan + stable permute (K3)
+    -> grouped SwiGLU GEMM1 + GEMM2 on tcgen05 (K4) -> combine (K5)
+    -> popularity-histogram update over the batch's routing (K2, A6)
+The resident set comes from the reference flow run on the GPU: routing trace
+(the reference's Markov generator, seed 17, calibration 0.6 / 0.8), fit on
+200 training prompts, predict_all_layers from the previous prompt, Eq. 2 over
+the 32 queued prompts, loading_targets + plan_loading, and the planned H2D
+loads from pinned host memory.  Activations are synthesised so that the gate
+(computed from x) reproduces the trace's routing.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config mixtral|switch]
+Under torchrun (N > 1) each rank runs an independent replica on its own 65,536
+tokens (weak scaling, no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MoE-layer tokens/sec (predicted-expert residency) at 1/2/4/8 B200; % roofline"
+
+CONFIGS = {
+    "mixtral": dict(workload="BASELINE config 2: Mixtral-8x7B-shaped MoE layer bf16, 8 experts top-2, 4 resident "
+                             "(predicted), batch 32 x 2048 tokens",
+                    E=8, k=2, L=4, d=4096, f=14336, act="swiglu", wm="topk_softmax", prompts=32, tokens=2048,
+                    train=200, layer_lambda=0.6, prompt_lambda=0.8, seed=17),
+    "switch": dict(workload="BASELINE config 3: Switch-base-128-shaped layer bf16, 128 experts top-1, 20% resident "
+                            "(L=26, predicted), 32 x 2048 tokens",
+                   E=128, k=1, L=26, d=768, f=3072, act="relu", wm="full_softmax", prompts=32, tokens=2048,
+                   train=200, layer_lambda=0.6, prompt_lambda=0.8, seed=17),
+}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return dict(hbm=d.get("hbm_gbs", 6650.0), bf16=d.get("bf16_tflops", 1590.0),
+                    bf16_sustained=d.get("bf16_tflops_sustained", 1400.0), source="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sustained=1400.0, source="fallback")
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# synthetic workload
+# ---------------------------------------------------------------------------
+def build_workload(cfg, device):
+    import torch
+
+    import paper_2503_06823_b200 as emoe
+    from paper_2503_06823_b200 import MoELayer
+
+    E, k, L, d, f = cfg["E"], cfg["k"], cfg["L"], cfg["d"], cfg["f"]
+    P, Tp, P_train = cfg["prompts"], cfg["tokens"], cfg["train"]
+    T = P * Tp
+    shape = emoe.ModelShape(1, E, k, expert_bytes=(3 if cfg["act"] == "swiglu" else 2) * d * f * 2)
+    trace = emoe.gen_routing_trace(shape, cfg["layer_lambda"], cfg["prompt_lambda"], 0, cfg["seed"], P_train + P, Tp)
+    train, serve = trace[:P_train], trace[P_train:]
+
+    # ---- predictor flow on the GPU (fit -> predict -> Eq. 2 -> targets -> plan)
+    pred = emoe.moesim._Pred(1, E, k, 1, 0.01)
+    dtrain = torch.from_numpy(np.ascontiguousarray(train)).to(device)
+    tid = torch.zeros(P_train, dtype=torch.int32, device=device)
+    emoe.moesim.check(emoe._lib.lib.emoe_hist_update(pred.h, emoe.moesim.C.c_void_p(dtrain.data_ptr()), P_train, Tp,
+                                                     emoe.moesim.C.c_void_p(tid.data_ptr()), None))
+    _, sets = emoe.prompt_expert_sets(train, P_train - 1)
+    set_arr, sizes = emoe.moesim._sets_array(sets, k)
+    wo = np.array([128.0])
+    sens = np.ones((1, 1), np.int32)
+    has = np.ones(1, np.uint8)
+    req_task = np.zeros(P, np.int32)
+    req_tok = np.full(P, Tp, np.int32)
+    resident0 = np.zeros((1, E), np.uint8)
+    budgets = np.array([L], np.int32)
+    agg = np.zeros((1, E))
+    ev = np.full((1, E), -1, np.int32)
+    ld = np.full((1, E), -1, np.int32)
+    ne = np.zeros(1, np.int32)
+    nl = np.zeros(1, np.int32)
+    de = np.zeros(1)
+    p_ = emoe.moesim._p
+    emoe.moesim.check(emoe._lib.lib.emoe_invocation_host(
+        pred.h, 0, p_(set_arr), p_(sizes), 1, p_(wo), p_(sens), p_(has), P, p_(req_task), p_(req_tok), 1,
+        p_(resident0), p_(budgets), 0.0, p_(agg), p_(ev), p_(ne), p_(ld), p_(nl), p_(de)))
+    loads = [int(e) for e in ld[0, : nl[0]]]
+
+    # ---- layer, weights (random-init, Mixtral/Switch shapes), planned loads
+    layer = MoELayer(d, f, E, k, activation=cfg["act"], dtype="bf16", weight_mode=cfg["wm"], num_slots=L,
+                     max_tokens=T)
+    g = torch.Generator(device=device).manual_seed(1234)
+    q, _ = torch.linalg.qr(torch.randn(d, E, generator=g, device=device))  # orthonormal gate rows
+    wg = q.T.contiguous()
+    layer.set_gate(wg.to(torch.bfloat16).cpu())
+    for e in range(E):
+        w1 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(torch.bfloat16).cpu()
+        w3 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(torch.bfloat16).cpu() \
+            if cfg["act"] == "swiglu" else None
+        w2 = (torch.randn(d, f, generator=g, device=device) / f ** 0.5).to(torch.bfloat16).cpu()
+        layer.register_expert(e, w1, w3, w2)
+    layer.begin_load([], loads)
+    layer.poll_loads(blocking=True)
+    load_bytes, load_ms = layer.last_load_stats()
+    torch.cuda.synchronize()
+
+    # ---- activations whose gate logits reproduce the serving trace
+    choices = serve.reshape(T, k)  # [P][1][Tp][k] -> token-major
+    lg = torch.rand(T, E, generator=g, device=device) * 8.0 - 4.0
+    lg = torch.round(lg * 64) / 64
+    ch = torch.from_numpy(np.ascontiguousarray(choices)).to(device).long()
+    for r in range(k):
+        lg.scatter_(1, ch[:, r:r + 1], 8.0 - r)
+    z = torch.randn(T, d, generator=g, device=device)
+    z = z - (z @ wg.T) @ wg
+    x = (lg @ wg + z).to(torch.bfloat16).contiguous()
+    del z, lg
+    info = dict(trace=trace, loads=loads, aggregate=agg[0].tolist(), load_bytes=load_bytes, load_ms=load_ms,
+                choices=choices, resident=layer.residency().tolist())
+    return layer, pred, x, info
+
+
+def cpu_reference_step(cfg, layer_info, x_host_f32, wg_f32, experts_f32, n_tokens, port, ref, threads):
+    """One bounded CPU step of the same workload: the reference's route_token
+    (oracle/_ref, single thread) + the oracle port of gate/permute/FFN/combine
+    (pthreads over all host cores).  Returns seconds."""
+    E, k = cfg["E"], cfg["k"]
+    resident = np.zeros(E, np.uint8)
+    resident[np.asarray(layer_info["resident"], bool)] = 1
+    x = x_host_f32[:n_tokens]
+    t0 = time.perf_counter()
+    logits = port.gate_logits(x, wg_f32)
+    o = port.gate_route(logits, k, 0 if cfg["wm"] == "topk_softmax" else 1, resident)
+    if ref is not None:
+        ref.route_tokens(o["topk_idx"], resident)
+    counts, offsets, pos, src = port.permute(o["served_idx"], E, 1)
+    Y = np.zeros((int(offsets[-1]), cfg["d"]), np.float32)
+    for e in range(E):
+        rows = np.arange(offsets[e], offsets[e + 1])
+        if rows.size == 0:
+            continue
+        w1, w3, w2 = experts_f32[e]
+        Y[rows] = port.expert_ffn(x[src[rows]], w1, w3, w2, 0 if cfg["act"] == "swiglu" else 1, True, threads)
+    port.combine(Y, pos, o["served_w"], True)
+    return time.perf_counter() - t0
+
+
+def cpu_setup(cfg, layer, x, n_tokens):
+    """Host copies (fp32) of the first n_tokens of x and of the resident experts' weights."""
+    from oracle.oracle import Port, Ref, have_ref
+
+    port = Port()
+    ref = Ref() if have_ref() else None
+    xs = x[:n_tokens].float().cpu().numpy()
+    return port, ref, xs
+
+
+def run_cpu_baseline(cfg, layer, x, info, target_s=10.0):
+    import torch
+
+    from oracle.oracle import Port, Ref, have_ref
+
+    port = Port()
+    ref = Ref() if have_ref() else None
+    threads = port.threads()
+    E = cfg["E"]
+    wg = layer_gate_f32(layer)
+    experts = layer_experts_f32(layer)
+    # calibrate the sample so the timed CPU work is ~target_s
+    n = 8
+    xs = x[:4096].float().cpu().numpy()
+    dt = cpu_reference_step(cfg, info, xs, wg, experts, n, port, ref, threads)
+    n = int(max(8, min(4096, n * target_s / max(dt, 1e-3))))
+    dt = cpu_reference_step(cfg, info, xs, wg, experts, n, port, ref, threads)
+    rt_ns = None
+    if ref is not None:
+        choices = info["choices"]
+        res = np.zeros(E, np.uint8)
+        res[np.asarray(info["resident"], bool)] = 1
+        rt_ns, _ = ref.time_route_tokens(choices, res, reps=3)
+    return dict(value=n / dt, unit="tokens/s", cores=threads, kind="port",
+                sample=f"{n} of {x.shape[0]} tokens through the full CPU path: oracle port (C, {threads} pthreads) "
+                       f"gate+top-k, permute, SwiGLU/ReLU FFN (fp64 accumulate), combine; reference route_token "
+                       f"(oracle/_ref, 1 thread) {'%.2f ns/token' % rt_ns if rt_ns else 'n/a'}",
+                seconds=dt)
+
+
+_HOST_CACHE = {}
+
+
+def layer_gate_f32(layer):
+    return _HOST_CACHE["wg"]
+
+
+def layer_experts_f32(layer):
+    return _HOST_CACHE["experts"]
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="emoe", choices=["emoe", "reference"])
+    ap.add_argument("--config", default="mixtral", choices=list(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl" if args.impl == "emoe" else "gloo")
+    if args.impl == "reference":
+        return main_reference(args, cfg, rank, world)
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    import paper_2503_06823_b200 as emoe
+    from paper_2503_06823_b200 import _lib
+
+    layer, pred, x, info = build_workload(cfg, device)
+    T = x.shape[0]
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+    P, Tp = cfg["prompts"], cfg["tokens"]
+    tid = torch.zeros(P, dtype=torch.int32, device=device)
+    import ctypes as C
+
+    def step():
+        layer.forward(x, out=y)
+        ws_topk = layer_ws_topk(layer)
+        emoe.moesim.check(_lib.lib.emoe_hist_update(pred.h, C.c_void_p(ws_topk), P, Tp, C.c_void_p(tid.data_ptr()),
+                                                    C.c_void_p(stream.cuda_stream)))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ws = layer.workspace()
+    counts = ws["counts"].cpu().numpy()
+    S = int(counts.sum())
+    hit_rate = float(ws["route_hit"].float().mean().item())
+    fallback = float((ws["route_rank"] == -1).float().mean().item())
+
+    layer.set_profiling(True)
+    launches0 = _lib.lib.emoe_kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = int(_lib.lib.emoe_kernel_launches() - launches0)
+    stages = layer.stage_times()
+    layer.set_profiling(False)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * T / (ms / 1e3)
+
+    # ---- end to end through the public host-buffer API (H2D x + D2H y every step)
+    x_host = x.cpu().pin_memory()
+    y_host = torch.empty_like(x_host).pin_memory()
+    for _ in range(2):
+        layer.forward_host(x_host, y_host)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        layer.forward_host(x_host, y_host)
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = dict(value=world * T / e2e_s, unit="tokens/s", h2d_bytes_per_step=x_host.numel() * 2,
+               d2h_bytes_per_step=y_host.numel() * 2, ms_per_step=e2e_s * 1e3)
+
+    # ---- roofline of the dominant kernel (the grouped FFN GEMMs)
+    peaks = load_peaks()
+    d, f = cfg["d"], cfg["f"]
+    nmat = 3 if cfg["act"] == "swiglu" else 2
+    ffn_flops = 2.0 * nmat * d * f * S
+    ffn_ms = stages["gemm1"] + stages["gemm2"]
+    achieved = ffn_flops / (ffn_ms / 1e3) / 1e12
+    roofline = dict(bound="tensor", achieved=round(achieved, 1), peak=peaks["bf16_sustained"], unit="TFLOP/s",
+                    frac=round(achieved / peaks["bf16_sustained"], 4), traffic=None,
+                    kernel="grouped_gemm_kernel (K4: GEMM1 SwiGLU + GEMM2), avg of the timed steps",
+                    algorithmic=f"2*{nmat}*d*f*S = {ffn_flops:.4g} FLOP per step (S={S} served rows)",
+                    peak_kind=f"bf16_tflops_sustained ({peaks['source']}); burst {peaks['bf16']}",
+                    frac_of_burst=round(achieved / peaks["bf16"], 4))
+    hbm_stages = {}
+    xb = T * d * 2
+    hbm_stages["route"] = (xb + T * k_of(cfg) * 8 + T * 9) / (stages["route"] / 1e3) / 1e9
+    hbm_stages["permute"] = (xb + S * d * 2 + 8 * S) / (stages["permute"] / 1e3) / 1e9
+    hbm_stages["combine"] = (S * d * 2 + xb + 4 * S) / (stages["combine"] / 1e3) / 1e9
+
+    out = dict(metric=METRIC, value=round(value, 1), unit="tokens/s", n_gpus=world, steps=args.steps,
+               warmup=args.warmup, ms_per_step=round(ms, 4), higher_is_better=True, scaling="weak",
+               vs_baseline=None, dtype="bf16", data="synthetic (random-init weights; routing = reference Markov "
+                                                     "trace embedded in x)",
+               config=dict(workload=cfg["workload"], tokens_per_step=T, num_experts=cfg["E"], top_k=cfg["k"],
+                           resident_experts=cfg["L"], resident_set=[e for e in range(cfg["E"])
+                                                                     if info["resident"][e]],
+                           d_model=d, d_ff=f, activation=cfg["act"], served_rows=S, hit_rate=round(hit_rate, 4),
+                           fallback_rate=round(fallback, 4),
+                           l2="inputs larger than L2: x is %.0f MB per step" % (xb / 1e6),
+                           parallelism=f"replicas{world}" if world > 1 else "single"),
+               roofline=roofline, e2e=e2e, gpu_launches=launches, clocks=clk.summary(),
+               stages_ms={kk: round(v, 4) for kk, v in stages.items()},
+               stage_hbm_gbs={kk: round(v, 1) for kk, v in hbm_stages.items()},
+               expert_load=dict(bytes=info["load_bytes"], ms=round(info["load_ms"], 3),
+                                h2d_gbs=round(info["load_bytes"] / max(info["load_ms"], 1e-9) / 1e6, 2),
+                                experts=info["loads"]))
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        _HOST_CACHE["wg"] = gate_f32(layer_gate_tensor(cfg, device))
+        _HOST_CACHE["experts"] = experts_f32(cfg, device, info)
+        out["cpu_baseline"] = run_cpu_baseline(cfg, layer, x, info)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def k_of(cfg):
+    return cfg["k"]
+
+
+def layer_ws_topk(layer):
+    from paper_2503_06823_b200._lib import Workspace, lib
+    import ctypes as C
+
+    w = Workspace()
+    lib.emoe_layer_workspace(layer.h, C.byref(w))
+    return w.topk_idx
+
+
+def layer_gate_tensor(cfg, device):
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(1234)
+    q, _ = torch.linalg.qr(torch.randn(cfg["d"], cfg["E"], generator=g, device=device))
+    return q.T.contiguous().to(torch.bfloat16)
+
+
+def gate_f32(wg):
+    return wg.float().cpu().numpy()
+
+
+def experts_f32(cfg, device, info):
+    """Regenerate the resident experts' weights with the bench's generator stream."""
+    import torch
+
+    d, f, E = cfg["d"], cfg["f"], cfg["E"]
+    g = torch.Generator(device=device).manual_seed(1234)
+    torch.linalg.qr(torch.randn(d, E, generator=g, device=device))
+    out = {}
+    for e in range(E):
+        w1 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(torch.bfloat16)
+        w3 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(torch.bfloat16) \
+            if cfg["act"] == "swiglu" else None
+        w2 = (torch.randn(d, f, generator=g, device=device) / f ** 0.5).to(torch.bfloat16)
+        if info["resident"][e]:
+            out[e] = (w1.float().cpu().numpy(), None if w3 is None else w3.float().cpu().numpy(),
+                      w2.float().cpu().numpy())
+    return out
+
+
+def main_reference(args, cfg, rank, world):
+    """--impl reference: the reference's CPU implementation of the path on this
+    host's cores (oracle/_ref route_token + the oracle port of the parts the
+    reference does not have), on bounded samples of the same workload."""
+    if rank != 0:
+        return
+    import torch
+
+    from oracle.oracle import Port, Ref, have_ref
+
+    import paper_2503_06823_b200 as emoe
+
+    port = Port()
+    ref = Ref() if have_ref() else None
+    threads = port.threads()
+    E, k, d, f = cfg["E"], cfg["k"], cfg["d"], cfg["f"]
+    # same synthetic inputs as the GPU arm, regenerated on the CPU (no GPU needed)
+    shape = emoe.ModelShape(1, E, k)
+    trace = emoe.gen_routing_trace(shape, cfg["layer_lambda"], cfg["prompt_lambda"], 0, cfg["seed"],
+                                   cfg["train"] + cfg["prompts"], cfg["tokens"])
+    train = trace[: cfg["train"]]
+    model = port.fit(train, np.zeros(cfg["train"], np.int32), 1, E)
+    model["smoothing"] = 0.01
+    sets, sizes = port.prompt_expert_sets(train, cfg["train"] - 1)
+    scores, _, _ = port.predict(model, 0, sets, sizes, k=k)
+    fitted = port.predicted_frequencies(model["task_counts"], 0.01, 0)[None]
+    agg = port.invocation_aggregate(scores, fitted, [128.0], np.ones((1, 1), np.int32), [1],
+                                    np.zeros(cfg["prompts"], np.int32), np.full(cfg["prompts"], cfg["tokens"]))
+    targets = port.loading_targets(agg, np.zeros((1, E), np.uint8), [cfg["L"]])[0]
+    resident = [1 if e in targets else 0 for e in range(E)]
+    info = dict(resident=resident, choices=trace[cfg["train"]:].reshape(-1, k))
+    g = torch.Generator().manual_seed(4321)
+    n = 16
+    x = (torch.randn(4096, d, generator=g)).to(torch.bfloat16).float().numpy()
+    wg = (torch.randn(E, d, generator=g) / d ** 0.5).to(torch.bfloat16).float().numpy()
+    experts = {}
+    for e in range(E):
+        if resident[e]:
+            w1 = (torch.randn(f, d, generator=g) / d ** 0.5).to(torch.bfloat16).float().numpy()
+            w3 = (torch.randn(f, d, generator=g) / d ** 0.5).to(torch.bfloat16).float().numpy() \
+                if cfg["act"] == "swiglu" else None
+            w2 = (torch.randn(d, f, generator=g) / f ** 0.5).to(torch.bfloat16).float().numpy()
+            experts[e] = (w1, w3, w2)
+    # size the per-step sample so W+K steps finish within a few minutes
+    dt = cpu_reference_step(cfg, info, x, wg, experts, n, port, ref, threads)
+    budget_s = 150.0 / (args.steps + args.warmup)
+    n = int(max(4, min(4096, n * budget_s / max(dt, 1e-3))))
+    for _ in range(args.warmup):
+        cpu_reference_step(cfg, info, x, wg, experts, n, port, ref, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_reference_step(cfg, info, x, wg, experts, n, port, ref, threads)
+    s = (time.perf_counter() - t0) / args.steps
+    value = n / s
+    out = dict(metric=METRIC, impl="reference", value=round(value, 3), unit="tokens/s", n_gpus=world,
+               steps=args.steps, warmup=args.warmup, ms_per_step=round(s * 1e3, 3), higher_is_better=True,
+               scaling="weak", vs_baseline=None, dtype="fp32 (fp64 accumulate)", data="synthetic",
+               config=dict(workload=cfg["workload"], tokens_per_step=n, parallelism="cpu"),
+               cpu_baseline=dict(value=round(value, 3), unit="tokens/s", cores=threads, kind="port",
+                                 sample=f"{n} tokens per step of the {cfg['prompts']}x{cfg['tokens']} batch: "
+                                        "reference route_token (oracle/_ref) + oracle port gate/permute/FFN/combine"),
+               e2e=dict(value=round(value, 3), unit="tokens/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

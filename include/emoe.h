@@ -1,0 +1,242 @@
+/* emoe.h -- C ABI of the B200-native predicted-residency MoE layer.
+ *
+ * This is the drop-in boundary for the hot path of the reference `moesim`
+ * library (/root/reference/proj/core).  Every entry point names the reference
+ * interface it replaces (file:line, relative to /root/reference/proj/core).
+ * Signatures are plain C: pointers, sizes and opaque handles; no C++ or torch
+ * types.  A C++ compat layer with the exact `moesim::` signatures and the
+ * ctypes binding used by the Python host mirror sit on top.
+ *
+ * Conventions
+ *   - Return codes mirror the reference's exception split:
+ *       EMOE_OK                 0
+ *       EMOE_ERR_RUNTIME        1  CUDA / driver / allocation failure
+ *       EMOE_ERR_VALIDATION     2  moesim::ValidationError (types.hpp:11-14)
+ *       EMOE_ERR_INVARIANT      3  std::logic_error (expert_store.cpp:47-54, :213)
+ *     emoe_last_error() returns the thread-local message of the last failure.
+ *   - `_dev` pointers are device pointers and the call is stream-ordered on
+ *     `stream` (a cudaStream_t, NULL = legacy default stream).  `_host`
+ *     pointers are host memory and the call returns after results are on the
+ *     host.
+ *   - Element types: `dtype` 0 = bf16, 1 = fp32 for activations and weights;
+ *     routing outputs are int32 / uint8 / fp32; predictor state is fp64/int64.
+ *   - Threading: one handle per owning thread/stream (Placement mutation is
+ *     single-owner); distinct handles are independent.
+ */
+#ifndef EMOE_H
+#define EMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EMOE_OK 0
+#define EMOE_ERR_RUNTIME 1
+#define EMOE_ERR_VALIDATION 2
+#define EMOE_ERR_INVARIANT 3
+
+#define EMOE_DTYPE_BF16 0
+#define EMOE_DTYPE_F32 1
+#define EMOE_ACT_SWIGLU 0
+#define EMOE_ACT_RELU 1
+#define EMOE_WEIGHTS_TOPK_SOFTMAX 0 /* Mixtral: softmax over the served top-k logits */
+#define EMOE_WEIGHTS_FULL_SOFTMAX 1 /* Switch: full-softmax probability of the served expert */
+
+const char* emoe_last_error(void);
+int emoe_version(void);
+
+/* ========================================================================
+ * A2  route_token  (expert_store.hpp:101-111, expert_store.cpp:206-220)
+ * Batched: token t's ranked gate choices are choices[t*k .. t*k+k).
+ * resident: [E] 0/1 residency of the layer (Placement::resident_, :41).
+ * scores: [E] layer scores or NULL for the empty score vector.
+ * Returns EMOE_ERR_INVARIANT when a token needs the fallback and no expert is
+ * resident ("route_token: no resident experts at layer").
+ * ====================================================================== */
+int emoe_route_tokens_host(const int32_t* choices, int64_t T, int k, const uint8_t* resident, int E,
+                           const double* scores, int32_t* out_expert, int32_t* out_rank, uint8_t* out_hit);
+
+/* ========================================================================
+ * MoE layer handle: gate weights, HBM expert slot pool (budget L), residency
+ * table, pinned host copies of every expert, routing/permute workspace.
+ * ====================================================================== */
+typedef struct emoe_layer emoe_layer;
+
+typedef struct {
+  int d_model;     /* d */
+  int d_ff;        /* f */
+  int num_experts; /* E (ModelShape::experts_per_layer, types.hpp:19) */
+  int top_k;       /* k (ModelShape::top_k, types.hpp:20) */
+  int activation;  /* EMOE_ACT_* */
+  int dtype;       /* EMOE_DTYPE_* */
+  int weight_mode; /* EMOE_WEIGHTS_* */
+  int num_slots;   /* HBM expert slots = resident budget L (Placement::budget) */
+  int64_t max_tokens;
+  int forced_miss; /* 1: a layer with no resident expert serves nothing (engine.cpp:533-537) */
+} emoe_layer_config;
+
+int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out);
+int emoe_layer_destroy(emoe_layer* layer);
+
+/* gate weights W_g [E][d] (layer dtype), host memory */
+int emoe_layer_set_gate_host(emoe_layer* layer, const void* wg);
+/* expert e's weights, host memory, copied into library-owned pinned buffers:
+ * w1, w3: [f][d] (w3 ignored for ReLU), w2: [d][f]  (layer dtype) */
+int emoe_layer_register_expert_host(emoe_layer* layer, int expert, const void* w1, const void* w3, const void* w2);
+
+/* Layer scores used by the route_token fallback (the engine's last aggregate
+ * row, engine.cpp:529-531).  scores == NULL sets the empty score vector. */
+int emoe_layer_set_scores_host(emoe_layer* layer, const double* scores);
+
+/* ========================================================================
+ * A8  apply_plan_layer / engine load schedule (expert_store.cpp:197-200,
+ * engine.cpp:431-464).  Two-phase residency exactly as the engine:
+ * evictions take effect at load start (stream-ordered on `stream`), loads
+ * become resident at load completion.  The H2D copies of the loaded experts
+ * run on the layer's side copy stream from pinned host memory and overlap
+ * compute; emoe_layer_poll_loads() flips them resident once complete
+ * (blocking = 1 waits).  Loading a resident expert, evicting a non-resident
+ * one or exceeding the slot budget returns EMOE_ERR_INVARIANT
+ * (Placement::load/evict, expert_store.cpp:46-57).
+ * ====================================================================== */
+int emoe_layer_begin_load(emoe_layer* layer, const int32_t* evictions, int n_evictions, const int32_t* loads,
+                          int n_loads, void* stream);
+int emoe_layer_poll_loads(emoe_layer* layer, int blocking, void* stream, int* still_pending);
+/* residency as seen by compute: out[E] 0/1 (Placement::residents, :24) */
+int emoe_layer_residency(const emoe_layer* layer, uint8_t* out);
+/* bytes of the last completed load batch and its H2D time in ms */
+int emoe_layer_last_load_stats(const emoe_layer* layer, double* bytes, double* ms);
+
+/* ========================================================================
+ * A1-A5  MoE layer forward (replaces the engine iteration's route loop and
+ * cost model, engine.cpp:524-546).  x, y: [T][d] in the layer dtype.
+ * logits_in (optional): [T][E] fp32 precomputed gate logits (routing-driven
+ * parity mode); when NULL the gate is computed from x.
+ * ====================================================================== */
+int emoe_moe_forward(emoe_layer* layer, const void* x_dev, const float* logits_in_dev, void* y_dev, int64_t T,
+                     void* stream);
+/* Same through host buffers: H2D of x, forward, D2H of y; returns after y is on the host. */
+int emoe_moe_forward_host(emoe_layer* layer, const void* x_host, void* y_host, int64_t T, void* stream);
+
+/* Route only (A1 + A2): fills the workspace routing fields. */
+int emoe_route(emoe_layer* layer, const void* x_dev, const float* logits_in_dev, int64_t T, void* stream);
+
+/* Device pointers of the last forward's intermediates (valid until the next
+ * call on the layer).  Sizes: T tokens, R = rows_cap permuted rows. */
+typedef struct {
+  int64_t T;
+  int64_t rows_cap;
+  float* logits;          /* [T][E] */
+  int32_t* topk_idx;      /* [T][k] gate choices, rank order */
+  int32_t* route_expert;  /* [T] RouteResult.expert */
+  int32_t* route_rank;    /* [T] RouteResult.rank (-1 = fallback) */
+  uint8_t* route_hit;     /* [T] RouteResult.hit */
+  int32_t* served_idx;    /* [T][k] served experts, -1 = empty slot */
+  float* served_w;        /* [T][k] served gate weights */
+  int32_t* counts;        /* [E] served rows per expert */
+  int64_t* seg_offsets;   /* [E+1] padded segment starts */
+  int32_t* pos;           /* [T][k] permuted row of each served slot, -1 = none */
+  int32_t* row_token;     /* [R] source token of each permuted row, -1 = padding */
+  void* x_perm;           /* [R][d] */
+  void* h;                /* [R][f] */
+  void* y_perm;           /* [R][d] */
+  int32_t* slot_of_expert; /* [E] HBM slot, -1 = not resident */
+  uint8_t* resident;      /* [E] */
+} emoe_workspace;
+int emoe_layer_workspace(emoe_layer* layer, emoe_workspace* out);
+
+/* Measurement hooks (no reference counterpart): CUDA events between the
+ * forward's stages on the forward's stream; ms[5] = route, scan+permute,
+ * FFN GEMM1, FFN GEMM2, combine, averaged over the profiled forwards since
+ * the previous emoe_layer_stage_times call. */
+int emoe_layer_set_profiling(emoe_layer* layer, int enable);
+int emoe_layer_stage_times(emoe_layer* layer, float* ms);
+/* kernels launched by this library since load (gpu_launches evidence) */
+long long emoe_kernel_launches(void);
+
+/* ========================================================================
+ * A6-A8  predictor: popularity histograms over routing history, prediction,
+ * Eq. 2, resident-set selection and load planning.
+ * ====================================================================== */
+typedef struct emoe_predictor emoe_predictor;
+
+/* TransitionModel (predictor.hpp:25-38): m layers, E experts, top_k,
+ * smoothing; num_tasks labels (indices into the caller's lexicographically
+ * sorted task ids = std::map order). */
+int emoe_predictor_create(int num_layers, int num_experts, int top_k, int num_tasks, double smoothing,
+                          emoe_predictor** out);
+int emoe_predictor_destroy(emoe_predictor* pred);
+int emoe_predictor_reset(emoe_predictor* pred);
+
+/* fit (predictor.cpp:137-185) as an incremental histogram on the GPU.
+ * trace_dev: [P][m][T][k] int32 routing history, task_ids_dev: [P] or NULL.
+ * Successive calls continue the prompt chain, so fit over a concatenation
+ * equals the sum of the calls (counts commute, test_predictor.cpp:284-296). */
+int emoe_hist_update(emoe_predictor* pred, const int32_t* trace_dev, int P, int T, const int32_t* task_ids_dev,
+                     void* stream);
+/* Export the tallies (exact integers as doubles): layer [(m-1)][E][E],
+ * prompt [m][E][E], task [num_tasks][m][E]. */
+int emoe_predictor_counts_host(emoe_predictor* pred, double* layer_counts, double* prompt_counts,
+                               double* task_counts);
+/* Load tallies (e.g. from a saved TransitionModel). */
+int emoe_predictor_set_counts_host(emoe_predictor* pred, const double* layer_counts, const double* prompt_counts,
+                                   const double* task_counts);
+
+/* dominant_expert / prompt_expert_sets (workload.cpp:350-377) for one prompt
+ * of a device trace [P][m][T][k]: dominant [m], sets [m][k] (-1 padded), sizes [m]. */
+int emoe_prompt_expert_sets(const int32_t* trace_dev, int P, int m, int T, int k, int prompt, int32_t* dominant_host,
+                            int32_t* sets_host, int32_t* sizes_host, void* stream);
+
+/* predict_all_layers (mode 0) / predict_chained (mode 1) / predict_layerwise
+ * (mode 2, `layer`) (predictor.cpp:187-220).  prev_sets [m][k] + sizes [m].
+ * Outputs scores [m][E] and experts [m][k] (+ counts [m]). */
+int emoe_predict_host(emoe_predictor* pred, int mode, const int32_t* prev_sets, const int32_t* prev_sizes, int layer,
+                      double* scores, int32_t* experts, int32_t* n_experts);
+/* predicted_frequencies (predictor.cpp:222-238); task = -1 for an unseen task */
+int emoe_predicted_frequencies_host(emoe_predictor* pred, int task, double* out);
+
+/* expected_tokens Eq. 2 (expert_store.cpp:59-106).  Tasks are indices into
+ * the sorted profile list: wo [n_tasks], sensitivity [n_tasks][m] with
+ * has_sens[i] = 0 for an empty vector; requests (running then incoming) as
+ * task index + input tokens; freqs [n_tasks][m][E] with freq_present[i]. */
+int emoe_expected_tokens_host(int m, int E, int n_tasks, const double* wo, const int32_t* sensitivity,
+                              const uint8_t* has_sens, int n_requests, const int32_t* req_task,
+                              const int32_t* req_tokens, const uint8_t* freq_present, const double* freqs,
+                              int task_aware, double* aggregate);
+/* select_experts / loading_targets (expert_store.cpp:111-157): out [m][E] */
+int emoe_select_experts_host(const double* aggregate, int m, int E, const int32_t* budgets, int32_t* out);
+int emoe_loading_targets_host(const double* aggregate, int m, int E, const uint8_t* resident, const int32_t* budgets,
+                              int32_t* out, int32_t* sizes);
+/* plan_loading (expert_store.cpp:159-195) */
+int emoe_plan_loading_host(const uint8_t* resident, const int32_t* budgets, int m, int E, const int32_t* target,
+                           const int32_t* target_sizes, const double* aggregate, double per_expert_seconds,
+                           int32_t* evictions, int32_t* n_evict, int32_t* loads, int32_t* n_load, double* duration,
+                           double* delta_e, int32_t* total_loads);
+
+/* One predictor invocation of the engine (engine.cpp:367-446) on the GPU:
+ * predict from the previous prompt's expert sets (mode 0 all-layers, 1
+ * chained), modulate by each profile's fitted frequencies, Eq. 2 over the
+ * requests, loading_targets against `resident` and plan_loading.  Outputs
+ * the aggregate [m][E] and the plan (evictions/loads [m][E] + counts). */
+int emoe_invocation_host(emoe_predictor* pred, int mode, const int32_t* prev_sets, const int32_t* prev_sizes,
+                         int n_tasks, const double* wo, const int32_t* sensitivity, const uint8_t* has_sens,
+                         int n_requests, const int32_t* req_task, const int32_t* req_tokens, int task_aware,
+                         const uint8_t* resident, const int32_t* budgets, double per_expert_seconds,
+                         double* aggregate, int32_t* evictions, int32_t* n_evict, int32_t* loads, int32_t* n_load,
+                         double* delta_e);
+
+/* ========================================================================
+ * Workload generator (workload.cpp:242-286, :455): the reference's Markov
+ * routing trace, bit-identical (std::mt19937_64), used for synthetic inputs.
+ * out: [P][m][T][k] host int32.
+ * ====================================================================== */
+int emoe_gen_routing_trace(int m, int E, int k, double layer_lambda, double prompt_lambda, int initial_expert,
+                           uint64_t seed, int P, int T, int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMOE_H */

@@ -1,0 +1,96 @@
+"""Loads the in-tree CUDA library (lib/libemoe.so) and declares its C ABI.
+
+There is no fallback: if the library is missing or was built for another
+architecture, importing the package raises.  Build it with
+``python -c "import __graft_entry__ as g; g.build()"`` or
+``make -C paper_2503_06823_b200/csrc -j``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libemoe.so"
+
+if not LIB_PATH.exists():
+    raise ImportError(
+        f"emoe CUDA library not built: {LIB_PATH} is missing (run `make -C paper_2503_06823_b200/csrc -j`)")
+
+lib = C.CDLL(str(LIB_PATH))
+
+vp = C.c_void_p
+i32 = C.c_int32
+i64 = C.c_int64
+dbl = C.c_double
+
+
+class LayerConfig(C.Structure):
+    _fields_ = [("d_model", C.c_int), ("d_ff", C.c_int), ("num_experts", C.c_int), ("top_k", C.c_int),
+                ("activation", C.c_int), ("dtype", C.c_int), ("weight_mode", C.c_int), ("num_slots", C.c_int),
+                ("max_tokens", i64), ("forced_miss", C.c_int)]
+
+
+class Workspace(C.Structure):
+    _fields_ = [("T", i64), ("rows_cap", i64), ("logits", vp), ("topk_idx", vp), ("route_expert", vp),
+                ("route_rank", vp), ("route_hit", vp), ("served_idx", vp), ("served_w", vp), ("counts", vp),
+                ("seg_offsets", vp), ("pos", vp), ("row_token", vp), ("x_perm", vp), ("h", vp), ("y_perm", vp),
+                ("slot_of_expert", vp), ("resident", vp)]
+
+
+def _decl(name, *argtypes):
+    fn = getattr(lib, name)
+    fn.argtypes = list(argtypes)
+    fn.restype = C.c_int
+    return fn
+
+
+lib.emoe_last_error.restype = C.c_char_p
+lib.emoe_last_error.argtypes = []
+_decl("emoe_version")
+_decl("emoe_route_tokens_host", vp, i64, C.c_int, vp, C.c_int, vp, vp, vp, vp)
+_decl("emoe_layer_create", C.POINTER(LayerConfig), C.POINTER(vp))
+_decl("emoe_layer_destroy", vp)
+_decl("emoe_layer_set_gate_host", vp, vp)
+_decl("emoe_layer_register_expert_host", vp, C.c_int, vp, vp, vp)
+_decl("emoe_layer_set_scores_host", vp, vp)
+_decl("emoe_layer_begin_load", vp, vp, C.c_int, vp, C.c_int, vp)
+_decl("emoe_layer_poll_loads", vp, C.c_int, vp, C.POINTER(C.c_int))
+_decl("emoe_layer_residency", vp, vp)
+_decl("emoe_layer_last_load_stats", vp, C.POINTER(dbl), C.POINTER(dbl))
+_decl("emoe_moe_forward", vp, vp, vp, vp, i64, vp)
+_decl("emoe_moe_forward_host", vp, vp, vp, i64, vp)
+_decl("emoe_route", vp, vp, vp, i64, vp)
+_decl("emoe_layer_workspace", vp, C.POINTER(Workspace))
+_decl("emoe_layer_set_profiling", vp, C.c_int)
+_decl("emoe_layer_stage_times", vp, vp)
+lib.emoe_kernel_launches.restype = C.c_longlong
+lib.emoe_kernel_launches.argtypes = []
+_decl("emoe_predictor_create", C.c_int, C.c_int, C.c_int, C.c_int, dbl, C.POINTER(vp))
+_decl("emoe_predictor_destroy", vp)
+_decl("emoe_predictor_reset", vp)
+_decl("emoe_hist_update", vp, vp, C.c_int, C.c_int, vp, vp)
+_decl("emoe_predictor_counts_host", vp, vp, vp, vp)
+_decl("emoe_predictor_set_counts_host", vp, vp, vp, vp)
+_decl("emoe_prompt_expert_sets", vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp)
+_decl("emoe_predict_host", vp, C.c_int, vp, vp, C.c_int, vp, vp, vp)
+_decl("emoe_predicted_frequencies_host", vp, C.c_int, vp)
+_decl("emoe_expected_tokens_host", C.c_int, C.c_int, C.c_int, vp, vp, vp, C.c_int, vp, vp, vp, vp, C.c_int, vp)
+_decl("emoe_select_experts_host", vp, C.c_int, C.c_int, vp, vp)
+_decl("emoe_loading_targets_host", vp, C.c_int, C.c_int, vp, vp, vp, vp)
+_decl("emoe_plan_loading_host", vp, vp, C.c_int, C.c_int, vp, vp, vp, dbl, vp, vp, vp, vp, vp, vp, vp)
+_decl("emoe_invocation_host", vp, C.c_int, vp, vp, C.c_int, vp, vp, vp, C.c_int, vp, vp, C.c_int, vp, vp, dbl, vp,
+      vp, vp, vp, vp, vp)
+_decl("emoe_gen_routing_trace", C.c_int, C.c_int, C.c_int, dbl, dbl, C.c_int, C.c_uint64, C.c_int, C.c_int, vp)
+
+# every symbol include/emoe.h declares (checked by tests/test_boundary.py)
+EXPORTED = [
+    "emoe_last_error", "emoe_version", "emoe_route_tokens_host", "emoe_layer_create", "emoe_layer_destroy",
+    "emoe_layer_set_gate_host", "emoe_layer_register_expert_host", "emoe_layer_set_scores_host",
+    "emoe_layer_begin_load", "emoe_layer_poll_loads", "emoe_layer_residency", "emoe_layer_last_load_stats",
+    "emoe_moe_forward", "emoe_moe_forward_host", "emoe_route", "emoe_layer_workspace", "emoe_layer_set_profiling",
+    "emoe_layer_stage_times", "emoe_kernel_launches", "emoe_predictor_create",
+    "emoe_predictor_destroy", "emoe_predictor_reset", "emoe_hist_update", "emoe_predictor_counts_host",
+    "emoe_predictor_set_counts_host", "emoe_prompt_expert_sets", "emoe_predict_host",
+    "emoe_predicted_frequencies_host", "emoe_expected_tokens_host", "emoe_select_experts_host",
+    "emoe_loading_targets_host", "emoe_plan_loading_host", "emoe_invocation_host", "emoe_gen_routing_trace",
+]

@@ -1,0 +1,78 @@
+// Host-side launchers for the emoe sm_100a kernels (internal interface; the
+// public boundary is include/emoe.h).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace emoe {
+
+// number of kernels this library launched (reported by bench.py as gpu_launches)
+void count_launch(int n = 1);
+long long launch_count();
+
+enum EpiKind { EPI_SWIGLU = 0, EPI_RELU = 1, EPI_STORE = 2 };
+enum DType { DT_BF16 = 0, DT_F32 = 1 };
+
+constexpr int kRouteBlockTokens = 128;  // tokens per route / permute block
+constexpr int kSegPad = 128;            // per-expert segment padding (GEMM BM)
+
+// Outputs of K1 (any pointer except served_idx / served_w / block_counts may be null).
+struct RouteOut {
+  float* logits;          // [T][E]
+  int32_t* topk_idx;      // [T][k]
+  int32_t* route_expert;  // [T]
+  int32_t* route_rank;    // [T]
+  uint8_t* route_hit;     // [T]
+  int32_t* served_idx;    // [T][k], -1 = empty slot
+  float* served_w;        // [T][k]
+  int32_t* block_counts;  // [ceil(T/128)][E]
+};
+
+struct RouteArgs {
+  int64_t T;
+  int d, E, k;
+  int weight_mode;          // 0 softmax over served subset, 1 full softmax prob
+  int forced_miss;          // engine.cpp:533-537 behaviour when no expert is resident
+  const uint8_t* resident;  // [E] device
+  const double* scores;     // [E] device or null (empty score vector)
+  int* error_flag;          // device int, set to 3 when a token needs a fallback and no expert is resident
+};
+
+// K1 from activations: logits = x . wg^T (bf16 x via mma.sync, fp32 x via FFMA) + routing
+void launch_gate_route(const void* x, const void* wg, int dtype, const RouteArgs& a, const RouteOut& o,
+                       cudaStream_t s);
+// K1 from precomputed logits [T][E] fp32 (routing-driven parity mode)
+void launch_route_from_logits(const float* logits, const RouteArgs& a, const RouteOut& o, cudaStream_t s);
+
+// A2 route_token over ranked gate choices [T][k] (no logits; served weights uniform)
+void launch_route_from_choices(const int32_t* choices, const RouteArgs& a, const RouteOut& o, cudaStream_t s);
+
+// K3a: per-expert totals, padded segment offsets, per-block bases
+void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32_t* counts,
+                 int64_t* seg_offsets, int64_t* block_base, cudaStream_t s);
+// K3b: stable permutation + row gather into the padded segments
+void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
+                    const int64_t* seg_offsets, const int64_t* block_base, void* x_perm, int32_t* pos,
+                    int32_t* row_token, cudaStream_t s);
+// K5: gate-weighted combine in fixed slot order
+void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int32_t* pos, const float* served_w,
+                    void* y, cudaStream_t s);
+
+// K4: tcgen05 grouped GEMM (bf16)
+CUtensorMap make_tmap_bf16_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+int gemm_smem_bytes();
+void launch_grouped_gemm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
+                         const int64_t* seg_offsets, const int32_t* slot_of_expert, int num_experts, int K,
+                         int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo, int num_sms,
+                         cudaStream_t stream);
+
+// K4 fp32 path (SIMT FFMA): same grouping/epilogues, fp32 in/out
+void launch_grouped_gemm_f32(int epi, const float* A, int64_t lda, const float* B, const float* B2,
+                             const int64_t* seg_offsets, const int32_t* slot_of_expert, int num_experts, int K,
+                             int N_out, int b_rows_per_slot, int64_t rows_cap, float* out, int64_t ldo,
+                             cudaStream_t stream);
+
+}  // namespace emoe

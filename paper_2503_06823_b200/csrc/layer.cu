@@ -1,0 +1,599 @@
+// C ABI: the MoE layer handle (gate, HBM expert slot pool, two-phase residency
+// with side-stream H2D loads, routing/permute/FFN/combine workspace) and the
+// batched route_token entry point.  See include/emoe.h for the contract.
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <cstring>
+#include <vector>
+
+#include "capi_util.h"
+#include "kernels.h"
+
+namespace emoe {
+
+std::string& last_error_slot() {
+  static thread_local std::string s;
+  return s;
+}
+
+static std::atomic<long long> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+namespace {
+
+constexpr int kMaxTableE = 256;
+
+struct TableUpdate {
+  int E;
+  uint8_t resident[kMaxTableE];
+  int32_t slot[kMaxTableE];
+};
+
+// Residency tables travel as kernel parameters: captured at launch, ordered
+// on the stream, no host staging buffer to race on.
+__global__ void set_tables_kernel(TableUpdate u, uint8_t* resident, int32_t* slot) {
+  for (int e = threadIdx.x; e < u.E; e += blockDim.x) {
+    resident[e] = u.resident[e];
+    slot[e] = u.slot[e];
+  }
+}
+
+template <typename T>
+T* dmalloc(size_t count) {
+  T* p = nullptr;
+  if (count) EMOE_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  return p;
+}
+
+}  // namespace
+}  // namespace emoe
+
+using namespace emoe;
+
+struct emoe_layer {
+  emoe_layer_config cfg{};
+  int elem = 2;
+  int num_sms = 148;
+  int64_t rows_cap = 0;
+  int route_blocks = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_evict = nullptr, ev_load_start = nullptr, ev_load_done = nullptr;
+
+  void* wg = nullptr;
+  void* w1_pool = nullptr;
+  void* w3_pool = nullptr;
+  void* w2_pool = nullptr;
+  int32_t* slot_dev = nullptr;
+  uint8_t* resident_dev = nullptr;
+  double* scores_dev = nullptr;
+  bool have_scores = false;
+
+  std::vector<void*> host_w1, host_w3, host_w2;  // library-owned pinned copies
+  std::vector<int> slot_of_expert;               // compute-visible
+  std::vector<int> expert_in_slot;
+  std::vector<uint8_t> resident;
+  std::vector<int> pending_experts, pending_slots;
+  double last_load_bytes = 0, last_load_ms = 0, pending_bytes = 0;
+
+  // workspace
+  float* logits = nullptr;
+  int32_t* topk = nullptr;
+  int32_t* r_expert = nullptr;
+  int32_t* r_rank = nullptr;
+  uint8_t* r_hit = nullptr;
+  int32_t* served_idx = nullptr;
+  float* served_w = nullptr;
+  int32_t* block_counts = nullptr;
+  int32_t* counts = nullptr;
+  int64_t* seg_offsets = nullptr;
+  int64_t* block_base = nullptr;
+  int32_t* pos = nullptr;
+  int32_t* row_token = nullptr;
+  void* x_perm = nullptr;
+  void* h = nullptr;
+  void* y_perm = nullptr;
+  void* x_in = nullptr;
+  void* y_out = nullptr;
+  int* err_flag = nullptr;
+  int64_t last_T = 0;
+
+  CUtensorMap ta1{}, tb1{}, tb3{}, ta2{}, tb2{};
+
+  size_t w1_elems() const { return (size_t)cfg.d_ff * cfg.d_model; }
+  size_t w2_elems() const { return (size_t)cfg.d_model * cfg.d_ff; }
+  bool swiglu() const { return cfg.activation == EMOE_ACT_SWIGLU; }
+
+  void push_tables(cudaStream_t s) {
+    TableUpdate u;
+    u.E = cfg.num_experts;
+    for (int e = 0; e < cfg.num_experts; ++e) {
+      u.resident[e] = resident[e];
+      u.slot[e] = slot_of_expert[e];
+    }
+    set_tables_kernel<<<1, 128, 0, s>>>(u, resident_dev, slot_dev);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+  }
+
+  int n_resident() const {
+    int n = 0;
+    for (uint8_t r : resident) n += r;
+    return n;
+  }
+
+  void finish_pending(cudaStream_t s) {
+    EMOE_CUDA(cudaStreamWaitEvent(s, ev_load_done, 0));
+    for (size_t i = 0; i < pending_experts.size(); ++i) {
+      resident[pending_experts[i]] = 1;
+      slot_of_expert[pending_experts[i]] = pending_slots[i];
+    }
+    float ms = 0;
+    EMOE_CUDA(cudaEventElapsedTime(&ms, ev_load_start, ev_load_done));
+    last_load_ms = ms;
+    last_load_bytes = pending_bytes;
+    pending_experts.clear();
+    pending_slots.clear();
+    push_tables(s);
+  }
+
+  void poll(bool blocking, cudaStream_t s, int* still) {
+    if (still) *still = 0;
+    if (pending_experts.empty()) return;
+    if (blocking) {
+      EMOE_CUDA(cudaEventSynchronize(ev_load_done));
+    } else {
+      cudaError_t q = cudaEventQuery(ev_load_done);
+      if (q == cudaErrorNotReady) {
+        if (still) *still = 1;
+        return;
+      }
+      EMOE_CUDA(q);
+    }
+    finish_pending(s);
+  }
+
+  void route(const void* x, const float* logits_in, int64_t T, cudaStream_t s) {
+    EMOE_REQUIRE(T >= 0 && T <= cfg.max_tokens, "moe_forward: T exceeds the layer's max_tokens");
+    if (n_resident() == 0 && !cfg.forced_miss)
+      throw InvariantError("route_token: no resident experts at layer");
+    RouteArgs a;
+    a.T = T;
+    a.d = cfg.d_model;
+    a.E = cfg.num_experts;
+    a.k = cfg.top_k;
+    a.weight_mode = cfg.weight_mode;
+    a.forced_miss = cfg.forced_miss;
+    a.resident = resident_dev;
+    a.scores = have_scores ? scores_dev : nullptr;
+    a.error_flag = err_flag;
+    RouteOut o{logits, topk, r_expert, r_rank, r_hit, served_idx, served_w, block_counts};
+    if (logits_in)
+      launch_route_from_logits(logits_in, a, o, s);
+    else
+      launch_gate_route(x, wg, cfg.dtype, a, o, s);
+    last_T = T;
+  }
+
+  // stage events for emoe_layer_stage_times (route, scan+permute, gemm1, gemm2, combine);
+  // one event set per profiled forward, averaged and recycled by stage_times()
+  bool profiling = false;
+  std::vector<std::array<cudaEvent_t, 6>> ev_pool;
+  size_t ev_used = 0;
+  void mark(int i, cudaStream_t s) {
+    if (!profiling) return;
+    if (i == 0 && ev_used == ev_pool.size()) {
+      std::array<cudaEvent_t, 6> set;
+      for (cudaEvent_t& e : set) EMOE_CUDA(cudaEventCreate(&e));
+      ev_pool.push_back(set);
+    }
+    EMOE_CUDA(cudaEventRecord(ev_pool[ev_used][i], s));
+    if (i == 5) ++ev_used;
+  }
+
+  void forward(const void* x, const float* logits_in, void* y, int64_t T, cudaStream_t s) {
+    poll(false, s, nullptr);
+    if (T == 0) {
+      route(x, logits_in, T, s);
+      return;
+    }
+    mark(0, s);
+    route(x, logits_in, T, s);
+    mark(1, s);
+    const int nb = (int)ceil_div(T, kRouteBlockTokens);
+    const int E = cfg.num_experts, d = cfg.d_model, f = cfg.d_ff;
+    launch_scan(block_counts, nb, E, kSegPad, counts, seg_offsets, block_base, s);
+    EMOE_CUDA(cudaMemsetAsync(row_token, 0xff, sizeof(int32_t) * rows_cap, s));
+    launch_permute(x, elem, T, d, E, cfg.top_k, served_idx, seg_offsets, block_base, x_perm, pos, row_token, s);
+    mark(2, s);
+    if (cfg.dtype == EMOE_DTYPE_BF16) {
+      launch_grouped_gemm(swiglu() ? EPI_SWIGLU : EPI_RELU, ta1, tb1, tb3, seg_offsets, slot_dev, E, d, f, f,
+                          static_cast<__nv_bfloat16*>(h), f, num_sms, s);
+      mark(3, s);
+      launch_grouped_gemm(EPI_STORE, ta2, tb2, tb2, seg_offsets, slot_dev, E, f, d, d,
+                          static_cast<__nv_bfloat16*>(y_perm), d, num_sms, s);
+      mark(4, s);
+    } else {
+      launch_grouped_gemm_f32(swiglu() ? EPI_SWIGLU : EPI_RELU, static_cast<const float*>(x_perm), d,
+                              static_cast<const float*>(w1_pool), static_cast<const float*>(w3_pool), seg_offsets,
+                              slot_dev, E, d, f, f, rows_cap, static_cast<float*>(h), f, s);
+      mark(3, s);
+      launch_grouped_gemm_f32(EPI_STORE, static_cast<const float*>(h), f, static_cast<const float*>(w2_pool),
+                              nullptr, seg_offsets, slot_dev, E, f, d, d, rows_cap, static_cast<float*>(y_perm), d,
+                              s);
+      mark(4, s);
+    }
+    launch_combine(y_perm, cfg.dtype, T, d, cfg.top_k, pos, served_w, y, s);
+    mark(5, s);
+  }
+
+  void begin_load(const int32_t* ev, int nev, const int32_t* ld, int nld, cudaStream_t s) {
+    const int E = cfg.num_experts;
+    if (!pending_experts.empty()) poll(true, s, nullptr);  // plans apply in order
+    std::vector<uint8_t> evicting(E, 0), loading(E, 0);
+    for (int i = 0; i < nev; ++i) {
+      EMOE_REQUIRE(ev[i] >= 0 && ev[i] < E, "begin_load: eviction index out of range");
+      if (!resident[ev[i]] || evicting[ev[i]]) throw InvariantError("placement: evicting non-resident expert");
+      evicting[ev[i]] = 1;
+    }
+    int after = n_resident() - nev;
+    for (int i = 0; i < nld; ++i) {
+      EMOE_REQUIRE(ld[i] >= 0 && ld[i] < E, "begin_load: load index out of range");
+      if ((resident[ld[i]] && !evicting[ld[i]]) || loading[ld[i]])
+        throw InvariantError("placement: loading resident expert");
+      if (!host_w1[ld[i]]) throw ValidationError("begin_load: expert weights were never registered");
+      loading[ld[i]] = 1;
+      if (++after > cfg.num_slots) throw InvariantError("placement: layer budget exceeded");
+    }
+    // phase 1 (load start): evictions take effect for compute enqueued after this point
+    for (int i = 0; i < nev; ++i) {
+      resident[ev[i]] = 0;
+      expert_in_slot[slot_of_expert[ev[i]]] = -1;
+      slot_of_expert[ev[i]] = -1;
+    }
+    push_tables(s);
+    if (nld == 0) return;
+    // the freed slots may still be read by compute already enqueued on `s`
+    EMOE_CUDA(cudaEventRecord(ev_evict, s));
+    EMOE_CUDA(cudaStreamWaitEvent(copy_stream, ev_evict, 0));
+    EMOE_CUDA(cudaEventRecord(ev_load_start, copy_stream));
+    pending_bytes = 0;
+    for (int i = 0; i < nld; ++i) {
+      int slot = -1;
+      for (int q = 0; q < cfg.num_slots; ++q)
+        if (expert_in_slot[q] < 0) {
+          slot = q;
+          break;
+        }
+      if (slot < 0) throw InvariantError("placement: layer budget exceeded");
+      expert_in_slot[slot] = ld[i];
+      const int e = ld[i];
+      const size_t b1 = w1_elems() * elem, b2 = w2_elems() * elem;
+      EMOE_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(w1_pool) + slot * b1, host_w1[e], b1, cudaMemcpyHostToDevice,
+                                copy_stream));
+      pending_bytes += (double)b1;
+      if (swiglu()) {
+        EMOE_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(w3_pool) + slot * b1, host_w3[e], b1,
+                                  cudaMemcpyHostToDevice, copy_stream));
+        pending_bytes += (double)b1;
+      }
+      EMOE_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(w2_pool) + slot * b2, host_w2[e], b2, cudaMemcpyHostToDevice,
+                                copy_stream));
+      pending_bytes += (double)b2;
+      pending_experts.push_back(e);
+      pending_slots.push_back(slot);
+    }
+    EMOE_CUDA(cudaEventRecord(ev_load_done, copy_stream));
+  }
+
+  void destroy() {
+    auto f = [](void* p) {
+      if (p) cudaFree(p);
+    };
+    for (void* p : {(void*)wg, w1_pool, w3_pool, w2_pool, (void*)slot_dev, (void*)resident_dev, (void*)scores_dev,
+                    (void*)logits, (void*)topk, (void*)r_expert, (void*)r_rank, (void*)r_hit, (void*)served_idx,
+                    (void*)served_w, (void*)block_counts, (void*)counts, (void*)seg_offsets, (void*)block_base,
+                    (void*)pos, (void*)row_token, x_perm, h, y_perm, x_in, y_out, (void*)err_flag})
+      f(p);
+    for (auto* v : {&host_w1, &host_w3, &host_w2})
+      for (void* p : *v)
+        if (p) cudaFreeHost(p);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (cudaEvent_t e : {ev_evict, ev_load_start, ev_load_done})
+      if (e) cudaEventDestroy(e);
+    for (auto& set : ev_pool)
+      for (cudaEvent_t e : set) cudaEventDestroy(e);
+  }
+};
+
+extern "C" {
+
+const char* emoe_last_error(void) { return last_error_slot().c_str(); }
+int emoe_version(void) { return 1; }
+
+int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
+  return guard([&] {
+    EMOE_REQUIRE(cfg && out, "layer_create: null argument");
+    const emoe_layer_config& c = *cfg;
+    EMOE_REQUIRE(c.num_experts >= 1 && c.num_experts <= 128, "layer.num_experts: must be in [1, 128]");
+    EMOE_REQUIRE(c.top_k >= 1 && c.top_k <= 8 && c.top_k <= c.num_experts, "layer.top_k: must be in [1, min(8, E)]");
+    EMOE_REQUIRE(c.num_slots >= 1 && c.num_slots <= c.num_experts, "layer.num_slots: must be in [1, E]");
+    EMOE_REQUIRE(c.max_tokens >= 1, "layer.max_tokens: must be >= 1");
+    EMOE_REQUIRE(c.dtype == EMOE_DTYPE_BF16 || c.dtype == EMOE_DTYPE_F32, "layer.dtype: unknown");
+    EMOE_REQUIRE(c.activation == EMOE_ACT_SWIGLU || c.activation == EMOE_ACT_RELU, "layer.activation: unknown");
+    if (c.dtype == EMOE_DTYPE_BF16) {
+      EMOE_REQUIRE(c.d_model % 256 == 0, "layer.d_model: bf16 path needs a multiple of 256");
+      EMOE_REQUIRE(c.d_ff % 256 == 0, "layer.d_ff: bf16 path needs a multiple of 256");
+    } else {
+      EMOE_REQUIRE(c.d_model % 64 == 0 && c.d_ff % 64 == 0, "layer: fp32 path needs d_model, d_ff % 64 == 0");
+    }
+    auto* L = new emoe_layer();
+    try {
+      L->cfg = c;
+      L->elem = c.dtype == EMOE_DTYPE_BF16 ? 2 : 4;
+      int dev = 0;
+      EMOE_CUDA(cudaGetDevice(&dev));
+      EMOE_CUDA(cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, dev));
+      const int E = c.num_experts, k = c.top_k;
+      const int64_t T = c.max_tokens;
+      L->rows_cap = T * k + (int64_t)E * kSegPad;
+      L->route_blocks = (int)ceil_div(T, kRouteBlockTokens);
+      EMOE_CUDA(cudaStreamCreateWithFlags(&L->copy_stream, cudaStreamNonBlocking));
+      EMOE_CUDA(cudaEventCreateWithFlags(&L->ev_evict, cudaEventDisableTiming));
+      EMOE_CUDA(cudaEventCreate(&L->ev_load_start));
+      EMOE_CUDA(cudaEventCreate(&L->ev_load_done));
+      const size_t el = L->elem;
+      L->wg = dmalloc<uint8_t>((size_t)E * c.d_model * el);
+      L->w1_pool = dmalloc<uint8_t>((size_t)c.num_slots * L->w1_elems() * el);
+      if (L->swiglu()) L->w3_pool = dmalloc<uint8_t>((size_t)c.num_slots * L->w1_elems() * el);
+      L->w2_pool = dmalloc<uint8_t>((size_t)c.num_slots * L->w2_elems() * el);
+      L->slot_dev = dmalloc<int32_t>(E);
+      L->resident_dev = dmalloc<uint8_t>(E);
+      L->scores_dev = dmalloc<double>(E);
+      L->logits = dmalloc<float>((size_t)T * E);
+      L->topk = dmalloc<int32_t>((size_t)T * k);
+      L->r_expert = dmalloc<int32_t>(T);
+      L->r_rank = dmalloc<int32_t>(T);
+      L->r_hit = dmalloc<uint8_t>(T);
+      L->served_idx = dmalloc<int32_t>((size_t)T * k);
+      L->served_w = dmalloc<float>((size_t)T * k);
+      L->block_counts = dmalloc<int32_t>((size_t)L->route_blocks * E);
+      L->counts = dmalloc<int32_t>(E);
+      L->seg_offsets = dmalloc<int64_t>(E + 1);
+      L->block_base = dmalloc<int64_t>((size_t)L->route_blocks * E);
+      L->pos = dmalloc<int32_t>((size_t)T * k);
+      L->row_token = dmalloc<int32_t>(L->rows_cap);
+      L->x_perm = dmalloc<uint8_t>((size_t)L->rows_cap * c.d_model * el);
+      L->h = dmalloc<uint8_t>((size_t)L->rows_cap * c.d_ff * el);
+      L->y_perm = dmalloc<uint8_t>((size_t)L->rows_cap * c.d_model * el);
+      L->err_flag = dmalloc<int>(1);
+      EMOE_CUDA(cudaMemset(L->x_perm, 0, (size_t)L->rows_cap * c.d_model * el));
+      EMOE_CUDA(cudaMemset(L->h, 0, (size_t)L->rows_cap * c.d_ff * el));
+      EMOE_CUDA(cudaMemset(L->y_perm, 0, (size_t)L->rows_cap * c.d_model * el));
+      EMOE_CUDA(cudaMemset(L->err_flag, 0, sizeof(int)));
+      EMOE_CUDA(cudaMemset(L->w1_pool, 0, (size_t)c.num_slots * L->w1_elems() * el));
+      if (L->w3_pool) EMOE_CUDA(cudaMemset(L->w3_pool, 0, (size_t)c.num_slots * L->w1_elems() * el));
+      EMOE_CUDA(cudaMemset(L->w2_pool, 0, (size_t)c.num_slots * L->w2_elems() * el));
+      L->host_w1.assign(E, nullptr);
+      L->host_w3.assign(E, nullptr);
+      L->host_w2.assign(E, nullptr);
+      L->slot_of_expert.assign(E, -1);
+      L->expert_in_slot.assign(c.num_slots, -1);
+      L->resident.assign(E, 0);
+      L->push_tables(0);
+      if (c.dtype == EMOE_DTYPE_BF16) {
+        const uint64_t d = c.d_model, f = c.d_ff;
+        L->ta1 = make_tmap_bf16_2d(L->x_perm, L->rows_cap, d, 128);
+        L->tb1 = make_tmap_bf16_2d(L->w1_pool, (uint64_t)c.num_slots * f, d, L->swiglu() ? 128 : 256);
+        L->tb3 = L->swiglu() ? make_tmap_bf16_2d(L->w3_pool, (uint64_t)c.num_slots * f, d, 128) : L->tb1;
+        L->ta2 = make_tmap_bf16_2d(L->h, L->rows_cap, f, 128);
+        L->tb2 = make_tmap_bf16_2d(L->w2_pool, (uint64_t)c.num_slots * d, f, 256);
+      }
+      EMOE_CUDA(cudaDeviceSynchronize());
+    } catch (...) {
+      L->destroy();
+      delete L;
+      throw;
+    }
+    *out = L;
+  });
+}
+
+int emoe_layer_destroy(emoe_layer* layer) {
+  return guard([&] {
+    if (!layer) return;
+    cudaDeviceSynchronize();
+    layer->destroy();
+    delete layer;
+  });
+}
+
+int emoe_layer_set_gate_host(emoe_layer* L, const void* wg) {
+  return guard([&] {
+    EMOE_REQUIRE(L && wg, "set_gate: null argument");
+    EMOE_CUDA(cudaMemcpy(L->wg, wg, (size_t)L->cfg.num_experts * L->cfg.d_model * L->elem, cudaMemcpyHostToDevice));
+  });
+}
+
+int emoe_layer_register_expert_host(emoe_layer* L, int e, const void* w1, const void* w3, const void* w2) {
+  return guard([&] {
+    EMOE_REQUIRE(L && w1 && w2, "register_expert: null weights");
+    EMOE_REQUIRE(e >= 0 && e < L->cfg.num_experts, "register_expert: expert index out of range");
+    EMOE_REQUIRE(!L->swiglu() || w3, "register_expert: SwiGLU needs w3");
+    const size_t b1 = L->w1_elems() * L->elem, b2 = L->w2_elems() * L->elem;
+    auto put = [&](std::vector<void*>& v, const void* src, size_t bytes) {
+      if (!v[e]) EMOE_CUDA(cudaHostAlloc(&v[e], bytes, cudaHostAllocDefault));
+      std::memcpy(v[e], src, bytes);
+    };
+    put(L->host_w1, w1, b1);
+    if (L->swiglu()) put(L->host_w3, w3, b1);
+    put(L->host_w2, w2, b2);
+  });
+}
+
+int emoe_layer_set_scores_host(emoe_layer* L, const double* scores) {
+  return guard([&] {
+    EMOE_REQUIRE(L, "set_scores: null layer");
+    if (!scores) {
+      L->have_scores = false;
+      return;
+    }
+    EMOE_CUDA(cudaMemcpy(L->scores_dev, scores, sizeof(double) * L->cfg.num_experts, cudaMemcpyHostToDevice));
+    L->have_scores = true;
+  });
+}
+
+int emoe_layer_begin_load(emoe_layer* L, const int32_t* evictions, int n_ev, const int32_t* loads, int n_ld,
+                          void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(L, "begin_load: null layer");
+    L->begin_load(evictions, n_ev, loads, n_ld, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int emoe_layer_poll_loads(emoe_layer* L, int blocking, void* stream, int* still_pending) {
+  return guard([&] {
+    EMOE_REQUIRE(L, "poll_loads: null layer");
+    L->poll(blocking != 0, static_cast<cudaStream_t>(stream), still_pending);
+  });
+}
+
+int emoe_layer_residency(const emoe_layer* L, uint8_t* out) {
+  return guard([&] {
+    EMOE_REQUIRE(L && out, "residency: null argument");
+    std::copy(L->resident.begin(), L->resident.end(), out);
+  });
+}
+
+int emoe_layer_last_load_stats(const emoe_layer* L, double* bytes, double* ms) {
+  return guard([&] {
+    EMOE_REQUIRE(L, "last_load_stats: null layer");
+    if (bytes) *bytes = L->last_load_bytes;
+    if (ms) *ms = L->last_load_ms;
+  });
+}
+
+int emoe_moe_forward(emoe_layer* L, const void* x, const float* logits_in, void* y, int64_t T, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(L && y && (x || logits_in), "moe_forward: null argument");
+    EMOE_REQUIRE(x, "moe_forward: x is required (the FFN consumes it)");
+    L->forward(x, logits_in, y, T, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int emoe_moe_forward_host(emoe_layer* L, const void* x_host, void* y_host, int64_t T, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(L && x_host && y_host, "moe_forward_host: null argument");
+    EMOE_REQUIRE(T >= 0 && T <= L->cfg.max_tokens, "moe_forward: T exceeds the layer's max_tokens");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t bytes = (size_t)T * L->cfg.d_model * L->elem;
+    if (!L->x_in) {
+      L->x_in = dmalloc<uint8_t>((size_t)L->cfg.max_tokens * L->cfg.d_model * L->elem);
+      L->y_out = dmalloc<uint8_t>((size_t)L->cfg.max_tokens * L->cfg.d_model * L->elem);
+    }
+    EMOE_CUDA(cudaMemcpyAsync(L->x_in, x_host, bytes, cudaMemcpyHostToDevice, s));
+    L->forward(L->x_in, nullptr, L->y_out, T, s);
+    EMOE_CUDA(cudaMemcpyAsync(y_host, L->y_out, bytes, cudaMemcpyDeviceToHost, s));
+    EMOE_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int emoe_route(emoe_layer* L, const void* x, const float* logits_in, int64_t T, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(L && (x || logits_in), "route: null argument");
+    L->poll(false, static_cast<cudaStream_t>(stream), nullptr);
+    L->route(x, logits_in, T, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int emoe_layer_workspace(emoe_layer* L, emoe_workspace* w) {
+  return guard([&] {
+    EMOE_REQUIRE(L && w, "workspace: null argument");
+    w->T = L->last_T;
+    w->rows_cap = L->rows_cap;
+    w->logits = L->logits;
+    w->topk_idx = L->topk;
+    w->route_expert = L->r_expert;
+    w->route_rank = L->r_rank;
+    w->route_hit = L->r_hit;
+    w->served_idx = L->served_idx;
+    w->served_w = L->served_w;
+    w->counts = L->counts;
+    w->seg_offsets = L->seg_offsets;
+    w->pos = L->pos;
+    w->row_token = L->row_token;
+    w->x_perm = L->x_perm;
+    w->h = L->h;
+    w->y_perm = L->y_perm;
+    w->slot_of_expert = L->slot_dev;
+    w->resident = L->resident_dev;
+  });
+}
+
+int emoe_layer_set_profiling(emoe_layer* L, int enable) {
+  return guard([&] {
+    EMOE_REQUIRE(L, "set_profiling: null layer");
+    L->profiling = enable != 0;
+    L->ev_used = 0;
+  });
+}
+
+int emoe_layer_stage_times(emoe_layer* L, float* ms) {
+  return guard([&] {
+    EMOE_REQUIRE(L && ms, "stage_times: null argument");
+    EMOE_REQUIRE(L->ev_used > 0, "stage_times: no profiled forward since the last call");
+    for (int i = 0; i < 5; ++i) ms[i] = 0.0f;
+    for (size_t n = 0; n < L->ev_used; ++n) {
+      auto& set = L->ev_pool[n];
+      EMOE_CUDA(cudaEventSynchronize(set[5]));
+      for (int i = 0; i < 5; ++i) {
+        float v = 0;
+        EMOE_CUDA(cudaEventElapsedTime(&v, set[i], set[i + 1]));
+        ms[i] += v / (float)L->ev_used;
+      }
+    }
+    L->ev_used = 0;
+  });
+}
+
+long long emoe_kernel_launches(void) { return launch_count(); }
+
+int emoe_route_tokens_host(const int32_t* choices, int64_t T, int k, const uint8_t* resident, int E,
+                           const double* scores, int32_t* out_expert, int32_t* out_rank, uint8_t* out_hit) {
+  return guard([&] {
+    EMOE_REQUIRE(E >= 1 && E <= 128, "route_tokens: E must be in [1, 128]");
+    EMOE_REQUIRE(k >= 1 && k <= 8, "route_tokens: k must be in [1, 8]");
+    for (int64_t i = 0; i < T * k; ++i)
+      EMOE_REQUIRE(choices[i] >= 0 && choices[i] < E, "route_tokens: gate choice out of range");
+    if (T == 0) return;
+    DevBuf<int32_t> dch(choices, (size_t)T * k);
+    DevBuf<uint8_t> dres(resident, E);
+    DevBuf<double> dsc(scores ? (size_t)E : 0);
+    if (scores) EMOE_CUDA(cudaMemcpy(dsc.p, scores, sizeof(double) * E, cudaMemcpyHostToDevice));
+    DevBuf<int32_t> dex(T), drk(T);
+    DevBuf<uint8_t> dhit(T);
+    DevBuf<int> flag(1);
+    EMOE_CUDA(cudaMemset(flag.p, 0, sizeof(int)));
+    RouteArgs a;
+    a.T = T;
+    a.d = 0;
+    a.E = E;
+    a.k = k;
+    a.weight_mode = 0;
+    a.forced_miss = 0;
+    a.resident = dres.p;
+    a.scores = scores ? dsc.p : nullptr;
+    a.error_flag = flag.p;
+    RouteOut o{nullptr, nullptr, dex.p, drk.p, dhit.p, nullptr, nullptr, nullptr};
+    launch_route_from_choices(dch.p, a, o, 0);
+    int f = 0;
+    EMOE_CUDA(cudaMemcpy(&f, flag.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (f == 3) throw InvariantError("route_token: no resident experts at layer");
+    dex.to_host(out_expert);
+    drk.to_host(out_rank);
+    dhit.to_host(out_hit);
+  });
+}
+
+}  // extern "C"

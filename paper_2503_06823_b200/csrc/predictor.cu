@@ -1,0 +1,855 @@
+// K2: popularity histograms over routing history (A6) and the predictor /
+// Eq. 2 / resident-set selection / load planning (A7, A8) on the GPU.
+//
+// A6 is the data-parallel part: one block per (prompt, layer) builds the
+// rank-0 and all-rank expert histograms and the layer-transition histogram of
+// that slice in shared memory and folds them into exact 64-bit global tallies
+// (the reference stores the same integers as doubles, predictor.cpp:164-183;
+// counts commute, so block order does not matter).  Dominant experts per
+// (prompt, layer) are reduced on the fly and the prompt-transition tally is a
+// second tiny kernel that also continues the chain across calls.
+//
+// A7/A8 are latency-bound fp64 control logic over m x E numbers.  They run as
+// single-block kernels whose every floating-point expression and summation
+// order matches the reference line for line; this file is compiled with
+// --fmad=false so no multiply-add is contracted (the reference's ISO C++
+// build has -ffp-contract=off).  Ranking uses a parallel stable rank
+// (position = number of elements that precede it under "score desc, index
+// asc"), which is exactly std::stable_sort's order for a strict total order.
+#include <algorithm>
+#include <vector>
+
+#include "capi_util.h"
+#include "kernels.h"
+
+namespace emoe {
+namespace {
+
+using u64 = unsigned long long;
+
+// ---------------------------------------------------------------------------
+// A6 histograms
+// ---------------------------------------------------------------------------
+__global__ void hist_kernel(const int32_t* __restrict__ trace, int P, int m, int T, int k, int E,
+                            const int32_t* __restrict__ task_ids, u64* __restrict__ layer_counts,
+                            u64* __restrict__ task_counts, int32_t* __restrict__ dom) {
+  extern __shared__ int sh[];
+  int* h0 = sh;          // [E] rank-0 counts
+  int* hall = sh + E;    // [E] all-rank counts
+  int* htr = sh + 2 * E;  // [E*E] layer transitions l -> l+1
+  const int p = blockIdx.x / m, l = blockIdx.x % m;
+  const bool do_trans = l + 1 < m;
+  const int nbins = 2 * E + (do_trans ? E * E : 0);
+  for (int i = threadIdx.x; i < nbins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int32_t* base = trace + ((int64_t)p * m + l) * T * k;
+  const int32_t* next = trace + ((int64_t)p * m + l + 1) * T * k;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    const int a = base[(int64_t)t * k];
+    atomicAdd(&h0[a], 1);
+    if (task_ids)
+      for (int r = 0; r < k; ++r) atomicAdd(&hall[base[(int64_t)t * k + r]], 1);
+    if (do_trans) atomicAdd(&htr[a * E + next[(int64_t)t * k]], 1);
+  }
+  __syncthreads();
+  if (task_ids) {
+    u64* dst = task_counts + ((int64_t)task_ids[p] * m + l) * E;
+    for (int e = threadIdx.x; e < E; e += blockDim.x)
+      if (hall[e]) atomicAdd(&dst[e], (u64)hall[e]);
+  }
+  if (do_trans) {
+    u64* dst = layer_counts + (int64_t)l * E * E;
+    for (int i = threadIdx.x; i < E * E; i += blockDim.x)
+      if (htr[i]) atomicAdd(&dst[i], (u64)htr[i]);
+  }
+  if (threadIdx.x == 0) {  // dominant_expert: modal rank-0, smallest index on ties (workload.cpp:350-361)
+    int best = 0;
+    for (int e = 1; e < E; ++e)
+      if (h0[e] > h0[best]) best = e;
+    dom[(int64_t)p * m + l] = best;
+  }
+}
+
+__global__ void prompt_trans_kernel(const int32_t* __restrict__ dom, int P, int m, int E, int32_t* __restrict__ last,
+                                    int has_last, u64* __restrict__ prompt_counts) {
+  // prompt n -> n+1 transitions of the dominant experts (predictor.cpp:176-183)
+  const int total = (P - 1 + (has_last ? 1 : 0)) * m;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int l = i % m;
+    int pi = i / m - (has_last ? 1 : 0);  // -1 = chain from the previous call
+    const int a = pi < 0 ? last[l] : dom[(int64_t)pi * m + l];
+    const int b = dom[(int64_t)(pi + 1) * m + l];
+    atomicAdd(&prompt_counts[((int64_t)l * E + a) * E + b], 1ull);
+  }
+}
+
+__global__ void save_last_kernel(const int32_t* __restrict__ dom, int P, int m, int32_t* __restrict__ last) {
+  for (int l = threadIdx.x; l < m; l += blockDim.x) last[l] = dom[(int64_t)(P - 1) * m + l];
+}
+
+// prompt_expert_sets (workload.cpp:363-377): one block per layer
+__global__ void prompt_sets_kernel(const int32_t* __restrict__ trace, int m, int T, int k, int E, int prompt,
+                                   int32_t* __restrict__ dom, int32_t* __restrict__ sets, int32_t* __restrict__ sizes) {
+  extern __shared__ int cnt[];
+  const int l = blockIdx.x;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
+  __syncthreads();
+  const int32_t* base = trace + ((int64_t)prompt * m + l) * T * k;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) atomicAdd(&cnt[base[(int64_t)t * k]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int best = 0;
+    for (int e = 1; e < E; ++e)
+      if (cnt[e] > cnt[best]) best = e;
+    dom[l] = best;
+    int n = 0;
+    for (int r = 0; r < k; ++r) {  // by count desc, index asc, only experts that occur
+      int b = -1;
+      for (int e = 0; e < E; ++e) {
+        if (cnt[e] <= 0) continue;
+        bool used = false;
+        for (int q = 0; q < n; ++q) used |= sets[l * k + q] == e;
+        if (used) continue;
+        if (b < 0 || cnt[e] > cnt[b]) b = e;
+      }
+      if (b < 0) break;
+      sets[l * k + n++] = b;
+    }
+    for (int r = n; r < k; ++r) sets[l * k + r] = -1;
+    sizes[l] = n;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// A7 / A8 device helpers (single block, blockDim >= 32)
+// ---------------------------------------------------------------------------
+constexpr int MAXE = 1024;
+
+// smoothed(counts)[j] for a u64 count row (predictor.cpp:13-24).  The sum is
+// computed left to right by every calling thread (identical value).
+__device__ double smoothed_at(const u64* row, int E, double s, int j) {
+  double sum = 0.0;
+  for (int q = 0; q < E; ++q) sum += (double)row[q];
+  const double denom = sum + s * E;
+  if (denom <= 0.0) return 1.0 / E;
+  return ((double)row[j] + s) / denom;
+}
+__device__ double smoothed_at_d(const double* row, int E, double s, int j) {
+  double sum = 0.0;
+  for (int q = 0; q < E; ++q) sum += row[q];
+  const double denom = sum + s * E;
+  if (denom <= 0.0) return 1.0 / E;
+  return (row[j] + s) / denom;
+}
+
+// stable rank under (score desc, index asc): order[pos] = i
+__device__ void ranked_indices_block(const double* row, int E, int* order) {
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {
+    const double si = row[i];
+    int pos = 0;
+    for (int j = 0; j < E; ++j) {
+      const double sj = row[j];
+      pos += (sj != si) ? (sj > si) : (j < i);
+    }
+    order[pos] = i;
+  }
+  __syncthreads();
+}
+
+// rank_scores (predictor.cpp:30-58) on a shared scores row; writes experts[0..min(k,E))
+__device__ int rank_scores_block(const double* scores, int E, int k, int* order, int32_t* experts) {
+  ranked_indices_block(scores, E, order);
+  __shared__ int n_out;
+  if (threadIdx.x == 0) {
+    int group_start = 0;
+    double leader = E > 0 ? scores[order[0]] : 0.0;
+    for (int i = 0; i <= E; ++i) {
+      const bool close = i == E || leader - scores[order[i]] > 1e-12 + 1e-3 * fabs(leader);
+      if (close) {
+        for (int a = group_start + 1; a < i; ++a) {  // sort the group by index
+          const int v = order[a];
+          int b = a - 1;
+          while (b >= group_start && order[b] > v) {
+            order[b + 1] = order[b];
+            --b;
+          }
+          order[b + 1] = v;
+        }
+        if (i < E) {
+          group_start = i;
+          leader = scores[order[i]];
+        }
+      }
+    }
+    const int n = k < E ? k : E;
+    for (int r = 0; r < n; ++r) experts[r] = order[r];
+    n_out = n;
+  }
+  __syncthreads();
+  return n_out;
+}
+
+// mean_rows (predictor.cpp:60-72) of u64 count rows `base[e]` over `from`
+__device__ void mean_rows_block(const u64* base, int E, double s, const int32_t* from, int n_from, double* scores) {
+  for (int j = threadIdx.x; j < E; j += blockDim.x) {
+    double acc = 0.0;
+    for (int i = 0; i < n_from; ++i) acc += smoothed_at(base + (int64_t)from[i] * E, E, s, j);
+    scores[j] = acc / (double)n_from;
+  }
+  __syncthreads();
+}
+
+struct PredictArgs {
+  int mode, layer, m, E, k;
+  double s;
+  const u64* layer_counts;
+  const u64* prompt_counts;
+  const int32_t* prev_sets;
+  const int32_t* prev_sizes;
+  double* scores;   // [m][E]
+  int32_t* experts;  // [m][k]
+  int32_t* n_experts;  // [m]
+};
+
+__device__ void predict_block(const PredictArgs& a, int* order, double* row) {
+  const int E = a.E, k = a.k;
+  if (a.mode == 0) {  // predict_all_layers
+    for (int l = 0; l < a.m; ++l) {
+      mean_rows_block(a.prompt_counts + (int64_t)l * E * E, E, a.s, a.prev_sets + l * k, a.prev_sizes[l], row);
+      for (int j = threadIdx.x; j < E; j += blockDim.x) a.scores[(int64_t)l * E + j] = row[j];
+      const int n = rank_scores_block(row, E, k, order, a.experts + l * k);
+      if (threadIdx.x == 0) a.n_experts[l] = n;
+      __syncthreads();
+    }
+  } else if (a.mode == 1) {  // predict_chained
+    mean_rows_block(a.prompt_counts, E, a.s, a.prev_sets, a.prev_sizes[0], row);
+    for (int j = threadIdx.x; j < E; j += blockDim.x) a.scores[j] = row[j];
+    int n = rank_scores_block(row, E, k, order, a.experts);
+    if (threadIdx.x == 0) a.n_experts[0] = n;
+    __syncthreads();
+    for (int l = 1; l < a.m; ++l) {
+      mean_rows_block(a.layer_counts + (int64_t)(l - 1) * E * E, E, a.s, a.experts + (l - 1) * k, n, row);
+      for (int j = threadIdx.x; j < E; j += blockDim.x) a.scores[(int64_t)l * E + j] = row[j];
+      n = rank_scores_block(row, E, k, order, a.experts + l * k);
+      if (threadIdx.x == 0) a.n_experts[l] = n;
+      __syncthreads();
+    }
+  } else {  // predict_layerwise
+    mean_rows_block(a.layer_counts + (int64_t)(a.layer - 1) * E * E, E, a.s, a.prev_sets, a.prev_sizes[0], row);
+    for (int j = threadIdx.x; j < E; j += blockDim.x) a.scores[j] = row[j];
+    const int n = rank_scores_block(row, E, k, order, a.experts);
+    if (threadIdx.x == 0) a.n_experts[0] = n;
+  }
+}
+
+__global__ void predict_kernel(PredictArgs a) {
+  __shared__ int order[MAXE];
+  __shared__ double row[MAXE];
+  predict_block(a, order, row);
+}
+
+// predicted_frequencies (predictor.cpp:222-238)
+__device__ void freq_block(const u64* task_counts, int n_tasks, int m, int E, double s, int task, double* out,
+                           double* raw) {
+  for (int l = 0; l < m; ++l) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      double v = 0.0;
+      if (task >= 0 && task < n_tasks) {
+        v = (double)task_counts[((int64_t)task * m + l) * E + e];
+      } else {
+        for (int t = 0; t < n_tasks; ++t) v += (double)task_counts[((int64_t)t * m + l) * E + e];
+      }
+      raw[e] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < E; e += blockDim.x) out[(int64_t)l * E + e] = smoothed_at_d(raw, E, s, e);
+    __syncthreads();
+  }
+}
+
+__global__ void freq_kernel(const u64* task_counts, int n_tasks, int m, int E, double s, int task, double* out) {
+  __shared__ double raw[MAXE];
+  freq_block(task_counts, n_tasks, m, E, s, task, out, raw);
+}
+
+struct Eq2Args {
+  int m, E, n_tasks;
+  const double* wo;
+  const int32_t* sens;
+  const uint8_t* has_sens;
+  int n_req;
+  const int32_t* req_task;
+  const int32_t* req_tokens;
+  const uint8_t* freq_present;
+  const double* freqs;  // [n_tasks][m][E]
+  int task_aware;
+  double* aggregate;  // [m][E]
+};
+
+// expected_tokens (expert_store.cpp:59-106): thread per (l, e), tasks in sorted order
+__device__ void eq2_block(const Eq2Args& a, double* tok, int* cnt) {
+  for (int t = threadIdx.x; t < a.n_tasks; t += blockDim.x) {
+    double s = 0.0;
+    int c = 0;
+    for (int i = 0; i < a.n_req; ++i)
+      if (a.req_task[i] == t) {
+        s += (double)a.req_tokens[i];
+        ++c;
+      }
+    tok[t] = s;
+    cnt[t] = c;
+  }
+  __syncthreads();
+  const int ME = a.m * a.E;
+  for (int i = threadIdx.x; i < ME; i += blockDim.x) {
+    const int l = i / a.E, e = i % a.E;
+    double agg = 0.0;
+    for (int t = 0; t < a.n_tasks; ++t) {
+      if (cnt[t] == 0) continue;
+      const double volume = tok[t] + cnt[t] * a.wo[t];
+      const bool sensitive = a.task_aware ? (!a.has_sens[t] || a.sens[t * a.m + l] != 0) : true;
+      if (!sensitive) continue;
+      double f = 1.0 / a.E;
+      if (a.freq_present[t]) f = a.freqs[((int64_t)t * a.m + l) * a.E + e];
+      const double grid = volume * f;
+      agg += grid;
+    }
+    a.aggregate[i] = agg;
+  }
+  __syncthreads();
+}
+
+constexpr int MAX_TASKS = 256;
+
+__global__ void eq2_kernel(Eq2Args a) {
+  __shared__ double tok[MAX_TASKS];
+  __shared__ int cnt[MAX_TASKS];
+  eq2_block(a, tok, cnt);
+}
+
+struct PlanArgs {
+  int m, E;
+  const double* aggregate;
+  const uint8_t* resident;  // [m][E]
+  const int32_t* budgets;
+  double per_expert;
+  int32_t* targets;  // [m][E]
+  int32_t* target_sizes;
+  int32_t* evictions;
+  int32_t* n_evict;
+  int32_t* loads;
+  int32_t* n_load;
+  double* duration;
+  double* delta_e;
+  int32_t* total_loads;
+  int targets_given;  // 1: use targets as input (plan_loading only)
+  int select_only;    // 1: select_experts only (no zero-row keep, no plan)
+};
+
+// select_experts + loading_targets + plan_loading (expert_store.cpp:111-195)
+__device__ void plan_block(const PlanArgs& a, int* order) {
+  const int E = a.E;
+  __shared__ int wanted[MAXE];
+  for (int l = 0; l < a.m; ++l) {
+    const double* row = a.aggregate + (int64_t)l * E;
+    ranked_indices_block(row, E, order);
+    if (!a.targets_given && threadIdx.x == 0) {
+      int n = a.budgets[l];
+      for (int i = 0; i < n; ++i) a.targets[l * E + i] = order[i];
+      if (!a.select_only) {
+        bool all_zero = true;
+        for (int e = 0; e < E; ++e)
+          if (row[e] != 0.0) {
+            all_zero = false;
+            break;
+          }
+        if (all_zero) {  // masked layer keeps current residents, lowest indices first
+          n = 0;
+          for (int e = 0; e < E && n < a.budgets[l]; ++e)
+            if (a.resident[l * E + e]) a.targets[l * E + n++] = e;
+        }
+      }
+      a.target_sizes[l] = n;
+    }
+    __syncthreads();
+    if (a.select_only) continue;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) wanted[e] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < a.target_sizes[l]; ++i) wanted[a.targets[l * E + i]] = 1;
+      int ne = 0, nl = 0;
+      for (int e = 0; e < E; ++e)
+        if (a.resident[l * E + e] && !wanted[e]) a.evictions[l * E + ne++] = e;
+      for (int i = 0; i < E; ++i) {
+        const int e = order[i];
+        if (wanted[e] && !a.resident[l * E + e]) a.loads[l * E + nl++] = e;
+      }
+      a.n_evict[l] = ne;
+      a.n_load[l] = nl;
+      a.duration[l] = (double)nl * a.per_expert;
+      if (l == 0) {
+        *a.delta_e = 0.0;
+        *a.total_loads = 0;
+      }
+      *a.delta_e += a.duration[l];
+      *a.total_loads += nl;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void plan_kernel(PlanArgs a) {
+  __shared__ int order[MAXE];
+  plan_block(a, order);
+}
+
+// engine invocation (engine.cpp:367-446): predict -> per-task modulation ->
+// Eq. 2 -> loading_targets -> plan_loading, all in one block
+struct InvocationArgs {
+  PredictArgs pred;
+  const u64* task_counts;  // fitted frequencies come from these
+  int n_tasks;
+  double* fitted;  // scratch [n_tasks][m][E]
+  double* freqs;   // scratch [n_tasks][m][E]
+  Eq2Args eq2;
+  PlanArgs plan;
+};
+
+__global__ void invocation_kernel(InvocationArgs a) {
+  __shared__ int order[MAXE];
+  __shared__ double row[MAXE];
+  __shared__ double tok[MAX_TASKS];
+  __shared__ int cnt[MAX_TASKS];
+  predict_block(a.pred, order, row);
+  __syncthreads();
+  const int m = a.pred.m, E = a.pred.E;
+  for (int t = 0; t < a.n_tasks; ++t)  // fitted_freq_ per profile (engine.cpp:256-257)
+    freq_block(a.task_counts, a.n_tasks, m, E, a.pred.s, t, a.fitted + (int64_t)t * m * E, row);
+  // rows[l][e] = score * fitted, normalised (engine.cpp:394-411)
+  for (int i = threadIdx.x; i < a.n_tasks * m; i += blockDim.x) {
+    const int t = i / m, l = i % m;
+    const double* sc = a.pred.scores + (int64_t)l * E;
+    const double* fit = a.fitted + ((int64_t)t * m + l) * E;
+    double* rows = a.freqs + ((int64_t)t * m + l) * E;
+    double sum = 0.0;
+    for (int e = 0; e < E; ++e) {
+      rows[e] = sc[e] * fit[e];
+      sum += rows[e];
+    }
+    if (sum <= 0.0) {
+      for (int e = 0; e < E; ++e) rows[e] = 1.0 / E;
+    } else {
+      for (int e = 0; e < E; ++e) rows[e] /= sum;
+    }
+  }
+  __syncthreads();
+  eq2_block(a.eq2, tok, cnt);
+  plan_block(a.plan, order);
+}
+
+}  // namespace
+}  // namespace emoe
+
+using namespace emoe;
+
+struct emoe_predictor {
+  int m = 0, E = 0, k = 0, n_tasks = 0;
+  double smoothing = 0.01;
+  u64* layer_counts = nullptr;
+  u64* prompt_counts = nullptr;
+  u64* task_counts = nullptr;
+  int32_t* last_dom = nullptr;
+  bool has_last = false;
+  int32_t* dom = nullptr;
+  size_t dom_cap = 0;
+
+  size_t n_layer() const { return (size_t)(m > 1 ? m - 1 : 0) * E * E; }
+  size_t n_prompt() const { return (size_t)m * E * E; }
+  size_t n_task() const { return (size_t)n_tasks * m * E; }
+  void zero() {
+    if (n_layer()) EMOE_CUDA(cudaMemset(layer_counts, 0, n_layer() * sizeof(u64)));
+    EMOE_CUDA(cudaMemset(prompt_counts, 0, n_prompt() * sizeof(u64)));
+    if (n_task()) EMOE_CUDA(cudaMemset(task_counts, 0, n_task() * sizeof(u64)));
+    has_last = false;
+  }
+};
+
+namespace {
+
+void check_sets(const int32_t* sets, const int32_t* sizes, int rows, int k, int E, const char* field) {
+  for (int l = 0; l < rows; ++l) {
+    if (sizes[l] <= 0) throw ValidationError(std::string(field) + ": empty expert set");
+    EMOE_REQUIRE(sizes[l] <= k, std::string(field) + ": set larger than top_k");
+    for (int i = 0; i < sizes[l]; ++i)
+      if (sets[l * k + i] < 0 || sets[l * k + i] >= E)
+        throw ValidationError(std::string(field) + ": expert index out of range");
+  }
+}
+
+PredictArgs make_predict_args(emoe_predictor* P, int mode, int layer, const int32_t* d_sets, const int32_t* d_sizes,
+                              double* d_scores, int32_t* d_experts, int32_t* d_n) {
+  PredictArgs a;
+  a.mode = mode;
+  a.layer = layer;
+  a.m = P->m;
+  a.E = P->E;
+  a.k = P->k;
+  a.s = P->smoothing;
+  a.layer_counts = P->layer_counts;
+  a.prompt_counts = P->prompt_counts;
+  a.prev_sets = d_sets;
+  a.prev_sizes = d_sizes;
+  a.scores = d_scores;
+  a.experts = d_experts;
+  a.n_experts = d_n;
+  return a;
+}
+
+void validate_predict(emoe_predictor* P, int mode, int layer, const int32_t* sets, const int32_t* sizes) {
+  EMOE_REQUIRE(mode >= 0 && mode <= 2, "predict: unknown mode");
+  if (mode == 2) EMOE_REQUIRE(layer >= 1 && layer < P->m, "predictor.layer: must be in [1, num_layers)");
+  check_sets(sets, sizes, mode == 0 ? P->m : 1, P->k, P->E, mode == 0 ? "predictor.prev_prompt" : "predictor.prev_experts");
+}
+
+void validate_eq2(int m, int E, int n_tasks, int n_req, const int32_t* req_task) {
+  EMOE_REQUIRE(m >= 1 && E >= 1 && E <= MAXE, "expected_tokens: invalid shape");
+  EMOE_REQUIRE(n_tasks <= MAX_TASKS, "expected_tokens: too many tasks");
+  for (int i = 0; i < n_req; ++i)
+    if (req_task[i] < 0 || req_task[i] >= n_tasks) throw ValidationError("expected_tokens.request: unknown task_id");
+}
+
+void validate_budgets(int m, int E, const int32_t* budgets) {
+  for (int l = 0; l < m; ++l)
+    EMOE_REQUIRE(budgets[l] >= 0 && budgets[l] <= E,
+                 "select_experts.budgets: entries must be in [0, experts_per_layer]");
+}
+
+}  // namespace
+
+extern "C" {
+
+int emoe_predictor_create(int m, int E, int k, int n_tasks, double smoothing, emoe_predictor** out) {
+  return guard([&] {
+    EMOE_REQUIRE(out, "predictor_create: null out");
+    EMOE_REQUIRE(m >= 1, "predictor.num_layers: must be >= 1");
+    EMOE_REQUIRE(E >= 1 && E <= MAXE, "predictor.num_experts: must be in [1, 1024]");
+    EMOE_REQUIRE(k >= 1 && k <= E, "predictor.top_k: must be in [1, num_experts]");
+    EMOE_REQUIRE(smoothing >= 0.0, "predictor.smoothing: must be >= 0");
+    EMOE_REQUIRE(n_tasks >= 0 && n_tasks <= MAX_TASKS, "predictor.num_tasks: out of range");
+    auto* P = new emoe_predictor();
+    P->m = m;
+    P->E = E;
+    P->k = k;
+    P->n_tasks = n_tasks;
+    P->smoothing = smoothing;
+    EMOE_CUDA(cudaMalloc(&P->layer_counts, std::max<size_t>(1, P->n_layer()) * sizeof(u64)));
+    EMOE_CUDA(cudaMalloc(&P->prompt_counts, P->n_prompt() * sizeof(u64)));
+    EMOE_CUDA(cudaMalloc(&P->task_counts, std::max<size_t>(1, P->n_task()) * sizeof(u64)));
+    EMOE_CUDA(cudaMalloc(&P->last_dom, m * sizeof(int32_t)));
+    P->zero();
+    *out = P;
+  });
+}
+
+int emoe_predictor_destroy(emoe_predictor* P) {
+  return guard([&] {
+    if (!P) return;
+    for (void* p : {(void*)P->layer_counts, (void*)P->prompt_counts, (void*)P->task_counts, (void*)P->last_dom,
+                    (void*)P->dom})
+      if (p) cudaFree(p);
+    delete P;
+  });
+}
+
+int emoe_predictor_reset(emoe_predictor* P) {
+  return guard([&] {
+    EMOE_REQUIRE(P, "predictor_reset: null");
+    P->zero();
+  });
+}
+
+int emoe_hist_update(emoe_predictor* P, const int32_t* trace, int nP, int T, const int32_t* task_ids, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(P && trace, "hist_update: null argument");
+    if (nP == 0) return;
+    EMOE_REQUIRE(T >= 1, "hist_update: tokens_per_prompt must be >= 1");
+    EMOE_REQUIRE(!task_ids || P->n_tasks > 0, "hist_update: task ids given but the predictor has no tasks");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t need = (size_t)nP * P->m;
+    if (need > P->dom_cap) {
+      if (P->dom) EMOE_CUDA(cudaFree(P->dom));
+      EMOE_CUDA(cudaMalloc(&P->dom, need * sizeof(int32_t)));
+      P->dom_cap = need;
+    }
+    const int E = P->E;
+    const size_t smem = (size_t)(2 * E + (P->m > 1 ? E * E : 0)) * sizeof(int);
+    EMOE_REQUIRE(smem <= 200 * 1024, "hist_update: E too large for the shared-memory histogram");
+    EMOE_CUDA(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    hist_kernel<<<nP * P->m, 256, smem, s>>>(trace, nP, P->m, T, P->k, E, task_ids, P->layer_counts, P->task_counts,
+                                             P->dom);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+    const int pairs = (nP - 1 + (P->has_last ? 1 : 0)) * P->m;
+    if (pairs > 0) {
+      prompt_trans_kernel<<<(pairs + 255) / 256, 256, 0, s>>>(P->dom, nP, P->m, E, P->last_dom, P->has_last ? 1 : 0,
+                                                              P->prompt_counts);
+      EMOE_CUDA(cudaGetLastError());
+    count_launch();
+    }
+    save_last_kernel<<<1, 128, 0, s>>>(P->dom, nP, P->m, P->last_dom);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+    P->has_last = true;
+  });
+}
+
+int emoe_predictor_counts_host(emoe_predictor* P, double* lc, double* pc, double* tc) {
+  return guard([&] {
+    EMOE_REQUIRE(P, "predictor_counts: null");
+    EMOE_CUDA(cudaDeviceSynchronize());
+    auto dump = [](const u64* d, size_t n, double* out) {
+      if (!n || !out) return;
+      std::vector<u64> h(n);
+      EMOE_CUDA(cudaMemcpy(h.data(), d, n * sizeof(u64), cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < n; ++i) out[i] = (double)h[i];
+    };
+    dump(P->layer_counts, P->n_layer(), lc);
+    dump(P->prompt_counts, P->n_prompt(), pc);
+    dump(P->task_counts, P->n_task(), tc);
+  });
+}
+
+int emoe_predictor_set_counts_host(emoe_predictor* P, const double* lc, const double* pc, const double* tc) {
+  return guard([&] {
+    EMOE_REQUIRE(P, "predictor_set_counts: null");
+    auto load = [](u64* d, size_t n, const double* in) {
+      if (!n || !in) return;
+      std::vector<u64> h(n);
+      for (size_t i = 0; i < n; ++i) {
+        EMOE_REQUIRE(in[i] >= 0.0 && in[i] == (double)(u64)in[i], "predictor counts must be non-negative integers");
+        h[i] = (u64)in[i];
+      }
+      EMOE_CUDA(cudaMemcpy(d, h.data(), n * sizeof(u64), cudaMemcpyHostToDevice));
+    };
+    load(P->layer_counts, P->n_layer(), lc);
+    load(P->prompt_counts, P->n_prompt(), pc);
+    load(P->task_counts, P->n_task(), tc);
+  });
+}
+
+int emoe_prompt_expert_sets(const int32_t* trace, int nP, int m, int T, int k, int prompt, int32_t* dominant,
+                            int32_t* sets, int32_t* sizes, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(trace && prompt >= 0 && prompt < nP && m >= 1 && T >= 1 && k >= 1, "prompt_expert_sets: bad args");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // E is bounded by the largest index seen; scan on the device is cheap but the
+    // caller's trace is device memory, so bound E by the predictor maximum.
+    const int E = MAXE;
+    DevBuf<int32_t> dd(m), ds((size_t)m * k), dz(m);
+    prompt_sets_kernel<<<m, 256, E * sizeof(int), s>>>(trace, m, T, k, E, prompt, dd.p, ds.p, dz.p);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+    EMOE_CUDA(cudaStreamSynchronize(s));
+    dd.to_host(dominant);
+    ds.to_host(sets);
+    dz.to_host(sizes);
+  });
+}
+
+int emoe_predict_host(emoe_predictor* P, int mode, const int32_t* sets, const int32_t* sizes, int layer,
+                      double* scores, int32_t* experts, int32_t* n_experts) {
+  return guard([&] {
+    EMOE_REQUIRE(P, "predict: null predictor");
+    validate_predict(P, mode, layer, sets, sizes);
+    const int rows = mode == 0 ? P->m : 1;
+    const int out_rows = mode == 1 ? P->m : rows;
+    DevBuf<int32_t> dsets(sets, (size_t)rows * P->k), dsizes(sizes, rows);
+    DevBuf<double> dsc((size_t)P->m * P->E);
+    DevBuf<int32_t> dex((size_t)P->m * P->k), dn(P->m);
+    EMOE_CUDA(cudaMemset(dex.p, 0xff, (size_t)P->m * P->k * sizeof(int32_t)));
+    predict_kernel<<<1, 128>>>(make_predict_args(P, mode, layer, dsets.p, dsizes.p, dsc.p, dex.p, dn.p));
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+    EMOE_CUDA(cudaDeviceSynchronize());
+    std::vector<double> hs((size_t)P->m * P->E);
+    std::vector<int32_t> he((size_t)P->m * P->k), hn(P->m);
+    dsc.to_host(hs.data());
+    dex.to_host(he.data());
+    dn.to_host(hn.data());
+    std::copy(hs.begin(), hs.begin() + (size_t)out_rows * P->E, scores);
+    std::copy(he.begin(), he.begin() + (size_t)out_rows * P->k, experts);
+    std::copy(hn.begin(), hn.begin() + out_rows, n_experts);
+  });
+}
+
+int emoe_predicted_frequencies_host(emoe_predictor* P, int task, double* out) {
+  return guard([&] {
+    EMOE_REQUIRE(P && out, "predicted_frequencies: null argument");
+    DevBuf<double> d((size_t)P->m * P->E);
+    freq_kernel<<<1, 128>>>(P->task_counts, P->n_tasks, P->m, P->E, P->smoothing, task, d.p);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+    EMOE_CUDA(cudaDeviceSynchronize());
+    d.to_host(out);
+  });
+}
+
+int emoe_expected_tokens_host(int m, int E, int n_tasks, const double* wo, const int32_t* sens, const uint8_t* has_sens,
+                              int n_req, const int32_t* req_task, const int32_t* req_tokens,
+                              const uint8_t* freq_present, const double* freqs, int task_aware, double* aggregate) {
+  return guard([&] {
+    validate_eq2(m, E, n_tasks, n_req, req_task);
+    const size_t nt = std::max(1, n_tasks);
+    DevBuf<double> dwo(nt), dfr(nt * m * E), dagg((size_t)m * E);
+    DevBuf<int32_t> dsens(nt * m), drt(std::max(1, n_req)), drn(std::max(1, n_req));
+    DevBuf<uint8_t> dhs(nt), dfp(nt);
+    if (n_tasks) {
+      EMOE_CUDA(cudaMemcpy(dwo.p, wo, n_tasks * sizeof(double), cudaMemcpyHostToDevice));
+      EMOE_CUDA(cudaMemcpy(dsens.p, sens, (size_t)n_tasks * m * sizeof(int32_t), cudaMemcpyHostToDevice));
+      EMOE_CUDA(cudaMemcpy(dhs.p, has_sens, n_tasks, cudaMemcpyHostToDevice));
+      EMOE_CUDA(cudaMemcpy(dfp.p, freq_present, n_tasks, cudaMemcpyHostToDevice));
+      EMOE_CUDA(cudaMemcpy(dfr.p, freqs, (size_t)n_tasks * m * E * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    if (n_req) {
+      EMOE_CUDA(cudaMemcpy(drt.p, req_task, n_req * sizeof(int32_t), cudaMemcpyHostToDevice));
+      EMOE_CUDA(cudaMemcpy(drn.p, req_tokens, n_req * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    Eq2Args a{m, E, n_tasks, dwo.p, dsens.p, dhs.p, n_req, drt.p, drn.p, dfp.p, dfr.p, task_aware, dagg.p};
+    eq2_kernel<<<1, 256>>>(a);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+    EMOE_CUDA(cudaDeviceSynchronize());
+    dagg.to_host(aggregate);
+  });
+}
+
+static void run_plan(int m, int E, const double* aggregate, const uint8_t* resident, const int32_t* budgets,
+                     double per_expert, int targets_given, int select_only, int32_t* targets, int32_t* target_sizes,
+                     int32_t* ev, int32_t* nev, int32_t* ld, int32_t* nld, double* dur, double* de, int32_t* tl) {
+  EMOE_REQUIRE(m >= 1 && E >= 1 && E <= MAXE, "plan: invalid shape");
+  const size_t ME = (size_t)m * E;
+  DevBuf<double> dagg(aggregate, ME), ddur(m), dde(1);
+  DevBuf<uint8_t> dres(ME);
+  if (resident)
+    EMOE_CUDA(cudaMemcpy(dres.p, resident, ME, cudaMemcpyHostToDevice));
+  else
+    EMOE_CUDA(cudaMemset(dres.p, 0, ME));
+  DevBuf<int32_t> dbud(budgets, m), dtg(ME), dts(m), dev(ME), dnev(m), dld(ME), dnld(m), dtl(1);
+  if (targets_given) {
+    EMOE_CUDA(cudaMemcpy(dtg.p, targets, ME * sizeof(int32_t), cudaMemcpyHostToDevice));
+    EMOE_CUDA(cudaMemcpy(dts.p, target_sizes, m * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  PlanArgs a{m, E, dagg.p, dres.p, dbud.p, per_expert, dtg.p, dts.p, dev.p, dnev.p, dld.p, dnld.p, ddur.p, dde.p,
+             dtl.p, targets_given, select_only};
+  plan_kernel<<<1, 128>>>(a);
+  EMOE_CUDA(cudaGetLastError());
+    count_launch();
+  EMOE_CUDA(cudaDeviceSynchronize());
+  if (!targets_given) {
+    if (targets) dtg.to_host(targets);
+    if (target_sizes) dts.to_host(target_sizes);
+  }
+  if (!select_only) {
+    if (ev) dev.to_host(ev);
+    if (nev) dnev.to_host(nev);
+    if (ld) dld.to_host(ld);
+    if (nld) dnld.to_host(nld);
+    if (dur) ddur.to_host(dur);
+    if (de) dde.to_host(de);
+    if (tl) dtl.to_host(tl);
+  }
+}
+
+int emoe_select_experts_host(const double* aggregate, int m, int E, const int32_t* budgets, int32_t* out) {
+  return guard([&] {
+    validate_budgets(m, E, budgets);
+    std::vector<int32_t> sizes(m);
+    run_plan(m, E, aggregate, nullptr, budgets, 0.0, 0, 1, out, sizes.data(), nullptr, nullptr, nullptr, nullptr,
+             nullptr, nullptr, nullptr);
+  });
+}
+
+int emoe_loading_targets_host(const double* aggregate, int m, int E, const uint8_t* resident, const int32_t* budgets,
+                              int32_t* out, int32_t* sizes) {
+  return guard([&] {
+    validate_budgets(m, E, budgets);
+    std::vector<int32_t> ev((size_t)m * E), nev(m), ld((size_t)m * E), nld(m), tl(1);
+    std::vector<double> dur(m), de(1);
+    run_plan(m, E, aggregate, resident, budgets, 0.0, 0, 0, out, sizes, ev.data(), nev.data(), ld.data(), nld.data(),
+             dur.data(), de.data(), tl.data());
+  });
+}
+
+int emoe_plan_loading_host(const uint8_t* resident, const int32_t* budgets, int m, int E, const int32_t* target,
+                           const int32_t* target_sizes, const double* aggregate, double per_expert, int32_t* ev,
+                           int32_t* nev, int32_t* ld, int32_t* nld, double* dur, double* de, int32_t* tl) {
+  return guard([&] {
+    for (int l = 0; l < m; ++l) {
+      if (target_sizes[l] > budgets[l]) throw ValidationError("plan_loading.target: exceeds layer budget");
+      std::vector<char> seen(E, 0);
+      for (int i = 0; i < target_sizes[l]; ++i) {
+        const int e = target[l * E + i];
+        if (e < 0 || e >= E) throw ValidationError("plan_loading.target: expert index out of range");
+        if (seen[e]) throw ValidationError("plan_loading.target: duplicate expert index");
+        seen[e] = 1;
+      }
+    }
+    std::vector<int32_t> tg(target, target + (size_t)m * E), ts(target_sizes, target_sizes + m);
+    run_plan(m, E, aggregate, resident, budgets, per_expert, 1, 0, tg.data(), ts.data(), ev, nev, ld, nld, dur, de,
+             tl);
+  });
+}
+
+int emoe_invocation_host(emoe_predictor* P, int mode, const int32_t* sets, const int32_t* sizes, int n_tasks,
+                         const double* wo, const int32_t* sens, const uint8_t* has_sens, int n_req,
+                         const int32_t* req_task, const int32_t* req_tokens, int task_aware, const uint8_t* resident,
+                         const int32_t* budgets, double per_expert, double* aggregate, int32_t* evictions,
+                         int32_t* n_evict, int32_t* loads, int32_t* n_load, double* delta_e) {
+  return guard([&] {
+    EMOE_REQUIRE(P, "invocation: null predictor");
+    EMOE_REQUIRE(mode == 0 || mode == 1, "invocation: mode must be 0 (all layers) or 1 (chained)");
+    EMOE_REQUIRE(n_tasks == P->n_tasks, "invocation: profile count must equal the predictor's task count");
+    validate_predict(P, mode, 0, sets, sizes);
+    validate_eq2(P->m, P->E, n_tasks, n_req, req_task);
+    validate_budgets(P->m, P->E, budgets);
+    const int m = P->m, E = P->E, k = P->k;
+    const size_t ME = (size_t)m * E, nt = std::max(1, n_tasks);
+    const int rows = mode == 0 ? m : 1;
+    DevBuf<int32_t> dsets(sets, (size_t)rows * k), dsizes(sizes, rows), dex((size_t)m * k), dn(m);
+    DevBuf<double> dsc(ME), dfit(nt * ME), dfreq(nt * ME), dwo(nt), dagg(ME), ddur(m), dde(1);
+    DevBuf<int32_t> dsens(nt * m), drt(std::max(1, n_req)), drn(std::max(1, n_req));
+    DevBuf<uint8_t> dhs(nt), dfp(nt), dres(resident, ME);
+    DevBuf<int32_t> dbud(budgets, m), dtg(ME), dts(m), dev(ME), dnev(m), dld(ME), dnld(m), dtl(1);
+    if (n_tasks) {
+      EMOE_CUDA(cudaMemcpy(dwo.p, wo, n_tasks * sizeof(double), cudaMemcpyHostToDevice));
+      EMOE_CUDA(cudaMemcpy(dsens.p, sens, (size_t)n_tasks * m * sizeof(int32_t), cudaMemcpyHostToDevice));
+      EMOE_CUDA(cudaMemcpy(dhs.p, has_sens, n_tasks, cudaMemcpyHostToDevice));
+      EMOE_CUDA(cudaMemset(dfp.p, 1, n_tasks));
+    }
+    if (n_req) {
+      EMOE_CUDA(cudaMemcpy(drt.p, req_task, n_req * sizeof(int32_t), cudaMemcpyHostToDevice));
+      EMOE_CUDA(cudaMemcpy(drn.p, req_tokens, n_req * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    InvocationArgs a;
+    a.pred = make_predict_args(P, mode, 0, dsets.p, dsizes.p, dsc.p, dex.p, dn.p);
+    a.task_counts = P->task_counts;
+    a.n_tasks = n_tasks;
+    a.fitted = dfit.p;
+    a.freqs = dfreq.p;
+    a.eq2 = Eq2Args{m, E, n_tasks, dwo.p, dsens.p, dhs.p, n_req, drt.p, drn.p, dfp.p, dfreq.p, task_aware, dagg.p};
+    a.plan = PlanArgs{m, E, dagg.p, dres.p, dbud.p, per_expert, dtg.p, dts.p, dev.p, dnev.p, dld.p, dnld.p, ddur.p,
+                      dde.p, dtl.p, 0, 0};
+    invocation_kernel<<<1, 128>>>(a);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+    EMOE_CUDA(cudaDeviceSynchronize());
+    dagg.to_host(aggregate);
+    dev.to_host(evictions);
+    dnev.to_host(n_evict);
+    dld.to_host(loads);
+    dnld.to_host(n_load);
+    dde.to_host(delta_e);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,412 @@
+// K1: gate logits + top-k + residency remap (route_token) + gate weights.
+//
+// bf16 activations: a block of 128 tokens x all E experts is one small GEMM
+// (x[128 x d] . wg[E x d]^T) on mma.sync.m16n8k16 (bf16 in, fp32 out): the
+// op is HBM-bound on reading x once (d*2 bytes per token), so the legacy
+// tensor path is enough to keep the FFMA pipe out of the way; x and wg
+// k-chunks are double-buffered in XOR-swizzled shared memory by cp.async.
+// fp32 activations (config 1) use a warp-per-token FFMA dot product.
+//
+// The routing epilogue runs one thread per token on the logits row in shared
+// memory and restates the reference exactly:
+//   top-k        descending logit, ascending index on ties
+//   route_token  first resident gate choice; else the resident expert with the
+//                highest layer score, smallest index on ties; empty scores ->
+//                smallest resident (expert_store.cpp:206-220)
+//   forced miss  no resident expert -> {choice0, -1, miss} (engine.cpp:533-537)
+// plus the builder-defined k-slot served set and weights.
+// Per-block expert counts feed the deterministic permutation (permute.cu).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace emoe {
+
+namespace {
+
+constexpr int RT = kRouteBlockTokens;  // 128 tokens per block
+constexpr int KC = 64;                 // k chunk (one 128-B row of bf16)
+constexpr int MAX_E = 128;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// XOR-swizzled [rows][64] bf16 tile: 16-B chunk c of row r lives at chunk c ^ (r & 7)
+__device__ __forceinline__ uint32_t swz(int r, int chunk) { return r * 128 + ((chunk ^ (r & 7)) << 4); }
+
+__device__ __forceinline__ void ldmatrix_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldmatrix_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+struct SharedRouteState {
+  uint8_t resident[MAX_E];
+  double scores[MAX_E];
+  int counts[MAX_E];
+  int n_res;
+  int first_res;
+};
+
+__device__ void load_route_state(SharedRouteState& st, const RouteArgs& a) {
+  for (int e = threadIdx.x; e < a.E; e += blockDim.x) {
+    st.resident[e] = a.resident[e];
+    st.scores[e] = a.scores ? a.scores[e] : 0.0;
+    st.counts[e] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n = 0, first = -1;
+    for (int e = 0; e < a.E; ++e)
+      if (st.resident[e]) {
+        if (first < 0) first = e;
+        ++n;
+      }
+    st.n_res = n;
+    st.first_res = first;
+  }
+  __syncthreads();
+}
+
+// Residency remap + served set + weights for one token whose ranked gate
+// choices are ti[0..k).  lg = logits row (null for choice input: the served
+// slots then share the weight uniformly).
+__device__ void route_tail(const int* ti, const float* lg, int64_t t, const RouteArgs& a, const RouteOut& o,
+                           SharedRouteState& st) {
+  const int E = a.E, k = a.k;
+  int ex = -1, rk = -1, hit = 0;
+  if (st.n_res == 0) {
+    ex = ti[0];
+    if (!a.forced_miss) atomicExch(a.error_flag, 3);
+  } else {
+    for (int r = 0; r < k; ++r)
+      if (st.resident[ti[r]]) {
+        ex = ti[r];
+        rk = r;
+        hit = r == 0;
+        break;
+      }
+    if (rk < 0) {
+      int best = st.first_res;
+      if (a.scores)
+        for (int e = 0; e < E; ++e)
+          if (st.resident[e] && st.scores[e] > st.scores[best]) best = e;
+      ex = best;
+    }
+  }
+  if (o.route_expert) o.route_expert[t] = ex;
+  if (o.route_rank) o.route_rank[t] = rk;
+  if (o.route_hit) o.route_hit[t] = (uint8_t)hit;
+
+  int si[8];
+  int ns = 0;
+  if (st.n_res > 0) {
+    if (rk >= 0) {
+      for (int r = 0; r < k; ++r)
+        if (st.resident[ti[r]]) si[ns++] = ti[r];
+    } else {
+      si[ns++] = ex;
+    }
+  }
+  float w[8];
+  if (lg == nullptr) {
+    for (int j = 0; j < ns; ++j) w[j] = 1.0f / ns;
+  } else if (a.weight_mode == 0) {
+    if (ns > 0) {
+      const float mx = lg[si[0]];
+      float den = 0.0f;
+      for (int j = 0; j < ns; ++j) {
+        w[j] = expf(lg[si[j]] - mx);
+        den += w[j];
+      }
+      for (int j = 0; j < ns; ++j) w[j] = w[j] / den;
+    }
+  } else {
+    const float mx = lg[ti[0]];
+    float den = 0.0f;
+    for (int e = 0; e < E; ++e) den += expf(lg[e] - mx);
+    for (int j = 0; j < ns; ++j) w[j] = expf(lg[si[j]] - mx) / den;
+  }
+  if (o.served_idx)
+    for (int j = 0; j < k; ++j) {
+      o.served_idx[t * k + j] = j < ns ? si[j] : -1;
+      o.served_w[t * k + j] = j < ns ? w[j] : 0.0f;
+    }
+  for (int j = 0; j < ns; ++j) atomicAdd(&st.counts[si[j]], 1);
+}
+
+// One token from its logits row: top-k (descending, ascending index on ties) then route_tail.
+__device__ void route_one_token(const float* lg, int64_t t, const RouteArgs& a, const RouteOut& o,
+                                SharedRouteState& st) {
+  const int E = a.E, k = a.k;
+  int ti[8];
+  uint32_t used[MAX_E / 32] = {0, 0, 0, 0};
+  for (int r = 0; r < k; ++r) {
+    int best = -1;
+    float bv = 0.0f;
+    for (int e = 0; e < E; ++e) {
+      if (used[e >> 5] & (1u << (e & 31))) continue;
+      float v = lg[e];
+      if (best < 0 || v > bv) {
+        best = e;
+        bv = v;
+      }
+    }
+    ti[r] = best;
+    used[best >> 5] |= 1u << (best & 31);
+    if (o.topk_idx) o.topk_idx[t * k + r] = best;
+  }
+  route_tail(ti, lg, t, a, o, st);
+}
+
+__device__ void flush_block_counts(const RouteArgs& a, const RouteOut& o, SharedRouteState& st) {
+  __syncthreads();
+  if (o.block_counts)
+    for (int e = threadIdx.x; e < a.E; e += blockDim.x) o.block_counts[(int64_t)blockIdx.x * a.E + e] = st.counts[e];
+}
+
+// ---------------------------------------------------------------------------
+// bf16: mma.sync gate.  NT = number of 8-expert column tiles (E <= 8*NT).
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(128) gate_route_bf16_kernel(const __nv_bfloat16* __restrict__ x,
+                                                              const __nv_bfloat16* __restrict__ wg, RouteArgs a,
+                                                              RouteOut o) {
+  constexpr int EP = NT * 8;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* xs = smem;                      // [2][RT][64] bf16
+  uint8_t* ws = smem + 2 * RT * 128;       // [2][EP][64] bf16
+  float* logits = reinterpret_cast<float*>(smem);  // reused after the K loop: [RT][EP+1]
+  __shared__ SharedRouteState st;
+
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int64_t t0 = (int64_t)blockIdx.x * RT;
+  const int d = a.d;
+  const int nk = d / KC;
+
+  auto issue = [&](int kc, int buf) {
+    uint8_t* xb = xs + buf * RT * 128;
+    uint8_t* wb = ws + buf * EP * 128;
+    for (int i = tid; i < RT * 8; i += 128) {
+      const int r = i >> 3, c = i & 7;
+      const int64_t t = t0 + r;
+      const bool ok = t < a.T;
+      cp_async16(xb + swz(r, c), x + (ok ? t : 0) * d + kc * KC + c * 8, ok);
+    }
+    for (int i = tid; i < EP * 8; i += 128) {
+      const int r = i >> 3, c = i & 7;
+      const bool ok = r < a.E;
+      cp_async16(wb + swz(r, c), wg + (int64_t)(ok ? r : 0) * d + kc * KC + c * 8, ok);
+    }
+    cp_async_commit();
+  };
+
+  float acc[2][NT][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.0f;
+
+  issue(0, 0);
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + 1 < nk) {
+      issue(kc + 1, (kc + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const uint32_t xb = smem_u32(xs + (kc & 1) * RT * 128);
+    const uint32_t wb = smem_u32(ws + (kc & 1) * EP * 128);
+#pragma unroll
+    for (int ks = 0; ks < KC / 16; ++ks) {
+      uint32_t af[2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int r = warp * 32 + mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int ch = ks * 2 + (lane >> 4);
+        ldmatrix_x4(xb + swz(r, ch), af[mt][0], af[mt][1], af[mt][2], af[mt][3]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        uint32_t b0, b1;
+        const int r = nt * 8 + (lane & 7);
+        const int ch = ks * 2 + ((lane >> 3) & 1);
+        ldmatrix_x2(wb + swz(r, ch), b0, b1);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) mma_bf16_16816(acc[mt][nt], af[mt][0], af[mt][1], af[mt][2], af[mt][3], b0, b1);
+      }
+    }
+    __syncthreads();
+  }
+
+  // accumulators -> logits tile in shared memory (stage buffers are free now)
+  const int g = lane >> 2, q = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int r = warp * 32 + mt * 16 + g;
+      const int c = nt * 8 + q * 2;
+      logits[r * (EP + 1) + c] = acc[mt][nt][0];
+      logits[r * (EP + 1) + c + 1] = acc[mt][nt][1];
+      logits[(r + 8) * (EP + 1) + c] = acc[mt][nt][2];
+      logits[(r + 8) * (EP + 1) + c + 1] = acc[mt][nt][3];
+    }
+  load_route_state(st, a);  // contains __syncthreads
+  const int64_t t = t0 + tid;
+  if (t < a.T) {
+    const float* lg = logits + tid * (EP + 1);
+    if (o.logits)
+      for (int e = 0; e < a.E; ++e) o.logits[t * a.E + e] = lg[e];
+    route_one_token(lg, t, a, o, st);
+  }
+  flush_block_counts(a, o, st);
+}
+
+// ---------------------------------------------------------------------------
+// fp32: warp-per-token FFMA gate, logits staged in shared memory
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) gate_route_f32_kernel(const float* __restrict__ x,
+                                                             const float* __restrict__ wg, RouteArgs a, RouteOut o) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  float* logits = reinterpret_cast<float*>(smem);  // [RT][E]
+  __shared__ SharedRouteState st;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t t0 = (int64_t)blockIdx.x * RT;
+  for (int r = warp; r < RT; r += 4) {
+    const int64_t t = t0 + r;
+    if (t >= a.T) break;
+    const float* xr = x + t * a.d;
+    for (int e = 0; e < a.E; ++e) {
+      const float* wr = wg + (int64_t)e * a.d;
+      float s = 0.0f;
+      for (int i = lane; i < a.d; i += 32) s = fmaf(xr[i], wr[i], s);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) logits[r * a.E + e] = s;
+    }
+  }
+  load_route_state(st, a);
+  const int64_t t = t0 + threadIdx.x;
+  if (t < a.T) {
+    const float* lg = logits + threadIdx.x * a.E;
+    if (o.logits)
+      for (int e = 0; e < a.E; ++e) o.logits[t * a.E + e] = lg[e];
+    route_one_token(lg, t, a, o, st);
+  }
+  flush_block_counts(a, o, st);
+}
+
+// ---------------------------------------------------------------------------
+// routing-driven mode: logits supplied by the caller
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) route_from_logits_kernel(const float* __restrict__ logits, RouteArgs a,
+                                                                RouteOut o) {
+  __shared__ SharedRouteState st;
+  load_route_state(st, a);
+  const int64_t t = (int64_t)blockIdx.x * RT + threadIdx.x;
+  if (t < a.T) {
+    const float* lg = logits + t * a.E;
+    if (o.logits && o.logits != logits)
+      for (int e = 0; e < a.E; ++e) o.logits[t * a.E + e] = lg[e];
+    route_one_token(lg, t, a, o, st);
+  }
+  flush_block_counts(a, o, st);
+}
+
+// route_token over caller-supplied ranked gate choices [T][k]
+__global__ void __launch_bounds__(128) route_from_choices_kernel(const int32_t* __restrict__ choices, RouteArgs a,
+                                                                 RouteOut o) {
+  __shared__ SharedRouteState st;
+  load_route_state(st, a);
+  const int64_t t = (int64_t)blockIdx.x * RT + threadIdx.x;
+  if (t < a.T) {
+    int ti[8];
+    for (int r = 0; r < a.k; ++r) ti[r] = choices[t * a.k + r];
+    route_tail(ti, nullptr, t, a, o, st);
+  }
+  flush_block_counts(a, o, st);
+}
+
+}  // namespace
+
+void launch_route_from_choices(const int32_t* choices, const RouteArgs& a, const RouteOut& o, cudaStream_t s) {
+  EMOE_REQUIRE(a.E >= 1 && a.E <= MAX_E, "route: num_experts must be in [1, 128]");
+  EMOE_REQUIRE(a.k >= 1 && a.k <= 8, "route: top_k must be in [1, 8]");
+  const int nblocks = (int)ceil_div(a.T, RT);
+  if (nblocks == 0) return;
+  route_from_choices_kernel<<<nblocks, RT, 0, s>>>(choices, a, o);
+  EMOE_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+void launch_gate_route(const void* x, const void* wg, int dtype, const RouteArgs& a, const RouteOut& o,
+                       cudaStream_t s) {
+  EMOE_REQUIRE(a.E >= 1 && a.E <= MAX_E, "route: num_experts must be in [1, 128]");
+  EMOE_REQUIRE(a.k >= 1 && a.k <= 8 && a.k <= a.E, "route: top_k must be in [1, min(8, E)]");
+  const int nblocks = (int)ceil_div(a.T, RT);
+  if (nblocks == 0) return;
+  if (dtype == DT_F32) {
+    const size_t smem = (size_t)RT * a.E * sizeof(float);
+    EMOE_REQUIRE(smem <= 48 * 1024, "route: fp32 logits tile exceeds 48 KB");
+    gate_route_f32_kernel<<<nblocks, 128, smem, s>>>(static_cast<const float*>(x), static_cast<const float*>(wg), a,
+                                                     o);
+  } else {
+    EMOE_REQUIRE(a.d % KC == 0, "route: d_model must be a multiple of 64 for bf16");
+    const int nt = (a.E + 7) / 8;
+    auto go = [&](auto kernel, int NTv) {
+      const int EP = NTv * 8;
+      size_t smem = (size_t)2 * RT * 128 + (size_t)2 * EP * 128;
+      const size_t lsm = (size_t)RT * (EP + 1) * sizeof(float);
+      if (lsm > smem) smem = lsm;
+      EMOE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kernel<<<nblocks, 128, smem, s>>>(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg),
+                                        a, o);
+    };
+    if (nt <= 1)
+      go(gate_route_bf16_kernel<1>, 1);
+    else if (nt <= 2)
+      go(gate_route_bf16_kernel<2>, 2);
+    else if (nt <= 4)
+      go(gate_route_bf16_kernel<4>, 4);
+    else if (nt <= 8)
+      go(gate_route_bf16_kernel<8>, 8);
+    else
+      go(gate_route_bf16_kernel<16>, 16);
+  }
+  EMOE_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+void launch_route_from_logits(const float* logits, const RouteArgs& a, const RouteOut& o, cudaStream_t s) {
+  EMOE_REQUIRE(a.E >= 1 && a.E <= MAX_E, "route: num_experts must be in [1, 128]");
+  EMOE_REQUIRE(a.k >= 1 && a.k <= 8 && a.k <= a.E, "route: top_k must be in [1, min(8, E)]");
+  const int nblocks = (int)ceil_div(a.T, RT);
+  if (nblocks == 0) return;
+  route_from_logits_kernel<<<nblocks, RT, 0, s>>>(logits, a, o);
+  EMOE_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+}  // namespace emoe

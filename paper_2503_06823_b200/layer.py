@@ -1,0 +1,183 @@
+"""MoELayer: the predicted-residency MoE layer forward over the C ABI.
+
+PyTorch is used only as plumbing here: device buffers, streams and pinned
+host memory.  All compute runs in lib/libemoe.so (sm_100a kernels).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, Optional, Sequence
+
+import numpy as np
+import torch
+
+from ._lib import LayerConfig, Workspace, lib
+from .moesim import check
+
+_DT = {"bf16": (0, torch.bfloat16, 2), "fp32": (1, torch.float32, 4)}
+_ACT = {"swiglu": 0, "relu": 1}
+_WM = {"topk_softmax": 0, "full_softmax": 1}
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class _CudaArray:
+    """Zero-copy view of a raw device pointer for torch.as_tensor."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _view(ptr, shape, torch_dtype):
+    if torch_dtype == torch.bfloat16:  # no bf16 typestr: view the bytes as int16 then reinterpret
+        return torch.as_tensor(_CudaArray(ptr, shape, "<i2"), device="cuda").view(torch.bfloat16)
+    ts = {torch.float32: "<f4", torch.int32: "<i4", torch.int64: "<i8", torch.uint8: "|u1"}[torch_dtype]
+    return torch.as_tensor(_CudaArray(ptr, shape, ts), device="cuda")
+
+
+class MoELayer:
+    def __init__(self, d_model: int, d_ff: int, num_experts: int, top_k: int, *, activation: str = "swiglu",
+                 dtype: str = "bf16", weight_mode: str = "topk_softmax", num_slots: Optional[int] = None,
+                 max_tokens: int = 65536, forced_miss: bool = False):
+        self.d, self.f, self.E, self.k = d_model, d_ff, num_experts, top_k
+        self.dtype_name = dtype
+        self.code, self.torch_dtype, self.elem = _DT[dtype]
+        self.activation = activation
+        self.num_slots = num_slots or num_experts
+        self.max_tokens = max_tokens
+        cfg = LayerConfig(d_model, d_ff, num_experts, top_k, _ACT[activation], self.code, _WM[weight_mode],
+                          self.num_slots, max_tokens, int(forced_miss))
+        h = C.c_void_p()
+        check(lib.emoe_layer_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.emoe_layer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    # -- weights ---------------------------------------------------------
+    def _host(self, t: torch.Tensor, shape) -> torch.Tensor:
+        t = t.detach().to("cpu", self.torch_dtype).contiguous()
+        assert tuple(t.shape) == tuple(shape), (t.shape, shape)
+        return t
+
+    def set_gate(self, wg: torch.Tensor) -> None:
+        wg = self._host(wg, (self.E, self.d))
+        check(lib.emoe_layer_set_gate_host(self.h, C.c_void_p(wg.data_ptr())))
+
+    def register_expert(self, e: int, w1: torch.Tensor, w3: Optional[torch.Tensor], w2: torch.Tensor) -> None:
+        w1 = self._host(w1, (self.f, self.d))
+        w2 = self._host(w2, (self.d, self.f))
+        w3p = None
+        if self.activation == "swiglu":
+            w3 = self._host(w3, (self.f, self.d))
+            w3p = C.c_void_p(w3.data_ptr())
+        check(lib.emoe_layer_register_expert_host(self.h, e, C.c_void_p(w1.data_ptr()), w3p,
+                                                  C.c_void_p(w2.data_ptr())))
+
+    def set_scores(self, scores: Optional[Sequence[float]]) -> None:
+        if scores is None or len(scores) == 0:
+            check(lib.emoe_layer_set_scores_host(self.h, None))
+            return
+        s = np.ascontiguousarray(np.asarray(scores, np.float64))
+        check(lib.emoe_layer_set_scores_host(self.h, s.ctypes.data_as(C.c_void_p)))
+
+    # -- residency (two-phase, engine.cpp:431-464) ------------------------
+    def begin_load(self, evictions: Sequence[int], loads: Sequence[int], stream=None) -> None:
+        ev = np.ascontiguousarray(np.asarray(list(evictions) or [0], np.int32))
+        ld = np.ascontiguousarray(np.asarray(list(loads) or [0], np.int32))
+        check(lib.emoe_layer_begin_load(self.h, ev.ctypes.data_as(C.c_void_p), len(evictions),
+                                        ld.ctypes.data_as(C.c_void_p), len(loads), _stream_ptr(stream)))
+
+    def poll_loads(self, blocking: bool = False, stream=None) -> bool:
+        pending = C.c_int(0)
+        check(lib.emoe_layer_poll_loads(self.h, int(blocking), _stream_ptr(stream), C.byref(pending)))
+        return bool(pending.value)
+
+    def residency(self) -> np.ndarray:
+        out = np.zeros(self.E, np.uint8)
+        check(lib.emoe_layer_residency(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def last_load_stats(self):
+        b, ms = C.c_double(0), C.c_double(0)
+        check(lib.emoe_layer_last_load_stats(self.h, C.byref(b), C.byref(ms)))
+        return b.value, ms.value
+
+    def load_initial(self, experts: Sequence[int]) -> None:
+        """Make `experts` resident (blocking), evicting whatever else is resident."""
+        cur = set(np.flatnonzero(self.residency()).tolist())
+        want = set(int(e) for e in experts)
+        self.begin_load(sorted(cur - want), sorted(want - cur))
+        self.poll_loads(blocking=True)
+        torch.cuda.synchronize()
+
+    # -- forward -----------------------------------------------------------
+    def forward(self, x: torch.Tensor, logits: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                stream=None) -> torch.Tensor:
+        assert x.is_cuda and x.dtype == self.torch_dtype and x.is_contiguous() and x.shape[1] == self.d
+        T = x.shape[0]
+        if out is None:
+            out = torch.empty_like(x)
+        lp = None
+        if logits is not None:
+            assert logits.is_cuda and logits.dtype == torch.float32 and logits.shape == (T, self.E)
+            lp = C.c_void_p(logits.contiguous().data_ptr())
+        check(lib.emoe_moe_forward(self.h, C.c_void_p(x.data_ptr()), lp, C.c_void_p(out.data_ptr()), T,
+                                   _stream_ptr(stream)))
+        return out
+
+    __call__ = forward
+
+    def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor, stream=None) -> torch.Tensor:
+        """End-to-end through host buffers: H2D of x, forward, D2H of y."""
+        assert x_host.device.type == "cpu" and x_host.dtype == self.torch_dtype and x_host.is_contiguous()
+        check(lib.emoe_moe_forward_host(self.h, C.c_void_p(x_host.data_ptr()), C.c_void_p(y_host.data_ptr()),
+                                        x_host.shape[0], _stream_ptr(stream)))
+        return y_host
+
+    def route(self, x: Optional[torch.Tensor] = None, logits: Optional[torch.Tensor] = None, stream=None) -> None:
+        T = x.shape[0] if x is not None else logits.shape[0]
+        check(lib.emoe_route(self.h, C.c_void_p(x.data_ptr()) if x is not None else None,
+                             C.c_void_p(logits.data_ptr()) if logits is not None else None, T, _stream_ptr(stream)))
+
+    def set_profiling(self, enable: bool = True) -> None:
+        check(lib.emoe_layer_set_profiling(self.h, int(enable)))
+
+    def stage_times(self) -> Dict[str, float]:
+        """ms of the last forward's stages (needs set_profiling(True))."""
+        ms = (C.c_float * 5)()
+        check(lib.emoe_layer_stage_times(self.h, ms))
+        return dict(zip(["route", "permute", "gemm1", "gemm2", "combine"], [float(v) for v in ms]))
+
+    def workspace(self) -> Dict[str, torch.Tensor]:
+        """Views of the last forward's intermediates (valid until the next call)."""
+        w = Workspace()
+        check(lib.emoe_layer_workspace(self.h, C.byref(w)))
+        T, R, E, k = w.T, w.rows_cap, self.E, self.k
+        return {
+            "logits": _view(w.logits, (T, E), torch.float32),
+            "topk_idx": _view(w.topk_idx, (T, k), torch.int32),
+            "route_expert": _view(w.route_expert, (T,), torch.int32),
+            "route_rank": _view(w.route_rank, (T,), torch.int32),
+            "route_hit": _view(w.route_hit, (T,), torch.uint8),
+            "served_idx": _view(w.served_idx, (T, k), torch.int32),
+            "served_w": _view(w.served_w, (T, k), torch.float32),
+            "counts": _view(w.counts, (E,), torch.int32),
+            "seg_offsets": _view(w.seg_offsets, (E + 1,), torch.int64),
+            "pos": _view(w.pos, (T, k), torch.int32),
+            "row_token": _view(w.row_token, (R,), torch.int32),
+            "x_perm": _view(w.x_perm, (R, self.d), self.torch_dtype),
+            "h": _view(w.h, (R, self.f), self.torch_dtype),
+            "y_perm": _view(w.y_perm, (R, self.d), self.torch_dtype),
+            "slot_of_expert": _view(w.slot_of_expert, (E,), torch.int32),
+            "resident": _view(w.resident, (E,), torch.uint8),
+        }

@@ -1,0 +1,142 @@
+"""GPU parity of the MoE layer forward (A1-A5) against the CPU oracle.
+
+Each stage is checked on the same inputs:
+  A1 gate logits (fp32 accumulate) vs oracle_gate_logits_f32   (tolerance)
+  A1+A2 top-k / route_token / served set given the GPU logits   (bit-exact)
+  A3 counts / padded offsets / positions / row sources          (bit-exact)
+     permuted rows == source rows                               (bit-exact)
+  A4 expert FFN rows vs oracle_expert_ffn (mirrored rounding)   (tolerance)
+  A5 combine vs oracle_combine of the GPU expert outputs        (tolerance)
+  end to end: sampled tokens vs the full oracle chain           (tolerance)
+"""
+import numpy as np
+import pytest
+import torch
+
+from helpers import (assert_bf16_close, assert_f32_close, build_layer, to_f32, trace_logits)
+
+CASES = {
+    # name: E, d, f, k, dtype, act, weight_mode, slots, resident, T
+    "mixtral_small": (8, 512, 1024, 2, "bf16", "swiglu", "topk_softmax", 4, [1, 3, 4, 6], 1000),
+    "mixtral_full_resident": (8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", 8, None, 640),
+    "switch_small": (32, 256, 512, 1, "bf16", "relu", "full_softmax", 8, [0, 2, 5, 7, 11, 19, 23, 31], 777),
+    "config1_fp32_phi05": (8, 1024, 3584, 2, "fp32", "swiglu", "topk_softmax", 4, [0, 2, 5, 7], 512),
+    "config1_fp32_phi1": (8, 1024, 3584, 2, "fp32", "swiglu", "topk_softmax", 8, None, 512),
+}
+
+
+def run_case(name, port, use_trace_logits=False, scores=None):
+    E, d, f, k, dtype, act, wm, slots, resident, T = CASES[name]
+    layer, wg, experts = build_layer(E, d, f, k, dtype, act, wm, slots, resident, max_tokens=max(T, 128))
+    if scores is not None:
+        layer.set_scores(scores)
+    g = torch.Generator().manual_seed(7)
+    td = torch.bfloat16 if dtype == "bf16" else torch.float32
+    x = torch.randn(T, d, generator=g).to(td)
+    xd = x.cuda()
+    logits_in = None
+    if use_trace_logits:
+        choices = np.stack([np.random.default_rng(3).permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+        logits_in = torch.from_numpy(trace_logits(choices, E)).cuda()
+    y = layer.forward(xd, logits=logits_in)
+    torch.cuda.synchronize()
+    ws = {key: v.clone() for key, v in layer.workspace().items()}
+    res = layer.residency()
+    return dict(layer=layer, wg=wg, experts=experts, x=x, y=y, ws=ws, resident=res, T=T, E=E, d=d, f=f, k=k,
+                dtype=dtype, act=act, wm=wm, logits_in=logits_in)
+
+
+def check_case(c, port, scores=None):
+    T, E, k, d, f = c["T"], c["E"], c["k"], c["d"], c["f"]
+    ws = c["ws"]
+    x32 = to_f32(c["x"])
+    lg = to_f32(ws["logits"])
+    # A1 logits
+    if c["logits_in"] is None:
+        ref_lg = port.gate_logits(x32, to_f32(c["wg"]))
+        err = np.abs(lg - ref_lg).max() / max(np.abs(ref_lg).max(), 1e-30)
+        assert err < 1e-4, f"gate logits rel err {err:.3e}"
+    else:
+        assert np.array_equal(lg, to_f32(c["logits_in"]))
+    # A1 + A2 on the GPU logits: bit-exact
+    o = port.gate_route(lg, k, 0 if c["wm"] == "topk_softmax" else 1, c["resident"], scores)
+    assert np.array_equal(to_f32(ws["topk_idx"]).astype(np.int32), o["topk_idx"])
+    assert np.array_equal(ws["route_expert"].cpu().numpy(), o["route_expert"])
+    assert np.array_equal(ws["route_rank"].cpu().numpy(), o["route_rank"])
+    assert np.array_equal(ws["route_hit"].cpu().numpy(), o["route_hit"])
+    served = ws["served_idx"].cpu().numpy()
+    assert np.array_equal(served, o["served_idx"])
+    np.testing.assert_allclose(ws["served_w"].cpu().numpy(), o["served_w"], rtol=2e-6, atol=1e-7)
+    # A3 permutation: bit-exact
+    counts, offsets, pos, src = port.permute(served, E, 128)
+    assert np.array_equal(ws["counts"].cpu().numpy(), counts)
+    assert np.array_equal(ws["seg_offsets"].cpu().numpy(), offsets)
+    assert np.array_equal(ws["pos"].cpu().numpy().astype(np.int64), pos)
+    R = int(offsets[-1])
+    assert np.array_equal(ws["row_token"][:R].cpu().numpy(), src)
+    valid = np.flatnonzero(src >= 0)
+    xp = ws["x_perm"][:R].cpu()
+    assert torch.equal(xp[valid], c["x"][src[valid]]), "permuted rows differ from their source rows"
+    # A4 expert FFN on sampled rows of every active expert (mirrored rounding)
+    rng = np.random.default_rng(0)
+    yp = to_f32(ws["y_perm"][:R])
+    bf = c["dtype"] == "bf16"
+    for e in range(E):
+        rows = np.arange(offsets[e], offsets[e] + counts[e])
+        if rows.size == 0:
+            continue
+        pick = rng.choice(rows, size=min(12, rows.size), replace=False)
+        w1, w3, w2 = (None if w is None else to_f32(w) for w in c["experts"][e])
+        ref = port.expert_ffn(x32[src[pick]], w1, w3, w2, 0 if c["act"] == "swiglu" else 1, bf)
+        (assert_bf16_close if bf else assert_f32_close)(yp[pick], ref, f"expert {e} FFN rows")
+    # A5 combine of the GPU expert outputs
+    yc = port.combine(yp, pos, ws["served_w"].cpu().numpy(), bf)
+    (assert_bf16_close if bf else assert_f32_close)(to_f32(c["y"]), yc, "combine")
+    # end to end on sampled tokens: oracle FFN for each served slot + oracle combine
+    toks = rng.choice(T, size=min(16, T), replace=False)
+    yref = np.zeros((toks.size, d), np.float32)
+    for i, t in enumerate(toks):
+        acc = np.zeros(d, np.float32)
+        for j in range(k):
+            e = served[t, j]
+            if e < 0:
+                continue
+            w1, w3, w2 = (None if w is None else to_f32(w) for w in c["experts"][e])
+            ye = port.expert_ffn(x32[t:t + 1], w1, w3, w2, 0 if c["act"] == "swiglu" else 1, bf)[0]
+            acc += np.float32(o["served_w"][t, j]) * ye
+        yref[i] = acc
+    if bf:
+        from oracle.oracle import bf16_round
+
+        yref = bf16_round(yref)
+        assert_bf16_close(to_f32(c["y"])[toks], yref, "end-to-end tokens")
+    else:
+        assert_f32_close(to_f32(c["y"])[toks], yref, "end-to-end tokens")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(CASES))
+def test_forward_parity(name, port):
+    c = run_case(name, port)
+    check_case(c, port)
+    c["layer"].close()
+
+
+@pytest.mark.gpu
+def test_forward_trace_logits_and_fallback_scores(port):
+    """Routing-driven mode (trace embedded as logits) with fallback scores set."""
+    scores = np.linspace(0.1, 0.8, 8)[::-1].copy()
+    c = run_case("mixtral_small", port, use_trace_logits=True, scores=scores)
+    check_case(c, port, scores=scores)
+    assert (c["ws"]["route_rank"].cpu().numpy() == -1).any(), "case should exercise the fallback path"
+    c["layer"].close()
+
+
+@pytest.mark.gpu
+def test_forward_deterministic(port):
+    c1 = run_case("mixtral_small", port)
+    y1 = c1["y"].clone()
+    c1["layer"].close()
+    c2 = run_case("mixtral_small", port)
+    assert torch.equal(y1, c2["y"]), "forward is not bit-reproducible"
+    c2["layer"].close()
