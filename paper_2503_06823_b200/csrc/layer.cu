@@ -228,6 +228,53 @@ struct emoe_layer {
     mark(5, s);
   }
 
+  // Host-buffer forward, pipelined in token chunks: the H2D copy of chunk i+1
+  // (in_stream) and the D2H copy of chunk i-1 (out_stream) overlap the forward
+  // of chunk i on the compute stream.  Per-token results do not depend on the
+  // chunking (every row's GEMM reduction order is fixed), so the output is
+  // bit-identical to a single forward over all T tokens.
+  cudaStream_t in_stream = nullptr, out_stream = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+
+  void forward_host(const void* x_host, void* y_host, int64_t T, cudaStream_t s) {
+    EMOE_REQUIRE(T >= 0 && T <= cfg.max_tokens, "moe_forward: T exceeds the layer's max_tokens");
+    const size_t row = (size_t)cfg.d_model * elem;
+    if (!x_in) {
+      x_in = dmalloc<uint8_t>((size_t)cfg.max_tokens * row);
+      y_out = dmalloc<uint8_t>((size_t)cfg.max_tokens * row);
+      EMOE_CUDA(cudaStreamCreateWithFlags(&in_stream, cudaStreamNonBlocking));
+      EMOE_CUDA(cudaStreamCreateWithFlags(&out_stream, cudaStreamNonBlocking));
+    }
+    int64_t chunk = std::max<int64_t>(8192, ceil_div(T, 8));
+    chunk = ceil_div(chunk, kRouteBlockTokens) * kRouteBlockTokens;
+    const int n = (int)std::max<int64_t>(1, ceil_div(T, chunk));
+    while ((int)chunk_ev.size() < 2 * n + 2) {
+      cudaEvent_t e;
+      EMOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      chunk_ev.push_back(e);
+    }
+    // earlier work on `s` may still read x_in / write y_out
+    EMOE_CUDA(cudaEventRecord(chunk_ev[2 * n], s));
+    EMOE_CUDA(cudaStreamWaitEvent(in_stream, chunk_ev[2 * n], 0));
+    for (int i = 0; i < n; ++i) {
+      const int64_t t0 = i * chunk, tn = std::min<int64_t>(chunk, T - t0);
+      uint8_t* xd = static_cast<uint8_t*>(x_in) + t0 * row;
+      uint8_t* yd = static_cast<uint8_t*>(y_out) + t0 * row;
+      EMOE_CUDA(cudaMemcpyAsync(xd, static_cast<const uint8_t*>(x_host) + t0 * row, tn * row,
+                                cudaMemcpyHostToDevice, in_stream));
+      EMOE_CUDA(cudaEventRecord(chunk_ev[2 * i], in_stream));
+      EMOE_CUDA(cudaStreamWaitEvent(s, chunk_ev[2 * i], 0));
+      forward(xd, nullptr, yd, tn, s);
+      EMOE_CUDA(cudaEventRecord(chunk_ev[2 * i + 1], s));
+      EMOE_CUDA(cudaStreamWaitEvent(out_stream, chunk_ev[2 * i + 1], 0));
+      EMOE_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(y_host) + t0 * row, yd, tn * row, cudaMemcpyDeviceToHost,
+                                out_stream));
+    }
+    EMOE_CUDA(cudaEventRecord(chunk_ev[2 * n + 1], out_stream));
+    EMOE_CUDA(cudaStreamWaitEvent(s, chunk_ev[2 * n + 1], 0));
+    EMOE_CUDA(cudaStreamSynchronize(s));
+  }
+
   void begin_load(const int32_t* ev, int nev, const int32_t* ld, int nld, cudaStream_t s) {
     const int E = cfg.num_experts;
     if (!pending_experts.empty()) poll(true, s, nullptr);  // plans apply in order
@@ -300,6 +347,9 @@ struct emoe_layer {
       for (void* p : *v)
         if (p) cudaFreeHost(p);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (in_stream) cudaStreamDestroy(in_stream);
+    if (out_stream) cudaStreamDestroy(out_stream);
+    for (cudaEvent_t e : chunk_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : {ev_evict, ev_load_start, ev_load_done})
       if (e) cudaEventDestroy(e);
     for (auto& set : ev_pool)
@@ -486,16 +536,7 @@ int emoe_moe_forward_host(emoe_layer* L, const void* x_host, void* y_host, int64
   return guard([&] {
     EMOE_REQUIRE(L && x_host && y_host, "moe_forward_host: null argument");
     EMOE_REQUIRE(T >= 0 && T <= L->cfg.max_tokens, "moe_forward: T exceeds the layer's max_tokens");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const size_t bytes = (size_t)T * L->cfg.d_model * L->elem;
-    if (!L->x_in) {
-      L->x_in = dmalloc<uint8_t>((size_t)L->cfg.max_tokens * L->cfg.d_model * L->elem);
-      L->y_out = dmalloc<uint8_t>((size_t)L->cfg.max_tokens * L->cfg.d_model * L->elem);
-    }
-    EMOE_CUDA(cudaMemcpyAsync(L->x_in, x_host, bytes, cudaMemcpyHostToDevice, s));
-    L->forward(L->x_in, nullptr, L->y_out, T, s);
-    EMOE_CUDA(cudaMemcpyAsync(y_host, L->y_out, bytes, cudaMemcpyDeviceToHost, s));
-    EMOE_CUDA(cudaStreamSynchronize(s));
+    L->forward_host(x_host, y_host, T, static_cast<cudaStream_t>(stream));
   });
 }
 

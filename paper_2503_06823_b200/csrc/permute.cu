@@ -18,94 +18,132 @@ namespace {
 
 constexpr int RT = kRouteBlockTokens;
 
-// One thread per expert walks the per-block counts in block order.
-__global__ void scan_kernel(const int32_t* __restrict__ block_counts, int nblocks, int E, int pad,
-                            int32_t* __restrict__ counts, int64_t* __restrict__ seg_offsets,
-                            int64_t* __restrict__ block_base) {
-  __shared__ int64_t totals[1024];
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int64_t run = 0;
-    for (int b = 0; b < nblocks; ++b) {
-      block_base[(int64_t)b * E + e] = run;
-      run += block_counts[(int64_t)b * E + e];
-    }
-    totals[e] = run;
-    counts[e] = (int32_t)run;
-  }
+// K3a, pass 1: one block per expert scans its per-block counts (block order)
+// into per-block bases and the expert total.
+__global__ void __launch_bounds__(256) scan_blocks_kernel(const int32_t* __restrict__ block_counts, int nblocks,
+                                                          int E, int64_t* __restrict__ block_base,
+                                                          int32_t* __restrict__ counts) {
+  __shared__ int64_t warp_tot[8];
+  __shared__ int64_t carry;
+  const int e = blockIdx.x, lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t off = 0;
-    for (int e = 0; e < E; ++e) {
-      seg_offsets[e] = off;
-      off += (totals[e] + pad - 1) / pad * pad;
+  for (int b0 = 0; b0 < nblocks; b0 += 256) {
+    const int b = b0 + threadIdx.x;
+    const int64_t v = b < nblocks ? block_counts[(int64_t)b * E + e] : 0;
+    int64_t incl = v;  // inclusive warp scan
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t n = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += n;
     }
-    seg_offsets[E] = off;
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    int64_t before = carry;
+    for (int w = 0; w < warp; ++w) before += warp_tot[w];
+    if (b < nblocks) block_base[(int64_t)b * E + e] = before + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 255) carry = before + incl;
+    __syncthreads();
   }
+  if (threadIdx.x == 0) counts[e] = (int32_t)carry;
 }
 
-// Block = 128 tokens (the route kernel's blocks), 4 warps x 32 tokens.
-__global__ void __launch_bounds__(128) permute_kernel(const uint8_t* __restrict__ x, int row_bytes, int64_t T, int E,
-                                                      int k, const int32_t* __restrict__ served_idx,
-                                                      const int64_t* __restrict__ seg_offsets,
-                                                      const int64_t* __restrict__ block_base,
-                                                      uint8_t* __restrict__ x_perm, int32_t* __restrict__ pos,
-                                                      int32_t* __restrict__ row_token) {
-  extern __shared__ int32_t warp_counts[];  // [4][E]
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t t = (int64_t)blockIdx.x * RT + threadIdx.x;
-  const bool valid = t < T;
-  int my[8];
-  for (int j = 0; j < k; ++j) my[j] = valid ? served_idx[t * k + j] : -1;
-  const uint32_t lt = (1u << lane) - 1u;
-  int rank[8];
-  for (int j = 0; j < k; ++j) rank[j] = 0;
-  // per expert: lanes (tokens) that serve it; a token serves an expert at most once
+// K3a, pass 2: padded segment offsets (a running sum over E experts)
+__global__ void seg_offsets_kernel(const int32_t* __restrict__ counts, int E, int pad,
+                                   int64_t* __restrict__ seg_offsets) {
+  if (threadIdx.x != 0) return;
+  int64_t off = 0;
   for (int e = 0; e < E; ++e) {
-    bool has = false;
-    for (int j = 0; j < k; ++j) has |= (my[j] == e);
-    const uint32_t m = __ballot_sync(0xffffffffu, has);
-    if (m == 0) {
-      if (lane == 0) warp_counts[warp * E + e] = 0;
-      continue;
+    seg_offsets[e] = off;
+    off += ((int64_t)counts[e] + pad - 1) / pad * pad;
+  }
+  seg_offsets[E] = off;
+}
+
+// K3b.  Block = 128 tokens (the route kernel's blocks).  Warps 0-3 rank their
+// 32 tokens per expert with ballots (stable token order, no atomics); then
+// all 8 warps gather rows, each lane keeping 8 16-byte loads in flight.
+constexpr int PERMUTE_THREADS = 256;
+constexpr int GATHER_UNROLL = 8;
+
+__global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
+    const uint8_t* __restrict__ x, int row_bytes, int64_t T, int E, int k, const int32_t* __restrict__ served_idx,
+    const int64_t* __restrict__ seg_offsets, const int64_t* __restrict__ block_base, uint8_t* __restrict__ x_perm,
+    int32_t* __restrict__ pos, int32_t* __restrict__ row_token) {
+  extern __shared__ int32_t sh[];
+  int32_t* warp_counts = sh;          // [4][E]
+  int32_t* dst_s = sh + 4 * E;        // [RT][k]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t t0 = (int64_t)blockIdx.x * RT;
+  int my[8];
+  int rank[8];
+  if (warp < 4) {
+    const int64_t t = t0 + threadIdx.x;
+    const bool valid = t < T;
+    for (int j = 0; j < k; ++j) {
+      my[j] = valid ? served_idx[t * k + j] : -1;
+      rank[j] = 0;
     }
-    if (lane == 0) warp_counts[warp * E + e] = __popc(m);
-    if (has)
-      for (int j = 0; j < k; ++j)
-        if (my[j] == e) rank[j] = __popc(m & lt);
+    const uint32_t lt = (1u << lane) - 1u;
+    // per expert: lanes (tokens) that serve it; a token serves an expert at most once
+    for (int e = 0; e < E; ++e) {
+      bool has = false;
+      for (int j = 0; j < k; ++j) has |= (my[j] == e);
+      const uint32_t m = __ballot_sync(0xffffffffu, has);
+      if (lane == 0) warp_counts[warp * E + e] = __popc(m);
+      if (has)
+        for (int j = 0; j < k; ++j)
+          if (my[j] == e) rank[j] = __popc(m & lt);
+    }
   }
   __syncthreads();
-  int32_t dst[8];
-  for (int j = 0; j < k; ++j) {
-    const int e = my[j];
-    if (e < 0) {
-      dst[j] = -1;
-      continue;
-    }
-    int64_t base = seg_offsets[e] + block_base[(int64_t)blockIdx.x * E + e];
-    for (int w = 0; w < warp; ++w) base += warp_counts[w * E + e];
-    dst[j] = (int32_t)(base + rank[j]);
-  }
-  if (valid)
+  if (warp < 4) {
+    const int64_t t = t0 + threadIdx.x;
     for (int j = 0; j < k; ++j) {
-      if (pos) pos[t * k + j] = dst[j];
-      if (row_token && dst[j] >= 0) row_token[dst[j]] = (int32_t)t;
+      const int e = my[j];
+      int32_t d = -1;
+      if (e >= 0) {
+        int64_t base = seg_offsets[e] + block_base[(int64_t)blockIdx.x * E + e];
+        for (int w = 0; w < warp; ++w) base += warp_counts[w * E + e];
+        d = (int32_t)(base + rank[j]);
+      }
+      dst_s[threadIdx.x * k + j] = d;
+      if (t < T) {
+        if (pos) pos[t * k + j] = d;
+        if (row_token && d >= 0) row_token[d] = (int32_t)t;
+      }
     }
-  // gather: the warp copies its 32 tokens' rows, 16 B per lane per step
+  }
+  __syncthreads();
+  // gather: warp w copies tokens w, w+8, ...; lanes own 16-byte column chunks
   const int nvec = row_bytes / 16;
-  for (int i = 0; i < 32; ++i) {
-    const int64_t tt = (int64_t)blockIdx.x * RT + warp * 32 + i;
+  for (int i = warp; i < RT; i += PERMUTE_THREADS / 32) {
+    const int64_t tt = t0 + i;
     if (tt >= T) break;
     int32_t d_i[8];
     int nd = 0;
     for (int j = 0; j < k; ++j) {
-      const int32_t v = __shfl_sync(0xffffffffu, dst[j], i);
+      const int32_t v = dst_s[i * k + j];
       if (v >= 0) d_i[nd++] = v;
     }
     if (nd == 0) continue;
     const uint4* src = reinterpret_cast<const uint4*>(x + tt * row_bytes);
-    for (int v = lane; v < nvec; v += 32) {
-      const uint4 val = __ldg(src + v);
-      for (int q = 0; q < nd; ++q) reinterpret_cast<uint4*>(x_perm + (int64_t)d_i[q] * row_bytes)[v] = val;
+    for (int v0 = 0; v0 < nvec; v0 += 32 * GATHER_UNROLL) {
+      uint4 val[GATHER_UNROLL];
+#pragma unroll
+      for (int u = 0; u < GATHER_UNROLL; ++u) {
+        const int v = v0 + u * 32 + lane;
+        if (v < nvec) val[u] = __ldg(src + v);
+      }
+      for (int q = 0; q < nd; ++q) {
+        uint4* out = reinterpret_cast<uint4*>(x_perm + (int64_t)d_i[q] * row_bytes);
+#pragma unroll
+        for (int u = 0; u < GATHER_UNROLL; ++u) {
+          const int v = v0 + u * 32 + lane;
+          if (v < nvec) out[v] = val[u];
+        }
+      }
     }
   }
 }
@@ -178,9 +216,11 @@ __global__ void __launch_bounds__(256) combine_f32_kernel(const float* __restric
 void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32_t* counts, int64_t* seg_offsets,
                  int64_t* block_base, cudaStream_t s) {
   EMOE_REQUIRE(E <= 1024, "scan: too many experts");
-  scan_kernel<<<1, 256, 0, s>>>(block_counts, nblocks, E, pad, counts, seg_offsets, block_base);
+  scan_blocks_kernel<<<E, 256, 0, s>>>(block_counts, nblocks, E, block_base, counts);
   EMOE_CUDA(cudaGetLastError());
-    count_launch();
+  seg_offsets_kernel<<<1, 32, 0, s>>>(counts, E, pad, seg_offsets);
+  EMOE_CUDA(cudaGetLastError());
+  count_launch(2);
 }
 
 void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
@@ -190,11 +230,12 @@ void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int 
   EMOE_REQUIRE(row_bytes % 16 == 0, "permute: row bytes must be a multiple of 16");
   const int nblocks = (int)ceil_div(T, RT);
   if (nblocks == 0) return;
-  permute_kernel<<<nblocks, RT, 4 * E * sizeof(int32_t), s>>>(
-      static_cast<const uint8_t*>(x), row_bytes, T, E, k, served_idx, seg_offsets, block_base,
-      static_cast<uint8_t*>(x_perm), pos, row_token);
+  const size_t smem = (4 * (size_t)E + (size_t)RT * k) * sizeof(int32_t);
+  permute_kernel<<<nblocks, PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
+                                                        served_idx, seg_offsets, block_base,
+                                                        static_cast<uint8_t*>(x_perm), pos, row_token);
   EMOE_CUDA(cudaGetLastError());
-    count_launch();
+  count_launch();
 }
 
 void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int32_t* pos, const float* served_w,

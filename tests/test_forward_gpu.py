@@ -36,7 +36,8 @@ def run_case(name, port, use_trace_logits=False, scores=None):
     xd = x.cuda()
     logits_in = None
     if use_trace_logits:
-        choices = np.stack([np.random.default_rng(3).permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+        crng = np.random.default_rng(3)
+        choices = np.stack([crng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
         logits_in = torch.from_numpy(trace_logits(choices, E)).cuda()
     y = layer.forward(xd, logits=logits_in)
     torch.cuda.synchronize()
@@ -140,3 +141,76 @@ def test_forward_deterministic(port):
     c2 = run_case("mixtral_small", port)
     assert torch.equal(y1, c2["y"]), "forward is not bit-reproducible"
     c2["layer"].close()
+
+
+@pytest.mark.gpu
+def test_forward_host_pipelined_equals_device_forward():
+    """The host-buffer API (chunked H2D / forward / D2H overlap) is bit-identical
+    to one device forward over all tokens, and chunk boundaries do not leak."""
+    from helpers import build_layer
+
+    T = 20000  # 3 chunks of 8192
+    layer, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", 4, [0, 3, 5, 6], max_tokens=T)
+    x = torch.randn(T, 256, generator=torch.Generator().manual_seed(21)).to(torch.bfloat16)
+    y_dev = layer.forward(x.cuda()).cpu()
+    y_host = torch.empty_like(x).pin_memory()
+    layer.forward_host(x.pin_memory(), y_host)
+    assert torch.equal(y_dev, y_host)
+    layer.close()
+
+
+@pytest.mark.gpu
+def test_forced_miss_and_no_resident_error():
+    """No resident expert: forced-miss layers serve nothing (y = 0, engine.cpp:533-537);
+    otherwise the forward raises the reference's logic_error."""
+    from paper_2503_06823_b200 import LogicError, MoELayer
+
+    from helpers import make_weights
+
+    wg, experts = make_weights(8, 256, 512, "bf16", "swiglu")
+    for forced in (True, False):
+        layer = MoELayer(256, 512, 8, 2, num_slots=4, max_tokens=256, forced_miss=forced)
+        layer.set_gate(wg)
+        x = torch.randn(256, 256).to(torch.bfloat16).cuda()
+        if forced:
+            y = layer.forward(x)
+            torch.cuda.synchronize()
+            assert torch.count_nonzero(y) == 0
+            ws = layer.workspace()
+            assert (ws["route_rank"] == -1).all() and (ws["served_idx"] == -1).all()
+            assert torch.equal(ws["route_expert"], ws["topk_idx"][:, 0])
+        else:
+            with pytest.raises(LogicError):
+                layer.forward(x)
+        layer.close()
+
+
+@pytest.mark.gpu
+def test_two_phase_residency_and_loads():
+    """Evictions apply at load start, loads at completion (engine.cpp:448-464);
+    double loads / evictions / budget overflow raise like Placement (expert_store.cpp:46-57)."""
+    from paper_2503_06823_b200 import LogicError
+
+    from helpers import build_layer
+
+    layer, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", 4, [0, 1, 2, 3], max_tokens=512)
+    assert layer.residency().tolist() == [1, 1, 1, 1, 0, 0, 0, 0]
+    with pytest.raises(LogicError):
+        layer.begin_load([], [0])          # already resident
+    with pytest.raises(LogicError):
+        layer.begin_load([5], [])          # not resident
+    with pytest.raises(LogicError):
+        layer.begin_load([], [4])          # budget 4 exceeded
+    layer.begin_load([1, 2], [6, 7])
+    res = layer.residency()
+    assert res[1] == 0 and res[2] == 0     # evictions visible immediately
+    layer.poll_loads(blocking=True)
+    assert layer.residency().tolist() == [1, 0, 0, 1, 0, 0, 1, 1]
+    b, ms = layer.last_load_stats()
+    assert b == 2 * 3 * 256 * 512 * 2 and ms > 0
+    x = torch.randn(300, 256).to(torch.bfloat16).cuda()
+    layer.forward(x)
+    torch.cuda.synchronize()
+    served = layer.workspace()["served_idx"].cpu().numpy()
+    assert set(np.unique(served[served >= 0]).tolist()) <= {0, 3, 6, 7}
+    layer.close()
