@@ -121,7 +121,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # synthetic workload
 # ---------------------------------------------------------------------------
-def build_workload(cfg, device):
+def build_workload(cfg, device, cta_group=0):
     import torch
 
     import paper_2503_06823_b200 as emoe
@@ -163,7 +163,7 @@ def build_workload(cfg, device):
 
     # ---- layer, weights (random-init, Mixtral/Switch shapes), planned loads
     layer = MoELayer(d, f, E, k, activation=cfg["act"], dtype="bf16", weight_mode=cfg["wm"], num_slots=L,
-                     max_tokens=T)
+                     max_tokens=T, gemm_cta_group=cta_group)
     g = torch.Generator(device=device).manual_seed(1234)
     q, _ = torch.linalg.qr(torch.randn(d, E, generator=g, device=device))  # orthonormal gate rows
     wg = q.T.contiguous()
@@ -281,6 +281,8 @@ def main():
     ap.add_argument("--config", default="mixtral", choices=list(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--gemm-cta-group", type=int, default=0, choices=[0, 1, 2],
+                    help="FFN GEMM CTA group (0 = the layer's auto choice)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -301,7 +303,7 @@ def main():
     import paper_2503_06823_b200 as emoe
     from paper_2503_06823_b200 import _lib
 
-    layer, pred, x, info = build_workload(cfg, device)
+    layer, pred, x, info = build_workload(cfg, device, args.gemm_cta_group)
     T = x.shape[0]
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream()
@@ -396,7 +398,8 @@ def main():
                            d_model=d, d_ff=f, activation=cfg["act"], served_rows=S, hit_rate=round(hit_rate, 4),
                            fallback_rate=round(fallback, 4),
                            l2="inputs larger than L2: x is %.0f MB per step" % (xb / 1e6),
-                           parallelism=f"replicas{world}" if world > 1 else "single"),
+                           parallelism=f"replicas{world}" if world > 1 else "single",
+                           gemm_cta_group=layer.gemm_cta_group, seg_pad=layer.seg_pad),
                roofline=roofline, e2e=e2e, gpu_launches=launches, clocks=clk.summary(),
                stages_ms={kk: round(v, 4) for kk, v in stages.items()},
                stage_hbm_gbs={kk: round(v, 1) for kk, v in hbm_stages.items()},

@@ -76,6 +76,8 @@ typedef struct {
   int num_slots;   /* HBM expert slots = resident budget L (Placement::budget) */
   int64_t max_tokens;
   int forced_miss; /* 1: a layer with no resident expert serves nothing (engine.cpp:533-537) */
+  int gemm_cta_group; /* bf16 FFN GEMM: 1 = one CTA per 128x256 tile, 2 = CTA pair per 256x256
+                         tile (segments padded to 256 rows), 0 = auto (2 when E <= 16) */
 } emoe_layer_config;
 
 int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out);
@@ -129,6 +131,8 @@ int emoe_route(emoe_layer* layer, const void* x_dev, const float* logits_in_dev,
 typedef struct {
   int64_t T;
   int64_t rows_cap;
+  int64_t seg_pad;        /* per-expert segment padding (rows) */
+  int64_t gemm_cta_group; /* CTA group the FFN GEMMs run with */
   float* logits;          /* [T][E] */
   int32_t* topk_idx;      /* [T][k] gate choices, rank order */
   int32_t* route_expert;  /* [T] RouteResult.expert */

@@ -27,11 +27,11 @@ dbl = C.c_double
 class LayerConfig(C.Structure):
     _fields_ = [("d_model", C.c_int), ("d_ff", C.c_int), ("num_experts", C.c_int), ("top_k", C.c_int),
                 ("activation", C.c_int), ("dtype", C.c_int), ("weight_mode", C.c_int), ("num_slots", C.c_int),
-                ("max_tokens", i64), ("forced_miss", C.c_int)]
+                ("max_tokens", i64), ("forced_miss", C.c_int), ("gemm_cta_group", C.c_int)]
 
 
 class Workspace(C.Structure):
-    _fields_ = [("T", i64), ("rows_cap", i64), ("logits", vp), ("topk_idx", vp), ("route_expert", vp),
+    _fields_ = [("T", i64), ("rows_cap", i64), ("seg_pad", i64), ("gemm_cta_group", i64), ("logits", vp), ("topk_idx", vp), ("route_expert", vp),
                 ("route_rank", vp), ("route_hit", vp), ("served_idx", vp), ("served_w", vp), ("counts", vp),
                 ("seg_offsets", vp), ("pos", vp), ("row_token", vp), ("x_perm", vp), ("h", vp), ("y_perm", vp),
                 ("slot_of_expert", vp), ("resident", vp)]

@@ -9,140 +9,232 @@
 //   EPI_RELU    B tile = 256 rows of W1, H = relu(X W1^T) -> bf16  (GEMM1, Switch)
 //   EPI_STORE   B tile = 256 rows of W2, Y = H W2^T -> bf16          (GEMM2)
 //
-// Hardware mapping (B200, one CTA per SM, 6 warps):
-//   warp 0      TMA producer: A (128 x 64) and B (256 x 64) bf16 tiles, 128-B
-//               swizzle, into a 4-stage shared-memory ring (48 KB / stage)
-//   warp 1      MMA issuer: one elected lane issues tcgen05.mma.cta_group::1
-//               kind::f16 M=128 N=256 K=16 (4 per 64-wide k-block); accumulators
-//               live in TMEM, double-buffered (2 x 256 of 512 columns) so the
-//               epilogue of tile i overlaps the mainloop of tile i+1
+// Hardware mapping (B200, one CTA per SM, 6 warps), CG = CTAs per MMA:
+//   CG = 1  tile 128 x 256: each CTA loads A 128x64 + B 256x64 per k-block
+//           (48 KB, 4-stage ring) and issues tcgen05.mma.cta_group::1 M=128.
+//   CG = 2  tile 256 x 256 on a CTA pair (cluster of 2 on one TPC): each CTA
+//           loads its own 128 rows of A and half of B (128x64 + 128x64 = 32 KB,
+//           6-stage ring); the leader issues tcgen05.mma.cta_group::2 M=256 that
+//           reads both CTAs' shared memory and writes each CTA's 128 accumulator
+//           rows to its own TMEM.  Per-SM shared-memory fill per MMA k-block drops
+//           from 48 KB to 32 KB (B is split across the pair).
+//   warp 0      TMA producer (128-B swizzle, L2 256-B promotion)
+//   warp 1      MMA issuer (one elected lane; tcgen05.commit -> mbarriers)
 //   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> activation -> bf16
-//               -> global (each warp owns its 32-lane TMEM quarter)
-// Segments are padded to 128 rows by the permute kernel, so every 128-row
-// block belongs to exactly one expert and all loads/stores stay in bounds.
-// Tiles are walked in a grouped raster (8 row blocks x all n blocks) so the
-// 148 concurrently running tiles share A and B tiles through L2.
+//               -> global; TMEM accumulators double-buffered (2 x 256 of 512
+//               columns) so the epilogue of tile i overlaps the MMAs of tile i+1.
+// Segments are padded to the tile M (128 / 256 rows) by the permute kernel, so
+// every tile row block belongs to exactly one expert and no load or store
+// crosses a segment.  Tiles are walked in a grouped raster: `group_m` row
+// blocks x all n blocks, sized on the host so the A panel (group_m x M x K x 2
+// bytes) stays L2-resident while the weight tiles stream past it.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace emoe {
 namespace gemm {
 
-constexpr int BM = 128;
 constexpr int BN = 256;  // UMMA N / accumulator columns per tile
 constexpr int BK = 64;   // one 128-byte swizzle row of bf16
-constexpr int STAGES = 4;
-constexpr int GROUP_M = 8;
-constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
-constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int MAX_EXPERTS = 256;
 constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 4096 /*barriers + offsets*/;
+
+template <int CG>
+struct Cfg {
+  static constexpr int TILE_M = 128 * CG;
+  static constexpr int B_ROWS = BN / CG;  // B rows held by one CTA
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 4096 /*barriers + offsets*/;
+};
 
 struct Params {
-  const int64_t* seg_offsets;   // [E+1], multiples of BM
+  const int64_t* seg_offsets;     // [E+1], multiples of TILE_M
   const int32_t* slot_of_expert;  // [E]
   int num_experts;
   int K;                // reduction length (multiple of BK)
   int n_blocks;         // output column blocks
   int out_block_cols;   // 128 (SwiGLU) or 256
   int b_rows_per_slot;  // rows of one expert in the B pool
+  int group_m;          // raster group (row blocks)
   __nv_bfloat16* out;
   int64_t ldo;
 };
 
 struct TileCoord {
-  int rb, nb, expert;
+  int mb, nb, expert;
 };
 
-__device__ __forceinline__ TileCoord decode_tile(int t, int total_rb, int n_blocks, const int64_t* offs,
-                                                 int num_experts) {
-  const int per_group = GROUP_M * n_blocks;
+__device__ __forceinline__ TileCoord decode_tile(int t, int total_mb, int n_blocks, int group_m, int tile_m,
+                                                 const int64_t* offs, int num_experts) {
+  const int per_group = group_m * n_blocks;
   const int g = t / per_group;
   const int local = t - g * per_group;
-  const int rows_in_group = min(GROUP_M, total_rb - g * GROUP_M);
+  const int rows_in_group = min(group_m, total_mb - g * group_m);
   TileCoord c;
   c.nb = local / rows_in_group;
-  c.rb = g * GROUP_M + (local - c.nb * rows_in_group);
-  const int64_t row = (int64_t)c.rb * BM;
+  c.mb = g * group_m + (local - c.nb * rows_in_group);
+  const int64_t row = (int64_t)c.mb * tile_m;
   int e = 0;
   while (e + 1 < num_experts && offs[e + 1] <= row) ++e;
   c.expert = e;
   return c;
 }
 
-template <int EPI>
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// ---- cta_group::2 flavours of the PTX wrappers ----
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* desc, uint64_t* leader_bar, void* smem_dst,
+                                                 int32_t c0, int32_t c1, uint64_t hint) {
+  // completion bytes go to the leader CTA's barrier (peer bit cleared)
+  const uint32_t bar = smem_u32(leader_bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar), "r"(c0), "r"(c1), "l"(hint)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {  // arrive on this offset in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {  // arrive on CTA 0's copy of `bar`
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+template <int EPI, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                         const __grid_constant__ CUtensorMap tmap_b2, Params p) {
+  using C = Cfg<CG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + STAGES * A_STAGE_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* tfull_bar = empty_bar + STAGES;  // [2]
-  uint64_t* tempty_bar = tfull_bar + 2;      // [2]
+  uint8_t* smem_b = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;  // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int64_t* s_offs = reinterpret_cast<int64_t*>(tmem_slot + 4);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int E = p.num_experts;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / CG;
+  const int num_clusters = gridDim.x / CG;
 
   for (int i = threadIdx.x; i <= E; i += NUM_THREADS) s_offs[i] = p.seg_offsets[i];
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
     if (EPI == EPI_SWIGLU) tma_prefetch_desc(&tmap_b2);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 128);
+      mbar_init(&tempty_bar[b], 4 * CG);  // one arrival per epilogue warp of every CTA
     }
     fence_barrier_init();
   }
   if (warp == 1) {
-    tmem_alloc(tmem_slot, TMEM_COLS);
-    tmem_relinquish();
+    if (CG == 1) {
+      tmem_alloc(tmem_slot, TMEM_COLS);
+      tmem_relinquish();
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync_all();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int total_rb = (int)(s_offs[E] / BM);
-  const int total_tiles = total_rb * p.n_blocks;
+  const int total_mb = (int)(s_offs[E] / C::TILE_M);
+  const int total_tiles = total_mb * p.n_blocks;
   const int k_blocks = p.K / BK;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (every CTA) =====================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const TileCoord c = decode_tile(t, total_rb, p.n_blocks, s_offs, E);
+      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+        const TileCoord c = decode_tile(t, total_mb, p.n_blocks, p.group_m, C::TILE_M, s_offs, E);
         const int slot = p.slot_of_expert[c.expert];
-        const int a_row = c.rb * BM;
-        const int b_row = slot * p.b_rows_per_slot + c.nb * (EPI == EPI_SWIGLU ? BN / 2 : BN);
+        const int a_row = c.mb * C::TILE_M + (int)rank * 128;
+        int b_row;
+        const CUtensorMap* tb = &tmap_b;
+        if (EPI == EPI_SWIGLU) {
+          b_row = slot * p.b_rows_per_slot + c.nb * (BN / 2);
+          if (CG == 2 && rank == 1) tb = &tmap_b2;  // pair: CTA0 holds the W1 half, CTA1 the W3 half
+        } else {
+          b_row = slot * p.b_rows_per_slot + c.nb * BN + (int)rank * C::B_ROWS;
+        }
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * C::STAGE_BYTES);
           const int kc = kb * BK;
-          tma_load_2d(&tmap_a, &full_bar[stage], smem_a + stage * A_STAGE_BYTES, kc, a_row, kCacheEvictNormal);
-          uint8_t* bdst = smem_b + stage * B_STAGE_BYTES;
-          if (EPI == EPI_SWIGLU) {
-            tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, kCacheEvictNormal);
-            tma_load_2d(&tmap_b2, &full_bar[stage], bdst + B_STAGE_BYTES / 2, kc, b_row, kCacheEvictNormal);
+          uint8_t* adst = smem_a + stage * C::A_BYTES;
+          uint8_t* bdst = smem_b + stage * C::B_BYTES;
+          if (CG == 1) {
+            tma_load_2d(&tmap_a, &full_bar[stage], adst, kc, a_row, kCacheEvictNormal);
+            if (EPI == EPI_SWIGLU) {
+              tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, kCacheEvictNormal);
+              tma_load_2d(&tmap_b2, &full_bar[stage], bdst + C::B_BYTES / 2, kc, b_row, kCacheEvictNormal);
+            } else {
+              tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, kCacheEvictNormal);
+            }
           } else {
-            tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, kCacheEvictNormal);
+            tma_load_2d_pair(&tmap_a, &full_bar[stage], adst, kc, a_row, kCacheEvictNormal);
+            tma_load_2d_pair(tb, &full_bar[stage], bdst, kc, b_row, kCacheEvictNormal);
           }
-          if (++stage == STAGES) {
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (CG == 2) {
+        // producer tail: every stage released, i.e. the leader's last
+        // multicast commits to this CTA's barriers have landed before exit
+        for (int i = 0; i < C::STAGES; ++i) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -150,13 +242,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+    // ===================== MMA issuer (leader CTA) =====================
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = umma_idesc_bf16(C::TILE_M, BN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+      for (int t = cluster_id; t < total_tiles; t += num_clusters, ++local) {
         const int buf = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tempty_bar[buf], acc_phase ^ 1);
@@ -165,34 +257,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          const uint64_t a_desc = umma_desc_sw128(smem_a + stage * A_STAGE_BYTES);
-          const uint64_t b_desc = umma_desc_sw128(smem_b + stage * B_STAGE_BYTES);
+          const uint64_t a_desc = umma_desc_sw128(smem_a + stage * C::A_BYTES);
+          const uint64_t b_desc = umma_desc_sw128(smem_b + stage * C::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             // advance 16 bf16 = 32 B inside the 128-B swizzle row
-            umma_bf16(tmem_d, a_desc + (uint64_t)(kk * 2), b_desc + (uint64_t)(kk * 2), idesc,
-                      (kb | kk) != 0 ? 1u : 0u);
+            const uint32_t acc = (kb | kk) != 0 ? 1u : 0u;
+            if (CG == 1)
+              umma_bf16(tmem_d, a_desc + (uint64_t)(kk * 2), b_desc + (uint64_t)(kk * 2), idesc, acc);
+            else
+              umma_bf16_pair(tmem_d, a_desc + (uint64_t)(kk * 2), b_desc + (uint64_t)(kk * 2), idesc, acc);
           }
-          umma_commit(&empty_bar[stage]);
-          if (++stage == STAGES) {
+          if (CG == 1)
+            umma_commit(&empty_bar[stage]);
+          else
+            umma_commit_pair(&empty_bar[stage]);
+          if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull_bar[buf]);
+        if (CG == 1)
+          umma_commit(&tfull_bar[buf]);
+        else
+          umma_commit_pair(&tfull_bar[buf]);
       }
     }
   } else {
-    // ===================== epilogue (warps 2..5) =====================
+    // ===================== epilogue (warps 2..5, every CTA) =====================
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     int local = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
-      const TileCoord c = decode_tile(t, total_rb, p.n_blocks, s_offs, E);
+    for (int t = cluster_id; t < total_tiles; t += num_clusters, ++local) {
+      const TileCoord c = decode_tile(t, total_mb, p.n_blocks, p.group_m, C::TILE_M, s_offs, E);
       const int buf = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
-      const int64_t row = (int64_t)c.rb * BM + quarter * 32 + lane;
+      const int64_t row = (int64_t)c.mb * C::TILE_M + rank * 128 + quarter * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + buf * BN;
       __nv_bfloat16* orow = p.out + row * p.ldo + (int64_t)c.nb * p.out_block_cols;
       if (EPI == EPI_SWIGLU) {
@@ -239,14 +340,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar[buf]);
+      if (lane == 0) {
+        if (CG == 1)
+          mbar_arrive(&tempty_bar[buf]);
+        else
+          mbar_arrive_leader(&tempty_bar[buf]);
+      }
     }
   }
 
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync_all();  // the leader's commits to our barriers and TMEM are done
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    if (CG == 1)
+      tmem_dealloc(tmem_base, TMEM_COLS);
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -285,14 +398,23 @@ CUtensorMap make_tmap_bf16_2d(const void* base, uint64_t rows, uint64_t cols, ui
   return m;
 }
 
-int gemm_smem_bytes() { return gemm::SMEM_BYTES; }
+int gemm_tile_m(int cta_group) { return 128 * cta_group; }
+int gemm_b_box_rows(int epi, int cta_group) { return epi == EPI_SWIGLU ? 128 : 256 / cta_group; }
 
-void launch_grouped_gemm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
-                         const int64_t* seg_offsets, const int32_t* slot_of_expert, int num_experts, int K,
-                         int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo, int num_sms,
-                         cudaStream_t stream) {
+// raster group: keep the A panel (group x tile_m rows x K) near 32 MB of L2
+static int group_rows(int K, int tile_m) {
+  const int64_t panel_row_bytes = (int64_t)tile_m * K * 2;
+  int g = (int)((32ll << 20) / panel_row_bytes);
+  return g < 2 ? 2 : (g > 64 ? 64 : g);
+}
+
+void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
+                         const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
+                         int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
+                         int num_sms, cudaStream_t stream) {
   EMOE_REQUIRE(num_experts <= gemm::MAX_EXPERTS, "grouped_gemm: too many experts");
   EMOE_REQUIRE(K % gemm::BK == 0, "grouped_gemm: K must be a multiple of 64");
+  EMOE_REQUIRE(cta_group == 1 || cta_group == 2, "grouped_gemm: cta_group must be 1 or 2");
   gemm::Params p;
   p.seg_offsets = seg_offsets;
   p.slot_of_expert = slot_of_expert;
@@ -302,24 +424,53 @@ void launch_grouped_gemm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, 
   EMOE_REQUIRE(N_out % p.out_block_cols == 0, "grouped_gemm: N must be a multiple of the column block");
   p.n_blocks = N_out / p.out_block_cols;
   p.b_rows_per_slot = b_rows_per_slot;
+  p.group_m = group_rows(K, 128 * cta_group);
   p.out = out;
   p.ldo = ldo;
-  auto run = [&](auto kernel) {
-    static bool attr_set[3] = {false, false, false};
-    if (!attr_set[epi]) {
-      EMOE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::SMEM_BYTES));
-      attr_set[epi] = true;
+  const int grid = cta_group == 2 ? (num_sms / 2) * 2 : num_sms;
+  auto run = [&](auto kernel, int smem, int idx) {
+    static bool attr_set[6] = {false, false, false, false, false, false};
+    if (!attr_set[idx]) {
+      EMOE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr_set[idx] = true;
     }
-    kernel<<<num_sms, gemm::NUM_THREADS, gemm::SMEM_BYTES, stream>>>(ta, tb, tb2, p);
+    if (cta_group == 1) {
+      kernel<<<grid, gemm::NUM_THREADS, smem, stream>>>(ta, tb, tb2, p);
+    } else {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(gemm::NUM_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      EMOE_CUDA(cudaLaunchKernelEx(&cfg, kernel, ta, tb, tb2, p));
+    }
     EMOE_CUDA(cudaGetLastError());
     count_launch();
   };
-  if (epi == EPI_SWIGLU)
-    run(gemm::grouped_gemm_kernel<EPI_SWIGLU>);
-  else if (epi == EPI_RELU)
-    run(gemm::grouped_gemm_kernel<EPI_RELU>);
-  else
-    run(gemm::grouped_gemm_kernel<EPI_STORE>);
+  using C1 = gemm::Cfg<1>;
+  using C2 = gemm::Cfg<2>;
+  if (cta_group == 1) {
+    if (epi == EPI_SWIGLU)
+      run(gemm::grouped_gemm_kernel<EPI_SWIGLU, 1>, C1::SMEM_BYTES, 0);
+    else if (epi == EPI_RELU)
+      run(gemm::grouped_gemm_kernel<EPI_RELU, 1>, C1::SMEM_BYTES, 1);
+    else
+      run(gemm::grouped_gemm_kernel<EPI_STORE, 1>, C1::SMEM_BYTES, 2);
+  } else {
+    if (epi == EPI_SWIGLU)
+      run(gemm::grouped_gemm_kernel<EPI_SWIGLU, 2>, C2::SMEM_BYTES, 3);
+    else if (epi == EPI_RELU)
+      run(gemm::grouped_gemm_kernel<EPI_RELU, 2>, C2::SMEM_BYTES, 4);
+    else
+      run(gemm::grouped_gemm_kernel<EPI_STORE, 2>, C2::SMEM_BYTES, 5);
+  }
 }
 
 }  // namespace emoe

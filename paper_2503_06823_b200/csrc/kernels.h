@@ -61,13 +61,14 @@ void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int 
 void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int32_t* pos, const float* served_w,
                     void* y, cudaStream_t s);
 
-// K4: tcgen05 grouped GEMM (bf16)
+// K4: tcgen05 grouped GEMM (bf16); cta_group 1 (tile 128x256) or 2 (CTA pair, tile 256x256)
 CUtensorMap make_tmap_bf16_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
-int gemm_smem_bytes();
-void launch_grouped_gemm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
-                         const int64_t* seg_offsets, const int32_t* slot_of_expert, int num_experts, int K,
-                         int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo, int num_sms,
-                         cudaStream_t stream);
+int gemm_tile_m(int cta_group);                 // segment padding the kernel needs
+int gemm_b_box_rows(int epi, int cta_group);    // TMA box rows of the weight operand
+void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
+                         const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
+                         int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
+                         int num_sms, cudaStream_t stream);
 
 // K4 fp32 path (SIMT FFMA): same grouping/epilogues, fp32 in/out
 void launch_grouped_gemm_f32(int epi, const float* A, int64_t lda, const float* B, const float* B2,

@@ -57,6 +57,8 @@ struct emoe_layer {
   int elem = 2;
   int num_sms = 148;
   int64_t rows_cap = 0;
+  int cta_group = 1;  // FFN GEMM CTA group
+  int seg_pad = kSegPad;
   int route_blocks = 0;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_evict = nullptr, ev_load_start = nullptr, ev_load_done = nullptr;
@@ -203,15 +205,15 @@ struct emoe_layer {
     mark(1, s);
     const int nb = (int)ceil_div(T, kRouteBlockTokens);
     const int E = cfg.num_experts, d = cfg.d_model, f = cfg.d_ff;
-    launch_scan(block_counts, nb, E, kSegPad, counts, seg_offsets, block_base, s);
+    launch_scan(block_counts, nb, E, seg_pad, counts, seg_offsets, block_base, s);
     EMOE_CUDA(cudaMemsetAsync(row_token, 0xff, sizeof(int32_t) * rows_cap, s));
     launch_permute(x, elem, T, d, E, cfg.top_k, served_idx, seg_offsets, block_base, x_perm, pos, row_token, s);
     mark(2, s);
     if (cfg.dtype == EMOE_DTYPE_BF16) {
-      launch_grouped_gemm(swiglu() ? EPI_SWIGLU : EPI_RELU, ta1, tb1, tb3, seg_offsets, slot_dev, E, d, f, f,
-                          static_cast<__nv_bfloat16*>(h), f, num_sms, s);
+      launch_grouped_gemm(swiglu() ? EPI_SWIGLU : EPI_RELU, cta_group, ta1, tb1, tb3, seg_offsets, slot_dev, E, d,
+                          f, f, static_cast<__nv_bfloat16*>(h), f, num_sms, s);
       mark(3, s);
-      launch_grouped_gemm(EPI_STORE, ta2, tb2, tb2, seg_offsets, slot_dev, E, f, d, d,
+      launch_grouped_gemm(EPI_STORE, cta_group, ta2, tb2, tb2, seg_offsets, slot_dev, E, f, d, d,
                           static_cast<__nv_bfloat16*>(y_perm), d, num_sms, s);
       mark(4, s);
     } else {
@@ -387,7 +389,10 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
       EMOE_CUDA(cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, dev));
       const int E = c.num_experts, k = c.top_k;
       const int64_t T = c.max_tokens;
-      L->rows_cap = T * k + (int64_t)E * kSegPad;
+      EMOE_REQUIRE(c.gemm_cta_group >= 0 && c.gemm_cta_group <= 2, "layer.gemm_cta_group: must be 0, 1 or 2");
+      L->cta_group = c.dtype == EMOE_DTYPE_BF16 ? (c.gemm_cta_group ? c.gemm_cta_group : (E <= 16 ? 2 : 1)) : 1;
+      L->seg_pad = c.dtype == EMOE_DTYPE_BF16 ? gemm_tile_m(L->cta_group) : kSegPad;
+      L->rows_cap = T * k + (int64_t)E * L->seg_pad;
       L->route_blocks = (int)ceil_div(T, kRouteBlockTokens);
       EMOE_CUDA(cudaStreamCreateWithFlags(&L->copy_stream, cudaStreamNonBlocking));
       EMOE_CUDA(cudaEventCreateWithFlags(&L->ev_evict, cudaEventDisableTiming));
@@ -434,11 +439,13 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
       L->push_tables(0);
       if (c.dtype == EMOE_DTYPE_BF16) {
         const uint64_t d = c.d_model, f = c.d_ff;
+        const int epi1 = L->swiglu() ? EPI_SWIGLU : EPI_RELU;
+        const uint32_t b1_box = gemm_b_box_rows(epi1, L->cta_group);
         L->ta1 = make_tmap_bf16_2d(L->x_perm, L->rows_cap, d, 128);
-        L->tb1 = make_tmap_bf16_2d(L->w1_pool, (uint64_t)c.num_slots * f, d, L->swiglu() ? 128 : 256);
-        L->tb3 = L->swiglu() ? make_tmap_bf16_2d(L->w3_pool, (uint64_t)c.num_slots * f, d, 128) : L->tb1;
+        L->tb1 = make_tmap_bf16_2d(L->w1_pool, (uint64_t)c.num_slots * f, d, b1_box);
+        L->tb3 = L->swiglu() ? make_tmap_bf16_2d(L->w3_pool, (uint64_t)c.num_slots * f, d, b1_box) : L->tb1;
         L->ta2 = make_tmap_bf16_2d(L->h, L->rows_cap, f, 128);
-        L->tb2 = make_tmap_bf16_2d(L->w2_pool, (uint64_t)c.num_slots * d, f, 256);
+        L->tb2 = make_tmap_bf16_2d(L->w2_pool, (uint64_t)c.num_slots * d, f, gemm_b_box_rows(EPI_STORE, L->cta_group));
       }
       EMOE_CUDA(cudaDeviceSynchronize());
     } catch (...) {
@@ -553,6 +560,8 @@ int emoe_layer_workspace(emoe_layer* L, emoe_workspace* w) {
     EMOE_REQUIRE(L && w, "workspace: null argument");
     w->T = L->last_T;
     w->rows_cap = L->rows_cap;
+    w->seg_pad = L->seg_pad;
+    w->gemm_cta_group = L->cta_group;
     w->logits = L->logits;
     w->topk_idx = L->topk;
     w->route_expert = L->r_expert;

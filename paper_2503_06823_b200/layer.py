@@ -42,7 +42,7 @@ def _view(ptr, shape, torch_dtype):
 class MoELayer:
     def __init__(self, d_model: int, d_ff: int, num_experts: int, top_k: int, *, activation: str = "swiglu",
                  dtype: str = "bf16", weight_mode: str = "topk_softmax", num_slots: Optional[int] = None,
-                 max_tokens: int = 65536, forced_miss: bool = False):
+                 max_tokens: int = 65536, forced_miss: bool = False, gemm_cta_group: int = 0):
         self.d, self.f, self.E, self.k = d_model, d_ff, num_experts, top_k
         self.dtype_name = dtype
         self.code, self.torch_dtype, self.elem = _DT[dtype]
@@ -50,7 +50,7 @@ class MoELayer:
         self.num_slots = num_slots or num_experts
         self.max_tokens = max_tokens
         cfg = LayerConfig(d_model, d_ff, num_experts, top_k, _ACT[activation], self.code, _WM[weight_mode],
-                          self.num_slots, max_tokens, int(forced_miss))
+                          self.num_slots, max_tokens, int(forced_miss), int(gemm_cta_group))
         h = C.c_void_p()
         check(lib.emoe_layer_create(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -163,6 +163,8 @@ class MoELayer:
         w = Workspace()
         check(lib.emoe_layer_workspace(self.h, C.byref(w)))
         T, R, E, k = w.T, w.rows_cap, self.E, self.k
+        self.seg_pad = int(w.seg_pad)
+        self.gemm_cta_group = int(w.gemm_cta_group)
         return {
             "logits": _view(w.logits, (T, E), torch.float32),
             "topk_idx": _view(w.topk_idx, (T, k), torch.int32),

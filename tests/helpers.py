@@ -36,12 +36,12 @@ def make_weights(E, d, f, dtype, act, seed=1234):
 
 
 def build_layer(E, d, f, k, dtype="bf16", act="swiglu", weight_mode="topk_softmax", slots=None, resident=None,
-                max_tokens=4096, seed=1234, forced_miss=False):
+                max_tokens=4096, seed=1234, forced_miss=False, gemm_cta_group=0):
     from paper_2503_06823_b200 import MoELayer
 
     wg, experts = make_weights(E, d, f, dtype, act, seed)
     layer = MoELayer(d, f, E, k, activation=act, dtype=dtype, weight_mode=weight_mode, num_slots=slots or E,
-                     max_tokens=max_tokens, forced_miss=forced_miss)
+                     max_tokens=max_tokens, forced_miss=forced_miss, gemm_cta_group=gemm_cta_group)
     layer.set_gate(wg)
     for e, (w1, w3, w2) in enumerate(experts):
         layer.register_expert(e, w1, w3, w2)

@@ -16,18 +16,22 @@ import torch
 from helpers import (assert_bf16_close, assert_f32_close, build_layer, to_f32, trace_logits)
 
 CASES = {
-    # name: E, d, f, k, dtype, act, weight_mode, slots, resident, T
-    "mixtral_small": (8, 512, 1024, 2, "bf16", "swiglu", "topk_softmax", 4, [1, 3, 4, 6], 1000),
-    "mixtral_full_resident": (8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", 8, None, 640),
-    "switch_small": (32, 256, 512, 1, "bf16", "relu", "full_softmax", 8, [0, 2, 5, 7, 11, 19, 23, 31], 777),
-    "config1_fp32_phi05": (8, 1024, 3584, 2, "fp32", "swiglu", "topk_softmax", 4, [0, 2, 5, 7], 512),
-    "config1_fp32_phi1": (8, 1024, 3584, 2, "fp32", "swiglu", "topk_softmax", 8, None, 512),
+    # name: E, d, f, k, dtype, act, weight_mode, slots, resident, T, gemm_cta_group (0 = auto)
+    "mixtral_small": (8, 512, 1024, 2, "bf16", "swiglu", "topk_softmax", 4, [1, 3, 4, 6], 1000, 0),
+    "mixtral_small_cta1": (8, 512, 1024, 2, "bf16", "swiglu", "topk_softmax", 4, [1, 3, 4, 6], 1000, 1),
+    "mixtral_full_resident": (8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", 8, None, 640, 0),
+    "switch_small": (32, 256, 512, 1, "bf16", "relu", "full_softmax", 8, [0, 2, 5, 7, 11, 19, 23, 31], 777, 0),
+    "switch_small_cta2": (32, 256, 512, 1, "bf16", "relu", "full_softmax", 8, [0, 2, 5, 7, 11, 19, 23, 31], 777,
+                          2),
+    "config1_fp32_phi05": (8, 1024, 3584, 2, "fp32", "swiglu", "topk_softmax", 4, [0, 2, 5, 7], 512, 0),
+    "config1_fp32_phi1": (8, 1024, 3584, 2, "fp32", "swiglu", "topk_softmax", 8, None, 512, 0),
 }
 
 
 def run_case(name, port, use_trace_logits=False, scores=None):
-    E, d, f, k, dtype, act, wm, slots, resident, T = CASES[name]
-    layer, wg, experts = build_layer(E, d, f, k, dtype, act, wm, slots, resident, max_tokens=max(T, 128))
+    E, d, f, k, dtype, act, wm, slots, resident, T, cg = CASES[name]
+    layer, wg, experts = build_layer(E, d, f, k, dtype, act, wm, slots, resident, max_tokens=max(T, 128),
+                                     gemm_cta_group=cg)
     if scores is not None:
         layer.set_scores(scores)
     g = torch.Generator().manual_seed(7)
@@ -69,7 +73,7 @@ def check_case(c, port, scores=None):
     assert np.array_equal(served, o["served_idx"])
     np.testing.assert_allclose(ws["served_w"].cpu().numpy(), o["served_w"], rtol=2e-6, atol=1e-7)
     # A3 permutation: bit-exact
-    counts, offsets, pos, src = port.permute(served, E, 128)
+    counts, offsets, pos, src = port.permute(served, E, c["layer"].seg_pad)
     assert np.array_equal(ws["counts"].cpu().numpy(), counts)
     assert np.array_equal(ws["seg_offsets"].cpu().numpy(), offsets)
     assert np.array_equal(ws["pos"].cpu().numpy().astype(np.int64), pos)

@@ -16,17 +16,17 @@ from helpers import build_layer  # noqa: E402
 
 
 def main():
-    a = [int(v) for v in sys.argv[1:]] + [0] * 6
-    T, d, f, E, k, slots = (a[0] or 2048, a[1] or 1024, a[2] or 2048, a[3] or 8, a[4] or 2, a[5] or 4)
+    a = [int(v) for v in sys.argv[1:]] + [0] * 7
+    T, d, f, E, k, slots, cg = (a[0] or 2048, a[1] or 1024, a[2] or 2048, a[3] or 8, a[4] or 2, a[5] or 4, a[6])
     layer, wg, experts = build_layer(E, d, f, k, "bf16", "swiglu", "topk_softmax", slots, list(range(0, E, 2))[:slots],
-                                     max_tokens=T)
+                                     max_tokens=T, gemm_cta_group=cg)
     x = torch.randn(T, d, generator=torch.Generator().manual_seed(5)).to(torch.bfloat16).cuda()
     y = layer.forward(x)
     torch.cuda.synchronize()
     ws = layer.workspace()
     off = ws["seg_offsets"].cpu().tolist()
     cnt = ws["counts"].cpu().tolist()
-    print("counts", cnt, "offsets", off)
+    print("cta_group", layer.gemm_cta_group, "counts", cnt, "offsets", off)
     ok = True
     for e in range(E):
         n = cnt[e]
