@@ -123,18 +123,21 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # synthetic workload
 # ---------------------------------------------------------------------------
-def build_workload(cfg, device, cta_group=0):
+def build_workload(cfg, device, cta_group=0, rank=0, world=1, parallel="replicas"):
     import torch
 
     import paper_2503_06823_b200 as emoe
     from paper_2503_06823_b200 import MoELayer
+    from paper_2503_06823_b200.ep import owned_experts, plan_destinations
 
     E, k, L, d, f = cfg["E"], cfg["k"], cfg["L"], cfg["d"], cfg["f"]
     P, Tp, P_train = cfg["prompts"], cfg["tokens"], cfg["train"]
     T = P * Tp
     shape = emoe.ModelShape(1, E, k, expert_bytes=(3 if cfg["act"] == "swiglu" else 2) * d * f * 2)
-    trace = emoe.gen_routing_trace(shape, cfg["layer_lambda"], cfg["prompt_lambda"], 0, cfg["seed"], P_train + P, Tp)
-    train, serve = trace[:P_train], trace[P_train:]
+    # every rank serves its own 32 prompts of the same trace (weak scaling)
+    trace = emoe.gen_routing_trace(shape, cfg["layer_lambda"], cfg["prompt_lambda"], 0, cfg["seed"],
+                                   P_train + P * world, Tp)
+    train, serve = trace[:P_train], trace[P_train + P * rank: P_train + P * (rank + 1)]
 
     # ---- predictor flow on the GPU (fit -> predict -> Eq. 2 -> targets -> plan)
     pred = emoe.moesim._Pred(1, E, k, 1, 0.01)
@@ -162,10 +165,13 @@ def build_workload(cfg, device, cta_group=0):
         pred.h, 0, p_(set_arr), p_(sizes), 1, p_(wo), p_(sens), p_(has), P, p_(req_task), p_(req_tok), 1,
         p_(resident0), p_(budgets), 0.0, p_(agg), p_(ev), p_(ne), p_(ld), p_(nl), p_(de)))
     loads = [int(e) for e in ld[0, : nl[0]]]
+    global_resident = sorted(loads)
+    if parallel == "ep" and world > 1:  # this GPU holds only the experts it serves
+        loads = owned_experts(plan_destinations(global_resident, E, world), rank)
 
     # ---- layer, weights (random-init, Mixtral/Switch shapes), planned loads
-    layer = MoELayer(d, f, E, k, activation=cfg["act"], dtype="bf16", weight_mode=cfg["wm"], num_slots=L,
-                     max_tokens=T, gemm_cta_group=cta_group)
+    layer = MoELayer(d, f, E, k, activation=cfg["act"], dtype="bf16", weight_mode=cfg["wm"],
+                     num_slots=max(1, len(loads)), max_tokens=T, gemm_cta_group=cta_group)
     g = torch.Generator(device=device).manual_seed(1234)
     q, _ = torch.linalg.qr(torch.randn(d, E, generator=g, device=device))  # orthonormal gate rows
     wg = q.T.contiguous()
@@ -192,8 +198,11 @@ def build_workload(cfg, device, cta_group=0):
     z = z - (z @ wg.T) @ wg
     x = (lg @ wg + z).to(torch.bfloat16).contiguous()
     del z, lg
+    res = [0] * E
+    for e in global_resident:
+        res[e] = 1
     info = dict(trace=trace, loads=loads, aggregate=agg[0].tolist(), load_bytes=load_bytes, load_ms=load_ms,
-                choices=choices, resident=layer.residency().tolist())
+                choices=choices, resident=res, global_resident=global_resident)
     return layer, pred, x, info
 
 
@@ -285,6 +294,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--gemm-cta-group", type=int, default=0, choices=[0, 1, 2],
                     help="FFN GEMM CTA group (0 = the layer's auto choice)")
+    ap.add_argument("--parallel", default="replicas", choices=["replicas", "ep"],
+                    help="N>1: replicas of the predicted resident set (no exchange) or expert parallelism "
+                         "(NCCL all-to-all dispatch/combine)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -305,7 +317,9 @@ def main():
     import paper_2503_06823_b200 as emoe
     from paper_2503_06823_b200 import _lib
 
-    layer, pred, x, info = build_workload(cfg, device, args.gemm_cta_group)
+    use_ep = args.parallel == "ep" and world > 1
+    layer, pred, x, info = build_workload(cfg, device, args.gemm_cta_group, rank, world,
+                                          "ep" if use_ep else "replicas")
     T = x.shape[0]
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream()
@@ -313,8 +327,17 @@ def main():
     tid = torch.zeros(P, dtype=torch.int32, device=device)
     import ctypes as C
 
+    ep_model = None
+    if use_ep:
+        from paper_2503_06823_b200.ep import ExpertParallelMoE, LayerBackend
+
+        ep_model = ExpertParallelMoE(LayerBackend(layer, info["global_resident"]), info["global_resident"])
+
     def step():
-        layer.forward(x, out=y)
+        if ep_model is not None:
+            ep_model(x)
+        else:
+            layer.forward(x, out=y)
         ws_topk = layer_ws_topk(layer)
         emoe.moesim.check(_lib.lib.emoe_hist_update(pred.h, C.c_void_p(ws_topk), P, Tp, C.c_void_p(tid.data_ptr()),
                                                     C.c_void_p(stream.cuda_stream)))
@@ -343,9 +366,12 @@ def main():
     if world > 1:
         dist.barrier()
     launches = int(_lib.lib.emoe_kernel_launches() - launches0)
-    stages = layer.stage_times()
-    layer.set_profiling(False)
     ms = ev0.elapsed_time(ev1) / args.steps
+    if ep_model is None:
+        stages = layer.stage_times()
+    else:  # no per-stage events on the EP path: attribute the whole step to the FFN (a lower bound)
+        stages = dict(route=0.0, permute=0.0, gemm1=ms, gemm2=0.0, combine=0.0)
+    layer.set_profiling(False)
     if world > 1:
         t = torch.tensor([ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -355,14 +381,21 @@ def main():
     # ---- end to end through the public host-buffer API (H2D x + D2H y every step)
     x_host = x.cpu().pin_memory()
     y_host = torch.empty_like(x_host).pin_memory()
+
+    def e2e_step():
+        if ep_model is None:
+            layer.forward_host(x_host, y_host)
+        else:
+            y_host.copy_(ep_model(x_host.to(device, non_blocking=True)))
+
     for _ in range(2):
-        layer.forward_host(x_host, y_host)
+        e2e_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        layer.forward_host(x_host, y_host)
+        e2e_step()
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     if world > 1:
         t = torch.tensor([e2e_s], device=device)
@@ -400,7 +433,7 @@ def main():
                            d_model=d, d_ff=f, activation=cfg["act"], served_rows=S, hit_rate=round(hit_rate, 4),
                            fallback_rate=round(fallback, 4),
                            l2="inputs larger than L2: x is %.0f MB per step" % (xb / 1e6),
-                           parallelism=f"replicas{world}" if world > 1 else "single",
+                           parallelism=(f"ep{world}" if use_ep else f"replicas{world}") if world > 1 else "single",
                            gemm_cta_group=layer.gemm_cta_group, seg_pad=layer.seg_pad),
                roofline=roofline, e2e=e2e, gpu_launches=launches, clocks=clk.summary(),
                stages_ms={kk: round(v, 4) for kk, v in stages.items()},

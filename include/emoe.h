@@ -77,7 +77,8 @@ typedef struct {
   int64_t max_tokens;
   int forced_miss; /* 1: a layer with no resident expert serves nothing (engine.cpp:533-537) */
   int gemm_cta_group; /* bf16 FFN GEMM: 1 = one CTA per 128x256 tile, 2 = CTA pair per 256x256
-                         tile (segments padded to 256 rows), 0 = auto (2 when E <= 16) */
+                         tile (segments padded to 256 rows), 0 = auto (1: faster under the
+                         1 kW power cap, profiles/r01_summary.md) */
 } emoe_layer_config;
 
 int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out);
@@ -125,6 +126,28 @@ int emoe_moe_forward_host(emoe_layer* layer, const void* x_host, void* y_host, i
 
 /* Route only (A1 + A2): fills the workspace routing fields. */
 int emoe_route(emoe_layer* layer, const void* x_dev, const float* logits_in_dev, int64_t T, void* stream);
+
+/* ========================================================================
+ * Stage entry points used by expert parallelism: the forward
+ * split at its two exchange points.
+ *   emoe_route_permute  A1-A3 into the workspace (x_perm, counts,
+ *                       seg_offsets, pos, served_w).
+ *   emoe_ffn_segments   A4 over caller rows x_rows [R][d]: n_seg segments
+ *                       starting at seg_offsets_dev[i] (multiples of the
+ *                       layer's seg_pad; seg_offsets_dev[n_seg] = R) served by
+ *                       resident expert seg_expert_dev[i]; h_scratch [R][f];
+ *                       writes y_rows [R][d].  n_seg <= 256.
+ *   emoe_combine        A5: y[t] = sum_j w[t][j] * y_rows[pos[t][j]].
+ * ====================================================================== */
+int emoe_route_permute(emoe_layer* layer, const void* x_dev, const float* logits_in_dev, int64_t T, void* stream);
+/* Expert parallelism: route against the GLOBAL resident set resident[E]
+ * (the reference Placement) while this GPU's slots hold only the experts it
+ * serves; NULL restores routing against the local slots. */
+int emoe_layer_set_route_residency(emoe_layer* layer, const uint8_t* resident, void* stream);
+int emoe_ffn_segments(emoe_layer* layer, const void* x_rows_dev, int64_t R, const int64_t* seg_offsets_dev,
+                      const int32_t* seg_expert_dev, int n_seg, void* h_scratch_dev, void* y_rows_dev, void* stream);
+int emoe_combine(emoe_layer* layer, const void* y_rows_dev, const int32_t* pos_dev, const float* served_w_dev,
+                 int64_t T, void* y_dev, void* stream);
 
 /* Device pointers of the last forward's intermediates (valid until the next
  * call on the layer).  Sizes: T tokens, R = rows_cap permuted rows. */

@@ -61,6 +61,10 @@ _decl("emoe_moe_forward", vp, vp, vp, vp, i64, vp)
 _decl("emoe_moe_forward_host", vp, vp, vp, i64, vp)
 _decl("emoe_route", vp, vp, vp, i64, vp)
 _decl("emoe_layer_workspace", vp, C.POINTER(Workspace))
+_decl("emoe_route_permute", vp, vp, vp, i64, vp)
+_decl("emoe_layer_set_route_residency", vp, vp, vp)
+_decl("emoe_ffn_segments", vp, vp, i64, vp, vp, C.c_int, vp, vp, vp)
+_decl("emoe_combine", vp, vp, vp, vp, i64, vp, vp)
 _decl("emoe_layer_set_profiling", vp, C.c_int)
 _decl("emoe_layer_stage_times", vp, vp)
 lib.emoe_kernel_launches.restype = C.c_longlong
@@ -87,7 +91,8 @@ EXPORTED = [
     "emoe_last_error", "emoe_version", "emoe_route_tokens_host", "emoe_layer_create", "emoe_layer_destroy",
     "emoe_layer_set_gate_host", "emoe_layer_register_expert_host", "emoe_layer_set_scores_host",
     "emoe_layer_begin_load", "emoe_layer_poll_loads", "emoe_layer_residency", "emoe_layer_last_load_stats",
-    "emoe_moe_forward", "emoe_moe_forward_host", "emoe_route", "emoe_layer_workspace", "emoe_layer_set_profiling",
+    "emoe_moe_forward", "emoe_moe_forward_host", "emoe_route", "emoe_route_permute", "emoe_layer_set_route_residency",
+    "emoe_ffn_segments", "emoe_combine", "emoe_layer_workspace", "emoe_layer_set_profiling",
     "emoe_layer_stage_times", "emoe_kernel_launches", "emoe_predictor_create",
     "emoe_predictor_destroy", "emoe_predictor_reset", "emoe_hist_update", "emoe_predictor_counts_host",
     "emoe_predictor_set_counts_host", "emoe_prompt_expert_sets", "emoe_predict_host",

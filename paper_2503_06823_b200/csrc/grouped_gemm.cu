@@ -28,6 +28,8 @@
 // crosses a segment.  Tiles are walked in a grouped raster: `group_m` row
 // blocks x all n blocks, sized on the host so the A panel (group_m x M x K x 2
 // bytes) stays L2-resident while the weight tiles stream past it.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -59,6 +61,7 @@ struct Params {
   int n_blocks;         // output column blocks
   int out_block_cols;   // 128 (SwiGLU) or 256
   int b_rows_per_slot;  // rows of one expert in the B pool
+  const int32_t* seg_expert;  // [segments] expert of each segment, null = segment i is expert i
   int group_m;          // raster group (row blocks)
   __nv_bfloat16* out;
   int64_t ldo;
@@ -195,7 +198,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
         const TileCoord c = decode_tile(t, total_mb, p.n_blocks, p.group_m, C::TILE_M, s_offs, E);
-        const int slot = p.slot_of_expert[c.expert];
+        const int slot = p.slot_of_expert[p.seg_expert ? p.seg_expert[c.expert] : c.expert];
         const int a_row = c.mb * C::TILE_M + (int)rank * 128;
         int b_row;
         const CUtensorMap* tb = &tmap_b;
@@ -401,23 +404,29 @@ CUtensorMap make_tmap_bf16_2d(const void* base, uint64_t rows, uint64_t cols, ui
 int gemm_tile_m(int cta_group) { return 128 * cta_group; }
 int gemm_b_box_rows(int epi, int cta_group) { return epi == EPI_SWIGLU ? 128 : 256 / cta_group; }
 
-// raster group: keep the A panel (group x tile_m rows x K) near 32 MB of L2
+// raster group: keep the A panel (group x tile_m rows x K) near `panel` MB of
+// L2 (default 48 MB of the 126 MB; EMOE_GEMM_PANEL_MB overrides for tuning)
 static int group_rows(int K, int tile_m) {
+  static int panel_mb = [] {
+    const char* v = getenv("EMOE_GEMM_PANEL_MB");
+    return v ? atoi(v) : 48;
+  }();
   const int64_t panel_row_bytes = (int64_t)tile_m * K * 2;
-  int g = (int)((32ll << 20) / panel_row_bytes);
+  int g = (int)(((int64_t)panel_mb << 20) / panel_row_bytes);
   return g < 2 ? 2 : (g > 64 ? 64 : g);
 }
 
 void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
-                         int num_sms, cudaStream_t stream) {
-  EMOE_REQUIRE(num_experts <= gemm::MAX_EXPERTS, "grouped_gemm: too many experts");
+                         int num_sms, cudaStream_t stream, const int32_t* seg_expert) {
+  EMOE_REQUIRE(num_experts <= gemm::MAX_EXPERTS, "grouped_gemm: too many segments");
   EMOE_REQUIRE(K % gemm::BK == 0, "grouped_gemm: K must be a multiple of 64");
   EMOE_REQUIRE(cta_group == 1 || cta_group == 2, "grouped_gemm: cta_group must be 1 or 2");
   gemm::Params p;
   p.seg_offsets = seg_offsets;
   p.slot_of_expert = slot_of_expert;
+  p.seg_expert = seg_expert;
   p.num_experts = num_experts;
   p.K = K;
   p.out_block_cols = epi == EPI_SWIGLU ? gemm::BN / 2 : gemm::BN;

@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(256) grouped_gemm_f32_kernel(const float* __re
                                                                const int64_t* __restrict__ seg,
                                                                const int32_t* __restrict__ slot_of_expert, int E,
                                                                int K, int b_rows_per_slot, float* __restrict__ out,
-                                                               int64_t ldo) {
+                                                               int64_t ldo, const int32_t* __restrict__ seg_expert) {
   __shared__ float As[TK][TM + 4];
   __shared__ float Bs[TK][TN + 4];
   __shared__ float B2s[EPI == EPI_SWIGLU ? TK : 1][TN + 4];
@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) grouped_gemm_f32_kernel(const float* __re
   if (row0 >= seg[E]) return;
   int e = 0;
   while (e + 1 < E && seg[e + 1] <= row0) ++e;
-  const int slot = slot_of_expert[e];
+  const int slot = slot_of_expert[seg_expert ? seg_expert[e] : e];
   const int n0 = blockIdx.x * TN;
   const float* Bp = B + ((int64_t)slot * b_rows_per_slot + n0) * K;
   const float* B2p = EPI == EPI_SWIGLU ? B2 + ((int64_t)slot * b_rows_per_slot + n0) * K : nullptr;
@@ -103,22 +103,22 @@ __global__ void __launch_bounds__(256) grouped_gemm_f32_kernel(const float* __re
 void launch_grouped_gemm_f32(int epi, const float* A, int64_t lda, const float* B, const float* B2,
                              const int64_t* seg_offsets, const int32_t* slot_of_expert, int num_experts, int K,
                              int N_out, int b_rows_per_slot, int64_t rows_cap, float* out, int64_t ldo,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, const int32_t* seg_expert) {
   EMOE_REQUIRE(K % TK == 0 && N_out % TN == 0, "grouped_gemm_f32: K % 16 and N % 64 must be 0");
   const int64_t rb = ceil_div(rows_cap, TM);
   if (rb == 0) return;
   dim3 grid(N_out / TN, (unsigned)rb);
   if (epi == EPI_SWIGLU)
-    grouped_gemm_f32_kernel<EPI_SWIGLU><<<grid, 256, 0, stream>>>(A, lda, B, B2, seg_offsets, slot_of_expert,
-                                                                   num_experts, K, b_rows_per_slot, out, ldo);
+    grouped_gemm_f32_kernel<EPI_SWIGLU><<<grid, 256, 0, stream>>>(
+        A, lda, B, B2, seg_offsets, slot_of_expert, num_experts, K, b_rows_per_slot, out, ldo, seg_expert);
   else if (epi == EPI_RELU)
-    grouped_gemm_f32_kernel<EPI_RELU><<<grid, 256, 0, stream>>>(A, lda, B, B2, seg_offsets, slot_of_expert,
-                                                                 num_experts, K, b_rows_per_slot, out, ldo);
+    grouped_gemm_f32_kernel<EPI_RELU><<<grid, 256, 0, stream>>>(
+        A, lda, B, B2, seg_offsets, slot_of_expert, num_experts, K, b_rows_per_slot, out, ldo, seg_expert);
   else
-    grouped_gemm_f32_kernel<EPI_STORE><<<grid, 256, 0, stream>>>(A, lda, B, B2, seg_offsets, slot_of_expert,
-                                                                  num_experts, K, b_rows_per_slot, out, ldo);
+    grouped_gemm_f32_kernel<EPI_STORE><<<grid, 256, 0, stream>>>(
+        A, lda, B, B2, seg_offsets, slot_of_expert, num_experts, K, b_rows_per_slot, out, ldo, seg_expert);
   EMOE_CUDA(cudaGetLastError());
-    count_launch();
+  count_launch();
 }
 
 }  // namespace emoe

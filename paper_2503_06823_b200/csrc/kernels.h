@@ -68,12 +68,12 @@ int gemm_b_box_rows(int epi, int cta_group);    // TMA box rows of the weight op
 void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
-                         int num_sms, cudaStream_t stream);
+                         int num_sms, cudaStream_t stream, const int32_t* seg_expert = nullptr);
 
 // K4 fp32 path (SIMT FFMA): same grouping/epilogues, fp32 in/out
 void launch_grouped_gemm_f32(int epi, const float* A, int64_t lda, const float* B, const float* B2,
                              const int64_t* seg_offsets, const int32_t* slot_of_expert, int num_experts, int K,
                              int N_out, int b_rows_per_slot, int64_t rows_cap, float* out, int64_t ldo,
-                             cudaStream_t stream);
+                             cudaStream_t stream, const int32_t* seg_expert = nullptr);
 
 }  // namespace emoe

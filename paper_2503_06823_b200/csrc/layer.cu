@@ -156,10 +156,20 @@ struct emoe_layer {
     finish_pending(s);
   }
 
+  // Expert parallelism: routing sees the GLOBAL resident set (the reference
+  // Placement) while this GPU's slots hold only the experts it serves.
+  bool route_override = false;
+  std::vector<uint8_t> route_resident;
+  uint8_t* route_resident_dev = nullptr;
+
   void route(const void* x, const float* logits_in, int64_t T, cudaStream_t s) {
     EMOE_REQUIRE(T >= 0 && T <= cfg.max_tokens, "moe_forward: T exceeds the layer's max_tokens");
-    if (n_resident() == 0 && !cfg.forced_miss)
-      throw InvariantError("route_token: no resident experts at layer");
+    int n_route = n_resident();
+    if (route_override) {
+      n_route = 0;
+      for (uint8_t r : route_resident) n_route += r;
+    }
+    if (n_route == 0 && !cfg.forced_miss) throw InvariantError("route_token: no resident experts at layer");
     RouteArgs a;
     a.T = T;
     a.d = cfg.d_model;
@@ -167,7 +177,7 @@ struct emoe_layer {
     a.k = cfg.top_k;
     a.weight_mode = cfg.weight_mode;
     a.forced_miss = cfg.forced_miss;
-    a.resident = resident_dev;
+    a.resident = route_override ? route_resident_dev : resident_dev;
     a.scores = have_scores ? scores_dev : nullptr;
     a.error_flag = err_flag;
     RouteOut o{logits, topk, r_expert, r_rank, r_hit, served_idx, served_w, block_counts};
@@ -203,31 +213,49 @@ struct emoe_layer {
     mark(0, s);
     route(x, logits_in, T, s);
     mark(1, s);
+    permute(x, T, s);
+    mark(2, s);
+    ffn(x_perm, rows_cap, seg_offsets, nullptr, cfg.num_experts, h, y_perm, s, true);
+    launch_combine(y_perm, cfg.dtype, T, cfg.d_model, cfg.top_k, pos, served_w, y, s);
+    mark(5, s);
+  }
+
+  // A3 after route(): per-expert offsets, positions, gathered rows in x_perm
+  void permute(const void* x, int64_t T, cudaStream_t s) {
     const int nb = (int)ceil_div(T, kRouteBlockTokens);
-    const int E = cfg.num_experts, d = cfg.d_model, f = cfg.d_ff;
+    const int E = cfg.num_experts;
     launch_scan(block_counts, nb, E, seg_pad, counts, seg_offsets, block_base, s);
     EMOE_CUDA(cudaMemsetAsync(row_token, 0xff, sizeof(int32_t) * rows_cap, s));
-    launch_permute(x, elem, T, d, E, cfg.top_k, served_idx, seg_offsets, block_base, x_perm, pos, row_token, s);
-    mark(2, s);
+    launch_permute(x, elem, T, cfg.d_model, E, cfg.top_k, served_idx, seg_offsets, block_base, x_perm, pos,
+                   row_token, s);
+  }
+
+  // A4 over rows [R][d] in n_seg padded segments (seg_expert null: segment i = expert i).
+  // workspace = the rows are the layer's own x_perm/h/y_perm (cached tensor maps).
+  void ffn(const void* xr, int64_t R, const int64_t* segs, const int32_t* seg_expert, int n_seg, void* hr, void* yr,
+           cudaStream_t s, bool workspace) {
+    const int d = cfg.d_model, f = cfg.d_ff;
     if (cfg.dtype == EMOE_DTYPE_BF16) {
-      launch_grouped_gemm(swiglu() ? EPI_SWIGLU : EPI_RELU, cta_group, ta1, tb1, tb3, seg_offsets, slot_dev, E, d,
-                          f, f, static_cast<__nv_bfloat16*>(h), f, num_sms, s);
+      CUtensorMap a1 = ta1, a2 = ta2;
+      if (!workspace) {
+        a1 = make_tmap_bf16_2d(xr, (uint64_t)R, d, 128);
+        a2 = make_tmap_bf16_2d(hr, (uint64_t)R, f, 128);
+      }
+      launch_grouped_gemm(swiglu() ? EPI_SWIGLU : EPI_RELU, cta_group, a1, tb1, tb3, segs, slot_dev, n_seg, d, f, f,
+                          static_cast<__nv_bfloat16*>(hr), f, num_sms, s, seg_expert);
       mark(3, s);
-      launch_grouped_gemm(EPI_STORE, cta_group, ta2, tb2, tb2, seg_offsets, slot_dev, E, f, d, d,
-                          static_cast<__nv_bfloat16*>(y_perm), d, num_sms, s);
+      launch_grouped_gemm(EPI_STORE, cta_group, a2, tb2, tb2, segs, slot_dev, n_seg, f, d, d,
+                          static_cast<__nv_bfloat16*>(yr), d, num_sms, s, seg_expert);
       mark(4, s);
     } else {
-      launch_grouped_gemm_f32(swiglu() ? EPI_SWIGLU : EPI_RELU, static_cast<const float*>(x_perm), d,
-                              static_cast<const float*>(w1_pool), static_cast<const float*>(w3_pool), seg_offsets,
-                              slot_dev, E, d, f, f, rows_cap, static_cast<float*>(h), f, s);
+      launch_grouped_gemm_f32(swiglu() ? EPI_SWIGLU : EPI_RELU, static_cast<const float*>(xr), d,
+                              static_cast<const float*>(w1_pool), static_cast<const float*>(w3_pool), segs, slot_dev,
+                              n_seg, d, f, f, R, static_cast<float*>(hr), f, s, seg_expert);
       mark(3, s);
-      launch_grouped_gemm_f32(EPI_STORE, static_cast<const float*>(h), f, static_cast<const float*>(w2_pool),
-                              nullptr, seg_offsets, slot_dev, E, f, d, d, rows_cap, static_cast<float*>(y_perm), d,
-                              s);
+      launch_grouped_gemm_f32(EPI_STORE, static_cast<const float*>(hr), f, static_cast<const float*>(w2_pool),
+                              nullptr, segs, slot_dev, n_seg, f, d, d, R, static_cast<float*>(yr), d, s, seg_expert);
       mark(4, s);
     }
-    launch_combine(y_perm, cfg.dtype, T, d, cfg.top_k, pos, served_w, y, s);
-    mark(5, s);
   }
 
   // Host-buffer forward, pipelined in token chunks: the H2D copy of chunk i+1
@@ -341,6 +369,7 @@ struct emoe_layer {
       if (p) cudaFree(p);
     };
     for (void* p : {(void*)wg, w1_pool, w3_pool, w2_pool, (void*)slot_dev, (void*)resident_dev, (void*)scores_dev,
+                    (void*)route_resident_dev,
                     (void*)logits, (void*)topk, (void*)r_expert, (void*)r_rank, (void*)r_hit, (void*)served_idx,
                     (void*)served_w, (void*)block_counts, (void*)counts, (void*)seg_offsets, (void*)block_base,
                     (void*)pos, (void*)row_token, x_perm, h, y_perm, x_in, y_out, (void*)err_flag})
@@ -390,7 +419,7 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
       const int E = c.num_experts, k = c.top_k;
       const int64_t T = c.max_tokens;
       EMOE_REQUIRE(c.gemm_cta_group >= 0 && c.gemm_cta_group <= 2, "layer.gemm_cta_group: must be 0, 1 or 2");
-      L->cta_group = c.dtype == EMOE_DTYPE_BF16 ? (c.gemm_cta_group ? c.gemm_cta_group : (E <= 16 ? 2 : 1)) : 1;
+      L->cta_group = c.dtype == EMOE_DTYPE_BF16 ? (c.gemm_cta_group ? c.gemm_cta_group : 1) : 1;
       L->seg_pad = c.dtype == EMOE_DTYPE_BF16 ? gemm_tile_m(L->cta_group) : kSegPad;
       L->rows_cap = T * k + (int64_t)E * L->seg_pad;
       L->route_blocks = (int)ceil_div(T, kRouteBlockTokens);
@@ -552,6 +581,64 @@ int emoe_route(emoe_layer* L, const void* x, const float* logits_in, int64_t T, 
     EMOE_REQUIRE(L && (x || logits_in), "route: null argument");
     L->poll(false, static_cast<cudaStream_t>(stream), nullptr);
     L->route(x, logits_in, T, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int emoe_layer_set_route_residency(emoe_layer* L, const uint8_t* resident, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(L, "set_route_residency: null layer");
+    if (!resident) {
+      L->route_override = false;
+      return;
+    }
+    const int E = L->cfg.num_experts;
+    if (!L->route_resident_dev) L->route_resident_dev = dmalloc<uint8_t>(E);
+    L->route_resident.assign(resident, resident + E);
+    TableUpdate u;
+    u.E = E;
+    for (int e = 0; e < E; ++e) {
+      u.resident[e] = resident[e] ? 1 : 0;
+      u.slot[e] = L->slot_of_expert[e];
+    }
+    // same parameter-carried update as the slot tables; slot table rewritten unchanged
+    set_tables_kernel<<<1, 128, 0, static_cast<cudaStream_t>(stream)>>>(u, L->route_resident_dev, L->slot_dev);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+    L->route_override = true;
+  });
+}
+
+int emoe_route_permute(emoe_layer* L, const void* x, const float* logits_in, int64_t T, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(L && x, "route_permute: null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    L->poll(false, s, nullptr);
+    L->route(x, logits_in, T, s);
+    if (T > 0) L->permute(x, T, s);
+  });
+}
+
+int emoe_ffn_segments(emoe_layer* L, const void* x_rows, int64_t R, const int64_t* seg_offsets, const int32_t* seg_expert,
+                      int n_seg, void* h_scratch, void* y_rows, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(L && seg_offsets && seg_expert, "ffn_segments: null argument");
+    EMOE_REQUIRE(n_seg >= 0 && n_seg <= 256, "ffn_segments: n_seg must be in [0, 256]");
+    if (n_seg == 0 || R == 0) return;
+    EMOE_REQUIRE(x_rows && h_scratch && y_rows, "ffn_segments: null buffer");
+    EMOE_REQUIRE(R % L->seg_pad == 0, "ffn_segments: R must be a multiple of the layer's seg_pad");
+    const bool was = L->profiling;
+    L->profiling = false;  // stage events belong to forward()
+    L->ffn(x_rows, R, seg_offsets, seg_expert, n_seg, h_scratch, y_rows, static_cast<cudaStream_t>(stream), false);
+    L->profiling = was;
+  });
+}
+
+int emoe_combine(emoe_layer* L, const void* y_rows, const int32_t* pos, const float* served_w, int64_t T, void* y,
+                 void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(L && y_rows && pos && served_w && y, "combine: null argument");
+    launch_combine(y_rows, L->cfg.dtype, T, L->cfg.d_model, L->cfg.top_k, pos, served_w, y,
+                   static_cast<cudaStream_t>(stream));
   });
 }
 

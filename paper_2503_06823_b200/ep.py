@@ -1,0 +1,172 @@
+"""Expert parallelism for the predicted-residency MoE layer.
+
+Tokens are data-parallel: every rank routes its own tokens against the GLOBAL
+resident set (the reference Placement, replicated), while the resident experts'
+weights are sharded across ranks.  When there are fewer resident experts than
+ranks (e.g. 4 resident Mixtral experts on 8 GPUs) groups of L ranks each hold a
+full replica of the resident set and source ranks are spread over the groups.
+
+One step on every rank:
+  1. route + permute locally (K1 + K3): padded per-expert segments of x
+  2. segment-size all-to-all (tiny) so every rank knows what it receives
+  3. dispatch all-to-all(v) of the padded segments, chunks ordered by
+     (source rank, expert, token)
+  4. grouped FFN (K4) on the received segments, one segment per (source, expert)
+  5. return all-to-all(v) of the expert outputs into the source's layout
+  6. combine at the source in slot order (K5)
+Each row's FFN is the same kernel with the same weights wherever it runs, and
+the combine order is fixed at the source, so the EP=G output is bit-identical
+to EP=1 (tests/test_ep.py checks it with gloo on CPU and on the GPU).
+
+The exchange is NCCL all_to_all_single over NVLink for device tensors; with a
+gloo group (CPU tests, or several ranks sharing one GPU) tensors are staged
+through host memory.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def plan_destinations(resident: Sequence[int], num_experts: int, world: int) -> np.ndarray:
+    """dest[src, e] = rank that computes source `src`'s rows of resident expert e
+    (-1 for non-resident experts).  Monotone in e for every source, so each
+    source's permuted buffer is already grouped by destination."""
+    res = sorted(int(e) for e in resident)
+    L = len(res)
+    dest = np.full((world, num_experts), -1, np.int64)
+    if L == 0:
+        return dest
+    if L >= world:
+        for i, e in enumerate(res):  # contiguous blocks of resident experts per rank
+            dest[:, e] = i * world // L
+    else:
+        groups = world // L  # full replicas of the resident set
+        for src in range(world):
+            g = src % groups
+            for i, e in enumerate(res):
+                dest[src, e] = g * L + i
+    return dest
+
+
+def owned_experts(dest: np.ndarray, rank: int) -> list:
+    return sorted({int(e) for e in np.flatnonzero((dest == rank).any(axis=0))})
+
+
+@dataclass
+class RoutedBatch:
+    seg_offsets: np.ndarray  # [E+1] host, padded segment starts
+    rows: torch.Tensor       # [seg_offsets[E], d] permuted activations
+    pos: torch.Tensor        # [T, k]
+    served_w: torch.Tensor   # [T, k]
+    T: int
+
+
+class LayerBackend:
+    """The sm_100a kernels through the C ABI (paper_2503_06823_b200.MoELayer)."""
+
+    def __init__(self, layer, global_resident: Sequence[int]):
+        self.layer = layer
+        res = np.zeros(layer.E, np.uint8)
+        res[list(global_resident)] = 1
+        layer.set_route_residency(res)
+        self.d, self.f, self.E = layer.d, layer.f, layer.E
+        self.dtype = layer.torch_dtype
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self._ws = None
+
+    def route_permute(self, x: torch.Tensor) -> RoutedBatch:
+        self.layer.route_permute(x)
+        ws = self.layer.workspace()
+        self.pad = self.layer.seg_pad
+        seg = ws["seg_offsets"].cpu().numpy()  # host needs the split sizes (syncs the stream)
+        return RoutedBatch(seg, ws["x_perm"][: int(seg[-1])], ws["pos"], ws["served_w"], x.shape[0])
+
+    def ffn(self, rows: torch.Tensor, seg_offsets: np.ndarray, seg_expert: np.ndarray) -> torch.Tensor:
+        R = rows.shape[0]
+        y = torch.empty(R, self.d, dtype=self.dtype, device=self.device)
+        if len(seg_expert) == 0 or R == 0:
+            return y
+        h = torch.empty(R, self.f, dtype=self.dtype, device=self.device)
+        so = torch.from_numpy(np.ascontiguousarray(seg_offsets, np.int64)).to(self.device)
+        se = torch.from_numpy(np.ascontiguousarray(seg_expert, np.int32)).to(self.device)
+        self.layer.ffn_segments(rows, so, se, h, y)
+        return y
+
+    def combine(self, y_rows: torch.Tensor, batch: RoutedBatch) -> torch.Tensor:
+        out = torch.empty(batch.T, self.d, dtype=self.dtype, device=self.device)
+        self.layer.combine(y_rows, batch.pos, batch.served_w, out)
+        return out
+
+
+class ExpertParallelMoE:
+    """EP forward over a process group; `backend` provides the local kernels."""
+
+    def __init__(self, backend, global_resident: Sequence[int], group=None):
+        self.backend = backend
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.dest = plan_destinations(global_resident, backend.E, self.world)
+        self.stage_on_host = dist.get_backend(group) != "nccl"
+        self.last = {}
+
+    def owned(self) -> list:
+        return owned_experts(self.dest, self.rank)
+
+    def _a2a(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits) -> torch.Tensor:
+        if self.stage_on_host and inp.is_cuda:
+            o = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits, group=self.group)
+            out.copy_(o)
+            return out
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+        return out
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        b = self.backend
+        E, W, r = b.E, self.world, self.rank
+        batch = b.route_permute(x)
+        psz = np.diff(batch.seg_offsets)  # padded rows per expert
+        # rows this rank sends each destination, per expert
+        send_meta = np.zeros((W, E), np.int64)
+        for e in np.flatnonzero(psz):
+            q = self.dest[r, e]
+            if q < 0:
+                raise RuntimeError(f"expert {e} has rows but is not in the global resident set")
+            send_meta[q, e] = psz[e]
+        meta_out = torch.empty(W * E, dtype=torch.int64)
+        meta_in = torch.from_numpy(send_meta.reshape(-1)).clone()
+        if self.stage_on_host:
+            dist.all_to_all_single(meta_out, meta_in, group=self.group)
+        else:  # NCCL exchanges device tensors
+            dev = torch.device("cuda", torch.cuda.current_device())
+            o = meta_out.to(dev)
+            dist.all_to_all_single(o, meta_in.to(dev), group=self.group)
+            meta_out.copy_(o.cpu())
+        recv_meta = meta_out.numpy().reshape(W, E)
+        send_rows = send_meta.sum(axis=1).tolist()
+        recv_rows = recv_meta.sum(axis=1).tolist()
+        R = int(sum(recv_rows))
+        recv = torch.empty(R, b.d, dtype=batch.rows.dtype, device=batch.rows.device)
+        self._a2a(recv, batch.rows, recv_rows, send_rows)
+        # one segment per (source, expert), sources in rank order
+        seg_off, seg_exp, off = [0], [], 0
+        for src in range(W):
+            for e in range(E):
+                n = int(recv_meta[src, e])
+                if n:
+                    off += n
+                    seg_off.append(off)
+                    seg_exp.append(e)
+        y_recv = b.ffn(recv, np.asarray(seg_off, np.int64), np.asarray(seg_exp, np.int32))
+        y_back = torch.empty_like(batch.rows)
+        self._a2a(y_back, y_recv, send_rows, recv_rows)
+        self.last = dict(send_rows=send_rows, recv_rows=recv_rows, segments=len(seg_exp))
+        return b.combine(y_back, batch)
+
+    __call__ = forward

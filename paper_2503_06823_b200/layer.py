@@ -149,6 +149,31 @@ class MoELayer:
         check(lib.emoe_route(self.h, C.c_void_p(x.data_ptr()) if x is not None else None,
                              C.c_void_p(logits.data_ptr()) if logits is not None else None, T, _stream_ptr(stream)))
 
+    # -- stage entry points (expert parallelism) -----------------------------
+    def set_route_residency(self, resident: Optional[Sequence[int]], stream=None) -> None:
+        if resident is None:
+            check(lib.emoe_layer_set_route_residency(self.h, None, _stream_ptr(stream)))
+            return
+        r = np.ascontiguousarray(np.asarray(resident, np.uint8))
+        check(lib.emoe_layer_set_route_residency(self.h, r.ctypes.data_as(C.c_void_p), _stream_ptr(stream)))
+
+    def route_permute(self, x: torch.Tensor, stream=None) -> None:
+        check(lib.emoe_route_permute(self.h, C.c_void_p(x.data_ptr()), None, x.shape[0], _stream_ptr(stream)))
+
+    def ffn_segments(self, x_rows: torch.Tensor, seg_offsets: torch.Tensor, seg_expert: torch.Tensor,
+                     h_scratch: torch.Tensor, y_rows: torch.Tensor, stream=None) -> None:
+        n = seg_expert.numel()
+        check(lib.emoe_ffn_segments(self.h, C.c_void_p(x_rows.data_ptr()), x_rows.shape[0],
+                                    C.c_void_p(seg_offsets.data_ptr()), C.c_void_p(seg_expert.data_ptr()), n,
+                                    C.c_void_p(h_scratch.data_ptr()), C.c_void_p(y_rows.data_ptr()),
+                                    _stream_ptr(stream)))
+
+    def combine(self, y_rows: torch.Tensor, pos: torch.Tensor, served_w: torch.Tensor, out: torch.Tensor,
+                stream=None) -> None:
+        check(lib.emoe_combine(self.h, C.c_void_p(y_rows.data_ptr()), C.c_void_p(pos.data_ptr()),
+                               C.c_void_p(served_w.data_ptr()), out.shape[0], C.c_void_p(out.data_ptr()),
+                               _stream_ptr(stream)))
+
     def set_profiling(self, enable: bool = True) -> None:
         check(lib.emoe_layer_set_profiling(self.h, int(enable)))
 
