@@ -405,11 +405,11 @@ int gemm_tile_m(int cta_group) { return 128 * cta_group; }
 int gemm_b_box_rows(int epi, int cta_group) { return epi == EPI_SWIGLU ? 128 : 256 / cta_group; }
 
 // raster group: keep the A panel (group x tile_m rows x K) near `panel` MB of
-// L2 (default 48 MB of the 126 MB; EMOE_GEMM_PANEL_MB overrides for tuning)
+// L2 (default 24 MB of the 126 MB; EMOE_GEMM_PANEL_MB overrides for tuning)
 static int group_rows(int K, int tile_m) {
   static int panel_mb = [] {
     const char* v = getenv("EMOE_GEMM_PANEL_MB");
-    return v ? atoi(v) : 48;
+    return v ? atoi(v) : 24;  // 24 MB measured best of {24, 48, 96} (profiles/r01_summary.md)
   }();
   const int64_t panel_row_bytes = (int64_t)tile_m * K * 2;
   int g = (int)(((int64_t)panel_mb << 20) / panel_row_bytes);
