@@ -197,6 +197,10 @@ int emoe_predictor_create(int num_layers, int num_experts, int top_k, int num_ta
                           emoe_predictor** out);
 int emoe_predictor_destroy(emoe_predictor* pred);
 int emoe_predictor_reset(emoe_predictor* pred);
+/* End the prompt chain: the next emoe_hist_update does not count a
+ * transition from the last prompt seen (an empty prompt in the reference
+ * breaks the chain, predictor.cpp:176-178). */
+int emoe_predictor_break_chain(emoe_predictor* pred);
 
 /* fit (predictor.cpp:137-185) as an incremental histogram on the GPU.
  * trace_dev: [P][m][T][k] int32 routing history, task_ids_dev: [P] or NULL.
@@ -204,6 +208,8 @@ int emoe_predictor_reset(emoe_predictor* pred);
  * equals the sum of the calls (counts commute, test_predictor.cpp:284-296). */
 int emoe_hist_update(emoe_predictor* pred, const int32_t* trace_dev, int P, int T, const int32_t* task_ids_dev,
                      void* stream);
+/* Same from host memory (copied to the device; returns when the update is done). */
+int emoe_hist_update_host(emoe_predictor* pred, const int32_t* trace_host, int P, int T, const int32_t* task_ids_host);
 /* Export the tallies (exact integers as doubles): layer [(m-1)][E][E],
  * prompt [m][E][E], task [num_tasks][m][E]. */
 int emoe_predictor_counts_host(emoe_predictor* pred, double* layer_counts, double* prompt_counts,

@@ -72,7 +72,9 @@ lib.emoe_kernel_launches.argtypes = []
 _decl("emoe_predictor_create", C.c_int, C.c_int, C.c_int, C.c_int, dbl, C.POINTER(vp))
 _decl("emoe_predictor_destroy", vp)
 _decl("emoe_predictor_reset", vp)
+_decl("emoe_predictor_break_chain", vp)
 _decl("emoe_hist_update", vp, vp, C.c_int, C.c_int, vp, vp)
+_decl("emoe_hist_update_host", vp, vp, C.c_int, C.c_int, vp)
 _decl("emoe_predictor_counts_host", vp, vp, vp, vp)
 _decl("emoe_predictor_set_counts_host", vp, vp, vp, vp)
 _decl("emoe_prompt_expert_sets", vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp)
@@ -94,7 +96,7 @@ EXPORTED = [
     "emoe_moe_forward", "emoe_moe_forward_host", "emoe_route", "emoe_route_permute", "emoe_layer_set_route_residency",
     "emoe_ffn_segments", "emoe_combine", "emoe_layer_workspace", "emoe_layer_set_profiling",
     "emoe_layer_stage_times", "emoe_kernel_launches", "emoe_predictor_create",
-    "emoe_predictor_destroy", "emoe_predictor_reset", "emoe_hist_update", "emoe_predictor_counts_host",
+    "emoe_predictor_destroy", "emoe_predictor_reset", "emoe_predictor_break_chain", "emoe_hist_update", "emoe_hist_update_host", "emoe_predictor_counts_host",
     "emoe_predictor_set_counts_host", "emoe_prompt_expert_sets", "emoe_predict_host",
     "emoe_predicted_frequencies_host", "emoe_expected_tokens_host", "emoe_select_experts_host",
     "emoe_loading_targets_host", "emoe_plan_loading_host", "emoe_invocation_host", "emoe_gen_routing_trace",

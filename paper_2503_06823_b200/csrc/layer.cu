@@ -704,14 +704,41 @@ int emoe_route_tokens_host(const int32_t* choices, int64_t T, int k, const uint8
     for (int64_t i = 0; i < T * k; ++i)
       EMOE_REQUIRE(choices[i] >= 0 && choices[i] < E, "route_tokens: gate choice out of range");
     if (T == 0) return;
-    DevBuf<int32_t> dch(choices, (size_t)T * k);
-    DevBuf<uint8_t> dres(resident, E);
-    DevBuf<double> dsc(scores ? (size_t)E : 0);
-    if (scores) EMOE_CUDA(cudaMemcpy(dsc.p, scores, sizeof(double) * E, cudaMemcpyHostToDevice));
-    DevBuf<int32_t> dex(T), drk(T);
-    DevBuf<uint8_t> dhit(T);
-    DevBuf<int> flag(1);
-    EMOE_CUDA(cudaMemset(flag.p, 0, sizeof(int)));
+    // Per-thread scratch reused across calls (the engine calls route_token per
+    // request per layer, engine.cpp:538): one pinned staging block, one device
+    // block, one H2D + one D2H copy per call.
+    //   in  = [flag i32 | pad | scores f64 x128 | resident u8 x128 | choices i32 x T*k]
+    //   out = [expert i32 x T | rank i32 x T | hit u8 x T]
+    struct Scratch {
+      uint8_t* host = nullptr;
+      uint8_t* dev = nullptr;
+      size_t cap = 0;
+      cudaStream_t s = nullptr;
+      ~Scratch() {
+        if (host) cudaFreeHost(host);
+        if (dev) cudaFree(dev);
+        if (s) cudaStreamDestroy(s);
+      }
+    };
+    static thread_local Scratch sc;
+    const size_t in_bytes = 16 + 128 * 8 + 128 + (size_t)T * k * 4;
+    const size_t in_pad = (in_bytes + 15) / 16 * 16;
+    const size_t total = in_pad + (size_t)T * 9;
+    if (total > sc.cap) {
+      if (sc.host) EMOE_CUDA(cudaFreeHost(sc.host));
+      if (sc.dev) EMOE_CUDA(cudaFree(sc.dev));
+      const size_t cap = std::max<size_t>(total * 2, 1 << 16);
+      EMOE_CUDA(cudaHostAlloc(&sc.host, cap, cudaHostAllocDefault));
+      EMOE_CUDA(cudaMalloc(&sc.dev, cap));
+      sc.cap = cap;
+    }
+    if (!sc.s) EMOE_CUDA(cudaStreamCreateWithFlags(&sc.s, cudaStreamNonBlocking));
+    uint8_t* h = sc.host;
+    std::memset(h, 0, 16);
+    if (scores) std::memcpy(h + 16, scores, sizeof(double) * E);
+    std::memcpy(h + 16 + 1024, resident, E);
+    std::memcpy(h + 16 + 1024 + 128, choices, (size_t)T * k * 4);
+    EMOE_CUDA(cudaMemcpyAsync(sc.dev, h, in_bytes, cudaMemcpyHostToDevice, sc.s));
     RouteArgs a;
     a.T = T;
     a.d = 0;
@@ -719,17 +746,22 @@ int emoe_route_tokens_host(const int32_t* choices, int64_t T, int k, const uint8
     a.k = k;
     a.weight_mode = 0;
     a.forced_miss = 0;
-    a.resident = dres.p;
-    a.scores = scores ? dsc.p : nullptr;
-    a.error_flag = flag.p;
-    RouteOut o{nullptr, nullptr, dex.p, drk.p, dhit.p, nullptr, nullptr, nullptr};
-    launch_route_from_choices(dch.p, a, o, 0);
+    a.resident = sc.dev + 16 + 1024;
+    a.scores = scores ? reinterpret_cast<const double*>(sc.dev + 16) : nullptr;
+    a.error_flag = reinterpret_cast<int*>(sc.dev);
+    uint8_t* out = sc.dev + in_pad;
+    RouteOut o{nullptr, nullptr, reinterpret_cast<int32_t*>(out), reinterpret_cast<int32_t*>(out + 4 * T),
+               out + 8 * T, nullptr, nullptr, nullptr};
+    launch_route_from_choices(reinterpret_cast<const int32_t*>(sc.dev + 16 + 1024 + 128), a, o, sc.s);
+    EMOE_CUDA(cudaMemcpyAsync(h, sc.dev, 4, cudaMemcpyDeviceToHost, sc.s));
+    EMOE_CUDA(cudaMemcpyAsync(h + in_pad, out, (size_t)T * 9, cudaMemcpyDeviceToHost, sc.s));
+    EMOE_CUDA(cudaStreamSynchronize(sc.s));
     int f = 0;
-    EMOE_CUDA(cudaMemcpy(&f, flag.p, sizeof(int), cudaMemcpyDeviceToHost));
+    std::memcpy(&f, h, 4);
     if (f == 3) throw InvariantError("route_token: no resident experts at layer");
-    dex.to_host(out_expert);
-    drk.to_host(out_rank);
-    dhit.to_host(out_hit);
+    std::memcpy(out_expert, h + in_pad, (size_t)T * 4);
+    std::memcpy(out_rank, h + in_pad + 4 * T, (size_t)T * 4);
+    std::memcpy(out_hit, h + in_pad + 8 * T, (size_t)T);
   });
 }
 

@@ -568,6 +568,13 @@ int emoe_predictor_reset(emoe_predictor* P) {
   });
 }
 
+int emoe_predictor_break_chain(emoe_predictor* P) {
+  return guard([&] {
+    EMOE_REQUIRE(P, "predictor_break_chain: null");
+    P->has_last = false;
+  });
+}
+
 int emoe_hist_update(emoe_predictor* P, const int32_t* trace, int nP, int T, const int32_t* task_ids, void* stream) {
   return guard([&] {
     EMOE_REQUIRE(P && trace, "hist_update: null argument");
@@ -600,6 +607,26 @@ int emoe_hist_update(emoe_predictor* P, const int32_t* trace, int nP, int T, con
     EMOE_CUDA(cudaGetLastError());
     count_launch();
     P->has_last = true;
+  });
+}
+
+int emoe_hist_update_host(emoe_predictor* P, const int32_t* trace, int nP, int T, const int32_t* task_ids) {
+  return guard([&] {
+    EMOE_REQUIRE(P && (trace || nP == 0), "hist_update_host: null argument");
+    if (nP == 0) return;
+    EMOE_REQUIRE(T >= 1, "hist_update: tokens_per_prompt must be >= 1");
+    const size_t n = (size_t)nP * P->m * T * P->k;
+    for (size_t i = 0; i < n; ++i)
+      EMOE_REQUIRE(trace[i] >= 0 && trace[i] < P->E, "predictor.trace: expert index out of range");
+    if (task_ids)
+      for (int p = 0; p < nP; ++p)
+        EMOE_REQUIRE(task_ids[p] >= 0 && task_ids[p] < P->n_tasks, "predictor.task_ids: index out of range");
+    DevBuf<int32_t> dt(trace, n);
+    DevBuf<int32_t> di(task_ids ? (size_t)nP : 0);
+    if (task_ids) EMOE_CUDA(cudaMemcpy(di.p, task_ids, nP * sizeof(int32_t), cudaMemcpyHostToDevice));
+    const int rc = emoe_hist_update(P, dt.p, nP, T, task_ids ? di.p : nullptr, nullptr);
+    if (rc != EMOE_OK) throw CudaError(last_error_slot());
+    EMOE_CUDA(cudaDeviceSynchronize());
   });
 }
 
