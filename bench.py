@@ -289,7 +289,10 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="emoe", choices=["emoe", "reference"])
-    ap.add_argument("--config", default="mixtral", choices=list(CONFIGS))
+    ap.add_argument("--config", default="mixtral", choices=list(CONFIGS) + ["stream"],
+                    help="stream = BASELINE config 5 (mixed-task 8k-token prompt stream over a 32-layer stack)")
+    ap.add_argument("--stream-layers", type=int, default=32)
+    ap.add_argument("--stream-prompts", type=int, default=80)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--gemm-cta-group", type=int, default=0, choices=[0, 1, 2],
@@ -299,6 +302,8 @@ def main():
                          "(NCCL all-to-all dispatch/combine)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.config == "stream":
+        return main_stream(args)
     cfg = CONFIGS[args.config]
 
     import torch
@@ -419,8 +424,13 @@ def main():
     ffn_flops = 2.0 * nmat * d * f * S
     ffn_ms = stages["gemm1"] + stages["gemm2"]
     achieved = ffn_flops / (ffn_ms / 1e3) / 1e12
+    traffic = None
+    tfile = ROOT / "profiles" / "ffn_gemm_dram_traffic.json"
+    if tfile.exists() and args.config == "mixtral":  # ncu capture of this workload (profiles/)
+        traffic = json.loads(tfile.read_text())["ffn_bytes_per_step"]
     roofline = dict(bound="tensor", achieved=round(achieved, 1), peak=peaks["bf16_sustained"], unit="TFLOP/s",
-                    frac=round(achieved / peaks["bf16_sustained"], 4), traffic=None,
+                    frac=round(achieved / peaks["bf16_sustained"], 4), traffic=traffic,
+                    traffic_unit="bytes per step (GEMM1 + GEMM2), ncu dram__bytes_read+write",
                     kernel="grouped_gemm_kernel (K4: GEMM1 SwiGLU + GEMM2), avg of the timed steps",
                     algorithmic=f"2*{nmat}*d*f*S = {ffn_flops:.4g} FLOP per step (S={S} served rows)",
                     peak_kind=f"bf16_tflops_sustained ({peaks['source']}); burst {peaks['bf16']}",
@@ -501,6 +511,80 @@ def experts_f32(cfg, device, info):
             out[e] = (w1.float().cpu().numpy(), None if w3 is None else w3.float().cpu().numpy(),
                       w2.float().cpu().numpy())
     return out
+
+
+def main_stream(args):
+    """BASELINE config 5: a mixed-task stream of 8k-token prompts ("conv" sensitive on
+    every layer, "cls" on none, mix 0.5/0.5) through a 32-layer Mixtral-shaped stack
+    with phi = 0.5 (4 of 8 experts per layer), predictor every p = 40 prompts and
+    skipped for windows with only insensitive requests, expert loads on a shared
+    side copy stream overlapped with compute.  Routing-driven: the gate logits of
+    prompt p / layer l embed the reference trace.  Single GPU."""
+    import torch
+
+    import paper_2503_06823_b200 as emoe
+    from paper_2503_06823_b200.serving import MoEStack, StreamConfig, TaskSpec, moesim_prompt_sets, run_stream
+
+    torch.cuda.set_device(0)
+    device = torch.device("cuda", 0)
+    m, E, k, L, d, f, T, p = args.stream_layers, 8, 2, 4, 4096, 14336, 8192, 40
+    tasks = {"cls": TaskSpec(16.0, [0] * m), "conv": TaskSpec(256.0, [1] * m)}
+    cfg = StreamConfig(m=m, E=E, k=k, L=L, d=d, f=f, tokens_per_prompt=T, period=p, mode=0, tasks=tasks)
+    P_train, P_serve = 60, args.stream_prompts
+    shape = emoe.ModelShape(m, E, k)
+    trace = emoe.gen_routing_trace(shape, 0.6, 0.8, 0, 17, P_train + P_serve, T)
+    rng = np.random.default_rng(5)
+    prompt_tasks = ["conv" if v < 0.5 else "cls" for v in rng.random(P_train + P_serve)]
+    # a window of only insensitive prompts exercises the skip
+    if P_serve >= 3 * p:
+        for q in range(P_train + 2 * p, P_train + 3 * p):
+            prompt_tasks[q] = "cls"
+    g = torch.Generator(device=device).manual_seed(1234)
+    host = [tuple((torch.randn(*s, generator=g, device=device) / s[1] ** 0.5).to(torch.bfloat16).cpu().pin_memory()
+                  for s in ((f, d), (f, d), (d, f))) for _ in range(E)]
+    gates = [torch.zeros(E, d, dtype=torch.bfloat16) for _ in range(m)]  # routing-driven: logits come from the trace
+    stack = MoEStack(cfg, host, gates)
+    trace_dev = torch.from_numpy(trace).to(device)
+    stack.fit(trace_dev[:P_train].contiguous(), prompt_tasks[:P_train])
+    # initial placement: the first plan from an empty device (blocking, untimed)
+    _, sets = moesim_prompt_sets(trace_dev, P_train - 1)
+    ops, _, _ = stack.invocation(sets, [(prompt_tasks[q], T) for q in range(P_train, P_train + p)])
+    stack.apply(ops)
+    for layer in stack.layers:
+        layer.poll_loads(blocking=True)
+    torch.cuda.synchronize()
+
+    def logits_of(q):  # [m][T][E]: logit[c_r] = 8 - r, others uniform in [-4, 4)
+        lg = torch.rand(m, T, E, generator=g, device=device) * 8.0 - 4.0
+        ch = trace_dev[q].long()
+        for r in range(k):
+            lg.scatter_(2, ch[:, :, r:r + 1], 8.0 - r)
+        return lg
+
+    x = torch.randn(T, d, generator=g, device=device).to(torch.bfloat16)
+    out = torch.empty_like(x)
+    hits = torch.zeros(m, dtype=torch.int64, device=device)
+    for q in range(P_train, P_train + args.warmup):  # warm-up prompts (no invocation)
+        stack.forward_prompt(x, logits_of(q), out, hits)
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        st = run_stream(stack, trace, trace_dev, prompt_tasks, x, logits_of, P_train, P_serve)
+    nmat = 3
+    served = None
+    flops_note = f"2*{nmat}*d*f per served (token, expert) per layer"
+    res = dict(metric=METRIC, value=round(st["tokens_per_s"], 1), unit="tokens/s", n_gpus=1, steps=P_serve,
+               warmup=args.warmup, ms_per_step=round(st["ms"] / P_serve, 3), higher_is_better=True, scaling="weak",
+               vs_baseline=None, dtype="bf16", data="synthetic (random-init weights; routing-driven from the "
+                                                   "reference Markov trace)",
+               config=dict(workload="BASELINE config 5: mixed-task stream, 8k-token prompts, %d-layer "
+                                     "Mixtral-shaped stack, phi=0.5, p=40, predictor skipped for insensitive "
+                                     "windows, loads overlapped" % m, prompts=P_serve, tokens_per_prompt=T,
+                           layers=m, tasks={n: dict(wo=t.wo, sensitive_layers=sum(t.sensitivity))
+                                            for n, t in tasks.items()}),
+               stream=dict((kk, v) for kk, v in st.items() if kk not in ("ms",)), clocks=clk.summary(),
+               note=flops_note, served=served)
+    print(json.dumps(res), flush=True)
+    stack.close()
 
 
 def main_reference(args, cfg, rank, world):

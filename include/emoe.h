@@ -90,6 +90,16 @@ int emoe_layer_set_gate_host(emoe_layer* layer, const void* wg);
  * w1, w3: [f][d] (w3 ignored for ReLU), w2: [d][f]  (layer dtype) */
 int emoe_layer_register_expert_host(emoe_layer* layer, int expert, const void* w1, const void* w3, const void* w2);
 
+/* Same, but the library keeps the caller's host pointers (no copy): they must
+ * stay valid and should be pinned (cudaHostAlloc / cudaHostRegister) for the
+ * side-stream copies to overlap compute.  Lets a stack of layers share one
+ * pinned copy of the weights. */
+int emoe_layer_register_expert_pinned(emoe_layer* layer, int expert, const void* w1, const void* w3, const void* w2);
+/* H2D expert loads go to `stream` (NULL = the layer's own copy stream).
+ * Layers sharing one copy stream load layer-sequentially, as the engine
+ * schedules them (engine.cpp:431-440). */
+int emoe_layer_set_copy_stream(emoe_layer* layer, void* stream);
+
 /* Layer scores used by the route_token fallback (the engine's last aggregate
  * row, engine.cpp:529-531).  scores == NULL sets the empty score vector. */
 int emoe_layer_set_scores_host(emoe_layer* layer, const double* scores);

@@ -53,6 +53,8 @@ _decl("emoe_layer_destroy", vp)
 _decl("emoe_layer_set_gate_host", vp, vp)
 _decl("emoe_layer_register_expert_host", vp, C.c_int, vp, vp, vp)
 _decl("emoe_layer_set_scores_host", vp, vp)
+_decl("emoe_layer_register_expert_pinned", vp, C.c_int, vp, vp, vp)
+_decl("emoe_layer_set_copy_stream", vp, vp)
 _decl("emoe_layer_begin_load", vp, vp, C.c_int, vp, C.c_int, vp)
 _decl("emoe_layer_poll_loads", vp, C.c_int, vp, C.POINTER(C.c_int))
 _decl("emoe_layer_residency", vp, vp)
@@ -91,7 +93,8 @@ _decl("emoe_gen_routing_trace", C.c_int, C.c_int, C.c_int, dbl, dbl, C.c_int, C.
 # every symbol include/emoe.h declares (checked by tests/test_boundary.py)
 EXPORTED = [
     "emoe_last_error", "emoe_version", "emoe_route_tokens_host", "emoe_layer_create", "emoe_layer_destroy",
-    "emoe_layer_set_gate_host", "emoe_layer_register_expert_host", "emoe_layer_set_scores_host",
+    "emoe_layer_set_gate_host", "emoe_layer_register_expert_host", "emoe_layer_register_expert_pinned",
+    "emoe_layer_set_copy_stream", "emoe_layer_set_scores_host",
     "emoe_layer_begin_load", "emoe_layer_poll_loads", "emoe_layer_residency", "emoe_layer_last_load_stats",
     "emoe_moe_forward", "emoe_moe_forward_host", "emoe_route", "emoe_route_permute", "emoe_layer_set_route_residency",
     "emoe_ffn_segments", "emoe_combine", "emoe_layer_workspace", "emoe_layer_set_profiling",

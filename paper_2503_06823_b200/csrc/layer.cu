@@ -332,9 +332,10 @@ struct emoe_layer {
     push_tables(s);
     if (nld == 0) return;
     // the freed slots may still be read by compute already enqueued on `s`
+    cudaStream_t cs = load_stream();
     EMOE_CUDA(cudaEventRecord(ev_evict, s));
-    EMOE_CUDA(cudaStreamWaitEvent(copy_stream, ev_evict, 0));
-    EMOE_CUDA(cudaEventRecord(ev_load_start, copy_stream));
+    EMOE_CUDA(cudaStreamWaitEvent(cs, ev_evict, 0));
+    EMOE_CUDA(cudaEventRecord(ev_load_start, cs));
     pending_bytes = 0;
     for (int i = 0; i < nld; ++i) {
       int slot = -1;
@@ -348,21 +349,25 @@ struct emoe_layer {
       const int e = ld[i];
       const size_t b1 = w1_elems() * elem, b2 = w2_elems() * elem;
       EMOE_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(w1_pool) + slot * b1, host_w1[e], b1, cudaMemcpyHostToDevice,
-                                copy_stream));
+                                cs));
       pending_bytes += (double)b1;
       if (swiglu()) {
         EMOE_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(w3_pool) + slot * b1, host_w3[e], b1,
-                                  cudaMemcpyHostToDevice, copy_stream));
+                                  cudaMemcpyHostToDevice, cs));
         pending_bytes += (double)b1;
       }
       EMOE_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(w2_pool) + slot * b2, host_w2[e], b2, cudaMemcpyHostToDevice,
-                                copy_stream));
+                                cs));
       pending_bytes += (double)b2;
       pending_experts.push_back(e);
       pending_slots.push_back(slot);
     }
-    EMOE_CUDA(cudaEventRecord(ev_load_done, copy_stream));
+    EMOE_CUDA(cudaEventRecord(ev_load_done, cs));
   }
+
+  cudaStream_t ext_copy_stream = nullptr;  // shared copy stream (layer-sequential loads)
+  std::vector<uint8_t> host_owned;         // 1 = library-owned pinned copy, 0 = caller pointer
+  cudaStream_t load_stream() const { return ext_copy_stream ? ext_copy_stream : copy_stream; }
 
   void destroy() {
     auto f = [](void* p) {
@@ -375,8 +380,8 @@ struct emoe_layer {
                     (void*)pos, (void*)row_token, x_perm, h, y_perm, x_in, y_out, (void*)err_flag})
       f(p);
     for (auto* v : {&host_w1, &host_w3, &host_w2})
-      for (void* p : *v)
-        if (p) cudaFreeHost(p);
+      for (size_t e = 0; e < v->size(); ++e)
+        if ((*v)[e] && e < host_owned.size() && host_owned[e]) cudaFreeHost((*v)[e]);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (in_stream) cudaStreamDestroy(in_stream);
     if (out_stream) cudaStreamDestroy(out_stream);
@@ -462,6 +467,7 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
       L->host_w1.assign(E, nullptr);
       L->host_w3.assign(E, nullptr);
       L->host_w2.assign(E, nullptr);
+      L->host_owned.assign(E, 1);
       L->slot_of_expert.assign(E, -1);
       L->expert_in_slot.assign(c.num_slots, -1);
       L->resident.assign(E, 0);
@@ -508,6 +514,10 @@ int emoe_layer_register_expert_host(emoe_layer* L, int e, const void* w1, const 
     EMOE_REQUIRE(e >= 0 && e < L->cfg.num_experts, "register_expert: expert index out of range");
     EMOE_REQUIRE(!L->swiglu() || w3, "register_expert: SwiGLU needs w3");
     const size_t b1 = L->w1_elems() * L->elem, b2 = L->w2_elems() * L->elem;
+    if (!L->host_owned[e]) {  // previously a caller pointer: start owning fresh copies
+      L->host_w1[e] = L->host_w3[e] = L->host_w2[e] = nullptr;
+      L->host_owned[e] = 1;
+    }
     auto put = [&](std::vector<void*>& v, const void* src, size_t bytes) {
       if (!v[e]) EMOE_CUDA(cudaHostAlloc(&v[e], bytes, cudaHostAllocDefault));
       std::memcpy(v[e], src, bytes);
@@ -515,6 +525,29 @@ int emoe_layer_register_expert_host(emoe_layer* L, int e, const void* w1, const 
     put(L->host_w1, w1, b1);
     if (L->swiglu()) put(L->host_w3, w3, b1);
     put(L->host_w2, w2, b2);
+  });
+}
+
+int emoe_layer_register_expert_pinned(emoe_layer* L, int e, const void* w1, const void* w3, const void* w2) {
+  return guard([&] {
+    EMOE_REQUIRE(L && w1 && w2, "register_expert: null weights");
+    EMOE_REQUIRE(e >= 0 && e < L->cfg.num_experts, "register_expert: expert index out of range");
+    EMOE_REQUIRE(!L->swiglu() || w3, "register_expert: SwiGLU needs w3");
+    if (L->host_owned[e])
+      for (auto* v : {&L->host_w1, &L->host_w3, &L->host_w2})
+        if ((*v)[e]) EMOE_CUDA(cudaFreeHost((*v)[e]));
+    L->host_owned[e] = 0;
+    L->host_w1[e] = const_cast<void*>(w1);
+    L->host_w3[e] = const_cast<void*>(w3);
+    L->host_w2[e] = const_cast<void*>(w2);
+  });
+}
+
+int emoe_layer_set_copy_stream(emoe_layer* L, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(L, "set_copy_stream: null layer");
+    if (!L->pending_experts.empty()) L->poll(true, L->load_stream(), nullptr);
+    L->ext_copy_stream = static_cast<cudaStream_t>(stream);
   });
 }
 

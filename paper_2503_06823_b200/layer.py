@@ -83,6 +83,22 @@ class MoELayer:
         check(lib.emoe_layer_register_expert_host(self.h, e, C.c_void_p(w1.data_ptr()), w3p,
                                                   C.c_void_p(w2.data_ptr())))
 
+    def register_expert_pinned(self, e: int, w1: torch.Tensor, w3: Optional[torch.Tensor], w2: torch.Tensor) -> None:
+        """Use caller-owned pinned host tensors for expert e (no copy; kept alive here)."""
+        for t in (w1, w2) + ((w3,) if w3 is not None else ()):
+            assert t.device.type == "cpu" and t.is_pinned() and t.is_contiguous() and t.dtype == self.torch_dtype
+        if not hasattr(self, "_pinned_refs"):
+            self._pinned_refs = {}
+        self._pinned_refs[e] = (w1, w3, w2)
+        check(lib.emoe_layer_register_expert_pinned(self.h, e, C.c_void_p(w1.data_ptr()),
+                                                    None if w3 is None else C.c_void_p(w3.data_ptr()),
+                                                    C.c_void_p(w2.data_ptr())))
+
+    def set_copy_stream(self, stream: Optional[torch.cuda.Stream]) -> None:
+        """Share one copy stream across layers so loads run layer-sequentially (engine.cpp:431-440)."""
+        self._copy_stream = stream
+        check(lib.emoe_layer_set_copy_stream(self.h, None if stream is None else C.c_void_p(stream.cuda_stream)))
+
     def set_scores(self, scores: Optional[Sequence[float]]) -> None:
         if scores is None or len(scores) == 0:
             check(lib.emoe_layer_set_scores_host(self.h, None))

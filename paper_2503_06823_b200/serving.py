@@ -1,0 +1,192 @@
+"""The eMoE serving loop on the GPU: a stack of MoE layers under predicted
+residency, periodic predictor invocations, task-aware skipping and expert
+loads on a side stream overlapped with compute.
+
+It restates the reference engine's predictor/load path with the real kernels
+in place of the cost model (SURVEY.md §8a A7/A8, §8f "DES caller"):
+  * invocation gating: the predictor fires when a prompt's arrival index is a
+    multiple of the period p (engine.cpp:320-323);
+  * invocation: predict from the previous prompt's per-layer expert sets,
+    modulate by each task's fitted frequencies, Eq. 2 over the running and
+    queued requests, loading_targets, plan_loading (engine.cpp:367-446) --
+    one GPU call, emoe_invocation_host;
+  * task-aware skip: when every request in the window belongs to a task that
+    is insensitive on every layer, Eq. 2 is all zeros and loading_targets keeps
+    the current residents (expert_store.cpp:140-157); the loop skips the
+    invocation outright and counts it;
+  * load schedule: per layer, evictions take effect at load start and loads at
+    completion (engine.cpp:448-464); all layers share one copy stream, so
+    layer l+1's copies start after layer l's (engine.cpp:431-440).  Compute
+    never waits: each layer's forward polls its loads without blocking.
+Routing follows the reference Markov trace (gate logits embedded from it,
+the routing-driven mode of emoe_moe_forward).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Sequence
+
+import numpy as np
+import torch
+
+from . import moesim
+from ._lib import lib
+from .layer import MoELayer
+from .moesim import _p, _sets_array, check
+
+
+@dataclass
+class TaskSpec:
+    wo: float                 # expected output tokens (TaskProfile::wo)
+    sensitivity: List[int]    # per layer, 1 = routing accuracy matters
+
+
+@dataclass
+class StreamConfig:
+    m: int = 32
+    E: int = 8
+    k: int = 2
+    L: int = 4
+    d: int = 4096
+    f: int = 14336
+    activation: str = "swiglu"
+    tokens_per_prompt: int = 8192
+    period: int = 40
+    mode: int = 0             # 0 = emoe_a (all layers), 1 = emoe_l (chained)
+    task_aware: bool = True
+    tasks: Dict[str, TaskSpec] = field(default_factory=dict)
+    per_expert_seconds: float = 0.0
+
+
+class MoEStack:
+    """m MoE layers sharing pinned host experts, one copy stream and one predictor."""
+
+    def __init__(self, cfg: StreamConfig, host_experts: Sequence, gate_weights: Sequence[torch.Tensor]):
+        self.cfg = cfg
+        self.names = sorted(cfg.tasks)
+        self.copy_stream = torch.cuda.Stream()
+        self.layers: List[MoELayer] = []
+        for l in range(cfg.m):
+            layer = MoELayer(cfg.d, cfg.f, cfg.E, cfg.k, activation=cfg.activation, num_slots=cfg.L,
+                             max_tokens=cfg.tokens_per_prompt)
+            layer.set_gate(gate_weights[l])
+            layer.set_copy_stream(self.copy_stream)
+            for e, (w1, w3, w2) in enumerate(host_experts):
+                layer.register_expert_pinned(e, w1, w3, w2)
+            self.layers.append(layer)
+        self.pred = moesim._Pred(cfg.m, cfg.E, cfg.k, len(self.names), 0.01)
+
+    def close(self):
+        for layer in self.layers:
+            layer.close()
+
+    # -- predictor --------------------------------------------------------------
+    def fit(self, trace_dev: torch.Tensor, task_ids: Sequence[str]) -> None:
+        """A6 over the training prompts (the engine fits once at setup, engine.cpp:249-258)."""
+        P, m, T, k = trace_dev.shape
+        tid = torch.tensor([self.names.index(t) for t in task_ids], dtype=torch.int32, device=trace_dev.device)
+        check(lib.emoe_hist_update(self.pred.h, C.c_void_p(trace_dev.data_ptr()), P, T, C.c_void_p(tid.data_ptr()),
+                                   None))
+
+    def invocation(self, prev_sets, requests: Sequence[tuple]):
+        """engine invocation on the GPU -> per-layer (evictions, loads), aggregate, delta_e."""
+        cfg = self.cfg
+        m, E = cfg.m, cfg.E
+        arr, sizes = _sets_array(prev_sets if cfg.mode == 0 else prev_sets[:1], cfg.k)
+        wo = np.array([cfg.tasks[n].wo for n in self.names], np.float64)
+        sens = np.array([cfg.tasks[n].sensitivity for n in self.names], np.int32).reshape(-1)
+        has = np.ones(len(self.names), np.uint8)
+        rt = np.array([self.names.index(t) for t, _ in requests], np.int32)
+        rn = np.array([n for _, n in requests], np.int32)
+        res = np.stack([layer.residency() for layer in self.layers]).astype(np.uint8)
+        budgets = np.full(m, cfg.L, np.int32)
+        agg = np.zeros((m, E))
+        ev = np.full((m, E), -1, np.int32)
+        ld = np.full((m, E), -1, np.int32)
+        ne = np.zeros(m, np.int32)
+        nl = np.zeros(m, np.int32)
+        de = np.zeros(1)
+        check(lib.emoe_invocation_host(self.pred.h, cfg.mode, _p(arr), _p(sizes), len(self.names), _p(wo), _p(sens),
+                                       _p(has), len(rt), _p(rt), _p(rn), int(cfg.task_aware), _p(res), _p(budgets),
+                                       cfg.per_expert_seconds, _p(agg), _p(ev), _p(ne), _p(ld), _p(nl), _p(de)))
+        ops = [([int(e) for e in ev[l, : ne[l]]], [int(e) for e in ld[l, : nl[l]]]) for l in range(m)]
+        return ops, agg, float(de[0])
+
+    def apply(self, ops, stream=None) -> int:
+        """Start the plan: per layer, evictions now, loads on the shared copy stream."""
+        n = 0
+        for layer, (evictions, loads) in zip(self.layers, ops):
+            if evictions or loads:
+                layer.begin_load(evictions, loads, stream)
+                n += len(loads)
+        return n
+
+    def forward_prompt(self, x: torch.Tensor, logits: torch.Tensor, out: torch.Tensor, hits: torch.Tensor) -> None:
+        """One prompt through every layer; routing-driven logits [m][T][E]."""
+        for l, layer in enumerate(self.layers):
+            layer.forward(x, logits=logits[l], out=out)
+            hits[l] += layer.workspace()["route_hit"].sum()
+
+
+def run_stream(stack: MoEStack, trace: np.ndarray, trace_dev: torch.Tensor, prompt_tasks: Sequence[str],
+               x: torch.Tensor, logits_of, first_prompt: int, n_prompts: int) -> dict:
+    """Serve prompts first_prompt .. first_prompt+n_prompts-1 of the trace.
+    logits_of(p) -> [m][T][E] fp32 device logits for prompt p."""
+    cfg = stack.cfg
+    T = cfg.tokens_per_prompt
+    sensitive = {n: any(cfg.tasks[n].sensitivity) for n in stack.names}
+    out = torch.empty_like(x)
+    hits = torch.zeros(cfg.m, dtype=torch.int64, device=x.device)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = dict(invocations=0, skipped_invocations=0, planned_loads=0, invocation_host_ms=0.0, fired_at=[],
+                 skipped_at=[])
+    load_events = []
+    torch.cuda.synchronize()
+    ev0.record()
+    for i in range(n_prompts):
+        p = first_prompt + i
+        if i % cfg.period == 0:  # predictor fires on this arrival (engine.cpp:320-323)
+            window = list(range(p, min(p + cfg.period, first_prompt + n_prompts)))
+            requests = [(prompt_tasks[q], T) for q in window]
+            if cfg.task_aware and not any(sensitive[t] for t, _ in requests):
+                stats["skipped_invocations"] += 1
+                stats["skipped_at"].append(i)
+            else:
+                t0 = time.perf_counter()
+                _, prev_sets = moesim_prompt_sets(trace_dev, p - 1)
+                ops, _, _ = stack.invocation(prev_sets, requests)
+                ls, le = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ls.record(stack.copy_stream)
+                stats["planned_loads"] += stack.apply(ops)
+                le.record(stack.copy_stream)
+                load_events.append((ls, le))
+                stats["invocation_host_ms"] += (time.perf_counter() - t0) * 1e3
+                stats["invocations"] += 1
+                stats["fired_at"].append(i)
+        stack.forward_prompt(x, logits_of(p), out, hits)
+    ev1.record()
+    torch.cuda.synchronize()
+    for layer in stack.layers:
+        layer.poll_loads(blocking=True)
+    ms = ev0.elapsed_time(ev1)
+    load_ms = sum(a.elapsed_time(b) for a, b in load_events)
+    expert_bytes = (3 if cfg.activation == "swiglu" else 2) * cfg.d * cfg.f * 2
+    load_bytes = stats["planned_loads"] * expert_bytes
+    stats.update(ms=ms, tokens=n_prompts * T, tokens_per_s=n_prompts * T / (ms / 1e3),
+                 hit_rate=float(hits.sum().item()) / (n_prompts * T * cfg.m), load_ms=load_ms, load_bytes=load_bytes,
+                 load_gbs=load_bytes / max(load_ms, 1e-9) / 1e6,
+                 load_overlap="compute never waits on loads: each layer polls its batch without blocking")
+    return stats
+
+
+def moesim_prompt_sets(trace_dev: torch.Tensor, prompt: int):
+    """dominant experts and prompt_expert_sets of one prompt of a device trace."""
+    P, m, T, k = trace_dev.shape
+    dom = np.zeros(m, np.int32)
+    sets = np.full((m, k), -1, np.int32)
+    sizes = np.zeros(m, np.int32)
+    check(lib.emoe_prompt_expert_sets(C.c_void_p(trace_dev.data_ptr()), P, m, T, k, prompt, _p(dom), _p(sets),
+                                      _p(sizes), None))
+    return dom.tolist(), [[int(e) for e in sets[l, : sizes[l]]] for l in range(m)]

@@ -1,0 +1,62 @@
+"""The serving loop on the GPU (predictor every p prompts, task-aware skip,
+layer-sequential side-stream loads) against the oracle's restatement of the
+engine's invocation chain (engine.cpp:320-323, 367-464)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def test_stream_invocations_and_residency_match_oracle(port, ref):
+    from helpers import trace_logits
+    from paper_2503_06823_b200.serving import MoEStack, StreamConfig, TaskSpec, run_stream
+
+    m, E, k, L, d, f, T, p = 4, 8, 2, 4, 256, 512, 256, 4
+    tasks = {"cls": TaskSpec(8.0, [0] * m), "conv": TaskSpec(32.0, [1] * m)}
+    cfg = StreamConfig(m=m, E=E, k=k, L=L, d=d, f=f, tokens_per_prompt=T, period=p, mode=0, tasks=tasks)
+    P_train, P_serve = 30, 16
+    trace = ref.gen_routing_trace(m, E, k, 0.6, 0.8, 0, 17, P_train + P_serve, T)
+    train_tasks = ["conv" if q % 3 else "cls" for q in range(P_train)]
+    serve_tasks = ["conv", "cls", "conv", "conv", "cls", "cls", "cls", "cls",
+                   "cls", "conv", "cls", "cls", "conv", "conv", "conv", "cls"]
+    prompt_tasks = train_tasks + serve_tasks
+    g = torch.Generator().manual_seed(3)
+    host = [tuple((torch.randn(*s, generator=g) / s[1] ** 0.5).to(torch.bfloat16).pin_memory()
+                  for s in ((f, d), (f, d), (d, f))) for _ in range(E)]
+    gates = [(torch.randn(E, d, generator=g) / d ** 0.5).to(torch.bfloat16) for _ in range(m)]
+    stack = MoEStack(cfg, host, gates)
+    trace_dev = torch.from_numpy(trace).cuda()
+    stack.fit(trace_dev[:P_train].contiguous(), train_tasks)
+    for layer in stack.layers:
+        layer.load_initial(range(L))
+    logits = {q: torch.from_numpy(np.stack([trace_logits(trace[q, l], E, seed=q * 31 + l) for l in range(m)])).cuda()
+              for q in range(P_train, P_train + P_serve)}
+    x = torch.randn(T, d, generator=g).to(torch.bfloat16).cuda()
+    st = run_stream(stack, trace, trace_dev, prompt_tasks, x, lambda q: logits[q], P_train, P_serve)
+    assert st["fired_at"] == [0, 8, 12] and st["skipped_at"] == [4], st
+
+    # oracle replay of the engine's invocation chain
+    names = sorted(tasks)
+    model = port.fit(trace[:P_train], np.array([names.index(t) for t in train_tasks], np.int32), len(names), E)
+    model["smoothing"] = 0.01
+    fitted = np.stack([port.predicted_frequencies(model["task_counts"], 0.01, i) for i in range(len(names))])
+    resident = np.zeros((m, E), np.uint8)
+    resident[:, :L] = 1
+    wo = np.array([tasks[n].wo for n in names])
+    sens = np.array([tasks[n].sensitivity for n in names], np.int32)
+    for i in st["fired_at"]:
+        q = P_train + i
+        sets, sizes = port.prompt_expert_sets(trace, q - 1)
+        scores, _, _ = port.predict(model, 0, sets, sizes, k=k)
+        window = list(range(q, min(q + p, P_train + P_serve)))
+        agg = port.invocation_aggregate(scores, fitted, wo, sens, np.ones(2, np.uint8),
+                                        [names.index(prompt_tasks[w]) for w in window], [T] * len(window), True)
+        targets = port.loading_targets(agg, resident, [L] * m)
+        resident = np.zeros((m, E), np.uint8)
+        for l in range(m):
+            resident[l, targets[l]] = 1
+    got = np.stack([layer.residency() for layer in stack.layers])
+    assert np.array_equal(got, resident)
+    assert st["planned_loads"] > 0 and 0.0 < st["hit_rate"] <= 1.0
+    stack.close()
