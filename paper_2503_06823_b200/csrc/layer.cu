@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <array>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -275,7 +276,11 @@ struct emoe_layer {
       EMOE_CUDA(cudaStreamCreateWithFlags(&in_stream, cudaStreamNonBlocking));
       EMOE_CUDA(cudaStreamCreateWithFlags(&out_stream, cudaStreamNonBlocking));
     }
-    int64_t chunk = std::max<int64_t>(8192, ceil_div(T, 8));
+    static const int n_chunks = [] {  // EMOE_H2D_CHUNKS overrides for tuning
+      const char* v = getenv("EMOE_H2D_CHUNKS");
+      return v ? std::max(1, atoi(v)) : 16;
+    }();
+    int64_t chunk = std::max<int64_t>(4096, ceil_div(T, n_chunks));
     chunk = ceil_div(chunk, kRouteBlockTokens) * kRouteBlockTokens;
     const int n = (int)std::max<int64_t>(1, ceil_div(T, chunk));
     while ((int)chunk_ev.size() < 2 * n + 2) {
