@@ -278,9 +278,9 @@ struct emoe_layer {
     }
     static const int n_chunks = [] {  // EMOE_H2D_CHUNKS overrides for tuning
       const char* v = getenv("EMOE_H2D_CHUNKS");
-      return v ? std::max(1, atoi(v)) : 16;
+      return v ? std::max(1, atoi(v)) : 8;  // 8 measured better than 16 (profiles/r01_summary.md)
     }();
-    int64_t chunk = std::max<int64_t>(4096, ceil_div(T, n_chunks));
+    int64_t chunk = std::max<int64_t>(8192, ceil_div(T, n_chunks));
     chunk = ceil_div(chunk, kRouteBlockTokens) * kRouteBlockTokens;
     const int n = (int)std::max<int64_t>(1, ceil_div(T, chunk));
     while ((int)chunk_ev.size() < 2 * n + 2) {
