@@ -131,8 +131,15 @@ int emoe_layer_last_load_stats(const emoe_layer* layer, double* bytes, double* m
  * ====================================================================== */
 int emoe_moe_forward(emoe_layer* layer, const void* x_dev, const float* logits_in_dev, void* y_dev, int64_t T,
                      void* stream);
-/* Same through host buffers: H2D of x, forward, D2H of y; returns after y is on the host. */
+/* Same through host buffers: H2D of x, forward, D2H of y; returns after y is on the host.
+ * Copies and compute are pipelined in token chunks (pinned buffers overlap). */
 int emoe_moe_forward_host(emoe_layer* layer, const void* x_host, void* y_host, int64_t T, void* stream);
+/* Asynchronous form for serving loops: enqueues H2D, forward and D2H and
+ * returns; consecutive calls alternate two device staging sets, so call i+1's
+ * H2D overlaps call i's compute and D2H.  x_host must stay unchanged and y_host
+ * unread until emoe_layer_wait_host() returns (it waits for every call made). */
+int emoe_moe_forward_host_async(emoe_layer* layer, const void* x_host, void* y_host, int64_t T, void* stream);
+int emoe_layer_wait_host(emoe_layer* layer);
 
 /* Route only (A1 + A2): fills the workspace routing fields. */
 int emoe_route(emoe_layer* layer, const void* x_dev, const float* logits_in_dev, int64_t T, void* stream);

@@ -264,17 +264,35 @@ struct emoe_layer {
   // of chunk i on the compute stream.  Per-token results do not depend on the
   // chunking (every row's GEMM reduction order is fixed), so the output is
   // bit-identical to a single forward over all T tokens.
+  // Two device staging sets: call i+1's H2D (into set b^1) overlaps call i's
+  // compute and D2H (set b).  Reuse of a set waits on events: H2D into x[b]
+  // after the compute that last read x[b]; compute into y[b] after the D2H
+  // that last read y[b].
   cudaStream_t in_stream = nullptr, out_stream = nullptr;
-  std::vector<cudaEvent_t> chunk_ev;
+  void* x_stage[2] = {nullptr, nullptr};
+  void* y_stage[2] = {nullptr, nullptr};
+  cudaEvent_t x_free[2] = {}, y_free[2] = {}, host_done = nullptr;
+  std::vector<cudaEvent_t> chunk_ev[2];
+  int stage_next = 0;
 
-  void forward_host(const void* x_host, void* y_host, int64_t T, cudaStream_t s) {
+  void forward_host_async(const void* x_host, void* y_host, int64_t T, cudaStream_t s) {
     EMOE_REQUIRE(T >= 0 && T <= cfg.max_tokens, "moe_forward: T exceeds the layer's max_tokens");
     const size_t row = (size_t)cfg.d_model * elem;
-    if (!x_in) {
-      x_in = dmalloc<uint8_t>((size_t)cfg.max_tokens * row);
-      y_out = dmalloc<uint8_t>((size_t)cfg.max_tokens * row);
+    if (!x_stage[0]) {
+      for (int b = 0; b < 2; ++b) {
+        x_stage[b] = dmalloc<uint8_t>((size_t)cfg.max_tokens * row);
+        y_stage[b] = dmalloc<uint8_t>((size_t)cfg.max_tokens * row);
+        EMOE_CUDA(cudaEventCreateWithFlags(&x_free[b], cudaEventDisableTiming));
+        EMOE_CUDA(cudaEventCreateWithFlags(&y_free[b], cudaEventDisableTiming));
+      }
+      EMOE_CUDA(cudaEventCreateWithFlags(&host_done, cudaEventDisableTiming));
       EMOE_CUDA(cudaStreamCreateWithFlags(&in_stream, cudaStreamNonBlocking));
       EMOE_CUDA(cudaStreamCreateWithFlags(&out_stream, cudaStreamNonBlocking));
+      // staging sets start free (events recorded once, complete immediately)
+      for (int b = 0; b < 2; ++b) {
+        EMOE_CUDA(cudaEventRecord(x_free[b], s));
+        EMOE_CUDA(cudaEventRecord(y_free[b], s));
+      }
     }
     static const int n_chunks = [] {  // EMOE_H2D_CHUNKS overrides for tuning
       const char* v = getenv("EMOE_H2D_CHUNKS");
@@ -283,31 +301,42 @@ struct emoe_layer {
     int64_t chunk = std::max<int64_t>(8192, ceil_div(T, n_chunks));
     chunk = ceil_div(chunk, kRouteBlockTokens) * kRouteBlockTokens;
     const int n = (int)std::max<int64_t>(1, ceil_div(T, chunk));
-    while ((int)chunk_ev.size() < 2 * n + 2) {
+    const int b = stage_next;
+    stage_next ^= 1;
+    auto& ev = chunk_ev[b];
+    while ((int)ev.size() < 2 * n) {
       cudaEvent_t e;
       EMOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      chunk_ev.push_back(e);
+      ev.push_back(e);
     }
-    // earlier work on `s` may still read x_in / write y_out
-    EMOE_CUDA(cudaEventRecord(chunk_ev[2 * n], s));
-    EMOE_CUDA(cudaStreamWaitEvent(in_stream, chunk_ev[2 * n], 0));
+    EMOE_CUDA(cudaStreamWaitEvent(in_stream, x_free[b], 0));
+    EMOE_CUDA(cudaStreamWaitEvent(s, y_free[b], 0));
     for (int i = 0; i < n; ++i) {
       const int64_t t0 = i * chunk, tn = std::min<int64_t>(chunk, T - t0);
-      uint8_t* xd = static_cast<uint8_t*>(x_in) + t0 * row;
-      uint8_t* yd = static_cast<uint8_t*>(y_out) + t0 * row;
+      uint8_t* xd = static_cast<uint8_t*>(x_stage[b]) + t0 * row;
+      uint8_t* yd = static_cast<uint8_t*>(y_stage[b]) + t0 * row;
       EMOE_CUDA(cudaMemcpyAsync(xd, static_cast<const uint8_t*>(x_host) + t0 * row, tn * row,
                                 cudaMemcpyHostToDevice, in_stream));
-      EMOE_CUDA(cudaEventRecord(chunk_ev[2 * i], in_stream));
-      EMOE_CUDA(cudaStreamWaitEvent(s, chunk_ev[2 * i], 0));
+      EMOE_CUDA(cudaEventRecord(ev[2 * i], in_stream));
+      EMOE_CUDA(cudaStreamWaitEvent(s, ev[2 * i], 0));
       forward(xd, nullptr, yd, tn, s);
-      EMOE_CUDA(cudaEventRecord(chunk_ev[2 * i + 1], s));
-      EMOE_CUDA(cudaStreamWaitEvent(out_stream, chunk_ev[2 * i + 1], 0));
+      EMOE_CUDA(cudaEventRecord(ev[2 * i + 1], s));
+      EMOE_CUDA(cudaStreamWaitEvent(out_stream, ev[2 * i + 1], 0));
       EMOE_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(y_host) + t0 * row, yd, tn * row, cudaMemcpyDeviceToHost,
                                 out_stream));
     }
-    EMOE_CUDA(cudaEventRecord(chunk_ev[2 * n + 1], out_stream));
-    EMOE_CUDA(cudaStreamWaitEvent(s, chunk_ev[2 * n + 1], 0));
-    EMOE_CUDA(cudaStreamSynchronize(s));
+    EMOE_CUDA(cudaEventRecord(x_free[b], s));
+    EMOE_CUDA(cudaEventRecord(y_free[b], out_stream));
+    EMOE_CUDA(cudaEventRecord(host_done, out_stream));
+  }
+
+  void wait_host() {
+    if (host_done) EMOE_CUDA(cudaEventSynchronize(host_done));
+  }
+
+  void forward_host(const void* x_host, void* y_host, int64_t T, cudaStream_t s) {
+    forward_host_async(x_host, y_host, T, s);
+    wait_host();
   }
 
   void begin_load(const int32_t* ev, int nev, const int32_t* ld, int nld, cudaStream_t s) {
@@ -382,7 +411,8 @@ struct emoe_layer {
                     (void*)route_resident_dev,
                     (void*)logits, (void*)topk, (void*)r_expert, (void*)r_rank, (void*)r_hit, (void*)served_idx,
                     (void*)served_w, (void*)block_counts, (void*)counts, (void*)seg_offsets, (void*)block_base,
-                    (void*)pos, (void*)row_token, x_perm, h, y_perm, x_in, y_out, (void*)err_flag})
+                    (void*)pos, (void*)row_token, x_perm, h, y_perm, x_in, y_out, (void*)err_flag, x_stage[0],
+                    x_stage[1], y_stage[0], y_stage[1]})
       f(p);
     for (auto* v : {&host_w1, &host_w3, &host_w2})
       for (size_t e = 0; e < v->size(); ++e)
@@ -390,7 +420,10 @@ struct emoe_layer {
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (in_stream) cudaStreamDestroy(in_stream);
     if (out_stream) cudaStreamDestroy(out_stream);
-    for (cudaEvent_t e : chunk_ev) cudaEventDestroy(e);
+    for (auto& v : chunk_ev)
+      for (cudaEvent_t e : v) cudaEventDestroy(e);
+    for (cudaEvent_t e : {x_free[0], x_free[1], y_free[0], y_free[1], host_done})
+      if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {ev_evict, ev_load_start, ev_load_done})
       if (e) cudaEventDestroy(e);
     for (auto& set : ev_pool)
@@ -611,6 +644,20 @@ int emoe_moe_forward_host(emoe_layer* L, const void* x_host, void* y_host, int64
     EMOE_REQUIRE(L && x_host && y_host, "moe_forward_host: null argument");
     EMOE_REQUIRE(T >= 0 && T <= L->cfg.max_tokens, "moe_forward: T exceeds the layer's max_tokens");
     L->forward_host(x_host, y_host, T, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int emoe_moe_forward_host_async(emoe_layer* L, const void* x_host, void* y_host, int64_t T, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(L && x_host && y_host, "moe_forward_host_async: null argument");
+    L->forward_host_async(x_host, y_host, T, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int emoe_layer_wait_host(emoe_layer* L) {
+  return guard([&] {
+    EMOE_REQUIRE(L, "wait_host: null layer");
+    L->wait_host();
   });
 }
 

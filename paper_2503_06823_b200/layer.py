@@ -160,6 +160,15 @@ class MoELayer:
                                         x_host.shape[0], _stream_ptr(stream)))
         return y_host
 
+    def forward_host_async(self, x_host: torch.Tensor, y_host: torch.Tensor, stream=None) -> None:
+        """Enqueue H2D + forward + D2H and return; call wait_host() before reading y_host."""
+        assert x_host.device.type == "cpu" and x_host.dtype == self.torch_dtype and x_host.is_contiguous()
+        check(lib.emoe_moe_forward_host_async(self.h, C.c_void_p(x_host.data_ptr()), C.c_void_p(y_host.data_ptr()),
+                                              x_host.shape[0], _stream_ptr(stream)))
+
+    def wait_host(self) -> None:
+        check(lib.emoe_layer_wait_host(self.h))
+
     def route(self, x: Optional[torch.Tensor] = None, logits: Optional[torch.Tensor] = None, stream=None) -> None:
         T = x.shape[0] if x is not None else logits.shape[0]
         check(lib.emoe_route(self.h, C.c_void_p(x.data_ptr()) if x is not None else None,

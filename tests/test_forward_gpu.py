@@ -218,3 +218,22 @@ def test_two_phase_residency_and_loads():
     served = layer.workspace()["served_idx"].cpu().numpy()
     assert set(np.unique(served[served >= 0]).tolist()) <= {0, 3, 6, 7}
     layer.close()
+
+
+@pytest.mark.gpu
+def test_forward_host_async_pipelined_calls():
+    """Back-to-back async host calls (alternating staging sets) give each call
+    the same bits as a device forward of its own input."""
+    from helpers import build_layer
+
+    T = 9000
+    layer, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", 4, [1, 2, 5, 6], max_tokens=T)
+    xs = [torch.randn(T, 256, generator=torch.Generator().manual_seed(40 + i)).to(torch.bfloat16).pin_memory()
+          for i in range(3)]
+    ys = [torch.empty_like(x).pin_memory() for x in xs]
+    for x, y in zip(xs, ys):
+        layer.forward_host_async(x, y)
+    layer.wait_host()
+    for x, y in zip(xs, ys):
+        assert torch.equal(layer.forward(x.cuda()).cpu(), y)
+    layer.close()
