@@ -332,6 +332,9 @@ class Ref:
                                        C.POINTER(C.c_double), C.POINTER(C.c_int32)]
         L.ref_gen_routing_trace.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
                                             C.c_uint64, C.c_int, C.c_int, _i32p]
+        L.ref_save_trace.argtypes = [_i32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p]
+        L.ref_fit_and_save_model.argtypes = [_i32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                             C.c_double, C.c_int, C.c_char_p]
         L.ref_rng_uniform.argtypes = [C.c_uint64, C.c_int64, _f64p]
         L.ref_rng_normal.argtypes = [C.c_uint64, C.c_int64, _f64p]
 
@@ -474,6 +477,20 @@ class Ref:
         self._chk(self.lib.ref_gen_routing_trace(m, E, k, layer_lambda, prompt_lambda, initial_expert, seed, P, T,
                                                  out))
         return out
+
+    def save_trace(self, trace, path):
+        trace = _a(trace, np.int32)
+        P, m, T, k = trace.shape
+        self._chk(self.lib.ref_save_trace(trace, P, m, T, k, str(path).encode()))
+
+    def fit_and_save_model(self, trace, task_ids, task_names, smoothing, num_experts, path):
+        trace = _a(trace, np.int32)
+        P, m, T, k = trace.shape
+        names = _names(task_names)
+        tid = None if task_ids is None else _a(task_ids, np.int32)
+        self._chk(self.lib.ref_fit_and_save_model(trace, P, m, T, k, None if tid is None else tid.ctypes.data,
+                                                  C.cast(names, C.c_void_p), smoothing, num_experts,
+                                                  str(path).encode()))
 
     def rng_uniform(self, seed, n):
         out = np.empty(n, np.float64)

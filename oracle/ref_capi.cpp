@@ -21,6 +21,7 @@
 #include "moesim/engine.hpp"
 #include "moesim/expert_store.hpp"
 #include "moesim/predictor.hpp"
+#include "moesim/report.hpp"
 #include "moesim/workload.hpp"
 
 using namespace moesim;
@@ -393,6 +394,22 @@ int ref_gen_routing_trace(int m, int E, int k, double layer_lambda, double promp
         for (int t2 = 0; t2 < T; ++t2)
           for (int r = 0; r < k; ++r)
             out[((static_cast<int64_t>(p) * m + l) * T + t2) * k + r] = t.experts[p][l][t2][r];
+  });
+}
+
+// save_trace (report.cpp:260-267) / save_model (predictor.cpp:240-252) of a
+// flat trace / fitted model, for byte-compatibility checks of the formats
+int ref_save_trace(const int32_t* trace, int P, int m, int T, int k, const char* path) {
+  return guard([&] { save_trace(make_trace(trace, P, m, T, k), path); });
+}
+int ref_fit_and_save_model(const int32_t* trace, int P, int m, int T, int k, const int32_t* task_ids,
+                           const char* const* task_names, double smoothing, int num_experts, const char* path) {
+  return guard([&] {
+    RoutingTrace t = make_trace(trace, P, m, T, k);
+    std::vector<std::string> ids;
+    if (task_ids)
+      for (int p = 0; p < P; ++p) ids.push_back(task_names[task_ids[p]]);
+    save_model(fit(t, ids, smoothing, num_experts), path);
   });
 }
 
