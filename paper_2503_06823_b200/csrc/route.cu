@@ -177,6 +177,130 @@ __device__ void route_one_token(const float* lg, int64_t t, const RouteArgs& a, 
   route_tail(ti, lg, t, a, o, st);
 }
 
+// Warp-cooperative form of route_one_token for many experts (E >= 32, e.g. the
+// Switch-base-128 config): lane L owns experts L, L+32, ...; the top-k, the
+// route_token fallback and the full-softmax denominator are warp reductions.
+// Same decisions as the serial form: top-k = largest logit, smallest index on
+// ties; fallback = largest layer score among residents, smallest index on ties.
+__device__ void route_one_token_warp(const float* lg, int64_t t, const RouteArgs& a, const RouteOut& o,
+                                     SharedRouteState& st) {
+  const int E = a.E, k = a.k, lane = threadIdx.x & 31;
+  constexpr unsigned FULL = 0xffffffffu;
+  int ti[8];
+  uint32_t used = 0;  // bit j: expert lane + 32 j already chosen
+  for (int r = 0; r < k; ++r) {
+    float bv = 0.0f;
+    int bi = -1;
+    for (int j = 0; lane + 32 * j < E; ++j) {
+      if (used & (1u << j)) continue;
+      const float v = lg[lane + 32 * j];
+      if (bi < 0 || v > bv) {
+        bv = v;
+        bi = lane + 32 * j;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ov = __shfl_xor_sync(FULL, bv, off);
+      const int oi = __shfl_xor_sync(FULL, bi, off);
+      if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    ti[r] = bi;
+    if ((bi & 31) == lane) used |= 1u << (bi >> 5);
+    if (lane == 0 && o.topk_idx) o.topk_idx[t * k + r] = bi;
+  }
+  int ex = -1, rk = -1, hit = 0;
+  if (st.n_res == 0) {
+    ex = ti[0];
+    if (!a.forced_miss && lane == 0) atomicExch(a.error_flag, 3);
+  } else {
+    for (int r = 0; r < k; ++r)
+      if (st.resident[ti[r]]) {
+        ex = ti[r];
+        rk = r;
+        hit = r == 0;
+        break;
+      }
+    if (rk < 0) {
+      ex = st.first_res;
+      if (a.scores) {  // warp argmax of scores over residents
+        double bs = 0.0;
+        int be = -1;
+        for (int e = lane; e < E; e += 32)
+          if (st.resident[e] && (be < 0 || st.scores[e] > bs)) {
+            bs = st.scores[e];
+            be = e;
+          }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double os = __shfl_xor_sync(FULL, bs, off);
+          const int oe = __shfl_xor_sync(FULL, be, off);
+          if (oe >= 0 && (be < 0 || os > bs || (os == bs && oe < be))) {
+            bs = os;
+            be = oe;
+          }
+        }
+        ex = be;
+      }
+    }
+  }
+  float den_full = 0.0f;
+  if (a.weight_mode != 0) {
+    const float mx = lg[ti[0]];
+    for (int e = lane; e < E; e += 32) den_full += expf(lg[e] - mx);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) den_full += __shfl_xor_sync(FULL, den_full, off);
+  }
+  if (lane != 0) return;
+  if (o.route_expert) o.route_expert[t] = ex;
+  if (o.route_rank) o.route_rank[t] = rk;
+  if (o.route_hit) o.route_hit[t] = (uint8_t)hit;
+  int si[8];
+  int ns = 0;
+  if (st.n_res > 0) {
+    if (rk >= 0) {
+      for (int r = 0; r < k; ++r)
+        if (st.resident[ti[r]]) si[ns++] = ti[r];
+    } else {
+      si[ns++] = ex;
+    }
+  }
+  float w[8];
+  if (a.weight_mode == 0) {
+    if (ns > 0) {
+      const float mx = lg[si[0]];
+      float den = 0.0f;
+      for (int j = 0; j < ns; ++j) {
+        w[j] = expf(lg[si[j]] - mx);
+        den += w[j];
+      }
+      for (int j = 0; j < ns; ++j) w[j] = w[j] / den;
+    }
+  } else {
+    const float mx = lg[ti[0]];
+    for (int j = 0; j < ns; ++j) w[j] = expf(lg[si[j]] - mx) / den_full;
+  }
+  if (o.served_idx)
+    for (int j = 0; j < k; ++j) {
+      o.served_idx[t * k + j] = j < ns ? si[j] : -1;
+      o.served_w[t * k + j] = j < ns ? w[j] : 0.0f;
+    }
+  for (int j = 0; j < ns; ++j) atomicAdd(&st.counts[si[j]], 1);
+}
+
+// block's logits tile [rows][ld] in shared memory -> global [T][E], coalesced
+__device__ void store_logits_tile(const float* tile, int ld, int64_t t0, const RouteArgs& a, const RouteOut& o) {
+  if (!o.logits) return;
+  const int64_t rows = min((int64_t)RT, a.T - t0);
+  for (int64_t i = threadIdx.x; i < rows * a.E; i += blockDim.x) {
+    const int r = (int)(i / a.E), e = (int)(i % a.E);
+    o.logits[t0 * a.E + i] = tile[r * ld + e];
+  }
+}
+
 __device__ void flush_block_counts(const RouteArgs& a, const RouteOut& o, SharedRouteState& st) {
   __syncthreads();
   if (o.block_counts)
@@ -274,12 +398,16 @@ __global__ void __launch_bounds__(128) gate_route_bf16_kernel(const __nv_bfloat1
       logits[(r + 8) * (EP + 1) + c + 1] = acc[mt][nt][3];
     }
   load_route_state(st, a);  // contains __syncthreads
-  const int64_t t = t0 + tid;
-  if (t < a.T) {
-    const float* lg = logits + tid * (EP + 1);
-    if (o.logits)
-      for (int e = 0; e < a.E; ++e) o.logits[t * a.E + e] = lg[e];
-    route_one_token(lg, t, a, o, st);
+  store_logits_tile(logits, EP + 1, t0, a, o);
+  if (a.E >= 32) {  // warp per token
+    for (int r = warp; r < RT; r += 4) {
+      const int64_t t = t0 + r;
+      if (t >= a.T) break;
+      route_one_token_warp(logits + r * (EP + 1), t, a, o, st);
+    }
+  } else {
+    const int64_t t = t0 + tid;
+    if (t < a.T) route_one_token(logits + tid * (EP + 1), t, a, o, st);
   }
   flush_block_counts(a, o, st);
 }
@@ -308,12 +436,16 @@ __global__ void __launch_bounds__(128) gate_route_f32_kernel(const float* __rest
     }
   }
   load_route_state(st, a);
-  const int64_t t = t0 + threadIdx.x;
-  if (t < a.T) {
-    const float* lg = logits + threadIdx.x * a.E;
-    if (o.logits)
-      for (int e = 0; e < a.E; ++e) o.logits[t * a.E + e] = lg[e];
-    route_one_token(lg, t, a, o, st);
+  store_logits_tile(logits, a.E, t0, a, o);
+  if (a.E >= 32) {
+    for (int r = warp; r < RT; r += 4) {
+      const int64_t t = t0 + r;
+      if (t >= a.T) break;
+      route_one_token_warp(logits + r * a.E, t, a, o, st);
+    }
+  } else {
+    const int64_t t = t0 + threadIdx.x;
+    if (t < a.T) route_one_token(logits + threadIdx.x * a.E, t, a, o, st);
   }
   flush_block_counts(a, o, st);
 }
@@ -325,12 +457,19 @@ __global__ void __launch_bounds__(128) route_from_logits_kernel(const float* __r
                                                                 RouteOut o) {
   __shared__ SharedRouteState st;
   load_route_state(st, a);
-  const int64_t t = (int64_t)blockIdx.x * RT + threadIdx.x;
-  if (t < a.T) {
-    const float* lg = logits + t * a.E;
-    if (o.logits && o.logits != logits)
-      for (int e = 0; e < a.E; ++e) o.logits[t * a.E + e] = lg[e];
-    route_one_token(lg, t, a, o, st);
+  const int64_t t0 = (int64_t)blockIdx.x * RT;
+  if (o.logits && o.logits != logits)
+    for (int64_t i = threadIdx.x; i < min((int64_t)RT, a.T - t0) * a.E; i += blockDim.x)
+      o.logits[t0 * a.E + i] = logits[t0 * a.E + i];
+  if (a.E >= 32) {
+    for (int r = threadIdx.x / 32; r < RT; r += 4) {
+      const int64_t t = t0 + r;
+      if (t >= a.T) break;
+      route_one_token_warp(logits + t * a.E, t, a, o, st);
+    }
+  } else {
+    const int64_t t = t0 + threadIdx.x;
+    if (t < a.T) route_one_token(logits + t * a.E, t, a, o, st);
   }
   flush_block_counts(a, o, st);
 }
