@@ -399,16 +399,10 @@ __global__ void __launch_bounds__(128) gate_route_bf16_kernel(const __nv_bfloat1
     }
   load_route_state(st, a);  // contains __syncthreads
   store_logits_tile(logits, EP + 1, t0, a, o);
-  if (a.E >= 32) {  // warp per token
-    for (int r = warp; r < RT; r += 4) {
-      const int64_t t = t0 + r;
-      if (t >= a.T) break;
-      route_one_token_warp(logits + r * (EP + 1), t, a, o, st);
-    }
-  } else {
-    const int64_t t = t0 + tid;
-    if (t < a.T) route_one_token(logits + tid * (EP + 1), t, a, o, st);
-  }
+  // thread per token: with the logits tile in shared memory even E = 128 costs
+  // only a few microseconds here (the mma.sync gate above is the cost for large E)
+  const int64_t t = t0 + tid;
+  if (t < a.T) route_one_token(logits + tid * (EP + 1), t, a, o, st);
   flush_block_counts(a, o, st);
 }
 
@@ -437,16 +431,8 @@ __global__ void __launch_bounds__(128) gate_route_f32_kernel(const float* __rest
   }
   load_route_state(st, a);
   store_logits_tile(logits, a.E, t0, a, o);
-  if (a.E >= 32) {
-    for (int r = warp; r < RT; r += 4) {
-      const int64_t t = t0 + r;
-      if (t >= a.T) break;
-      route_one_token_warp(logits + r * a.E, t, a, o, st);
-    }
-  } else {
-    const int64_t t = t0 + threadIdx.x;
-    if (t < a.T) route_one_token(logits + threadIdx.x * a.E, t, a, o, st);
-  }
+  const int64_t t = t0 + threadIdx.x;
+  if (t < a.T) route_one_token(logits + threadIdx.x * a.E, t, a, o, st);
   flush_block_counts(a, o, st);
 }
 
