@@ -64,6 +64,10 @@ struct Params {
   const int32_t* seg_expert;  // [segments] expert of each segment, null = segment i is expert i
   int group_m;          // raster group (row blocks)
   __nv_bfloat16* out;
+  float* out_f32;       // EPI_F32 output
+  int64_t row_limit;    // EPI_F32: rows >= row_limit not stored
+  int col_limit;        // EPI_F32: columns >= col_limit not stored (multiple of 32)
+  int64_t single_rows;  // > 0: one segment [0, single_rows) instead of seg_offsets
   int64_t ldo;
 };
 
@@ -153,7 +157,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int cluster_id = blockIdx.x / CG;
   const int num_clusters = gridDim.x / CG;
 
-  for (int i = threadIdx.x; i <= E; i += NUM_THREADS) s_offs[i] = p.seg_offsets[i];
+  for (int i = threadIdx.x; i <= E; i += NUM_THREADS)
+    s_offs[i] = p.single_rows > 0 ? (i == 0 ? 0 : p.single_rows) : p.seg_offsets[i];
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
@@ -320,6 +325,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int v = 0; v < 4; ++v)
             dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
         }
+      } else if (EPI == EPI_F32) {
+        // fp32 accumulators straight out (dense gate GEMM): rows >= row_limit
+        // and columns >= col_limit are not stored
+        float* frow = p.out_f32 + row * p.ldo;
+        const bool row_ok = row < p.row_limit;
+#pragma unroll 1
+        for (int cc = 0; cc < BN; cc += 32) {
+          uint32_t a[32];
+          tmem_ld_32x32b_x32(taddr + cc, a);
+          tmem_ld_wait();
+          if (row_ok && cc < p.col_limit) {
+            uint4* dst = reinterpret_cast<uint4*>(frow + cc);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) dst[v] = make_uint4(a[4 * v], a[4 * v + 1], a[4 * v + 2], a[4 * v + 3]);
+          }
+        }
       } else {
 #pragma unroll 1
         for (int cc = 0; cc < BN; cc += 32) {
@@ -416,6 +437,9 @@ static int group_rows(int K, int tile_m) {
   return g < 2 ? 2 : (g > 64 ? 64 : g);
 }
 
+static void launch_params(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
+                          const CUtensorMap& tb2, const gemm::Params& p, int num_sms, cudaStream_t stream);
+
 void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
@@ -436,9 +460,45 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
   p.group_m = group_rows(K, 128 * cta_group);
   p.out = out;
   p.ldo = ldo;
+  p.out_f32 = nullptr;
+  p.row_limit = 0;
+  p.col_limit = 0;
+  p.single_rows = 0;
+  launch_params(epi, cta_group, ta, tb, tb2, p, num_sms, stream);
+}
+
+__device__ int32_t g_slot_zero = 0;
+
+void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int K, int N_out, float* out,
+                           int64_t ldo, int col_limit, int num_sms, cudaStream_t stream) {
+  EMOE_REQUIRE(K % gemm::BK == 0, "dense_gemm: K must be a multiple of 64");
+  EMOE_REQUIRE(N_out % gemm::BN == 0, "dense_gemm: N must be a multiple of 256");
+  gemm::Params p;
+  void* zero = nullptr;
+  EMOE_CUDA(cudaGetSymbolAddress(&zero, g_slot_zero));
+  p.seg_offsets = nullptr;
+  p.slot_of_expert = static_cast<const int32_t*>(zero);
+  p.seg_expert = nullptr;
+  p.num_experts = 1;
+  p.K = K;
+  p.out_block_cols = gemm::BN;
+  p.n_blocks = N_out / gemm::BN;
+  p.b_rows_per_slot = 0;
+  p.group_m = group_rows(K, 128);
+  p.out = nullptr;
+  p.ldo = ldo;
+  p.out_f32 = out;
+  p.row_limit = M;
+  p.col_limit = col_limit;
+  p.single_rows = ceil_div(M, 128) * 128;
+  launch_params(EPI_F32, 1, ta, tb, tb, p, num_sms, stream);
+}
+
+static void launch_params(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
+                          const CUtensorMap& tb2, const gemm::Params& p, int num_sms, cudaStream_t stream) {
   const int grid = cta_group == 2 ? (num_sms / 2) * 2 : num_sms;
   auto run = [&](auto kernel, int smem, int idx) {
-    static bool attr_set[6] = {false, false, false, false, false, false};
+    static bool attr_set[7] = {false, false, false, false, false, false, false};
     if (!attr_set[idx]) {
       EMOE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr_set[idx] = true;
@@ -470,6 +530,8 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
       run(gemm::grouped_gemm_kernel<EPI_SWIGLU, 1>, C1::SMEM_BYTES, 0);
     else if (epi == EPI_RELU)
       run(gemm::grouped_gemm_kernel<EPI_RELU, 1>, C1::SMEM_BYTES, 1);
+    else if (epi == EPI_F32)
+      run(gemm::grouped_gemm_kernel<EPI_F32, 1>, C1::SMEM_BYTES, 6);
     else
       run(gemm::grouped_gemm_kernel<EPI_STORE, 1>, C1::SMEM_BYTES, 2);
   } else {

@@ -13,7 +13,7 @@ namespace emoe {
 void count_launch(int n = 1);
 long long launch_count();
 
-enum EpiKind { EPI_SWIGLU = 0, EPI_RELU = 1, EPI_STORE = 2 };
+enum EpiKind { EPI_SWIGLU = 0, EPI_RELU = 1, EPI_STORE = 2, EPI_F32 = 3 };
 enum DType { DT_BF16 = 0, DT_F32 = 1 };
 
 constexpr int kRouteBlockTokens = 128;  // tokens per route / permute block
@@ -69,6 +69,11 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
                          int num_sms, cudaStream_t stream, const int32_t* seg_expert = nullptr);
+
+// K1 for many experts: the gate as one dense tcgen05 GEMM with fp32 output,
+// out[M][ldo] = A[M][K] . B[N_out][K]^T, columns >= col_limit (multiple of 32) not stored
+void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int K, int N_out, float* out,
+                           int64_t ldo, int col_limit, int num_sms, cudaStream_t stream);
 
 // K4 fp32 path (SIMT FFMA): same grouping/epilogues, fp32 in/out
 void launch_grouped_gemm_f32(int epi, const float* A, int64_t lda, const float* B, const float* B2,

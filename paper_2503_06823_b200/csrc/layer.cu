@@ -157,6 +157,13 @@ struct emoe_layer {
     finish_pending(s);
   }
 
+  // Gate on tcgen05 for E in {32, 64, 96, 128} (bf16): W_g zero-padded to 256 rows.
+  void* wg_pad = nullptr;
+  CUtensorMap t_gate{};
+  bool tc_gate() const {
+    return cfg.dtype == EMOE_DTYPE_BF16 && cfg.num_experts >= 32 && cfg.num_experts % 32 == 0 && wg_pad;
+  }
+
   // Expert parallelism: routing sees the GLOBAL resident set (the reference
   // Placement) while this GPU's slots hold only the experts it serves.
   bool route_override = false;
@@ -182,10 +189,17 @@ struct emoe_layer {
     a.scores = have_scores ? scores_dev : nullptr;
     a.error_flag = err_flag;
     RouteOut o{logits, topk, r_expert, r_rank, r_hit, served_idx, served_w, block_counts};
-    if (logits_in)
+    if (logits_in) {
       launch_route_from_logits(logits_in, a, o, s);
-    else
+    } else if (tc_gate()) {
+      // many experts: the gate is a real GEMM (T x d x E); run it on tcgen05
+      // into the fp32 logits buffer, then route from the logits
+      const CUtensorMap tx = make_tmap_bf16_2d(x, (uint64_t)T, cfg.d_model, 128);
+      launch_dense_gemm_f32(tx, t_gate, T, cfg.d_model, 256, logits, cfg.num_experts, cfg.num_experts, num_sms, s);
+      launch_route_from_logits(logits, a, o, s);
+    } else {
       launch_gate_route(x, wg, cfg.dtype, a, o, s);
+    }
     last_T = T;
   }
 
@@ -408,7 +422,7 @@ struct emoe_layer {
       if (p) cudaFree(p);
     };
     for (void* p : {(void*)wg, w1_pool, w3_pool, w2_pool, (void*)slot_dev, (void*)resident_dev, (void*)scores_dev,
-                    (void*)route_resident_dev,
+                    (void*)route_resident_dev, wg_pad,
                     (void*)logits, (void*)topk, (void*)r_expert, (void*)r_rank, (void*)r_hit, (void*)served_idx,
                     (void*)served_w, (void*)block_counts, (void*)counts, (void*)seg_offsets, (void*)block_base,
                     (void*)pos, (void*)row_token, x_perm, h, y_perm, x_in, y_out, (void*)err_flag, x_stage[0],
@@ -542,7 +556,17 @@ int emoe_layer_destroy(emoe_layer* layer) {
 int emoe_layer_set_gate_host(emoe_layer* L, const void* wg) {
   return guard([&] {
     EMOE_REQUIRE(L && wg, "set_gate: null argument");
-    EMOE_CUDA(cudaMemcpy(L->wg, wg, (size_t)L->cfg.num_experts * L->cfg.d_model * L->elem, cudaMemcpyHostToDevice));
+    const size_t bytes = (size_t)L->cfg.num_experts * L->cfg.d_model * L->elem;
+    EMOE_CUDA(cudaMemcpy(L->wg, wg, bytes, cudaMemcpyHostToDevice));
+    const int E = L->cfg.num_experts;
+    if (L->cfg.dtype == EMOE_DTYPE_BF16 && E >= 32 && E % 32 == 0 && E <= 256) {
+      if (!L->wg_pad) {
+        L->wg_pad = dmalloc<uint8_t>((size_t)256 * L->cfg.d_model * 2);
+        EMOE_CUDA(cudaMemset(L->wg_pad, 0, (size_t)256 * L->cfg.d_model * 2));
+        L->t_gate = make_tmap_bf16_2d(L->wg_pad, 256, L->cfg.d_model, 256);
+      }
+      EMOE_CUDA(cudaMemcpy(L->wg_pad, wg, bytes, cudaMemcpyHostToDevice));
+    }
   });
 }
 
