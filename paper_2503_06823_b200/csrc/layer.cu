@@ -310,7 +310,8 @@ struct emoe_layer {
     }
     static const int n_chunks = [] {  // EMOE_H2D_CHUNKS overrides for tuning
       const char* v = getenv("EMOE_H2D_CHUNKS");
-      return v ? std::max(1, atoi(v)) : 8;  // 8 measured better than 16 (profiles/r01_summary.md)
+      // 4 measured best of {2, 4, 8, 16} with the async two-staging-set pipeline
+      return v ? std::max(1, atoi(v)) : 4;
     }();
     int64_t chunk = std::max<int64_t>(8192, ceil_div(T, n_chunks));
     chunk = ceil_div(chunk, kRouteBlockTokens) * kRouteBlockTokens;
