@@ -50,15 +50,22 @@ __global__ void __launch_bounds__(256) scan_blocks_kernel(const int32_t* __restr
 }
 
 // K3a, pass 2: padded segment offsets (a running sum over E experts)
-__global__ void seg_offsets_kernel(const int32_t* __restrict__ counts, int E, int pad,
-                                   int64_t* __restrict__ seg_offsets) {
-  if (threadIdx.x != 0) return;
-  int64_t off = 0;
-  for (int e = 0; e < E; ++e) {
-    seg_offsets[e] = off;
-    off += ((int64_t)counts[e] + pad - 1) / pad * pad;
+// (one block of 1024 threads, Hillis-Steele scan in shared memory)
+__global__ void __launch_bounds__(1024) seg_offsets_kernel(const int32_t* __restrict__ counts, int E, int pad,
+                                                           int64_t* __restrict__ seg_offsets) {
+  __shared__ int64_t buf[2][1024];
+  const int i = threadIdx.x;
+  const int64_t v = i < E ? ((int64_t)counts[i] + pad - 1) / pad * pad : 0;
+  int cur = 0;
+  buf[cur][i] = v;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    buf[cur ^ 1][i] = buf[cur][i] + (i >= off ? buf[cur][i - off] : 0);
+    cur ^= 1;
+    __syncthreads();
   }
-  seg_offsets[E] = off;
+  if (i < E) seg_offsets[i] = buf[cur][i] - v;  // exclusive
+  if (i == E - 1) seg_offsets[E] = buf[cur][i];
 }
 
 // K3b.  Block = 128 tokens (the route kernel's blocks).  Warps 0-3 rank their
@@ -218,7 +225,7 @@ void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32
   EMOE_REQUIRE(E <= 1024, "scan: too many experts");
   scan_blocks_kernel<<<E, 256, 0, s>>>(block_counts, nblocks, E, block_base, counts);
   EMOE_CUDA(cudaGetLastError());
-  seg_offsets_kernel<<<1, 32, 0, s>>>(counts, E, pad, seg_offsets);
+  seg_offsets_kernel<<<1, 1024, 0, s>>>(counts, E, pad, seg_offsets);
   EMOE_CUDA(cudaGetLastError());
   count_launch(2);
 }

@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(128) gate_route_f32_kernel(const float* __rest
 // ---------------------------------------------------------------------------
 // routing-driven mode: logits supplied by the caller
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) route_from_logits_kernel(const float* __restrict__ logits, RouteArgs a,
+__global__ void __launch_bounds__(512) route_from_logits_kernel(const float* __restrict__ logits, RouteArgs a,
                                                                 RouteOut o) {
   __shared__ SharedRouteState st;
   load_route_state(st, a);
@@ -447,13 +447,14 @@ __global__ void __launch_bounds__(128) route_from_logits_kernel(const float* __r
   if (o.logits && o.logits != logits)
     for (int64_t i = threadIdx.x; i < min((int64_t)RT, a.T - t0) * a.E; i += blockDim.x)
       o.logits[t0 * a.E + i] = logits[t0 * a.E + i];
-  if (a.E >= 32) {
-    for (int r = threadIdx.x / 32; r < RT; r += 4) {
+  if (a.E >= 32) {  // warp per token, blockDim / 32 tokens in flight per block
+    const int nw = blockDim.x / 32;
+    for (int r = threadIdx.x / 32; r < RT; r += nw) {
       const int64_t t = t0 + r;
       if (t >= a.T) break;
       route_one_token_warp(logits + t * a.E, t, a, o, st);
     }
-  } else {
+  } else if (threadIdx.x < RT) {
     const int64_t t = t0 + threadIdx.x;
     if (t < a.T) route_one_token(logits + t * a.E, t, a, o, st);
   }
@@ -529,9 +530,9 @@ void launch_route_from_logits(const float* logits, const RouteArgs& a, const Rou
   EMOE_REQUIRE(a.k >= 1 && a.k <= 8 && a.k <= a.E, "route: top_k must be in [1, min(8, E)]");
   const int nblocks = (int)ceil_div(a.T, RT);
   if (nblocks == 0) return;
-  route_from_logits_kernel<<<nblocks, RT, 0, s>>>(logits, a, o);
+  route_from_logits_kernel<<<nblocks, a.E >= 32 ? 512 : RT, 0, s>>>(logits, a, o);
   EMOE_CUDA(cudaGetLastError());
-    count_launch();
+  count_launch();
 }
 
 }  // namespace emoe
