@@ -93,15 +93,25 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
       rank[j] = 0;
     }
     const uint32_t lt = (1u << lane) - 1u;
-    // per expert: lanes (tokens) that serve it; a token serves an expert at most once
-    for (int e = 0; e < E; ++e) {
-      bool has = false;
-      for (int j = 0; j < k; ++j) has |= (my[j] == e);
-      const uint32_t m = __ballot_sync(0xffffffffu, has);
-      if (lane == 0) warp_counts[warp * E + e] = __popc(m);
-      if (has)
-        for (int j = 0; j < k; ++j)
-          if (my[j] == e) rank[j] = __popc(m & lt);
+    if (k == 1) {  // one served slot: lanes with the same expert form one match group
+      for (int e = lane; e < E; e += 32) warp_counts[warp * E + e] = 0;
+      __syncwarp();
+      const uint32_t m = __match_any_sync(0xffffffffu, my[0]);
+      if (my[0] >= 0) {
+        rank[0] = __popc(m & lt);
+        if (rank[0] == 0) warp_counts[warp * E + my[0]] = __popc(m);
+      }
+    } else {
+      // per expert: lanes (tokens) that serve it; a token serves an expert at most once
+      for (int e = 0; e < E; ++e) {
+        bool has = false;
+        for (int j = 0; j < k; ++j) has |= (my[j] == e);
+        const uint32_t m = __ballot_sync(0xffffffffu, has);
+        if (lane == 0) warp_counts[warp * E + e] = __popc(m);
+        if (has)
+          for (int j = 0; j < k; ++j)
+            if (my[j] == e) rank[j] = __popc(m & lt);
+      }
     }
   }
   __syncthreads();
