@@ -41,6 +41,10 @@ constexpr int BK = 64;   // one 128-byte swizzle row of bf16
 constexpr int MAX_EXPERTS = 256;
 constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;
+// epilogue output staging for the TMA store: per epilogue warp two 32x32 bf16
+// boxes (64-B swizzled rows), double-buffered against the bulk-store engine
+constexpr int OUT_BOX_BYTES = 32 * 32 * 2;
+constexpr int OUT_STAGE_BYTES = 4 * 2 * OUT_BOX_BYTES;
 
 template <int CG>
 struct Cfg {
@@ -50,7 +54,8 @@ struct Cfg {
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 4096 /*barriers + offsets*/;
+  static constexpr int SMEM_BYTES =
+      STAGES * STAGE_BYTES + 1024 /*align*/ + 4096 /*barriers + offsets*/ + OUT_STAGE_BYTES;
 };
 
 struct Params {
@@ -69,6 +74,7 @@ struct Params {
   int col_limit;        // EPI_F32: columns >= col_limit not stored (multiple of 32)
   int64_t single_rows;  // > 0: one segment [0, single_rows) instead of seg_offsets
   int64_t ldo;
+  int tma_store;        // bf16 epilogues: 1 = stage in smem + TMA bulk store, 0 = direct st.global
 };
 
 struct TileCoord {
@@ -133,10 +139,52 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {  // arrive o
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 
+// ---- TMA bulk store of the epilogue boxes ----
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* desc, const void* smem_src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(desc)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// One warp's 32 rows x 32 bf16 columns (lane = row, packed[16] = its 64 B)
+// to global.  TMA path: the warp's staging box (64-B rows, SWIZZLE_64B: 16-B
+// chunk c of row r sits at chunk c ^ ((r >> 1) & 3), which also makes the
+// 8-lane store phases bank-conflict free), then one bulk tensor store issued
+// by lane 0; the box is reused two stores later (wait_group.read 1).
+__device__ __forceinline__ void store_box(const Params& p, const CUtensorMap* tmap_out, uint8_t* stage_box,
+                                          __nv_bfloat16* orow, const uint32_t (&packed)[16], int lane, int col,
+                                          int64_t row0) {
+  if (p.tma_store) {
+    if (lane == 0) bulk_wait_read1();
+    __syncwarp();
+    const int sw = (lane >> 1) & 3;
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+      *reinterpret_cast<uint4*>(stage_box + lane * 64 + ((v ^ sw) << 4)) =
+          make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmap_out, stage_box, col, (int32_t)row0);
+      bulk_commit();
+    }
+  } else {
+    uint4* dst = reinterpret_cast<uint4*>(orow);
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+      dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+  }
+}
+
 template <int EPI, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                        const __grid_constant__ CUtensorMap tmap_b2, Params p) {
+                        const __grid_constant__ CUtensorMap tmap_b2, const __grid_constant__ CUtensorMap tmap_out,
+                        Params p) {
   using C = Cfg<CG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -148,6 +196,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tempty_bar = tfull_bar + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int64_t* s_offs = reinterpret_cast<int64_t*>(tmem_slot + 4);
+  uint8_t* out_stage = smem + C::STAGES * C::STAGE_BYTES + 4096;  // 1024-B aligned
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -294,6 +343,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else {
     // ===================== epilogue (warps 2..5, every CTA) =====================
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    uint8_t* my_stage = out_stage + (warp - 2) * 2 * OUT_BOX_BYTES;
+    int box = 0;
     int local = 0;
     for (int t = cluster_id; t < total_tiles; t += num_clusters, ++local) {
       const TileCoord c = decode_tile(t, total_mb, p.n_blocks, p.group_m, C::TILE_M, s_offs, E);
@@ -301,9 +352,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
-      const int64_t row = (int64_t)c.mb * C::TILE_M + rank * 128 + quarter * 32 + lane;
+      const int64_t row0 = (int64_t)c.mb * C::TILE_M + rank * 128 + quarter * 32;
+      const int64_t row = row0 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + buf * BN;
-      __nv_bfloat16* orow = p.out + row * p.ldo + (int64_t)c.nb * p.out_block_cols;
+      const int col0 = c.nb * p.out_block_cols;
+      __nv_bfloat16* orow = p.out + row * p.ldo + col0;
       if (EPI == EPI_SWIGLU) {
 #pragma unroll 1
         for (int cc = 0; cc < BN / 2; cc += 32) {
@@ -320,10 +373,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             float h1 = g1 / (1.0f + __expf(-g1)) * u1;
             packed[j] = pack_bf16x2(h0, h1);
           }
-          uint4* dst = reinterpret_cast<uint4*>(orow + cc);
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-            dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+          store_box(p, &tmap_out, my_stage + box * OUT_BOX_BYTES, orow + cc, packed, lane, col0 + cc, row0);
+          box ^= 1;
         }
       } else if (EPI == EPI_F32) {
         // fp32 accumulators straight out (dense gate GEMM): rows >= row_limit
@@ -357,10 +408,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             packed[j] = pack_bf16x2(v0, v1);
           }
-          uint4* dst = reinterpret_cast<uint4*>(orow + cc);
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-            dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+          store_box(p, &tmap_out, my_stage + box * OUT_BOX_BYTES, orow + cc, packed, lane, col0 + cc, row0);
+          box ^= 1;
         }
       }
       tc_fence_before();
@@ -371,6 +420,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_arrive_leader(&tempty_bar[buf]);
       }
     }
+    if (EPI != EPI_F32 && p.tma_store && lane == 0) bulk_wait_all();
   }
 
   if (CG == 2)
@@ -422,6 +472,28 @@ CUtensorMap make_tmap_bf16_2d(const void* base, uint64_t rows, uint64_t cols, ui
   return m;
 }
 
+// 2-D bf16 output [rows][cols] as the epilogue's TMA store target: 32 x 32 box, 64-B swizzle
+CUtensorMap make_tmap_bf16_store(const void* base, uint64_t rows, uint64_t cols) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (store) failed: " + std::to_string((int)r));
+  return m;
+}
+
+static bool tma_store_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("EMOE_GEMM_TMA_STORE");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 int gemm_tile_m(int cta_group) { return 128 * cta_group; }
 int gemm_b_box_rows(int epi, int cta_group) { return epi == EPI_SWIGLU ? 128 : 256 / cta_group; }
 
@@ -438,12 +510,13 @@ static int group_rows(int K, int tile_m) {
 }
 
 static void launch_params(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
-                          const CUtensorMap& tb2, const gemm::Params& p, int num_sms, cudaStream_t stream);
+                          const CUtensorMap& tb2, const CUtensorMap& to, const gemm::Params& p, int num_sms,
+                          cudaStream_t stream);
 
 void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
-                         int num_sms, cudaStream_t stream, const int32_t* seg_expert) {
+                         int num_sms, cudaStream_t stream, const int32_t* seg_expert, const CUtensorMap* tmap_out) {
   EMOE_REQUIRE(num_experts <= gemm::MAX_EXPERTS, "grouped_gemm: too many segments");
   EMOE_REQUIRE(K % gemm::BK == 0, "grouped_gemm: K must be a multiple of 64");
   EMOE_REQUIRE(cta_group == 1 || cta_group == 2, "grouped_gemm: cta_group must be 1 or 2");
@@ -464,7 +537,8 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
   p.row_limit = 0;
   p.col_limit = 0;
   p.single_rows = 0;
-  launch_params(epi, cta_group, ta, tb, tb2, p, num_sms, stream);
+  p.tma_store = tmap_out != nullptr && tma_store_enabled();
+  launch_params(epi, cta_group, ta, tb, tb2, p.tma_store ? *tmap_out : ta, p, num_sms, stream);
 }
 
 __device__ int32_t g_slot_zero = 0;
@@ -491,11 +565,13 @@ void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t
   p.row_limit = M;
   p.col_limit = col_limit;
   p.single_rows = ceil_div(M, 128) * 128;
-  launch_params(EPI_F32, 1, ta, tb, tb, p, num_sms, stream);
+  p.tma_store = 0;
+  launch_params(EPI_F32, 1, ta, tb, tb, ta, p, num_sms, stream);
 }
 
 static void launch_params(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
-                          const CUtensorMap& tb2, const gemm::Params& p, int num_sms, cudaStream_t stream) {
+                          const CUtensorMap& tb2, const CUtensorMap& to, const gemm::Params& p, int num_sms,
+                          cudaStream_t stream) {
   const int grid = cta_group == 2 ? (num_sms / 2) * 2 : num_sms;
   auto run = [&](auto kernel, int smem, int idx) {
     static bool attr_set[7] = {false, false, false, false, false, false, false};
@@ -504,7 +580,7 @@ static void launch_params(int epi, int cta_group, const CUtensorMap& ta, const C
       attr_set[idx] = true;
     }
     if (cta_group == 1) {
-      kernel<<<grid, gemm::NUM_THREADS, smem, stream>>>(ta, tb, tb2, p);
+      kernel<<<grid, gemm::NUM_THREADS, smem, stream>>>(ta, tb, tb2, to, p);
     } else {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
@@ -518,7 +594,7 @@ static void launch_params(int epi, int cta_group, const CUtensorMap& ta, const C
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      EMOE_CUDA(cudaLaunchKernelEx(&cfg, kernel, ta, tb, tb2, p));
+      EMOE_CUDA(cudaLaunchKernelEx(&cfg, kernel, ta, tb, tb2, to, p));
     }
     EMOE_CUDA(cudaGetLastError());
     count_launch();

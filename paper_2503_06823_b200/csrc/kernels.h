@@ -63,12 +63,14 @@ void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int
 
 // K4: tcgen05 grouped GEMM (bf16); cta_group 1 (tile 128x256) or 2 (CTA pair, tile 256x256)
 CUtensorMap make_tmap_bf16_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+CUtensorMap make_tmap_bf16_store(const void* base, uint64_t rows, uint64_t cols);  // epilogue store target
 int gemm_tile_m(int cta_group);                 // segment padding the kernel needs
 int gemm_b_box_rows(int epi, int cta_group);    // TMA box rows of the weight operand
 void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
-                         int num_sms, cudaStream_t stream, const int32_t* seg_expert = nullptr);
+                         int num_sms, cudaStream_t stream, const int32_t* seg_expert = nullptr,
+                         const CUtensorMap* tmap_out = nullptr);  // null: direct st.global epilogue
 
 // K1 for many experts: the gate as one dense tcgen05 GEMM with fp32 output,
 // out[M][ldo] = A[M][K] . B[N_out][K]^T, columns >= col_limit (multiple of 32) not stored

@@ -102,7 +102,7 @@ struct emoe_layer {
   int* err_flag = nullptr;
   int64_t last_T = 0;
 
-  CUtensorMap ta1{}, tb1{}, tb3{}, ta2{}, tb2{};
+  CUtensorMap ta1{}, tb1{}, tb3{}, ta2{}, tb2{}, to1{}, to2{};
 
   size_t w1_elems() const { return (size_t)cfg.d_ff * cfg.d_model; }
   size_t w2_elems() const { return (size_t)cfg.d_model * cfg.d_ff; }
@@ -251,16 +251,18 @@ struct emoe_layer {
            cudaStream_t s, bool workspace) {
     const int d = cfg.d_model, f = cfg.d_ff;
     if (cfg.dtype == EMOE_DTYPE_BF16) {
-      CUtensorMap a1 = ta1, a2 = ta2;
+      CUtensorMap a1 = ta1, a2 = ta2, o1 = to1, o2 = to2;
       if (!workspace) {
         a1 = make_tmap_bf16_2d(xr, (uint64_t)R, d, 128);
         a2 = make_tmap_bf16_2d(hr, (uint64_t)R, f, 128);
+        o1 = make_tmap_bf16_store(hr, (uint64_t)R, f);
+        o2 = make_tmap_bf16_store(yr, (uint64_t)R, d);
       }
       launch_grouped_gemm(swiglu() ? EPI_SWIGLU : EPI_RELU, cta_group, a1, tb1, tb3, segs, slot_dev, n_seg, d, f, f,
-                          static_cast<__nv_bfloat16*>(hr), f, num_sms, s, seg_expert);
+                          static_cast<__nv_bfloat16*>(hr), f, num_sms, s, seg_expert, &o1);
       mark(3, s);
       launch_grouped_gemm(EPI_STORE, cta_group, a2, tb2, tb2, segs, slot_dev, n_seg, f, d, d,
-                          static_cast<__nv_bfloat16*>(yr), d, num_sms, s, seg_expert);
+                          static_cast<__nv_bfloat16*>(yr), d, num_sms, s, seg_expert, &o2);
       mark(4, s);
     } else {
       launch_grouped_gemm_f32(swiglu() ? EPI_SWIGLU : EPI_RELU, static_cast<const float*>(xr), d,
@@ -534,6 +536,8 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
         L->tb3 = L->swiglu() ? make_tmap_bf16_2d(L->w3_pool, (uint64_t)c.num_slots * f, d, b1_box) : L->tb1;
         L->ta2 = make_tmap_bf16_2d(L->h, L->rows_cap, f, 128);
         L->tb2 = make_tmap_bf16_2d(L->w2_pool, (uint64_t)c.num_slots * d, f, gemm_b_box_rows(EPI_STORE, L->cta_group));
+        L->to1 = make_tmap_bf16_store(L->h, L->rows_cap, f);
+        L->to2 = make_tmap_bf16_store(L->y_perm, L->rows_cap, d);
       }
       EMOE_CUDA(cudaDeviceSynchronize());
     } catch (...) {
