@@ -77,8 +77,9 @@ typedef struct {
   int64_t max_tokens;
   int forced_miss; /* 1: a layer with no resident expert serves nothing (engine.cpp:533-537) */
   int gemm_cta_group; /* bf16 FFN GEMM: 1 = one CTA per 128x256 tile, 2 = CTA pair per 256x256
-                         tile (segments padded to 256 rows), 0 = auto (1: faster under the
-                         1 kW power cap, profiles/r01_summary.md) */
+                         tile (segments padded to 256 rows), 0 = auto (2 when d_model <= 2048:
+                         short-K GEMMs are L2-feed bound; else 1: faster under the 1 kW power
+                         cap; profiles/r01_cta_group_ab.jsonl) */
 } emoe_layer_config;
 
 int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out);

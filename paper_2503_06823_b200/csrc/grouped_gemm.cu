@@ -41,10 +41,11 @@ constexpr int BK = 64;   // one 128-byte swizzle row of bf16
 constexpr int MAX_EXPERTS = 256;
 constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;
-// epilogue output staging for the TMA store: per epilogue warp two 32x32 bf16
-// boxes (64-B swizzled rows), double-buffered against the bulk-store engine
-constexpr int OUT_BOX_BYTES = 32 * 32 * 2;
-constexpr int OUT_STAGE_BYTES = 4 * 2 * OUT_BOX_BYTES;
+// epilogue output staging for the TMA store: one 32-row x 64-column bf16 box
+// (128-B swizzled rows) per epilogue warp
+constexpr int OUT_BOX_COLS = 64;
+constexpr int OUT_BOX_BYTES = 32 * OUT_BOX_COLS * 2;
+constexpr int OUT_STAGE_BYTES = 4 * OUT_BOX_BYTES;
 
 template <int CG>
 struct Cfg {
@@ -133,11 +134,6 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {  // arrive on 
       "h"((uint16_t)0x3)
       : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {  // arrive on CTA 0's copy of `bar`
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
-}
 
 // ---- TMA bulk store of the epilogue boxes ----
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* desc, const void* smem_src, int32_t c0, int32_t c1) {
@@ -147,24 +143,37 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* desc, const void
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// One warp's 32 rows x 32 bf16 columns (lane = row, packed[16] = its 64 B)
-// to global.  TMA path: the warp's staging box (64-B rows, SWIZZLE_64B: 16-B
-// chunk c of row r sits at chunk c ^ ((r >> 1) & 3), which also makes the
+// TMEM-empty signal: the accumulator reads are complete (tcgen05.wait::ld),
+// nothing else needs ordering, so the arrive is relaxed (a release arrive
+// costs a full memory barrier per tile)
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader_relaxed(uint64_t* bar) {  // CTA 0's copy of `bar`
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+// One warp's 32 rows x 64 bf16 columns (lane = row, packed[32] = its 128 B)
+// to global.  TMA path: the warp's staging box (128-B rows, SWIZZLE_128B:
+// 16-B chunk c of row r sits at chunk c ^ (r & 7), which also makes the
 // 8-lane store phases bank-conflict free), then one bulk tensor store issued
-// by lane 0; the box is reused two stores later (wait_group.read 1).
+// by lane 0.  The box is reused by the warp's next store (wait_group.read 0
+// first — by then the previous chunk's TMEM loads and math have hidden it).
 __device__ __forceinline__ void store_box(const Params& p, const CUtensorMap* tmap_out, uint8_t* stage_box,
-                                          __nv_bfloat16* orow, const uint32_t (&packed)[16], int lane, int col,
+                                          __nv_bfloat16* orow, const uint32_t (&packed)[32], int lane, int col,
                                           int64_t row0) {
   if (p.tma_store) {
-    if (lane == 0) bulk_wait_read1();
+    if (lane == 0) bulk_wait_read0();
     __syncwarp();
-    const int sw = (lane >> 1) & 3;
+    const int sw = lane & 7;
 #pragma unroll
-    for (int v = 0; v < 4; ++v)
-      *reinterpret_cast<uint4*>(stage_box + lane * 64 + ((v ^ sw) << 4)) =
+    for (int v = 0; v < 8; ++v)
+      *reinterpret_cast<uint4*>(stage_box + lane * 128 + ((v ^ sw) << 4)) =
           make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
     fence_proxy_async();
     __syncwarp();
@@ -175,7 +184,7 @@ __device__ __forceinline__ void store_box(const Params& p, const CUtensorMap* tm
   } else {
     uint4* dst = reinterpret_cast<uint4*>(orow);
 #pragma unroll
-    for (int v = 0; v < 4; ++v)
+    for (int v = 0; v < 8; ++v)
       dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
   }
 }
@@ -343,8 +352,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else {
     // ===================== epilogue (warps 2..5, every CTA) =====================
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    uint8_t* my_stage = out_stage + (warp - 2) * 2 * OUT_BOX_BYTES;
-    int box = 0;
+    uint8_t* my_stage = out_stage + (warp - 2) * OUT_BOX_BYTES;
     int local = 0;
     for (int t = cluster_id; t < total_tiles; t += num_clusters, ++local) {
       const TileCoord c = decode_tile(t, total_mb, p.n_blocks, p.group_m, C::TILE_M, s_offs, E);
@@ -359,22 +367,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __nv_bfloat16* orow = p.out + row * p.ldo + col0;
       if (EPI == EPI_SWIGLU) {
 #pragma unroll 1
-        for (int cc = 0; cc < BN / 2; cc += 32) {
-          uint32_t g[32], u[32];
-          tmem_ld_32x32b_x32(taddr + cc, g);
-          tmem_ld_32x32b_x32(taddr + BN / 2 + cc, u);
+        for (int cc = 0; cc < BN / 2; cc += OUT_BOX_COLS) {
+          uint32_t g0[32], g1[32], u0[32], u1[32];
+          tmem_ld_32x32b_x32(taddr + cc, g0);
+          tmem_ld_32x32b_x32(taddr + cc + 32, g1);
+          tmem_ld_32x32b_x32(taddr + BN / 2 + cc, u0);
+          tmem_ld_32x32b_x32(taddr + BN / 2 + cc + 32, u1);
           tmem_ld_wait();
-          uint32_t packed[16];
+          uint32_t packed[32];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float g0 = __uint_as_float(g[2 * j]), g1 = __uint_as_float(g[2 * j + 1]);
-            float u0 = __uint_as_float(u[2 * j]), u1 = __uint_as_float(u[2 * j + 1]);
-            float h0 = g0 / (1.0f + __expf(-g0)) * u0;
-            float h1 = g1 / (1.0f + __expf(-g1)) * u1;
+          for (int j = 0; j < 32; ++j) {
+            const bool hi = j >= 16;
+            const int q = 2 * (j & 15);
+            const float ga = __uint_as_float(hi ? g1[q] : g0[q]), gb = __uint_as_float(hi ? g1[q + 1] : g0[q + 1]);
+            const float ua = __uint_as_float(hi ? u1[q] : u0[q]), ub = __uint_as_float(hi ? u1[q + 1] : u0[q + 1]);
+            const float h0 = ga / (1.0f + __expf(-ga)) * ua;
+            const float h1 = gb / (1.0f + __expf(-gb)) * ub;
             packed[j] = pack_bf16x2(h0, h1);
           }
-          store_box(p, &tmap_out, my_stage + box * OUT_BOX_BYTES, orow + cc, packed, lane, col0 + cc, row0);
-          box ^= 1;
+          store_box(p, &tmap_out, my_stage, orow + cc, packed, lane, col0 + cc, row0);
         }
       } else if (EPI == EPI_F32) {
         // fp32 accumulators straight out (dense gate GEMM): rows >= row_limit
@@ -394,30 +405,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       } else {
 #pragma unroll 1
-        for (int cc = 0; cc < BN; cc += 32) {
-          uint32_t a[32];
-          tmem_ld_32x32b_x32(taddr + cc, a);
+        for (int cc = 0; cc < BN; cc += OUT_BOX_COLS) {
+          uint32_t a0[32], a1[32];
+          tmem_ld_32x32b_x32(taddr + cc, a0);
+          tmem_ld_32x32b_x32(taddr + cc + 32, a1);
           tmem_ld_wait();
-          uint32_t packed[16];
+          uint32_t packed[32];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float v0 = __uint_as_float(a[2 * j]), v1 = __uint_as_float(a[2 * j + 1]);
+          for (int j = 0; j < 32; ++j) {
+            const int q = 2 * (j & 15);
+            float v0 = __uint_as_float(j < 16 ? a0[q] : a1[q]), v1 = __uint_as_float(j < 16 ? a0[q + 1] : a1[q + 1]);
             if (EPI == EPI_RELU) {
               v0 = fmaxf(v0, 0.0f);
               v1 = fmaxf(v1, 0.0f);
             }
             packed[j] = pack_bf16x2(v0, v1);
           }
-          store_box(p, &tmap_out, my_stage + box * OUT_BOX_BYTES, orow + cc, packed, lane, col0 + cc, row0);
-          box ^= 1;
+          store_box(p, &tmap_out, my_stage, orow + cc, packed, lane, col0 + cc, row0);
         }
       }
       tc_fence_before();
       if (lane == 0) {
         if (CG == 1)
-          mbar_arrive(&tempty_bar[buf]);
+          mbar_arrive_relaxed(&tempty_bar[buf]);
         else
-          mbar_arrive_leader(&tempty_bar[buf]);
+          mbar_arrive_leader_relaxed(&tempty_bar[buf]);
       }
     }
     if (EPI != EPI_F32 && p.tma_store && lane == 0) bulk_wait_all();
@@ -472,15 +484,15 @@ CUtensorMap make_tmap_bf16_2d(const void* base, uint64_t rows, uint64_t cols, ui
   return m;
 }
 
-// 2-D bf16 output [rows][cols] as the epilogue's TMA store target: 32 x 32 box, 64-B swizzle
+// 2-D bf16 output [rows][cols] as the epilogue's TMA store target: 32 rows x 64 columns, 128-B swizzle
 CUtensorMap make_tmap_bf16_store(const void* base, uint64_t rows, uint64_t cols) {
   CUtensorMap m;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {gemm::OUT_BOX_COLS, 32};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (store) failed: " + std::to_string((int)r));
   return m;

@@ -479,7 +479,12 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
       const int E = c.num_experts, k = c.top_k;
       const int64_t T = c.max_tokens;
       EMOE_REQUIRE(c.gemm_cta_group >= 0 && c.gemm_cta_group <= 2, "layer.gemm_cta_group: must be 0, 1 or 2");
-      L->cta_group = c.dtype == EMOE_DTYPE_BF16 ? (c.gemm_cta_group ? c.gemm_cta_group : 1) : 1;
+      // auto: short-K layers (d_model <= 2048) are fed from L2 at ~96 B/clk/SM by the
+      // 128x256 tile and gain from the CTA pair's halved operand traffic (Switch shape
+      // +6%); large layers run at the power cap, where 1-CTA is 9% faster (Mixtral
+      // shape) — profiles/r01_cta_group_ab.jsonl
+      const int auto_cg = c.d_model <= 2048 ? 2 : 1;
+      L->cta_group = c.dtype == EMOE_DTYPE_BF16 ? (c.gemm_cta_group ? c.gemm_cta_group : auto_cg) : 1;
       L->seg_pad = c.dtype == EMOE_DTYPE_BF16 ? gemm_tile_m(L->cta_group) : kSegPad;
       L->rows_cap = T * k + (int64_t)E * L->seg_pad;
       L->route_blocks = (int)ceil_div(T, kRouteBlockTokens);

@@ -133,33 +133,31 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
     }
   }
   __syncthreads();
-  // gather: warp w copies tokens w, w+8, ...; lanes own 16-byte column chunks
+  // gather: the block's rows x (row_bytes / 16) chunks as one flat index space
+  // (consecutive threads -> consecutive 16-B chunks of the contiguous x rows),
+  // GATHER_UNROLL independent loads in flight per thread whatever d is
   const int nvec = row_bytes / 16;
-  for (int i = warp; i < RT; i += PERMUTE_THREADS / 32) {
-    const int64_t tt = t0 + i;
-    if (tt >= T) break;
-    int32_t d_i[8];
-    int nd = 0;
-    for (int j = 0; j < k; ++j) {
-      const int32_t v = dst_s[i * k + j];
-      if (v >= 0) d_i[nd++] = v;
+  const int rows = (int)min((int64_t)RT, T - t0);
+  const int total = rows * nvec;
+  const uint4* src = reinterpret_cast<const uint4*>(x + t0 * row_bytes);
+  for (int base = threadIdx.x; base < total; base += PERMUTE_THREADS * GATHER_UNROLL) {
+    uint4 val[GATHER_UNROLL];
+    int tok[GATHER_UNROLL];
+#pragma unroll
+    for (int u = 0; u < GATHER_UNROLL; ++u) {
+      const int i = base + u * PERMUTE_THREADS;
+      tok[u] = i < total ? i / nvec : -1;
+      if (tok[u] >= 0 && dst_s[tok[u] * k] < 0) tok[u] = -1;  // token served nowhere
+      if (tok[u] >= 0) val[u] = __ldg(src + i);
     }
-    if (nd == 0) continue;
-    const uint4* src = reinterpret_cast<const uint4*>(x + tt * row_bytes);
-    for (int v0 = 0; v0 < nvec; v0 += 32 * GATHER_UNROLL) {
-      uint4 val[GATHER_UNROLL];
 #pragma unroll
-      for (int u = 0; u < GATHER_UNROLL; ++u) {
-        const int v = v0 + u * 32 + lane;
-        if (v < nvec) val[u] = __ldg(src + v);
-      }
-      for (int q = 0; q < nd; ++q) {
-        uint4* out = reinterpret_cast<uint4*>(x_perm + (int64_t)d_i[q] * row_bytes);
-#pragma unroll
-        for (int u = 0; u < GATHER_UNROLL; ++u) {
-          const int v = v0 + u * 32 + lane;
-          if (v < nvec) out[v] = val[u];
-        }
+    for (int u = 0; u < GATHER_UNROLL; ++u) {
+      if (tok[u] < 0) continue;
+      const int v = base + u * PERMUTE_THREADS - tok[u] * nvec;
+      for (int j = 0; j < k; ++j) {
+        const int32_t d = dst_s[tok[u] * k + j];
+        if (d < 0) break;  // served slots are compacted to the front
+        reinterpret_cast<uint4*>(x_perm + (int64_t)d * row_bytes)[v] = val[u];
       }
     }
   }

@@ -64,8 +64,12 @@ struct SharedRouteState {
   int counts[MAX_E];
   int n_res;
   int first_res;
+  int fallback;  // route_token's fallback expert: token-independent, computed once per block
 };
 
+// Residency tables into shared memory; warp 0 derives the resident count, the
+// first resident and the fallback expert (largest layer score among residents,
+// smallest index on ties: the serial scan of engine.cpp's route_token).
 __device__ void load_route_state(SharedRouteState& st, const RouteArgs& a) {
   for (int e = threadIdx.x; e < a.E; e += blockDim.x) {
     st.resident[e] = a.resident[e];
@@ -73,15 +77,36 @@ __device__ void load_route_state(SharedRouteState& st, const RouteArgs& a) {
     st.counts[e] = 0;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int n = 0, first = -1;
-    for (int e = 0; e < a.E; ++e)
-      if (st.resident[e]) {
-        if (first < 0) first = e;
-        ++n;
+  if (threadIdx.x < 32) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x;
+    int n = 0, first = -1, be = -1;
+    double bs = 0.0;
+    for (int e0 = 0; e0 < a.E; e0 += 32) {
+      const int e = e0 + lane;
+      const bool r = e < a.E && st.resident[e];
+      const unsigned m = __ballot_sync(FULL, r);
+      n += __popc(m);
+      if (first < 0 && m) first = e0 + __ffs(m) - 1;
+      if (r && (be < 0 || st.scores[e] > bs)) {
+        bs = st.scores[e];
+        be = e;
       }
-    st.n_res = n;
-    st.first_res = first;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double os = __shfl_xor_sync(FULL, bs, off);
+      const int oe = __shfl_xor_sync(FULL, be, off);
+      if (oe >= 0 && (be < 0 || os > bs || (os == bs && oe < be))) {
+        bs = os;
+        be = oe;
+      }
+    }
+    if (lane == 0) {
+      st.n_res = n;
+      st.first_res = first;
+      st.fallback = a.scores ? be : first;
+    }
   }
   __syncthreads();
 }
@@ -104,13 +129,7 @@ __device__ void route_tail(const int* ti, const float* lg, int64_t t, const Rout
         hit = r == 0;
         break;
       }
-    if (rk < 0) {
-      int best = st.first_res;
-      if (a.scores)
-        for (int e = 0; e < E; ++e)
-          if (st.resident[e] && st.scores[e] > st.scores[best]) best = e;
-      ex = best;
-    }
+    if (rk < 0) ex = st.fallback;
   }
   if (o.route_expert) o.route_expert[t] = ex;
   if (o.route_rank) o.route_rank[t] = rk;
@@ -159,7 +178,21 @@ __device__ void route_one_token(const float* lg, int64_t t, const RouteArgs& a, 
   const int E = a.E, k = a.k;
   int ti[8];
   uint32_t used[MAX_E / 32] = {0, 0, 0, 0};
-  for (int r = 0; r < k; ++r) {
+  {  // first choice: plain argmax (no exclusions)
+    int best = 0;
+    float bv = lg[0];
+    for (int e = 1; e < E; ++e) {
+      const float v = lg[e];
+      if (v > bv) {
+        best = e;
+        bv = v;
+      }
+    }
+    ti[0] = best;
+    used[best >> 5] |= 1u << (best & 31);
+    if (o.topk_idx) o.topk_idx[t * k] = best;
+  }
+  for (int r = 1; r < k; ++r) {
     int best = -1;
     float bv = 0.0f;
     for (int e = 0; e < E; ++e) {
@@ -175,120 +208,6 @@ __device__ void route_one_token(const float* lg, int64_t t, const RouteArgs& a, 
     if (o.topk_idx) o.topk_idx[t * k + r] = best;
   }
   route_tail(ti, lg, t, a, o, st);
-}
-
-// Warp-cooperative form of route_one_token for many experts (E >= 32, e.g. the
-// Switch-base-128 config): lane L owns experts L, L+32, ...; the top-k, the
-// route_token fallback and the full-softmax denominator are warp reductions.
-// Same decisions as the serial form: top-k = largest logit, smallest index on
-// ties; fallback = largest layer score among residents, smallest index on ties.
-__device__ void route_one_token_warp(const float* lg, int64_t t, const RouteArgs& a, const RouteOut& o,
-                                     SharedRouteState& st) {
-  const int E = a.E, k = a.k, lane = threadIdx.x & 31;
-  constexpr unsigned FULL = 0xffffffffu;
-  int ti[8];
-  uint32_t used = 0;  // bit j: expert lane + 32 j already chosen
-  for (int r = 0; r < k; ++r) {
-    float bv = 0.0f;
-    int bi = -1;
-    for (int j = 0; lane + 32 * j < E; ++j) {
-      if (used & (1u << j)) continue;
-      const float v = lg[lane + 32 * j];
-      if (bi < 0 || v > bv) {
-        bv = v;
-        bi = lane + 32 * j;
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const float ov = __shfl_xor_sync(FULL, bv, off);
-      const int oi = __shfl_xor_sync(FULL, bi, off);
-      if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    ti[r] = bi;
-    if ((bi & 31) == lane) used |= 1u << (bi >> 5);
-    if (lane == 0 && o.topk_idx) o.topk_idx[t * k + r] = bi;
-  }
-  int ex = -1, rk = -1, hit = 0;
-  if (st.n_res == 0) {
-    ex = ti[0];
-    if (!a.forced_miss && lane == 0) atomicExch(a.error_flag, 3);
-  } else {
-    for (int r = 0; r < k; ++r)
-      if (st.resident[ti[r]]) {
-        ex = ti[r];
-        rk = r;
-        hit = r == 0;
-        break;
-      }
-    if (rk < 0) {
-      ex = st.first_res;
-      if (a.scores) {  // warp argmax of scores over residents
-        double bs = 0.0;
-        int be = -1;
-        for (int e = lane; e < E; e += 32)
-          if (st.resident[e] && (be < 0 || st.scores[e] > bs)) {
-            bs = st.scores[e];
-            be = e;
-          }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          const double os = __shfl_xor_sync(FULL, bs, off);
-          const int oe = __shfl_xor_sync(FULL, be, off);
-          if (oe >= 0 && (be < 0 || os > bs || (os == bs && oe < be))) {
-            bs = os;
-            be = oe;
-          }
-        }
-        ex = be;
-      }
-    }
-  }
-  float den_full = 0.0f;
-  if (a.weight_mode != 0) {
-    const float mx = lg[ti[0]];
-    for (int e = lane; e < E; e += 32) den_full += expf(lg[e] - mx);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) den_full += __shfl_xor_sync(FULL, den_full, off);
-  }
-  if (lane != 0) return;
-  if (o.route_expert) o.route_expert[t] = ex;
-  if (o.route_rank) o.route_rank[t] = rk;
-  if (o.route_hit) o.route_hit[t] = (uint8_t)hit;
-  int si[8];
-  int ns = 0;
-  if (st.n_res > 0) {
-    if (rk >= 0) {
-      for (int r = 0; r < k; ++r)
-        if (st.resident[ti[r]]) si[ns++] = ti[r];
-    } else {
-      si[ns++] = ex;
-    }
-  }
-  float w[8];
-  if (a.weight_mode == 0) {
-    if (ns > 0) {
-      const float mx = lg[si[0]];
-      float den = 0.0f;
-      for (int j = 0; j < ns; ++j) {
-        w[j] = expf(lg[si[j]] - mx);
-        den += w[j];
-      }
-      for (int j = 0; j < ns; ++j) w[j] = w[j] / den;
-    }
-  } else {
-    const float mx = lg[ti[0]];
-    for (int j = 0; j < ns; ++j) w[j] = expf(lg[si[j]] - mx) / den_full;
-  }
-  if (o.served_idx)
-    for (int j = 0; j < k; ++j) {
-      o.served_idx[t * k + j] = j < ns ? si[j] : -1;
-      o.served_w[t * k + j] = j < ns ? w[j] : 0.0f;
-    }
-  for (int j = 0; j < ns; ++j) atomicAdd(&st.counts[si[j]], 1);
 }
 
 // block's logits tile [rows][ld] in shared memory -> global [T][E], coalesced
@@ -439,25 +358,45 @@ __global__ void __launch_bounds__(128) gate_route_f32_kernel(const float* __rest
 // ---------------------------------------------------------------------------
 // routing-driven mode: logits supplied by the caller
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(512) route_from_logits_kernel(const float* __restrict__ logits, RouteArgs a,
-                                                                RouteOut o) {
+// Routing from precomputed logits.  Many experts (E >= 32): the block's 128
+// logits rows are staged in shared memory with coalesced 16-B loads (row pitch
+// E + 1 floats, so the per-thread row scans are bank-conflict free) and every
+// thread routes its own token from its row — the same serial top-k / softmax
+// order as the reference, ~4 instructions per logit.
+__global__ void __launch_bounds__(RT) route_from_logits_kernel(const float* __restrict__ logits, RouteArgs a,
+                                                               RouteOut o) {
   __shared__ SharedRouteState st;
+  extern __shared__ float s_rows[];  // [RT][E + 1] when E >= 32
   load_route_state(st, a);
   const int64_t t0 = (int64_t)blockIdx.x * RT;
+  const int rows = (int)min((int64_t)RT, a.T - t0);
+  const float* src = logits + t0 * a.E;
   if (o.logits && o.logits != logits)
-    for (int64_t i = threadIdx.x; i < min((int64_t)RT, a.T - t0) * a.E; i += blockDim.x)
-      o.logits[t0 * a.E + i] = logits[t0 * a.E + i];
-  if (a.E >= 32) {  // warp per token, blockDim / 32 tokens in flight per block
-    const int nw = blockDim.x / 32;
-    for (int r = threadIdx.x / 32; r < RT; r += nw) {
-      const int64_t t = t0 + r;
-      if (t >= a.T) break;
-      route_one_token_warp(logits + t * a.E, t, a, o, st);
+    for (int64_t i = threadIdx.x; i < (int64_t)rows * a.E; i += blockDim.x) o.logits[t0 * a.E + i] = src[i];
+  const float* lg = src + (int64_t)threadIdx.x * a.E;
+  if (a.E >= 32) {
+    const int ld = a.E + 1, n = rows * a.E;
+    if ((a.E & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+      const float4* src4 = reinterpret_cast<const float4*>(src);
+      for (int i = threadIdx.x; i < n / 4; i += RT) {
+        const float4 v = __ldg(src4 + i);
+        const int r = (4 * i) / a.E, c = 4 * i - r * a.E;
+        float* d = s_rows + r * ld + c;
+        d[0] = v.x;
+        d[1] = v.y;
+        d[2] = v.z;
+        d[3] = v.w;
+      }
+    } else {
+      for (int i = threadIdx.x; i < n; i += RT) {
+        const int r = i / a.E;
+        s_rows[r * ld + (i - r * a.E)] = __ldg(src + i);
+      }
     }
-  } else if (threadIdx.x < RT) {
-    const int64_t t = t0 + threadIdx.x;
-    if (t < a.T) route_one_token(logits + t * a.E, t, a, o, st);
+    __syncthreads();
+    lg = s_rows + threadIdx.x * ld;
   }
+  if (threadIdx.x < rows) route_one_token(lg, t0 + threadIdx.x, a, o, st);
   flush_block_counts(a, o, st);
 }
 
@@ -530,7 +469,14 @@ void launch_route_from_logits(const float* logits, const RouteArgs& a, const Rou
   EMOE_REQUIRE(a.k >= 1 && a.k <= 8 && a.k <= a.E, "route: top_k must be in [1, min(8, E)]");
   const int nblocks = (int)ceil_div(a.T, RT);
   if (nblocks == 0) return;
-  route_from_logits_kernel<<<nblocks, a.E >= 32 ? 512 : RT, 0, s>>>(logits, a, o);
+  const int smem = a.E >= 32 ? RT * (a.E + 1) * (int)sizeof(float) : 0;
+  static bool attr = false;
+  if (!attr) {
+    EMOE_CUDA(cudaFuncSetAttribute(route_from_logits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   RT * (MAX_E + 1) * (int)sizeof(float)));
+    attr = true;
+  }
+  route_from_logits_kernel<<<nblocks, RT, smem, s>>>(logits, a, o);
   EMOE_CUDA(cudaGetLastError());
   count_launch();
 }
