@@ -293,6 +293,9 @@ def main():
                     help="stream = BASELINE config 5 (mixed-task 8k-token prompt stream over a 32-layer stack)")
     ap.add_argument("--stream-layers", type=int, default=32)
     ap.add_argument("--stream-prompts", type=int, default=80)
+    ap.add_argument("--residency", default="predicted", choices=["predicted", "dynamic"],
+                    help="--config stream: eMoE predicted residency, or the reference's on-demand baseline "
+                         "(engine.cpp:469-502) for comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--gemm-cta-group", type=int, default=0, choices=[0, 1, 2],
@@ -578,7 +581,8 @@ def main_stream(args):
         stack.forward_prompt(x, logits_of(q), out, hits)
     torch.cuda.synchronize()
     with ClockSampler(0) as clk:
-        st = run_stream(stack, trace, trace_dev, prompt_tasks, x, logits_of, P_train, P_serve)
+        st = run_stream(stack, trace, trace_dev, prompt_tasks, x, logits_of, P_train, P_serve,
+                        residency=args.residency)
     nmat = 3
     served = None
     flops_note = f"2*{nmat}*d*f per served (token, expert) per layer"
@@ -586,9 +590,13 @@ def main_stream(args):
                warmup=args.warmup, ms_per_step=round(st["ms"] / P_serve, 3), higher_is_better=True, scaling="weak",
                vs_baseline=None, dtype="bf16", data="synthetic (random-init weights; routing-driven from the "
                                                    "reference Markov trace)",
-               config=dict(workload="BASELINE config 5: mixed-task stream, 8k-token prompts, %d-layer "
+               config=dict(workload=("BASELINE config 5: mixed-task stream, 8k-token prompts, %d-layer "
                                      "Mixtral-shaped stack, phi=0.5, p=40, predictor skipped for insensitive "
-                                     "windows, loads overlapped" % m, prompts=P_serve, tokens_per_prompt=T,
+                                     "windows, loads overlapped" % m) if args.residency == "predicted" else
+                           ("BASELINE config 5 stream, %d-layer Mixtral-shaped stack, phi=0.5, ON-DEMAND "
+                            "residency baseline (engine.cpp:469-502): per layer keep the experts the prompt "
+                            "demands most, load missing ones synchronously" % m),
+                           residency=args.residency, prompts=P_serve, tokens_per_prompt=T,
                            layers=m, tasks={n: dict(wo=t.wo, sensitive_layers=sum(t.sensitivity))
                                             for n, t in tasks.items()}),
                stream=dict((kk, v) for kk, v in st.items() if kk not in ("ms",)), clocks=clk.summary(),

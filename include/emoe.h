@@ -145,6 +145,11 @@ int emoe_layer_wait_host(emoe_layer* layer);
 /* Route only (A1 + A2): fills the workspace routing fields. */
 int emoe_route(emoe_layer* layer, const void* x_dev, const float* logits_in_dev, int64_t T, void* stream);
 
+/* Demand of the last route / forward: counts_host[E] = tokens whose rank-0
+ * gate choice is e (the per-layer demand map of the on-demand baseline,
+ * engine.cpp:469-478 dynamic_transfers).  Synchronous on `stream`. */
+int emoe_layer_gate_demand(emoe_layer* layer, int64_t* counts_host, void* stream);
+
 /* ========================================================================
  * Stage entry points used by expert parallelism: the forward
  * split at its two exchange points.

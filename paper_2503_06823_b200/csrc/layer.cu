@@ -41,6 +41,19 @@ __global__ void set_tables_kernel(TableUpdate u, uint8_t* resident, int32_t* slo
   }
 }
 
+// engine.cpp:473-478 demand map: tokens per rank-0 gate choice (integer
+// atomics: exact and order-independent)
+__global__ void gate_demand_kernel(const int32_t* topk, int64_t T, int k, int E, unsigned long long* counts) {
+  __shared__ unsigned int h[kMaxTableE];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) h[e] = 0;
+  __syncthreads();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[topk[t * k]], 1u);
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (h[e]) atomicAdd(&counts[e], (unsigned long long)h[e]);
+}
+
 template <typename T>
 T* dmalloc(size_t count) {
   T* p = nullptr;
@@ -101,6 +114,7 @@ struct emoe_layer {
   void* y_out = nullptr;
   int* err_flag = nullptr;
   int64_t last_T = 0;
+  unsigned long long* demand_dev = nullptr;  // emoe_layer_gate_demand scratch
 
   CUtensorMap ta1{}, tb1{}, tb3{}, ta2{}, tb2{}, to1{}, to2{};
 
@@ -425,7 +439,7 @@ struct emoe_layer {
       if (p) cudaFree(p);
     };
     for (void* p : {(void*)wg, w1_pool, w3_pool, w2_pool, (void*)slot_dev, (void*)resident_dev, (void*)scores_dev,
-                    (void*)route_resident_dev, wg_pad,
+                    (void*)route_resident_dev, wg_pad, (void*)demand_dev,
                     (void*)logits, (void*)topk, (void*)r_expert, (void*)r_rank, (void*)r_hit, (void*)served_idx,
                     (void*)served_w, (void*)block_counts, (void*)counts, (void*)seg_offsets, (void*)block_base,
                     (void*)pos, (void*)row_token, x_perm, h, y_perm, x_in, y_out, (void*)err_flag, x_stage[0],
@@ -700,6 +714,27 @@ int emoe_route(emoe_layer* L, const void* x, const float* logits_in, int64_t T, 
     EMOE_REQUIRE(L && (x || logits_in), "route: null argument");
     L->poll(false, static_cast<cudaStream_t>(stream), nullptr);
     L->route(x, logits_in, T, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int emoe_layer_gate_demand(emoe_layer* L, int64_t* counts_host, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(L && counts_host, "gate_demand: null argument");
+    const int E = L->cfg.num_experts;
+    EMOE_REQUIRE(E <= kMaxTableE, "gate_demand: too many experts");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!L->demand_dev) L->demand_dev = dmalloc<unsigned long long>(E);
+    EMOE_CUDA(cudaMemsetAsync(L->demand_dev, 0, sizeof(unsigned long long) * E, s));
+    if (L->last_T > 0) {
+      const int blocks = (int)std::min<int64_t>(ceil_div(L->last_T, (int64_t)256), (int64_t)L->num_sms * 4);
+      gate_demand_kernel<<<blocks, 256, 0, s>>>(L->topk, L->last_T, L->cfg.top_k, E, L->demand_dev);
+      EMOE_CUDA(cudaGetLastError());
+      count_launch();
+    }
+    std::vector<unsigned long long> h(E);
+    EMOE_CUDA(cudaMemcpyAsync(h.data(), L->demand_dev, sizeof(unsigned long long) * E, cudaMemcpyDeviceToHost, s));
+    EMOE_CUDA(cudaStreamSynchronize(s));
+    for (int e = 0; e < E; ++e) counts_host[e] = (int64_t)h[e];
   });
 }
 

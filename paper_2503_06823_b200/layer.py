@@ -174,6 +174,13 @@ class MoELayer:
         check(lib.emoe_route(self.h, C.c_void_p(x.data_ptr()) if x is not None else None,
                              C.c_void_p(logits.data_ptr()) if logits is not None else None, T, _stream_ptr(stream)))
 
+    def gate_demand(self, stream=None) -> np.ndarray:
+        """[E] int64: tokens of the last route/forward whose rank-0 gate choice is e
+        (the on-demand baseline's demand map, engine.cpp:469-478)."""
+        out = np.zeros(self.E, np.int64)
+        check(lib.emoe_layer_gate_demand(self.h, out.ctypes.data_as(C.c_void_p), _stream_ptr(stream)))
+        return out
+
     # -- stage entry points (expert parallelism) -----------------------------
     def set_route_residency(self, resident: Optional[Sequence[int]], stream=None) -> None:
         if resident is None:

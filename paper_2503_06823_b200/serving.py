@@ -130,10 +130,30 @@ class MoEStack:
             hits[l] += layer.workspace()["route_hit"].sum()
 
 
+def dynamic_targets(demand: np.ndarray, resident: np.ndarray, budget: int):
+    """On-demand baseline for one layer (engine.cpp:469-497 dynamic_transfers):
+    keep the `budget` experts with the largest demand (stable: ascending index on
+    ties, experts without demand never kept); evict the other residents
+    (ascending), load the kept non-residents (ascending).  -> (evictions, loads)"""
+    ranked = sorted((e for e in range(len(demand)) if demand[e] > 0), key=lambda e: (-int(demand[e]), e))[:budget]
+    needed = set(ranked)
+    evictions = [int(e) for e in np.flatnonzero(resident) if e not in needed]
+    loads = [e for e in sorted(needed) if not resident[e]]
+    return evictions, loads
+
+
 def run_stream(stack: MoEStack, trace: np.ndarray, trace_dev: torch.Tensor, prompt_tasks: Sequence[str],
-               x: torch.Tensor, logits_of, first_prompt: int, n_prompts: int) -> dict:
+               x: torch.Tensor, logits_of, first_prompt: int, n_prompts: int, residency: str = "predicted") -> dict:
     """Serve prompts first_prompt .. first_prompt+n_prompts-1 of the trace.
-    logits_of(p) -> [m][T][E] fp32 device logits for prompt p."""
+    logits_of(p) -> [m][T][E] fp32 device logits for prompt p.
+    residency "predicted": the eMoE path above.  "dynamic": the reference's
+    on-demand baseline -- no predictor; before each
+    layer's forward the gate runs, the layer keeps the experts this prompt
+    demands most and loads the missing ones synchronously on the critical path."""
+    if residency not in ("predicted", "dynamic"):
+        raise ValueError("residency must be 'predicted' or 'dynamic'")
+    if residency == "dynamic":
+        return _run_stream_dynamic(stack, x, logits_of, first_prompt, n_prompts)
     cfg = stack.cfg
     T = cfg.tokens_per_prompt
     sensitive = {n: any(cfg.tasks[n].sensitivity) for n in stack.names}
@@ -174,11 +194,43 @@ def run_stream(stack: MoEStack, trace: np.ndarray, trace_dev: torch.Tensor, prom
     load_ms = sum(a.elapsed_time(b) for a, b in load_events)
     expert_bytes = (3 if cfg.activation == "swiglu" else 2) * cfg.d * cfg.f * 2
     load_bytes = stats["planned_loads"] * expert_bytes
-    stats.update(ms=ms, tokens=n_prompts * T, tokens_per_s=n_prompts * T / (ms / 1e3),
+    stats.update(residency="predicted", ms=ms, tokens=n_prompts * T, tokens_per_s=n_prompts * T / (ms / 1e3),
                  hit_rate=float(hits.sum().item()) / (n_prompts * T * cfg.m), load_ms=load_ms, load_bytes=load_bytes,
                  load_gbs=load_bytes / max(load_ms, 1e-9) / 1e6,
                  load_overlap="compute never waits on loads: each layer polls its batch without blocking")
     return stats
+
+
+def _run_stream_dynamic(stack: MoEStack, x: torch.Tensor, logits_of, first_prompt: int, n_prompts: int) -> dict:
+    cfg = stack.cfg
+    T = cfg.tokens_per_prompt
+    out = torch.empty_like(x)
+    hits = torch.zeros(cfg.m, dtype=torch.int64, device=x.device)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    loads_total, load_ms = 0, 0.0
+    torch.cuda.synchronize()
+    ev0.record()
+    for i in range(n_prompts):
+        lg = logits_of(first_prompt + i)
+        for l, layer in enumerate(stack.layers):
+            layer.route(logits=lg[l])
+            evictions, loads = dynamic_targets(layer.gate_demand(), layer.residency(), cfg.L)
+            if evictions or loads:
+                layer.begin_load(evictions, loads)
+                layer.poll_loads(blocking=True)  # on the critical path (engine.cpp:498-501)
+                loads_total += len(loads)
+                load_ms += layer.last_load_stats()[1]
+            layer.forward(x, logits=lg[l], out=out)
+            hits[l] += layer.workspace()["route_hit"].sum()
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    expert_bytes = (3 if cfg.activation == "swiglu" else 2) * cfg.d * cfg.f * 2
+    load_bytes = loads_total * expert_bytes
+    return dict(residency="dynamic", ms=ms, tokens=n_prompts * T, tokens_per_s=n_prompts * T / (ms / 1e3),
+                hit_rate=float(hits.sum().item()) / (n_prompts * T * cfg.m), planned_loads=loads_total,
+                load_ms=load_ms, load_bytes=load_bytes, load_gbs=load_bytes / max(load_ms, 1e-9) / 1e6,
+                load_overlap="none: every layer waits for its on-demand loads before computing")
 
 
 def moesim_prompt_sets(trace_dev: torch.Tensor, prompt: int):

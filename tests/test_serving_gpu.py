@@ -60,3 +60,53 @@ def test_stream_invocations_and_residency_match_oracle(port, ref):
     assert np.array_equal(got, resident)
     assert st["planned_loads"] > 0 and 0.0 < st["hit_rate"] <= 1.0
     stack.close()
+
+
+def _engine_dynamic_replay(trace, first, n, m, E, L, resident):
+    """engine.cpp:469-497 dynamic_transfers, restated for prompt batches: per layer,
+    demand = tokens per rank-0 choice; keep the top-L by demand (map order breaks
+    ties); evict the rest; load the missing.  Returns residency and load count."""
+    loads = 0
+    hits = 0
+    for q in range(first, first + n):
+        for l in range(m):
+            demand = np.bincount(trace[q, l, :, 0], minlength=E)
+            ranked = sorted([e for e in range(E) if demand[e] > 0], key=lambda e: (-demand[e], e))[:L]
+            loads += sum(1 for e in ranked if not resident[l, e])
+            resident[l] = 0
+            resident[l, ranked] = 1
+            hits += int(resident[l, trace[q, l, :, 0]].sum())
+    return resident, loads, hits
+
+
+def test_dynamic_residency_matches_engine_replay(ref):
+    from helpers import trace_logits
+    from paper_2503_06823_b200.serving import MoEStack, StreamConfig, TaskSpec, run_stream
+
+    m, E, k, L, d, f, T = 3, 8, 2, 3, 256, 512, 512
+    tasks = {"conv": TaskSpec(32.0, [1] * m)}
+    cfg = StreamConfig(m=m, E=E, k=k, L=L, d=d, f=f, tokens_per_prompt=T, period=4, mode=0, tasks=tasks)
+    P = 6
+    trace = ref.gen_routing_trace(m, E, k, 0.3, 0.3, 0, 23, P, T)
+    g = torch.Generator().manual_seed(5)
+    host = [tuple((torch.randn(*s, generator=g) / s[1] ** 0.5).to(torch.bfloat16).pin_memory()
+                  for s in ((f, d), (f, d), (d, f))) for _ in range(E)]
+    gates = [torch.zeros(E, d, dtype=torch.bfloat16) for _ in range(m)]
+    stack = MoEStack(cfg, host, gates)
+    for layer in stack.layers:
+        layer.load_initial(range(L))
+    logits = {q: torch.from_numpy(np.stack([trace_logits(trace[q, l], E, seed=q * 7 + l) for l in range(m)])).cuda()
+              for q in range(P)}
+    # the demand map read back from the GPU route is the rank-0 histogram of the trace
+    stack.layers[0].route(logits=logits[0][0])
+    assert np.array_equal(stack.layers[0].gate_demand(), np.bincount(trace[0, 0, :, 0], minlength=E))
+    x = torch.randn(T, d, generator=g).to(torch.bfloat16).cuda()
+    st = run_stream(stack, trace, None, ["conv"] * P, x, lambda q: logits[q], 0, P, residency="dynamic")
+    resident = np.zeros((m, E), np.uint8)
+    resident[:, :L] = 1
+    want, loads, hits = _engine_dynamic_replay(trace, 0, P, m, E, L, resident)
+    got = np.stack([layer.residency() for layer in stack.layers])
+    assert np.array_equal(got, want)
+    assert st["planned_loads"] == loads
+    assert st["hit_rate"] == pytest.approx(hits / (P * T * m), abs=0)
+    stack.close()
