@@ -233,6 +233,90 @@ def _run_stream_dynamic(stack: MoEStack, x: torch.Tensor, logits_of, first_promp
                 load_overlap="none: every layer waits for its on-demand loads before computing")
 
 
+def profile_cost_model(stack: MoEStack, x: torch.Tensor, logits: torch.Tensor, sets, requests,
+                       reps: int = 3) -> dict:
+    """The reference CostModel (cost_model.hpp:10-21; scenario JSON "cost" object,
+    scenario.cpp:252-260) measured on this GPU, i.e. the "profiled dE and c" the
+    scheduler's Eq. 3 / Alg. 1 and the engine's iteration clock consume
+    (engine.cpp:334, :545-546):
+      per_token_cost        c = seconds per token through all m layers (no loads);
+      hd_bandwidth          pinned host -> HBM expert copies on the copy stream;
+      per_expert_transfer   fixed cost per expert copy beyond bytes / bandwidth;
+      predictor_invocation_cost  one GPU invocation (predict .. plan_loading);
+      contention_factor     compute slowdown while expert copies are in flight.
+    logits: [m][T][E] routing-driven logits; sets/requests: an invocation's inputs.
+    Leaves every layer's residency as it found it."""
+    cfg = stack.cfg
+    T = x.shape[0]
+    out = torch.empty_like(x)
+    hits = torch.zeros(cfg.m, dtype=torch.int64, device=x.device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def stack_ms():
+        stack.forward_prompt(x, logits, out, hits)  # warm
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            stack.forward_prompt(x, logits, out, hits)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    base_ms = stack_ms()
+    # expert copies: swap one resident expert of layer 0 for a non-resident one and back
+    layer = stack.layers[0]
+    res = layer.residency()
+    r_in, r_out = int(np.flatnonzero(res)[0]), int(np.flatnonzero(res == 0)[0])
+    one = []
+    for ev, ld in [([r_in], [r_out]), ([r_out], [r_in])] * reps:
+        layer.begin_load(ev, ld)
+        layer.poll_loads(blocking=True)
+        one.append(layer.last_load_stats())
+    # a batch of all L residents of layer 0 (swapped out and back) for the bandwidth
+    resident = [int(e) for e in np.flatnonzero(res)]
+    others = [int(e) for e in np.flatnonzero(res == 0)][: len(resident)]
+    layer.begin_load(resident[: len(others)], others)
+    layer.poll_loads(blocking=True)
+    many = layer.last_load_stats()
+    layer.begin_load(others, resident[: len(others)])
+    layer.poll_loads(blocking=True)
+    many_back = layer.last_load_stats()
+    bw = (many[0] + many_back[0]) / ((many[1] + many_back[1]) / 1e3)
+    one_s = float(np.median([ms for _, ms in one])) / 1e3
+    setup = max(one_s - one[0][0] / bw, 1e-7)
+    # contention: a few forwards of layer 1 alone, then the same while layer 0's
+    # copies are in flight on the copy stream (the copies outlast them)
+    contention = 1.0
+    if cfg.m > 1:
+        probe = stack.layers[1]
+        n_fwd = 3
+        e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+        def probe_ms(copying: bool):
+            if copying:
+                layer.begin_load(resident[: len(others)], others)
+            e2.record()
+            for _ in range(n_fwd):
+                probe.forward(x, logits=logits[1], out=out)
+            e3.record()
+            torch.cuda.synchronize()
+            if copying:
+                layer.poll_loads(blocking=True)
+                layer.begin_load(others, resident[: len(others)])
+                layer.poll_loads(blocking=True)
+            return e2.elapsed_time(e3)
+
+        probe_ms(False)
+        contention = max(1.0, probe_ms(True) / probe_ms(False))
+    # one predictor invocation (host wall time, GPU kernels included)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        stack.invocation(sets, requests)
+    inv_s = (time.perf_counter() - t0) / reps
+    return dict(per_token_cost=base_ms / 1e3 / T, per_expert_transfer=setup, hd_bandwidth=bw,
+                predictor_invocation_cost=inv_s, contention_factor=contention)
+
+
 def moesim_prompt_sets(trace_dev: torch.Tensor, prompt: int):
     """dominant experts and prompt_expert_sets of one prompt of a device trace."""
     P, m, T, k = trace_dev.shape

@@ -110,3 +110,31 @@ def test_dynamic_residency_matches_engine_replay(ref):
     assert st["planned_loads"] == loads
     assert st["hit_rate"] == pytest.approx(hits / (P * T * m), abs=0)
     stack.close()
+
+
+def test_profile_cost_model_is_a_valid_reference_cost(ref):
+    """The measured CostModel satisfies CostModel::validate (types.cpp:7-14) and
+    leaves the stack's residency untouched."""
+    from helpers import trace_logits
+    from paper_2503_06823_b200.serving import MoEStack, StreamConfig, TaskSpec, profile_cost_model
+
+    m, E, k, L, d, f, T = 3, 8, 2, 4, 256, 512, 512
+    tasks = {"conv": TaskSpec(32.0, [1] * m)}
+    cfg = StreamConfig(m=m, E=E, k=k, L=L, d=d, f=f, tokens_per_prompt=T, period=4, mode=0, tasks=tasks)
+    trace = ref.gen_routing_trace(m, E, k, 0.6, 0.8, 0, 17, 12, T)
+    g = torch.Generator().manual_seed(9)
+    host = [tuple((torch.randn(*s, generator=g) / s[1] ** 0.5).to(torch.bfloat16).pin_memory()
+                  for s in ((f, d), (f, d), (d, f))) for _ in range(E)]
+    stack = MoEStack(cfg, host, [torch.zeros(E, d, dtype=torch.bfloat16) for _ in range(m)])
+    trace_dev = torch.from_numpy(trace).cuda()
+    stack.fit(trace_dev[:10].contiguous(), ["conv"] * 10)
+    for layer in stack.layers:
+        layer.load_initial(range(L))
+    before = np.stack([layer.residency() for layer in stack.layers])
+    lg = torch.from_numpy(np.stack([trace_logits(trace[11, l], E, seed=l) for l in range(m)])).cuda()
+    x = torch.randn(T, d, generator=g).to(torch.bfloat16).cuda()
+    cost = profile_cost_model(stack, x, lg, [[0, 1]] * m, [("conv", T)] * 4, reps=2)
+    assert cost["per_token_cost"] > 0 and cost["per_expert_transfer"] > 0 and cost["hd_bandwidth"] > 1e9
+    assert cost["predictor_invocation_cost"] > 0 and cost["contention_factor"] >= 1.0
+    assert np.array_equal(np.stack([layer.residency() for layer in stack.layers]), before)
+    stack.close()
