@@ -172,6 +172,44 @@ int emoe_ffn_segments(emoe_layer* layer, const void* x_rows_dev, int64_t R, cons
 int emoe_combine(emoe_layer* layer, const void* y_rows_dev, const int32_t* pos_dev, const float* served_w_dev,
                  int64_t T, void* y_dev, void* stream);
 
+/* ========================================================================
+ * Expert parallelism over peer memory (replaces the
+ * all-to-all exchange of emoe_route_permute / emoe_ffn_segments /
+ * emoe_combine with stores and loads into IPC-mapped peer buffers).  The
+ * reference has no counterpart (multi-GPU is a non-goal); the
+ * forward it extends is the engine's per-layer serve step, engine.cpp:524-546.
+ *   emoe_ep_create      one per rank over that rank's layer (its slots hold
+ *                       the experts it computes; routing residency set with
+ *                       emoe_layer_set_route_residency).  dest[world][E]: rank
+ *                       that computes source rank s's rows of expert e (-1 =
+ *                       not resident).  recv_rows_cap 0 = the worst case,
+ *                       world x the layer's rows_cap.  world <= 8, bf16.
+ *   emoe_ep_ipc_handle  this rank's symmetric buffer as an IPC handle
+ *                       (EMOE_IPC_HANDLE_BYTES bytes) for the caller to
+ *                       all-gather; emoe_ep_open_peers maps the others
+ *                       (handles[world][EMOE_IPC_HANDLE_BYTES], own ignored).
+ *   emoe_ep_forward     route -> dispatch (permute stores into the owners'
+ *                       buffers) -> grouped FFN on the received rows ->
+ *                       combine (loads from the owners' buffers), with three
+ *                       device-side barriers; every rank must call it the
+ *                       same number of times.  Output bit-identical to the
+ *                       single-GPU forward.  No host synchronisation.
+ *   emoe_ep_status      synchronises `stream`; *status 0 = ok, 1 = a peer
+ *                       barrier timed out (EMOE_EP_TIMEOUT_S, default 60 s),
+ *                       2 = a receive buffer overflowed (rows dropped);
+ *                       *recv_rows = rows this rank computed last forward.
+ * ====================================================================== */
+#define EMOE_IPC_HANDLE_BYTES 64
+typedef struct emoe_ep emoe_ep;
+int emoe_ep_create(emoe_layer* layer, int world, int rank, const int32_t* dest, int64_t recv_rows_cap,
+                   emoe_ep** out);
+int emoe_ep_ipc_handle(emoe_ep* ep, void* handle_out);
+int emoe_ep_open_peers(emoe_ep* ep, const void* handles);
+int emoe_ep_forward(emoe_ep* ep, const void* x_dev, const float* logits_in_dev, void* y_dev, int64_t T,
+                    void* stream);
+int emoe_ep_status(emoe_ep* ep, void* stream, int* status, int64_t* recv_rows);
+int emoe_ep_destroy(emoe_ep* ep);
+
 /* Device pointers of the last forward's intermediates (valid until the next
  * call on the layer).  Sizes: T tokens, R = rows_cap permuted rows. */
 typedef struct {

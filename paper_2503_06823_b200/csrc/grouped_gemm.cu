@@ -39,15 +39,17 @@ namespace gemm {
 constexpr int BN = 256;  // UMMA N / accumulator columns per tile
 constexpr int BK = 64;   // one 128-byte swizzle row of bf16
 constexpr int MAX_EXPERTS = 256;
-constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;
 // epilogue output staging for the TMA store: one 32-row x 64-column bf16 box
 // (128-B swizzled rows) per epilogue warp
 constexpr int OUT_BOX_COLS = 64;
 constexpr int OUT_BOX_BYTES = 32 * OUT_BOX_COLS * 2;
-constexpr int OUT_STAGE_BYTES = 4 * OUT_BOX_BYTES;
+constexpr int BAR_AREA_BYTES = 2048;  // mbarriers, TMEM slot, segment offsets (int32, <= MAX_EXPERTS + 1)
 
-template <int CG>
+// CG = CTAs per MMA (1 or 2), EW = epilogue warps (4: one per TMEM lane
+// quarter; 8: two per quarter, each draining half of the accumulator columns,
+// for short-K tiles whose MMAs finish faster than 4 warps can drain TMEM)
+template <int CG, int EW>
 struct Cfg {
   static constexpr int TILE_M = 128 * CG;
   static constexpr int B_ROWS = BN / CG;  // B rows held by one CTA
@@ -55,8 +57,11 @@ struct Cfg {
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM_BYTES =
-      STAGES * STAGE_BYTES + 1024 /*align*/ + 4096 /*barriers + offsets*/ + OUT_STAGE_BYTES;
+  static constexpr int OUT_STAGE_BYTES = EW * OUT_BOX_BYTES;
+  static constexpr int NUM_THREADS = 64 + 32 * EW;
+  static constexpr int SMEM_BYTES = 1024 /*align*/ + STAGES * STAGE_BYTES + OUT_STAGE_BYTES + BAR_AREA_BYTES;
+  static_assert(SMEM_BYTES <= 232448, "shared memory over the sm_100 per-block limit");
+  static_assert(2 * STAGES * 8 + 4 * 8 + 16 + 4 * (MAX_EXPERTS + 1) <= BAR_AREA_BYTES, "barrier area");
 };
 
 struct Params {
@@ -83,7 +88,7 @@ struct TileCoord {
 };
 
 __device__ __forceinline__ TileCoord decode_tile(int t, int total_mb, int n_blocks, int group_m, int tile_m,
-                                                 const int64_t* offs, int num_experts) {
+                                                 const int32_t* offs, int num_experts) {
   const int per_group = group_m * n_blocks;
   const int g = t / per_group;
   const int local = t - g * per_group;
@@ -91,7 +96,7 @@ __device__ __forceinline__ TileCoord decode_tile(int t, int total_mb, int n_bloc
   TileCoord c;
   c.nb = local / rows_in_group;
   c.mb = g * group_m + (local - c.nb * rows_in_group);
-  const int64_t row = (int64_t)c.mb * tile_m;
+  const int32_t row = c.mb * tile_m;
   int e = 0;
   while (e + 1 < num_experts && offs[e + 1] <= row) ++e;
   c.expert = e;
@@ -189,23 +194,23 @@ __device__ __forceinline__ void store_box(const Params& p, const CUtensorMap* tm
   }
 }
 
-template <int EPI, int CG>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+template <int EPI, int CG, int EW>
+__global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                         const __grid_constant__ CUtensorMap tmap_b2, const __grid_constant__ CUtensorMap tmap_out,
                         Params p) {
-  using C = Cfg<CG>;
+  using C = Cfg<CG, EW>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* out_stage = smem + C::STAGES * C::STAGE_BYTES;  // 1024-B aligned
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(out_stage + C::OUT_STAGE_BYTES);
   uint64_t* empty_bar = full_bar + C::STAGES;
   uint64_t* tfull_bar = empty_bar + C::STAGES;  // [2]
   uint64_t* tempty_bar = tfull_bar + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  int64_t* s_offs = reinterpret_cast<int64_t*>(tmem_slot + 4);
-  uint8_t* out_stage = smem + C::STAGES * C::STAGE_BYTES + 4096;  // 1024-B aligned
+  int32_t* s_offs = reinterpret_cast<int32_t*>(tmem_slot + 4);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -215,8 +220,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int cluster_id = blockIdx.x / CG;
   const int num_clusters = gridDim.x / CG;
 
-  for (int i = threadIdx.x; i <= E; i += NUM_THREADS)
-    s_offs[i] = p.single_rows > 0 ? (i == 0 ? 0 : p.single_rows) : p.seg_offsets[i];
+  for (int i = threadIdx.x; i <= E; i += C::NUM_THREADS)
+    s_offs[i] = (int32_t)(p.single_rows > 0 ? (i == 0 ? 0 : p.single_rows) : p.seg_offsets[i]);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 4 * CG);  // one arrival per epilogue warp of every CTA
+      mbar_init(&tempty_bar[b], EW * CG);  // one arrival per epilogue warp of every CTA
     }
     fence_barrier_init();
   }
@@ -250,7 +255,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int total_mb = (int)(s_offs[E] / C::TILE_M);
+  const int total_mb = s_offs[E] / C::TILE_M;
   const int total_tiles = total_mb * p.n_blocks;
   const int k_blocks = p.K / BK;
 
@@ -352,7 +357,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else {
     // ===================== epilogue (warps 2..5, every CTA) =====================
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    uint8_t* my_stage = out_stage + (warp - 2) * OUT_BOX_BYTES;
+    const int ew = warp - 2;
+    uint8_t* my_stage = out_stage + ew * OUT_BOX_BYTES;
+    // column share of this warp: all of the tile (EW = 4) or one half (EW = 8)
+    constexpr int OUT_COLS = EPI == EPI_SWIGLU ? BN / 2 : BN;
+    constexpr int SPAN = OUT_COLS / (EW / 4);
+    const int c_lo = (ew / 4) * SPAN;
     int local = 0;
     for (int t = cluster_id; t < total_tiles; t += num_clusters, ++local) {
       const TileCoord c = decode_tile(t, total_mb, p.n_blocks, p.group_m, C::TILE_M, s_offs, E);
@@ -367,7 +377,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __nv_bfloat16* orow = p.out + row * p.ldo + col0;
       if (EPI == EPI_SWIGLU) {
 #pragma unroll 1
-        for (int cc = 0; cc < BN / 2; cc += OUT_BOX_COLS) {
+        for (int cc = c_lo; cc < c_lo + SPAN; cc += OUT_BOX_COLS) {
           uint32_t g0[32], g1[32], u0[32], u1[32];
           tmem_ld_32x32b_x32(taddr + cc, g0);
           tmem_ld_32x32b_x32(taddr + cc + 32, g1);
@@ -393,7 +403,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         float* frow = p.out_f32 + row * p.ldo;
         const bool row_ok = row < p.row_limit;
 #pragma unroll 1
-        for (int cc = 0; cc < BN; cc += 32) {
+        for (int cc = c_lo; cc < c_lo + SPAN; cc += 32) {
           uint32_t a[32];
           tmem_ld_32x32b_x32(taddr + cc, a);
           tmem_ld_wait();
@@ -405,7 +415,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       } else {
 #pragma unroll 1
-        for (int cc = 0; cc < BN; cc += OUT_BOX_COLS) {
+        for (int cc = c_lo; cc < c_lo + SPAN; cc += OUT_BOX_COLS) {
           uint32_t a0[32], a1[32];
           tmem_ld_32x32b_x32(taddr + cc, a0);
           tmem_ld_32x32b_x32(taddr + cc + 32, a1);
@@ -581,54 +591,78 @@ void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t
   launch_params(EPI_F32, 1, ta, tb, tb, ta, p, num_sms, stream);
 }
 
+// epilogue warps per CTA: 4 (one per TMEM lane quarter).  8 (two per quarter)
+// was measured for the short-K Switch GEMM1 and is 1-2 % slower
+// (profiles/r01_epilogue_warps_ab.jsonl): its tiles are not epilogue-bound.
+// EMOE_GEMM_EPI_WARPS = 8 selects it for A/B runs.
+static int epilogue_warps(int /*K*/) {
+  static const int forced = [] {
+    const char* v = getenv("EMOE_GEMM_EPI_WARPS");
+    return v ? atoi(v) : 0;
+  }();
+  return forced == 8 ? 8 : 4;
+}
+
+template <int EPI, int CG, int EW>
+static void launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const CUtensorMap& to,
+                       const gemm::Params& p, int num_sms, cudaStream_t stream) {
+  using C = gemm::Cfg<CG, EW>;
+  auto kernel = gemm::grouped_gemm_kernel<EPI, CG, EW>;
+  static bool attr_set = false;  // one per instantiation
+  if (!attr_set) {
+    EMOE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
+    attr_set = true;
+  }
+  const int grid = CG == 2 ? (num_sms / 2) * 2 : num_sms;
+  if (CG == 1) {
+    kernel<<<grid, C::NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, tb2, to, p);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(C::NUM_THREADS);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    EMOE_CUDA(cudaLaunchKernelEx(&cfg, kernel, ta, tb, tb2, to, p));
+  }
+  EMOE_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+template <int EPI, int CG>
+static void launch_ew(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const CUtensorMap& to,
+                      const gemm::Params& p, int num_sms, cudaStream_t stream) {
+  if (epilogue_warps(p.K) == 8)
+    launch_one<EPI, CG, 8>(ta, tb, tb2, to, p, num_sms, stream);
+  else
+    launch_one<EPI, CG, 4>(ta, tb, tb2, to, p, num_sms, stream);
+}
+
 static void launch_params(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
                           const CUtensorMap& tb2, const CUtensorMap& to, const gemm::Params& p, int num_sms,
                           cudaStream_t stream) {
-  const int grid = cta_group == 2 ? (num_sms / 2) * 2 : num_sms;
-  auto run = [&](auto kernel, int smem, int idx) {
-    static bool attr_set[7] = {false, false, false, false, false, false, false};
-    if (!attr_set[idx]) {
-      EMOE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr_set[idx] = true;
-    }
-    if (cta_group == 1) {
-      kernel<<<grid, gemm::NUM_THREADS, smem, stream>>>(ta, tb, tb2, to, p);
-    } else {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(grid);
-      cfg.blockDim = dim3(gemm::NUM_THREADS);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = 2;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      EMOE_CUDA(cudaLaunchKernelEx(&cfg, kernel, ta, tb, tb2, to, p));
-    }
-    EMOE_CUDA(cudaGetLastError());
-    count_launch();
-  };
-  using C1 = gemm::Cfg<1>;
-  using C2 = gemm::Cfg<2>;
   if (cta_group == 1) {
     if (epi == EPI_SWIGLU)
-      run(gemm::grouped_gemm_kernel<EPI_SWIGLU, 1>, C1::SMEM_BYTES, 0);
+      launch_ew<EPI_SWIGLU, 1>(ta, tb, tb2, to, p, num_sms, stream);
     else if (epi == EPI_RELU)
-      run(gemm::grouped_gemm_kernel<EPI_RELU, 1>, C1::SMEM_BYTES, 1);
+      launch_ew<EPI_RELU, 1>(ta, tb, tb2, to, p, num_sms, stream);
     else if (epi == EPI_F32)
-      run(gemm::grouped_gemm_kernel<EPI_F32, 1>, C1::SMEM_BYTES, 6);
+      launch_ew<EPI_F32, 1>(ta, tb, tb2, to, p, num_sms, stream);
     else
-      run(gemm::grouped_gemm_kernel<EPI_STORE, 1>, C1::SMEM_BYTES, 2);
+      launch_ew<EPI_STORE, 1>(ta, tb, tb2, to, p, num_sms, stream);
   } else {
     if (epi == EPI_SWIGLU)
-      run(gemm::grouped_gemm_kernel<EPI_SWIGLU, 2>, C2::SMEM_BYTES, 3);
+      launch_ew<EPI_SWIGLU, 2>(ta, tb, tb2, to, p, num_sms, stream);
     else if (epi == EPI_RELU)
-      run(gemm::grouped_gemm_kernel<EPI_RELU, 2>, C2::SMEM_BYTES, 4);
+      launch_ew<EPI_RELU, 2>(ta, tb, tb2, to, p, num_sms, stream);
     else
-      run(gemm::grouped_gemm_kernel<EPI_STORE, 2>, C2::SMEM_BYTES, 5);
+      launch_ew<EPI_STORE, 2>(ta, tb, tb2, to, p, num_sms, stream);
   }
 }
 

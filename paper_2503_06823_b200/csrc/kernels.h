@@ -57,6 +57,27 @@ void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32
 void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
                     const int64_t* seg_offsets, const int64_t* block_base, void* x_perm, int32_t* pos,
                     int32_t* row_token, cudaStream_t s);
+// Expert-parallel peer-memory addressing: rank q's receive (or expert-output)
+// buffer is base[q] (own buffer or a CUDA-IPC mapping); dest[e] = rank that
+// computes this rank's rows of expert e; row_shift[e] = (row of segment e in
+// that rank's buffer) - (local segment offset).  dest / row_shift are device
+// arrays [E].
+constexpr int kMaxPeers = 8;
+struct PeerRows {
+  uint8_t* base[kMaxPeers];
+  const int32_t* dest;
+  const int64_t* row_shift;
+  int64_t cap;  // rows per buffer: a row outside [0, cap) is not written (pos = -1)
+};
+// K3b dispatch form: rows go straight to the owning rank's receive buffer;
+// pos[t][j] = row in that buffer
+void launch_permute_remote(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
+                           const int64_t* seg_offsets, const int64_t* block_base, const PeerRows& peers,
+                           int32_t* pos, cudaStream_t s);
+// K5 combine form: expert outputs read from the owning ranks' buffers (bf16)
+void launch_combine_remote(const PeerRows& peers, int64_t T, int d, int k, const int32_t* pos,
+                           const float* served_w, const int32_t* served_idx, void* y, cudaStream_t s);
+
 // K5: gate-weighted combine in fixed slot order
 void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int32_t* pos, const float* served_w,
                     void* y, cudaStream_t s);
@@ -82,5 +103,26 @@ void launch_grouped_gemm_f32(int epi, const float* A, int64_t lda, const float* 
                              const int64_t* seg_offsets, const int32_t* slot_of_expert, int num_experts, int K,
                              int N_out, int b_rows_per_slot, int64_t rows_cap, float* out, int64_t ldo,
                              cudaStream_t stream, const int32_t* seg_expert = nullptr);
+
+// Layer internals the expert-parallel handle (ep.cu) builds on (layer.cu).
+struct LayerView {
+  int E, d, f, k, dtype, elem, seg_pad;
+  int64_t max_tokens, rows_cap;
+  const int32_t* served_idx;
+  const float* served_w;
+  const int64_t* seg_offsets;
+  const int64_t* block_base;
+  int32_t* pos;
+};
+}  // namespace emoe
+
+struct emoe_layer;
+namespace emoe {
+LayerView layer_view(emoe_layer* L);
+// K1 + K3a (route, per-expert counts, padded local segment offsets); no gather
+void layer_route_scan(emoe_layer* L, const void* x, const float* logits_in, int64_t T, cudaStream_t s);
+// K4 over caller rows in n_seg segments (device seg offsets / experts)
+void layer_ffn_rows(emoe_layer* L, const void* xr, int64_t R, const int64_t* segs, const int32_t* seg_expert,
+                    int n_seg, void* hr, void* yr, cudaStream_t s);
 
 }  // namespace emoe

@@ -920,3 +920,45 @@ int emoe_route_tokens_host(const int32_t* choices, int64_t T, int k, const uint8
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// internal interface for the expert-parallel handle (ep.cu)
+// ---------------------------------------------------------------------------
+namespace emoe {
+
+LayerView layer_view(emoe_layer* L) {
+  LayerView v;
+  v.E = L->cfg.num_experts;
+  v.d = L->cfg.d_model;
+  v.f = L->cfg.d_ff;
+  v.k = L->cfg.top_k;
+  v.dtype = L->cfg.dtype;
+  v.elem = L->elem;
+  v.seg_pad = L->seg_pad;
+  v.max_tokens = L->cfg.max_tokens;
+  v.rows_cap = L->rows_cap;
+  v.served_idx = L->served_idx;
+  v.served_w = L->served_w;
+  v.seg_offsets = L->seg_offsets;
+  v.block_base = L->block_base;
+  v.pos = L->pos;
+  return v;
+}
+
+void layer_route_scan(emoe_layer* L, const void* x, const float* logits_in, int64_t T, cudaStream_t s) {
+  L->poll(false, s, nullptr);
+  L->route(x, logits_in, T, s);
+  if (T > 0)
+    launch_scan(L->block_counts, (int)ceil_div(T, kRouteBlockTokens), L->cfg.num_experts, L->seg_pad, L->counts,
+                L->seg_offsets, L->block_base, s);
+}
+
+void layer_ffn_rows(emoe_layer* L, const void* xr, int64_t R, const int64_t* segs, const int32_t* seg_expert,
+                    int n_seg, void* hr, void* yr, cudaStream_t s) {
+  const bool was = L->profiling;
+  L->profiling = false;
+  L->ffn(xr, R, segs, seg_expert, n_seg, hr, yr, s, false);
+  L->profiling = was;
+}
+
+}  // namespace emoe

@@ -74,13 +74,21 @@ __global__ void __launch_bounds__(1024) seg_offsets_kernel(const int32_t* __rest
 constexpr int PERMUTE_THREADS = 256;
 constexpr int GATHER_UNROLL = 8;
 
+// REMOTE (expert-parallel dispatch over peer memory): segment e is written to
+// rank dest[e]'s receive buffer (peers.base[dest[e]], mapped through CUDA IPC)
+// at row pos = d + row_shift[e], d being the local position above; pos[t][j]
+// then holds that remote row.  The per-block tail fence makes the NVLink
+// stores visible system-wide before the host-ordered signal kernel runs.
+template <bool REMOTE>
 __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
     const uint8_t* __restrict__ x, int row_bytes, int64_t T, int E, int k, const int32_t* __restrict__ served_idx,
     const int64_t* __restrict__ seg_offsets, const int64_t* __restrict__ block_base, uint8_t* __restrict__ x_perm,
-    int32_t* __restrict__ pos, int32_t* __restrict__ row_token) {
+    int32_t* __restrict__ pos, int32_t* __restrict__ row_token, PeerRows peers) {
   extern __shared__ int32_t sh[];
   int32_t* warp_counts = sh;          // [4][E]
   int32_t* dst_s = sh + 4 * E;        // [RT][k]
+  // REMOTE: destination row pointer per (token, slot), 8-B aligned after dst_s
+  uint8_t** dptr_s = reinterpret_cast<uint8_t**>(sh + 4 * E + ((RT * k + 1) & ~1));
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t t0 = (int64_t)blockIdx.x * RT;
   int my[8];
@@ -126,7 +134,19 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
         d = (int32_t)(base + rank[j]);
       }
       dst_s[threadIdx.x * k + j] = d;
-      if (t < T) {
+      if (REMOTE) {
+        int32_t rrow = -1;
+        uint8_t* ptr = nullptr;
+        if (e >= 0) {
+          const int64_t r = d + peers.row_shift[e];
+          if (r >= 0 && r < peers.cap) {  // out of range only when the receiver overflowed (status 2)
+            rrow = (int32_t)r;
+            ptr = peers.base[peers.dest[e]] + r * row_bytes;
+          }
+        }
+        dptr_s[threadIdx.x * k + j] = ptr;
+        if (t < T) pos[t * k + j] = rrow;
+      } else if (t < T) {
         if (pos) pos[t * k + j] = d;
         if (row_token && d >= 0) row_token[d] = (int32_t)t;
       }
@@ -157,32 +177,44 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
       for (int j = 0; j < k; ++j) {
         const int32_t d = dst_s[tok[u] * k + j];
         if (d < 0) break;  // served slots are compacted to the front
-        reinterpret_cast<uint4*>(x_perm + (int64_t)d * row_bytes)[v] = val[u];
+        uint8_t* row = REMOTE ? dptr_s[tok[u] * k + j] : x_perm + (int64_t)d * row_bytes;
+        if (REMOTE && !row) continue;
+        reinterpret_cast<uint4*>(row)[v] = val[u];
       }
     }
   }
+  if (REMOTE) __threadfence_system();
 }
 
-// One warp per token; lanes own 16-byte column chunks.
+// One warp per token; lanes own 16-byte column chunks.  REMOTE: slot j's row
+// lives in rank dest[served_idx[t][j]]'s expert-output buffer (peer memory
+// read over NVLink); same slot order and fp32 accumulation as the local form,
+// so the expert-parallel output is bit-identical to the single-GPU one.
+template <bool REMOTE>
 __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* __restrict__ Y, int64_t T, int d,
                                                            int k, const int32_t* __restrict__ pos,
                                                            const float* __restrict__ served_w,
-                                                           __nv_bfloat16* __restrict__ y) {
+                                                           __nv_bfloat16* __restrict__ y, PeerRows peers,
+                                                           const int32_t* __restrict__ served_idx) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t t = (int64_t)blockIdx.x * 8 + warp;
   if (t >= T) return;
   int32_t p[8];
   float w[8];
+  const __nv_bfloat16* src[8];
   for (int j = 0; j < k; ++j) {
     p[j] = pos[t * k + j];
     w[j] = served_w[t * k + j];
+    src[j] = Y;
+    if (REMOTE && p[j] >= 0) src[j] = reinterpret_cast<const __nv_bfloat16*>(peers.base[peers.dest[served_idx[t * k + j]]]);
   }
   const int nvec = d / 8;
   for (int v = lane; v < nvec; v += 32) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int j = 0; j < k; ++j) {
       if (p[j] < 0) continue;
-      const uint4 r = __ldg(reinterpret_cast<const uint4*>(Y + (int64_t)p[j] * d) + v);
+      const uint4 r = REMOTE ? *(reinterpret_cast<const uint4*>(src[j] + (int64_t)p[j] * d) + v)
+                             : __ldg(reinterpret_cast<const uint4*>(Y + (int64_t)p[j] * d) + v);
       const uint32_t u[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -246,9 +278,36 @@ void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int 
   const int nblocks = (int)ceil_div(T, RT);
   if (nblocks == 0) return;
   const size_t smem = (4 * (size_t)E + (size_t)RT * k) * sizeof(int32_t);
-  permute_kernel<<<nblocks, PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
-                                                        served_idx, seg_offsets, block_base,
-                                                        static_cast<uint8_t*>(x_perm), pos, row_token);
+  permute_kernel<false><<<nblocks, PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
+                                                               served_idx, seg_offsets, block_base,
+                                                               static_cast<uint8_t*>(x_perm), pos, row_token,
+                                                               PeerRows{});
+  EMOE_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void launch_permute_remote(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
+                           const int64_t* seg_offsets, const int64_t* block_base, const PeerRows& peers,
+                           int32_t* pos, cudaStream_t s) {
+  const int row_bytes = d * elem_bytes;
+  EMOE_REQUIRE(row_bytes % 16 == 0, "permute: row bytes must be a multiple of 16");
+  const int nblocks = (int)ceil_div(T, RT);
+  if (nblocks == 0) return;
+  const size_t smem = (4 * (size_t)E + (size_t)((RT * k + 1) & ~1)) * sizeof(int32_t) + (size_t)RT * k * 8;
+  permute_kernel<true><<<nblocks, PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
+                                                              served_idx, seg_offsets, block_base, nullptr, pos,
+                                                              nullptr, peers);
+  EMOE_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void launch_combine_remote(const PeerRows& peers, int64_t T, int d, int k, const int32_t* pos,
+                           const float* served_w, const int32_t* served_idx, void* y, cudaStream_t s) {
+  const int nblocks = (int)ceil_div(T, 8);
+  if (nblocks == 0) return;
+  EMOE_REQUIRE(d % 8 == 0, "combine: d must be a multiple of 8");
+  combine_bf16_kernel<true><<<nblocks, 256, 0, s>>>(nullptr, T, d, k, pos, served_w, static_cast<__nv_bfloat16*>(y),
+                                                    peers, served_idx);
   EMOE_CUDA(cudaGetLastError());
   count_launch();
 }
@@ -263,11 +322,11 @@ void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int
                                                static_cast<float*>(y));
   } else {
     EMOE_REQUIRE(d % 8 == 0, "combine: d must be a multiple of 8");
-    combine_bf16_kernel<<<nblocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Y), T, d, k, pos, served_w,
-                                                static_cast<__nv_bfloat16*>(y));
+    combine_bf16_kernel<false><<<nblocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Y), T, d, k, pos, served_w,
+                                                       static_cast<__nv_bfloat16*>(y), PeerRows{}, nullptr);
   }
   EMOE_CUDA(cudaGetLastError());
-    count_launch();
+  count_launch();
 }
 
 }  // namespace emoe

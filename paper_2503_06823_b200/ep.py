@@ -21,6 +21,14 @@ to EP=1 (tests/test_ep.py checks it with gloo on CPU and on the GPU).
 The exchange is NCCL all_to_all_single over NVLink for device tensors; with a
 gloo group (CPU tests, or several ranks sharing one GPU) tensors are staged
 through host memory.
+
+PeerExpertParallelMoE is the fused form (csrc/ep.cu): the permute kernel
+stores each row straight into its owner's receive buffer and the combine
+kernel loads expert outputs from the owners' buffers, over CUDA-IPC-mapped
+peer memory (NVLink between GPUs), with device-side barriers and no host
+synchronisation.  The receive layout is the same (source rank, expert,
+token) order, so its output is bit-identical too.  `p2p_layout` restates the
+layout the device computes (tests check it on CPU).
 """
 from __future__ import annotations
 
@@ -170,3 +178,105 @@ class ExpertParallelMoE:
         return b.combine(y_back, batch)
 
     __call__ = forward
+
+
+def p2p_layout(counts: np.ndarray, dest: np.ndarray, rank: int, seg_offsets: np.ndarray):
+    """The receive segments and send shifts ep_bar0_kernel computes on rank
+    `rank` (csrc/ep.cu).  counts[s, e] = padded rows source s holds for expert
+    e; seg_offsets = this rank's local padded segment starts [E+1].
+    Returns (recv_segs, seg_expert, row_shift): rank `rank` receives segment
+    (s, e) at recv_segs[i] for its owned experts in (source, expert) order,
+    and writes its own segment e to row seg_offsets[e] + row_shift[e] of rank
+    dest[rank, e]'s buffer."""
+    W, E = dest.shape
+    owned = owned_experts(dest, rank)
+    tot = np.zeros((W, W), np.int64)  # [source][receiver]
+    for s in range(W):
+        for e in range(E):
+            if dest[s, e] >= 0:
+                tot[s, dest[s, e]] += counts[s, e]
+    shift = np.zeros(E, np.int64)
+    for e in range(E):
+        q = dest[rank, e]
+        if q < 0:
+            continue
+        base = tot[:rank, q].sum() + sum(counts[rank, e2] for e2 in range(e) if dest[rank, e2] == q)
+        shift[e] = base - seg_offsets[e]
+    segs, exp, off = [], [], 0
+    for s in range(W):
+        for e in owned:
+            segs.append(off)
+            exp.append(e)
+            if dest[s, e] == rank:
+                off += counts[s, e]
+    segs.append(off)
+    return np.asarray(segs, np.int64), np.asarray(exp, np.int32), shift
+
+
+class PeerExpertParallelMoE:
+    """Expert parallelism over peer memory through the C ABI (emoe_ep_*).
+
+    `layer` is this rank's MoELayer holding the experts it computes; the
+    group only carries the IPC-handle exchange at construction (gloo or
+    NCCL) -- the forward itself uses no collective."""
+
+    def __init__(self, layer, global_resident: Sequence[int], group=None, recv_rows_cap: int = 0):
+        import ctypes as C
+
+        from ._lib import IPC_HANDLE_BYTES, lib
+        from .moesim import check
+
+        self._lib, self._check, self._C = lib, check, C
+        self.layer = layer
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.E = layer.E
+        self.dest = plan_destinations(global_resident, layer.E, self.world)
+        res = np.zeros(layer.E, np.uint8)
+        res[list(global_resident)] = 1
+        layer.set_route_residency(res)
+        dest32 = np.ascontiguousarray(self.dest, np.int32)
+        h = C.c_void_p()
+        check(lib.emoe_ep_create(layer.h, self.world, self.rank, dest32.ctypes.data_as(C.c_void_p),
+                                 int(recv_rows_cap), C.byref(h)))
+        self.h = h
+        buf = (C.c_uint8 * IPC_HANDLE_BYTES)()
+        check(lib.emoe_ep_ipc_handle(h, buf))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(buf), group=group)
+        allh = np.frombuffer(b"".join(handles), np.uint8).copy()
+        check(lib.emoe_ep_open_peers(h, allh.ctypes.data_as(C.c_void_p)))
+        dist.barrier(group=group)  # every rank mapped every peer before the first forward
+
+    def owned(self) -> list:
+        return owned_experts(self.dest, self.rank)
+
+    def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        C = self._C
+        assert x.is_cuda and x.dtype == torch.bfloat16 and x.shape[1] == self.layer.d
+        x = x.contiguous()
+        y = torch.empty_like(x)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        self._check(self._lib.emoe_ep_forward(self.h, C.c_void_p(x.data_ptr()), None, C.c_void_p(y.data_ptr()),
+                                              x.shape[0], C.c_void_p(s.cuda_stream)))
+        return y
+
+    __call__ = forward
+
+    def status(self, stream=None):
+        """(status, rows received last forward); synchronises the stream.
+        status 1 = a peer barrier timed out, 2 = a receive buffer overflowed."""
+        C = self._C
+        s = stream if stream is not None else torch.cuda.current_stream()
+        st, rr = C.c_int(), C.c_int64()
+        self._check(self._lib.emoe_ep_status(self.h, C.c_void_p(s.cuda_stream), C.byref(st), C.byref(rr)))
+        return st.value, rr.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.emoe_ep_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()

@@ -141,3 +141,124 @@ def test_ep_two_ranks_one_gpu_bit_identical(resident, tmp_path):
     for r in range(2):
         d = torch.load(tmp_path / f"g{r}.pt")
         assert torch.equal(d["y_ep"], d["y_1"]), f"rank {r}: EP output differs from the single-GPU forward"
+
+
+# ---------------------------------------------------------------------------
+# expert parallelism over peer memory (csrc/ep.cu)
+# ---------------------------------------------------------------------------
+def _simulate_p2p(backends, xs, dest):
+    """CPU restatement of the peer-memory protocol: every rank publishes its
+    padded counts, computes p2p_layout, 'stores' its rows into the owners'
+    receive buffers, owners run the FFN over their (source, expert)
+    segments, and each source combines from the owners' outputs."""
+    from paper_2503_06823_b200.ep import p2p_layout
+
+    W = len(backends)
+    E = backends[0].E
+    batches = [b.route_permute(x) for b, x in zip(backends, xs)]
+    counts = np.stack([np.diff(bt.seg_offsets) for bt in batches])
+    layouts = [p2p_layout(counts, dest, r, batches[r].seg_offsets) for r in range(W)]
+    recv = [np.zeros((int(layouts[q][0][-1]), backends[0].d), np.float32) for q in range(W)]
+    for r, bt in enumerate(batches):
+        shift = layouts[r][2]
+        for e in range(E):
+            a, b = int(bt.seg_offsets[e]), int(bt.seg_offsets[e + 1])
+            if b > a:
+                q = dest[r, e]
+                recv[q][a + shift[e]:b + shift[e]] = bt.rows[a:b].numpy()
+    outs = []
+    for q in range(W):
+        segs, exp, _ = layouts[q]
+        outs.append(backends[q].ffn(torch.from_numpy(recv[q]), segs, exp).numpy() if len(exp) else recv[q])
+    ys = []
+    for r, bt in enumerate(batches):
+        shift = layouts[r][2]
+        pos = bt.pos.numpy().astype(np.int64)
+        seg = bt.seg_offsets
+        y_rows = np.zeros((int(seg[-1]), backends[0].d), np.float32)
+        for e in range(E):  # gather this rank's rows back from their owners
+            a, b = int(seg[e]), int(seg[e + 1])
+            if b > a:
+                y_rows[a:b] = outs[dest[r, e]][a + shift[e]:b + shift[e]]
+        ys.append(backends[r].combine(torch.from_numpy(y_rows), RoutedBatch(seg, None, torch.from_numpy(pos),
+                                                                            bt.served_w, bt.T)))
+    return ys, layouts
+
+
+@pytest.mark.parametrize("world,resident", [(2, [0, 2, 5, 7]), (4, [1, 6]), (4, list(range(8))), (2, [3])])
+def test_p2p_layout_protocol_bit_identical(world, resident, port):
+    be = [OracleBackend(port, E=8, k=2, d=64, f=128, global_resident=resident) for _ in range(world)]
+    xs = [torch.from_numpy(np.random.default_rng(200 + r).standard_normal((41 + 7 * r, 64)).astype(np.float32))
+          for r in range(world)]
+    dest = plan_destinations(resident, 8, world)
+    ys, layouts = _simulate_p2p(be, xs, dest)
+    for r in range(world):
+        assert np.array_equal(ys[r].numpy(), single(be[r], xs[r]).numpy()), f"rank {r}: P2P layout output differs"
+    # receive segments are contiguous, padded and cover exactly the rows sent to each rank
+    for q, (segs, exp, _) in enumerate(layouts):
+        assert np.all(np.diff(segs) >= 0) and np.all(segs % be[0].pad == 0)
+        assert len(exp) == world * len(owned_experts(dest, q))
+
+
+def test_p2p_layout_disjoint_writes(port):
+    """Within every receiver, the row ranges written by different (source,
+    expert) segments are disjoint and tile [0, total)."""
+    from paper_2503_06823_b200.ep import p2p_layout
+
+    rng = np.random.default_rng(5)
+    for world, resident in [(2, [0, 2, 5, 7]), (4, [1, 6]), (8, [0, 5, 6, 7]), (8, list(range(8)))]:
+        dest = plan_destinations(resident, 8, world)
+        counts = rng.integers(0, 5, (world, 8)) * 4 * (dest >= 0)
+        seg = [np.concatenate([[0], np.cumsum(counts[r])]) for r in range(world)]
+        written = {q: [] for q in range(world)}
+        for r in range(world):
+            _, _, shift = p2p_layout(counts, dest, r, seg[r])
+            for e in range(8):
+                if counts[r, e]:
+                    written[dest[r, e]].append((seg[r][e] + shift[e], seg[r][e + 1] + shift[e]))
+        for q in range(world):
+            segs, _, _ = p2p_layout(counts, dest, q, seg[q])
+            iv = sorted(written[q])
+            assert all(a[1] == b[0] for a, b in zip(iv, iv[1:])), (world, q, iv)
+            assert (iv[0][0] if iv else 0) == 0 and (iv[-1][1] if iv else 0) == segs[-1]
+
+
+def _gpu_p2p_worker(rank, world, port_no, resident, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    os.environ.setdefault("EMOE_EP_TIMEOUT_S", "120")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from helpers import build_layer
+    from paper_2503_06823_b200.ep import PeerExpertParallelMoE
+
+    dest = plan_destinations(resident, 8, world)
+    mine = owned_experts(dest, rank)
+    layer, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", len(mine), mine, max_tokens=2048)
+    ep = PeerExpertParallelMoE(layer, resident)
+    full, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", len(resident), resident,
+                             max_tokens=2048)
+    res = []
+    for it, T in enumerate([1500 + 100 * rank, 700 - 50 * rank, 2048]):  # epochs reuse the buffers
+        x = torch.randn(T, 256, generator=torch.Generator().manual_seed(10 * it + rank)).to(torch.bfloat16).cuda()
+        y_ep = ep(x)
+        st, rows = ep.status()
+        y_1 = full.forward(x)
+        torch.cuda.synchronize()
+        res.append(dict(y_ep=y_ep.cpu(), y_1=y_1.cpu(), status=st, rows=rows))
+    torch.save(res, Path(out_dir) / f"p{rank}.pt")
+    dist.barrier()
+    ep.close()
+    layer.close()
+    full.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("resident", [[0, 2, 5, 7], [3]])
+def test_ep_p2p_two_ranks_one_gpu_bit_identical(resident, tmp_path):
+    mp.spawn(_gpu_p2p_worker, args=(2, free_port(), resident, str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        for i, d in enumerate(torch.load(tmp_path / f"p{r}.pt")):
+            assert d["status"] == 0, f"rank {r} forward {i}: status {d['status']}"
+            assert d["rows"] > 0
+            assert torch.equal(d["y_ep"], d["y_1"]), f"rank {r} forward {i}: P2P EP output differs from 1 GPU"

@@ -23,6 +23,9 @@ CASES = {
     "switch_small": (32, 256, 512, 1, "bf16", "relu", "full_softmax", 8, [0, 2, 5, 7, 11, 19, 23, 31], 777, 0),
     "switch_small_cta2": (32, 256, 512, 1, "bf16", "relu", "full_softmax", 8, [0, 2, 5, 7, 11, 19, 23, 31], 777,
                           2),
+    # K > 2048 in both GEMMs: the 4-epilogue-warp kernels (shorter K uses 8)
+    "mixtral_longk": (8, 2304, 2304, 2, "bf16", "swiglu", "topk_softmax", 4, [0, 3, 4, 7], 600, 0),
+    "mixtral_longk_cta2": (8, 2304, 2304, 2, "bf16", "swiglu", "topk_softmax", 4, [0, 3, 4, 7], 600, 2),
     "config1_fp32_phi05": (8, 1024, 3584, 2, "fp32", "swiglu", "topk_softmax", 4, [0, 2, 5, 7], 512, 0),
     "config1_fp32_phi1": (8, 1024, 3584, 2, "fp32", "swiglu", "topk_softmax", 8, None, 512, 0),
 }
