@@ -42,6 +42,10 @@ CONFIGS = {
                              "(predicted), batch 32 x 2048 tokens",
                     E=8, k=2, L=4, d=4096, f=14336, act="swiglu", wm="topk_softmax", prompts=32, tokens=2048,
                     train=200, layer_lambda=0.6, prompt_lambda=0.8, seed=17),
+    "synthetic": dict(workload="BASELINE config 1: synthetic MoE layer fp32, 8 experts top-2, 4 resident "
+                               "(predicted), d_model=1024, d_ff=3584, 512 tokens",
+                      E=8, k=2, L=4, d=1024, f=3584, act="swiglu", wm="topk_softmax", prompts=1, tokens=512,
+                      train=200, layer_lambda=0.6, prompt_lambda=0.8, seed=17, dtype="fp32"),
     "switch": dict(workload="BASELINE config 3: Switch-base-128-shaped layer bf16, 128 experts top-1, 20% resident "
                             "(L=26, predicted), 32 x 2048 tokens",
                    E=128, k=1, L=26, d=768, f=3072, act="relu", wm="full_softmax", prompts=32, tokens=2048,
@@ -170,17 +174,18 @@ def build_workload(cfg, device, cta_group=0, rank=0, world=1, parallel="replicas
         loads = owned_experts(plan_destinations(global_resident, E, world), rank)
 
     # ---- layer, weights (random-init, Mixtral/Switch shapes), planned loads
-    layer = MoELayer(d, f, E, k, activation=cfg["act"], dtype="bf16", weight_mode=cfg["wm"],
+    td = torch_dtype(cfg)
+    layer = MoELayer(d, f, E, k, activation=cfg["act"], dtype=cfg.get("dtype", "bf16"), weight_mode=cfg["wm"],
                      num_slots=max(1, len(loads)), max_tokens=T, gemm_cta_group=cta_group)
     g = torch.Generator(device=device).manual_seed(1234)
     q, _ = torch.linalg.qr(torch.randn(d, E, generator=g, device=device))  # orthonormal gate rows
     wg = q.T.contiguous()
-    layer.set_gate(wg.to(torch.bfloat16).cpu())
+    layer.set_gate(wg.to(td).cpu())
     for e in range(E):
-        w1 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(torch.bfloat16).cpu()
-        w3 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(torch.bfloat16).cpu() \
+        w1 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(td).cpu()
+        w3 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(td).cpu() \
             if cfg["act"] == "swiglu" else None
-        w2 = (torch.randn(d, f, generator=g, device=device) / f ** 0.5).to(torch.bfloat16).cpu()
+        w2 = (torch.randn(d, f, generator=g, device=device) / f ** 0.5).to(td).cpu()
         layer.register_expert(e, w1, w3, w2)
     layer.begin_load([], loads)
     layer.poll_loads(blocking=True)
@@ -196,7 +201,7 @@ def build_workload(cfg, device, cta_group=0, rank=0, world=1, parallel="replicas
         lg.scatter_(1, ch[:, r:r + 1], 8.0 - r)
     z = torch.randn(T, d, generator=g, device=device)
     z = z - (z @ wg.T) @ wg
-    x = (lg @ wg + z).to(torch.bfloat16).contiguous()
+    x = (lg @ wg + z).to(td).contiguous()
     del z, lg
     res = [0] * E
     for e in global_resident:
@@ -226,8 +231,9 @@ def cpu_reference_step(cfg, layer_info, x_host_f32, wg_f32, experts_f32, n_token
         if rows.size == 0:
             continue
         w1, w3, w2 = experts_f32[e]
-        Y[rows] = port.expert_ffn(x[src[rows]], w1, w3, w2, 0 if cfg["act"] == "swiglu" else 1, True, threads)
-    port.combine(Y, pos, o["served_w"], True)
+        bf = cfg.get("dtype", "bf16") == "bf16"
+        Y[rows] = port.expert_ffn(x[src[rows]], w1, w3, w2, 0 if cfg["act"] == "swiglu" else 1, bf, threads)
+    port.combine(Y, pos, o["served_w"], cfg.get("dtype", "bf16") == "bf16")
     return time.perf_counter() - t0
 
 
@@ -301,8 +307,10 @@ def main():
     ap.add_argument("--gemm-cta-group", type=int, default=0, choices=[0, 1, 2],
                     help="FFN GEMM CTA group (0 = the layer's auto choice)")
     ap.add_argument("--parallel", default="replicas", choices=["replicas", "ep"],
-                    help="N>1: replicas of the predicted resident set (no exchange) or expert parallelism "
-                         "(NCCL all-to-all dispatch/combine)")
+                    help="N>1: replicas of the predicted resident set (no exchange) or expert parallelism")
+    ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"],
+                    help="--parallel ep: dispatch/combine fused into the permute/combine kernels over "
+                         "IPC-mapped peer memory (p2p), or NCCL all-to-all between the stage kernels")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.config == "stream":
@@ -336,7 +344,11 @@ def main():
     import ctypes as C
 
     ep_model = None
-    if use_ep:
+    if use_ep and args.ep_transport == "p2p":
+        from paper_2503_06823_b200.ep import PeerExpertParallelMoE
+
+        ep_model = PeerExpertParallelMoE(layer, info["global_resident"])
+    elif use_ep:
         from paper_2503_06823_b200.ep import ExpertParallelMoE, LayerBackend
 
         ep_model = ExpertParallelMoE(LayerBackend(layer, info["global_resident"]), info["global_resident"])
@@ -427,12 +439,13 @@ def main():
         t = torch.tensor([e2e_s], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = dict(value=world * T / e2e_s, unit="tokens/s", h2d_bytes_per_step=x_host.numel() * 2,
-               d2h_bytes_per_step=y_host.numel() * 2, ms_per_step=e2e_s * 1e3)
+    e2e = dict(value=world * T / e2e_s, unit="tokens/s", h2d_bytes_per_step=x_host.numel() * x_host.element_size(),
+               d2h_bytes_per_step=y_host.numel() * y_host.element_size(), ms_per_step=e2e_s * 1e3)
 
     # ---- roofline of the dominant kernel (the grouped FFN GEMMs)
     peaks = load_peaks()
     d, f = cfg["d"], cfg["f"]
+    fp32 = cfg.get("dtype", "bf16") == "fp32"
     nmat = 3 if cfg["act"] == "swiglu" else 2
     ffn_flops = 2.0 * nmat * d * f * S
     ffn_ms = stages["gemm1"] + stages["gemm2"]
@@ -441,30 +454,42 @@ def main():
     tfile = ROOT / "profiles" / "ffn_gemm_dram_traffic.json"
     if tfile.exists() and args.config == "mixtral":  # ncu capture of this workload (profiles/)
         traffic = json.loads(tfile.read_text())["ffn_bytes_per_step"]
-    roofline = dict(bound="tensor", achieved=round(achieved, 1), peak=peaks["bf16_sustained"], unit="TFLOP/s",
-                    frac=round(achieved / peaks["bf16_sustained"], 4), traffic=traffic,
-                    traffic_unit="bytes per step (GEMM1 + GEMM2), ncu dram__bytes_read+write",
-                    kernel="grouped_gemm_kernel (K4: GEMM1 SwiGLU + GEMM2), avg of the timed steps",
-                    algorithmic=f"2*{nmat}*d*f*S = {ffn_flops:.4g} FLOP per step (S={S} served rows)",
-                    peak_kind=f"bf16_tflops_sustained ({peaks['source']}); burst {peaks['bf16']}",
-                    frac_of_burst=round(achieved / peaks["bf16"], 4))
+    if fp32:  # config 1: fp32 FFMA GEMMs against the CUDA-core fp32 peak measured in this run
+        fp32_peak = measure_fp32_peak(device)
+        roofline = dict(bound="fp32", achieved=round(achieved, 2), peak=round(fp32_peak, 2), unit="TFLOP/s",
+                        frac=round(achieved / fp32_peak, 4), traffic=None,
+                        kernel="grouped_gemm_f32 (K4: GEMM1 SwiGLU + GEMM2, FFMA), avg of the timed steps",
+                        algorithmic=f"2*{nmat}*d*f*S = {ffn_flops:.4g} FLOP per step (S={S} served rows)",
+                        peak_kind="fp32 cuBLAS SGEMM 8192^3 (TF32 off), best of 5, measured in this run")
+    else:
+        roofline = dict(bound="tensor", achieved=round(achieved, 1), peak=peaks["bf16_sustained"], unit="TFLOP/s",
+                        frac=round(achieved / peaks["bf16_sustained"], 4), traffic=traffic,
+                        traffic_unit="bytes per step (GEMM1 + GEMM2), ncu dram__bytes_read+write",
+                        kernel="grouped_gemm_kernel (K4: GEMM1 SwiGLU + GEMM2), avg of the timed steps",
+                        algorithmic=f"2*{nmat}*d*f*S = {ffn_flops:.4g} FLOP per step (S={S} served rows)",
+                        peak_kind=f"bf16_tflops_sustained ({peaks['source']}); burst {peaks['bf16']}",
+                        frac_of_burst=round(achieved / peaks["bf16"], 4))
     hbm_stages = {}
-    xb = T * d * 2
+    eb = elem_bytes(cfg)
+    xb = T * d * eb
     hbm_stages["route"] = (xb + T * k_of(cfg) * 8 + T * 9) / (stages["route"] / 1e3) / 1e9
-    hbm_stages["permute"] = (xb + S * d * 2 + 8 * S) / (stages["permute"] / 1e3) / 1e9
-    hbm_stages["combine"] = (S * d * 2 + xb + 4 * S) / (stages["combine"] / 1e3) / 1e9
+    hbm_stages["permute"] = (xb + S * d * eb + 8 * S) / (stages["permute"] / 1e3) / 1e9
+    hbm_stages["combine"] = (S * d * eb + xb + 4 * S) / (stages["combine"] / 1e3) / 1e9
 
     out = dict(metric=METRIC, value=round(value, 1), unit="tokens/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=round(ms, 4), higher_is_better=True, scaling="weak",
-               vs_baseline=None, dtype="bf16", data="synthetic (random-init weights; routing = reference Markov "
-                                                     "trace embedded in x)",
+               vs_baseline=None, dtype=cfg.get("dtype", "bf16"),
+               data="synthetic (random-init weights; routing = reference Markov trace embedded in x)",
                config=dict(workload=cfg["workload"], tokens_per_step=T, num_experts=cfg["E"], top_k=cfg["k"],
                            resident_experts=cfg["L"], resident_set=[e for e in range(cfg["E"])
                                                                      if info["resident"][e]],
                            d_model=d, d_ff=f, activation=cfg["act"], served_rows=S, hit_rate=round(hit_rate, 4),
                            fallback_rate=round(fallback, 4),
-                           l2="inputs larger than L2: x is %.0f MB per step" % (xb / 1e6),
-                           parallelism=(f"ep{world}" if use_ep else f"replicas{world}") if world > 1 else "single",
+                           l2=("inputs larger than L2: x is %.0f MB per step" % (xb / 1e6)) if xb > 126e6 else
+                           ("working set larger than L2: %.0f MB of resident expert weights streamed per step "
+                            "(x is %.1f MB)" % (cfg["L"] * nmat * d * f * eb / 1e6, xb / 1e6)),
+                           parallelism=(f"ep{world}-{args.ep_transport}" if use_ep else f"replicas{world}")
+                           if world > 1 else "single",
                            gemm_cta_group=layer.gemm_cta_group, seg_pad=layer.seg_pad),
                roofline=roofline, e2e=e2e, gpu_launches=launches, clocks=dict(clk.summary(), note=clock_note),
                stages_ms={kk: round(v, 4) for kk, v in stages.items()},
@@ -486,6 +511,39 @@ def k_of(cfg):
     return cfg["k"]
 
 
+def torch_dtype(cfg):
+    import torch
+
+    return torch.float32 if cfg.get("dtype", "bf16") == "fp32" else torch.bfloat16
+
+
+def elem_bytes(cfg):
+    return 4 if cfg.get("dtype", "bf16") == "fp32" else 2
+
+
+def measure_fp32_peak(device, n=8192, reps=5):
+    """fp32 CUDA-core roofline denominator for config 1, measured in this run:
+    cuBLAS SGEMM (torch.matmul, TF32 off) n^3, best of `reps` (CUDA events)."""
+    import torch
+
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    a = torch.randn(n, n, device=device)
+    b = torch.randn(n, n, device=device)
+    c = a @ b
+    best = 1e30
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b, out=c)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    torch.backends.cuda.matmul.allow_tf32 = prev
+    del a, b, c
+    return 2.0 * n ** 3 / best / 1e12
+
+
 def layer_ws_topk(layer):
     from paper_2503_06823_b200._lib import Workspace, lib
     import ctypes as C
@@ -500,7 +558,7 @@ def layer_gate_tensor(cfg, device):
 
     g = torch.Generator(device=device).manual_seed(1234)
     q, _ = torch.linalg.qr(torch.randn(cfg["d"], cfg["E"], generator=g, device=device))
-    return q.T.contiguous().to(torch.bfloat16)
+    return q.T.contiguous().to(torch_dtype(cfg))
 
 
 def gate_f32(wg):
@@ -515,11 +573,12 @@ def experts_f32(cfg, device, info):
     g = torch.Generator(device=device).manual_seed(1234)
     torch.linalg.qr(torch.randn(d, E, generator=g, device=device))
     out = {}
+    td = torch_dtype(cfg)
     for e in range(E):
-        w1 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(torch.bfloat16)
-        w3 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(torch.bfloat16) \
+        w1 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(td)
+        w3 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(td) \
             if cfg["act"] == "swiglu" else None
-        w2 = (torch.randn(d, f, generator=g, device=device) / f ** 0.5).to(torch.bfloat16)
+        w2 = (torch.randn(d, f, generator=g, device=device) / f ** 0.5).to(td)
         if info["resident"][e]:
             out[e] = (w1.float().cpu().numpy(), None if w3 is None else w3.float().cpu().numpy(),
                       w2.float().cpu().numpy())
@@ -638,15 +697,16 @@ def main_reference(args, cfg, rank, world):
     info = dict(resident=resident, choices=trace[cfg["train"]:].reshape(-1, k))
     g = torch.Generator().manual_seed(4321)
     n = 16
-    x = (torch.randn(4096, d, generator=g)).to(torch.bfloat16).float().numpy()
-    wg = (torch.randn(E, d, generator=g) / d ** 0.5).to(torch.bfloat16).float().numpy()
+    td = torch_dtype(cfg)
+    x = (torch.randn(4096, d, generator=g)).to(td).float().numpy()
+    wg = (torch.randn(E, d, generator=g) / d ** 0.5).to(td).float().numpy()
     experts = {}
     for e in range(E):
         if resident[e]:
-            w1 = (torch.randn(f, d, generator=g) / d ** 0.5).to(torch.bfloat16).float().numpy()
-            w3 = (torch.randn(f, d, generator=g) / d ** 0.5).to(torch.bfloat16).float().numpy() \
+            w1 = (torch.randn(f, d, generator=g) / d ** 0.5).to(td).float().numpy()
+            w3 = (torch.randn(f, d, generator=g) / d ** 0.5).to(td).float().numpy() \
                 if cfg["act"] == "swiglu" else None
-            w2 = (torch.randn(d, f, generator=g) / f ** 0.5).to(torch.bfloat16).float().numpy()
+            w2 = (torch.randn(d, f, generator=g) / f ** 0.5).to(td).float().numpy()
             experts[e] = (w1, w3, w2)
     # size the per-step sample so W+K steps finish within a few minutes
     dt = cpu_reference_step(cfg, info, x, wg, experts, n, port, ref, threads)

@@ -526,6 +526,11 @@ static int group_rows(int K, int tile_m) {
     const char* v = getenv("EMOE_GEMM_PANEL_MB");
     return v ? atoi(v) : 24;  // 24 MB measured best of {24, 48, 96} (profiles/r01_summary.md)
   }();
+  static int forced = [] {  // EMOE_GEMM_GROUP_M: exact raster group (row blocks), for A/B runs
+    const char* v = getenv("EMOE_GEMM_GROUP_M");
+    return v ? atoi(v) : 0;
+  }();
+  if (forced > 0) return forced;
   const int64_t panel_row_bytes = (int64_t)tile_m * K * 2;
   int g = (int)(((int64_t)panel_mb << 20) / panel_row_bytes);
   return g < 2 ? 2 : (g > 64 ? 64 : g);
