@@ -520,12 +520,16 @@ int gemm_tile_m(int cta_group) { return 128 * cta_group; }
 int gemm_b_box_rows(int epi, int cta_group) { return epi == EPI_SWIGLU ? 128 : 256 / cta_group; }
 
 // raster group: keep the A panel (group x tile_m rows x K) near `panel` MB of
-// L2 (default 24 MB of the 126 MB; EMOE_GEMM_PANEL_MB overrides for tuning)
+// L2: 24 MB for long reductions (Mixtral shape, K >= 2048: best of
+// 2/8/24/48/96 MB), 4 MB for short ones (Switch GEMM1, K = 768: 4-8 MB beat
+// 24 MB by 4 %, profiles/r01_raster_sweep.jsonl).  EMOE_GEMM_PANEL_MB
+// overrides for tuning.
 static int group_rows(int K, int tile_m) {
-  static int panel_mb = [] {
+  static int panel_env = [] {
     const char* v = getenv("EMOE_GEMM_PANEL_MB");
-    return v ? atoi(v) : 24;  // 24 MB measured best of {24, 48, 96} (profiles/r01_summary.md)
+    return v ? atoi(v) : 0;
   }();
+  const int panel_mb = panel_env > 0 ? panel_env : (K >= 2048 ? 24 : 4);
   static int forced = [] {  // EMOE_GEMM_GROUP_M: exact raster group (row blocks), for A/B runs
     const char* v = getenv("EMOE_GEMM_GROUP_M");
     return v ? atoi(v) : 0;

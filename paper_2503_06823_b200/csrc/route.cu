@@ -328,30 +328,62 @@ __global__ void __launch_bounds__(128) gate_route_bf16_kernel(const __nv_bfloat1
 // ---------------------------------------------------------------------------
 // fp32: warp-per-token FFMA gate, logits staged in shared memory
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) gate_route_f32_kernel(const float* __restrict__ x,
-                                                             const float* __restrict__ wg, RouteArgs a, RouteOut o) {
+// fp32 gate (config 1): 16 warps per 128-token block, 8 tokens per warp; each
+// lane keeps 8 experts' partial dot products over float4 slices of x and W_g
+// (x row read once per 8 experts), then a warp reduction per expert.
+constexpr int F32_GATE_THREADS = 512;
+__global__ void __launch_bounds__(F32_GATE_THREADS) gate_route_f32_kernel(const float* __restrict__ x,
+                                                                          const float* __restrict__ wg, RouteArgs a,
+                                                                          RouteOut o) {
   extern __shared__ __align__(128) uint8_t smem[];
   float* logits = reinterpret_cast<float*>(smem);  // [RT][E]
   __shared__ SharedRouteState st;
+  constexpr int NW = F32_GATE_THREADS / 32;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t t0 = (int64_t)blockIdx.x * RT;
-  for (int r = warp; r < RT; r += 4) {
+  const bool vec = (a.d & 3) == 0;
+  for (int r = warp; r < RT; r += NW) {
     const int64_t t = t0 + r;
     if (t >= a.T) break;
     const float* xr = x + t * a.d;
-    for (int e = 0; e < a.E; ++e) {
-      const float* wr = wg + (int64_t)e * a.d;
-      float s = 0.0f;
-      for (int i = lane; i < a.d; i += 32) s = fmaf(xr[i], wr[i], s);
+    for (int e0 = 0; e0 < a.E; e0 += 8) {
+      const int ne = min(8, a.E - e0);
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (vec) {
+        for (int i = lane * 4; i < a.d; i += 128) {
+          const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + i));
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      if (lane == 0) logits[r * a.E + e] = s;
+          for (int j = 0; j < 8; ++j) {
+            if (j < ne) {
+              const float4 wv = __ldg(reinterpret_cast<const float4*>(wg + (int64_t)(e0 + j) * a.d + i));
+              acc[j] = fmaf(xv.x, wv.x, acc[j]);
+              acc[j] = fmaf(xv.y, wv.y, acc[j]);
+              acc[j] = fmaf(xv.z, wv.z, acc[j]);
+              acc[j] = fmaf(xv.w, wv.w, acc[j]);
+            }
+          }
+        }
+      } else {
+        for (int i = lane; i < a.d; i += 32) {
+          const float xv = xr[i];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < ne) acc[j] = fmaf(xv, wg[(int64_t)(e0 + j) * a.d + i], acc[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float v = acc[j];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0 && j < ne) logits[r * a.E + e0 + j] = v;
+      }
     }
   }
   load_route_state(st, a);
   store_logits_tile(logits, a.E, t0, a, o);
   const int64_t t = t0 + threadIdx.x;
-  if (t < a.T) route_one_token(logits + threadIdx.x * a.E, t, a, o, st);
+  if (threadIdx.x < RT && t < a.T) route_one_token(logits + threadIdx.x * a.E, t, a, o, st);
   flush_block_counts(a, o, st);
 }
 
@@ -435,7 +467,7 @@ void launch_gate_route(const void* x, const void* wg, int dtype, const RouteArgs
   if (dtype == DT_F32) {
     const size_t smem = (size_t)RT * a.E * sizeof(float);
     EMOE_REQUIRE(smem <= 48 * 1024, "route: fp32 logits tile exceeds 48 KB");
-    gate_route_f32_kernel<<<nblocks, 128, smem, s>>>(static_cast<const float*>(x), static_cast<const float*>(wg), a,
+    gate_route_f32_kernel<<<nblocks, F32_GATE_THREADS, smem, s>>>(static_cast<const float*>(x), static_cast<const float*>(wg), a,
                                                      o);
   } else {
     EMOE_REQUIRE(a.d % KC == 0, "route: d_model must be a multiple of 64 for bf16");
