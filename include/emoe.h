@@ -230,7 +230,8 @@ typedef struct {
   int32_t* row_token;     /* [R] source token of each permuted row, -1 = padding */
   void* x_perm;           /* [R][d] */
   void* h;                /* [R][f] */
-  void* y_perm;           /* [R][d] */
+  void* y_perm;           /* [R][d]; NULL after a top-1 bf16 forward, whose
+                             GEMM2 epilogue writes y directly (fused combine) */
   int32_t* slot_of_expert; /* [E] HBM slot, -1 = not resident */
   uint8_t* resident;      /* [E] */
 } emoe_workspace;

@@ -81,6 +81,12 @@ struct Params {
   int64_t single_rows;  // > 0: one segment [0, single_rows) instead of seg_offsets
   int64_t ldo;
   int tma_store;        // bf16 epilogues: 1 = stage in smem + TMA bulk store, 0 = direct st.global
+  // EPI_STORE with the top-1 combine fused (K5 for k = 1): row r's output goes
+  // to scatter_out[scatter_tok[r]] scaled by scatter_w[token] (skipped when the
+  // token is -1, i.e. a padding row); null = store the permuted rows
+  const int32_t* scatter_tok;
+  const float* scatter_w;
+  __nv_bfloat16* scatter_out;
 };
 
 struct TileCoord {
@@ -413,6 +419,35 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
             for (int v = 0; v < 8; ++v) dst[v] = make_uint4(a[4 * v], a[4 * v + 1], a[4 * v + 2], a[4 * v + 3]);
           }
         }
+      } else if (EPI == EPI_STORE && p.scatter_tok != nullptr) {
+        // top-1 combine fused: y[t] = w_t * bf16(Y_row), the same two roundings
+        // as the separate combine (bit-identical), each lane's 128-B row
+        // chunk stored straight into its token's row
+        const int tok = p.scatter_tok[row];
+        const float w = tok >= 0 ? p.scatter_w[tok] : 0.0f;
+        __nv_bfloat16* yrow = p.scatter_out + (int64_t)(tok < 0 ? 0 : tok) * p.ldo + col0;
+#pragma unroll 1
+        for (int cc = c_lo; cc < c_lo + SPAN; cc += OUT_BOX_COLS) {
+          uint32_t a0[32], a1[32];
+          tmem_ld_32x32b_x32(taddr + cc, a0);
+          tmem_ld_32x32b_x32(taddr + cc + 32, a1);
+          tmem_ld_wait();
+          if (tok >= 0) {
+            uint4* dst = reinterpret_cast<uint4*>(yrow + cc);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              uint32_t q4[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int j = 4 * v + u, q = 2 * (j & 15);
+                const uint32_t y2 = pack_bf16x2(__uint_as_float(j < 16 ? a0[q] : a1[q]),
+                                                __uint_as_float(j < 16 ? a0[q + 1] : a1[q + 1]));
+                q4[u] = pack_bf16x2(w * bf16_lo(y2), w * bf16_hi(y2));
+              }
+              dst[v] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+            }
+          }
+        }
       } else {
 #pragma unroll 1
         for (int cc = c_lo; cc < c_lo + SPAN; cc += OUT_BOX_COLS) {
@@ -547,8 +582,10 @@ static void launch_params(int epi, int cta_group, const CUtensorMap& ta, const C
 void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
-                         int num_sms, cudaStream_t stream, const int32_t* seg_expert, const CUtensorMap* tmap_out) {
+                         int num_sms, cudaStream_t stream, const int32_t* seg_expert, const CUtensorMap* tmap_out,
+                         const ScatterCombine* scatter) {
   EMOE_REQUIRE(num_experts <= gemm::MAX_EXPERTS, "grouped_gemm: too many segments");
+  EMOE_REQUIRE(!scatter || epi == EPI_STORE, "grouped_gemm: the fused combine needs the GEMM2 epilogue");
   EMOE_REQUIRE(K % gemm::BK == 0, "grouped_gemm: K must be a multiple of 64");
   EMOE_REQUIRE(cta_group == 1 || cta_group == 2, "grouped_gemm: cta_group must be 1 or 2");
   gemm::Params p;
@@ -568,7 +605,10 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
   p.row_limit = 0;
   p.col_limit = 0;
   p.single_rows = 0;
-  p.tma_store = tmap_out != nullptr && tma_store_enabled();
+  p.tma_store = tmap_out != nullptr && tma_store_enabled() && !scatter;
+  p.scatter_tok = scatter ? scatter->row_token : nullptr;
+  p.scatter_w = scatter ? scatter->weight : nullptr;
+  p.scatter_out = scatter ? scatter->y : nullptr;
   launch_params(epi, cta_group, ta, tb, tb2, p.tma_store ? *tmap_out : ta, p, num_sms, stream);
 }
 
@@ -597,6 +637,9 @@ void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t
   p.col_limit = col_limit;
   p.single_rows = ceil_div(M, 128) * 128;
   p.tma_store = 0;
+  p.scatter_tok = nullptr;
+  p.scatter_w = nullptr;
+  p.scatter_out = nullptr;
   launch_params(EPI_F32, 1, ta, tb, tb, ta, p, num_sms, stream);
 }
 

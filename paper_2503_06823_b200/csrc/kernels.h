@@ -87,11 +87,18 @@ CUtensorMap make_tmap_bf16_2d(const void* base, uint64_t rows, uint64_t cols, ui
 CUtensorMap make_tmap_bf16_store(const void* base, uint64_t rows, uint64_t cols);  // epilogue store target
 int gemm_tile_m(int cta_group);                 // segment padding the kernel needs
 int gemm_b_box_rows(int epi, int cta_group);    // TMA box rows of the weight operand
+// top-1 combine fused into GEMM2's epilogue: y[row_token[r]] = weight[token] * Y[r]
+struct ScatterCombine {
+  const int32_t* row_token;  // [R], -1 = padding row
+  const float* weight;       // [T] (served_w with k = 1)
+  __nv_bfloat16* y;          // [T][ldo]
+};
 void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
                          int num_sms, cudaStream_t stream, const int32_t* seg_expert = nullptr,
-                         const CUtensorMap* tmap_out = nullptr);  // null: direct st.global epilogue
+                         const CUtensorMap* tmap_out = nullptr,  // null: direct st.global epilogue
+                         const ScatterCombine* scatter = nullptr);
 
 // K1 for many experts: the gate as one dense tcgen05 GEMM with fp32 output,
 // out[M][ldo] = A[M][K] . B[N_out][K]^T, columns >= col_limit (multiple of 32) not stored

@@ -244,10 +244,29 @@ struct emoe_layer {
     mark(1, s);
     permute(x, T, s);
     mark(2, s);
-    ffn(x_perm, rows_cap, seg_offsets, nullptr, cfg.num_experts, h, y_perm, s, true);
-    launch_combine(y_perm, cfg.dtype, T, cfg.d_model, cfg.top_k, pos, served_w, y, s);
+    if (fused_combine()) {  // top-1: GEMM2's epilogue writes y directly (K5 fused)
+      const ScatterCombine sc{row_token, served_w, static_cast<__nv_bfloat16*>(y)};
+      ffn(x_perm, rows_cap, seg_offsets, nullptr, cfg.num_experts, h, y_perm, s, true, &sc);
+      y_perm_valid = false;
+    } else {
+      ffn(x_perm, rows_cap, seg_offsets, nullptr, cfg.num_experts, h, y_perm, s, true);
+      launch_combine(y_perm, cfg.dtype, T, cfg.d_model, cfg.top_k, pos, served_w, y, s);
+      y_perm_valid = true;
+    }
     mark(5, s);
   }
+
+  // top-1 bf16 layers without forced misses serve every token exactly once, so
+  // the combine is a scaled row scatter GEMM2's epilogue can do
+  // (EMOE_FUSED_COMBINE=0 keeps the separate K5 for A/B runs)
+  bool fused_combine() const {
+    static const bool on = [] {
+      const char* v = getenv("EMOE_FUSED_COMBINE");
+      return !(v && v[0] == '0');
+    }();
+    return on && cfg.dtype == EMOE_DTYPE_BF16 && cfg.top_k == 1 && !cfg.forced_miss;
+  }
+  bool y_perm_valid = true;
 
   // A3 after route(): per-expert offsets, positions, gathered rows in x_perm
   void permute(const void* x, int64_t T, cudaStream_t s) {
@@ -262,7 +281,7 @@ struct emoe_layer {
   // A4 over rows [R][d] in n_seg padded segments (seg_expert null: segment i = expert i).
   // workspace = the rows are the layer's own x_perm/h/y_perm (cached tensor maps).
   void ffn(const void* xr, int64_t R, const int64_t* segs, const int32_t* seg_expert, int n_seg, void* hr, void* yr,
-           cudaStream_t s, bool workspace) {
+           cudaStream_t s, bool workspace, const ScatterCombine* scatter = nullptr) {
     const int d = cfg.d_model, f = cfg.d_ff;
     if (cfg.dtype == EMOE_DTYPE_BF16) {
       CUtensorMap a1 = ta1, a2 = ta2, o1 = to1, o2 = to2;
@@ -276,7 +295,7 @@ struct emoe_layer {
                           static_cast<__nv_bfloat16*>(hr), f, num_sms, s, seg_expert, &o1);
       mark(3, s);
       launch_grouped_gemm(EPI_STORE, cta_group, a2, tb2, tb2, segs, slot_dev, n_seg, f, d, d,
-                          static_cast<__nv_bfloat16*>(yr), d, num_sms, s, seg_expert, &o2);
+                          static_cast<__nv_bfloat16*>(yr), d, num_sms, s, seg_expert, &o2, scatter);
       mark(4, s);
     } else {
       launch_grouped_gemm_f32(swiglu() ? EPI_SWIGLU : EPI_RELU, static_cast<const float*>(xr), d,
@@ -816,7 +835,7 @@ int emoe_layer_workspace(emoe_layer* L, emoe_workspace* w) {
     w->row_token = L->row_token;
     w->x_perm = L->x_perm;
     w->h = L->h;
-    w->y_perm = L->y_perm;
+    w->y_perm = L->y_perm_valid ? L->y_perm : nullptr;  // null: GEMM2 wrote y directly (top-1 fused combine)
     w->slot_of_expert = L->slot_dev;
     w->resident = L->resident_dev;
   });

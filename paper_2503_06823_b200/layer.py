@@ -236,7 +236,7 @@ class MoELayer:
             "row_token": _view(w.row_token, (R,), torch.int32),
             "x_perm": _view(w.x_perm, (R, self.d), self.torch_dtype),
             "h": _view(w.h, (R, self.f), self.torch_dtype),
-            "y_perm": _view(w.y_perm, (R, self.d), self.torch_dtype),
+            "y_perm": _view(w.y_perm, (R, self.d), self.torch_dtype) if w.y_perm else None,
             "slot_of_expert": _view(w.slot_of_expert, (E,), torch.int32),
             "resident": _view(w.resident, (E,), torch.uint8),
         }

@@ -48,7 +48,7 @@ def run_case(name, port, use_trace_logits=False, scores=None):
         logits_in = torch.from_numpy(trace_logits(choices, E)).cuda()
     y = layer.forward(xd, logits=logits_in)
     torch.cuda.synchronize()
-    ws = {key: v.clone() for key, v in layer.workspace().items()}
+    ws = {key: (None if v is None else v.clone()) for key, v in layer.workspace().items()}
     res = layer.residency()
     return dict(layer=layer, wg=wg, experts=experts, x=x, y=y, ws=ws, resident=res, T=T, E=E, d=d, f=f, k=k,
                 dtype=dtype, act=act, wm=wm, logits_in=logits_in)
@@ -87,8 +87,10 @@ def check_case(c, port, scores=None):
     assert torch.equal(xp[valid], c["x"][src[valid]]), "permuted rows differ from their source rows"
     # A4 expert FFN on sampled rows of every active expert (mirrored rounding)
     rng = np.random.default_rng(0)
-    yp = to_f32(ws["y_perm"][:R])
     bf = c["dtype"] == "bf16"
+    fused = ws["y_perm"] is None  # top-1: GEMM2's epilogue wrote y directly (fused combine)
+    yp = None if fused else to_f32(ws["y_perm"][:R])
+    y32 = to_f32(c["y"])
     for e in range(E):
         rows = np.arange(offsets[e], offsets[e] + counts[e])
         if rows.size == 0:
@@ -96,10 +98,17 @@ def check_case(c, port, scores=None):
         pick = rng.choice(rows, size=min(12, rows.size), replace=False)
         w1, w3, w2 = (None if w is None else to_f32(w) for w in c["experts"][e])
         ref = port.expert_ffn(x32[src[pick]], w1, w3, w2, 0 if c["act"] == "swiglu" else 1, bf)
-        (assert_bf16_close if bf else assert_f32_close)(yp[pick], ref, f"expert {e} FFN rows")
+        if fused:  # the sampled rows' tokens: y[t] = bf16(w_t * Y_row)
+            from oracle.oracle import bf16_round
+
+            w = o["served_w"][src[pick], 0].astype(np.float32)[:, None]
+            assert_bf16_close(y32[src[pick]], bf16_round(w * ref), f"expert {e} FFN rows (fused combine)")
+        else:
+            (assert_bf16_close if bf else assert_f32_close)(yp[pick], ref, f"expert {e} FFN rows")
     # A5 combine of the GPU expert outputs
-    yc = port.combine(yp, pos, ws["served_w"].cpu().numpy(), bf)
-    (assert_bf16_close if bf else assert_f32_close)(to_f32(c["y"]), yc, "combine")
+    if not fused:
+        yc = port.combine(yp, pos, ws["served_w"].cpu().numpy(), bf)
+        (assert_bf16_close if bf else assert_f32_close)(to_f32(c["y"]), yc, "combine")
     # end to end on sampled tokens: oracle FFN for each served slot + oracle combine
     toks = rng.choice(T, size=min(16, T), replace=False)
     yref = np.zeros((toks.size, d), np.float32)
@@ -240,3 +249,38 @@ def test_forward_host_async_pipelined_calls():
     for x, y in zip(xs, ys):
         assert torch.equal(layer.forward(x.cuda()).cpu(), y)
     layer.close()
+
+
+_FUSED_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+from helpers import build_layer
+E, d, f, cg, T = {args!r}
+layer, _, _ = build_layer(E, d, f, 1, "bf16", "relu", "full_softmax", 8, [0, 2, 5, 7, 11, 19, 23, 31][:8],
+                          max_tokens=T, gemm_cta_group=cg)
+x = torch.randn(T, d, generator=torch.Generator().manual_seed(3)).to(torch.bfloat16).cuda()
+y = layer.forward(x)
+torch.save(dict(y=y.cpu(), fused=layer.workspace()["y_perm"] is None), {out!r})
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [(32, 256, 512, 1, 777), (32, 256, 512, 2, 777), (32, 768, 1024, 2, 3001)])
+def test_top1_fused_combine_bit_identical(args, tmp_path):
+    """Top-1 layers: GEMM2's epilogue scattering w_t * Y_row into y (default)
+    is bit-identical to GEMM2 + the separate combine (EMOE_FUSED_COMBINE=0)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    outs = []
+    for flag in ("1", "0"):
+        out = tmp_path / f"y{flag}.pt"
+        code = _FUSED_SCRIPT.format(root=str(root), tests=str(root / "tests"), args=args, out=str(out))
+        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, EMOE_FUSED_COMBINE=flag),
+                       timeout=300)
+        outs.append(torch.load(out))
+    assert outs[0]["fused"] and not outs[1]["fused"]
+    assert torch.equal(outs[0]["y"], outs[1]["y"])
