@@ -454,7 +454,20 @@ def main():
     tfile = ROOT / "profiles" / "ffn_gemm_dram_traffic.json"
     if tfile.exists() and args.config == "mixtral":  # ncu capture of this workload (profiles/)
         traffic = json.loads(tfile.read_text())["ffn_bytes_per_step"]
-    if fp32:  # config 1: fp32 FFMA GEMMs against the CUDA-core fp32 peak measured in this run
+    if fp32 and layer.fp32_tensor_core:
+        # config 1 on tcgen05 3xTF32: three TF32 MMAs per fp32 product, so the
+        # roofline is a third of the TF32 tensor peak measured in this run
+        tf32_peak = measure_tf32_peak(device)
+        fp32_peak = measure_fp32_peak(device)
+        roofline = dict(bound="tensor", achieved=round(achieved, 2), peak=round(tf32_peak / 3, 2), unit="TFLOP/s",
+                        frac=round(achieved / (tf32_peak / 3), 4), traffic=None,
+                        kernel="gemm_tf32x3_kernel (K4: GEMM1 SwiGLU + GEMM2, 3xTF32 on tcgen05), avg of the "
+                               "timed steps",
+                        algorithmic=f"2*{nmat}*d*f*S = {ffn_flops:.4g} fp32 FLOP per step (S={S} served rows)",
+                        peak_kind="TF32 cuBLAS 8192^3 / 3 (three TF32 products per fp32 product), measured in this "
+                                  f"run: TF32 {tf32_peak:.1f} TFLOP/s",
+                        fp32_ffma_peak=round(fp32_peak, 2), frac_of_fp32_ffma_peak=round(achieved / fp32_peak, 4))
+    elif fp32:  # SIMT FFMA kernel against the CUDA-core fp32 peak measured in this run
         fp32_peak = measure_fp32_peak(device)
         roofline = dict(bound="fp32", achieved=round(achieved, 2), peak=round(fp32_peak, 2), unit="TFLOP/s",
                         frac=round(achieved / fp32_peak, 4), traffic=None,
@@ -519,6 +532,28 @@ def torch_dtype(cfg):
 
 def elem_bytes(cfg):
     return 4 if cfg.get("dtype", "bf16") == "fp32" else 2
+
+
+def measure_tf32_peak(device, n=8192, reps=5):
+    """TF32 tensor-core peak (cuBLAS, torch.matmul with TF32 on), best of `reps`."""
+    import torch
+
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    a = torch.randn(n, n, device=device)
+    b = torch.randn(n, n, device=device)
+    c = a @ b
+    best = 1e30
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b, out=c)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    torch.backends.cuda.matmul.allow_tf32 = prev
+    del a, b, c
+    return 2.0 * n ** 3 / best / 1e12
 
 
 def measure_fp32_peak(device, n=8192, reps=5):

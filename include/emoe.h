@@ -234,6 +234,7 @@ typedef struct {
                              GEMM2 epilogue writes y directly (fused combine) */
   int32_t* slot_of_expert; /* [E] HBM slot, -1 = not resident */
   uint8_t* resident;      /* [E] */
+  int64_t fp32_tensor_core; /* fp32 layer: 1 = FFN GEMMs on tcgen05 (3xTF32), 0 = SIMT FFMA */
 } emoe_workspace;
 int emoe_layer_workspace(emoe_layer* layer, emoe_workspace* out);
 

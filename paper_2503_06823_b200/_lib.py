@@ -34,7 +34,7 @@ class Workspace(C.Structure):
     _fields_ = [("T", i64), ("rows_cap", i64), ("seg_pad", i64), ("gemm_cta_group", i64), ("logits", vp), ("topk_idx", vp), ("route_expert", vp),
                 ("route_rank", vp), ("route_hit", vp), ("served_idx", vp), ("served_w", vp), ("counts", vp),
                 ("seg_offsets", vp), ("pos", vp), ("row_token", vp), ("x_perm", vp), ("h", vp), ("y_perm", vp),
-                ("slot_of_expert", vp), ("resident", vp)]
+                ("slot_of_expert", vp), ("resident", vp), ("fp32_tensor_core", i64)]
 
 
 def _decl(name, *argtypes):

@@ -105,7 +105,25 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
 void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int K, int N_out, float* out,
                            int64_t ldo, int col_limit, int num_sms, cudaStream_t stream);
 
-// K4 fp32 path (SIMT FFMA): same grouping/epilogues, fp32 in/out
+// K4 fp32 path on tensor cores (3xTF32, grouped_gemm_tf32.cu): operands
+// pre-split into tf32 hi and fp32 lo parts; tensor maps from make_tmap_f32_2d
+// (box = 32 fp32 x box_rows, 128-B swizzle)
+struct Tf32Operands {
+  CUtensorMap a_hi, a_lo, b_hi, b_lo, b2_hi, b2_lo;  // b2: SwiGLU W3 (else = b)
+};
+CUtensorMap make_tmap_f32_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+bool gemm_tf32x3_supported(int epi, int K, int N_out);
+int gemm_tf32x3_b_box_rows(int epi);
+// x -> tf32(x) in hi (hi may alias x), x - tf32(x) in lo; n % 4 == 0
+void launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t s);
+// GEMM1 (SwiGLU/ReLU): out_hi/out_lo = split(H); GEMM2 (STORE): out_hi = Y
+void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t* seg_offsets,
+                                const int32_t* slot_of_expert, const int32_t* seg_expert, int n_seg, int K, int N_out,
+                                int b_rows_per_slot, float* out_hi, float* out_lo, int64_t ldo, int num_sms,
+                                cudaStream_t stream);
+
+// K4 fp32 path (SIMT FFMA): same grouping/epilogues, fp32 in/out (shapes the
+// 3xTF32 kernel does not tile)
 void launch_grouped_gemm_f32(int epi, const float* A, int64_t lda, const float* B, const float* B2,
                              const int64_t* seg_offsets, const int32_t* slot_of_expert, int num_experts, int K,
                              int N_out, int b_rows_per_slot, int64_t rows_cap, float* out, int64_t ldo,

@@ -118,6 +118,23 @@ struct emoe_layer {
 
   CUtensorMap ta1{}, tb1{}, tb3{}, ta2{}, tb2{}, to1{}, to2{};
 
+  // fp32 layers on tensor cores (3xTF32, grouped_gemm_tf32.cu): the slot
+  // pools hold tf32(W) in place and W - tf32(W) in the *_lo twins (split on
+  // load); GEMM1 reads x split into x_hi / x_lo and writes H as h (hi) + h_lo
+  bool tf32 = false;
+  void* w1_lo = nullptr;
+  void* w3_lo = nullptr;
+  void* w2_lo = nullptr;
+  float* x_hi = nullptr;
+  float* x_lo = nullptr;
+  float* h_lo = nullptr;
+  Tf32Operands op1{}, op2{};
+  // growable scratch for emoe_ffn_segments on caller rows (fp32)
+  float* sx_hi = nullptr;
+  float* sx_lo = nullptr;
+  float* sh_lo = nullptr;
+  int64_t s_rows = 0;
+
   size_t w1_elems() const { return (size_t)cfg.d_ff * cfg.d_model; }
   size_t w2_elems() const { return (size_t)cfg.d_model * cfg.d_ff; }
   bool swiglu() const { return cfg.activation == EMOE_ACT_SWIGLU; }
@@ -297,6 +314,34 @@ struct emoe_layer {
       launch_grouped_gemm(EPI_STORE, cta_group, a2, tb2, tb2, segs, slot_dev, n_seg, f, d, d,
                           static_cast<__nv_bfloat16*>(yr), d, num_sms, s, seg_expert, &o2, scatter);
       mark(4, s);
+    } else if (tf32) {
+      const int epi1 = swiglu() ? EPI_SWIGLU : EPI_RELU;
+      float *xh = x_hi, *xl = x_lo, *hl = h_lo;
+      Tf32Operands o1 = op1, o2 = op2;
+      if (!workspace) {  // caller rows: split into the growable scratch
+        if (R > s_rows) {
+          for (float* q : {sx_hi, sx_lo, sh_lo})
+            if (q) EMOE_CUDA(cudaFree(q));
+          sx_hi = dmalloc<float>((size_t)R * d);
+          sx_lo = dmalloc<float>((size_t)R * d);
+          sh_lo = dmalloc<float>((size_t)R * f);
+          s_rows = R;
+        }
+        xh = sx_hi;
+        xl = sx_lo;
+        hl = sh_lo;
+        o1.a_hi = make_tmap_f32_2d(xh, (uint64_t)R, d, 128);
+        o1.a_lo = make_tmap_f32_2d(xl, (uint64_t)R, d, 128);
+        o2.a_hi = make_tmap_f32_2d(hr, (uint64_t)R, f, 128);
+        o2.a_lo = make_tmap_f32_2d(hl, (uint64_t)R, f, 128);
+      }
+      launch_split_tf32(static_cast<const float*>(xr), xh, xl, R * d, s);
+      launch_grouped_gemm_tf32x3(epi1, o1, segs, slot_dev, seg_expert, n_seg, d, f, f, static_cast<float*>(hr), hl,
+                                 f, num_sms, s);
+      mark(3, s);
+      launch_grouped_gemm_tf32x3(EPI_STORE, o2, segs, slot_dev, seg_expert, n_seg, f, d, d, static_cast<float*>(yr),
+                                 nullptr, d, num_sms, s);
+      mark(4, s);
     } else {
       launch_grouped_gemm_f32(swiglu() ? EPI_SWIGLU : EPI_RELU, static_cast<const float*>(xr), d,
                               static_cast<const float*>(w1_pool), static_cast<const float*>(w3_pool), segs, slot_dev,
@@ -443,6 +488,16 @@ struct emoe_layer {
       EMOE_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(w2_pool) + slot * b2, host_w2[e], b2, cudaMemcpyHostToDevice,
                                 cs));
       pending_bytes += (double)b2;
+      if (tf32) {  // tf32 hi in place + fp32 lo twin, on the copy stream before the load event
+        auto split = [&](void* pool, void* lo, size_t elems) {
+          float* w = reinterpret_cast<float*>(static_cast<uint8_t*>(pool) + slot * elems * 4);
+          launch_split_tf32(w, w, reinterpret_cast<float*>(static_cast<uint8_t*>(lo) + slot * elems * 4),
+                            (int64_t)elems, cs);
+        };
+        split(w1_pool, w1_lo, w1_elems());
+        if (swiglu()) split(w3_pool, w3_lo, w1_elems());
+        split(w2_pool, w2_lo, w2_elems());
+      }
       pending_experts.push_back(e);
       pending_slots.push_back(slot);
     }
@@ -462,7 +517,8 @@ struct emoe_layer {
                     (void*)logits, (void*)topk, (void*)r_expert, (void*)r_rank, (void*)r_hit, (void*)served_idx,
                     (void*)served_w, (void*)block_counts, (void*)counts, (void*)seg_offsets, (void*)block_base,
                     (void*)pos, (void*)row_token, x_perm, h, y_perm, x_in, y_out, (void*)err_flag, x_stage[0],
-                    x_stage[1], y_stage[0], y_stage[1]})
+                    x_stage[1], y_stage[0], y_stage[1], w1_lo, w3_lo, w2_lo, (void*)x_hi, (void*)x_lo,
+                    (void*)h_lo, (void*)sx_hi, (void*)sx_lo, (void*)sh_lo})
       f(p);
     for (auto* v : {&host_w1, &host_w3, &host_w2})
       for (size_t e = 0; e < v->size(); ++e)
@@ -576,6 +632,40 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
         L->tb2 = make_tmap_bf16_2d(L->w2_pool, (uint64_t)c.num_slots * d, f, gemm_b_box_rows(EPI_STORE, L->cta_group));
         L->to1 = make_tmap_bf16_store(L->h, L->rows_cap, f);
         L->to2 = make_tmap_bf16_store(L->y_perm, L->rows_cap, d);
+      } else {
+        // fp32: 3xTF32 on tcgen05 where the shape tiles (EMOE_F32_GEMM=ffma keeps the SIMT kernel)
+        const char* mode = getenv("EMOE_F32_GEMM");
+        const int epi1 = L->swiglu() ? EPI_SWIGLU : EPI_RELU;
+        const uint64_t d = c.d_model, f = c.d_ff, slots = c.num_slots;
+        L->tf32 = !(mode && std::strcmp(mode, "ffma") == 0) && gemm_tf32x3_supported(epi1, (int)d, (int)f) &&
+                  gemm_tf32x3_supported(EPI_STORE, (int)f, (int)d);
+        if (L->tf32) {
+          const size_t pw1 = slots * L->w1_elems() * 4, pw2 = slots * L->w2_elems() * 4;
+          L->w1_lo = dmalloc<uint8_t>(pw1);
+          EMOE_CUDA(cudaMemset(L->w1_lo, 0, pw1));
+          if (L->swiglu()) {
+            L->w3_lo = dmalloc<uint8_t>(pw1);
+            EMOE_CUDA(cudaMemset(L->w3_lo, 0, pw1));
+          }
+          L->w2_lo = dmalloc<uint8_t>(pw2);
+          EMOE_CUDA(cudaMemset(L->w2_lo, 0, pw2));
+          L->x_hi = dmalloc<float>((size_t)L->rows_cap * d);
+          L->x_lo = dmalloc<float>((size_t)L->rows_cap * d);
+          L->h_lo = dmalloc<float>((size_t)L->rows_cap * f);
+          const uint32_t bb = gemm_tf32x3_b_box_rows(epi1), bb2 = gemm_tf32x3_b_box_rows(EPI_STORE);
+          L->op1.a_hi = make_tmap_f32_2d(L->x_hi, L->rows_cap, d, 128);
+          L->op1.a_lo = make_tmap_f32_2d(L->x_lo, L->rows_cap, d, 128);
+          L->op1.b_hi = make_tmap_f32_2d(L->w1_pool, slots * f, d, bb);
+          L->op1.b_lo = make_tmap_f32_2d(L->w1_lo, slots * f, d, bb);
+          L->op1.b2_hi = L->swiglu() ? make_tmap_f32_2d(L->w3_pool, slots * f, d, bb) : L->op1.b_hi;
+          L->op1.b2_lo = L->swiglu() ? make_tmap_f32_2d(L->w3_lo, slots * f, d, bb) : L->op1.b_lo;
+          L->op2.a_hi = make_tmap_f32_2d(L->h, L->rows_cap, f, 128);
+          L->op2.a_lo = make_tmap_f32_2d(L->h_lo, L->rows_cap, f, 128);
+          L->op2.b_hi = make_tmap_f32_2d(L->w2_pool, slots * d, f, bb2);
+          L->op2.b_lo = make_tmap_f32_2d(L->w2_lo, slots * d, f, bb2);
+          L->op2.b2_hi = L->op2.b_hi;
+          L->op2.b2_lo = L->op2.b_lo;
+        }
       }
       EMOE_CUDA(cudaDeviceSynchronize());
     } catch (...) {
@@ -838,6 +928,7 @@ int emoe_layer_workspace(emoe_layer* L, emoe_workspace* w) {
     w->y_perm = L->y_perm_valid ? L->y_perm : nullptr;  // null: GEMM2 wrote y directly (top-1 fused combine)
     w->slot_of_expert = L->slot_dev;
     w->resident = L->resident_dev;
+    w->fp32_tensor_core = L->tf32 ? 1 : 0;
   });
 }
 

@@ -222,6 +222,7 @@ class MoELayer:
         T, R, E, k = w.T, w.rows_cap, self.E, self.k
         self.seg_pad = int(w.seg_pad)
         self.gemm_cta_group = int(w.gemm_cta_group)
+        self.fp32_tensor_core = bool(w.fp32_tensor_core)
         return {
             "logits": _view(w.logits, (T, E), torch.float32),
             "topk_idx": _view(w.topk_idx, (T, k), torch.int32),

@@ -28,6 +28,7 @@ CASES = {
     "mixtral_longk_cta2": (8, 2304, 2304, 2, "bf16", "swiglu", "topk_softmax", 4, [0, 3, 4, 7], 600, 2),
     "config1_fp32_phi05": (8, 1024, 3584, 2, "fp32", "swiglu", "topk_softmax", 4, [0, 2, 5, 7], 512, 0),
     "config1_fp32_phi1": (8, 1024, 3584, 2, "fp32", "swiglu", "topk_softmax", 8, None, 512, 0),
+    "fp32_relu_top1": (16, 256, 512, 1, "fp32", "relu", "full_softmax", 8, [0, 2, 5, 7, 9, 11, 13, 15], 500, 0),
 }
 
 
