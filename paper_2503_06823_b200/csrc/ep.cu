@@ -1,32 +1,38 @@
-// Expert parallelism over peer memory: token dispatch fused
-// into the permute kernel (NVLink stores straight into the owning rank's
-// receive buffer) and the combine reading expert outputs from the owning
-// ranks' buffers (NVLink loads).  No all-to-all, no host synchronisation.
+// Expert parallelism over peer memory: the token dispatch is
+// fused into the permute kernel (NVLink stores straight into the owning
+// rank's receive buffer) and the return into GEMM2's epilogue (each expert
+// output row stored straight into its source rank's own permuted layout), so
+// the combine runs locally.  No all-to-all, no host synchronisation.
 //
 // Every rank allocates one symmetric region (same size everywhere) and maps
 // every peer's region through CUDA IPC:
-//   flags   u64 [3 phases][kMaxPeers]   epoch written by each source rank
-//   cnt     i32 [kMaxPeers][E]          padded segment sizes of every source
-//   recv_x  bf16 [recv_cap][d]          rows dispatched to this rank
-//   recv_y  bf16 [recv_cap][d]          this rank's expert outputs for them
+//   flags    u64 [3 phases][kMaxPeers]   epoch written by each source rank
+//   cnt      i32 [kMaxPeers][E]          padded segment sizes of every source
+//   recv_x   bf16 [recv_cap][d]          rows dispatched to this rank
+//   y_local  bf16 [rows_cap][d]          expert outputs of this rank's own rows,
+//                                        in its local permuted layout
 // One forward, all on the caller's stream:
 //   K1 + K3a  route and scan locally (layer_route_scan)
 //   bar0      publish this rank's padded counts to every peer, signal, wait
-//             for all ranks, then compute the receive segments and, per
-//             local expert, the row shift into its owner's receive buffer
+//             for all ranks, then derive from the replicated count table the
+//             receive segments, per local expert the row shift into its
+//             owner's receive buffer, and per receive segment the row shift
+//             back into its source's layout
 //   K3b       permute_kernel<REMOTE>: rows -> owner's recv_x (peer stores)
 //   bar1      signal + wait: every source finished writing to this rank
-//   K4        grouped GEMMs over the (source, expert) segments of recv_x
-//   bar2      signal + wait: every rank's expert outputs are complete
-//   K5        combine_bf16_kernel<REMOTE>: y[t] = sum_j w_j Y_owner[row]
+//   K4        grouped GEMMs over the (source, expert) segments of recv_x;
+//             GEMM2's epilogue pushes each row to its source's y_local
+//   bar2      signal + wait: every rank's pushes have landed
+//   K5        combine_bf16_kernel over the local y_local (slot order)
 // Receive layout on rank q: segments ordered by (source rank, expert), the
-// same order the NCCL path (ep.py) uses, so rows meet the same GEMM tiles'
-// arithmetic and the output is bit-identical to EP=1.
+// same order the NCCL path (ep.py) uses; every row meets the same GEMM
+// arithmetic and the combine order is fixed at the source, so the output is
+// bit-identical to EP=1.
 // Buffer reuse across forwards needs no extra barrier: a source writes cnt /
 // recv_x of forward n+1 only after its own bar2 of forward n, which every
-// rank reaches only after its layout reads of forward n; rank q's GEMM of
-// n+1 overwrites recv_y only after bar1 of n+1, i.e. after every peer
-// finished its combine of n.
+// rank reaches only after its layout reads of forward n; GEMM2 of forward
+// n+1 pushes into a source's y_local only after bar1 of n+1, i.e. after every
+// rank finished its combine of forward n.
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -90,6 +96,7 @@ struct LayoutArgs {
   int64_t recv_cap;
   int64_t* recv_segs;  // [W * n_owned + 1]
   int64_t* row_shift;  // [E]
+  int64_t* out_shift;  // [W * n_owned] receive row -> row in the source's layout
   int64_t* recv_rows;  // [1]
 };
 
@@ -140,14 +147,20 @@ __global__ void __launch_bounds__(256) ep_bar0_kernel(PeerSym sym, int W, int ra
       if (a.dest[rank * E + e2] == q) base += cnt[rank * E + e2];
     a.row_shift[e] = base - a.seg_offsets[e];
   }
-  // receive segments: (source, owned expert) in order
+  // receive segments: (source, owned expert) in order; the return shift maps
+  // receive row r of segment (s, e) to row r + shift of source s's layout
+  // (its padded segment e starts at the exclusive prefix of its counts)
   if (threadIdx.x == 0) {
     int64_t off = 0;
     int i = 0;
     for (int s = 0; s < W; ++s)
       for (int j = 0; j < a.n_owned; ++j) {
         const int e = a.owned[j];
-        a.recv_segs[i++] = off;
+        int64_t src_off = 0;
+        for (int e2 = 0; e2 < e; ++e2) src_off += cnt[s * E + e2];
+        a.recv_segs[i] = off;
+        a.out_shift[i] = src_off - off;
+        ++i;
         if (a.dest[s * E + e] == rank) off += cnt[s * E + e];
       }
     a.recv_segs[i] = off;
@@ -185,7 +198,7 @@ struct emoe_ep {
   uint64_t timeout_ns = 0;
 
   uint8_t* sym = nullptr;  // own symmetric region
-  size_t sym_bytes = 0, off_cnt = 0, off_x = 0, off_y = 0;
+  size_t sym_bytes = 0, off_cnt = 0, off_x = 0, off_y = 0;  // off_y: y_local
   uint8_t* peer[kMaxPeers] = {};  // symmetric regions of every rank (own = sym)
   bool opened = false;
 
@@ -194,6 +207,8 @@ struct emoe_ep {
   int64_t* row_shift = nullptr;
   int64_t* recv_segs = nullptr;
   int32_t* seg_expert = nullptr;  // [W * n_owned]
+  int32_t* seg_rank = nullptr;    // [W * n_owned] source rank of each receive segment
+  int64_t* out_shift = nullptr;   // [W * n_owned]
   int64_t* recv_rows = nullptr;
   int* status = nullptr;
   void* h = nullptr;
@@ -223,7 +238,7 @@ struct emoe_ep {
       EMOE_CUDA(cudaMemsetAsync(const_cast<int64_t*>(v.seg_offsets), 0, sizeof(int64_t) * (v.E + 1), s));
     }
     const int n_owned = (int)owned.size();
-    LayoutArgs a{v.seg_offsets, dest_dev, owned_dev, n_owned, recv_cap, recv_segs, row_shift, recv_rows};
+    LayoutArgs a{v.seg_offsets, dest_dev, owned_dev, n_owned, recv_cap, recv_segs, row_shift, out_shift, recv_rows};
     const PeerSym ps = peer_sym();
     ep_bar0_kernel<<<1, 256, 0, s>>>(ps, W, rank, v.E, epoch, timeout_ns, status, a);
     EMOE_CUDA(cudaGetLastError());
@@ -231,19 +246,24 @@ struct emoe_ep {
                           v.pos, s);
     ep_bar_kernel<<<1, 32, 0, s>>>(ps, W, rank, 1, epoch, timeout_ns, status);
     EMOE_CUDA(cudaGetLastError());
-    if (n_owned > 0)
-      layer_ffn_rows(layer, sym + off_x, recv_cap, recv_segs, seg_expert, W * n_owned, h, sym + off_y, s);
+    if (n_owned > 0) {
+      PeerOut po{};
+      for (int q = 0; q < W; ++q) po.base[q] = peer[q] + off_y;
+      po.seg_rank = seg_rank;
+      po.seg_shift = out_shift;
+      layer_ffn_rows(layer, sym + off_x, recv_cap, recv_segs, seg_expert, W * n_owned, h, sym + off_y, s, &po);
+    }
     ep_bar_kernel<<<1, 32, 0, s>>>(ps, W, rank, 2, epoch, timeout_ns, status);
     EMOE_CUDA(cudaGetLastError());
     count_launch(3);
-    launch_combine_remote(rows(off_y), T, v.d, v.k, v.pos, v.served_w, v.served_idx, y, s);
+    launch_combine(sym + off_y, DT_BF16, T, v.d, v.k, v.pos, v.served_w, y, s);
   }
 
   void destroy() {
     for (int q = 0; q < W; ++q)
       if (peer[q] && peer[q] != sym) cudaIpcCloseMemHandle(peer[q]);
     for (void* p : {(void*)sym, (void*)dest_dev, (void*)owned_dev, (void*)row_shift, (void*)recv_segs,
-                    (void*)seg_expert, (void*)recv_rows, (void*)status, h})
+                    (void*)seg_expert, (void*)seg_rank, (void*)out_shift, (void*)recv_rows, (void*)status, h})
       if (p) cudaFree(p);
   }
 };
@@ -286,7 +306,7 @@ int emoe_ep_create(emoe_layer* layer, int world, int rank, const int32_t* dest, 
       ep->off_cnt = align256(sizeof(uint64_t) * kPhases * kMaxPeers);
       ep->off_x = align256(ep->off_cnt + sizeof(int32_t) * kMaxPeers * E);
       ep->off_y = align256(ep->off_x + (size_t)ep->recv_cap * row);
-      ep->sym_bytes = align256(ep->off_y + (size_t)ep->recv_cap * row);
+      ep->sym_bytes = align256(ep->off_y + (size_t)v.rows_cap * row);
       ep->sym = dmalloc<uint8_t>(ep->sym_bytes);
       EMOE_CUDA(cudaMemset(ep->sym, 0, ep->sym_bytes));
       ep->dest_dev = dmalloc<int32_t>(dv.size());
@@ -298,9 +318,17 @@ int emoe_ep_create(emoe_layer* layer, int world, int rank, const int32_t* dest, 
       const int n_seg = world * (int)owned.size();
       ep->recv_segs = dmalloc<int64_t>(n_seg + 1);
       ep->seg_expert = dmalloc<int32_t>(std::max(1, n_seg));
-      std::vector<int32_t> se;
-      for (int s = 0; s < world; ++s) se.insert(se.end(), owned.begin(), owned.end());
-      if (n_seg) EMOE_CUDA(cudaMemcpy(ep->seg_expert, se.data(), se.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+      ep->seg_rank = dmalloc<int32_t>(std::max(1, n_seg));
+      ep->out_shift = dmalloc<int64_t>(std::max(1, n_seg));
+      std::vector<int32_t> se, sr;
+      for (int s = 0; s < world; ++s) {
+        se.insert(se.end(), owned.begin(), owned.end());
+        sr.insert(sr.end(), owned.size(), s);
+      }
+      if (n_seg) {
+        EMOE_CUDA(cudaMemcpy(ep->seg_expert, se.data(), se.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        EMOE_CUDA(cudaMemcpy(ep->seg_rank, sr.data(), sr.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+      }
       ep->recv_rows = dmalloc<int64_t>(1);
       ep->status = dmalloc<int>(1);
       EMOE_CUDA(cudaMemset(ep->status, 0, sizeof(int)));

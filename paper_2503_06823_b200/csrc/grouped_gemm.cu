@@ -87,6 +87,11 @@ struct Params {
   const int32_t* scatter_tok;
   const float* scatter_w;
   __nv_bfloat16* scatter_out;
+  // EPI_STORE pushing each segment's rows to its source rank's buffer
+  // (expert parallelism over peer memory); null = local output
+  const int32_t* seg_out_rank;
+  const int64_t* seg_out_shift;
+  uint8_t* out_peer[kMaxPeers];
 };
 
 struct TileCoord {
@@ -419,6 +424,30 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
             for (int v = 0; v < 8; ++v) dst[v] = make_uint4(a[4 * v], a[4 * v + 1], a[4 * v + 2], a[4 * v + 3]);
           }
         }
+      } else if (EPI == EPI_STORE && p.seg_out_rank != nullptr) {
+        // expert parallelism: the tile's rows belong to one (source, expert)
+        // segment; write them into the source rank's permuted layout over
+        // NVLink (each lane's 128-B row chunk, posted stores)
+        __nv_bfloat16* prow = reinterpret_cast<__nv_bfloat16*>(p.out_peer[p.seg_out_rank[c.expert]]) +
+                              (row + p.seg_out_shift[c.expert]) * p.ldo + col0;
+#pragma unroll 1
+        for (int cc = c_lo; cc < c_lo + SPAN; cc += OUT_BOX_COLS) {
+          uint32_t a0[32], a1[32];
+          tmem_ld_32x32b_x32(taddr + cc, a0);
+          tmem_ld_32x32b_x32(taddr + cc + 32, a1);
+          tmem_ld_wait();
+          uint4* dst = reinterpret_cast<uint4*>(prow + cc);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            uint32_t q4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = 4 * v + u, q = 2 * (j & 15);
+              q4[u] = pack_bf16x2(__uint_as_float(j < 16 ? a0[q] : a1[q]), __uint_as_float(j < 16 ? a0[q + 1] : a1[q + 1]));
+            }
+            dst[v] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+          }
+        }
       } else if (EPI == EPI_STORE && p.scatter_tok != nullptr) {
         // top-1 combine fused: y[t] = w_t * bf16(Y_row), the same two roundings
         // as the separate combine (bit-identical), each lane's 128-B row
@@ -478,6 +507,7 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
       }
     }
     if (EPI != EPI_F32 && p.tma_store && lane == 0) bulk_wait_all();
+    if (EPI == EPI_STORE && p.seg_out_rank != nullptr) __threadfence_system();  // pushes visible to the peers
   }
 
   if (CG == 2)
@@ -583,7 +613,7 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
                          int num_sms, cudaStream_t stream, const int32_t* seg_expert, const CUtensorMap* tmap_out,
-                         const ScatterCombine* scatter) {
+                         const ScatterCombine* scatter, const PeerOut* peer_out) {
   EMOE_REQUIRE(num_experts <= gemm::MAX_EXPERTS, "grouped_gemm: too many segments");
   EMOE_REQUIRE(!scatter || epi == EPI_STORE, "grouped_gemm: the fused combine needs the GEMM2 epilogue");
   EMOE_REQUIRE(K % gemm::BK == 0, "grouped_gemm: K must be a multiple of 64");
@@ -605,7 +635,11 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
   p.row_limit = 0;
   p.col_limit = 0;
   p.single_rows = 0;
-  p.tma_store = tmap_out != nullptr && tma_store_enabled() && !scatter;
+  EMOE_REQUIRE(!peer_out || epi == EPI_STORE, "grouped_gemm: peer output needs the GEMM2 epilogue");
+  p.tma_store = tmap_out != nullptr && tma_store_enabled() && !scatter && !peer_out;
+  p.seg_out_rank = peer_out ? peer_out->seg_rank : nullptr;
+  p.seg_out_shift = peer_out ? peer_out->seg_shift : nullptr;
+  for (int q = 0; q < kMaxPeers; ++q) p.out_peer[q] = peer_out ? peer_out->base[q] : nullptr;
   p.scatter_tok = scatter ? scatter->row_token : nullptr;
   p.scatter_w = scatter ? scatter->weight : nullptr;
   p.scatter_out = scatter ? scatter->y : nullptr;
@@ -640,6 +674,8 @@ void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t
   p.scatter_tok = nullptr;
   p.scatter_w = nullptr;
   p.scatter_out = nullptr;
+  p.seg_out_rank = nullptr;
+  p.seg_out_shift = nullptr;
   launch_params(EPI_F32, 1, ta, tb, tb, ta, p, num_sms, stream);
 }
 

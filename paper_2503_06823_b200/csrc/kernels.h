@@ -69,14 +69,19 @@ struct PeerRows {
   const int64_t* row_shift;
   int64_t cap;  // rows per buffer: a row outside [0, cap) is not written (pos = -1)
 };
+// GEMM2 return form: segment i's output rows go to rank seg_rank[i]'s buffer
+// base[seg_rank[i]] at row (r + seg_shift[i]) -- the source's own permuted
+// layout -- with NVLink stores from the epilogue (device arrays [n_seg])
+struct PeerOut {
+  uint8_t* base[kMaxPeers];
+  const int32_t* seg_rank;
+  const int64_t* seg_shift;
+};
 // K3b dispatch form: rows go straight to the owning rank's receive buffer;
-// pos[t][j] = row in that buffer
+// pos[t][j] stays the local permuted row (where the pushed output returns)
 void launch_permute_remote(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
                            const int64_t* seg_offsets, const int64_t* block_base, const PeerRows& peers,
                            int32_t* pos, cudaStream_t s);
-// K5 combine form: expert outputs read from the owning ranks' buffers (bf16)
-void launch_combine_remote(const PeerRows& peers, int64_t T, int d, int k, const int32_t* pos,
-                           const float* served_w, const int32_t* served_idx, void* y, cudaStream_t s);
 
 // K5: gate-weighted combine in fixed slot order
 void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int32_t* pos, const float* served_w,
@@ -87,6 +92,7 @@ CUtensorMap make_tmap_bf16_2d(const void* base, uint64_t rows, uint64_t cols, ui
 CUtensorMap make_tmap_bf16_store(const void* base, uint64_t rows, uint64_t cols);  // epilogue store target
 int gemm_tile_m(int cta_group);                 // segment padding the kernel needs
 int gemm_b_box_rows(int epi, int cta_group);    // TMA box rows of the weight operand
+struct PeerOut;  // expert parallelism: GEMM2 rows pushed to their source ranks (below)
 // top-1 combine fused into GEMM2's epilogue: y[row_token[r]] = weight[token] * Y[r]
 struct ScatterCombine {
   const int32_t* row_token;  // [R], -1 = padding row
@@ -98,7 +104,7 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
                          int num_sms, cudaStream_t stream, const int32_t* seg_expert = nullptr,
                          const CUtensorMap* tmap_out = nullptr,  // null: direct st.global epilogue
-                         const ScatterCombine* scatter = nullptr);
+                         const ScatterCombine* scatter = nullptr, const PeerOut* peer_out = nullptr);
 
 // K1 for many experts: the gate as one dense tcgen05 GEMM with fp32 output,
 // out[M][ldo] = A[M][K] . B[N_out][K]^T, columns >= col_limit (multiple of 32) not stored
@@ -148,6 +154,6 @@ LayerView layer_view(emoe_layer* L);
 void layer_route_scan(emoe_layer* L, const void* x, const float* logits_in, int64_t T, cudaStream_t s);
 // K4 over caller rows in n_seg segments (device seg offsets / experts)
 void layer_ffn_rows(emoe_layer* L, const void* xr, int64_t R, const int64_t* segs, const int32_t* seg_expert,
-                    int n_seg, void* hr, void* yr, cudaStream_t s);
+                    int n_seg, void* hr, void* yr, cudaStream_t s, const PeerOut* peer_out = nullptr);
 
 }  // namespace emoe

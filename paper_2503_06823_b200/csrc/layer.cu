@@ -298,7 +298,8 @@ struct emoe_layer {
   // A4 over rows [R][d] in n_seg padded segments (seg_expert null: segment i = expert i).
   // workspace = the rows are the layer's own x_perm/h/y_perm (cached tensor maps).
   void ffn(const void* xr, int64_t R, const int64_t* segs, const int32_t* seg_expert, int n_seg, void* hr, void* yr,
-           cudaStream_t s, bool workspace, const ScatterCombine* scatter = nullptr) {
+           cudaStream_t s, bool workspace, const ScatterCombine* scatter = nullptr,
+           const PeerOut* peer_out = nullptr) {
     const int d = cfg.d_model, f = cfg.d_ff;
     if (cfg.dtype == EMOE_DTYPE_BF16) {
       CUtensorMap a1 = ta1, a2 = ta2, o1 = to1, o2 = to2;
@@ -312,7 +313,7 @@ struct emoe_layer {
                           static_cast<__nv_bfloat16*>(hr), f, num_sms, s, seg_expert, &o1);
       mark(3, s);
       launch_grouped_gemm(EPI_STORE, cta_group, a2, tb2, tb2, segs, slot_dev, n_seg, f, d, d,
-                          static_cast<__nv_bfloat16*>(yr), d, num_sms, s, seg_expert, &o2, scatter);
+                          static_cast<__nv_bfloat16*>(yr), d, num_sms, s, seg_expert, &o2, scatter, peer_out);
       mark(4, s);
     } else if (tf32) {
       const int epi1 = swiglu() ? EPI_SWIGLU : EPI_RELU;
@@ -1064,10 +1065,10 @@ void layer_route_scan(emoe_layer* L, const void* x, const float* logits_in, int6
 }
 
 void layer_ffn_rows(emoe_layer* L, const void* xr, int64_t R, const int64_t* segs, const int32_t* seg_expert,
-                    int n_seg, void* hr, void* yr, cudaStream_t s) {
+                    int n_seg, void* hr, void* yr, cudaStream_t s, const PeerOut* peer_out) {
   const bool was = L->profiling;
   L->profiling = false;
-  L->ffn(xr, R, segs, seg_expert, n_seg, hr, yr, s, false);
+  L->ffn(xr, R, segs, seg_expert, n_seg, hr, yr, s, false, nullptr, peer_out);
   L->profiling = was;
 }
 

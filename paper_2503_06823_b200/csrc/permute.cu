@@ -9,6 +9,8 @@
 // Data movement: x is read once (one warp per token, 16-byte vectors) and
 // written to each of its <= k destinations; the combine reads each served row
 // of Y once and writes y once, accumulating in fp32 in slot order.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -134,18 +136,16 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
         d = (int32_t)(base + rank[j]);
       }
       dst_s[threadIdx.x * k + j] = d;
+      if (blockIdx.y != 0) continue;  // column-split blocks: block row 0 writes the positions
       if (REMOTE) {
-        int32_t rrow = -1;
         uint8_t* ptr = nullptr;
         if (e >= 0) {
           const int64_t r = d + peers.row_shift[e];
-          if (r >= 0 && r < peers.cap) {  // out of range only when the receiver overflowed (status 2)
-            rrow = (int32_t)r;
+          if (r >= 0 && r < peers.cap)  // out of range only when the receiver overflowed (status 2)
             ptr = peers.base[peers.dest[e]] + r * row_bytes;
-          }
         }
         dptr_s[threadIdx.x * k + j] = ptr;
-        if (t < T) pos[t * k + j] = rrow;
+        if (t < T) pos[t * k + j] = ptr ? d : -1;  // outputs return to this local row
       } else if (t < T) {
         if (pos) pos[t * k + j] = d;
         if (row_token && d >= 0) row_token[d] = (int32_t)t;
@@ -156,7 +156,10 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
   // gather: the block's rows x (row_bytes / 16) chunks as one flat index space
   // (consecutive threads -> consecutive 16-B chunks of the contiguous x rows),
   // GATHER_UNROLL independent loads in flight per thread whatever d is
-  const int nvec = row_bytes / 16;
+  // (small T: gridDim.y blocks share a token block, each gathering one column slice)
+  const int nvec_all = row_bytes / 16;
+  const int v0 = (int)((int64_t)nvec_all * blockIdx.y / gridDim.y);
+  const int nvec = (int)((int64_t)nvec_all * (blockIdx.y + 1) / gridDim.y) - v0;
   const int rows = (int)min((int64_t)RT, T - t0);
   const int total = rows * nvec;
   const uint4* src = reinterpret_cast<const uint4*>(x + t0 * row_bytes);
@@ -168,12 +171,12 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
       const int i = base + u * PERMUTE_THREADS;
       tok[u] = i < total ? i / nvec : -1;
       if (tok[u] >= 0 && dst_s[tok[u] * k] < 0) tok[u] = -1;  // token served nowhere
-      if (tok[u] >= 0) val[u] = __ldg(src + i);
+      if (tok[u] >= 0) val[u] = __ldg(src + (int64_t)tok[u] * nvec_all + v0 + (i - tok[u] * nvec));
     }
 #pragma unroll
     for (int u = 0; u < GATHER_UNROLL; ++u) {
       if (tok[u] < 0) continue;
-      const int v = base + u * PERMUTE_THREADS - tok[u] * nvec;
+      const int v = v0 + base + u * PERMUTE_THREADS - tok[u] * nvec;
       for (int j = 0; j < k; ++j) {
         const int32_t d = dst_s[tok[u] * k + j];
         if (d < 0) break;  // served slots are compacted to the front
@@ -186,35 +189,26 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
   if (REMOTE) __threadfence_system();
 }
 
-// One warp per token; lanes own 16-byte column chunks.  REMOTE: slot j's row
-// lives in rank dest[served_idx[t][j]]'s expert-output buffer (peer memory
-// read over NVLink); same slot order and fp32 accumulation as the local form,
-// so the expert-parallel output is bit-identical to the single-GPU one.
-template <bool REMOTE>
+// One warp per token; lanes own 16-byte column chunks.
 __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* __restrict__ Y, int64_t T, int d,
                                                            int k, const int32_t* __restrict__ pos,
                                                            const float* __restrict__ served_w,
-                                                           __nv_bfloat16* __restrict__ y, PeerRows peers,
-                                                           const int32_t* __restrict__ served_idx) {
+                                                           __nv_bfloat16* __restrict__ y) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t t = (int64_t)blockIdx.x * 8 + warp;
   if (t >= T) return;
   int32_t p[8];
   float w[8];
-  const __nv_bfloat16* src[8];
   for (int j = 0; j < k; ++j) {
     p[j] = pos[t * k + j];
     w[j] = served_w[t * k + j];
-    src[j] = Y;
-    if (REMOTE && p[j] >= 0) src[j] = reinterpret_cast<const __nv_bfloat16*>(peers.base[peers.dest[served_idx[t * k + j]]]);
   }
   const int nvec = d / 8;
   for (int v = lane; v < nvec; v += 32) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int j = 0; j < k; ++j) {
       if (p[j] < 0) continue;
-      const uint4 r = REMOTE ? *(reinterpret_cast<const uint4*>(src[j] + (int64_t)p[j] * d) + v)
-                             : __ldg(reinterpret_cast<const uint4*>(Y + (int64_t)p[j] * d) + v);
+      const uint4 r = __ldg(reinterpret_cast<const uint4*>(Y + (int64_t)p[j] * d) + v);
       const uint32_t u[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -278,7 +272,10 @@ void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int 
   const int nblocks = (int)ceil_div(T, RT);
   if (nblocks == 0) return;
   const size_t smem = (4 * (size_t)E + (size_t)RT * k) * sizeof(int32_t);
-  permute_kernel<false><<<nblocks, PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
+  // few token blocks (small T): split each block's rows by columns over
+  // gridDim.y blocks so the gather still spans the GPU (>= 8 x 16 B per row slice)
+  const int ny = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * 148, nblocks), row_bytes / 16 / 8));
+  permute_kernel<false><<<dim3(nblocks, ny), PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
                                                                served_idx, seg_offsets, block_base,
                                                                static_cast<uint8_t*>(x_perm), pos, row_token,
                                                                PeerRows{});
@@ -301,17 +298,6 @@ void launch_permute_remote(const void* x, int elem_bytes, int64_t T, int d, int 
   count_launch();
 }
 
-void launch_combine_remote(const PeerRows& peers, int64_t T, int d, int k, const int32_t* pos,
-                           const float* served_w, const int32_t* served_idx, void* y, cudaStream_t s) {
-  const int nblocks = (int)ceil_div(T, 8);
-  if (nblocks == 0) return;
-  EMOE_REQUIRE(d % 8 == 0, "combine: d must be a multiple of 8");
-  combine_bf16_kernel<true><<<nblocks, 256, 0, s>>>(nullptr, T, d, k, pos, served_w, static_cast<__nv_bfloat16*>(y),
-                                                    peers, served_idx);
-  EMOE_CUDA(cudaGetLastError());
-  count_launch();
-}
-
 void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int32_t* pos, const float* served_w,
                     void* y, cudaStream_t s) {
   const int nblocks = (int)ceil_div(T, 8);
@@ -322,8 +308,8 @@ void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int
                                                static_cast<float*>(y));
   } else {
     EMOE_REQUIRE(d % 8 == 0, "combine: d must be a multiple of 8");
-    combine_bf16_kernel<false><<<nblocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Y), T, d, k, pos, served_w,
-                                                       static_cast<__nv_bfloat16*>(y), PeerRows{}, nullptr);
+    combine_bf16_kernel<<<nblocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Y), T, d, k, pos, served_w,
+                                                static_cast<__nv_bfloat16*>(y));
   }
   EMOE_CUDA(cudaGetLastError());
   count_launch();

@@ -23,10 +23,10 @@ gloo group (CPU tests, or several ranks sharing one GPU) tensors are staged
 through host memory.
 
 PeerExpertParallelMoE is the fused form (csrc/ep.cu): the permute kernel
-stores each row straight into its owner's receive buffer and the combine
-kernel loads expert outputs from the owners' buffers, over CUDA-IPC-mapped
-peer memory (NVLink between GPUs), with device-side barriers and no host
-synchronisation.  The receive layout is the same (source rank, expert,
+stores each row straight into its owner's receive buffer and GEMM2's epilogue
+stores each expert output row straight back into its source's permuted
+layout, over CUDA-IPC-mapped peer memory (NVLink between GPUs), with
+device-side barriers and no host synchronisation; the combine is local.  The receive layout is the same (source rank, expert,
 token) order, so its output is bit-identical too.  `p2p_layout` restates the
 layout the device computes (tests check it on CPU).
 """
@@ -184,10 +184,12 @@ def p2p_layout(counts: np.ndarray, dest: np.ndarray, rank: int, seg_offsets: np.
     """The receive segments and send shifts ep_bar0_kernel computes on rank
     `rank` (csrc/ep.cu).  counts[s, e] = padded rows source s holds for expert
     e; seg_offsets = this rank's local padded segment starts [E+1].
-    Returns (recv_segs, seg_expert, row_shift): rank `rank` receives segment
-    (s, e) at recv_segs[i] for its owned experts in (source, expert) order,
-    and writes its own segment e to row seg_offsets[e] + row_shift[e] of rank
-    dest[rank, e]'s buffer."""
+    Returns (recv_segs, seg_expert, row_shift, seg_src, out_shift): rank
+    `rank` receives segment i = (seg_src[i], seg_expert[i]) at recv_segs[i]
+    in (source, expert) order and pushes its outputs back to row r +
+    out_shift[i] of the source's own permuted layout; it writes its own
+    segment e to row seg_offsets[e] + row_shift[e] of rank dest[rank, e]'s
+    receive buffer."""
     W, E = dest.shape
     owned = owned_experts(dest, rank)
     tot = np.zeros((W, W), np.int64)  # [source][receiver]
@@ -202,15 +204,18 @@ def p2p_layout(counts: np.ndarray, dest: np.ndarray, rank: int, seg_offsets: np.
             continue
         base = tot[:rank, q].sum() + sum(counts[rank, e2] for e2 in range(e) if dest[rank, e2] == q)
         shift[e] = base - seg_offsets[e]
-    segs, exp, off = [], [], 0
+    segs, exp, src, out, off = [], [], [], [], 0
     for s in range(W):
         for e in owned:
             segs.append(off)
             exp.append(e)
+            src.append(s)
+            out.append(int(counts[s, :e].sum()) - off)  # source s's padded segment e starts at its count prefix
             if dest[s, e] == rank:
                 off += counts[s, e]
     segs.append(off)
-    return np.asarray(segs, np.int64), np.asarray(exp, np.int32), shift
+    return (np.asarray(segs, np.int64), np.asarray(exp, np.int32), shift, np.asarray(src, np.int32),
+            np.asarray(out, np.int64))
 
 
 class PeerExpertParallelMoE:

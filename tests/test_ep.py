@@ -166,22 +166,23 @@ def _simulate_p2p(backends, xs, dest):
             if b > a:
                 q = dest[r, e]
                 recv[q][a + shift[e]:b + shift[e]] = bt.rows[a:b].numpy()
-    outs = []
+    # every owner pushes each received segment's outputs back into the
+    # source's own permuted layout (GEMM2's epilogue on the GPU)
+    y_local = [np.zeros((int(bt.seg_offsets[-1]), backends[0].d), np.float32) for bt in batches]
     for q in range(W):
-        segs, exp, _ = layouts[q]
-        outs.append(backends[q].ffn(torch.from_numpy(recv[q]), segs, exp).numpy() if len(exp) else recv[q])
+        segs, exp, _, src, out_shift = layouts[q]
+        if not len(exp):
+            continue
+        out = backends[q].ffn(torch.from_numpy(recv[q]), segs, exp).numpy()
+        for i in range(len(exp)):
+            a, b = int(segs[i]), int(segs[i + 1])
+            if b > a:
+                y_local[src[i]][a + out_shift[i]:b + out_shift[i]] = out[a:b]
     ys = []
     for r, bt in enumerate(batches):
-        shift = layouts[r][2]
         pos = bt.pos.numpy().astype(np.int64)
-        seg = bt.seg_offsets
-        y_rows = np.zeros((int(seg[-1]), backends[0].d), np.float32)
-        for e in range(E):  # gather this rank's rows back from their owners
-            a, b = int(seg[e]), int(seg[e + 1])
-            if b > a:
-                y_rows[a:b] = outs[dest[r, e]][a + shift[e]:b + shift[e]]
-        ys.append(backends[r].combine(torch.from_numpy(y_rows), RoutedBatch(seg, None, torch.from_numpy(pos),
-                                                                            bt.served_w, bt.T)))
+        ys.append(backends[r].combine(torch.from_numpy(y_local[r]),
+                                      RoutedBatch(bt.seg_offsets, None, torch.from_numpy(pos), bt.served_w, bt.T)))
     return ys, layouts
 
 
@@ -195,7 +196,7 @@ def test_p2p_layout_protocol_bit_identical(world, resident, port):
     for r in range(world):
         assert np.array_equal(ys[r].numpy(), single(be[r], xs[r]).numpy()), f"rank {r}: P2P layout output differs"
     # receive segments are contiguous, padded and cover exactly the rows sent to each rank
-    for q, (segs, exp, _) in enumerate(layouts):
+    for q, (segs, exp, _, _, _) in enumerate(layouts):
         assert np.all(np.diff(segs) >= 0) and np.all(segs % be[0].pad == 0)
         assert len(exp) == world * len(owned_experts(dest, q))
 
@@ -212,15 +213,23 @@ def test_p2p_layout_disjoint_writes(port):
         seg = [np.concatenate([[0], np.cumsum(counts[r])]) for r in range(world)]
         written = {q: [] for q in range(world)}
         for r in range(world):
-            _, _, shift = p2p_layout(counts, dest, r, seg[r])
+            _, _, shift, _, _ = p2p_layout(counts, dest, r, seg[r])
             for e in range(8):
                 if counts[r, e]:
                     written[dest[r, e]].append((seg[r][e] + shift[e], seg[r][e + 1] + shift[e]))
+        pushed = {r: [] for r in range(world)}
         for q in range(world):
-            segs, _, _ = p2p_layout(counts, dest, q, seg[q])
+            segs, _, _, src, out_shift = p2p_layout(counts, dest, q, seg[q])
             iv = sorted(written[q])
             assert all(a[1] == b[0] for a, b in zip(iv, iv[1:])), (world, q, iv)
             assert (iv[0][0] if iv else 0) == 0 and (iv[-1][1] if iv else 0) == segs[-1]
+            for i in range(len(src)):
+                if segs[i + 1] > segs[i]:
+                    pushed[int(src[i])].append((segs[i] + out_shift[i], segs[i + 1] + out_shift[i]))
+        # the return pushes land exactly on each source's own padded segments
+        for r in range(world):
+            want = sorted((seg[r][e], seg[r][e + 1]) for e in range(8) if counts[r, e])
+            assert sorted(pushed[r]) == want, (world, r)
 
 
 def _gpu_p2p_worker(rank, world, port_no, resident, out_dir):
