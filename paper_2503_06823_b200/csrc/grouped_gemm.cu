@@ -92,6 +92,9 @@ struct Params {
   const int32_t* seg_out_rank;
   const int64_t* seg_out_shift;
   uint8_t* out_peer[kMaxPeers];
+  // L2 policies of the operand loads: the raster keeps an A panel resident
+  // while the weight tiles stream past it
+  uint64_t hint_a, hint_b;
 };
 
 struct TileCoord {
@@ -294,16 +297,16 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
           uint8_t* adst = smem_a + stage * C::A_BYTES;
           uint8_t* bdst = smem_b + stage * C::B_BYTES;
           if (CG == 1) {
-            tma_load_2d(&tmap_a, &full_bar[stage], adst, kc, a_row, kCacheEvictNormal);
+            tma_load_2d(&tmap_a, &full_bar[stage], adst, kc, a_row, p.hint_a);
             if (EPI == EPI_SWIGLU) {
-              tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, kCacheEvictNormal);
-              tma_load_2d(&tmap_b2, &full_bar[stage], bdst + C::B_BYTES / 2, kc, b_row, kCacheEvictNormal);
+              tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, p.hint_b);
+              tma_load_2d(&tmap_b2, &full_bar[stage], bdst + C::B_BYTES / 2, kc, b_row, p.hint_b);
             } else {
-              tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, kCacheEvictNormal);
+              tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, p.hint_b);
             }
           } else {
-            tma_load_2d_pair(&tmap_a, &full_bar[stage], adst, kc, a_row, kCacheEvictNormal);
-            tma_load_2d_pair(tb, &full_bar[stage], bdst, kc, b_row, kCacheEvictNormal);
+            tma_load_2d_pair(&tmap_a, &full_bar[stage], adst, kc, a_row, p.hint_a);
+            tma_load_2d_pair(tb, &full_bar[stage], bdst, kc, b_row, p.hint_b);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -589,6 +592,19 @@ int gemm_b_box_rows(int epi, int cta_group) { return epi == EPI_SWIGLU ? 128 : 2
 // 2/8/24/48/96 MB), 4 MB for short ones (Switch GEMM1, K = 768: 4-8 MB beat
 // 24 MB by 4 %, profiles/r01_raster_sweep.jsonl).  EMOE_GEMM_PANEL_MB
 // overrides for tuning.
+// L2 policies for the operand loads (EMOE_GEMM_L2_HINTS): 0 = evict-normal
+// for both; 1 = A panel evict-last, weight tiles evict-first (measured 3x the
+// DRAM traffic: a weight tile is shared by the group's row blocks, which do
+// not run in lockstep); 2 = A panel evict-last, weights normal
+static void l2_hints(uint64_t& a, uint64_t& b) {
+  static const int mode = [] {
+    const char* v = getenv("EMOE_GEMM_L2_HINTS");
+    return v ? atoi(v) : 0;
+  }();
+  a = mode == 1 || mode == 2 ? kCacheEvictLast : kCacheEvictNormal;
+  b = mode == 1 ? kCacheEvictFirst : kCacheEvictNormal;
+}
+
 static int group_rows(int K, int tile_m) {
   static int panel_env = [] {
     const char* v = getenv("EMOE_GEMM_PANEL_MB");
@@ -629,6 +645,7 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
   p.n_blocks = N_out / p.out_block_cols;
   p.b_rows_per_slot = b_rows_per_slot;
   p.group_m = group_rows(K, 128 * cta_group);
+  l2_hints(p.hint_a, p.hint_b);
   p.out = out;
   p.ldo = ldo;
   p.out_f32 = nullptr;
@@ -664,6 +681,8 @@ void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t
   p.n_blocks = N_out / gemm::BN;
   p.b_rows_per_slot = 0;
   p.group_m = group_rows(K, 128);
+  p.hint_a = kCacheEvictNormal;
+  p.hint_b = kCacheEvictNormal;
   p.out = nullptr;
   p.ldo = ldo;
   p.out_f32 = out;
