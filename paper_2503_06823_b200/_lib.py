@@ -8,9 +8,11 @@ architecture, importing the package raises.  Build it with
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libemoe.so"
+# EMOE_LIB_PATH: an alternative build of the same library (compile-time A/B variants)
+LIB_PATH = Path(os.environ.get("EMOE_LIB_PATH") or Path(__file__).resolve().parent / "lib" / "libemoe.so")
 
 if not LIB_PATH.exists():
     raise ImportError(

@@ -53,7 +53,13 @@ template <int CG, int EW>
 struct Cfg {
   static constexpr int TILE_M = 128 * CG;
   static constexpr int B_ROWS = BN / CG;  // B rows held by one CTA
-  static constexpr int STAGES = CG == 1 ? 4 : 6;
+#ifndef EMOE_CG1_STAGES
+#define EMOE_CG1_STAGES 4
+#endif
+#ifndef EMOE_CG2_STAGES
+#define EMOE_CG2_STAGES 6
+#endif
+  static constexpr int STAGES = CG == 1 ? EMOE_CG1_STAGES : EMOE_CG2_STAGES;
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;

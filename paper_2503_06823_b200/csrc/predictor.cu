@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cstring>
+
 #include "capi_util.h"
 #include "kernels.h"
 
@@ -463,6 +465,31 @@ struct emoe_predictor {
   int32_t* dom = nullptr;
   size_t dom_cap = 0;
 
+  // Invocation path (emoe_invocation_host, called every p prompts while the
+  // layers compute): its own stream, ordered after the last histogram update
+  // by an event, and one persistent device arena + pinned host staging block
+  // (inputs packed and uploaded with one copy, outputs downloaded with one), so
+  // an invocation allocates nothing and never synchronises the whole device.
+  cudaStream_t inv_stream = nullptr;
+  cudaEvent_t hist_done = nullptr;
+  bool hist_recorded = false;
+  uint8_t* arena_dev = nullptr;
+  uint8_t* arena_host = nullptr;
+  size_t arena_cap = 0;
+  void arena_reserve(size_t bytes) {
+    if (bytes <= arena_cap) return;
+    if (arena_dev) {
+      EMOE_CUDA(cudaStreamSynchronize(inv_stream));
+      EMOE_CUDA(cudaFree(arena_dev));
+      EMOE_CUDA(cudaFreeHost(arena_host));
+      arena_dev = arena_host = nullptr;
+    }
+    const size_t cap = std::max<size_t>(bytes, 2 * arena_cap);
+    EMOE_CUDA(cudaMalloc(&arena_dev, cap));
+    EMOE_CUDA(cudaHostAlloc(&arena_host, cap, cudaHostAllocDefault));
+    arena_cap = cap;
+  }
+
   size_t n_layer() const { return (size_t)(m > 1 ? m - 1 : 0) * E * E; }
   size_t n_prompt() const { return (size_t)m * E * E; }
   size_t n_task() const { return (size_t)n_tasks * m * E; }
@@ -470,6 +497,7 @@ struct emoe_predictor {
     if (n_layer()) EMOE_CUDA(cudaMemset(layer_counts, 0, n_layer() * sizeof(u64)));
     EMOE_CUDA(cudaMemset(prompt_counts, 0, n_prompt() * sizeof(u64)));
     if (n_task()) EMOE_CUDA(cudaMemset(task_counts, 0, n_task() * sizeof(u64)));
+    EMOE_CUDA(cudaDeviceSynchronize());  // visible to the invocation stream (not ordered with the legacy stream)
     has_last = false;
   }
 };
@@ -546,6 +574,8 @@ int emoe_predictor_create(int m, int E, int k, int n_tasks, double smoothing, em
     EMOE_CUDA(cudaMalloc(&P->prompt_counts, P->n_prompt() * sizeof(u64)));
     EMOE_CUDA(cudaMalloc(&P->task_counts, std::max<size_t>(1, P->n_task()) * sizeof(u64)));
     EMOE_CUDA(cudaMalloc(&P->last_dom, m * sizeof(int32_t)));
+    EMOE_CUDA(cudaStreamCreateWithFlags(&P->inv_stream, cudaStreamNonBlocking));
+    EMOE_CUDA(cudaEventCreateWithFlags(&P->hist_done, cudaEventDisableTiming));
     P->zero();
     *out = P;
   });
@@ -554,9 +584,13 @@ int emoe_predictor_create(int m, int E, int k, int n_tasks, double smoothing, em
 int emoe_predictor_destroy(emoe_predictor* P) {
   return guard([&] {
     if (!P) return;
+    cudaDeviceSynchronize();
     for (void* p : {(void*)P->layer_counts, (void*)P->prompt_counts, (void*)P->task_counts, (void*)P->last_dom,
-                    (void*)P->dom})
+                    (void*)P->dom, (void*)P->arena_dev})
       if (p) cudaFree(p);
+    if (P->arena_host) cudaFreeHost(P->arena_host);
+    if (P->inv_stream) cudaStreamDestroy(P->inv_stream);
+    if (P->hist_done) cudaEventDestroy(P->hist_done);
     delete P;
   });
 }
@@ -606,6 +640,8 @@ int emoe_hist_update(emoe_predictor* P, const int32_t* trace, int nP, int T, con
     save_last_kernel<<<1, 128, 0, s>>>(P->dom, nP, P->m, P->last_dom);
     EMOE_CUDA(cudaGetLastError());
     count_launch();
+    EMOE_CUDA(cudaEventRecord(P->hist_done, s));  // the next invocation reads the counts after this
+    P->hist_recorded = true;
     P->has_last = true;
   });
 }
@@ -661,6 +697,7 @@ int emoe_predictor_set_counts_host(emoe_predictor* P, const double* lc, const do
     load(P->layer_counts, P->n_layer(), lc);
     load(P->prompt_counts, P->n_prompt(), pc);
     load(P->task_counts, P->n_task(), tc);
+    EMOE_CUDA(cudaDeviceSynchronize());  // copies complete before the invocation stream reads them
   });
 }
 
@@ -842,40 +879,69 @@ int emoe_invocation_host(emoe_predictor* P, int mode, const int32_t* sets, const
     const int m = P->m, E = P->E, k = P->k;
     const size_t ME = (size_t)m * E, nt = std::max(1, n_tasks);
     const int rows = mode == 0 ? m : 1;
-    DevBuf<int32_t> dsets(sets, (size_t)rows * k), dsizes(sizes, rows), dex((size_t)m * k), dn(m);
-    DevBuf<double> dsc(ME), dfit(nt * ME), dfreq(nt * ME), dwo(nt), dagg(ME), ddur(m), dde(1);
-    DevBuf<int32_t> dsens(nt * m), drt(std::max(1, n_req)), drn(std::max(1, n_req));
-    DevBuf<uint8_t> dhs(nt), dfp(nt), dres(resident, ME);
-    DevBuf<int32_t> dbud(budgets, m), dtg(ME), dts(m), dev(ME), dnev(m), dld(ME), dnld(m), dtl(1);
+    // arena layout: [uploaded inputs | downloaded outputs | device scratch]
+    size_t off = 0;
+    auto put = [&](size_t bytes) {
+      const size_t o = off;
+      off = (off + bytes + 255) / 256 * 256;
+      return o;
+    };
+    const size_t o_sets = put((size_t)rows * k * 4), o_sizes = put((size_t)rows * 4), o_wo = put(nt * 8),
+                 o_sens = put(nt * m * 4), o_hs = put(nt), o_fp = put(nt), o_rt = put(std::max(1, n_req) * 4),
+                 o_rn = put(std::max(1, n_req) * 4), o_res = put(ME), o_bud = put((size_t)m * 4);
+    const size_t in_bytes = off;
+    const size_t o_agg = put(ME * 8), o_ev = put(ME * 4), o_nev = put((size_t)m * 4), o_ld = put(ME * 4),
+                 o_nld = put((size_t)m * 4), o_de = put(8);
+    const size_t out_end = off;
+    const size_t o_ex = put((size_t)m * k * 4), o_n = put((size_t)m * 4), o_sc = put(ME * 8), o_fit = put(nt * ME * 8),
+                 o_freq = put(nt * ME * 8), o_dur = put((size_t)m * 8), o_tg = put(ME * 4), o_ts = put((size_t)m * 4),
+                 o_tl = put(4);
+    P->arena_reserve(off);
+    cudaStream_t s = P->inv_stream;
+    EMOE_CUDA(cudaStreamSynchronize(s));  // the staging block is free (previous invocation done)
+    uint8_t* h = P->arena_host;
+    uint8_t* d = P->arena_dev;
+    std::memcpy(h + o_sets, sets, (size_t)rows * k * 4);
+    std::memcpy(h + o_sizes, sizes, (size_t)rows * 4);
     if (n_tasks) {
-      EMOE_CUDA(cudaMemcpy(dwo.p, wo, n_tasks * sizeof(double), cudaMemcpyHostToDevice));
-      EMOE_CUDA(cudaMemcpy(dsens.p, sens, (size_t)n_tasks * m * sizeof(int32_t), cudaMemcpyHostToDevice));
-      EMOE_CUDA(cudaMemcpy(dhs.p, has_sens, n_tasks, cudaMemcpyHostToDevice));
-      EMOE_CUDA(cudaMemset(dfp.p, 1, n_tasks));
+      std::memcpy(h + o_wo, wo, n_tasks * sizeof(double));
+      std::memcpy(h + o_sens, sens, (size_t)n_tasks * m * sizeof(int32_t));
+      std::memcpy(h + o_hs, has_sens, n_tasks);
+      std::memset(h + o_fp, 1, n_tasks);
     }
     if (n_req) {
-      EMOE_CUDA(cudaMemcpy(drt.p, req_task, n_req * sizeof(int32_t), cudaMemcpyHostToDevice));
-      EMOE_CUDA(cudaMemcpy(drn.p, req_tokens, n_req * sizeof(int32_t), cudaMemcpyHostToDevice));
+      std::memcpy(h + o_rt, req_task, n_req * sizeof(int32_t));
+      std::memcpy(h + o_rn, req_tokens, n_req * sizeof(int32_t));
     }
+    std::memcpy(h + o_res, resident, ME);
+    std::memcpy(h + o_bud, budgets, (size_t)m * 4);
+    auto i32 = [&](size_t o) { return reinterpret_cast<int32_t*>(d + o); };
+    auto f64 = [&](size_t o) { return reinterpret_cast<double*>(d + o); };
     InvocationArgs a;
-    a.pred = make_predict_args(P, mode, 0, dsets.p, dsizes.p, dsc.p, dex.p, dn.p);
+    a.pred = make_predict_args(P, mode, 0, i32(o_sets), i32(o_sizes), f64(o_sc), i32(o_ex), i32(o_n));
     a.task_counts = P->task_counts;
     a.n_tasks = n_tasks;
-    a.fitted = dfit.p;
-    a.freqs = dfreq.p;
-    a.eq2 = Eq2Args{m, E, n_tasks, dwo.p, dsens.p, dhs.p, n_req, drt.p, drn.p, dfp.p, dfreq.p, task_aware, dagg.p};
-    a.plan = PlanArgs{m, E, dagg.p, dres.p, dbud.p, per_expert, dtg.p, dts.p, dev.p, dnev.p, dld.p, dnld.p, ddur.p,
-                      dde.p, dtl.p, 0, 0};
-    invocation_kernel<<<1, 128>>>(a);
+    a.fitted = f64(o_fit);
+    a.freqs = f64(o_freq);
+    a.eq2 = Eq2Args{m,         E,         n_tasks,       f64(o_wo),         i32(o_sens),
+                    d + o_hs,  n_req,     i32(o_rt),     i32(o_rn),         d + o_fp,
+                    f64(o_freq), task_aware, f64(o_agg)};
+    a.plan = PlanArgs{m,          E,          f64(o_agg), d + o_res,  i32(o_bud), per_expert, i32(o_tg), i32(o_ts),
+                      i32(o_ev),  i32(o_nev), i32(o_ld),  i32(o_nld), f64(o_dur), f64(o_de), i32(o_tl), 0,
+                      0};
+    if (P->hist_recorded) EMOE_CUDA(cudaStreamWaitEvent(s, P->hist_done, 0));
+    EMOE_CUDA(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, s));
+    invocation_kernel<<<1, 128, 0, s>>>(a);
     EMOE_CUDA(cudaGetLastError());
     count_launch();
-    EMOE_CUDA(cudaDeviceSynchronize());
-    dagg.to_host(aggregate);
-    dev.to_host(evictions);
-    dnev.to_host(n_evict);
-    dld.to_host(loads);
-    dnld.to_host(n_load);
-    dde.to_host(delta_e);
+    EMOE_CUDA(cudaMemcpyAsync(h + o_agg, d + o_agg, out_end - o_agg, cudaMemcpyDeviceToHost, s));
+    EMOE_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(aggregate, h + o_agg, ME * 8);
+    std::memcpy(evictions, h + o_ev, ME * 4);
+    std::memcpy(n_evict, h + o_nev, (size_t)m * 4);
+    std::memcpy(loads, h + o_ld, ME * 4);
+    std::memcpy(n_load, h + o_nld, (size_t)m * 4);
+    std::memcpy(delta_e, h + o_de, 8);
   });
 }
 
