@@ -387,6 +387,52 @@ __global__ void __launch_bounds__(F32_GATE_THREADS) gate_route_f32_kernel(const 
   flush_block_counts(a, o, st);
 }
 
+// fp32 gate logits only, one warp per token (small T: the fused kernel above
+// has one block per 128 tokens, too few blocks to cover the GPU), followed by
+// route_from_logits_kernel.  Same dot-product order as the fused kernel.
+__global__ void __launch_bounds__(256) gate_logits_f32_kernel(const float* __restrict__ x,
+                                                              const float* __restrict__ wg, int64_t T, int d, int E,
+                                                              float* __restrict__ logits) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t t = (int64_t)blockIdx.x * 8 + warp;
+  if (t >= T) return;
+  const float* xr = x + t * d;
+  const bool vec = (d & 3) == 0;
+  for (int e0 = 0; e0 < E; e0 += 8) {
+    const int ne = min(8, E - e0);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (vec) {
+      for (int i = lane * 4; i < d; i += 128) {
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + i));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j < ne) {
+            const float4 wv = __ldg(reinterpret_cast<const float4*>(wg + (int64_t)(e0 + j) * d + i));
+            acc[j] = fmaf(xv.x, wv.x, acc[j]);
+            acc[j] = fmaf(xv.y, wv.y, acc[j]);
+            acc[j] = fmaf(xv.z, wv.z, acc[j]);
+            acc[j] = fmaf(xv.w, wv.w, acc[j]);
+          }
+        }
+      }
+    } else {
+      for (int i = lane; i < d; i += 32) {
+        const float xv = xr[i];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < ne) acc[j] = fmaf(xv, wg[(int64_t)(e0 + j) * d + i], acc[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float v = acc[j];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0 && j < ne) logits[t * E + e0 + j] = v;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // routing-driven mode: logits supplied by the caller
 // ---------------------------------------------------------------------------
@@ -464,7 +510,15 @@ void launch_gate_route(const void* x, const void* wg, int dtype, const RouteArgs
   EMOE_REQUIRE(a.k >= 1 && a.k <= 8 && a.k <= a.E, "route: top_k must be in [1, min(8, E)]");
   const int nblocks = (int)ceil_div(a.T, RT);
   if (nblocks == 0) return;
-  if (dtype == DT_F32) {
+  if (dtype == DT_F32 && o.logits && nblocks < 74) {
+    // small T: logits with one warp per token over the whole GPU, then routing
+    gate_logits_f32_kernel<<<(unsigned)ceil_div(a.T, 8), 256, 0, s>>>(
+        static_cast<const float*>(x), static_cast<const float*>(wg), a.T, a.d, a.E, o.logits);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+    launch_route_from_logits(o.logits, a, o, s);
+    return;
+  } else if (dtype == DT_F32) {
     const size_t smem = (size_t)RT * a.E * sizeof(float);
     EMOE_REQUIRE(smem <= 48 * 1024, "route: fp32 logits tile exceeds 48 KB");
     gate_route_f32_kernel<<<nblocks, F32_GATE_THREADS, smem, s>>>(static_cast<const float*>(x), static_cast<const float*>(wg), a,

@@ -271,3 +271,45 @@ def test_ep_p2p_two_ranks_one_gpu_bit_identical(resident, tmp_path):
             assert d["status"] == 0, f"rank {r} forward {i}: status {d['status']}"
             assert d["rows"] > 0
             assert torch.equal(d["y_ep"], d["y_1"]), f"rank {r} forward {i}: P2P EP output differs from 1 GPU"
+
+
+def _gpu_p2p_fault_worker(rank, world, port_no, case, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no), EMOE_EP_TIMEOUT_S="2")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from helpers import build_layer
+    from paper_2503_06823_b200.ep import PeerExpertParallelMoE
+
+    resident = [0, 2, 5, 7]
+    dest = plan_destinations(resident, 8, world)
+    mine = owned_experts(dest, rank)
+    layer, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", len(mine), mine, max_tokens=2048)
+    ep = PeerExpertParallelMoE(layer, resident, recv_rows_cap=256 if case == "overflow" else 0)
+    x = torch.randn(1500, 256, generator=torch.Generator().manual_seed(rank)).to(torch.bfloat16).cuda()
+    res = {}
+    if case == "overflow" or rank == 0:  # "timeout": rank 1 never joins the forward
+        y = ep(x)
+        res["status"], res["rows"] = ep.status()
+        res["finite"] = bool(torch.isfinite(y.float()).all())
+    torch.save(res, Path(out_dir) / f"f{rank}.pt")
+    dist.barrier()
+    ep.close()
+    layer.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["overflow", "timeout"])
+def test_ep_p2p_fault_status(case, tmp_path):
+    """A receive buffer too small for the routed rows drops them and reports
+    status 2 on every rank (all ranks derive the same layout); a peer that
+    never arrives makes the barrier give up after EMOE_EP_TIMEOUT_S with
+    status 1 instead of hanging the GPU."""
+    mp.spawn(_gpu_p2p_fault_worker, args=(2, free_port(), case, str(tmp_path)), nprocs=2, join=True)
+    r0 = torch.load(tmp_path / "f0.pt")
+    if case == "overflow":
+        r1 = torch.load(tmp_path / "f1.pt")
+        assert r0["status"] == 2 and r1["status"] == 2
+        assert r0["finite"] and r1["finite"]
+    else:
+        assert r0["status"] == 1
