@@ -101,21 +101,29 @@ struct Params {
   // L2 policies of the operand loads: the raster keeps an A panel resident
   // while the weight tiles stream past it
   uint64_t hint_a, hint_b;
+  int group_n;  // column panel width in n-blocks (>= n_blocks: whole width)
 };
 
 struct TileCoord {
   int mb, nb, expert;
 };
 
+// Tile order: column panels of group_n n-blocks (group_n >= n_blocks: one
+// panel) walked one after another; inside a panel, groups of group_m row
+// blocks, each sweeping the panel's n-blocks with the row block fastest.
 __device__ __forceinline__ TileCoord decode_tile(int t, int total_mb, int n_blocks, int group_m, int tile_m,
-                                                 const int32_t* offs, int num_experts) {
-  const int per_group = group_m * n_blocks;
+                                                 const int32_t* offs, int num_experts, int group_n) {
+  const int ng = t / (total_mb * group_n);  // column panel
+  const int n0 = ng * group_n;
+  const int gn = min(group_n, n_blocks - n0);
+  t -= ng * total_mb * group_n;
+  const int per_group = group_m * gn;
   const int g = t / per_group;
   const int local = t - g * per_group;
   const int rows_in_group = min(group_m, total_mb - g * group_m);
   TileCoord c;
-  c.nb = local / rows_in_group;
-  c.mb = g * group_m + (local - c.nb * rows_in_group);
+  c.nb = n0 + local / rows_in_group;
+  c.mb = g * group_m + (local - (c.nb - n0) * rows_in_group);
   const int32_t row = c.mb * tile_m;
   int e = 0;
   while (e + 1 < num_experts && offs[e + 1] <= row) ++e;
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
-        const TileCoord c = decode_tile(t, total_mb, p.n_blocks, p.group_m, C::TILE_M, s_offs, E);
+        const TileCoord c = decode_tile(t, total_mb, p.n_blocks, p.group_m, C::TILE_M, s_offs, E, p.group_n);
         const int slot = p.slot_of_expert[p.seg_expert ? p.seg_expert[c.expert] : c.expert];
         const int a_row = c.mb * C::TILE_M + (int)rank * 128;
         int b_row;
@@ -385,7 +393,7 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
     const int c_lo = (ew / 4) * SPAN;
     int local = 0;
     for (int t = cluster_id; t < total_tiles; t += num_clusters, ++local) {
-      const TileCoord c = decode_tile(t, total_mb, p.n_blocks, p.group_m, C::TILE_M, s_offs, E);
+      const TileCoord c = decode_tile(t, total_mb, p.n_blocks, p.group_m, C::TILE_M, s_offs, E, p.group_n);
       const int buf = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull_bar[buf], acc_phase);
@@ -611,6 +619,29 @@ static void l2_hints(uint64_t& a, uint64_t& b) {
   b = mode == 1 ? kCacheEvictFirst : kCacheEvictNormal;
 }
 
+// Column-panel raster: the weight panel (npanel n-blocks) stays L2-resident
+// (evict-last) while every row block streams past it once per panel
+// (evict-first; a row block's npanel tiles run concurrently), group_m = 1.
+// Default: GEMM2 with K >= 8192 (Mixtral shape: K = 14336, each 128 x 256
+// tile touches 11 MB of operands, so the row-panel raster's concurrent tiles
+// outgrow L2 and W2 is re-streamed per row group) uses 8-block panels:
+// DRAM reads 13.2 -> 9.4 GB, +37 MHz at the power cap, +1.8 % tokens/s
+// (profiles/r01_gemm_npanel_ab.jsonl); GEMM1 panels raise its traffic.
+// EMOE_GEMM1_NPANEL / EMOE_GEMM2_NPANEL override (0 = off).
+static int npanel_for(int epi, int K) {
+  static const int g1 = [] {
+    const char* v = getenv("EMOE_GEMM1_NPANEL");
+    return v ? atoi(v) : -1;
+  }();
+  static const int g2 = [] {
+    const char* v = getenv("EMOE_GEMM2_NPANEL");
+    return v ? atoi(v) : -1;
+  }();
+  if (epi == EPI_STORE) return g2 >= 0 ? g2 : (K >= 8192 ? 8 : 0);
+  if (epi == EPI_SWIGLU || epi == EPI_RELU) return g1 >= 0 ? g1 : 0;
+  return 0;
+}
+
 static int group_rows(int K, int tile_m) {
   static int panel_env = [] {
     const char* v = getenv("EMOE_GEMM_PANEL_MB");
@@ -652,6 +683,13 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
   p.b_rows_per_slot = b_rows_per_slot;
   p.group_m = group_rows(K, 128 * cta_group);
   l2_hints(p.hint_a, p.hint_b);
+  p.group_n = p.n_blocks;
+  if (const int np = npanel_for(epi, K); np > 0 && np < p.n_blocks) {
+    p.group_n = np;
+    p.group_m = 1;
+    p.hint_a = kCacheEvictFirst;
+    p.hint_b = kCacheEvictLast;
+  }
   p.out = out;
   p.ldo = ldo;
   p.out_f32 = nullptr;
@@ -687,6 +725,7 @@ void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t
   p.n_blocks = N_out / gemm::BN;
   p.b_rows_per_slot = 0;
   p.group_m = group_rows(K, 128);
+  p.group_n = p.n_blocks;
   p.hint_a = kCacheEvictNormal;
   p.hint_b = kCacheEvictNormal;
   p.out = nullptr;
