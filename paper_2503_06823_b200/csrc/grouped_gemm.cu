@@ -685,9 +685,13 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
   l2_hints(p.hint_a, p.hint_b);
   p.group_n = p.n_blocks;
   if (const int np = npanel_for(epi, K); np > 0 && np < p.n_blocks) {
+    static const bool a_first = [] {  // EMOE_GEMM_PANEL_A_NORMAL=1: row blocks evict-normal (A/B runs)
+      const char* v = getenv("EMOE_GEMM_PANEL_A_NORMAL");
+      return !(v && v[0] == '1');
+    }();
     p.group_n = np;
     p.group_m = 1;
-    p.hint_a = kCacheEvictFirst;
+    p.hint_a = a_first ? kCacheEvictFirst : kCacheEvictNormal;
     p.hint_b = kCacheEvictLast;
   }
   p.out = out;
