@@ -285,3 +285,36 @@ def test_top1_fused_combine_bit_identical(args, tmp_path):
         outs.append(torch.load(out))
     assert outs[0]["fused"] and not outs[1]["fused"]
     assert torch.equal(outs[0]["y"], outs[1]["y"])
+
+
+_RASTER_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+from helpers import build_layer
+layer, _, _ = build_layer(8, 768, 2048, 2, "bf16", "swiglu", "topk_softmax", 4, [1, 3, 4, 6], max_tokens=3000,
+                          gemm_cta_group={cg})
+x = torch.randn(2999, 768, generator=torch.Generator().manual_seed(5)).to(torch.bfloat16).cuda()
+torch.save(layer.forward(x).cpu(), {out!r})
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cg", [1, 2])
+def test_column_panel_raster_bit_identical(cg, tmp_path):
+    """The tile order (row panels vs column panels with their L2 policies,
+    the long-K GEMM2 default) never changes a tile's arithmetic: outputs are
+    bit-identical across rasters."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    outs = []
+    for env in ({"EMOE_GEMM1_NPANEL": "0", "EMOE_GEMM2_NPANEL": "0"},
+                {"EMOE_GEMM1_NPANEL": "5", "EMOE_GEMM2_NPANEL": "1"}):
+        out = tmp_path / f"y{len(outs)}.pt"
+        code = _RASTER_SCRIPT.format(root=str(root), tests=str(root / "tests"), cg=cg, out=str(out))
+        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, **env), timeout=300)
+        outs.append(torch.load(out))
+    assert torch.equal(outs[0], outs[1])
