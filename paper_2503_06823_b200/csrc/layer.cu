@@ -391,8 +391,9 @@ struct emoe_layer {
     }
     static const int n_chunks = [] {  // EMOE_H2D_CHUNKS overrides for tuning
       const char* v = getenv("EMOE_H2D_CHUNKS");
-      // 4 measured best of {2, 4, 8, 16} with the async two-staging-set pipeline
-      return v ? std::max(1, atoi(v)) : 4;
+      // 2: best of {1, 2, 4} with the async two-staging-set pipeline over 20
+      // calls (profiles/r01_e2e_chunks_s40.jsonl; 1-4 are within 1.5 %)
+      return v ? std::max(1, atoi(v)) : 2;
     }();
     int64_t chunk = std::max<int64_t>(8192, ceil_div(T, n_chunks));
     chunk = ceil_div(chunk, kRouteBlockTokens) * kRouteBlockTokens;
