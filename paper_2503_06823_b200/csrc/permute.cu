@@ -274,7 +274,12 @@ void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int 
   const size_t smem = (4 * (size_t)E + (size_t)RT * k) * sizeof(int32_t);
   // few token blocks (small T): split each block's rows by columns over
   // gridDim.y blocks so the gather still spans the GPU (>= 8 x 16 B per row slice)
-  const int ny = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * 148, nblocks), row_bytes / 16 / 8));
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  const int ny = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * sms, nblocks), row_bytes / 16 / 8));
   permute_kernel<false><<<dim3(nblocks, ny), PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
                                                                served_idx, seg_offsets, block_base,
                                                                static_cast<uint8_t*>(x_perm), pos, row_token,
