@@ -1,0 +1,123 @@
+"""Parity at BASELINE.json's full sizes (configs 2 and 3: T = 65,536 tokens,
+the Mixtral- and Switch-shaped layers) on the GPU.
+
+The CPU oracle cannot run the whole FFN at these sizes in a test, so the
+checks are the ones that do not depend on size:
+  * routing of every token bit-exact against the oracle given the GPU's
+    logits; the logits themselves against fp32 accumulation on sampled tokens
+  * counts, padded offsets, positions and row sources bit-exact for every
+    token; positions unique, segments stable in token order
+  * expert FFN rows on a sample from every active expert and end-to-end
+    outputs on sampled tokens against the oracle chain (mirrored bf16
+    rounding, the bf16 tolerance)
+  * conservation: every served (token, expert) pair owns exactly one row
+"""
+import numpy as np
+import pytest
+import torch
+
+from helpers import assert_bf16_close, to_f32
+
+pytestmark = pytest.mark.gpu
+
+
+def full_layer(E, d, f, k, act, wm, resident, T):
+    from paper_2503_06823_b200 import MoELayer
+
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    layer = MoELayer(d, f, E, k, activation=act, dtype="bf16", weight_mode=wm, num_slots=len(resident),
+                     max_tokens=T)
+    wg = (torch.randn(E, d, generator=g, device="cuda") / d ** 0.5).to(torch.bfloat16)
+    layer.set_gate(wg)
+    experts = {}
+    for e in resident:  # only the resident set is ever loaded
+        w1 = (torch.randn(f, d, generator=g, device="cuda") / d ** 0.5).to(torch.bfloat16)
+        w3 = (torch.randn(f, d, generator=g, device="cuda") / d ** 0.5).to(torch.bfloat16) if act == "swiglu" else None
+        w2 = (torch.randn(d, f, generator=g, device="cuda") / f ** 0.5).to(torch.bfloat16)
+        layer.register_expert(e, w1, w3, w2)
+        experts[e] = (w1, w3, w2)
+    layer.load_initial(resident)
+    x = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    return layer, wg, experts, x
+
+
+@pytest.mark.parametrize("cfg", ["config2_mixtral", "config3_switch"])
+def test_full_size_parity(cfg, port):
+    from oracle.oracle import bf16_round
+
+    if cfg == "config2_mixtral":
+        E, d, f, k, act, wm, resident = 8, 4096, 14336, 2, "swiglu", "topk_softmax", [0, 5, 6, 7]
+    else:
+        E, d, f, k, act, wm = 128, 768, 3072, 1, "relu", "full_softmax"
+        resident = sorted(np.random.default_rng(26).choice(128, 26, replace=False).tolist())
+    T = 65536
+    layer, wg, experts, x = full_layer(E, d, f, k, act, wm, resident, T)
+    y = layer.forward(x)
+    torch.cuda.synchronize()
+    ws = {key: (None if v is None else v.clone()) for key, v in layer.workspace().items()}
+    res = layer.residency()
+    rng = np.random.default_rng(0)
+
+    # logits: fp32 accumulation on sampled tokens
+    lg = to_f32(ws["logits"])
+    sample = rng.choice(T, 256, replace=False)
+    ref_lg = port.gate_logits(to_f32(x[torch.from_numpy(sample).cuda()]), to_f32(wg))
+    assert np.abs(lg[sample] - ref_lg).max() / np.abs(ref_lg).max() < 1e-4
+    # routing of every token, bit-exact given the GPU logits
+    o = port.gate_route(lg, k, 0 if wm == "topk_softmax" else 1, res)
+    served = ws["served_idx"].cpu().numpy()
+    assert np.array_equal(served, o["served_idx"])
+    assert np.array_equal(ws["route_expert"].cpu().numpy(), o["route_expert"])
+    assert np.array_equal(ws["route_rank"].cpu().numpy(), o["route_rank"])
+    assert np.array_equal(ws["route_hit"].cpu().numpy(), o["route_hit"])
+    np.testing.assert_allclose(ws["served_w"].cpu().numpy(), o["served_w"], rtol=2e-6, atol=1e-7)
+    # permutation of every token, bit-exact; conservation and stability
+    counts, offsets, pos, src = port.permute(served, E, layer.seg_pad)
+    assert np.array_equal(ws["counts"].cpu().numpy(), counts)
+    assert np.array_equal(ws["seg_offsets"].cpu().numpy(), offsets)
+    gpos = ws["pos"].cpu().numpy().astype(np.int64)
+    assert np.array_equal(gpos, pos)
+    R = int(offsets[-1])
+    row_token = ws["row_token"][:R].cpu().numpy()
+    assert np.array_equal(row_token, src)
+    valid = gpos[gpos >= 0]
+    assert valid.size == int((served >= 0).sum()) == int(counts.sum())
+    assert np.unique(valid).size == valid.size
+    for e in np.flatnonzero(counts):
+        seg = row_token[offsets[e]:offsets[e] + counts[e]]
+        assert np.all(np.diff(seg) > 0), f"segment {e} not in token order"
+    # expert FFN rows (through y for the fused top-1 combine) and end-to-end tokens
+    y32 = to_f32(y)
+    host_w = {}
+
+    def weights(e):
+        if e not in host_w:
+            host_w[e] = tuple(None if w is None else to_f32(w) for w in experts[e])
+        return host_w[e]
+
+    # 16 rows per expert: at K = 4096 / 14336 the norm-wise GPU-vs-mirrored
+    # error is ~8.5e-4 (profiles/r01_fullsize_error_budget.txt); a 3-row
+    # sample scatters around it by +-25 %
+    for e in np.flatnonzero(counts)[:8]:
+        rows = rng.choice(np.arange(offsets[e], offsets[e] + counts[e]), size=min(16, int(counts[e])), replace=False)
+        toks = src[rows]
+        w1, w3, w2 = weights(int(e))
+        xs = to_f32(x[torch.from_numpy(toks).cuda()])
+        ref = port.expert_ffn(xs, w1, w3, w2, 0 if act == "swiglu" else 1, True)
+        if ws["y_perm"] is not None:
+            assert_bf16_close(to_f32(ws["y_perm"][torch.from_numpy(rows).cuda()]), ref, f"expert {e} rows")
+        else:  # top-1 fused combine: y[t] = bf16(w_t * bf16(Y_row))
+            w = o["served_w"][toks, 0].astype(np.float32)[:, None]
+            assert_bf16_close(y32[toks], bf16_round(w * ref), f"expert {e} rows (fused combine)")
+    toks = rng.choice(T, 16, replace=False)
+    yref = np.zeros((toks.size, d), np.float32)
+    for i, t in enumerate(toks):
+        for j in range(k):
+            e = served[t, j]
+            if e < 0:
+                continue
+            w1, w3, w2 = weights(int(e))
+            ye = port.expert_ffn(to_f32(x[int(t):int(t) + 1]), w1, w3, w2, 0 if act == "swiglu" else 1, True)[0]
+            yref[i] += np.float32(o["served_w"][t, j]) * ye
+    assert_bf16_close(y32[toks], bf16_round(yref), "end-to-end tokens")
+    layer.close()
