@@ -48,7 +48,11 @@ def test_route_tokens_random_vs_reference(seed, ref):
 
 # ---------------- A6 fit / dominant / sets ----------------
 @pytest.mark.parametrize("case", [(3, 8, 2, 0.6, 0.8, 40, 64), (1, 8, 2, 0.6, 0.8, 30, 2048), (6, 128, 1, 0.5, 0.9, 20, 300),
-                                  (4, 32, 4, 0.3, 0.4, 25, 17)])
+                                  (4, 32, 4, 0.3, 0.4, 25, 17),
+                                  # BASELINE sizes: config 2/3 history (200 prompts of 2048 tokens),
+                                  # config 5 (32 layers, 8k-token prompts)
+                                  (1, 8, 2, 0.6, 0.8, 200, 2048), (1, 128, 1, 0.6, 0.8, 200, 2048),
+                                  (32, 8, 2, 0.6, 0.8, 40, 8192)])
 def test_fit_matches_reference(case, ref):
     m, E, k, ll, pl, P, T = case
     tr = ref.gen_routing_trace(m, E, k, ll, pl, 0, 17, P, T)
