@@ -102,6 +102,7 @@ struct Params {
   // while the weight tiles stream past it
   uint64_t hint_a, hint_b;
   int group_n;  // column panel width in n-blocks (>= n_blocks: whole width)
+  uint64_t hint_out;  // L2 policy of the TMA output stores (0: none)
 };
 
 struct TileCoord {
@@ -169,6 +170,13 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {  // arrive on 
 }
 
 // ---- TMA bulk store of the epilogue boxes ----
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* desc, const void* smem_src, int32_t c0,
+                                                  int32_t c1, uint64_t hint) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+                   reinterpret_cast<uint64_t>(desc)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "l"(hint)
+               : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* desc, const void* smem_src, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(desc)),
@@ -211,7 +219,10 @@ __device__ __forceinline__ void store_box(const Params& p, const CUtensorMap* tm
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
-      tma_store_2d(tmap_out, stage_box, col, (int32_t)row0);
+      if (p.hint_out)
+        tma_store_2d_hint(tmap_out, stage_box, col, (int32_t)row0, p.hint_out);
+      else
+        tma_store_2d(tmap_out, stage_box, col, (int32_t)row0);
       bulk_commit();
     }
   } else {
@@ -684,6 +695,13 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
   p.group_m = group_rows(K, 128 * cta_group);
   l2_hints(p.hint_a, p.hint_b);
   p.group_n = p.n_blocks;
+  {  // EMOE_GEMM_STORE_HINT: 0 none (default), 1 evict-first, 2 evict-last (A/B runs)
+    static const int sh = [] {
+      const char* v = getenv("EMOE_GEMM_STORE_HINT");
+      return v ? atoi(v) : 0;
+    }();
+    p.hint_out = sh == 1 ? kCacheEvictFirst : (sh == 2 ? kCacheEvictLast : 0);
+  }
   if (const int np = npanel_for(epi, K); np > 0 && np < p.n_blocks) {
     static const bool a_first = [] {  // EMOE_GEMM_PANEL_A_NORMAL=1: row blocks evict-normal (A/B runs)
       const char* v = getenv("EMOE_GEMM_PANEL_A_NORMAL");
@@ -730,6 +748,7 @@ void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t
   p.b_rows_per_slot = 0;
   p.group_m = group_rows(K, 128);
   p.group_n = p.n_blocks;
+  p.hint_out = 0;
   p.hint_a = kCacheEvictNormal;
   p.hint_b = kCacheEvictNormal;
   p.out = nullptr;
