@@ -295,8 +295,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="emoe", choices=["emoe", "reference"])
-    ap.add_argument("--config", default="mixtral", choices=list(CONFIGS) + ["stream"],
-                    help="stream = BASELINE config 5 (mixed-task 8k-token prompt stream over a 32-layer stack)")
+    ap.add_argument("--config", default="mixtral", choices=list(CONFIGS) + ["stream", "stack"],
+                    help="stream = BASELINE config 5 (mixed-task 8k-token prompt stream over a 32-layer stack); "
+                         "stack = BASELINE config 4 (32-layer Mixtral-shaped stack, 32 x 2048 tokens per GPU)")
     ap.add_argument("--stream-layers", type=int, default=32)
     ap.add_argument("--stream-prompts", type=int, default=80)
     ap.add_argument("--residency", default="predicted", choices=["predicted", "dynamic"],
@@ -315,6 +316,8 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.config == "stream":
         return main_stream(args)
+    if args.config == "stack":
+        return main_stack(args)
     cfg = CONFIGS[args.config]
 
     import torch
@@ -697,6 +700,146 @@ def main_stream(args):
                note=flops_note, served=served)
     print(json.dumps(res), flush=True)
     stack.close()
+
+
+def main_stack(args):
+    """BASELINE config 4 without the exchange: a 32-layer Mixtral-shaped stack
+    (E=8, top-2, 4 predicted-resident experts per layer, bf16), 32 x 2048
+    tokens per GPU per step, layers chained (y of layer l is x of layer l+1)
+    on one shared activation workspace, routing-driven by the reference
+    Markov trace (per-layer gate logits embed it), resident sets from one GPU
+    predictor invocation.  A step = the forward through all layers + the A6
+    histogram update of the batch.  N > 1: replicas (each GPU its own batch,
+    weak scaling); the expert-parallel form is bench.py --parallel ep."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2503_06823_b200 as emoe
+    from paper_2503_06823_b200 import _lib
+    from paper_2503_06823_b200.serving import MoEStack, StreamConfig, TaskSpec, moesim_prompt_sets
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    m, E, k, L, d, f, P, Tp = args.stream_layers, 8, 2, 4, 4096, 14336, 32, 2048
+    T = P * Tp
+    cfg = StreamConfig(m=m, E=E, k=k, L=L, d=d, f=f, tokens_per_prompt=T, period=40, mode=0,
+                       tasks={"conv": TaskSpec(256.0, [1] * m)})
+    P_train = 60
+    trace = emoe.gen_routing_trace(emoe.ModelShape(m, E, k), 0.6, 0.8, 0, 17, P_train + P * world, Tp)
+    g = torch.Generator(device=device).manual_seed(1234)
+    host = [tuple((torch.randn(*sh, generator=g, device=device) / sh[1] ** 0.5).to(torch.bfloat16).cpu()
+                  .pin_memory() for sh in ((f, d), (f, d), (d, f))) for _ in range(E)]
+    stack = MoEStack(cfg, host, [torch.zeros(E, d, dtype=torch.bfloat16) for _ in range(m)])
+    trace_dev = torch.from_numpy(trace).to(device)
+    stack.fit(trace_dev[:P_train].contiguous(), ["conv"] * P_train)
+    _, sets = moesim_prompt_sets(trace_dev, P_train - 1)
+    ops, _, _ = stack.invocation(sets, [("conv", Tp)] * P)
+    stack.apply(ops)
+    for layer in stack.layers:
+        layer.poll_loads(blocking=True)
+    torch.cuda.synchronize()
+    serve = trace_dev[P_train + rank * P: P_train + (rank + 1) * P].contiguous()  # [P][m][Tp][k]
+    ch = serve.permute(1, 0, 2, 3).reshape(m, T, k).long()
+    lg = torch.rand(m, T, E, generator=g, device=device) * 8.0 - 4.0
+    for r in range(k):
+        lg.scatter_(2, ch[:, :, r:r + 1], 8.0 - r)
+    x = torch.randn(T, d, generator=g, device=device).to(torch.bfloat16)
+    bufs = [torch.empty_like(x), torch.empty_like(x)]
+    tid = torch.zeros(P, dtype=torch.int32, device=device)
+    stream = torch.cuda.current_stream()
+    import ctypes as C
+
+    def step(src=None):
+        h = x if src is None else src
+        for l, layer in enumerate(stack.layers):
+            h = layer.forward(h, logits=lg[l], out=bufs[l % 2])
+        emoe.moesim.check(_lib.lib.emoe_hist_update(stack.pred.h, C.c_void_p(serve.data_ptr()), P, Tp,
+                                                    C.c_void_p(tid.data_ptr()), C.c_void_p(stream.cuda_stream)))
+        return h
+
+    # served rows per layer (for the FFN FLOP count)
+    S_total = 0
+    h = x
+    for l, layer in enumerate(stack.layers):
+        h = layer.forward(h, logits=lg[l], out=bufs[l % 2])
+        S_total += int(layer.workspace()["counts"].sum().item())
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    for layer in stack.layers:
+        layer.set_profiling(True)
+    launches0 = _lib.lib.emoe_kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = int(_lib.lib.emoe_kernel_launches() - launches0)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    gemm_ms = 0.0
+    for layer in stack.layers:
+        st = layer.stage_times()
+        gemm_ms += st["gemm1"] + st["gemm2"]
+        layer.set_profiling(False)
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * T / (ms / 1e3)
+    # end to end: pinned host x in, the stack, y back to host, every step
+    x_host = x.cpu().pin_memory()
+    y_host = torch.empty_like(x_host).pin_memory()
+    x_dev = torch.empty_like(x)
+    e2e_steps = max(2, args.steps // 2)
+    step(x_dev.copy_(x_host, non_blocking=True))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        y_host.copy_(step(x_dev.copy_(x_host, non_blocking=True)), non_blocking=True)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    peaks = load_peaks()
+    ffn_flops = 2.0 * 3 * d * f * S_total
+    achieved = ffn_flops / (gemm_ms / 1e3) / 1e12
+    out = dict(metric=METRIC, value=round(value, 1), unit="tokens/s", n_gpus=world, steps=args.steps,
+               warmup=args.warmup, ms_per_step=round(ms, 3), higher_is_better=True, scaling="weak",
+               vs_baseline=None, dtype="bf16",
+               data="synthetic (random-init weights; routing-driven from the reference Markov trace)",
+               config=dict(workload=f"BASELINE config 4 (without the exchange): {m}-layer Mixtral-shaped MoE stack "
+                                    f"bf16, 8 experts top-2, 4 predicted resident per layer, {P} x {Tp} tokens per "
+                                    "GPU through every layer", layers=m, tokens_per_step=T,
+                           served_rows_all_layers=S_total, workspace="one shared activation workspace",
+                           parallelism=f"replicas{world}" if world > 1 else "single",
+                           l2="inputs larger than L2: x is %.0f MB per layer" % (T * d * 2 / 1e6)),
+               roofline=dict(bound="tensor", achieved=round(achieved, 1), peak=peaks["bf16_sustained"],
+                             unit="TFLOP/s", frac=round(achieved / peaks["bf16_sustained"], 4),
+                             kernel="grouped_gemm_kernel (GEMM1 + GEMM2 of every layer), stage events",
+                             algorithmic=f"2*3*d*f*S summed over layers = {ffn_flops:.4g} FLOP per step"),
+               e2e=dict(value=world * T / e2e_s, unit="tokens/s", h2d_bytes_per_step=x_host.numel() * 2,
+                        d2h_bytes_per_step=y_host.numel() * 2, ms_per_step=e2e_s * 1e3),
+               gpu_launches=launches, clocks=clk.summary(), per_layer_ms=round(ms / m, 3),
+               resident_per_layer=[[int(e) for e in np.flatnonzero(layer.residency())] for layer in stack.layers[:4]])
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    stack.close()
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main_reference(args, cfg, rank, world):

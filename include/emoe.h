@@ -238,6 +238,15 @@ typedef struct {
 } emoe_workspace;
 int emoe_layer_workspace(emoe_layer* layer, emoe_workspace* out);
 
+/* Run `layer` on `donor`'s workspace (routing outputs, permutation and the
+ * FFN row buffers: ~6.5 GB for a Mixtral-shaped layer at 65,536 tokens)
+ * instead of its own, which is released: a stack of layers executed one
+ * after another on one stream needs one workspace, not one per layer.  Same
+ * shape, dtype, max_tokens and GEMM tiling required; the donor must outlive
+ * the borrower and the two must not run concurrently.  The workspace views
+ * (emoe_layer_workspace) of both then describe whichever ran last. */
+int emoe_layer_share_workspace(emoe_layer* layer, const emoe_layer* donor);
+
 /* Measurement hooks (no reference counterpart): CUDA events between the
  * forward's stages on the forward's stream; ms[5] = route, scan+permute,
  * FFN GEMM1, FFN GEMM2, combine, averaged over the profiled forwards since

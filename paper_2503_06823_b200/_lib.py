@@ -68,6 +68,7 @@ _decl("emoe_layer_wait_host", vp)
 _decl("emoe_route", vp, vp, vp, i64, vp)
 _decl("emoe_layer_gate_demand", vp, vp, vp)
 _decl("emoe_layer_workspace", vp, C.POINTER(Workspace))
+_decl("emoe_layer_share_workspace", vp, vp)
 _decl("emoe_route_permute", vp, vp, vp, i64, vp)
 _decl("emoe_layer_set_route_residency", vp, vp, vp)
 _decl("emoe_ffn_segments", vp, vp, i64, vp, vp, C.c_int, vp, vp, vp)
@@ -110,7 +111,7 @@ EXPORTED = [
     "emoe_layer_begin_load", "emoe_layer_poll_loads", "emoe_layer_residency", "emoe_layer_last_load_stats",
     "emoe_moe_forward", "emoe_moe_forward_host", "emoe_moe_forward_host_async", "emoe_layer_wait_host", "emoe_route", "emoe_layer_gate_demand", "emoe_route_permute", "emoe_layer_set_route_residency",
     "emoe_ffn_segments", "emoe_combine", "emoe_ep_create", "emoe_ep_ipc_handle", "emoe_ep_open_peers",
-    "emoe_ep_forward", "emoe_ep_status", "emoe_ep_destroy", "emoe_layer_workspace", "emoe_layer_set_profiling",
+    "emoe_ep_forward", "emoe_ep_status", "emoe_ep_destroy", "emoe_layer_workspace", "emoe_layer_share_workspace", "emoe_layer_set_profiling",
     "emoe_layer_stage_times", "emoe_kernel_launches", "emoe_predictor_create",
     "emoe_predictor_destroy", "emoe_predictor_reset", "emoe_predictor_break_chain", "emoe_hist_update", "emoe_hist_update_host", "emoe_predictor_counts_host",
     "emoe_predictor_set_counts_host", "emoe_prompt_expert_sets", "emoe_predict_host",

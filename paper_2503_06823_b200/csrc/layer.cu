@@ -114,6 +114,9 @@ struct emoe_layer {
   void* y_out = nullptr;
   int* err_flag = nullptr;
   int64_t last_T = 0;
+  // workspace borrowed from another layer (emoe_layer_share_workspace): the
+  // buffers below the routing tables belong to the donor and are not freed here
+  bool borrowed_ws = false;
   unsigned long long* demand_dev = nullptr;  // emoe_layer_gate_demand scratch
 
   CUtensorMap ta1{}, tb1{}, tb3{}, ta2{}, tb2{}, to1{}, to2{};
@@ -510,17 +513,24 @@ struct emoe_layer {
   std::vector<uint8_t> host_owned;         // 1 = library-owned pinned copy, 0 = caller pointer
   cudaStream_t load_stream() const { return ext_copy_stream ? ext_copy_stream : copy_stream; }
 
+  // the per-forward workspace (routing outputs, permutation, FFN rows)
+  std::vector<void*> workspace_buffers() const {
+    return {(void*)logits,       (void*)topk,   (void*)r_expert,    (void*)r_rank,    (void*)r_hit,
+            (void*)served_idx,   (void*)served_w, (void*)block_counts, (void*)counts, (void*)seg_offsets,
+            (void*)block_base,   (void*)pos,    (void*)row_token,   x_perm,           h,
+            y_perm,              (void*)x_hi,   (void*)x_lo,        (void*)h_lo};
+  }
+
   void destroy() {
     auto f = [](void* p) {
       if (p) cudaFree(p);
     };
+    if (!borrowed_ws)
+      for (void* p : workspace_buffers()) f(p);
     for (void* p : {(void*)wg, w1_pool, w3_pool, w2_pool, (void*)slot_dev, (void*)resident_dev, (void*)scores_dev,
-                    (void*)route_resident_dev, wg_pad, (void*)demand_dev,
-                    (void*)logits, (void*)topk, (void*)r_expert, (void*)r_rank, (void*)r_hit, (void*)served_idx,
-                    (void*)served_w, (void*)block_counts, (void*)counts, (void*)seg_offsets, (void*)block_base,
-                    (void*)pos, (void*)row_token, x_perm, h, y_perm, x_in, y_out, (void*)err_flag, x_stage[0],
-                    x_stage[1], y_stage[0], y_stage[1], w1_lo, w3_lo, w2_lo, (void*)x_hi, (void*)x_lo,
-                    (void*)h_lo, (void*)sx_hi, (void*)sx_lo, (void*)sh_lo})
+                    (void*)route_resident_dev, wg_pad, (void*)demand_dev, x_in, y_out, (void*)err_flag, x_stage[0],
+                    x_stage[1], y_stage[0], y_stage[1], w1_lo, w3_lo, w2_lo, (void*)sx_hi, (void*)sx_lo,
+                    (void*)sh_lo})
       f(p);
     for (auto* v : {&host_w1, &host_w3, &host_w2})
       for (size_t e = 0; e < v->size(); ++e)
@@ -685,6 +695,51 @@ int emoe_layer_destroy(emoe_layer* layer) {
     cudaDeviceSynchronize();
     layer->destroy();
     delete layer;
+  });
+}
+
+int emoe_layer_share_workspace(emoe_layer* L, const emoe_layer* donor) {
+  return guard([&] {
+    EMOE_REQUIRE(L && donor && L != donor, "share_workspace: need two distinct layers");
+    EMOE_REQUIRE(!donor->borrowed_ws, "share_workspace: the donor must own its workspace");
+    const emoe_layer_config &a = L->cfg, &b = donor->cfg;
+    EMOE_REQUIRE(a.d_model == b.d_model && a.d_ff == b.d_ff && a.num_experts == b.num_experts &&
+                     a.top_k == b.top_k && a.dtype == b.dtype && a.max_tokens == b.max_tokens &&
+                     L->rows_cap == donor->rows_cap && L->tf32 == donor->tf32,
+                 "share_workspace: layers differ in shape, dtype, max_tokens or GEMM tiling");
+    EMOE_CUDA(cudaDeviceSynchronize());  // nothing in flight on the buffers being released
+    if (!L->borrowed_ws)
+      for (void* p : L->workspace_buffers())
+        if (p) EMOE_CUDA(cudaFree(p));
+    L->logits = donor->logits;
+    L->topk = donor->topk;
+    L->r_expert = donor->r_expert;
+    L->r_rank = donor->r_rank;
+    L->r_hit = donor->r_hit;
+    L->served_idx = donor->served_idx;
+    L->served_w = donor->served_w;
+    L->block_counts = donor->block_counts;
+    L->counts = donor->counts;
+    L->seg_offsets = donor->seg_offsets;
+    L->block_base = donor->block_base;
+    L->pos = donor->pos;
+    L->row_token = donor->row_token;
+    L->x_perm = donor->x_perm;
+    L->h = donor->h;
+    L->y_perm = donor->y_perm;
+    L->x_hi = donor->x_hi;
+    L->x_lo = donor->x_lo;
+    L->h_lo = donor->h_lo;
+    // tensor maps over the (now shared) activation buffers; the weight maps stay
+    L->ta1 = donor->ta1;
+    L->ta2 = donor->ta2;
+    L->to1 = donor->to1;
+    L->to2 = donor->to2;
+    L->op1.a_hi = donor->op1.a_hi;
+    L->op1.a_lo = donor->op1.a_lo;
+    L->op2.a_hi = donor->op2.a_hi;
+    L->op2.a_lo = donor->op2.a_lo;
+    L->borrowed_ws = true;
   });
 }
 

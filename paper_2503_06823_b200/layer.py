@@ -215,6 +215,11 @@ class MoELayer:
         check(lib.emoe_layer_stage_times(self.h, ms))
         return dict(zip(["route", "permute", "gemm1", "gemm2", "combine"], [float(v) for v in ms]))
 
+    def share_workspace(self, donor: "MoELayer") -> None:
+        """Run on `donor`'s workspace (released here); see emoe_layer_share_workspace."""
+        check(lib.emoe_layer_share_workspace(self.h, donor.h))
+        self._ws_donor = donor  # keep the owner alive
+
     def workspace(self) -> Dict[str, torch.Tensor]:
         """Views of the last forward's intermediates (valid until the next call)."""
         w = Workspace()

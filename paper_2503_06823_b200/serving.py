@@ -61,9 +61,13 @@ class StreamConfig:
 
 
 class MoEStack:
-    """m MoE layers sharing pinned host experts, one copy stream and one predictor."""
+    """m MoE layers sharing pinned host experts, one copy stream, one predictor
+    and (share_workspace) one activation workspace: the layers run one after
+    another on one stream, so layer 0's routing/permutation/FFN buffers serve
+    all of them (a Mixtral-shaped layer at 65,536 tokens needs ~6.5 GB)."""
 
-    def __init__(self, cfg: StreamConfig, host_experts: Sequence, gate_weights: Sequence[torch.Tensor]):
+    def __init__(self, cfg: StreamConfig, host_experts: Sequence, gate_weights: Sequence[torch.Tensor],
+                 share_workspace: bool = True):
         self.cfg = cfg
         self.names = sorted(cfg.tasks)
         self.copy_stream = torch.cuda.Stream()
@@ -71,6 +75,8 @@ class MoEStack:
         for l in range(cfg.m):
             layer = MoELayer(cfg.d, cfg.f, cfg.E, cfg.k, activation=cfg.activation, num_slots=cfg.L,
                              max_tokens=cfg.tokens_per_prompt)
+            if share_workspace and self.layers:
+                layer.share_workspace(self.layers[0])
             layer.set_gate(gate_weights[l])
             layer.set_copy_stream(self.copy_stream)
             for e, (w1, w3, w2) in enumerate(host_experts):
@@ -79,7 +85,7 @@ class MoEStack:
         self.pred = moesim._Pred(cfg.m, cfg.E, cfg.k, len(self.names), 0.01)
 
     def close(self):
-        for layer in self.layers:
+        for layer in reversed(self.layers):  # borrowers before the workspace owner
             layer.close()
 
     # -- predictor --------------------------------------------------------------

@@ -138,3 +138,32 @@ def test_profile_cost_model_is_a_valid_reference_cost(ref):
     assert cost["predictor_invocation_cost"] > 0 and cost["contention_factor"] >= 1.0
     assert np.array_equal(np.stack([layer.residency() for layer in stack.layers]), before)
     stack.close()
+
+
+def test_stack_shared_workspace_bit_identical():
+    """A stack whose layers share one workspace (the default) computes the
+    same outputs, layer by layer, as one with a workspace per layer; a layer
+    chain (y of layer l feeds layer l+1) exercises the reuse."""
+    from paper_2503_06823_b200.serving import MoEStack, StreamConfig
+
+    m, E, k, L, d, f, T = 3, 8, 2, 4, 256, 512, 700
+    cfg = StreamConfig(m=m, E=E, k=k, L=L, d=d, f=f, tokens_per_prompt=1024, period=4, mode=0, tasks={})
+    g = torch.Generator().manual_seed(9)
+    host = [tuple((torch.randn(*s, generator=g) / s[1] ** 0.5).to(torch.bfloat16).pin_memory()
+                  for s in ((f, d), (f, d), (d, f))) for _ in range(E)]
+    gates = [(torch.randn(E, d, generator=g) / d ** 0.5).to(torch.bfloat16) for _ in range(m)]
+    x = torch.randn(T, d, generator=g).to(torch.bfloat16).cuda()
+    outs = []
+    for share in (True, False):
+        stack = MoEStack(cfg, host, gates, share_workspace=share)
+        for l, layer in enumerate(stack.layers):
+            layer.load_initial([(l + j) % E for j in range(L)])
+        h, ys = x, []
+        for layer in stack.layers:
+            h = layer.forward(h)
+            ys.append(h.clone())
+        torch.cuda.synchronize()
+        outs.append(ys)
+        stack.close()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
