@@ -213,10 +213,13 @@ struct PredictArgs {
   int32_t* n_experts;  // [m]
 };
 
-__device__ void predict_block(const PredictArgs& a, int* order, double* row) {
+// l0/l1: the layers of predict_all_layers this block handles (layers are
+// independent in that mode; chained / layerwise ignore the range)
+__device__ void predict_block(const PredictArgs& a, int* order, double* row, int l0 = 0, int l1 = -1) {
   const int E = a.E, k = a.k;
+  if (l1 < 0) l1 = a.m;
   if (a.mode == 0) {  // predict_all_layers
-    for (int l = 0; l < a.m; ++l) {
+    for (int l = l0; l < l1; ++l) {
       mean_rows_block(a.prompt_counts + (int64_t)l * E * E, E, a.s, a.prev_sets + l * k, a.prev_sizes[l], row);
       for (int j = threadIdx.x; j < E; j += blockDim.x) a.scores[(int64_t)l * E + j] = row[j];
       const int n = rank_scores_block(row, E, k, order, a.experts + l * k);
@@ -252,8 +255,9 @@ __global__ void predict_kernel(PredictArgs a) {
 
 // predicted_frequencies (predictor.cpp:222-238)
 __device__ void freq_block(const u64* task_counts, int n_tasks, int m, int E, double s, int task, double* out,
-                           double* raw) {
-  for (int l = 0; l < m; ++l) {
+                           double* raw, int l0 = 0, int l1 = -1) {
+  if (l1 < 0) l1 = m;
+  for (int l = l0; l < l1; ++l) {
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
       double v = 0.0;
       if (task >= 0 && task < n_tasks) {
@@ -289,7 +293,8 @@ struct Eq2Args {
 };
 
 // expected_tokens (expert_store.cpp:59-106): thread per (l, e), tasks in sorted order
-__device__ void eq2_block(const Eq2Args& a, double* tok, int* cnt) {
+__device__ void eq2_block(const Eq2Args& a, double* tok, int* cnt, int l0 = 0, int l1 = -1) {
+  if (l1 < 0) l1 = a.m;
   for (int t = threadIdx.x; t < a.n_tasks; t += blockDim.x) {
     double s = 0.0;
     int c = 0;
@@ -302,9 +307,9 @@ __device__ void eq2_block(const Eq2Args& a, double* tok, int* cnt) {
     cnt[t] = c;
   }
   __syncthreads();
-  const int ME = a.m * a.E;
+  const int ME = (l1 - l0) * a.E;
   for (int i = threadIdx.x; i < ME; i += blockDim.x) {
-    const int l = i / a.E, e = i % a.E;
+    const int l = l0 + i / a.E, e = i % a.E;
     double agg = 0.0;
     for (int t = 0; t < a.n_tasks; ++t) {
       if (cnt[t] == 0) continue;
@@ -316,7 +321,7 @@ __device__ void eq2_block(const Eq2Args& a, double* tok, int* cnt) {
       const double grid = volume * f;
       agg += grid;
     }
-    a.aggregate[i] = agg;
+    a.aggregate[(int64_t)l * a.E + e] = agg;
   }
   __syncthreads();
 }
@@ -349,10 +354,13 @@ struct PlanArgs {
 };
 
 // select_experts + loading_targets + plan_loading (expert_store.cpp:111-195)
-__device__ void plan_block(const PlanArgs& a, int* order) {
+// l0/l1: layer range; accumulate = 0 leaves delta_e / total_loads to
+// plan_finalize_kernel (several blocks, one layer each)
+__device__ void plan_block(const PlanArgs& a, int* order, int l0 = 0, int l1 = -1, bool accumulate = true) {
   const int E = a.E;
   __shared__ int wanted[MAXE];
-  for (int l = 0; l < a.m; ++l) {
+  if (l1 < 0) l1 = a.m;
+  for (int l = l0; l < l1; ++l) {
     const double* row = a.aggregate + (int64_t)l * E;
     ranked_indices_block(row, E, order);
     if (!a.targets_given && threadIdx.x == 0) {
@@ -389,12 +397,14 @@ __device__ void plan_block(const PlanArgs& a, int* order) {
       a.n_evict[l] = ne;
       a.n_load[l] = nl;
       a.duration[l] = (double)nl * a.per_expert;
-      if (l == 0) {
-        *a.delta_e = 0.0;
-        *a.total_loads = 0;
+      if (accumulate) {
+        if (l == 0) {
+          *a.delta_e = 0.0;
+          *a.total_loads = 0;
+        }
+        *a.delta_e += a.duration[l];
+        *a.total_loads += nl;
       }
-      *a.delta_e += a.duration[l];
-      *a.total_loads += nl;
     }
     __syncthreads();
   }
@@ -417,19 +427,25 @@ struct InvocationArgs {
   PlanArgs plan;
 };
 
+// predict_all_layers (mode 0): one block per layer -- every step below is
+// per layer -- and plan_finalize_kernel sums delta_e in layer order (the
+// reference's sequential sum, bit for bit); predict_chained (mode 1): one
+// block over all layers (layer l's prediction feeds layer l + 1).
 __global__ void invocation_kernel(InvocationArgs a) {
   __shared__ int order[MAXE];
   __shared__ double row[MAXE];
   __shared__ double tok[MAX_TASKS];
   __shared__ int cnt[MAX_TASKS];
-  predict_block(a.pred, order, row);
-  __syncthreads();
   const int m = a.pred.m, E = a.pred.E;
+  const bool per_layer = gridDim.x > 1;
+  const int l0 = per_layer ? (int)blockIdx.x : 0, l1 = per_layer ? l0 + 1 : m;
+  predict_block(a.pred, order, row, l0, l1);
+  __syncthreads();
   for (int t = 0; t < a.n_tasks; ++t)  // fitted_freq_ per profile (engine.cpp:256-257)
-    freq_block(a.task_counts, a.n_tasks, m, E, a.pred.s, t, a.fitted + (int64_t)t * m * E, row);
+    freq_block(a.task_counts, a.n_tasks, m, E, a.pred.s, t, a.fitted + (int64_t)t * m * E, row, l0, l1);
   // rows[l][e] = score * fitted, normalised (engine.cpp:394-411)
-  for (int i = threadIdx.x; i < a.n_tasks * m; i += blockDim.x) {
-    const int t = i / m, l = i % m;
+  for (int i = threadIdx.x; i < a.n_tasks * (l1 - l0); i += blockDim.x) {
+    const int t = i / (l1 - l0), l = l0 + i % (l1 - l0);
     const double* sc = a.pred.scores + (int64_t)l * E;
     const double* fit = a.fitted + ((int64_t)t * m + l) * E;
     double* rows = a.freqs + ((int64_t)t * m + l) * E;
@@ -445,8 +461,20 @@ __global__ void invocation_kernel(InvocationArgs a) {
     }
   }
   __syncthreads();
-  eq2_block(a.eq2, tok, cnt);
-  plan_block(a.plan, order);
+  eq2_block(a.eq2, tok, cnt, l0, l1);
+  plan_block(a.plan, order, l0, l1, !per_layer);
+}
+
+__global__ void plan_finalize_kernel(PlanArgs a) {
+  if (threadIdx.x != 0) return;
+  double de = 0.0;
+  int nl = 0;
+  for (int l = 0; l < a.m; ++l) {
+    de += a.duration[l];
+    nl += a.n_load[l];
+  }
+  *a.delta_e = de;
+  *a.total_loads = nl;
 }
 
 }  // namespace
@@ -931,9 +959,15 @@ int emoe_invocation_host(emoe_predictor* P, int mode, const int32_t* sets, const
                       0};
     if (P->hist_recorded) EMOE_CUDA(cudaStreamWaitEvent(s, P->hist_done, 0));
     EMOE_CUDA(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, s));
-    invocation_kernel<<<1, 128, 0, s>>>(a);
+    const int blocks = mode == 0 ? m : 1;
+    invocation_kernel<<<blocks, 128, 0, s>>>(a);
     EMOE_CUDA(cudaGetLastError());
     count_launch();
+    if (blocks > 1) {
+      plan_finalize_kernel<<<1, 32, 0, s>>>(a.plan);
+      EMOE_CUDA(cudaGetLastError());
+      count_launch();
+    }
     EMOE_CUDA(cudaMemcpyAsync(h + o_agg, d + o_agg, out_end - o_agg, cudaMemcpyDeviceToHost, s));
     EMOE_CUDA(cudaStreamSynchronize(s));
     std::memcpy(aggregate, h + o_agg, ME * 8);
