@@ -58,6 +58,13 @@ struct Params {
   float* out_hi;  // GEMM1: tf32(H); GEMM2: Y
   float* out_lo;  // GEMM1: H - tf32(H); GEMM2: null
   int64_t ldo;
+  // split-K (few output tiles): work item = (tile, split); split s reduces
+  // k-blocks [s KB / k_splits, (s + 1) KB / k_splits) and stores its raw
+  // fp32 accumulators to partial[s][row][nb * BN + col]; splitk_reduce_kernel
+  // sums the splits in order and applies the epilogue
+  int k_splits;
+  float* partial;
+  int64_t partial_rows;
 };
 
 // D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, 1 CTA
@@ -146,19 +153,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   const int total_mb = s_offs[S] / BM;
   const int total_tiles = total_mb * p.n_blocks;
+  const int total_items = total_tiles * p.k_splits;
   const int k_blocks = p.K / BK;
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int w = blockIdx.x; w < total_items; w += gridDim.x) {
+        const int t = w / p.k_splits, split = w - t * p.k_splits;
         int mb, nb, seg;
         decode(t, total_mb, p.n_blocks, p.group_m, s_offs, S, mb, nb, seg);
         const int slot = p.slot_of_expert[p.seg_expert ? p.seg_expert[seg] : seg];
         const int a_row = mb * BM;
         const int b_row = slot * p.b_rows_per_slot + nb * (EPI == EPI_SWIGLU ? BN / 2 : BN);
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        const int kbeg = split * k_blocks / p.k_splits, kend = (split + 1) * k_blocks / p.k_splits;
+        for (int kb = kbeg; kb < kend; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
           uint8_t* st = smem + stage * STAGE_BYTES;
@@ -194,13 +204,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t chunk = 0;  // chunks issued by this CTA (slot = chunk % SLOTS)
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        for (int kb0 = 0; kb0 < k_blocks; kb0 += CHUNK_KB, ++chunk) {
+      for (int w = blockIdx.x; w < total_items; w += gridDim.x) {
+        const int split = w % p.k_splits;
+        const int kbeg = split * k_blocks / p.k_splits, kend = (split + 1) * k_blocks / p.k_splits;
+        for (int kb0 = kbeg; kb0 < kend; kb0 += CHUNK_KB, ++chunk) {
           const int slot = chunk % SLOTS;
           mbar_wait(&tempty_bar[slot], ((chunk / SLOTS) & 1) ^ 1);
           tc_fence_after();
           const uint32_t tmem_d = tmem_base + slot * BN;
-          const int kb1 = min(k_blocks, kb0 + CHUNK_KB);
+          const int kb1 = min(kend, kb0 + CHUNK_KB);
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&full_bar[stage], phase);
             tc_fence_after();
@@ -227,13 +239,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else {  // ===== epilogue: warps 2..5, TMEM lane quarter = warp % 4
     const int quarter = warp & 3;
     uint32_t chunk = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    for (int w = blockIdx.x; w < total_items; w += gridDim.x) {
+      const int t = w / p.k_splits, split = w - t * p.k_splits;
+      const int kbeg = split * k_blocks / p.k_splits, kend = (split + 1) * k_blocks / p.k_splits;
       int mb, nb, seg;
       decode(t, total_mb, p.n_blocks, p.group_m, s_offs, S, mb, nb, seg);
       float acc[BN];
 #pragma unroll
       for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
-      for (int kb0 = 0; kb0 < k_blocks; kb0 += CHUNK_KB, ++chunk) {
+      for (int kb0 = kbeg; kb0 < kend; kb0 += CHUNK_KB, ++chunk) {
         const int slot = chunk % SLOTS;
         mbar_wait(&tfull_bar[slot], (chunk / SLOTS) & 1);
         tc_fence_after();
@@ -250,6 +264,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) mbar_arrive(&tempty_bar[slot]);
       }
       const int64_t row = (int64_t)mb * BM + quarter * 32 + lane;
+      if (p.k_splits > 1) {  // raw partial sums; the reduce kernel finishes the tile
+        float* dst = p.partial + ((int64_t)split * p.partial_rows + row) * ((int64_t)p.n_blocks * BN) + nb * BN;
+#pragma unroll
+        for (int j = 0; j < BN; j += 4)
+          *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        continue;
+      }
       const int col0 = nb * p.out_block_cols;
       float* ohi = p.out_hi + row * p.ldo + col0;
       float* olo = p.out_lo ? p.out_lo + row * p.ldo + col0 : nullptr;
@@ -304,6 +325,43 @@ __global__ void split_tf32_kernel(const float4* x, float4* hi, float4* __restric
     l.w = v.w - h.w;
     hi[i] = h;
     lo[i] = l;
+  }
+}
+
+// split-K: out = epilogue(sum over splits of partial, in split order); one
+// thread per output element (SwiGLU: gate column c and up column 64 + c of
+// the tile's accumulators)
+template <int EPI>
+__global__ void splitk_reduce_kernel(const float* __restrict__ partial, int k_splits, int64_t rows, int n_blocks,
+                                     int out_block_cols, float* __restrict__ out_hi, float* __restrict__ out_lo,
+                                     int64_t ldo) {
+  const int64_t n_out = rows * (int64_t)n_blocks * out_block_cols;
+  const int64_t acc_cols = (int64_t)n_blocks * BN;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_out; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / ((int64_t)n_blocks * out_block_cols);
+    const int oc = (int)(i - row * (int64_t)n_blocks * out_block_cols);
+    const int nb = oc / out_block_cols, c = oc - nb * out_block_cols;
+    const float* src = partial + row * acc_cols + nb * BN + c;
+    float g = 0.0f, u = 0.0f;
+    for (int sp = 0; sp < k_splits; ++sp) {
+      g += src[(int64_t)sp * rows * acc_cols];
+      if (EPI == EPI_SWIGLU) u += src[(int64_t)sp * rows * acc_cols + BN / 2];
+    }
+    float v;
+    if (EPI == EPI_SWIGLU)
+      v = g / (1.0f + expf(-g)) * u;
+    else if (EPI == EPI_RELU)
+      v = fmaxf(g, 0.0f);
+    else
+      v = g;
+    const int64_t o = row * ldo + oc;
+    if (EPI == EPI_STORE) {
+      out_hi[o] = v;
+    } else {
+      const float h = round_tf32(v);
+      out_hi[o] = h;
+      out_lo[o] = v - h;
+    }
   }
 }
 
@@ -368,7 +426,7 @@ static void launch_kernel(const Tf32Operands& ops, const tf32x3::Params& p, int 
 void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t* seg_offsets,
                                 const int32_t* slot_of_expert, const int32_t* seg_expert, int n_seg, int K, int N_out,
                                 int b_rows_per_slot, float* out_hi, float* out_lo, int64_t ldo, int num_sms,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, const SplitK* split) {
   using namespace tf32x3;
   EMOE_REQUIRE(n_seg >= 1 && n_seg <= MAX_SEGS, "gemm_tf32x3: segment count out of range");
   EMOE_REQUIRE(gemm_tf32x3_supported(epi, K, N_out), "gemm_tf32x3: K % 32 and N % tile must be 0");
@@ -387,12 +445,42 @@ void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t*
   p.out_hi = out_hi;
   p.out_lo = out_lo;
   p.ldo = ldo;
+  p.k_splits = 1;
+  p.partial = nullptr;
+  p.partial_rows = 0;
+  // split-K when even the row capacity gives fewer than two waves of tiles
+  // (small token batches: config 1's GEMM2 has <= 128 tiles for 148 SMs)
+  if (split && split->partial) {
+    const int64_t max_tiles = split->rows / BM * p.n_blocks;
+    int ks = 1;
+    while (ks < 4 && max_tiles * ks < 2 * num_sms && (K / BK) / (2 * ks) >= 2 * CHUNK_KB) ks *= 2;
+    if (ks > 1 && (size_t)ks * split->rows * p.n_blocks * BN <= split->capacity) {
+      p.k_splits = ks;
+      p.partial = split->partial;
+      p.partial_rows = split->rows;
+    }
+  }
   if (epi == EPI_SWIGLU)
     launch_kernel<EPI_SWIGLU>(ops, p, num_sms, stream);
   else if (epi == EPI_RELU)
     launch_kernel<EPI_RELU>(ops, p, num_sms, stream);
   else
     launch_kernel<EPI_STORE>(ops, p, num_sms, stream);
+  if (p.k_splits > 1) {
+    const int64_t n_out = split->rows * p.n_blocks * p.out_block_cols;
+    const int blocks = (int)std::min<int64_t>(ceil_div(n_out, 256), (int64_t)num_sms * 8);
+    if (epi == EPI_SWIGLU)
+      splitk_reduce_kernel<EPI_SWIGLU><<<blocks, 256, 0, stream>>>(p.partial, p.k_splits, split->rows, p.n_blocks,
+                                                                    p.out_block_cols, out_hi, out_lo, ldo);
+    else if (epi == EPI_RELU)
+      splitk_reduce_kernel<EPI_RELU><<<blocks, 256, 0, stream>>>(p.partial, p.k_splits, split->rows, p.n_blocks,
+                                                                  p.out_block_cols, out_hi, out_lo, ldo);
+    else
+      splitk_reduce_kernel<EPI_STORE><<<blocks, 256, 0, stream>>>(p.partial, p.k_splits, split->rows, p.n_blocks,
+                                                                   p.out_block_cols, out_hi, out_lo, ldo);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+  }
 }
 
 }  // namespace emoe

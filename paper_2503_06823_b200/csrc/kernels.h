@@ -122,11 +122,18 @@ bool gemm_tf32x3_supported(int epi, int K, int N_out);
 int gemm_tf32x3_b_box_rows(int epi);
 // x -> tf32(x) in hi (hi may alias x), x - tf32(x) in lo; n % 4 == 0
 void launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t s);
+// split-K scratch for small batches: `rows` = the row capacity of the
+// operands, `capacity` floats at `partial`
+struct SplitK {
+  float* partial;
+  size_t capacity;
+  int64_t rows;
+};
 // GEMM1 (SwiGLU/ReLU): out_hi/out_lo = split(H); GEMM2 (STORE): out_hi = Y
 void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t* seg_offsets,
                                 const int32_t* slot_of_expert, const int32_t* seg_expert, int n_seg, int K, int N_out,
                                 int b_rows_per_slot, float* out_hi, float* out_lo, int64_t ldo, int num_sms,
-                                cudaStream_t stream);
+                                cudaStream_t stream, const SplitK* split = nullptr);
 
 // K4 fp32 path (SIMT FFMA): same grouping/epilogues, fp32 in/out (shapes the
 // 3xTF32 kernel does not tile)

@@ -132,6 +132,9 @@ struct emoe_layer {
   float* x_lo = nullptr;
   float* h_lo = nullptr;
   Tf32Operands op1{}, op2{};
+  // split-K partial sums for small batches (grouped_gemm_tf32.cu)
+  float* splitk = nullptr;
+  size_t splitk_cap = 0;
   // growable scratch for emoe_ffn_segments on caller rows (fp32)
   float* sx_hi = nullptr;
   float* sx_lo = nullptr;
@@ -340,11 +343,12 @@ struct emoe_layer {
         o2.a_lo = make_tmap_f32_2d(hl, (uint64_t)R, f, 128);
       }
       launch_split_tf32(static_cast<const float*>(xr), xh, xl, R * d, s);
+      const SplitK sk{splitk, splitk_cap, R};
       launch_grouped_gemm_tf32x3(epi1, o1, segs, slot_dev, seg_expert, n_seg, d, f, f, static_cast<float*>(hr), hl,
-                                 f, num_sms, s);
+                                 f, num_sms, s, &sk);
       mark(3, s);
       launch_grouped_gemm_tf32x3(EPI_STORE, o2, segs, slot_dev, seg_expert, n_seg, f, d, d, static_cast<float*>(yr),
-                                 nullptr, d, num_sms, s);
+                                 nullptr, d, num_sms, s, &sk);
       mark(4, s);
     } else {
       launch_grouped_gemm_f32(swiglu() ? EPI_SWIGLU : EPI_RELU, static_cast<const float*>(xr), d,
@@ -530,7 +534,7 @@ struct emoe_layer {
     for (void* p : {(void*)wg, w1_pool, w3_pool, w2_pool, (void*)slot_dev, (void*)resident_dev, (void*)scores_dev,
                     (void*)route_resident_dev, wg_pad, (void*)demand_dev, x_in, y_out, (void*)err_flag, x_stage[0],
                     x_stage[1], y_stage[0], y_stage[1], w1_lo, w3_lo, w2_lo, (void*)sx_hi, (void*)sx_lo,
-                    (void*)sh_lo})
+                    (void*)sh_lo, (void*)splitk})
       f(p);
     for (auto* v : {&host_w1, &host_w3, &host_w2})
       for (size_t e = 0; e < v->size(); ++e)
@@ -677,6 +681,15 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
           L->op2.b_lo = make_tmap_f32_2d(L->w2_lo, slots * d, f, bb2);
           L->op2.b2_hi = L->op2.b_hi;
           L->op2.b2_lo = L->op2.b_lo;
+          // split-K scratch when a GEMM has under two waves of tiles even at
+          // the row capacity (up to 4 splits of 128 accumulator columns)
+          size_t need = 0;
+          for (const int nb : {epi1 == EPI_SWIGLU ? (int)f / 64 : (int)f / 128, (int)d / 128})
+            if (L->rows_cap / 128 * nb < 2 * L->num_sms) need = std::max(need, (size_t)4 * L->rows_cap * nb * 128);
+          if (need) {
+            L->splitk = dmalloc<float>(need);
+            L->splitk_cap = need;
+          }
         }
       }
       EMOE_CUDA(cudaDeviceSynchronize());
