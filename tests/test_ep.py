@@ -313,3 +313,34 @@ def test_ep_p2p_fault_status(case, tmp_path):
         assert r0["finite"] and r1["finite"]
     else:
         assert r0["status"] == 1
+
+
+def _gpu_p2p_single_worker(rank, world, port_no, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from helpers import build_layer
+    from paper_2503_06823_b200.ep import PeerExpertParallelMoE
+
+    resident = [1, 2, 6]
+    layer, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", 3, resident, max_tokens=1024)
+    ep = PeerExpertParallelMoE(layer, resident)
+    full, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", 3, resident, max_tokens=1024)
+    x = torch.randn(1000, 256, generator=torch.Generator().manual_seed(2)).to(torch.bfloat16).cuda()
+    y_ep = ep(x)
+    st, rows = ep.status()
+    torch.save(dict(y_ep=y_ep.cpu(), y_1=full.forward(x).cpu(), status=st), Path(out_dir) / "s.pt")
+    ep.close()
+    layer.close()
+    full.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_ep_p2p_single_rank(tmp_path):
+    """World size 1: the peer-memory path degenerates to local stores and a
+    self-barrier and still equals the plain forward."""
+    mp.spawn(_gpu_p2p_single_worker, args=(1, free_port(), str(tmp_path)), nprocs=1, join=True)
+    d = torch.load(tmp_path / "s.pt")
+    assert d["status"] == 0
+    assert torch.equal(d["y_ep"], d["y_1"])
