@@ -138,7 +138,9 @@ int emoe_moe_forward_host(emoe_layer* layer, const void* x_host, void* y_host, i
 /* Asynchronous form for serving loops: enqueues H2D, forward and D2H and
  * returns; consecutive calls alternate two device staging sets, so call i+1's
  * H2D overlaps call i's compute and D2H.  x_host must stay unchanged and y_host
- * unread until emoe_layer_wait_host() returns (it waits for every call made). */
+ * unread until emoe_layer_wait_host() returns (it waits for every call made).
+ * Loads are polled once per call: every chunk of a call sees the same
+ * residency, as one emoe_moe_forward over all T tokens would. */
 int emoe_moe_forward_host_async(emoe_layer* layer, const void* x_host, void* y_host, int64_t T, void* stream);
 int emoe_layer_wait_host(emoe_layer* layer);
 

@@ -256,8 +256,10 @@ struct emoe_layer {
     if (i == 5) ++ev_used;
   }
 
-  void forward(const void* x, const float* logits_in, void* y, int64_t T, cudaStream_t s) {
-    poll(false, s, nullptr);
+  // poll_loads = false: the caller polled already (a chunked host call uses
+  // one residency snapshot for all its chunks)
+  void forward(const void* x, const float* logits_in, void* y, int64_t T, cudaStream_t s, bool poll_loads = true) {
+    if (poll_loads) poll(false, s, nullptr);
     if (T == 0) {
       route(x, logits_in, T, s);
       return;
@@ -415,6 +417,7 @@ struct emoe_layer {
     }
     EMOE_CUDA(cudaStreamWaitEvent(in_stream, x_free[b], 0));
     EMOE_CUDA(cudaStreamWaitEvent(s, y_free[b], 0));
+    poll(false, s, nullptr);  // one residency snapshot for every chunk of this call
     for (int i = 0; i < n; ++i) {
       const int64_t t0 = i * chunk, tn = std::min<int64_t>(chunk, T - t0);
       uint8_t* xd = static_cast<uint8_t*>(x_stage[b]) + t0 * row;
@@ -423,7 +426,7 @@ struct emoe_layer {
                                 cudaMemcpyHostToDevice, in_stream));
       EMOE_CUDA(cudaEventRecord(ev[2 * i], in_stream));
       EMOE_CUDA(cudaStreamWaitEvent(s, ev[2 * i], 0));
-      forward(xd, nullptr, yd, tn, s);
+      forward(xd, nullptr, yd, tn, s, false);
       EMOE_CUDA(cudaEventRecord(ev[2 * i + 1], s));
       EMOE_CUDA(cudaStreamWaitEvent(out_stream, ev[2 * i + 1], 0));
       EMOE_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(y_host) + t0 * row, yd, tn * row, cudaMemcpyDeviceToHost,
