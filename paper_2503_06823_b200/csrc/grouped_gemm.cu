@@ -3,11 +3,15 @@
 // One persistent, warp-specialised kernel computes, for every resident expert
 // e with rows X[off_e : off_e + n_e) of the permuted activations,
 //     out[rows, n-block] = epilogue( X_rows . W_e[n-block rows]^T )
-// with three epilogues:
+// with four epilogues:
 //   EPI_SWIGLU  B tile = 128 rows of W1 + the same 128 rows of W3,
 //               H = silu(X W1^T) * (X W3^T) -> bf16  (GEMM1, Mixtral / synthetic)
 //   EPI_RELU    B tile = 256 rows of W1, H = relu(X W1^T) -> bf16  (GEMM1, Switch)
-//   EPI_STORE   B tile = 256 rows of W2, Y = H W2^T -> bf16          (GEMM2)
+//   EPI_STORE   B tile = 256 rows of W2, Y = H W2^T -> bf16          (GEMM2); or
+//               with the top-1 combine fused (rows scattered to y[t], scaled
+//               by the token's weight), or with each row pushed into its
+//               source rank's layout over peer memory (expert parallelism)
+//   EPI_F32     fp32 accumulators out (the dense gate GEMM, E >= 32)
 //
 // Hardware mapping (B200, one CTA per SM, 6 warps), CG = CTAs per MMA:
 //   CG = 1  tile 128 x 256: each CTA loads A 128x64 + B 256x64 per k-block
@@ -27,7 +31,9 @@
 // every tile row block belongs to exactly one expert and no load or store
 // crosses a segment.  Tiles are walked in a grouped raster: `group_m` row
 // blocks x all n blocks, sized on the host so the A panel (group_m x M x K x 2
-// bytes) stays L2-resident while the weight tiles stream past it.
+// bytes) stays L2-resident while the weight tiles stream past it; long-K
+// GEMM2s walk column panels of `group_n` weight n-blocks instead (weights
+// evict-last, rows evict-first), see npanel_for().
 #include <cstdlib>
 
 #include "common.cuh"
