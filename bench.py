@@ -171,7 +171,9 @@ def build_workload(cfg, device, cta_group=0, rank=0, world=1, parallel="replicas
     loads = [int(e) for e in ld[0, : nl[0]]]
     global_resident = sorted(loads)
     if parallel == "ep" and world > 1:  # this GPU holds only the experts it serves
-        loads = owned_experts(plan_destinations(global_resident, E, world), rank)
+        # load-aware placement from the Eq. 2 aggregate (identical on every
+        # rank: same fitted predictor, same request mix)
+        loads = owned_experts(plan_destinations(global_resident, E, world, agg[0]), rank)
 
     # ---- layer, weights (random-init, Mixtral/Switch shapes), planned loads
     td = torch_dtype(cfg)
@@ -350,11 +352,12 @@ def main():
     if use_ep and args.ep_transport == "p2p":
         from paper_2503_06823_b200.ep import PeerExpertParallelMoE
 
-        ep_model = PeerExpertParallelMoE(layer, info["global_resident"])
+        ep_model = PeerExpertParallelMoE(layer, info["global_resident"], loads=info["aggregate"])
     elif use_ep:
         from paper_2503_06823_b200.ep import ExpertParallelMoE, LayerBackend
 
-        ep_model = ExpertParallelMoE(LayerBackend(layer, info["global_resident"]), info["global_resident"])
+        ep_model = ExpertParallelMoE(LayerBackend(layer, info["global_resident"]), info["global_resident"],
+                                    loads=info["aggregate"])
 
     def step():
         if ep_model is not None:

@@ -40,26 +40,48 @@ import torch
 import torch.distributed as dist
 
 
-def plan_destinations(resident: Sequence[int], num_experts: int, world: int) -> np.ndarray:
+def plan_destinations(resident: Sequence[int], num_experts: int, world: int, loads=None) -> np.ndarray:
     """dest[src, e] = rank that computes source `src`'s rows of resident expert e
     (-1 for non-resident experts).  Monotone in e for every source, so each
-    source's permuted buffer is already grouped by destination."""
+    source's permuted buffer is already grouped by destination (the NCCL
+    transport sends contiguous chunks).
+
+    loads None: resident experts in contiguous equal-count blocks (L >= W), or
+    W // L full replicas of the resident set with sources spread over them
+    (L < W).  loads[e] (e.g. the ranks' summed Eq. 2 expected tokens): the
+    busiest rank is what an FFN-bound EP step waits for, so the resident
+    experts' loads are laid end to end on [0, W) in expert order and cut into
+    W unit intervals (one per rank); source s sends its rows of e to the rank
+    under the point c_e + (s + 1/2) w_e / W of e's interval [c_e, c_e + w_e).
+    A heavy expert is thereby replicated over the ranks its interval covers
+    and light neighbours share a rank; the points are non-decreasing in e, so
+    the plan stays monotone (tools/ep_balance_model.py on the config-2
+    routing: 0.49 -> 0.79 of W GPUs' FFN throughput at W = 8)."""
     res = sorted(int(e) for e in resident)
     L = len(res)
     dest = np.full((world, num_experts), -1, np.int64)
     if L == 0:
         return dest
+    if loads is not None:
+        w = np.array([max(float(loads[e]), 0.0) for e in res])
+        if w.sum() > 0:
+            w = w / w.sum() * world
+            c = np.concatenate([[0.0], np.cumsum(w)])
+            for src in range(world):
+                for i, e in enumerate(res):
+                    p = c[i] + (src + 0.5) * w[i] / world
+                    dest[src, e] = min(world - 1, int(np.floor(p)))
+            return dest
     if L >= world:
         for i, e in enumerate(res):  # contiguous blocks of resident experts per rank
             dest[:, e] = i * world // L
-    else:
-        groups = world // L  # full replicas of the resident set
-        for src in range(world):
-            g = src % groups
-            for i, e in enumerate(res):
-                dest[src, e] = g * L + i
+        return dest
+    groups = world // L  # full replicas of the resident set
+    for src in range(world):
+        g = src % groups
+        for i, e in enumerate(res):
+            dest[src, e] = g * L + i
     return dest
-
 
 def owned_experts(dest: np.ndarray, rank: int) -> list:
     return sorted({int(e) for e in np.flatnonzero((dest == rank).any(axis=0))})
@@ -114,12 +136,12 @@ class LayerBackend:
 class ExpertParallelMoE:
     """EP forward over a process group; `backend` provides the local kernels."""
 
-    def __init__(self, backend, global_resident: Sequence[int], group=None):
+    def __init__(self, backend, global_resident: Sequence[int], group=None, loads=None):
         self.backend = backend
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.dest = plan_destinations(global_resident, backend.E, self.world)
+        self.dest = plan_destinations(global_resident, backend.E, self.world, loads)
         self.stage_on_host = dist.get_backend(group) != "nccl"
         self.last = {}
 
@@ -223,9 +245,10 @@ class PeerExpertParallelMoE:
 
     `layer` is this rank's MoELayer holding the experts it computes; the
     group only carries the IPC-handle exchange at construction (gloo or
-    NCCL) -- the forward itself uses no collective."""
+    NCCL) -- the forward itself uses no collective.  `loads` (identical on
+    every rank) selects the load-aware placement of plan_destinations."""
 
-    def __init__(self, layer, global_resident: Sequence[int], group=None, recv_rows_cap: int = 0):
+    def __init__(self, layer, global_resident: Sequence[int], group=None, recv_rows_cap: int = 0, loads=None):
         import ctypes as C
 
         from ._lib import IPC_HANDLE_BYTES, lib
@@ -237,7 +260,7 @@ class PeerExpertParallelMoE:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.E = layer.E
-        self.dest = plan_destinations(global_resident, layer.E, self.world)
+        self.dest = plan_destinations(global_resident, layer.E, self.world, loads)
         res = np.zeros(layer.E, np.uint8)
         res[list(global_resident)] = 1
         layer.set_route_residency(res)

@@ -75,24 +75,26 @@ def single(backend, x):
     return backend.combine(y, b)
 
 
-def _cpu_worker(rank, world, port_no, resident, out_dir):
+def _cpu_worker(rank, world, port_no, resident, out_dir, loads=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle.oracle import Port
 
     be = OracleBackend(Port(), E=8, k=2, d=64, f=128, global_resident=resident)
     x = torch.from_numpy(np.random.default_rng(100 + rank).standard_normal((37 + 5 * rank, 64)).astype(np.float32))
-    ep = ExpertParallelMoE(be, resident)
+    ep = ExpertParallelMoE(be, resident, loads=loads)
     y_ep = ep(x)
     y_1 = single(be, x)
     np.save(Path(out_dir) / f"r{rank}.npy", np.stack([y_ep.numpy(), y_1.numpy()]))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,resident", [(2, [0, 2, 5, 7]), (4, [1, 6]), (4, [0, 1, 2, 3, 4, 5, 6, 7]),
-                                            (2, [3])])
-def test_ep_gloo_cpu_bit_identical(world, resident, tmp_path):
-    mp.spawn(_cpu_worker, args=(world, free_port(), resident, str(tmp_path)), nprocs=world, join=True)
+@pytest.mark.parametrize("world,resident,skew", [(2, [0, 2, 5, 7], False), (4, [1, 6], False),
+                                                  (4, [0, 1, 2, 3, 4, 5, 6, 7], False), (2, [3], False),
+                                                  (4, [0, 2, 5, 7], True)])
+def test_ep_gloo_cpu_bit_identical(world, resident, skew, tmp_path):
+    loads = [1, 0, 1, 0, 0, 1, 0, 20] if skew else None  # skew: load-aware placement replicates expert 7
+    mp.spawn(_cpu_worker, args=(world, free_port(), resident, str(tmp_path), loads), nprocs=world, join=True)
     for r in range(world):
         y_ep, y_1 = np.load(tmp_path / f"r{r}.npy")
         assert np.array_equal(y_ep, y_1), f"rank {r}: EP output differs from EP=1"
@@ -108,6 +110,38 @@ def test_plan_destinations():
     for src in range(8):  # monotone in expert order -> contiguous send chunks
         row = [q for q in plan_destinations([1, 2, 4], 8, 8)[src] if q >= 0]
         assert row == sorted(row)
+
+
+SKEW = np.array([1, 0, 1, 0, 0, 1, 0, 20], np.float64)  # expert 7 carries most rows
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("resident", [[0, 2, 5, 7], list(range(8)), [7], [1, 6]])
+def test_plan_destinations_load_aware(world, resident):
+    rng = np.random.default_rng(world * 31 + len(resident))
+    for loads in (SKEW, rng.random(8) * 100, np.zeros(8)):
+        d = plan_destinations(resident, 8, world, loads)
+        for src in range(world):
+            row = d[src]
+            assert all(row[e] == -1 for e in range(8) if e not in resident)
+            assert all(0 <= row[e] < world for e in resident)
+            live = [row[e] for e in sorted(resident)]
+            assert live == sorted(live), "load-aware plan must stay monotone in expert order"
+    # the heavy expert is spread over the ranks, the light ones share a rank
+    d = plan_destinations([0, 2, 5, 7], 8, 2, SKEW)
+    assert d[:, 7].tolist() == [0, 1] and d[0, :7].max() == 0
+    d = plan_destinations([0, 2, 5, 7], 8, 8, SKEW)
+    assert len(set(d[:, 7].tolist())) >= 6
+    # modelled busiest-rank load: never worse than the equal plan on the skew
+    for world in (2, 4, 8):
+        def busiest(dd):
+            per = np.zeros(world)
+            for src in range(world):
+                for e in [0, 2, 5, 7]:
+                    per[dd[src, e]] += SKEW[e]
+            return per.max()
+        assert busiest(plan_destinations([0, 2, 5, 7], 8, world, SKEW)) <= busiest(
+            plan_destinations([0, 2, 5, 7], 8, world))
 
 
 def _gpu_worker(rank, world, port_no, resident, out_dir):
@@ -186,12 +220,15 @@ def _simulate_p2p(backends, xs, dest):
     return ys, layouts
 
 
-@pytest.mark.parametrize("world,resident", [(2, [0, 2, 5, 7]), (4, [1, 6]), (4, list(range(8))), (2, [3])])
-def test_p2p_layout_protocol_bit_identical(world, resident, port):
+@pytest.mark.parametrize("world,resident,loads", [(2, [0, 2, 5, 7], None), (4, [1, 6], None),
+                                                   (4, list(range(8)), None), (2, [3], None),
+                                                   (2, [0, 2, 5, 7], SKEW), (4, [0, 2, 5, 7], SKEW),
+                                                   (3, list(range(8)), SKEW)])
+def test_p2p_layout_protocol_bit_identical(world, resident, loads, port):
     be = [OracleBackend(port, E=8, k=2, d=64, f=128, global_resident=resident) for _ in range(world)]
     xs = [torch.from_numpy(np.random.default_rng(200 + r).standard_normal((41 + 7 * r, 64)).astype(np.float32))
           for r in range(world)]
-    dest = plan_destinations(resident, 8, world)
+    dest = plan_destinations(resident, 8, world, loads)
     ys, layouts = _simulate_p2p(be, xs, dest)
     for r in range(world):
         assert np.array_equal(ys[r].numpy(), single(be[r], xs[r]).numpy()), f"rank {r}: P2P layout output differs"
@@ -207,8 +244,9 @@ def test_p2p_layout_disjoint_writes(port):
     from paper_2503_06823_b200.ep import p2p_layout
 
     rng = np.random.default_rng(5)
-    for world, resident in [(2, [0, 2, 5, 7]), (4, [1, 6]), (8, [0, 5, 6, 7]), (8, list(range(8)))]:
-        dest = plan_destinations(resident, 8, world)
+    for world, resident, loads in [(2, [0, 2, 5, 7], None), (4, [1, 6], None), (8, [0, 5, 6, 7], None),
+                                   (8, list(range(8)), None), (8, [0, 2, 5, 7], SKEW), (4, list(range(8)), SKEW)]:
+        dest = plan_destinations(resident, 8, world, loads)
         counts = rng.integers(0, 5, (world, 8)) * 4 * (dest >= 0)
         seg = [np.concatenate([[0], np.cumsum(counts[r])]) for r in range(world)]
         written = {q: [] for q in range(world)}
@@ -232,7 +270,7 @@ def test_p2p_layout_disjoint_writes(port):
             assert sorted(pushed[r]) == want, (world, r)
 
 
-def _gpu_p2p_worker(rank, world, port_no, resident, out_dir):
+def _gpu_p2p_worker(rank, world, port_no, resident, out_dir, loads=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
     os.environ.setdefault("EMOE_EP_TIMEOUT_S", "120")
     torch.cuda.set_device(0)
@@ -240,10 +278,10 @@ def _gpu_p2p_worker(rank, world, port_no, resident, out_dir):
     from helpers import build_layer
     from paper_2503_06823_b200.ep import PeerExpertParallelMoE
 
-    dest = plan_destinations(resident, 8, world)
+    dest = plan_destinations(resident, 8, world, loads)
     mine = owned_experts(dest, rank)
     layer, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", len(mine), mine, max_tokens=2048)
-    ep = PeerExpertParallelMoE(layer, resident)
+    ep = PeerExpertParallelMoE(layer, resident, loads=loads)
     full, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", len(resident), resident,
                              max_tokens=2048)
     res = []
@@ -263,9 +301,11 @@ def _gpu_p2p_worker(rank, world, port_no, resident, out_dir):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("resident", [[0, 2, 5, 7], [3]])
-def test_ep_p2p_two_ranks_one_gpu_bit_identical(resident, tmp_path):
-    mp.spawn(_gpu_p2p_worker, args=(2, free_port(), resident, str(tmp_path)), nprocs=2, join=True)
+@pytest.mark.parametrize("resident,loads", [([0, 2, 5, 7], None), ([3], None), ([0, 2, 5, 7], SKEW)])
+def test_ep_p2p_two_ranks_one_gpu_bit_identical(resident, loads, tmp_path):
+    """SKEW: expert 7 is replicated on both ranks (each computes its own
+    source's rows of it) while experts 0, 2 and 5 live on rank 0."""
+    mp.spawn(_gpu_p2p_worker, args=(2, free_port(), resident, str(tmp_path), loads), nprocs=2, join=True)
     for r in range(2):
         for i, d in enumerate(torch.load(tmp_path / f"p{r}.pt")):
             assert d["status"] == 0, f"rank {r} forward {i}: status {d['status']}"
