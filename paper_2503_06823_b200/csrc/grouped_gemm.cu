@@ -738,7 +738,7 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
 __device__ int32_t g_slot_zero = 0;
 
 void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int K, int N_out, float* out,
-                           int64_t ldo, int col_limit, int num_sms, cudaStream_t stream) {
+                           int64_t ldo, int col_limit, int num_sms, cudaStream_t stream, int cta_group) {
   EMOE_REQUIRE(K % gemm::BK == 0, "dense_gemm: K must be a multiple of 64");
   EMOE_REQUIRE(N_out % gemm::BN == 0, "dense_gemm: N must be a multiple of 256");
   gemm::Params p;
@@ -752,7 +752,7 @@ void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t
   p.out_block_cols = gemm::BN;
   p.n_blocks = N_out / gemm::BN;
   p.b_rows_per_slot = 0;
-  p.group_m = group_rows(K, 128);
+  p.group_m = group_rows(K, 128 * cta_group);
   p.group_n = p.n_blocks;
   p.hint_out = 0;
   p.hint_a = kCacheEvictNormal;
@@ -762,14 +762,14 @@ void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t
   p.out_f32 = out;
   p.row_limit = M;
   p.col_limit = col_limit;
-  p.single_rows = ceil_div(M, 128) * 128;
+  p.single_rows = ceil_div(M, 128 * cta_group) * (128 * cta_group);
   p.tma_store = 0;
   p.scatter_tok = nullptr;
   p.scatter_w = nullptr;
   p.scatter_out = nullptr;
   p.seg_out_rank = nullptr;
   p.seg_out_shift = nullptr;
-  launch_params(EPI_F32, 1, ta, tb, tb, ta, p, num_sms, stream);
+  launch_params(EPI_F32, cta_group, ta, tb, tb, ta, p, num_sms, stream);
 }
 
 // epilogue warps per CTA: 4 (one per TMEM lane quarter).  8 (two per quarter)
@@ -842,6 +842,8 @@ static void launch_params(int epi, int cta_group, const CUtensorMap& ta, const C
       launch_ew<EPI_SWIGLU, 2>(ta, tb, tb2, to, p, num_sms, stream);
     else if (epi == EPI_RELU)
       launch_ew<EPI_RELU, 2>(ta, tb, tb2, to, p, num_sms, stream);
+    else if (epi == EPI_F32)
+      launch_ew<EPI_F32, 2>(ta, tb, tb2, to, p, num_sms, stream);
     else
       launch_ew<EPI_STORE, 2>(ta, tb, tb2, to, p, num_sms, stream);
   }

@@ -109,7 +109,7 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
 // K1 for many experts: the gate as one dense tcgen05 GEMM with fp32 output,
 // out[M][ldo] = A[M][K] . B[N_out][K]^T, columns >= col_limit (multiple of 32) not stored
 void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int K, int N_out, float* out,
-                           int64_t ldo, int col_limit, int num_sms, cudaStream_t stream);
+                           int64_t ldo, int col_limit, int num_sms, cudaStream_t stream, int cta_group = 1);
 
 // K4 fp32 path on tensor cores (3xTF32, grouped_gemm_tf32.cu): operands
 // pre-split into tf32 hi and fp32 lo parts; tensor maps from make_tmap_f32_2d

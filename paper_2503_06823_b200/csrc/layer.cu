@@ -196,7 +196,7 @@ struct emoe_layer {
 
   // Gate on tcgen05 for E in {32, 64, 96, 128} (bf16): W_g zero-padded to 256 rows.
   void* wg_pad = nullptr;
-  CUtensorMap t_gate{};
+  CUtensorMap t_gate{}, t_gate2{};  // box 256 rows (1 CTA per MMA) / 128 rows (CTA pair)
   bool tc_gate() const {
     return cfg.dtype == EMOE_DTYPE_BF16 && cfg.num_experts >= 32 && cfg.num_experts % 32 == 0 && wg_pad;
   }
@@ -232,7 +232,12 @@ struct emoe_layer {
       // many experts: the gate is a real GEMM (T x d x E); run it on tcgen05
       // into the fp32 logits buffer, then route from the logits
       const CUtensorMap tx = make_tmap_bf16_2d(x, (uint64_t)T, cfg.d_model, 128);
-      launch_dense_gemm_f32(tx, t_gate, T, cfg.d_model, 256, logits, cfg.num_experts, cfg.num_experts, num_sms, s);
+      static const int gate_cg = [] {  // EMOE_GATE_CG=2: the gate GEMM on CTA pairs (A/B runs)
+        const char* v = getenv("EMOE_GATE_CG");
+        return v && v[0] == '2' ? 2 : 1;
+      }();
+      launch_dense_gemm_f32(tx, gate_cg == 2 ? t_gate2 : t_gate, T, cfg.d_model, 256, logits, cfg.num_experts,
+                            cfg.num_experts, num_sms, s, gate_cg);
       launch_route_from_logits(logits, a, o, s);
     } else {
       launch_gate_route(x, wg, cfg.dtype, a, o, s);
@@ -769,7 +774,11 @@ int emoe_layer_set_gate_host(emoe_layer* L, const void* wg) {
       if (!L->wg_pad) {
         L->wg_pad = dmalloc<uint8_t>((size_t)256 * L->cfg.d_model * 2);
         EMOE_CUDA(cudaMemset(L->wg_pad, 0, (size_t)256 * L->cfg.d_model * 2));
-        L->t_gate = make_tmap_bf16_2d(L->wg_pad, 256, L->cfg.d_model, 256);
+        // the map covers the E real rows only: the rest of the 256-row B box is
+        // out of bounds, zero-filled by the TMA without reading memory (mapping
+        // all 256 padded rows doubled the gate's operand bytes at E = 128)
+        L->t_gate = make_tmap_bf16_2d(L->wg_pad, E, L->cfg.d_model, 256);
+        L->t_gate2 = make_tmap_bf16_2d(L->wg_pad, E, L->cfg.d_model, 128);
       }
       EMOE_CUDA(cudaMemcpy(L->wg_pad, wg, bytes, cudaMemcpyHostToDevice));
     }
