@@ -306,7 +306,7 @@ def main():
                     help="--config stream: eMoE predicted residency, or the reference's on-demand baseline "
                          "(engine.cpp:469-502) for comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=40)
+    ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--gemm-cta-group", type=int, default=0, choices=[0, 1, 2],
                     help="FFN GEMM CTA group (0 = the layer's auto choice)")
     ap.add_argument("--parallel", default="replicas", choices=["replicas", "ep"],
