@@ -634,6 +634,7 @@ def main_stream(args):
     side copy stream overlapped with compute.  Routing-driven: the gate logits of
     prompt p / layer l embed the reference trace.  Single GPU."""
     import torch
+    import torch.distributed as dist
 
     import paper_2503_06823_b200 as emoe
     from paper_2503_06823_b200.serving import MoEStack, StreamConfig, TaskSpec, moesim_prompt_sets, run_stream
@@ -658,7 +659,10 @@ def main_stream(args):
     gates = [torch.zeros(E, d, dtype=torch.bfloat16) for _ in range(m)]  # routing-driven: logits come from the trace
     stack = MoEStack(cfg, host, gates)
     trace_dev = torch.from_numpy(trace).to(device)
-    stack.fit(trace_dev[:P_train].contiguous(), prompt_tasks[:P_train])
+    # N > 1: every rank tallies a shard of the training prompts and one
+    # all-reduce merges them (ep.fit_sharded; identical to one fit)
+    stack.fit(trace_dev[:P_train].contiguous(), prompt_tasks[:P_train],
+              group=dist.group.WORLD if dist.is_initialized() and dist.get_world_size() > 1 else None)
     # initial placement: the first plan from an empty device (blocking, untimed)
     _, sets = moesim_prompt_sets(trace_dev, P_train - 1)
     ops, _, _ = stack.invocation(sets, [(prompt_tasks[q], T) for q in range(P_train, P_train + p)])
@@ -739,7 +743,8 @@ def main_stack(args):
                   .pin_memory() for sh in ((f, d), (f, d), (d, f))) for _ in range(E)]
     stack = MoEStack(cfg, host, [torch.zeros(E, d, dtype=torch.bfloat16) for _ in range(m)])
     trace_dev = torch.from_numpy(trace).to(device)
-    stack.fit(trace_dev[:P_train].contiguous(), ["conv"] * P_train)
+    stack.fit(trace_dev[:P_train].contiguous(), ["conv"] * P_train,
+              group=dist.group.WORLD if dist.is_initialized() and dist.get_world_size() > 1 else None)
     _, sets = moesim_prompt_sets(trace_dev, P_train - 1)
     ops, _, _ = stack.invocation(sets, [("conv", Tp)] * P)
     stack.apply(ops)

@@ -292,6 +292,16 @@ int emoe_predictor_counts_host(emoe_predictor* pred, double* layer_counts, doubl
 int emoe_predictor_set_counts_host(emoe_predictor* pred, const double* layer_counts, const double* prompt_counts,
                                    const double* task_counts);
 
+/* The tallies as one int64 device vector [layer | prompt | task] of
+ * emoe_predictor_count_size() entries, stream-ordered after pending
+ * histogram updates.  Multi-GPU: each rank fits its own prompts and the
+ * ranks sum their deltas with one all-reduce (counts commute,
+ * test_predictor.cpp:284-296), so A7/A8 then run identically
+ * on every rank (paper_2503_06823_b200/ep.py HistogramSync). */
+int emoe_predictor_count_size(emoe_predictor* pred, int64_t* n);
+int emoe_predictor_counts_dev(emoe_predictor* pred, int64_t* dst_dev, void* stream);
+int emoe_predictor_set_counts_dev(emoe_predictor* pred, const int64_t* src_dev, void* stream);
+
 /* dominant_expert / prompt_expert_sets (workload.cpp:350-377) for one prompt
  * of a device trace [P][m][T][k]: dominant [m], sets [m][k] (-1 padded), sizes [m]. */
 int emoe_prompt_expert_sets(const int32_t* trace_dev, int P, int m, int T, int k, int prompt, int32_t* dominant_host,

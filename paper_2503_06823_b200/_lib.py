@@ -92,6 +92,9 @@ _decl("emoe_hist_update", vp, vp, C.c_int, C.c_int, vp, vp)
 _decl("emoe_hist_update_host", vp, vp, C.c_int, C.c_int, vp)
 _decl("emoe_predictor_counts_host", vp, vp, vp, vp)
 _decl("emoe_predictor_set_counts_host", vp, vp, vp, vp)
+_decl("emoe_predictor_count_size", vp, C.POINTER(C.c_int64))
+_decl("emoe_predictor_counts_dev", vp, vp, vp)
+_decl("emoe_predictor_set_counts_dev", vp, vp, vp)
 _decl("emoe_prompt_expert_sets", vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp)
 _decl("emoe_predict_host", vp, C.c_int, vp, vp, C.c_int, vp, vp, vp)
 _decl("emoe_predicted_frequencies_host", vp, C.c_int, vp)
@@ -114,7 +117,8 @@ EXPORTED = [
     "emoe_ep_forward", "emoe_ep_status", "emoe_ep_destroy", "emoe_layer_workspace", "emoe_layer_share_workspace", "emoe_layer_set_profiling",
     "emoe_layer_stage_times", "emoe_kernel_launches", "emoe_predictor_create",
     "emoe_predictor_destroy", "emoe_predictor_reset", "emoe_predictor_break_chain", "emoe_hist_update", "emoe_hist_update_host", "emoe_predictor_counts_host",
-    "emoe_predictor_set_counts_host", "emoe_prompt_expert_sets", "emoe_predict_host",
+    "emoe_predictor_set_counts_host", "emoe_predictor_count_size", "emoe_predictor_counts_dev",
+    "emoe_predictor_set_counts_dev", "emoe_prompt_expert_sets", "emoe_predict_host",
     "emoe_predicted_frequencies_host", "emoe_expected_tokens_host", "emoe_select_experts_host",
     "emoe_loading_targets_host", "emoe_plan_loading_host", "emoe_invocation_host", "emoe_gen_routing_trace",
 ]

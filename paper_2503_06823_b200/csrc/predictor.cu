@@ -729,6 +729,46 @@ int emoe_predictor_set_counts_host(emoe_predictor* P, const double* lc, const do
   });
 }
 
+int emoe_predictor_count_size(emoe_predictor* P, int64_t* n) {
+  return guard([&] {
+    EMOE_REQUIRE(P && n, "predictor_count_size: null");
+    *n = (int64_t)(P->n_layer() + P->n_prompt() + P->n_task());
+  });
+}
+
+// Stream-ordered device copies of the tallies as one int64 vector
+// [layer | prompt | task]: the all-reduce of per-rank histogram deltas
+// runs on these without a host round trip.
+int emoe_predictor_counts_dev(emoe_predictor* P, int64_t* dst, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(P && dst, "predictor_counts_dev: null");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (P->hist_recorded) EMOE_CUDA(cudaStreamWaitEvent(s, P->hist_done, 0));
+    size_t off = 0;
+    for (auto [d, n] : {std::pair<const u64*, size_t>{P->layer_counts, P->n_layer()},
+                        {P->prompt_counts, P->n_prompt()}, {P->task_counts, P->n_task()}}) {
+      if (n) EMOE_CUDA(cudaMemcpyAsync(dst + off, d, n * sizeof(u64), cudaMemcpyDeviceToDevice, s));
+      off += n;
+    }
+  });
+}
+
+int emoe_predictor_set_counts_dev(emoe_predictor* P, const int64_t* src, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(P && src, "predictor_set_counts_dev: null");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (P->hist_recorded) EMOE_CUDA(cudaStreamWaitEvent(s, P->hist_done, 0));
+    size_t off = 0;
+    for (auto [d, n] : {std::pair<u64*, size_t>{P->layer_counts, P->n_layer()}, {P->prompt_counts, P->n_prompt()},
+                        {P->task_counts, P->n_task()}}) {
+      if (n) EMOE_CUDA(cudaMemcpyAsync(d, src + off, n * sizeof(u64), cudaMemcpyDeviceToDevice, s));
+      off += n;
+    }
+    EMOE_CUDA(cudaEventRecord(P->hist_done, s));  // invocations read the merged counts after this
+    P->hist_recorded = true;
+  });
+}
+
 int emoe_prompt_expert_sets(const int32_t* trace, int nP, int m, int T, int k, int prompt, int32_t* dominant,
                             int32_t* sets, int32_t* sizes, void* stream) {
   return guard([&] {

@@ -308,3 +308,120 @@ class PeerExpertParallelMoE:
 
     def __del__(self):
         self.close()
+
+
+# ---------------------------------------------------------------------------
+# predictor under multi-GPU: per-rank histograms merged by one all-reduce
+# ---------------------------------------------------------------------------
+def _all_reduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place SUM over the group; gloo groups stage CUDA tensors through the host."""
+    if t.is_cuda and dist.get_backend(group) != "nccl":
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, group=group)
+    return t
+
+
+class PredictorCounts:
+    """Device int64 view of an emoe_predictor's tallies [layer | prompt | task]
+    (emoe_predictor_counts_dev / emoe_predictor_set_counts_dev)."""
+
+    def __init__(self, pred_handle, device=None):
+        import ctypes as C
+
+        from ._lib import lib
+        from .moesim import check
+
+        self._lib, self._check, self._C = lib, check, C
+        self.h = pred_handle
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        n = C.c_int64()
+        check(lib.emoe_predictor_count_size(self.h, C.byref(n)))
+        self.n = int(n.value)
+
+    def export(self) -> torch.Tensor:
+        C = self._C
+        t = torch.empty(self.n, dtype=torch.int64, device=self.device)
+        s = torch.cuda.current_stream(self.device)
+        self._check(self._lib.emoe_predictor_counts_dev(self.h, C.c_void_p(t.data_ptr()), C.c_void_p(s.cuda_stream)))
+        return t
+
+    def import_(self, t: torch.Tensor) -> None:
+        C = self._C
+        assert t.dtype == torch.int64 and t.is_cuda and t.numel() == self.n
+        t = t.contiguous()
+        s = torch.cuda.current_stream(self.device)
+        self._check(self._lib.emoe_predictor_set_counts_dev(self.h, C.c_void_p(t.data_ptr()),
+                                                            C.c_void_p(s.cuda_stream)))
+
+
+class HistogramSync:
+    """A6 under data parallelism: every rank tallies its own
+    prompts, and merge() replaces every rank's tallies by the common state
+    plus the SUM of all ranks' local deltas, in exact int64 (counts commute,
+    test_predictor.cpp:284-296).  A7/A8 then run identically on every rank,
+    so the residency tables stay replicated.
+
+    `io` has export() -> int64 tensor and import_(tensor) (PredictorCounts for
+    an emoe_predictor).  The ranks' tallies must be identical when the sync
+    is created (e.g. fresh predictors).  mark_local() excludes the updates
+    made since the last merge from this rank's delta -- used to prime the
+    prompt chain with the previous shard's last prompt, whose own tallies
+    belong to the rank that owns it (fit_sharded)."""
+
+    def __init__(self, io, group=None):
+        self.io = io
+        self.group = group
+        self.common = io.export().clone()
+        self.mark = self.common.clone()
+
+    def mark_local(self) -> None:
+        self.mark = self.io.export().clone()
+
+    def merge(self) -> torch.Tensor:
+        delta = self.io.export() - self.mark
+        _all_reduce_sum(delta, self.group)
+        merged = self.common + delta
+        self.io.import_(merged)
+        self.common = merged.clone()
+        self.mark = merged.clone()
+        return merged
+
+
+def shard_range(P: int, world: int, rank: int):
+    """Contiguous prompt shard [a, b) of rank `rank`."""
+    return P * rank // world, P * (rank + 1) // world
+
+
+def fit_sharded(pred_handle, trace_dev: torch.Tensor, task_ids_dev, group=None) -> None:
+    """fit over all P prompts of trace_dev [P, m, T, k] with each rank of the
+    group tallying a contiguous shard, then one all-reduce: the merged
+    tallies equal a single fit over the whole trace (bit-exact), because
+    rank r first replays prompt a_r - 1 (only to continue the prompt chain;
+    mark_local drops its tallies) and so counts the boundary transition
+    a_r - 1 -> a_r itself."""
+    import ctypes as C
+
+    from ._lib import lib
+    from .moesim import check
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    P, m, T, k = trace_dev.shape
+    sync = HistogramSync(PredictorCounts(pred_handle, trace_dev.device), group)
+    a, b = shard_range(P, world, rank)
+    s = torch.cuda.current_stream(trace_dev.device)
+
+    def update(lo, hi):
+        tid = None if task_ids_dev is None else C.c_void_p(task_ids_dev[lo:hi].data_ptr())
+        check(lib.emoe_hist_update(pred_handle, C.c_void_p(trace_dev[lo:hi].data_ptr()), hi - lo, T, tid,
+                                   C.c_void_p(s.cuda_stream)))
+
+    if b > a:
+        if a > 0:
+            update(a - 1, a)
+            sync.mark_local()
+        update(a, b)
+    sync.merge()
+

@@ -30,6 +30,7 @@ from typing import Dict, List, Sequence
 
 import numpy as np
 import torch
+import torch.distributed as dist
 
 from . import moesim
 from ._lib import lib
@@ -89,10 +90,17 @@ class MoEStack:
             layer.close()
 
     # -- predictor --------------------------------------------------------------
-    def fit(self, trace_dev: torch.Tensor, task_ids: Sequence[str]) -> None:
-        """A6 over the training prompts (the engine fits once at setup, engine.cpp:249-258)."""
+    def fit(self, trace_dev: torch.Tensor, task_ids: Sequence[str], group=None) -> None:
+        """A6 over the training prompts (the engine fits once at setup, engine.cpp:249-258).
+        With a process group of several ranks every rank tallies a shard and
+        the tallies are merged (ep.fit_sharded): identical to one fit."""
         P, m, T, k = trace_dev.shape
         tid = torch.tensor([self.names.index(t) for t in task_ids], dtype=torch.int32, device=trace_dev.device)
+        if group is not None and dist.get_world_size(group) > 1:
+            from .ep import fit_sharded
+
+            fit_sharded(self.pred.h, trace_dev, tid, group)
+            return
         check(lib.emoe_hist_update(self.pred.h, C.c_void_p(trace_dev.data_ptr()), P, T, C.c_void_p(tid.data_ptr()),
                                    None))
 

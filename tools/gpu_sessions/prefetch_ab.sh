@@ -1,5 +1,6 @@
 #!/bin/bash
 # A/B: L2 prefetch of the next tile's operand boxes in the grouped GEMM producer
+# (the prefetch code was reverted after this A/B: profiles/r01_gemm_l2_prefetch_ab.jsonl)
 mkdir -p gpurun_out
 out=gpurun_out/prefetch_ab.jsonl; : > $out
 EMOE_GEMM_PREFETCH=1 timeout 600 python -m pytest tests/test_forward_gpu.py -m gpu -x -q > gpurun_out/prefetch_tests.log 2>&1; echo rc=$? >> gpurun_out/prefetch_tests.log
