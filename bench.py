@@ -127,7 +127,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # synthetic workload
 # ---------------------------------------------------------------------------
-def build_workload(cfg, device, cta_group=0, rank=0, world=1, parallel="replicas"):
+def build_workload(cfg, device, cta_group=0, rank=0, world=1, parallel="replicas", strong=False):
     import torch
 
     import paper_2503_06823_b200 as emoe
@@ -136,12 +136,14 @@ def build_workload(cfg, device, cta_group=0, rank=0, world=1, parallel="replicas
 
     E, k, L, d, f = cfg["E"], cfg["k"], cfg["L"], cfg["d"], cfg["f"]
     P, Tp, P_train = cfg["prompts"], cfg["tokens"], cfg["train"]
-    T = P * Tp
+    # weak scaling: every rank serves its own P prompts of the same trace;
+    # strong: the ranks split one batch of P prompts
+    Pr = P // world if strong else P
+    T = Pr * Tp
     shape = emoe.ModelShape(1, E, k, expert_bytes=(3 if cfg["act"] == "swiglu" else 2) * d * f * 2)
-    # every rank serves its own 32 prompts of the same trace (weak scaling)
     trace = emoe.gen_routing_trace(shape, cfg["layer_lambda"], cfg["prompt_lambda"], 0, cfg["seed"],
-                                   P_train + P * world, Tp)
-    train, serve = trace[:P_train], trace[P_train + P * rank: P_train + P * (rank + 1)]
+                                   P_train + Pr * world, Tp)
+    train, serve = trace[:P_train], trace[P_train + Pr * rank: P_train + Pr * (rank + 1)]
 
     # ---- predictor flow on the GPU (fit -> predict -> Eq. 2 -> targets -> plan)
     pred = emoe.moesim._Pred(1, E, k, 1, 0.01)
@@ -309,6 +311,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--gemm-cta-group", type=int, default=0, choices=[0, 1, 2],
                     help="FFN GEMM CTA group (0 = the layer's auto choice)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = every GPU serves the config's full batch (default); strong = the "
+                         "config's batch is split over the GPUs (N must divide its 32 prompts)")
     ap.add_argument("--parallel", default="replicas", choices=["replicas", "ep"],
                     help="N>1: replicas of the predicted resident set (no exchange) or expert parallelism")
     ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"],
@@ -339,12 +344,15 @@ def main():
     from paper_2503_06823_b200 import _lib
 
     use_ep = args.parallel == "ep" and world > 1
+    strong = args.scaling == "strong" and world > 1
+    if strong and cfg["prompts"] % world:
+        raise SystemExit(f"--scaling strong: {world} GPUs do not divide the {cfg['prompts']} prompts")
     layer, pred, x, info = build_workload(cfg, device, args.gemm_cta_group, rank, world,
-                                          "ep" if use_ep else "replicas")
+                                          "ep" if use_ep else "replicas", strong)
     T = x.shape[0]
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream()
-    P, Tp = cfg["prompts"], cfg["tokens"]
+    P, Tp = cfg["prompts"] // (world if strong else 1), cfg["tokens"]
     tid = torch.zeros(P, dtype=torch.int32, device=device)
     import ctypes as C
 
@@ -496,10 +504,12 @@ def main():
     hbm_stages["combine"] = (S * d * eb + xb + 4 * S) / (stages["combine"] / 1e3) / 1e9
 
     out = dict(metric=METRIC, value=round(value, 1), unit="tokens/s", n_gpus=world, steps=args.steps,
-               warmup=args.warmup, ms_per_step=round(ms, 4), higher_is_better=True, scaling="weak",
+               warmup=args.warmup, ms_per_step=round(ms, 4), higher_is_better=True,
+               scaling="strong" if strong else "weak",
                vs_baseline=None, dtype=cfg.get("dtype", "bf16"),
                data="synthetic (random-init weights; routing = reference Markov trace embedded in x)",
-               config=dict(workload=cfg["workload"], tokens_per_step=T, num_experts=cfg["E"], top_k=cfg["k"],
+               config=dict(workload=cfg["workload"] + (f" split over {world} GPUs" if strong else ""),
+                           tokens_per_step=T, tokens_per_gpu=T, num_experts=cfg["E"], top_k=cfg["k"],
                            resident_experts=cfg["L"], resident_set=[e for e in range(cfg["E"])
                                                                      if info["resident"][e]],
                            d_model=d, d_ff=f, activation=cfg["act"], served_rows=S, hit_rate=round(hit_rate, 4),
@@ -733,11 +743,15 @@ def main_stack(args):
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     m, E, k, L, d, f, P, Tp = args.stream_layers, 8, 2, 4, 4096, 14336, 32, 2048
-    T = P * Tp
+    strong = args.scaling == "strong" and world > 1
+    if strong and P % world:
+        raise SystemExit(f"--scaling strong: {world} GPUs do not divide the {P} prompts")
+    Pr = P // world if strong else P  # prompts this rank serves
+    T = Pr * Tp
     cfg = StreamConfig(m=m, E=E, k=k, L=L, d=d, f=f, tokens_per_prompt=T, period=40, mode=0,
                        tasks={"conv": TaskSpec(256.0, [1] * m)})
     P_train = 60
-    trace = emoe.gen_routing_trace(emoe.ModelShape(m, E, k), 0.6, 0.8, 0, 17, P_train + P * world, Tp)
+    trace = emoe.gen_routing_trace(emoe.ModelShape(m, E, k), 0.6, 0.8, 0, 17, P_train + Pr * world, Tp)
     g = torch.Generator(device=device).manual_seed(1234)
     host = [tuple((torch.randn(*sh, generator=g, device=device) / sh[1] ** 0.5).to(torch.bfloat16).cpu()
                   .pin_memory() for sh in ((f, d), (f, d), (d, f))) for _ in range(E)]
@@ -751,14 +765,14 @@ def main_stack(args):
     for layer in stack.layers:
         layer.poll_loads(blocking=True)
     torch.cuda.synchronize()
-    serve = trace_dev[P_train + rank * P: P_train + (rank + 1) * P].contiguous()  # [P][m][Tp][k]
+    serve = trace_dev[P_train + rank * Pr: P_train + (rank + 1) * Pr].contiguous()  # [Pr][m][Tp][k]
     ch = serve.permute(1, 0, 2, 3).reshape(m, T, k).long()
     lg = torch.rand(m, T, E, generator=g, device=device) * 8.0 - 4.0
     for r in range(k):
         lg.scatter_(2, ch[:, :, r:r + 1], 8.0 - r)
     x = torch.randn(T, d, generator=g, device=device).to(torch.bfloat16)
     bufs = [torch.empty_like(x), torch.empty_like(x)]
-    tid = torch.zeros(P, dtype=torch.int32, device=device)
+    tid = torch.zeros(Pr, dtype=torch.int32, device=device)
     stream = torch.cuda.current_stream()
     import ctypes as C
 
@@ -766,7 +780,7 @@ def main_stack(args):
         h = x if src is None else src
         for l, layer in enumerate(stack.layers):
             h = layer.forward(h, logits=lg[l], out=bufs[l % 2])
-        emoe.moesim.check(_lib.lib.emoe_hist_update(stack.pred.h, C.c_void_p(serve.data_ptr()), P, Tp,
+        emoe.moesim.check(_lib.lib.emoe_hist_update(stack.pred.h, C.c_void_p(serve.data_ptr()), Pr, Tp,
                                                     C.c_void_p(tid.data_ptr()), C.c_void_p(stream.cuda_stream)))
         return h
 
@@ -826,11 +840,11 @@ def main_stack(args):
     ffn_flops = 2.0 * 3 * d * f * S_total
     achieved = ffn_flops / (gemm_ms / 1e3) / 1e12
     out = dict(metric=METRIC, value=round(value, 1), unit="tokens/s", n_gpus=world, steps=args.steps,
-               warmup=args.warmup, ms_per_step=round(ms, 3), higher_is_better=True, scaling="weak",
-               vs_baseline=None, dtype="bf16",
+               warmup=args.warmup, ms_per_step=round(ms, 3), higher_is_better=True,
+               scaling="strong" if strong else "weak", vs_baseline=None, dtype="bf16",
                data="synthetic (random-init weights; routing-driven from the reference Markov trace)",
                config=dict(workload=f"BASELINE config 4 (without the exchange): {m}-layer Mixtral-shaped MoE stack "
-                                    f"bf16, 8 experts top-2, 4 predicted resident per layer, {P} x {Tp} tokens per "
+                                    f"bf16, 8 experts top-2, 4 predicted resident per layer, {Pr} x {Tp} tokens per "
                                     "GPU through every layer", layers=m, tokens_per_step=T,
                            served_rows_all_layers=S_total, workspace="one shared activation workspace",
                            parallelism=f"replicas{world}" if world > 1 else "single",
