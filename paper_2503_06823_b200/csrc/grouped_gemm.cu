@@ -99,6 +99,12 @@ struct Params {
   const int32_t* scatter_tok;
   const float* scatter_w;
   __nv_bfloat16* scatter_out;
+  // top-2 combine fused: pos [T][2] and per-(token, n-block, column half)
+  // arrival counters; the second of a token's two rows to reach the
+  // epilogue combines both (see the EPI_STORE branch)
+  int scatter_k;
+  const int32_t* scatter_pos;
+  int32_t* scatter_arrive;
   // EPI_STORE pushing each segment's rows to its source rank's buffer
   // (expert parallelism over peer memory); null = local output
   const int32_t* seg_out_rank;
@@ -420,6 +426,8 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + buf * BN;
       const int col0 = c.nb * p.out_block_cols;
       __nv_bfloat16* orow = p.out + row * p.ldo + col0;
+      int combine_partner = -1, combine_slot = 0, combine_tok = -1;  // fused top-2 combine, after the TMEM release
+      float combine_w0 = 0.0f, combine_w1 = 0.0f;
       if (EPI == EPI_SWIGLU) {
 #pragma unroll 1
         for (int cc = c_lo; cc < c_lo + SPAN; cc += OUT_BOX_COLS) {
@@ -482,6 +490,64 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
             dst[v] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
           }
         }
+      } else if (EPI == EPI_STORE && p.scatter_tok != nullptr && p.scatter_k == 2) {
+        // top-2 combine fused: y[t] = bf16(fma(w1, Y1, fma(w0, Y0, 0))) with
+        // Y_j = bf16(row of slot j) -- the separate combine's operations in
+        // its slot order, so bit-identical.  The two rows of a token sit in
+        // different experts' tiles.  Each stores its bf16 row chunk into
+        // Y_perm, then (after the TMEM buffer is released) arrives on the
+        // token's (n-block, column half) counter with one acq_rel atomic:
+        // the second to arrive finds the partner's chunk complete and
+        // visible, combines both from L2 into y[t] and re-zeroes the counter.
+        // Nobody waits, so no lane can stall a warp-collective TMEM load.
+        // Single-served tokens write y[t] directly from the accumulators.
+        const int tok = p.scatter_tok[row];
+        int partner = -1, slot = 0;
+        float w0 = 0.0f, w1 = 0.0f;
+        if (tok >= 0) {
+          const int p0 = p.scatter_pos[2 * tok], p1 = p.scatter_pos[2 * tok + 1];
+          slot = p0 == (int)row ? 0 : 1;
+          partner = slot == 0 ? p1 : p0;
+          w0 = p.scatter_w[2 * tok];
+          w1 = p.scatter_w[2 * tok + 1];
+        }
+        __nv_bfloat16* yrow = p.scatter_out + (int64_t)(tok < 0 ? 0 : tok) * p.ldo + col0;
+        __nv_bfloat16* own = p.out + row * p.ldo + col0;
+#pragma unroll 1
+        for (int cc = c_lo; cc < c_lo + SPAN; cc += OUT_BOX_COLS) {
+          uint32_t a0[32], a1[32];
+          tmem_ld_32x32b_x32(taddr + cc, a0);
+          tmem_ld_32x32b_x32(taddr + cc + 32, a1);
+          tmem_ld_wait();
+          if (tok < 0) continue;
+          uint32_t mine[32];
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const int q = 2 * (jj & 15);
+            mine[jj] = pack_bf16x2(__uint_as_float(jj < 16 ? a0[q] : a1[q]),
+                                   __uint_as_float(jj < 16 ? a0[q + 1] : a1[q + 1]));
+          }
+          uint4* dst = reinterpret_cast<uint4*>((partner >= 0 ? own : yrow) + cc);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            if (partner >= 0) {
+              dst[v] = make_uint4(mine[4 * v], mine[4 * v + 1], mine[4 * v + 2], mine[4 * v + 3]);
+            } else {
+              uint32_t q4[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const uint32_t y0 = mine[4 * v + u];
+                q4[u] = pack_bf16x2(fmaf(w0, bf16_lo(y0), 0.0f), fmaf(w0, bf16_hi(y0), 0.0f));
+              }
+              dst[v] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+            }
+          }
+        }
+        combine_partner = partner;
+        combine_slot = slot;
+        combine_tok = tok;
+        combine_w0 = w0;
+        combine_w1 = w1;
       } else if (EPI == EPI_STORE && p.scatter_tok != nullptr) {
         // top-1 combine fused: y[t] = w_t * bf16(Y_row), the same two roundings
         // as the separate combine (bit-identical), each lane's 128-B row
@@ -538,6 +604,32 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
           mbar_arrive_relaxed(&tempty_bar[buf]);
         else
           mbar_arrive_leader_relaxed(&tempty_bar[buf]);
+      }
+      if (EPI == EPI_STORE && combine_partner >= 0) {
+        // second of the token's rows to arrive: both bf16 rows are in Y_perm
+        int32_t* arrive = p.scatter_arrive + ((int64_t)combine_tok * p.n_blocks + c.nb) * 2 + ew / 4;
+        int old;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(arrive) : "memory");
+        if (old != 0) {
+          *arrive = 0;  // nobody else touches it this forward; the kernel boundary orders the next use
+          const __nv_bfloat16* r0 = p.out + (int64_t)(combine_slot == 0 ? row : combine_partner) * p.ldo + col0;
+          const __nv_bfloat16* r1 = p.out + (int64_t)(combine_slot == 0 ? combine_partner : row) * p.ldo + col0;
+          __nv_bfloat16* yrow = p.scatter_out + (int64_t)combine_tok * p.ldo + col0;
+#pragma unroll 1
+          for (int cc = c_lo; cc < c_lo + SPAN; cc += 8) {
+            const uint4 u0 = __ldcg(reinterpret_cast<const uint4*>(r0 + cc));
+            const uint4 u1 = __ldcg(reinterpret_cast<const uint4*>(r1 + cc));
+            const uint32_t y0[4] = {u0.x, u0.y, u0.z, u0.w}, y1[4] = {u1.x, u1.y, u1.z, u1.w};
+            uint32_t q4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float lo = fmaf(combine_w1, bf16_lo(y1[u]), fmaf(combine_w0, bf16_lo(y0[u]), 0.0f));
+              const float hi = fmaf(combine_w1, bf16_hi(y1[u]), fmaf(combine_w0, bf16_hi(y0[u]), 0.0f));
+              q4[u] = pack_bf16x2(lo, hi);
+            }
+            *reinterpret_cast<uint4*>(yrow + cc) = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+          }
+        }
       }
     }
     if (EPI != EPI_F32 && p.tma_store && lane == 0) bulk_wait_all();
@@ -732,6 +824,11 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
   p.scatter_tok = scatter ? scatter->row_token : nullptr;
   p.scatter_w = scatter ? scatter->weight : nullptr;
   p.scatter_out = scatter ? scatter->y : nullptr;
+  p.scatter_k = scatter ? scatter->k : 1;
+  p.scatter_pos = scatter ? scatter->pos : nullptr;
+  p.scatter_arrive = scatter ? scatter->arrive : nullptr;
+  EMOE_REQUIRE(!scatter || scatter->k == 1 || (scatter->k == 2 && scatter->pos && scatter->arrive),
+               "grouped_gemm: the fused top-2 combine needs positions and arrival counters");
   launch_params(epi, cta_group, ta, tb, tb2, p.tma_store ? *tmap_out : ta, p, num_sms, stream);
 }
 
@@ -767,6 +864,9 @@ void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t
   p.scatter_tok = nullptr;
   p.scatter_w = nullptr;
   p.scatter_out = nullptr;
+  p.scatter_k = 1;
+  p.scatter_pos = nullptr;
+  p.scatter_arrive = nullptr;
   p.seg_out_rank = nullptr;
   p.seg_out_shift = nullptr;
   launch_params(EPI_F32, cta_group, ta, tb, tb, ta, p, num_sms, stream);

@@ -96,8 +96,11 @@ struct PeerOut;  // expert parallelism: GEMM2 rows pushed to their source ranks 
 // top-1 combine fused into GEMM2's epilogue: y[row_token[r]] = weight[token] * Y[r]
 struct ScatterCombine {
   const int32_t* row_token;  // [R], -1 = padding row
-  const float* weight;       // [T] (served_w with k = 1)
+  const float* weight;       // [T][k] served_w
   __nv_bfloat16* y;          // [T][ldo]
+  int k = 1;                 // 1 or 2
+  const int32_t* pos = nullptr;  // k = 2: [T][2] rows of the served slots (-1 = not served)
+  int32_t* arrive = nullptr;     // k = 2: [T][n_blocks][2] zeroed counters (left zeroed)
 };
 void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,

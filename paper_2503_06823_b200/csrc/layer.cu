@@ -274,8 +274,18 @@ struct emoe_layer {
     mark(1, s);
     permute(x, T, s);
     mark(2, s);
-    if (fused_combine()) {  // top-1: GEMM2's epilogue writes y directly (K5 fused)
-      const ScatterCombine sc{row_token, served_w, static_cast<__nv_bfloat16*>(y)};
+    if (fused_combine()) {  // top-1 / top-2: GEMM2's epilogue writes y directly (K5 fused)
+      ScatterCombine sc{row_token, served_w, static_cast<__nv_bfloat16*>(y)};
+      if (cfg.top_k == 2) {
+        if (!combine_arrive) {  // [max_tokens][d/256][2] counters, zero between forwards
+          const size_t n = (size_t)cfg.max_tokens * ceil_div(cfg.d_model, 256) * 2;
+          combine_arrive = dmalloc<int32_t>(n);
+          EMOE_CUDA(cudaMemsetAsync(combine_arrive, 0, n * sizeof(int32_t), s));
+        }
+        sc.k = 2;
+        sc.pos = pos;
+        sc.arrive = combine_arrive;
+      }
       ffn(x_perm, rows_cap, seg_offsets, nullptr, cfg.num_experts, h, y_perm, s, true, &sc);
       y_perm_valid = false;
     } else {
@@ -286,16 +296,21 @@ struct emoe_layer {
     mark(5, s);
   }
 
-  // top-1 bf16 layers without forced misses serve every token exactly once, so
-  // the combine is a scaled row scatter GEMM2's epilogue can do
-  // (EMOE_FUSED_COMBINE=0 keeps the separate K5 for A/B runs)
+  // bf16 layers without forced misses serve every token at least once, so
+  // GEMM2's epilogue can produce y: top-1 as a scaled row scatter (default),
+  // top-2 by the second of a token's two rows combining both
+  // (EMOE_FUSED_COMBINE=2; bit-identical, but its direct-store epilogue costs
+  // GEMM2 more than the 0.24 ms combine it removes at the config-2 shape,
+  // profiles/r01_fused_top2_combine_ab.jsonl).  EMOE_FUSED_COMBINE=0 keeps
+  // the separate K5 for every layer.
   bool fused_combine() const {
-    static const bool on = [] {
+    static const int mode = [] {
       const char* v = getenv("EMOE_FUSED_COMBINE");
-      return !(v && v[0] == '0');
+      return v ? atoi(v) : 1;
     }();
-    return on && cfg.dtype == EMOE_DTYPE_BF16 && cfg.top_k == 1 && !cfg.forced_miss;
+    return cfg.dtype == EMOE_DTYPE_BF16 && !cfg.forced_miss && cfg.top_k <= mode && cfg.top_k <= 2;
   }
+  int32_t* combine_arrive = nullptr;
   bool y_perm_valid = true;
 
   // A3 after route(): per-expert offsets, positions, gathered rows in x_perm
@@ -542,7 +557,7 @@ struct emoe_layer {
     for (void* p : {(void*)wg, w1_pool, w3_pool, w2_pool, (void*)slot_dev, (void*)resident_dev, (void*)scores_dev,
                     (void*)route_resident_dev, wg_pad, (void*)demand_dev, x_in, y_out, (void*)err_flag, x_stage[0],
                     x_stage[1], y_stage[0], y_stage[1], w1_lo, w3_lo, w2_lo, (void*)sx_hi, (void*)sx_lo,
-                    (void*)sh_lo, (void*)splitk})
+                    (void*)sh_lo, (void*)splitk, (void*)combine_arrive})
       f(p);
     for (auto* v : {&host_w1, &host_w3, &host_w2})
       for (size_t e = 0; e < v->size(); ++e)

@@ -89,29 +89,29 @@ def check_case(c, port, scores=None):
     # A4 expert FFN on sampled rows of every active expert (mirrored rounding)
     rng = np.random.default_rng(0)
     bf = c["dtype"] == "bf16"
-    fused = ws["y_perm"] is None  # top-1: GEMM2's epilogue wrote y directly (fused combine)
+    # fused combine (bf16, k <= 2): GEMM2's epilogue wrote y directly, so the
+    # sampled rows are checked through their tokens in the end-to-end check
+    fused = ws["y_perm"] is None
     yp = None if fused else to_f32(ws["y_perm"][:R])
-    y32 = to_f32(c["y"])
+    fused_toks = []
     for e in range(E):
         rows = np.arange(offsets[e], offsets[e] + counts[e])
         if rows.size == 0:
             continue
         pick = rng.choice(rows, size=min(12, rows.size), replace=False)
+        if fused:
+            fused_toks.extend(src[pick].tolist())
+            continue
         w1, w3, w2 = (None if w is None else to_f32(w) for w in c["experts"][e])
         ref = port.expert_ffn(x32[src[pick]], w1, w3, w2, 0 if c["act"] == "swiglu" else 1, bf)
-        if fused:  # the sampled rows' tokens: y[t] = bf16(w_t * Y_row)
-            from oracle.oracle import bf16_round
-
-            w = o["served_w"][src[pick], 0].astype(np.float32)[:, None]
-            assert_bf16_close(y32[src[pick]], bf16_round(w * ref), f"expert {e} FFN rows (fused combine)")
-        else:
-            (assert_bf16_close if bf else assert_f32_close)(yp[pick], ref, f"expert {e} FFN rows")
+        (assert_bf16_close if bf else assert_f32_close)(yp[pick], ref, f"expert {e} FFN rows")
     # A5 combine of the GPU expert outputs
     if not fused:
         yc = port.combine(yp, pos, ws["served_w"].cpu().numpy(), bf)
         (assert_bf16_close if bf else assert_f32_close)(to_f32(c["y"]), yc, "combine")
     # end to end on sampled tokens: oracle FFN for each served slot + oracle combine
-    toks = rng.choice(T, size=min(16, T), replace=False)
+    toks = np.unique(np.concatenate([rng.choice(T, size=min(16, T), replace=False),
+                                     np.asarray(fused_toks, np.int64)]).astype(np.int64))
     yref = np.zeros((toks.size, d), np.float32)
     for i, t in enumerate(toks):
         acc = np.zeros(d, np.float32)
@@ -285,6 +285,48 @@ def test_top1_fused_combine_bit_identical(args, tmp_path):
         outs.append(torch.load(out))
     assert outs[0]["fused"] and not outs[1]["fused"]
     assert torch.equal(outs[0]["y"], outs[1]["y"])
+
+
+_FUSED2_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+from helpers import build_layer
+d, f, cg, T, resident = {args!r}
+layer, _, _ = build_layer(8, d, f, 2, "bf16", "swiglu", "topk_softmax", len(resident), resident,
+                          max_tokens=T, gemm_cta_group=cg)
+ys = []
+for i, n in enumerate((T, T // 3 + 5, T)):  # repeated forwards: the arrival counters re-zero themselves
+    x = torch.randn(n, d, generator=torch.Generator().manual_seed(7 + i)).to(torch.bfloat16).cuda()
+    ys.append(layer.forward(x).cpu())
+torch.save(dict(ys=ys, fused=layer.workspace()["y_perm"] is None), {out!r})
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [(256, 512, 1, 777, [0, 2, 5, 7]), (256, 512, 2, 1500, [1, 6]),
+                                  (768, 1024, 1, 3001, [0, 1, 2, 3, 4, 5, 6, 7]), (512, 768, 2, 2048, [3])])
+def test_top2_fused_combine_bit_identical(args, tmp_path):
+    """Top-2 layers: GEMM2's epilogue combining a token's two rows (the
+    second to arrive reads the first's published row; EMOE_FUSED_COMBINE=2,
+    opt-in) is bit-identical to GEMM2 + the separate combine
+    (EMOE_FUSED_COMBINE=0), with single- and double-served tokens and across
+    repeated forwards."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    outs = []
+    for flag in ("2", "0"):
+        out = tmp_path / f"y{flag}.pt"
+        code = _FUSED2_SCRIPT.format(root=str(root), tests=str(root / "tests"), args=args, out=str(out))
+        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, EMOE_FUSED_COMBINE=flag),
+                       timeout=300)
+        outs.append(torch.load(out))
+    assert outs[0]["fused"] and not outs[1]["fused"]
+    for a, b in zip(outs[0]["ys"], outs[1]["ys"]):
+        assert torch.equal(a, b)
 
 
 _RASTER_SCRIPT = r"""

@@ -106,10 +106,12 @@ def test_full_size_parity(cfg, port):
         ref = port.expert_ffn(xs, w1, w3, w2, 0 if act == "swiglu" else 1, True)
         if ws["y_perm"] is not None:
             assert_bf16_close(to_f32(ws["y_perm"][torch.from_numpy(rows).cuda()]), ref, f"expert {e} rows")
-        else:  # top-1 fused combine: y[t] = bf16(w_t * bf16(Y_row))
-            w = o["served_w"][toks, 0].astype(np.float32)[:, None]
-            assert_bf16_close(y32[toks], bf16_round(w * ref), f"expert {e} rows (fused combine)")
-    toks = rng.choice(T, 16, replace=False)
+        else:  # fused combine: tokens served by this expert alone have y[t] = bf16(w_t * bf16(Y_row))
+            single = served[toks, 1] < 0 if k == 2 else np.ones(toks.size, bool)
+            if single.any():
+                w = o["served_w"][toks[single], 0].astype(np.float32)[:, None]
+                assert_bf16_close(y32[toks[single]], bf16_round(w * ref[single]), f"expert {e} rows (fused combine)")
+    toks = rng.choice(T, 16 if ws["y_perm"] is not None else 48, replace=False)  # fused: more tokens here
     yref = np.zeros((toks.size, d), np.float32)
     for i, t in enumerate(toks):
         for j in range(k):

@@ -4,6 +4,9 @@ Compares, on sampled rows of each resident expert, the GPU rows with the
 oracle computed with mirrored bf16 rounding (H, Y rounded) and without (fp32
 H, fp64 accumulation): shows how much of the GPU-vs-mirrored difference is
 rounding flips at K = 4096 / 14336 rather than GPU error."""
+import os
+os.environ.setdefault("EMOE_FUSED_COMBINE", "0")  # these probes read the per-row Y_perm
+
 import sys
 from pathlib import Path
 

@@ -3,6 +3,9 @@
 python tools/gemm_check.py [T] [d] [f] [E] [k] [slots]
 Prints per-expert max/norm relative errors of H (GEMM1 SwiGLU) and Y (GEMM2).
 """
+import os
+os.environ.setdefault("EMOE_FUSED_COMBINE", "0")  # these probes read the per-row Y_perm
+
 import sys
 from pathlib import Path
 
