@@ -454,7 +454,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = dict(value=world * T / e2e_s, unit="tokens/s", h2d_bytes_per_step=x_host.numel() * x_host.element_size(),
-               d2h_bytes_per_step=y_host.numel() * y_host.element_size(), ms_per_step=e2e_s * 1e3)
+               d2h_bytes_per_step=y_host.numel() * y_host.element_size(), ms_per_step=e2e_s * 1e3,
+               calls=args.e2e_steps,
+               note="emoe_moe_forward_host_async per call (H2D x, K1-K5, D2H y), wall clock over the calls; "
+                    "the device-timed step also runs the A6 histogram update and per-stage events, which "
+                    "this path does not (about 5 % of a config-1 step, < 0.1 % of config 2)")
 
     # ---- roofline of the dominant kernel (the grouped FFN GEMMs)
     peaks = load_peaks()
