@@ -311,7 +311,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 // x -> (tf32(x), x - tf32(x)) into hi (may alias x) / lo, n multiple of 4
-__global__ void split_tf32_kernel(const float4* x, float4* hi, float4* __restrict__ lo, int64_t n4) {
+// rows_dev (nullable): the device's row count (seg_offsets[E]); rows past it
+// are never read by the GEMMs, so they are not split
+__global__ void split_tf32_kernel(const float4* x, float4* hi, float4* __restrict__ lo, int64_t n4,
+                                  const int64_t* rows_dev, int64_t row4) {
+  if (rows_dev) n4 = min(n4, *rows_dev * row4);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 v = x[i];
     float4 h, l;
@@ -334,8 +338,10 @@ __global__ void split_tf32_kernel(const float4* x, float4* hi, float4* __restric
 template <int EPI>
 __global__ void splitk_reduce_kernel(const float* __restrict__ partial, int k_splits, int64_t rows, int n_blocks,
                                      int out_block_cols, float* __restrict__ out_hi, float* __restrict__ out_lo,
-                                     int64_t ldo) {
-  const int64_t n_out = rows * (int64_t)n_blocks * out_block_cols;
+                                     int64_t ldo, const int64_t* __restrict__ rows_dev) {
+  // rows = the partial buffer's row stride; only the rows the GEMM wrote
+  // (seg_offsets[E] on the device) are reduced
+  const int64_t n_out = min(rows, *rows_dev) * (int64_t)n_blocks * out_block_cols;
   const int64_t acc_cols = (int64_t)n_blocks * BN;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_out; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / ((int64_t)n_blocks * out_block_cols);
@@ -391,13 +397,15 @@ CUtensorMap make_tmap_f32_2d(const void* base, uint64_t rows, uint64_t cols, uin
   return m;
 }
 
-void launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t s) {
+void launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t s, const int64_t* rows_dev,
+                       int row_elems) {
   EMOE_REQUIRE(n % 4 == 0, "split_tf32: element count must be a multiple of 4");
+  EMOE_REQUIRE(!rows_dev || row_elems % 4 == 0, "split_tf32: row length must be a multiple of 4");
   if (n == 0) return;
   const int64_t n4 = n / 4;
   const int blocks = (int)std::min<int64_t>(ceil_div(n4, 256), 148 * 8);
   tf32x3::split_tf32_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(hi),
-                                                   reinterpret_cast<float4*>(lo), n4);
+                                                   reinterpret_cast<float4*>(lo), n4, rows_dev, row_elems / 4);
   EMOE_CUDA(cudaGetLastError());
   count_launch();
 }
@@ -471,13 +479,16 @@ void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t*
     const int blocks = (int)std::min<int64_t>(ceil_div(n_out, 256), (int64_t)num_sms * 8);
     if (epi == EPI_SWIGLU)
       splitk_reduce_kernel<EPI_SWIGLU><<<blocks, 256, 0, stream>>>(p.partial, p.k_splits, split->rows, p.n_blocks,
-                                                                    p.out_block_cols, out_hi, out_lo, ldo);
+                                                                    p.out_block_cols, out_hi, out_lo, ldo,
+                                                                   seg_offsets + n_seg);
     else if (epi == EPI_RELU)
       splitk_reduce_kernel<EPI_RELU><<<blocks, 256, 0, stream>>>(p.partial, p.k_splits, split->rows, p.n_blocks,
-                                                                  p.out_block_cols, out_hi, out_lo, ldo);
+                                                                  p.out_block_cols, out_hi, out_lo, ldo,
+                                                                   seg_offsets + n_seg);
     else
       splitk_reduce_kernel<EPI_STORE><<<blocks, 256, 0, stream>>>(p.partial, p.k_splits, split->rows, p.n_blocks,
-                                                                   p.out_block_cols, out_hi, out_lo, ldo);
+                                                                   p.out_block_cols, out_hi, out_lo, ldo,
+                                                                   seg_offsets + n_seg);
     EMOE_CUDA(cudaGetLastError());
     count_launch();
   }

@@ -124,7 +124,9 @@ CUtensorMap make_tmap_f32_2d(const void* base, uint64_t rows, uint64_t cols, uin
 bool gemm_tf32x3_supported(int epi, int K, int N_out);
 int gemm_tf32x3_b_box_rows(int epi);
 // x -> tf32(x) in hi (hi may alias x), x - tf32(x) in lo; n % 4 == 0
-void launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t s);
+// rows_dev (optional): device row count bounding the split to rows * row_elems
+void launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t s,
+                       const int64_t* rows_dev = nullptr, int row_elems = 0);
 // split-K scratch for small batches: `rows` = the row capacity of the
 // operands, `capacity` floats at `partial`
 struct SplitK {

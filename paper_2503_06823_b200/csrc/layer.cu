@@ -364,7 +364,7 @@ struct emoe_layer {
         o2.a_hi = make_tmap_f32_2d(hr, (uint64_t)R, f, 128);
         o2.a_lo = make_tmap_f32_2d(hl, (uint64_t)R, f, 128);
       }
-      launch_split_tf32(static_cast<const float*>(xr), xh, xl, R * d, s);
+      launch_split_tf32(static_cast<const float*>(xr), xh, xl, R * d, s, segs + n_seg, d);
       const SplitK sk{splitk, splitk_cap, R};
       launch_grouped_gemm_tf32x3(epi1, o1, segs, slot_dev, seg_expert, n_seg, d, f, f, static_cast<float*>(hr), hl,
                                  f, num_sms, s, &sk);

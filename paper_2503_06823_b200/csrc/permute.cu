@@ -203,8 +203,9 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
     p[j] = pos[t * k + j];
     w[j] = served_w[t * k + j];
   }
-  const int nvec = d / 8;
-  for (int v = lane; v < nvec; v += 32) {
+  const int nvec = d / 8;  // gridDim.y blocks share a token group, each a column slice (small T)
+  const int v1 = (int)((int64_t)nvec * (blockIdx.y + 1) / gridDim.y);
+  for (int v = (int)((int64_t)nvec * blockIdx.y / gridDim.y) + lane; v < v1; v += 32) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int j = 0; j < k; ++j) {
       if (p[j] < 0) continue;
@@ -238,7 +239,8 @@ __global__ void __launch_bounds__(256) combine_f32_kernel(const float* __restric
     w[j] = served_w[t * k + j];
   }
   const int nvec = d / 4;
-  for (int v = lane; v < nvec; v += 32) {
+  const int v1 = (int)((int64_t)nvec * (blockIdx.y + 1) / gridDim.y);
+  for (int v = (int)((int64_t)nvec * blockIdx.y / gridDim.y) + lane; v < v1; v += 32) {
     float4 acc = make_float4(0, 0, 0, 0);
     for (int j = 0; j < k; ++j) {
       if (p[j] < 0) continue;
@@ -307,14 +309,23 @@ void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int
                     void* y, cudaStream_t s) {
   const int nblocks = (int)ceil_div(T, 8);
   if (nblocks == 0) return;
+  // few token groups (small T): split the columns over gridDim.y blocks so
+  // the combine still spans the GPU (>= 32 vectors per slice)
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  const int nvec = dtype == DT_F32 ? d / 4 : d / 8;
+  const int ny = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * sms, nblocks), nvec / 32));
   if (dtype == DT_F32) {
     EMOE_REQUIRE(d % 4 == 0, "combine: d must be a multiple of 4");
-    combine_f32_kernel<<<nblocks, 256, 0, s>>>(static_cast<const float*>(Y), T, d, k, pos, served_w,
-                                               static_cast<float*>(y));
+    combine_f32_kernel<<<dim3(nblocks, ny), 256, 0, s>>>(static_cast<const float*>(Y), T, d, k, pos, served_w,
+                                                         static_cast<float*>(y));
   } else {
     EMOE_REQUIRE(d % 8 == 0, "combine: d must be a multiple of 8");
-    combine_bf16_kernel<<<nblocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Y), T, d, k, pos, served_w,
-                                                static_cast<__nv_bfloat16*>(y));
+    combine_bf16_kernel<<<dim3(nblocks, ny), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Y), T, d, k, pos,
+                                                          served_w, static_cast<__nv_bfloat16*>(y));
   }
   EMOE_CUDA(cudaGetLastError());
   count_launch();
