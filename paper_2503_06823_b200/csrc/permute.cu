@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) scan_blocks_kernel(const int32_t* __restr
 }
 
 // K3a, pass 2: padded segment offsets (a running sum over E experts)
-// (one block of 1024 threads, Hillis-Steele scan in shared memory)
+// (one block of the next power of two >= E threads, Hillis-Steele scan in shared memory)
 __global__ void __launch_bounds__(1024) seg_offsets_kernel(const int32_t* __restrict__ counts, int E, int pad,
                                                            int64_t* __restrict__ seg_offsets) {
   __shared__ int64_t buf[2][1024];
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(1024) seg_offsets_kernel(const int32_t* __rest
   int cur = 0;
   buf[cur][i] = v;
   __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {
     buf[cur ^ 1][i] = buf[cur][i] + (i >= off ? buf[cur][i - off] : 0);
     cur ^= 1;
     __syncthreads();
@@ -261,7 +261,9 @@ void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32
   EMOE_REQUIRE(E <= 1024, "scan: too many experts");
   scan_blocks_kernel<<<E, 256, 0, s>>>(block_counts, nblocks, E, block_base, counts);
   EMOE_CUDA(cudaGetLastError());
-  seg_offsets_kernel<<<1, 1024, 0, s>>>(counts, E, pad, seg_offsets);
+  int threads = 32;  // a power of two >= E: the scan's rounds are log2(threads)
+  while (threads < E) threads *= 2;
+  seg_offsets_kernel<<<1, threads, 0, s>>>(counts, E, pad, seg_offsets);
   EMOE_CUDA(cudaGetLastError());
   count_launch(2);
 }

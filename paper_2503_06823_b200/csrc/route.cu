@@ -390,6 +390,8 @@ __global__ void __launch_bounds__(F32_GATE_THREADS) gate_route_f32_kernel(const 
 // fp32 gate logits only, one warp per token (small T: the fused kernel above
 // has one block per 128 tokens, too few blocks to cover the GPU), followed by
 // route_from_logits_kernel.  Same dot-product order as the fused kernel.
+// blockIdx.y selects a slice of the experts (each expert's sum is computed
+// in the same order whatever the slicing), so small T still spans the GPU.
 __global__ void __launch_bounds__(256) gate_logits_f32_kernel(const float* __restrict__ x,
                                                               const float* __restrict__ wg, int64_t T, int d, int E,
                                                               float* __restrict__ logits) {
@@ -398,8 +400,9 @@ __global__ void __launch_bounds__(256) gate_logits_f32_kernel(const float* __res
   if (t >= T) return;
   const float* xr = x + t * d;
   const bool vec = (d & 3) == 0;
-  for (int e0 = 0; e0 < E; e0 += 8) {
-    const int ne = min(8, E - e0);
+  const int e_beg = E * blockIdx.y / gridDim.y, e_end = E * (blockIdx.y + 1) / gridDim.y;
+  for (int e0 = e_beg; e0 < e_end; e0 += 8) {
+    const int ne = min(8, e_end - e0);
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (vec) {
       for (int i = lane * 4; i < d; i += 128) {
@@ -523,8 +526,10 @@ void launch_gate_route(const void* x, const void* wg, int dtype, const RouteArgs
   if (nblocks == 0) return;
   if (dtype == DT_F32 && o.logits && nblocks < 74) {
     // small T: logits with one warp per token over the whole GPU, then routing
-    gate_logits_f32_kernel<<<(unsigned)ceil_div(a.T, 8), 256, 0, s>>>(
-        static_cast<const float*>(x), static_cast<const float*>(wg), a.T, a.d, a.E, o.logits);
+    const int nbx = (int)ceil_div(a.T, 8);
+    const int ny = std::max(1, std::min((2 * 148 + nbx - 1) / nbx, (a.E + 1) / 2));  // >= 2 experts per warp
+    gate_logits_f32_kernel<<<dim3(nbx, ny), 256, 0, s>>>(static_cast<const float*>(x),
+                                                          static_cast<const float*>(wg), a.T, a.d, a.E, o.logits);
     EMOE_CUDA(cudaGetLastError());
     count_launch();
     launch_route_from_logits(o.logits, a, o, s);
