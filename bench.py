@@ -311,6 +311,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--gemm-cta-group", type=int, default=0, choices=[0, 1, 2],
                     help="FFN GEMM CTA group (0 = the layer's auto choice)")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay each step as one captured CUDA graph (stage times then from eager steps "
+                         "after the timed region) or launch it eagerly; auto = graph for the sub-millisecond "
+                         "steps of configs 1 and 3 (launch-bound: +27 %% / +6 %%, profiles/r01_cuda_graph_ab.jsonl), "
+                         "eager for config 2 (stage events inside the timed region)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = every GPU serves the config's full batch (default); strong = the "
                          "config's batch is split over the GPUs (N must divide its 32 prompts)")
@@ -367,17 +372,17 @@ def main():
         ep_model = ExpertParallelMoE(LayerBackend(layer, info["global_resident"]), info["global_resident"],
                                     loads=info["aggregate"])
 
-    def step():
+    def eager_step():
         if ep_model is not None:
             ep_model(x)
         else:
             layer.forward(x, out=y)
         ws_topk = layer_ws_topk(layer)
         emoe.moesim.check(_lib.lib.emoe_hist_update(pred.h, C.c_void_p(ws_topk), P, Tp, C.c_void_p(tid.data_ptr()),
-                                                    C.c_void_p(stream.cuda_stream)))
+                                                    C.c_void_p(torch.cuda.current_stream().cuda_stream)))
 
     for _ in range(args.warmup):
-        step()
+        eager_step()
     torch.cuda.synchronize()
     ws = layer.workspace()
     counts = ws["counts"].cpu().numpy()
@@ -385,7 +390,31 @@ def main():
     hit_rate = float(ws["route_hit"].float().mean().item())
     fallback = float((ws["route_rank"] == -1).float().mean().item())
 
-    layer.set_profiling(True)
+    # --graph on: the step as one CUDA graph (every kernel of the step
+    # replayed as a whole: no per-launch host or queue gaps, which matter for
+    # the small configs; EP steps stay eager).  The per-stage events are not
+    # captured (their timestamps inside replays were not trustworthy), so the
+    # stage times then come from eager steps right after the timed region.
+    graph = None
+    launches_per_step = 0
+    use_graph = args.graph == "on" or (args.graph == "auto" and args.config in ("synthetic", "switch"))
+    if use_graph and ep_model is None:
+        l0 = _lib.lib.emoe_kernel_launches()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+            eager_step()
+        launches_per_step = int(_lib.lib.emoe_kernel_launches() - l0)
+        graph.replay()  # warm replay
+        torch.cuda.synchronize()
+    else:
+        layer.set_profiling(True)
+
+    def step():
+        if graph is not None:
+            graph.replay()
+        else:
+            eager_step()
+
     launches0 = _lib.lib.emoe_kernel_launches()
     if world > 1:
         dist.barrier()
@@ -397,7 +426,7 @@ def main():
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
-    launches = int(_lib.lib.emoe_kernel_launches() - launches0)
+    launches = int(_lib.lib.emoe_kernel_launches() - launches0) + launches_per_step * args.steps
     clock_note = "sampled during the timed region"
     if len(clk.lines) < 3:  # timed region shorter than the sampler period: sample a continuation of the same loop
         with ClockSampler(local) as clk:
@@ -410,6 +439,11 @@ def main():
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     if ep_model is None:
+        if graph is not None:  # stage times from eager steps after the timed replays
+            layer.set_profiling(True)
+            for _ in range(args.steps):
+                eager_step()
+            torch.cuda.synchronize()
         stages = layer.stage_times()
     else:  # no per-stage events on the EP path: attribute the whole step to the FFN (a lower bound)
         stages = dict(route=0.0, permute=0.0, gemm1=ms, gemm2=0.0, combine=0.0)
@@ -514,6 +548,8 @@ def main():
                data="synthetic (random-init weights; routing = reference Markov trace embedded in x)",
                config=dict(workload=cfg["workload"] + (f" split over {world} GPUs" if strong else ""),
                            tokens_per_step=T, tokens_per_gpu=T, num_experts=cfg["E"], top_k=cfg["k"],
+                           step_launch=("one CUDA graph per step (replayed); stages_ms and the roofline from as many "
+                                        "eager steps right after the timed region") if graph is not None else "eager",
                            resident_experts=cfg["L"], resident_set=[e for e in range(cfg["E"])
                                                                      if info["resident"][e]],
                            d_model=d, d_ff=f, activation=cfg["act"], served_rows=S, hit_rate=round(hit_rate, 4),

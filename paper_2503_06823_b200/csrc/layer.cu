@@ -257,7 +257,13 @@ struct emoe_layer {
       for (cudaEvent_t& e : set) EMOE_CUDA(cudaEventCreate(&e));
       ev_pool.push_back(set);
     }
-    EMOE_CUDA(cudaEventRecord(ev_pool[ev_used][i], s));
+    // inside a stream capture the events must be external record nodes (a
+    // plain record would only order the capture)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    EMOE_CUDA(cudaStreamIsCapturing(s, &cap));
+    EMOE_CUDA(cudaEventRecordWithFlags(ev_pool[ev_used][i], s,
+                                       cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal
+                                                                            : cudaEventRecordDefault));
     if (i == 5) ++ev_used;
   }
 
