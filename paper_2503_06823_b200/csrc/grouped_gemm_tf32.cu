@@ -461,7 +461,14 @@ void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t*
   if (split && split->partial) {
     const int64_t max_tiles = split->rows / BM * p.n_blocks;
     int ks = 1;
-    while (ks < 4 && max_tiles * ks < 2 * num_sms && (K / BK) / (2 * ks) >= 2 * CHUNK_KB) ks *= 2;
+    // at most 2 splits: config 1's GEMM2 runs 64.0 us with 4 splits, 59.7 us with 2 (the
+    // reduce reads half the partials; profiles/r01_tf32_splitk_ab.jsonl)
+    while (ks < 2 && max_tiles * ks < 2 * num_sms && (K / BK) / (2 * ks) >= 2 * CHUNK_KB) ks *= 2;
+    static const int forced = [] {  // EMOE_TF32_SPLITK=n: force n splits where the scratch allows (A/B runs)
+      const char* v = getenv("EMOE_TF32_SPLITK");
+      return v ? atoi(v) : 0;
+    }();
+    if (forced > 0) ks = forced;
     if (ks > 1 && (size_t)ks * split->rows * p.n_blocks * BN <= split->capacity) {
       p.k_splits = ks;
       p.partial = split->partial;

@@ -714,7 +714,8 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
           // the row capacity (up to 4 splits of 128 accumulator columns)
           size_t need = 0;
           for (const int nb : {epi1 == EPI_SWIGLU ? (int)f / 64 : (int)f / 128, (int)d / 128})
-            if (L->rows_cap / 128 * nb < 2 * L->num_sms) need = std::max(need, (size_t)4 * L->rows_cap * nb * 128);
+            if (L->rows_cap / 128 * nb < 2 * L->num_sms || getenv("EMOE_TF32_SPLITK"))  // (forced splits: A/B runs)
+              need = std::max(need, (size_t)4 * L->rows_cap * nb * 128);
           if (need) {
             L->splitk = dmalloc<float>(need);
             L->splitk_cap = need;
