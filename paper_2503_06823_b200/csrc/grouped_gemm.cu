@@ -50,7 +50,7 @@ constexpr int TMEM_COLS = 512;
 // (128-B swizzled rows) per epilogue warp
 constexpr int OUT_BOX_COLS = 64;
 constexpr int OUT_BOX_BYTES = 32 * OUT_BOX_COLS * 2;
-constexpr int BAR_AREA_BYTES = 2048;  // mbarriers, TMEM slot, segment offsets (int32, <= MAX_EXPERTS + 1)
+constexpr int BAR_AREA_BYTES = 2048;  // mbarriers, TMEM slot, segment offsets (int32) and slots (int16)
 
 // CG = CTAs per MMA (1 or 2), EW = epilogue warps (4: one per TMEM lane
 // quarter; 8: two per quarter, each draining half of the accumulator columns,
@@ -73,7 +73,8 @@ struct Cfg {
   static constexpr int NUM_THREADS = 64 + 32 * EW;
   static constexpr int SMEM_BYTES = 1024 /*align*/ + STAGES * STAGE_BYTES + OUT_STAGE_BYTES + BAR_AREA_BYTES;
   static_assert(SMEM_BYTES <= 232448, "shared memory over the sm_100 per-block limit");
-  static_assert(2 * STAGES * 8 + 4 * 8 + 16 + 4 * (MAX_EXPERTS + 1) <= BAR_AREA_BYTES, "barrier area");
+  static_assert(2 * STAGES * 8 + 4 * 8 + 16 + 4 * (MAX_EXPERTS + 1) + 2 * MAX_EXPERTS <= BAR_AREA_BYTES,
+                "barrier area");
 };
 
 struct Params {
@@ -138,8 +139,16 @@ __device__ __forceinline__ TileCoord decode_tile(int t, int total_mb, int n_bloc
   c.nb = n0 + local / rows_in_group;
   c.mb = g * group_m + (local - (c.nb - n0) * rows_in_group);
   const int32_t row = c.mb * tile_m;
-  int e = 0;
-  while (e + 1 < num_experts && offs[e + 1] <= row) ++e;
+  // last segment starting at or before `row` (binary search: E = 128 made the
+  // linear scan a ~2K-cycle per-tile stall of the producer warp)
+  int e = 0, hi = num_experts - 1;
+  while (e < hi) {
+    const int mid = (e + hi + 1) >> 1;
+    if (offs[mid] <= row)
+      e = mid;
+    else
+      hi = mid - 1;
+  }
   c.expert = e;
   return c;
 }
@@ -262,6 +271,8 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
   uint64_t* tempty_bar = tfull_bar + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int32_t* s_offs = reinterpret_cast<int32_t*>(tmem_slot + 4);
+  int16_t* s_slot = reinterpret_cast<int16_t*>(s_offs + MAX_EXPERTS + 1);  // weight slot of each segment
+                                                                            // (the producer's per-tile lookup)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -273,6 +284,8 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
 
   for (int i = threadIdx.x; i <= E; i += C::NUM_THREADS)
     s_offs[i] = (int32_t)(p.single_rows > 0 ? (i == 0 ? 0 : p.single_rows) : p.seg_offsets[i]);
+  for (int i = threadIdx.x; i < E; i += C::NUM_THREADS)
+    s_slot[i] = (int16_t)p.slot_of_expert[p.seg_expert ? p.seg_expert[i] : i];
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
@@ -317,7 +330,7 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
       uint32_t phase = 0;
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
         const TileCoord c = decode_tile(t, total_mb, p.n_blocks, p.group_m, C::TILE_M, s_offs, E, p.group_n);
-        const int slot = p.slot_of_expert[p.seg_expert ? p.seg_expert[c.expert] : c.expert];
+        const int slot = s_slot[c.expert];
         const int a_row = c.mb * C::TILE_M + (int)rank * 128;
         int b_row;
         const CUtensorMap* tb = &tmap_b;
