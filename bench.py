@@ -527,13 +527,21 @@ def main():
                         algorithmic=f"2*{nmat}*d*f*S = {ffn_flops:.4g} FLOP per step (S={S} served rows)",
                         peak_kind="fp32 cuBLAS SGEMM 8192^3 (TF32 off), best of 5, measured in this run")
     else:
-        roofline = dict(bound="tensor", achieved=round(achieved, 1), peak=peaks["bf16_sustained"], unit="TFLOP/s",
-                        frac=round(achieved / peaks["bf16_sustained"], 4), traffic=traffic,
+        # the sustained (power-capped) rate for a timed region long enough to
+        # reach it, the burst rate for a short one (config 3: 20 steps = 10 ms)
+        long_region = args.steps * ms >= 150.0
+        peak = peaks["bf16_sustained"] if long_region else peaks["bf16"]
+        roofline = dict(bound="tensor", achieved=round(achieved, 1), peak=peak, unit="TFLOP/s",
+                        frac=round(achieved / peak, 4), traffic=traffic,
                         traffic_unit="bytes per step (GEMM1 + GEMM2), ncu dram__bytes_read+write",
                         kernel="grouped_gemm_kernel (K4: GEMM1 SwiGLU + GEMM2), avg of the timed steps",
                         algorithmic=f"2*{nmat}*d*f*S = {ffn_flops:.4g} FLOP per step (S={S} served rows)",
-                        peak_kind=f"bf16_tflops_sustained ({peaks['source']}); burst {peaks['bf16']}",
-                        frac_of_burst=round(achieved / peaks["bf16"], 4))
+                        peak_kind=(f"bf16_tflops_sustained ({peaks['source']}; timed region >= 150 ms); "
+                                   f"burst {peaks['bf16']}") if long_region else
+                                  (f"bf16_tflops burst ({peaks['source']}; timed region {args.steps * ms:.0f} ms "
+                                   f"< 150 ms); sustained {peaks['bf16_sustained']}"),
+                        frac_of_burst=round(achieved / peaks["bf16"], 4),
+                        frac_of_sustained=round(achieved / peaks["bf16_sustained"], 4))
     hbm_stages = {}
     eb = elem_bytes(cfg)
     xb = T * d * eb
