@@ -44,6 +44,7 @@ constexpr int CHUNK_KB = 4;  // k-blocks (128 of K) per accumulator chunk
 constexpr int TMEM_COLS = SLOTS * BN;
 constexpr int MAX_SEGS = 256;
 constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 4096;
+static_assert(2 * STAGES * 8 + 2 * SLOTS * 8 + 16 + 4 * (2 * MAX_SEGS + 1) <= 4096, "barrier / table area");
 
 struct Params {
   const int64_t* seg_offsets;     // [n_seg + 1], multiples of 128
@@ -128,10 +129,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tempty_bar = tfull_bar + SLOTS;  // [SLOTS]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + SLOTS);
   int32_t* s_offs = reinterpret_cast<int32_t*>(tmem_slot + 4);
+  int32_t* s_slot = s_offs + MAX_SEGS + 1;  // weight slot per segment: no dependent global loads per tile
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int S = p.n_seg;
   for (int i = threadIdx.x; i <= S; i += NUM_THREADS) s_offs[i] = (int32_t)p.seg_offsets[i];
+  for (int i = threadIdx.x; i < S; i += NUM_THREADS) s_slot[i] = p.slot_of_expert[p.seg_expert ? p.seg_expert[i] : i];
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&ta_hi);
     tma_prefetch_desc(&ta_lo);
@@ -172,7 +175,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int t = w / p.k_splits, split = w - t * p.k_splits;
         int mb, nb, seg;
         decode(t, total_mb, p.n_blocks, p.group_m, s_offs, S, mb, nb, seg);
-        const int slot = p.slot_of_expert[p.seg_expert ? p.seg_expert[seg] : seg];
+        const int slot = s_slot[seg];
         const int a_row = mb * BM;
         const int b_row = slot * p.b_rows_per_slot + nb * (EPI == EPI_SWIGLU ? BN / 2 : BN);
         const int kbeg = split * k_blocks / p.k_splits, kend = (split + 1) * k_blocks / p.k_splits;
