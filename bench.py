@@ -308,6 +308,8 @@ def main():
                     help="--config stream: eMoE predicted residency, or the reference's on-demand baseline "
                          "(engine.cpp:469-502) for comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="--impl reference: seconds of CPU work for the warm-up + timed steps together")
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--gemm-cta-group", type=int, default=0, choices=[0, 1, 2],
                     help="FFN GEMM CTA group (0 = the layer's auto choice)")
@@ -958,7 +960,7 @@ def main_reference(args, cfg, rank, world):
             experts[e] = (w1, w3, w2)
     # size the per-step sample so W+K steps finish within a few minutes
     dt = cpu_reference_step(cfg, info, x, wg, experts, n, port, ref, threads)
-    budget_s = 150.0 / (args.steps + args.warmup)
+    budget_s = args.ref_budget_s / (args.steps + args.warmup)
     n = int(max(4, min(4096, n * budget_s / max(dt, 1e-3))))
     for _ in range(args.warmup):
         cpu_reference_step(cfg, info, x, wg, experts, n, port, ref, threads)
