@@ -42,6 +42,14 @@ __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + 
 // ---------------------------------------------------------------------------
 // bf16 helpers
 // ---------------------------------------------------------------------------
+// fp32 -> tf32 (10 explicit mantissa bits), round to nearest even, low 13
+// bits zero, so x - round_tf32(x) is the exact remainder (3xTF32 hi / lo split)
+__device__ __forceinline__ float round_tf32(float x) {
+  uint32_t u = __float_as_uint(x);
+  u = (u + 0xFFFu + ((u >> 13) & 1u)) & ~0x1FFFu;
+  return __uint_as_float(u);
+}
+
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

@@ -87,11 +87,7 @@ __host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N) {
 // x rounded to 10 explicit mantissa bits (nearest, ties to even) with the low
 // 13 bits exactly zero, so x - round_tf32(x) is the exact remainder (cvt.rna.tf32
 // leaves the low bits unspecified).  Finite inputs only (weights/activations).
-__device__ __forceinline__ float round_tf32(float x) {
-  uint32_t u = __float_as_uint(x);
-  u = (u + 0xFFFu + ((u >> 13) & 1u)) & ~0x1FFFu;
-  return __uint_as_float(u);
-}
+using emoe::round_tf32;
 
 __device__ __forceinline__ void decode(int t, int total_mb, int n_blocks, int group_m, const int32_t* offs, int n_seg,
                                        int& mb, int& nb, int& seg) {

@@ -56,7 +56,7 @@ void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32
 // K3b: stable permutation + row gather into the padded segments
 void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
                     const int64_t* seg_offsets, const int64_t* block_base, void* x_perm, int32_t* pos,
-                    int32_t* row_token, cudaStream_t s);
+                    int32_t* row_token, cudaStream_t s, float* x_hi = nullptr, float* x_lo = nullptr);
 // Expert-parallel peer-memory addressing: rank q's receive (or expert-output)
 // buffer is base[q] (own buffer or a CUDA-IPC mapping); dest[e] = rank that
 // computes this rank's rows of expert e; row_shift[e] = (row of segment e in

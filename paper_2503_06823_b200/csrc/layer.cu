@@ -325,9 +325,13 @@ struct emoe_layer {
     const int E = cfg.num_experts;
     launch_scan(block_counts, nb, E, seg_pad, counts, seg_offsets, block_base, s);
     EMOE_CUDA(cudaMemsetAsync(row_token, 0xff, sizeof(int32_t) * rows_cap, s));
+    // 3xTF32 layers: the permute also writes the hi / lo split of every row
+    // (the GEMM reads only those), so ffn() skips the separate split pass
     launch_permute(x, elem, T, cfg.d_model, E, cfg.top_k, served_idx, seg_offsets, block_base, x_perm, pos,
-                   row_token, s);
+                   row_token, s, tf32 ? x_hi : nullptr, tf32 ? x_lo : nullptr);
+    perm_split_done = tf32;
   }
+  bool perm_split_done = false;  // x_hi / x_lo hold the split of x_perm's rows
 
   // A4 over rows [R][d] in n_seg padded segments (seg_expert null: segment i = expert i).
   // workspace = the rows are the layer's own x_perm/h/y_perm (cached tensor maps).
@@ -370,7 +374,8 @@ struct emoe_layer {
         o2.a_hi = make_tmap_f32_2d(hr, (uint64_t)R, f, 128);
         o2.a_lo = make_tmap_f32_2d(hl, (uint64_t)R, f, 128);
       }
-      launch_split_tf32(static_cast<const float*>(xr), xh, xl, R * d, s, segs + n_seg, d);
+      if (!(workspace && perm_split_done && xr == x_perm))
+        launch_split_tf32(static_cast<const float*>(xr), xh, xl, R * d, s, segs + n_seg, d);
       const SplitK sk{splitk, splitk_cap, R};
       launch_grouped_gemm_tf32x3(epi1, o1, segs, slot_dev, seg_expert, n_seg, d, f, f, static_cast<float*>(hr), hl,
                                  f, num_sms, s, &sk);

@@ -85,7 +85,8 @@ template <bool REMOTE>
 __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
     const uint8_t* __restrict__ x, int row_bytes, int64_t T, int E, int k, const int32_t* __restrict__ served_idx,
     const int64_t* __restrict__ seg_offsets, const int64_t* __restrict__ block_base, uint8_t* __restrict__ x_perm,
-    int32_t* __restrict__ pos, int32_t* __restrict__ row_token, PeerRows peers) {
+    int32_t* __restrict__ pos, int32_t* __restrict__ row_token, PeerRows peers, float* __restrict__ x_hi,
+    float* __restrict__ x_lo) {
   extern __shared__ int32_t sh[];
   int32_t* warp_counts = sh;          // [4][E]
   int32_t* dst_s = sh + 4 * E;        // [RT][k]
@@ -183,6 +184,13 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
         uint8_t* row = REMOTE ? dptr_s[tok[u] * k + j] : x_perm + (int64_t)d * row_bytes;
         if (REMOTE && !row) continue;
         reinterpret_cast<uint4*>(row)[v] = val[u];
+        if (!REMOTE && x_hi) {  // fp32 rows of a 3xTF32 layer: the hi / lo split as well
+          const float4 f = *reinterpret_cast<const float4*>(&val[u]);
+          const float4 h = make_float4(round_tf32(f.x), round_tf32(f.y), round_tf32(f.z), round_tf32(f.w));
+          reinterpret_cast<float4*>(x_hi + (int64_t)d * (row_bytes / 4))[v] = h;
+          reinterpret_cast<float4*>(x_lo + (int64_t)d * (row_bytes / 4))[v] =
+              make_float4(f.x - h.x, f.y - h.y, f.z - h.z, f.w - h.w);
+        }
       }
     }
   }
@@ -270,7 +278,8 @@ void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32
 
 void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
                     const int64_t* seg_offsets, const int64_t* block_base, void* x_perm, int32_t* pos,
-                    int32_t* row_token, cudaStream_t s) {
+                    int32_t* row_token, cudaStream_t s, float* x_hi, float* x_lo) {
+  EMOE_REQUIRE(!x_hi || (elem_bytes == 4 && x_lo), "permute: the tf32 split needs fp32 rows and both outputs");
   const int row_bytes = d * elem_bytes;
   EMOE_REQUIRE(row_bytes % 16 == 0, "permute: row bytes must be a multiple of 16");
   const int nblocks = (int)ceil_div(T, RT);
@@ -287,7 +296,7 @@ void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int 
   permute_kernel<false><<<dim3(nblocks, ny), PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
                                                                served_idx, seg_offsets, block_base,
                                                                static_cast<uint8_t*>(x_perm), pos, row_token,
-                                                               PeerRows{});
+                                                               PeerRows{}, x_hi, x_lo);
   EMOE_CUDA(cudaGetLastError());
   count_launch();
 }
@@ -302,7 +311,7 @@ void launch_permute_remote(const void* x, int elem_bytes, int64_t T, int d, int 
   const size_t smem = (4 * (size_t)E + (size_t)((RT * k + 1) & ~1)) * sizeof(int32_t) + (size_t)RT * k * 8;
   permute_kernel<true><<<nblocks, PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
                                                               served_idx, seg_offsets, block_base, nullptr, pos,
-                                                              nullptr, peers);
+                                                              nullptr, peers, nullptr, nullptr);
   EMOE_CUDA(cudaGetLastError());
   count_launch();
 }
