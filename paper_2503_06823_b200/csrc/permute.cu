@@ -81,7 +81,10 @@ constexpr int GATHER_UNROLL = 8;
 // at row pos = d + row_shift[e], d being the local position above; pos[t][j]
 // then holds that remote row.  The per-block tail fence makes the NVLink
 // stores visible system-wide before the host-ordered signal kernel runs.
-template <bool REMOTE>
+// SPLIT (fp32 rows of a 3xTF32 layer): also write each row's tf32 hi / lo
+// parts to x_hi / x_lo (a separate instantiation, so the other layers' permute
+// carries none of it)
+template <bool REMOTE, bool SPLIT = false>
 __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
     const uint8_t* __restrict__ x, int row_bytes, int64_t T, int E, int k, const int32_t* __restrict__ served_idx,
     const int64_t* __restrict__ seg_offsets, const int64_t* __restrict__ block_base, uint8_t* __restrict__ x_perm,
@@ -184,7 +187,7 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
         uint8_t* row = REMOTE ? dptr_s[tok[u] * k + j] : x_perm + (int64_t)d * row_bytes;
         if (REMOTE && !row) continue;
         reinterpret_cast<uint4*>(row)[v] = val[u];
-        if (!REMOTE && x_hi) {  // fp32 rows of a 3xTF32 layer: the hi / lo split as well
+        if (SPLIT) {  // fp32 rows of a 3xTF32 layer: the hi / lo split as well
           const float4 f = *reinterpret_cast<const float4*>(&val[u]);
           const float4 h = make_float4(round_tf32(f.x), round_tf32(f.y), round_tf32(f.z), round_tf32(f.w));
           reinterpret_cast<float4*>(x_hi + (int64_t)d * (row_bytes / 4))[v] = h;
@@ -293,10 +296,11 @@ void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int 
     return n;
   }();
   const int ny = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * sms, nblocks), row_bytes / 16 / 8));
-  permute_kernel<false><<<dim3(nblocks, ny), PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
-                                                               served_idx, seg_offsets, block_base,
-                                                               static_cast<uint8_t*>(x_perm), pos, row_token,
-                                                               PeerRows{}, x_hi, x_lo);
+  auto kernel = x_hi ? permute_kernel<false, true> : permute_kernel<false, false>;
+  kernel<<<dim3(nblocks, ny), PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
+                                                          served_idx, seg_offsets, block_base,
+                                                          static_cast<uint8_t*>(x_perm), pos, row_token, PeerRows{},
+                                                          x_hi, x_lo);
   EMOE_CUDA(cudaGetLastError());
   count_launch();
 }
