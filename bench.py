@@ -125,8 +125,76 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# synthetic workload
+# synthetic workload: one deterministic CPU generator shared by both arms
 # ---------------------------------------------------------------------------
+X_CHUNK = 4096  # x is generated in 4096-row chunks, each from its own seed
+DIGEST_ROWS = 256  # input_digest covers these first rows of x (both arms)
+
+
+def input_gate(cfg):
+    """Gate weights [E][d] in float64: orthonormal rows (QR of a seeded N(0,1)
+    matrix), so x can be built to reproduce a routing trace exactly."""
+    import torch
+
+    g = torch.Generator().manual_seed(1234)
+    q, _ = torch.linalg.qr(torch.randn(cfg["d"], cfg["E"], generator=g, dtype=torch.float64))
+    return q.T.contiguous()
+
+
+def input_expert(cfg, e):
+    """Expert e's weights in the config dtype, seeded per (layer 0, expert,
+    matrix) = 1234 ^ (e << 4 | mat): W1, W3 ~ N(0, 1/d),
+    W2 ~ N(0, 1/f); W3 is None for ReLU experts."""
+    import torch
+
+    d, f, td = cfg["d"], cfg["f"], torch_dtype(cfg)
+
+    def mat(j, rows, cols, fan_in):
+        g = torch.Generator().manual_seed(1234 ^ (e << 4 | j))
+        return (torch.randn(rows, cols, generator=g) / fan_in ** 0.5).to(td)
+
+    w3 = mat(1, f, d, d) if cfg["act"] == "swiglu" else None
+    return mat(0, f, d, d), w3, mat(2, d, f, f)
+
+
+def input_x(cfg, wg64, choices, rows):
+    """The first `rows` activations [rows][d] of the serving batch: chunk c
+    (rows 4096c ..) from its own seed, x = logits . W_g + noise orthogonal
+    to W_g's rows, where logit[c_r] = 8 - r at the trace's ranked choices and
+    the rest uniform in [-4, 4) (multiples of 1/64): the gate computed from x
+    reproduces the trace's routing.  float64 arithmetic on the CPU, rounded
+    to the config dtype, so both bench arms hold the same bits."""
+    import torch
+
+    E, d, k, td = cfg["E"], cfg["d"], cfg["k"], torch_dtype(cfg)
+    out = torch.empty(rows, d, dtype=td)
+    ch = torch.from_numpy(np.ascontiguousarray(choices[:rows])).long()
+    for c0 in range(0, rows, X_CHUNK):
+        n = min(X_CHUNK, rows - c0)
+        g = torch.Generator().manual_seed(7919 * (c0 // X_CHUNK + 1) + 1234)
+        lg = torch.round((torch.rand(n, E, generator=g, dtype=torch.float64) * 8.0 - 4.0) * 64) / 64
+        for r in range(k):
+            lg.scatter_(1, ch[c0:c0 + n, r:r + 1], 8.0 - r)
+        z = torch.randn(n, d, generator=g).double()
+        z -= (z @ wg64.T) @ wg64
+        out[c0:c0 + n] = (lg @ wg64 + z).to(td)
+    return out
+
+
+def input_digest(x_rows, wg, experts):
+    """sha256 over the bytes both arms compute on (x sample rows, W_g, the
+    resident experts' weights): equal digests = same inputs."""
+    import hashlib
+
+    import torch
+
+    h = hashlib.sha256()
+    for t in [x_rows, wg] + [w for e in sorted(experts) for w in experts[e] if w is not None]:
+        t = t.contiguous()
+        h.update((t.view(torch.int16) if t.dtype == torch.bfloat16 else t).numpy().tobytes())
+    return h.hexdigest()[:16]
+
+
 def build_workload(cfg, device, cta_group=0, rank=0, world=1, parallel="replicas", strong=False):
     import torch
 
@@ -177,41 +245,35 @@ def build_workload(cfg, device, cta_group=0, rank=0, world=1, parallel="replicas
         # rank: same fitted predictor, same request mix)
         loads = owned_experts(plan_destinations(global_resident, E, world, agg[0]), rank)
 
-    # ---- layer, weights (random-init, Mixtral/Switch shapes), planned loads
+    # ---- inputs (CPU generator shared with --impl reference), layer, planned loads
+    wg64 = input_gate(cfg)
     td = torch_dtype(cfg)
     layer = MoELayer(d, f, E, k, activation=cfg["act"], dtype=cfg.get("dtype", "bf16"), weight_mode=cfg["wm"],
                      num_slots=max(1, len(loads)), max_tokens=T, gemm_cta_group=cta_group)
-    g = torch.Generator(device=device).manual_seed(1234)
-    q, _ = torch.linalg.qr(torch.randn(d, E, generator=g, device=device))  # orthonormal gate rows
-    wg = q.T.contiguous()
-    layer.set_gate(wg.to(td).cpu())
+    layer.set_gate(wg64.to(td))
+    experts = {}
     for e in range(E):
-        w1 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(td).cpu()
-        w3 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(td).cpu() \
-            if cfg["act"] == "swiglu" else None
-        w2 = (torch.randn(d, f, generator=g, device=device) / f ** 0.5).to(td).cpu()
+        w1, w3, w2 = input_expert(cfg, e)
         layer.register_expert(e, w1, w3, w2)
+        if e in global_resident:
+            experts[e] = (w1, w3, w2)
     layer.begin_load([], loads)
     layer.poll_loads(blocking=True)
+    # route_token's fallback scores = the invocation's aggregate (engine.cpp:424, :529-531)
+    layer.set_scores(agg[0])
     load_bytes, load_ms = layer.last_load_stats()
     torch.cuda.synchronize()
 
     # ---- activations whose gate logits reproduce the serving trace
     choices = serve.reshape(T, k)  # [P][1][Tp][k] -> token-major
-    lg = torch.rand(T, E, generator=g, device=device) * 8.0 - 4.0
-    lg = torch.round(lg * 64) / 64
-    ch = torch.from_numpy(np.ascontiguousarray(choices)).to(device).long()
-    for r in range(k):
-        lg.scatter_(1, ch[:, r:r + 1], 8.0 - r)
-    z = torch.randn(T, d, generator=g, device=device)
-    z = z - (z @ wg.T) @ wg
-    x = (lg @ wg + z).to(td).contiguous()
-    del z, lg
+    x_host = input_x(cfg, wg64, choices, T)
+    x = x_host.to(device)
     res = [0] * E
     for e in global_resident:
         res[e] = 1
     info = dict(trace=trace, loads=loads, aggregate=agg[0].tolist(), load_bytes=load_bytes, load_ms=load_ms,
-                choices=choices, resident=res, global_resident=global_resident)
+                choices=choices, resident=res, global_resident=global_resident, x_host=x_host,
+                wg=wg64.to(td), experts=experts)
     return layer, pred, x, info
 
 
@@ -225,9 +287,10 @@ def cpu_reference_step(cfg, layer_info, x_host_f32, wg_f32, experts_f32, n_token
     x = x_host_f32[:n_tokens]
     t0 = time.perf_counter()
     logits = port.gate_logits(x, wg_f32)
-    o = port.gate_route(logits, k, 0 if cfg["wm"] == "topk_softmax" else 1, resident)
+    o = port.gate_route(logits, k, 0 if cfg["wm"] == "topk_softmax" else 1, resident,
+                        scores=layer_info.get("aggregate"))
     if ref is not None:
-        ref.route_tokens(o["topk_idx"], resident)
+        ref.route_tokens(o["topk_idx"], resident, scores=layer_info.get("aggregate"))
     counts, offsets, pos, src = port.permute(o["served_idx"], E, 1)
     Y = np.zeros((int(offsets[-1]), cfg["d"]), np.float32)
     for e in range(E):
@@ -241,55 +304,42 @@ def cpu_reference_step(cfg, layer_info, x_host_f32, wg_f32, experts_f32, n_token
     return time.perf_counter() - t0
 
 
-def cpu_setup(cfg, layer, x, n_tokens):
-    """Host copies (fp32) of the first n_tokens of x and of the resident experts' weights."""
-    from oracle.oracle import Port, Ref, have_ref
-
-    port = Port()
-    ref = Ref() if have_ref() else None
-    xs = x[:n_tokens].float().cpu().numpy()
-    return port, ref, xs
+def f32_inputs(x_rows, wg, experts):
+    """float32 numpy copies for the oracle port."""
+    to = lambda t: None if t is None else t.float().numpy()  # noqa: E731
+    return to(x_rows), to(wg), {e: tuple(to(w) for w in ws) for e, ws in experts.items()}
 
 
-def run_cpu_baseline(cfg, layer, x, info, target_s=10.0):
-    import torch
+CPU_PATH_NOTE = ("oracle port = the repo's CPU restatement (C, scalar loops with fp64 accumulation, pthreads): "
+                 "a correctness oracle timed with a stopwatch, not a tuned CPU kernel; route_token is the "
+                 "reference's own code (oracle/_ref)")
 
+
+def run_cpu_baseline(cfg, x_rows, wg, experts, info, target_s=10.0):
+    """cpu_baseline of the GPU arm: the bounded CPU path on the first rows of
+    the same x, with the same weights and resident set."""
     from oracle.oracle import Port, Ref, have_ref
 
     port = Port()
     ref = Ref() if have_ref() else None
     threads = port.threads()
-    E = cfg["E"]
-    wg = layer_gate_f32(layer)
-    experts = layer_experts_f32(layer)
-    # calibrate the sample so the timed CPU work is ~target_s
-    n = 8
-    xs = x[:4096].float().cpu().numpy()
-    dt = cpu_reference_step(cfg, info, xs, wg, experts, n, port, ref, threads)
-    n = int(max(8, min(4096, n * target_s / max(dt, 1e-3))))
-    dt = cpu_reference_step(cfg, info, xs, wg, experts, n, port, ref, threads)
+    T = x_rows.shape[0]
+    xs, wgf, ex = f32_inputs(x_rows[: min(X_CHUNK, T)], wg, experts)
+    # calibrate the sample so the timed CPU work is ~target_s (never more rows than the batch has)
+    n = min(8, T)
+    dt = cpu_reference_step(cfg, info, xs, wgf, ex, n, port, ref, threads)
+    n = int(max(min(8, T), min(X_CHUNK, T, n * target_s / max(dt, 1e-3))))
+    dt = cpu_reference_step(cfg, info, xs, wgf, ex, n, port, ref, threads)
     rt_ns = None
     if ref is not None:
-        choices = info["choices"]
-        res = np.zeros(E, np.uint8)
+        res = np.zeros(cfg["E"], np.uint8)
         res[np.asarray(info["resident"], bool)] = 1
-        rt_ns, _ = ref.time_route_tokens(choices, res, reps=3)
+        rt_ns, _ = ref.time_route_tokens(info["choices"], res, reps=3)
     return dict(value=n / dt, unit="tokens/s", cores=threads, kind="port",
-                sample=f"{n} of {x.shape[0]} tokens through the full CPU path: oracle port (C, {threads} pthreads) "
-                       f"gate+top-k, permute, SwiGLU/ReLU FFN (fp64 accumulate), combine; reference route_token "
-                       f"(oracle/_ref, 1 thread) {'%.2f ns/token' % rt_ns if rt_ns else 'n/a'}",
-                seconds=dt)
-
-
-_HOST_CACHE = {}
-
-
-def layer_gate_f32(layer):
-    return _HOST_CACHE["wg"]
-
-
-def layer_experts_f32(layer):
-    return _HOST_CACHE["experts"]
+                sample=f"{n} of {T} tokens through the full CPU path: gate+top-k, permute, SwiGLU/ReLU FFN, "
+                       f"combine ({threads} pthreads); reference route_token "
+                       f"{'%.2f ns/token' % rt_ns if rt_ns else 'n/a'}; {CPU_PATH_NOTE}",
+                seconds=dt, input_digest=input_digest(x_rows[:DIGEST_ROWS], wg, experts))
 
 
 # ---------------------------------------------------------------------------
@@ -577,9 +627,7 @@ def main():
                                 h2d_gbs=round(info["load_bytes"] / max(info["load_ms"], 1e-9) / 1e6, 2),
                                 experts=info["loads"]))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        _HOST_CACHE["wg"] = gate_f32(layer_gate_tensor(cfg, device))
-        _HOST_CACHE["experts"] = experts_f32(cfg, device, info)
-        out["cpu_baseline"] = run_cpu_baseline(cfg, layer, x, info)
+        out["cpu_baseline"] = run_cpu_baseline(cfg, info["x_host"], info["wg"], info["experts"], info)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -654,38 +702,6 @@ def layer_ws_topk(layer):
     return w.topk_idx
 
 
-def layer_gate_tensor(cfg, device):
-    import torch
-
-    g = torch.Generator(device=device).manual_seed(1234)
-    q, _ = torch.linalg.qr(torch.randn(cfg["d"], cfg["E"], generator=g, device=device))
-    return q.T.contiguous().to(torch_dtype(cfg))
-
-
-def gate_f32(wg):
-    return wg.float().cpu().numpy()
-
-
-def experts_f32(cfg, device, info):
-    """Regenerate the resident experts' weights with the bench's generator stream."""
-    import torch
-
-    d, f, E = cfg["d"], cfg["f"], cfg["E"]
-    g = torch.Generator(device=device).manual_seed(1234)
-    torch.linalg.qr(torch.randn(d, E, generator=g, device=device))
-    out = {}
-    td = torch_dtype(cfg)
-    for e in range(E):
-        w1 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(td)
-        w3 = (torch.randn(f, d, generator=g, device=device) / d ** 0.5).to(td) \
-            if cfg["act"] == "swiglu" else None
-        w2 = (torch.randn(d, f, generator=g, device=device) / f ** 0.5).to(td)
-        if info["resident"][e]:
-            out[e] = (w1.float().cpu().numpy(), None if w3 is None else w3.float().cpu().numpy(),
-                      w2.float().cpu().numpy())
-    return out
-
-
 def main_stream(args):
     """BASELINE config 5: a mixed-task stream of 8k-token prompts ("conv" sensitive on
     every layer, "cls" on none, mix 0.5/0.5) through a 32-layer Mixtral-shaped stack
@@ -725,8 +741,9 @@ def main_stream(args):
               group=dist.group.WORLD if dist.is_initialized() and dist.get_world_size() > 1 else None)
     # initial placement: the first plan from an empty device (blocking, untimed)
     _, sets = moesim_prompt_sets(trace_dev, P_train - 1)
-    ops, _, _ = stack.invocation(sets, [(prompt_tasks[q], T) for q in range(P_train, P_train + p)])
+    ops, agg, _ = stack.invocation(sets, [(prompt_tasks[q], T) for q in range(P_train, P_train + p)])
     stack.apply(ops)
+    stack.set_scores(agg)
     for layer in stack.layers:
         layer.poll_loads(blocking=True)
     torch.cuda.synchronize()
@@ -810,8 +827,9 @@ def main_stack(args):
     stack.fit(trace_dev[:P_train].contiguous(), ["conv"] * P_train,
               group=dist.group.WORLD if dist.is_initialized() and dist.get_world_size() > 1 else None)
     _, sets = moesim_prompt_sets(trace_dev, P_train - 1)
-    ops, _, _ = stack.invocation(sets, [("conv", Tp)] * P)
+    ops, agg, _ = stack.invocation(sets, [("conv", Tp)] * P)
     stack.apply(ops)
+    stack.set_scores(agg)
     for layer in stack.layers:
         layer.poll_loads(blocking=True)
     torch.cuda.synchronize()
@@ -916,66 +934,70 @@ def main_stack(args):
 
 def main_reference(args, cfg, rank, world):
     """--impl reference: the reference's CPU implementation of the path on this
-    host's cores (oracle/_ref route_token + the oracle port of the parts the
-    reference does not have), on bounded samples of the same workload."""
+    host's cores, on bounded samples of the same workload.  It never imports
+    the product package: the routing trace comes from the reference's own
+    generator (oracle/_ref, workload.cpp:242-286), the resident set from the
+    reference's fit / prompt_expert_sets / predict / predicted_frequencies /
+    loading_targets (oracle/_ref) with the engine's invocation aggregate
+    (engine.cpp:367-417, oracle port), the inputs from the same CPU generator
+    as the GPU arm (input_gate / input_expert / input_x: same seeds, same
+    bits; input_digest proves it), route_token from oracle/_ref and gate /
+    permute / FFN / combine from the oracle port."""
     if rank != 0:
         return
     import torch
 
     from oracle.oracle import Port, Ref, have_ref
 
-    import paper_2503_06823_b200 as emoe
-
-    port = Port()
-    ref = Ref() if have_ref() else None
+    if not have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (the reference build) is missing"}))
+        return
+    port, ref = Port(), Ref()
     threads = port.threads()
-    E, k, d, f = cfg["E"], cfg["k"], cfg["d"], cfg["f"]
-    # same synthetic inputs as the GPU arm, regenerated on the CPU (no GPU needed)
-    shape = emoe.ModelShape(1, E, k)
-    trace = emoe.gen_routing_trace(shape, cfg["layer_lambda"], cfg["prompt_lambda"], 0, cfg["seed"],
-                                   cfg["train"] + cfg["prompts"], cfg["tokens"])
-    train = trace[: cfg["train"]]
-    model = port.fit(train, np.zeros(cfg["train"], np.int32), 1, E)
-    model["smoothing"] = 0.01
-    sets, sizes = port.prompt_expert_sets(train, cfg["train"] - 1)
-    scores, _, _ = port.predict(model, 0, sets, sizes, k=k)
-    fitted = port.predicted_frequencies(model["task_counts"], 0.01, 0)[None]
+    E, k, d, f, L = cfg["E"], cfg["k"], cfg["d"], cfg["f"], cfg["L"]
+    P, Tp, P_train = cfg["prompts"], cfg["tokens"], cfg["train"]
+    T = P * Tp
+    trace = ref.gen_routing_trace(1, E, k, cfg["layer_lambda"], cfg["prompt_lambda"], 0, cfg["seed"],
+                                  P_train + P, Tp)
+    train = trace[:P_train]
+    model = ref.fit(train, np.zeros(P_train, np.int32), ["t0"], 0.01, E)
+    _, sets, sizes = ref.prompt_expert_sets(train, P_train - 1)
+    scores, _, _ = ref.predict(model, 0, sets, sizes, k=k)
+    fitted = ref.predicted_frequencies(model["task_counts"], ["t0"], 0.01, "t0")[None]
     agg = port.invocation_aggregate(scores, fitted, [128.0], np.ones((1, 1), np.int32), [1],
-                                    np.zeros(cfg["prompts"], np.int32), np.full(cfg["prompts"], cfg["tokens"]))
-    targets = port.loading_targets(agg, np.zeros((1, E), np.uint8), [cfg["L"]])[0]
+                                    np.zeros(P, np.int32), np.full(P, Tp))
+    targets = ref.loading_targets(agg, np.zeros((1, E), np.uint8), [L])[0]
     resident = [1 if e in targets else 0 for e in range(E)]
-    info = dict(resident=resident, choices=trace[cfg["train"]:].reshape(-1, k))
-    g = torch.Generator().manual_seed(4321)
-    n = 16
-    td = torch_dtype(cfg)
-    x = (torch.randn(4096, d, generator=g)).to(td).float().numpy()
-    wg = (torch.randn(E, d, generator=g) / d ** 0.5).to(td).float().numpy()
-    experts = {}
-    for e in range(E):
-        if resident[e]:
-            w1 = (torch.randn(f, d, generator=g) / d ** 0.5).to(td).float().numpy()
-            w3 = (torch.randn(f, d, generator=g) / d ** 0.5).to(td).float().numpy() \
-                if cfg["act"] == "swiglu" else None
-            w2 = (torch.randn(d, f, generator=g) / f ** 0.5).to(td).float().numpy()
-            experts[e] = (w1, w3, w2)
+    choices = trace[P_train:].reshape(-1, k)
+    info = dict(resident=resident, choices=choices, aggregate=agg[0].tolist())
+    wg64 = input_gate(cfg)
+    wg = wg64.to(torch_dtype(cfg))
+    experts = {e: input_expert(cfg, e) for e in range(E) if resident[e]}
+    rows = min(X_CHUNK, T)
+    x_rows = input_x(cfg, wg64, choices, rows)
+    digest = input_digest(x_rows[:DIGEST_ROWS], wg, experts)
+    xs, wgf, ex = f32_inputs(x_rows, wg, experts)
     # size the per-step sample so W+K steps finish within a few minutes
-    dt = cpu_reference_step(cfg, info, x, wg, experts, n, port, ref, threads)
+    n = min(16, rows)
+    dt = cpu_reference_step(cfg, info, xs, wgf, ex, n, port, ref, threads)
     budget_s = args.ref_budget_s / (args.steps + args.warmup)
-    n = int(max(4, min(4096, n * budget_s / max(dt, 1e-3))))
+    n = int(max(min(4, rows), min(rows, n * budget_s / max(dt, 1e-3))))
     for _ in range(args.warmup):
-        cpu_reference_step(cfg, info, x, wg, experts, n, port, ref, threads)
+        cpu_reference_step(cfg, info, xs, wgf, ex, n, port, ref, threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        cpu_reference_step(cfg, info, x, wg, experts, n, port, ref, threads)
+        cpu_reference_step(cfg, info, xs, wgf, ex, n, port, ref, threads)
     s = (time.perf_counter() - t0) / args.steps
     value = n / s
+    sample = (f"the first {n} of the {P}x{Tp} = {T} tokens per step (same x rows, weights and resident set as "
+              f"the GPU arm; input_digest {digest}): {CPU_PATH_NOTE}; {threads} host threads")
     out = dict(metric=METRIC, impl="reference", value=round(value, 3), unit="tokens/s", n_gpus=world,
                steps=args.steps, warmup=args.warmup, ms_per_step=round(s * 1e3, 3), higher_is_better=True,
                scaling="weak", vs_baseline=None, dtype="fp32 (fp64 accumulate)", data="synthetic",
-               config=dict(workload=cfg["workload"], tokens_per_step=n, parallelism="cpu"),
-               cpu_baseline=dict(value=round(value, 3), unit="tokens/s", cores=threads, kind="port",
-                                 sample=f"{n} tokens per step of the {cfg['prompts']}x{cfg['tokens']} batch: "
-                                        "reference route_token (oracle/_ref) + oracle port gate/permute/FFN/combine"),
+               config=dict(workload=cfg["workload"], tokens_per_step=n, parallelism="cpu",
+                           resident_set=[e for e in range(E) if resident[e]], input_digest=digest,
+                           same_config=True),
+               cpu_baseline=dict(value=round(value, 3), unit="tokens/s", cores=threads, kind="port", sample=sample),
                e2e=dict(value=round(value, 3), unit="tokens/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(out), flush=True)
 

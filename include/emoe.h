@@ -102,7 +102,14 @@ int emoe_layer_register_expert_pinned(emoe_layer* layer, int expert, const void*
 int emoe_layer_set_copy_stream(emoe_layer* layer, void* stream);
 
 /* Layer scores used by the route_token fallback (the engine's last aggregate
- * row, engine.cpp:529-531).  scores == NULL sets the empty score vector. */
+ * row, set when an invocation completes: engine.cpp:424, :529-531).
+ * scores == NULL sets the empty score vector.  Stream-ordered: the [E]
+ * scores travel as the arguments of a kernel enqueued on `stream`, so
+ * forwards enqueued earlier on `stream` still route with the old scores and
+ * later ones with the new (no host staging buffer, no device-wide sync). */
+int emoe_layer_set_scores(emoe_layer* layer, const double* scores, void* stream);
+/* Same, then synchronises the legacy default stream (kept for callers of the
+ * blocking form). */
 int emoe_layer_set_scores_host(emoe_layer* layer, const double* scores);
 
 /* ========================================================================

@@ -902,11 +902,7 @@ static void launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
                        const gemm::Params& p, int num_sms, cudaStream_t stream) {
   using C = gemm::Cfg<CG, EW>;
   auto kernel = gemm::grouped_gemm_kernel<EPI, CG, EW>;
-  static bool attr_set = false;  // one per instantiation
-  if (!attr_set) {
-    EMOE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
-    attr_set = true;
-  }
+  ensure_max_dynamic_smem(reinterpret_cast<const void*>(kernel), C::SMEM_BYTES);
   const int grid = CG == 2 ? (num_sms / 2) * 2 : num_sms;
   if (CG == 1) {
     kernel<<<grid, C::NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, tb2, to, p);

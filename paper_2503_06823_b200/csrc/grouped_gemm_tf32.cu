@@ -423,15 +423,11 @@ bool gemm_tf32x3_supported(int epi, int K, int N_out) {
 
 int gemm_tf32x3_b_box_rows(int epi) { return epi == EPI_SWIGLU ? tf32x3::BN / 2 : tf32x3::BN; }
 
-// one function (and one "attribute set" flag) per kernel instantiation
+// one function per kernel instantiation
 template <int EPI>
 static void launch_kernel(const Tf32Operands& ops, const tf32x3::Params& p, int num_sms, cudaStream_t stream) {
   using namespace tf32x3;
-  static bool attr = false;
-  if (!attr) {
-    EMOE_CUDA(cudaFuncSetAttribute(gemm_tf32x3_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr = true;
-  }
+  ensure_max_dynamic_smem(reinterpret_cast<const void*>(gemm_tf32x3_kernel<EPI>), SMEM_BYTES);
   gemm_tf32x3_kernel<EPI><<<num_sms, NUM_THREADS, SMEM_BYTES, stream>>>(ops.a_hi, ops.a_lo, ops.b_hi, ops.b_lo,
                                                                        ops.b2_hi, ops.b2_lo, p);
   EMOE_CUDA(cudaGetLastError());

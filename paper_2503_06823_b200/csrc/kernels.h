@@ -12,6 +12,9 @@ namespace emoe {
 // number of kernels this library launched (reported by bench.py as gpu_launches)
 void count_launch(int n = 1);
 long long launch_count();
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device: set it once per
+// (device, kernel) before a launch needing more than 48 KB (thread-safe)
+void ensure_max_dynamic_smem(const void* func, int bytes);
 
 enum EpiKind { EPI_SWIGLU = 0, EPI_RELU = 1, EPI_STORE = 2, EPI_F32 = 3 };
 enum DType { DT_BF16 = 0, DT_F32 = 1 };

@@ -6,6 +6,8 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "capi_util.h"
@@ -21,6 +23,18 @@ std::string& last_error_slot() {
 static std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+void ensure_max_dynamic_smem(const void* func, int bytes) {
+  int dev = 0;
+  EMOE_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{dev, func}];
+  if (have >= bytes) return;
+  EMOE_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
+}
 
 namespace {
 
@@ -39,6 +53,14 @@ __global__ void set_tables_kernel(TableUpdate u, uint8_t* resident, int32_t* slo
     resident[e] = u.resident[e];
     slot[e] = u.slot[e];
   }
+}
+
+struct ScoresUpdate {
+  int E;
+  double v[kMaxTableE];
+};
+__global__ void set_scores_kernel(ScoresUpdate u, double* scores) {
+  for (int e = threadIdx.x; e < u.E; e += blockDim.x) scores[e] = u.v[e];
 }
 
 // engine.cpp:473-478 demand map: tokens per rank-0 gate choice (integer
@@ -855,16 +877,27 @@ int emoe_layer_set_copy_stream(emoe_layer* L, void* stream) {
   });
 }
 
-int emoe_layer_set_scores_host(emoe_layer* L, const double* scores) {
+int emoe_layer_set_scores(emoe_layer* L, const double* scores, void* stream) {
   return guard([&] {
     EMOE_REQUIRE(L, "set_scores: null layer");
-    if (!scores) {
+    if (!scores) {  // later route launches pass a null score pointer
       L->have_scores = false;
       return;
     }
-    EMOE_CUDA(cudaMemcpy(L->scores_dev, scores, sizeof(double) * L->cfg.num_experts, cudaMemcpyHostToDevice));
+    ScoresUpdate u;
+    u.E = L->cfg.num_experts;
+    for (int e = 0; e < u.E; ++e) u.v[e] = scores[e];
+    set_scores_kernel<<<1, 128, 0, static_cast<cudaStream_t>(stream)>>>(u, L->scores_dev);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
     L->have_scores = true;
   });
+}
+
+int emoe_layer_set_scores_host(emoe_layer* L, const double* scores) {
+  const int rc = emoe_layer_set_scores(L, scores, nullptr);
+  if (rc != 0) return rc;
+  return guard([&] { EMOE_CUDA(cudaStreamSynchronize(nullptr)); });
 }
 
 int emoe_layer_begin_load(emoe_layer* L, const int32_t* evictions, int n_ev, const int32_t* loads, int n_ld,

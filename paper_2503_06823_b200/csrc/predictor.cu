@@ -653,7 +653,7 @@ int emoe_hist_update(emoe_predictor* P, const int32_t* trace, int nP, int T, con
     const int E = P->E;
     const size_t smem = (size_t)(2 * E + (P->m > 1 ? E * E : 0)) * sizeof(int);
     EMOE_REQUIRE(smem <= 200 * 1024, "hist_update: E too large for the shared-memory histogram");
-    EMOE_CUDA(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(hist_kernel), (int)smem);
     hist_kernel<<<nP * P->m, 256, smem, s>>>(trace, nP, P->m, T, P->k, E, task_ids, P->layer_counts, P->task_counts,
                                              P->dom);
     EMOE_CUDA(cudaGetLastError());

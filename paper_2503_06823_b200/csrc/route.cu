@@ -547,7 +547,7 @@ void launch_gate_route(const void* x, const void* wg, int dtype, const RouteArgs
       size_t smem = (size_t)2 * RT * 128 + (size_t)2 * EP * 128;
       const size_t lsm = (size_t)RT * (EP + 1) * sizeof(float);
       if (lsm > smem) smem = lsm;
-      EMOE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ensure_max_dynamic_smem(reinterpret_cast<const void*>(kernel), (int)smem);
       kernel<<<nblocks, 128, smem, s>>>(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg),
                                         a, o);
     };
@@ -571,13 +571,8 @@ void launch_route_from_logits(const float* logits, const RouteArgs& a, const Rou
   EMOE_REQUIRE(a.k >= 1 && a.k <= 8 && a.k <= a.E, "route: top_k must be in [1, min(8, E)]");
   const int nblocks = (int)ceil_div(a.T, RT);
   if (nblocks == 0) return;
-  static bool attr = false;
-  if (!attr) {
-    EMOE_CUDA(cudaFuncSetAttribute(route_from_logits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   RT * (MAX_E + 1) * (int)sizeof(float)));
-    attr = true;
-  }
   const int smem = a.E >= 32 ? RT * (a.E + 1) * (int)sizeof(float) : 0;
+  if (smem > 48 * 1024) ensure_max_dynamic_smem(reinterpret_cast<const void*>(route_from_logits_kernel), smem);
   route_from_logits_kernel<<<nblocks, RT, smem, s>>>(logits, a, o);
   EMOE_CUDA(cudaGetLastError());
   count_launch();

@@ -3,7 +3,8 @@
 // benchmark can build the same inputs without the reference.  The stream is
 // std::mt19937_64 with the reference's hand-written transforms
 // (distributions.hpp:12-34), so a seed gives the reference's trace bit for bit
-// (checked in tests/test_workload_trace.py).
+// (checked against the reference-generated golden traces in
+// tests/test_oracle.py::test_product_trace_generator_matches_golden).
 #include <cstdint>
 #include <random>
 #include <vector>

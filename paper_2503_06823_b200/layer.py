@@ -99,12 +99,16 @@ class MoELayer:
         self._copy_stream = stream
         check(lib.emoe_layer_set_copy_stream(self.h, None if stream is None else C.c_void_p(stream.cuda_stream)))
 
-    def set_scores(self, scores: Optional[Sequence[float]]) -> None:
+    def set_scores(self, scores: Optional[Sequence[float]], stream=None) -> None:
+        """route_token fallback scores (the engine's last aggregate row of this
+        layer, engine.cpp:424, :529-531); None = the empty score vector.
+        Ordered on `stream` (default: the current stream) like a forward."""
         if scores is None or len(scores) == 0:
-            check(lib.emoe_layer_set_scores_host(self.h, None))
+            check(lib.emoe_layer_set_scores(self.h, None, _stream_ptr(stream)))
             return
         s = np.ascontiguousarray(np.asarray(scores, np.float64))
-        check(lib.emoe_layer_set_scores_host(self.h, s.ctypes.data_as(C.c_void_p)))
+        assert s.shape == (self.E,), f"scores must have {self.E} entries"
+        check(lib.emoe_layer_set_scores(self.h, s.ctypes.data_as(C.c_void_p), _stream_ptr(stream)))
 
     # -- residency (two-phase, engine.cpp:431-464) ------------------------
     def begin_load(self, evictions: Sequence[int], loads: Sequence[int], stream=None) -> None:
@@ -153,21 +157,38 @@ class MoELayer:
 
     __call__ = forward
 
+    def _check_host_pair(self, x_host: torch.Tensor, y_host: torch.Tensor) -> None:
+        for name, t in (("x_host", x_host), ("y_host", y_host)):
+            assert t.device.type == "cpu" and t.dtype == self.torch_dtype and t.is_contiguous(), \
+                f"{name} must be a contiguous CPU {self.torch_dtype} tensor"
+        assert x_host.dim() == 2 and x_host.shape[1] == self.d, f"x_host must be [T, {self.d}]"
+        assert tuple(y_host.shape) == tuple(x_host.shape), "y_host must have x_host's shape"
+
     def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor, stream=None) -> torch.Tensor:
         """End-to-end through host buffers: H2D of x, forward, D2H of y."""
-        assert x_host.device.type == "cpu" and x_host.dtype == self.torch_dtype and x_host.is_contiguous()
+        self._check_host_pair(x_host, y_host)
         check(lib.emoe_moe_forward_host(self.h, C.c_void_p(x_host.data_ptr()), C.c_void_p(y_host.data_ptr()),
                                         x_host.shape[0], _stream_ptr(stream)))
         return y_host
 
     def forward_host_async(self, x_host: torch.Tensor, y_host: torch.Tensor, stream=None) -> None:
-        """Enqueue H2D + forward + D2H and return; call wait_host() before reading y_host."""
-        assert x_host.device.type == "cpu" and x_host.dtype == self.torch_dtype and x_host.is_contiguous()
+        """Enqueue H2D + forward + D2H and return; call wait_host() before reading y_host.
+        The queued copies hold raw pointers the torch allocator does not
+        track, so every host pair is referenced here until wait_host()
+        (deduplicated by address: a caller cycling through a few buffers adds
+        nothing; more than 16 distinct pairs in flight waits first)."""
+        self._check_host_pair(x_host, y_host)
+        refs = self.__dict__.setdefault("_async_refs", {})
+        key = (x_host.data_ptr(), y_host.data_ptr())
+        if key not in refs and len(refs) >= 16:
+            self.wait_host()
         check(lib.emoe_moe_forward_host_async(self.h, C.c_void_p(x_host.data_ptr()), C.c_void_p(y_host.data_ptr()),
                                               x_host.shape[0], _stream_ptr(stream)))
+        refs[key] = (x_host, y_host)
 
     def wait_host(self) -> None:
         check(lib.emoe_layer_wait_host(self.h))
+        self.__dict__.get("_async_refs", {}).clear()
 
     def route(self, x: Optional[torch.Tensor] = None, logits: Optional[torch.Tensor] = None, stream=None) -> None:
         T = x.shape[0] if x is not None else logits.shape[0]

@@ -128,6 +128,13 @@ class MoEStack:
         ops = [([int(e) for e in ev[l, : ne[l]]], [int(e) for e in ld[l, : nl[l]]]) for l in range(m)]
         return ops, agg, float(de[0])
 
+    def set_scores(self, aggregate, stream=None) -> None:
+        """The engine keeps the invocation's aggregate as every layer's route_token
+        fallback scores (last_aggregate_, engine.cpp:424, :529-531); applied
+        stream-ordered, so forwards already enqueued keep the previous scores."""
+        for l, layer in enumerate(self.layers):
+            layer.set_scores(np.asarray(aggregate[l], np.float64), stream)
+
     def apply(self, ops, stream=None) -> int:
         """Start the plan: per layer, evictions now, loads on the shared copy stream."""
         n = 0
@@ -185,12 +192,17 @@ def run_stream(stack: MoEStack, trace: np.ndarray, trace_dev: torch.Tensor, prom
             window = list(range(p, min(p + cfg.period, first_prompt + n_prompts)))
             requests = [(prompt_tasks[q], T) for q in window]
             if cfg.task_aware and not any(sensitive[t] for t, _ in requests):
+                # the reference would run the invocation and get an all-zero
+                # aggregate (Eq. 2 is 0 on insensitive layers): residents kept
+                # (loading_targets), and the fallback scores become zeros
+                stack.set_scores(np.zeros((cfg.m, cfg.E)))
                 stats["skipped_invocations"] += 1
                 stats["skipped_at"].append(i)
             else:
                 t0 = time.perf_counter()
                 _, prev_sets = moesim_prompt_sets(trace_dev, p - 1)
-                ops, _, _ = stack.invocation(prev_sets, requests)
+                ops, agg, _ = stack.invocation(prev_sets, requests)
+                stack.set_scores(agg)
                 ls, le = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 ls.record(stack.copy_stream)
                 stats["planned_loads"] += stack.apply(ops)

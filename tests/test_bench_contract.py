@@ -35,6 +35,34 @@ def test_reference_arm_contract():
     assert cb["value"] == d["value"] and cb["cores"] >= 1
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["config"]["tokens_per_step"] <= 512 and "of the 1x512 = 512 tokens" in cb["sample"]
+
+
+def test_reference_arm_is_independent_of_the_product():
+    """--impl reference runs the reference's code and the oracle only: the
+    product package is never imported and libemoe.so never mapped."""
+    from oracle.oracle import have_port, have_ref
+
+    if not (have_port() and have_ref()):
+        pytest.skip("oracle not built")
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--config', 'synthetic', "
+            "'--steps', '1', '--warmup', '3', '--ref-budget-s', '2']; runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "print('PRODUCT', any(m.startswith('paper_2503_06823_b200') for m in sys.modules), 'libemoe.so' in maps)")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "PRODUCT False False" in out.stdout, out.stdout[-2000:]
+
+
+@pytest.mark.gpu
+def test_both_arms_same_inputs():
+    """The reference arm and the GPU arm's cpu_baseline hash the same input
+    bytes (x rows, W_g, resident experts) and agree on the resident set."""
+    ref = run_bench("--impl", "reference", "--config", "synthetic", "--steps", "1", "--warmup", "3",
+                    "--ref-budget-s", "4")
+    gpu = run_bench("--config", "synthetic", "--steps", "3", "--warmup", "3", "--e2e-steps", "2")
+    assert ref["config"]["input_digest"] == gpu["cpu_baseline"]["input_digest"]
+    assert ref["config"]["resident_set"] == gpu["config"]["resident_set"]
 
 
 @pytest.mark.gpu
@@ -51,4 +79,5 @@ def test_gpu_arm_contract(graph):
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
     cb = d["cpu_baseline"]
     assert cb["value"] > 0 and cb["cores"] >= 1 and cb["kind"] in ("port", "reference")
+    assert " of 512 tokens" in cb["sample"]  # the sample never exceeds the batch
     assert d["config"]["step_launch"].startswith("one CUDA graph" if graph == "on" else "eager")

@@ -59,6 +59,20 @@ def test_stream_invocations_and_residency_match_oracle(port, ref):
     got = np.stack([layer.residency() for layer in stack.layers])
     assert np.array_equal(got, resident)
     assert st["planned_loads"] > 0 and 0.0 < st["hit_rate"] <= 1.0
+    # route_token's fallback (no gate choice resident) takes the resident expert
+    # with the highest score of the last invocation's aggregate
+    # (engine.cpp:424, :529-532): every layer's routing of the last prompt
+    # against the reference route_token with those scores, fallback tokens included
+    q = P_train + P_serve - 1
+    n_fallback = 0
+    for l, layer in enumerate(stack.layers):
+        layer.forward(x, logits=logits[q][l])
+        ws = layer.workspace()
+        ex, rk, hit = ref.route_tokens(trace[q, l], resident[l], scores=agg[l])
+        assert np.array_equal(ws["route_expert"].cpu().numpy(), ex), f"layer {l}: route_token expert"
+        assert np.array_equal(ws["route_rank"].cpu().numpy(), rk), f"layer {l}: route_token rank"
+        n_fallback += int((rk == -1).sum())
+    assert n_fallback > 0, "no fallback token in the check"
     stack.close()
 
 
