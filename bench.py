@@ -200,7 +200,7 @@ def build_workload(cfg, device, cta_group=0, rank=0, world=1, parallel="replicas
 
     import paper_2503_06823_b200 as emoe
     from paper_2503_06823_b200 import MoELayer
-    from paper_2503_06823_b200.ep import owned_experts, plan_destinations
+    from paper_2503_06823_b200.ep import owned_experts, plan_shares
 
     E, k, L, d, f = cfg["E"], cfg["k"], cfg["L"], cfg["d"], cfg["f"]
     P, Tp, P_train = cfg["prompts"], cfg["tokens"], cfg["train"]
@@ -243,7 +243,7 @@ def build_workload(cfg, device, cta_group=0, rank=0, world=1, parallel="replicas
     if parallel == "ep" and world > 1:  # this GPU holds only the experts it serves
         # load-aware placement from the Eq. 2 aggregate (identical on every
         # rank: same fitted predictor, same request mix)
-        loads = owned_experts(plan_destinations(global_resident, E, world, agg[0]), rank)
+        loads = owned_experts(plan_shares(global_resident, E, world, agg[0]), rank)
 
     # ---- inputs (CPU generator shared with --impl reference), layer, planned loads
     wg64 = input_gate(cfg)
@@ -343,7 +343,15 @@ def run_cpu_baseline(cfg, x_rows, wg, experts, info, target_s=10.0):
 
 
 # ---------------------------------------------------------------------------
-def main():
+def parallelism_label(world, parallel, transport):
+    """config.parallelism: "single" at N=1; under torchrun "ep{N}-{transport}"
+    (the default) or "replicas{N}"."""
+    if world <= 1:
+        return "single"
+    return f"ep{world}-{transport}" if parallel == "ep" else f"replicas{world}"
+
+
+def build_parser():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -371,12 +379,20 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = every GPU serves the config's full batch (default); strong = the "
                          "config's batch is split over the GPUs (N must divide its 32 prompts)")
-    ap.add_argument("--parallel", default="replicas", choices=["replicas", "ep"],
-                    help="N>1: replicas of the predicted resident set (no exchange) or expert parallelism")
+    ap.add_argument("--parallel", default="ep", choices=["replicas", "ep"],
+                    help="N>1: expert parallelism (default; the north star's split: each GPU computes its share "
+                         "of the resident experts' rows, tokens exchanged over NVLink) or replicas of the "
+                         "predicted resident set (no exchange)")
+    ap.add_argument("--ep-recv-cap", type=int, default=0,
+                    help="--parallel ep: receive-buffer rows per GPU (0 = the worst case, world x rows_cap)")
     ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"],
                     help="--parallel ep: dispatch/combine fused into the permute/combine kernels over "
                          "IPC-mapped peer memory (p2p), or NCCL all-to-all between the stage kernels")
-    args = ap.parse_args()
+    return ap
+
+
+def main():
+    args = build_parser().parse_args()
     args.warmup = max(args.warmup, 3)
     if args.config == "stream":
         return main_stream(args)
@@ -391,6 +407,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        nccl_log_to_stderr()
         dist.init_process_group("nccl" if args.impl == "emoe" else "gloo")
     if args.impl == "reference":
         return main_reference(args, cfg, rank, world)
@@ -414,10 +431,12 @@ def main():
     import ctypes as C
 
     ep_model = None
+    ep_stats = ep_stages = None
     if use_ep and args.ep_transport == "p2p":
         from paper_2503_06823_b200.ep import PeerExpertParallelMoE
 
-        ep_model = PeerExpertParallelMoE(layer, info["global_resident"], loads=info["aggregate"])
+        ep_model = PeerExpertParallelMoE(layer, info["global_resident"], loads=info["aggregate"],
+                                         recv_rows_cap=args.ep_recv_cap)
     elif use_ep:
         from paper_2503_06823_b200.ep import ExpertParallelMoE, LayerBackend
 
@@ -426,7 +445,7 @@ def main():
 
     def eager_step():
         if ep_model is not None:
-            ep_model(x)
+            ep_model(x, out=y) if args.ep_transport == "p2p" else ep_model(x)
         else:
             layer.forward(x, out=y)
         ws_topk = layer_ws_topk(layer)
@@ -458,6 +477,8 @@ def main():
         launches_per_step = int(_lib.lib.emoe_kernel_launches() - l0)
         graph.replay()  # warm replay
         torch.cuda.synchronize()
+    elif ep_model is not None and args.ep_transport == "p2p":
+        ep_model.set_profiling(True)
     else:
         layer.set_profiling(True)
 
@@ -497,7 +518,13 @@ def main():
                 eager_step()
             torch.cuda.synchronize()
         stages = layer.stage_times()
-    else:  # no per-stage events on the EP path: attribute the whole step to the FFN (a lower bound)
+    elif args.ep_transport == "p2p":  # the EP forward's own stage events
+        ep_stages = ep_model.stage_times()
+        ep_model.set_profiling(False)
+        ep_stats = ep_model.stats()
+        stages = dict(route=ep_stages["route"], permute=ep_stages["dispatch"], gemm1=ep_stages["gemm1"],
+                      gemm2=ep_stages["gemm2_return"], combine=ep_stages["combine"])
+    else:  # NCCL transport: stage boundaries are host-synchronous collectives; the whole step as FFN (a bound)
         stages = dict(route=0.0, permute=0.0, gemm1=ms, gemm2=0.0, combine=0.0)
     layer.set_profiling(False)
     if world > 1:
@@ -551,7 +578,10 @@ def main():
     d, f = cfg["d"], cfg["f"]
     fp32 = cfg.get("dtype", "bf16") == "fp32"
     nmat = 3 if cfg["act"] == "swiglu" else 2
-    ffn_flops = 2.0 * nmat * d * f * S
+    # the FFN rows this GPU computes: its own served rows (single GPU,
+    # replicas) or, under EP, the rows the split assigned it
+    S_ffn = ep_stats["rows_computed_real"] if ep_stats else S
+    ffn_flops = 2.0 * nmat * d * f * S_ffn
     ffn_ms = stages["gemm1"] + stages["gemm2"]
     achieved = ffn_flops / (ffn_ms / 1e3) / 1e12
     traffic = None
@@ -587,7 +617,8 @@ def main():
                         frac=round(achieved / peak, 4), traffic=traffic,
                         traffic_unit="bytes per step (GEMM1 + GEMM2), ncu dram__bytes_read+write",
                         kernel="grouped_gemm_kernel (K4: GEMM1 SwiGLU + GEMM2), avg of the timed steps",
-                        algorithmic=f"2*{nmat}*d*f*S = {ffn_flops:.4g} FLOP per step (S={S} served rows)",
+                        algorithmic=f"2*{nmat}*d*f*S = {ffn_flops:.4g} FLOP per step (S={S_ffn} rows computed "
+                                    f"on this GPU)",
                         peak_kind=(f"bf16_tflops_sustained ({peaks['source']}; timed region >= 150 ms); "
                                    f"burst {peaks['bf16']}") if long_region else
                                   (f"bf16_tflops burst ({peaks['source']}; timed region {args.steps * ms:.0f} ms "
@@ -617,8 +648,7 @@ def main():
                            l2=("inputs larger than L2: x is %.0f MB per step" % (xb / 1e6)) if xb > 126e6 else
                            ("working set larger than L2: %.0f MB of resident expert weights streamed per step "
                             "(x is %.1f MB)" % (cfg["L"] * nmat * d * f * eb / 1e6, xb / 1e6)),
-                           parallelism=(f"ep{world}-{args.ep_transport}" if use_ep else f"replicas{world}")
-                           if world > 1 else "single",
+                           parallelism=parallelism_label(world, args.parallel, args.ep_transport),
                            gemm_cta_group=layer.gemm_cta_group, seg_pad=layer.seg_pad),
                roofline=roofline, e2e=e2e, gpu_launches=launches, clocks=dict(clk.summary(), note=clock_note),
                stages_ms={kk: round(v, 4) for kk, v in stages.items()},
@@ -626,12 +656,48 @@ def main():
                expert_load=dict(bytes=info["load_bytes"], ms=round(info["load_ms"], 3),
                                 h2d_gbs=round(info["load_bytes"] / max(info["load_ms"], 1e-9) / 1e6, 2),
                                 experts=info["loads"]))
+    if ep_stats:
+        out["ep"] = ep_report(ep_model, ep_stages, ep_stats, world, rank, device)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = run_cpu_baseline(cfg, info["x_host"], info["wg"], info["experts"], info)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def nccl_log_to_stderr():
+    """NCCL's communicator lines (transport: NVLink P2P / NVLS) on stderr, so
+    stdout keeps the one JSON line."""
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,P2P,NVLS")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
+
+def ep_report(ep_models, stages, stats, world, rank, device):
+    """The EP step's stage times (rank 0's events; summed over layers for a
+    stack), exchange volume and NVLink rates, and the placement; the busiest
+    rank's FFN rows against the mean (the FFN-bound step waits for it)."""
+    import torch
+    import torch.distributed as dist
+
+    models = ep_models if isinstance(ep_models, (list, tuple)) else [ep_models]
+    t = torch.tensor([float(stats["rows_computed_real"])], device=device)
+    rows = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(rows, t)
+    rows = [float(r.item()) for r in rows]
+    disp_ms, ret_ms = stages["dispatch"], stages["gemm2_return"]
+    return dict(transport="p2p: dispatch fused into the permute (NVLink stores into the computing rank's receive "
+                          "buffer), return fused into GEMM2's epilogue, device-side barriers",
+                stages_ms={k: round(v, 4) for k, v in stages.items()},
+                exchange=dict(dispatch_bytes_to_peers=stats["dispatch_bytes_to_peers"],
+                              return_bytes_to_peers=stats["return_bytes_to_peers"],
+                              dispatch_nvlink_gbs=round(stats["dispatch_bytes_to_peers"] / max(disp_ms, 1e-9) / 1e6, 1),
+                              note="bytes of this rank's rows stored to peers in the dispatch kernel, and of the "
+                                   "expert outputs it pushes back to their sources from GEMM2 (summed over layers "
+                                   "for a stack); GB/s over the dispatch stage"),
+                rows_computed_per_rank=rows, balance_mean_over_max=round(sum(rows) / len(rows) / max(max(rows), 1), 4),
+                placement=[m.owned() for m in models][:4], layers=len(models))
 
 
 def k_of(cfg):
@@ -787,30 +853,42 @@ def main_stream(args):
 
 
 def main_stack(args):
-    """BASELINE config 4 without the exchange: a 32-layer Mixtral-shaped stack
-    (E=8, top-2, 4 predicted-resident experts per layer, bf16), 32 x 2048
-    tokens per GPU per step, layers chained (y of layer l is x of layer l+1)
-    on one shared activation workspace, routing-driven by the reference
-    Markov trace (per-layer gate logits embed it), resident sets from one GPU
-    predictor invocation.  A step = the forward through all layers + the A6
-    histogram update of the batch.  N > 1: replicas (each GPU its own batch,
-    weak scaling); the expert-parallel form is bench.py --parallel ep."""
+    """BASELINE config 4: a 32-layer Mixtral-shaped stack (E=8, top-2, 4
+    predicted-resident experts per layer, bf16), 32 x 2048 tokens per GPU per
+    step, layers chained (y of layer l is x of layer l+1) on one shared
+    activation workspace.  Every layer runs its gate on its input (random
+    N(0, 1/d) gate weights); the reference Markov trace is added to the
+    gate's logits as a bias (EMOE_LOGITS_ADD), so routing follows the trace
+    the predictor was fitted on while the gate's arithmetic is real.
+    Resident sets from one GPU predictor invocation (fit over the ranks'
+    shards, merged by one all-reduce).  A step = the forward through all
+    layers + the A6 histogram update of the batch.
+    N > 1, --parallel ep (default): expert parallelism, every layer its own
+    load-aware placement (plan_shares of its Eq. 2 aggregate), all layers on
+    one symmetric peer-memory region; --parallel replicas: each GPU holds the
+    resident sets.  Weak scaling (every GPU its own 32 x 2048 tokens) unless
+    --scaling strong."""
     import torch
     import torch.distributed as dist
 
     import paper_2503_06823_b200 as emoe
     from paper_2503_06823_b200 import _lib
+    from paper_2503_06823_b200.ep import PeerExpertParallelMoE, owned_experts, plan_shares
     from paper_2503_06823_b200.serving import MoEStack, StreamConfig, TaskSpec, moesim_prompt_sets
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        nccl_log_to_stderr()
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     m, E, k, L, d, f, P, Tp = args.stream_layers, 8, 2, 4, 4096, 14336, 32, 2048
     strong = args.scaling == "strong" and world > 1
+    use_ep = args.parallel == "ep" and world > 1
+    if use_ep and args.ep_transport != "p2p":
+        raise SystemExit("--config stack: expert parallelism runs the p2p transport")
     if strong and P % world:
         raise SystemExit(f"--scaling strong: {world} GPUs do not divide the {P} prompts")
     Pr = P // world if strong else P  # prompts this rank serves
@@ -822,22 +900,34 @@ def main_stack(args):
     g = torch.Generator(device=device).manual_seed(1234)
     host = [tuple((torch.randn(*sh, generator=g, device=device) / sh[1] ** 0.5).to(torch.bfloat16).cpu()
                   .pin_memory() for sh in ((f, d), (f, d), (d, f))) for _ in range(E)]
-    stack = MoEStack(cfg, host, [torch.zeros(E, d, dtype=torch.bfloat16) for _ in range(m)])
+    gates = [(torch.randn(E, d, generator=g, device=device) / d ** 0.5).to(torch.bfloat16).cpu() for _ in range(m)]
+    stack = MoEStack(cfg, host, gates)
+    for layer in stack.layers:
+        layer.set_logits_mode("add")
     trace_dev = torch.from_numpy(trace).to(device)
     stack.fit(trace_dev[:P_train].contiguous(), ["conv"] * P_train,
               group=dist.group.WORLD if dist.is_initialized() and dist.get_world_size() > 1 else None)
     _, sets = moesim_prompt_sets(trace_dev, P_train - 1)
     ops, agg, _ = stack.invocation(sets, [("conv", Tp)] * P)
-    stack.apply(ops)
+    eps = []
+    if use_ep:  # every layer: its resident set spread over the ranks by its own Eq. 2 loads
+        for l, layer in enumerate(stack.layers):
+            res_l = sorted(ops[l][1])  # the plan's loads onto an empty GPU = the resident set
+            layer.begin_load([], owned_experts(plan_shares(res_l, E, world, agg[l]), rank))
+            eps.append(PeerExpertParallelMoE(layer, res_l, loads=agg[l], share_with=eps[0] if eps else None,
+                                             recv_rows_cap=args.ep_recv_cap))
+    else:
+        stack.apply(ops)
     stack.set_scores(agg)
     for layer in stack.layers:
         layer.poll_loads(blocking=True)
     torch.cuda.synchronize()
     serve = trace_dev[P_train + rank * Pr: P_train + (rank + 1) * Pr].contiguous()  # [Pr][m][Tp][k]
     ch = serve.permute(1, 0, 2, 3).reshape(m, T, k).long()
-    lg = torch.rand(m, T, E, generator=g, device=device) * 8.0 - 4.0
+    lg = torch.round((torch.rand(m, T, E, generator=g, device=device) * 8.0 - 4.0) * 64) / 64
     for r in range(k):
         lg.scatter_(2, ch[:, :, r:r + 1], 8.0 - r)
+    lg *= 16.0  # the trace bias dominates the gate's own logits (~N(0, |x|^2 / d))
     x = torch.randn(T, d, generator=g, device=device).to(torch.bfloat16)
     bufs = [torch.empty_like(x), torch.empty_like(x)]
     tid = torch.zeros(Pr, dtype=torch.int32, device=device)
@@ -847,22 +937,28 @@ def main_stack(args):
     def step(src=None):
         h = x if src is None else src
         for l, layer in enumerate(stack.layers):
-            h = layer.forward(h, logits=lg[l], out=bufs[l % 2])
+            if use_ep:
+                h = eps[l](h, logits=lg[l], out=bufs[l % 2])
+            else:
+                h = layer.forward(h, logits=lg[l], out=bufs[l % 2])
         emoe.moesim.check(_lib.lib.emoe_hist_update(stack.pred.h, C.c_void_p(serve.data_ptr()), Pr, Tp,
                                                     C.c_void_p(tid.data_ptr()), C.c_void_p(stream.cuda_stream)))
         return h
 
-    # served rows per layer (for the FFN FLOP count)
-    S_total = 0
+    # served rows and hits per layer of one step
+    S_total, hits = 0, 0
     h = x
     for l, layer in enumerate(stack.layers):
-        h = layer.forward(h, logits=lg[l], out=bufs[l % 2])
-        S_total += int(layer.workspace()["counts"].sum().item())
+        h = eps[l](h, logits=lg[l], out=bufs[l % 2]) if use_ep else layer.forward(h, logits=lg[l], out=bufs[l % 2])
+        ws = layer.workspace()
+        S_total += int(ws["counts"].sum().item())
+        hits += int(ws["route_hit"].sum().item())
+    topk_match = bool(torch.equal(stack.layers[-1].workspace()["topk_idx"].long(), ch[-1]))
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    for layer in stack.layers:
-        layer.set_profiling(True)
+    for obj in (eps if use_ep else stack.layers):
+        obj.set_profiling(True)
     launches0 = _lib.lib.emoe_kernel_launches()
     if world > 1:
         dist.barrier()
@@ -876,11 +972,21 @@ def main_stack(args):
         torch.cuda.synchronize()
     launches = int(_lib.lib.emoe_kernel_launches() - launches0)
     ms = ev0.elapsed_time(ev1) / args.steps
-    gemm_ms = 0.0
-    for layer in stack.layers:
-        st = layer.stage_times()
-        gemm_ms += st["gemm1"] + st["gemm2"]
-        layer.set_profiling(False)
+    stages, ep_stats = {}, None
+    for obj in (eps if use_ep else stack.layers):
+        for key, v in obj.stage_times().items():
+            stages[key] = stages.get(key, 0.0) + v
+        obj.set_profiling(False)
+    if use_ep:
+        ep_stats = {}
+        for ep in eps:
+            for key, v in ep.stats().items():
+                ep_stats[key] = ep_stats.get(key, 0) + v
+        gemm_ms = stages["gemm1"] + stages["gemm2_return"]
+        S_ffn = ep_stats["rows_computed_real"]
+    else:
+        gemm_ms = stages["gemm1"] + stages["gemm2"]
+        S_ffn = S_total
     if world > 1:
         t = torch.tensor([ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -905,28 +1011,37 @@ def main_stack(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     peaks = load_peaks()
-    ffn_flops = 2.0 * 3 * d * f * S_total
+    ffn_flops = 2.0 * 3 * d * f * S_ffn
     achieved = ffn_flops / (gemm_ms / 1e3) / 1e12
     out = dict(metric=METRIC, value=round(value, 1), unit="tokens/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=round(ms, 3), higher_is_better=True,
                scaling="strong" if strong else "weak", vs_baseline=None, dtype="bf16",
-               data="synthetic (random-init weights; routing-driven from the reference Markov trace)",
-               config=dict(workload=f"BASELINE config 4 (without the exchange): {m}-layer Mixtral-shaped MoE stack "
-                                    f"bf16, 8 experts top-2, 4 predicted resident per layer, {Pr} x {Tp} tokens per "
-                                    "GPU through every layer", layers=m, tokens_per_step=T,
-                           served_rows_all_layers=S_total, workspace="one shared activation workspace",
-                           parallelism=f"replicas{world}" if world > 1 else "single",
+               data="synthetic (random-init weights; gate computed on x, routing biased to the reference Markov "
+                    "trace)",
+               config=dict(workload=f"BASELINE config 4: {m}-layer Mixtral-shaped MoE stack bf16, 8 experts top-2, "
+                                    f"4 predicted resident per layer, {Pr} x {Tp} tokens per GPU through every layer",
+                           layers=m, tokens_per_step=T, served_rows_all_layers=S_total,
+                           hit_rate=round(hits / (T * m), 4), routing_follows_trace=topk_match,
+                           workspace="one shared activation workspace" + (
+                               " + one shared EP peer-memory region" if use_ep else ""),
+                           parallelism=parallelism_label(world, args.parallel, "p2p"),
                            l2="inputs larger than L2: x is %.0f MB per layer" % (T * d * 2 / 1e6)),
                roofline=dict(bound="tensor", achieved=round(achieved, 1), peak=peaks["bf16_sustained"],
                              unit="TFLOP/s", frac=round(achieved / peaks["bf16_sustained"], 4),
                              kernel="grouped_gemm_kernel (GEMM1 + GEMM2 of every layer), stage events",
-                             algorithmic=f"2*3*d*f*S summed over layers = {ffn_flops:.4g} FLOP per step"),
+                             algorithmic=f"2*3*d*f*S summed over layers = {ffn_flops:.4g} FLOP per step "
+                                         f"(S = {S_ffn} rows computed on this GPU)"),
                e2e=dict(value=world * T / e2e_s, unit="tokens/s", h2d_bytes_per_step=x_host.numel() * 2,
                         d2h_bytes_per_step=y_host.numel() * 2, ms_per_step=e2e_s * 1e3),
                gpu_launches=launches, clocks=clk.summary(), per_layer_ms=round(ms / m, 3),
+               stages_ms={kk: round(v, 3) for kk, v in stages.items()},
                resident_per_layer=[[int(e) for e in np.flatnonzero(layer.residency())] for layer in stack.layers[:4]])
+    if use_ep:
+        out["ep"] = ep_report(eps, stages, ep_stats, world, rank, device)
     if rank == 0:
         print(json.dumps(out), flush=True)
+    for ep in eps:
+        ep.close()
     stack.close()
     if world > 1:
         dist.destroy_process_group()

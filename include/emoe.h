@@ -101,6 +101,17 @@ int emoe_layer_register_expert_pinned(emoe_layer* layer, int expert, const void*
  * schedules them (engine.cpp:431-440). */
 int emoe_layer_set_copy_stream(emoe_layer* layer, void* stream);
 
+/* What a forward does with caller logits (logits_in of emoe_moe_forward,
+ * emoe_route, emoe_route_permute, emoe_ep_forward):
+ *   EMOE_LOGITS_REPLACE (default)  routing-driven parity mode: logits_in
+ *       replaces the gate (x is still the FFN's input);
+ *   EMOE_LOGITS_ADD  the gate runs on x and logits_in [T][E] fp32 is added to
+ *       its fp32 logits before top-k (a serving trace imposed as a bias on a
+ *       real gate computation); the workspace logits hold the sum. */
+#define EMOE_LOGITS_REPLACE 0
+#define EMOE_LOGITS_ADD 1
+int emoe_layer_set_logits_mode(emoe_layer* layer, int mode);
+
 /* Layer scores used by the route_token fallback (the engine's last aggregate
  * row, set when an invocation completes: engine.cpp:424, :529-531).
  * scores == NULL sets the empty score vector.  Stream-ordered: the [E]
@@ -189,17 +200,26 @@ int emoe_combine(emoe_layer* layer, const void* y_rows_dev, const int32_t* pos_d
  * forward it extends is the engine's per-layer serve step, engine.cpp:524-546.
  *   emoe_ep_create      one per rank over that rank's layer (its slots hold
  *                       the experts it computes; routing residency set with
- *                       emoe_layer_set_route_residency).  dest[world][E]: rank
- *                       that computes source rank s's rows of expert e (-1 =
- *                       not resident).  recv_rows_cap 0 = the worst case,
- *                       world x the layer's rows_cap.  world <= 8, bf16.
+ *                       emoe_layer_set_route_residency).  cum_shares[E][world]
+ *                       (int64, fixed point 2^24 = 1): cumulative share of
+ *                       expert e's rows computed on ranks <= q, non-decreasing
+ *                       over q and ending at 2^24; a row of -1 = not resident.
+ *                       Each forward splits e's rows (all sources, in source
+ *                       order) at those shares, rounded to the segment padding,
+ *                       so a hot expert is shared token by token.  recv_rows_cap
+ *                       0 = the worst case, world x the layer's rows_cap.
+ *                       share_with (NULL or another rank-local handle of the
+ *                       same world/rank and layer shape): reuse its symmetric
+ *                       region, IPC mappings and epoch -- the layers of a stack
+ *                       share one region (open peers once, on the first).
+ *                       world <= 8, bf16.
  *   emoe_ep_ipc_handle  this rank's symmetric buffer as an IPC handle
  *                       (EMOE_IPC_HANDLE_BYTES bytes) for the caller to
  *                       all-gather; emoe_ep_open_peers maps the others
  *                       (handles[world][EMOE_IPC_HANDLE_BYTES], own ignored).
- *   emoe_ep_forward     route -> dispatch (permute stores into the owners'
- *                       buffers) -> grouped FFN on the received rows ->
- *                       combine (loads from the owners' buffers), with three
+ *   emoe_ep_forward     route -> dispatch (permute stores into the computing
+ *                       ranks' buffers) -> grouped FFN on the received rows,
+ *                       GEMM2 pushing outputs back -> local combine, with three
  *                       device-side barriers; every rank must call it the
  *                       same number of times.  Output bit-identical to the
  *                       single-GPU forward.  No host synchronisation.
@@ -207,16 +227,33 @@ int emoe_combine(emoe_layer* layer, const void* y_rows_dev, const int32_t* pos_d
  *                       barrier timed out (EMOE_EP_TIMEOUT_S, default 60 s),
  *                       2 = a receive buffer overflowed (rows dropped);
  *                       *recv_rows = rows this rank computed last forward.
+ *   emoe_ep_stats       synchronises `stream`; out[5] of the last forward:
+ *                       rows this rank computed (padded), real rows it sent
+ *                       to peers, real rows it received from peers, real rows
+ *                       it routed, real rows it computed.
+ *   emoe_ep_layout      synchronises `stream`; the last forward's send pieces
+ *                       piece_end / piece_shift [E][world] and receive layout
+ *                       recv_segs [world*n_owned+1] / out_shift [world*n_owned]
+ *                       (any pointer may be NULL; for tests).
+ *   emoe_ep_set_profiling / emoe_ep_stage_times   per-forward CUDA events;
+ *                       ms[8] averaged over the profiled forwards: route,
+ *                       count exchange (bar0), dispatch, dispatch wait,
+ *                       gemm1, gemm2 + return pushes, return wait, combine.
  * ====================================================================== */
 #define EMOE_IPC_HANDLE_BYTES 64
 typedef struct emoe_ep emoe_ep;
-int emoe_ep_create(emoe_layer* layer, int world, int rank, const int32_t* dest, int64_t recv_rows_cap,
-                   emoe_ep** out);
+int emoe_ep_create(emoe_layer* layer, int world, int rank, const int64_t* cum_shares, int64_t recv_rows_cap,
+                   emoe_ep* share_with, emoe_ep** out);
 int emoe_ep_ipc_handle(emoe_ep* ep, void* handle_out);
 int emoe_ep_open_peers(emoe_ep* ep, const void* handles);
 int emoe_ep_forward(emoe_ep* ep, const void* x_dev, const float* logits_in_dev, void* y_dev, int64_t T,
                     void* stream);
 int emoe_ep_status(emoe_ep* ep, void* stream, int* status, int64_t* recv_rows);
+int emoe_ep_stats(emoe_ep* ep, void* stream, int64_t* out);
+int emoe_ep_layout(emoe_ep* ep, void* stream, int64_t* piece_end, int64_t* piece_shift, int64_t* recv_segs,
+                   int64_t* out_shift);
+int emoe_ep_set_profiling(emoe_ep* ep, int enable);
+int emoe_ep_stage_times(emoe_ep* ep, float* ms);
 int emoe_ep_destroy(emoe_ep* ep);
 
 /* Device pointers of the last forward's intermediates (valid until the next

@@ -56,6 +56,7 @@ _decl("emoe_layer_set_gate_host", vp, vp)
 _decl("emoe_layer_register_expert_host", vp, C.c_int, vp, vp, vp)
 _decl("emoe_layer_set_scores_host", vp, vp)
 _decl("emoe_layer_set_scores", vp, vp, vp)
+_decl("emoe_layer_set_logits_mode", vp, C.c_int)
 _decl("emoe_layer_register_expert_pinned", vp, C.c_int, vp, vp, vp)
 _decl("emoe_layer_set_copy_stream", vp, vp)
 _decl("emoe_layer_begin_load", vp, vp, C.c_int, vp, C.c_int, vp)
@@ -74,11 +75,15 @@ _decl("emoe_route_permute", vp, vp, vp, i64, vp)
 _decl("emoe_layer_set_route_residency", vp, vp, vp)
 _decl("emoe_ffn_segments", vp, vp, i64, vp, vp, C.c_int, vp, vp, vp)
 _decl("emoe_combine", vp, vp, vp, vp, i64, vp, vp)
-_decl("emoe_ep_create", vp, C.c_int, C.c_int, vp, i64, C.POINTER(vp))
+_decl("emoe_ep_create", vp, C.c_int, C.c_int, vp, i64, vp, C.POINTER(vp))
 _decl("emoe_ep_ipc_handle", vp, vp)
 _decl("emoe_ep_open_peers", vp, vp)
 _decl("emoe_ep_forward", vp, vp, vp, vp, i64, vp)
 _decl("emoe_ep_status", vp, vp, C.POINTER(C.c_int), C.POINTER(i64))
+_decl("emoe_ep_stats", vp, vp, vp)
+_decl("emoe_ep_layout", vp, vp, vp, vp, vp, vp)
+_decl("emoe_ep_set_profiling", vp, C.c_int)
+_decl("emoe_ep_stage_times", vp, vp)
 _decl("emoe_ep_destroy", vp)
 IPC_HANDLE_BYTES = 64
 _decl("emoe_layer_set_profiling", vp, C.c_int)
@@ -111,11 +116,12 @@ _decl("emoe_gen_routing_trace", C.c_int, C.c_int, C.c_int, dbl, dbl, C.c_int, C.
 EXPORTED = [
     "emoe_last_error", "emoe_version", "emoe_route_tokens_host", "emoe_layer_create", "emoe_layer_destroy",
     "emoe_layer_set_gate_host", "emoe_layer_register_expert_host", "emoe_layer_register_expert_pinned",
-    "emoe_layer_set_copy_stream", "emoe_layer_set_scores_host", "emoe_layer_set_scores",
+    "emoe_layer_set_copy_stream", "emoe_layer_set_scores_host", "emoe_layer_set_scores", "emoe_layer_set_logits_mode",
     "emoe_layer_begin_load", "emoe_layer_poll_loads", "emoe_layer_residency", "emoe_layer_last_load_stats",
     "emoe_moe_forward", "emoe_moe_forward_host", "emoe_moe_forward_host_async", "emoe_layer_wait_host", "emoe_route", "emoe_layer_gate_demand", "emoe_route_permute", "emoe_layer_set_route_residency",
     "emoe_ffn_segments", "emoe_combine", "emoe_ep_create", "emoe_ep_ipc_handle", "emoe_ep_open_peers",
-    "emoe_ep_forward", "emoe_ep_status", "emoe_ep_destroy", "emoe_layer_workspace", "emoe_layer_share_workspace", "emoe_layer_set_profiling",
+    "emoe_ep_forward", "emoe_ep_status", "emoe_ep_stats", "emoe_ep_layout", "emoe_ep_set_profiling",
+    "emoe_ep_stage_times", "emoe_ep_destroy", "emoe_layer_workspace", "emoe_layer_share_workspace", "emoe_layer_set_profiling",
     "emoe_layer_stage_times", "emoe_kernel_launches", "emoe_predictor_create",
     "emoe_predictor_destroy", "emoe_predictor_reset", "emoe_predictor_break_chain", "emoe_hist_update", "emoe_hist_update_host", "emoe_predictor_counts_host",
     "emoe_predictor_set_counts_host", "emoe_predictor_count_size", "emoe_predictor_counts_dev",

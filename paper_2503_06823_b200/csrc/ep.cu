@@ -1,40 +1,57 @@
 // Expert parallelism over peer memory: the token dispatch is
-// fused into the permute kernel (NVLink stores straight into the owning
+// fused into the permute kernel (NVLink stores straight into the computing
 // rank's receive buffer) and the return into GEMM2's epilogue (each expert
 // output row stored straight into its source rank's own permuted layout), so
 // the combine runs locally.  No all-to-all, no host synchronisation.
 //
+// Placement: every resident expert e is spread over a run of consecutive
+// ranks with cumulative shares cum[e][q] (units of 2^-24; ep.plan_shares cuts
+// the experts' expected loads, laid end to end in expert order, into one
+// unit interval per rank).  Per forward, every rank derives from the
+// replicated table of all ranks' counts the same split: e's rows, ordered by
+// (source rank, local row), are cut at B_e(q) = pad * round(N_e/pad * cum[e][q]
+// / 2^24) and rank q computes rows [B_e(q-1), B_e(q)).  A hot expert's rows
+// are thereby shared by its ranks token by token (not source by source), so
+// the busiest rank carries its share of the batch whatever the per-source
+// skew.  Pieces are multiples of the segment padding, so every receive
+// segment stays GEMM-tile aligned.
+//
 // Every rank allocates one symmetric region (same size everywhere) and maps
-// every peer's region through CUDA IPC:
+// every peer's region through CUDA IPC.  The layers of a stack share one
+// region (emoe_ep_create's share_with), so the receive / expert-output / H
+// buffers exist once per GPU, not once per layer:
 //   flags    u64 [3 phases][kMaxPeers]   epoch written by each source rank
-//   cnt      i32 [kMaxPeers][E]          padded segment sizes of every source
+//   cnt      i32 [kMaxPeers][E]          real (unpadded) per-expert counts of every source
 //   recv_x   bf16 [recv_cap][d]          rows dispatched to this rank
 //   y_local  bf16 [rows_cap][d]          expert outputs of this rank's own rows,
 //                                        in its local permuted layout
 // One forward, all on the caller's stream:
 //   K1 + K3a  route and scan locally (layer_route_scan)
-//   bar0      publish this rank's padded counts to every peer, signal, wait
-//             for all ranks, then derive from the replicated count table the
-//             receive segments, per local expert the row shift into its
-//             owner's receive buffer, and per receive segment the row shift
-//             back into its source's layout
-//   K3b       permute_kernel<REMOTE>: rows -> owner's recv_x (peer stores)
+//   bar0      publish this rank's counts to every peer, signal, wait for all
+//             ranks, then derive from the replicated table the split, this
+//             rank's receive segments (source, owned expert) with the row
+//             shift of each back into its source's layout, and its send
+//             pieces (per expert, per computing rank: local row end + shift)
+//   K3b       permute_kernel<REMOTE>: rows -> computing rank's recv_x (peer stores)
 //   bar1      signal + wait: every source finished writing to this rank
 //   K4        grouped GEMMs over the (source, expert) segments of recv_x;
 //             GEMM2's epilogue pushes each row to its source's y_local
 //   bar2      signal + wait: every rank's pushes have landed
 //   K5        combine_bf16_kernel over the local y_local (slot order)
-// Receive layout on rank q: segments ordered by (source rank, expert), the
-// same order the NCCL path (ep.py) uses; every row meets the same GEMM
-// arithmetic and the combine order is fixed at the source, so the output is
-// bit-identical to EP=1.
-// Buffer reuse across forwards needs no extra barrier: a source writes cnt /
-// recv_x of forward n+1 only after its own bar2 of forward n, which every
-// rank reaches only after its layout reads of forward n; GEMM2 of forward
-// n+1 pushes into a source's y_local only after bar1 of n+1, i.e. after every
-// rank finished its combine of forward n.
+// Every row meets the same GEMM arithmetic wherever it runs and the combine
+// order is fixed at the source, so the output is bit-identical to EP=1.
+// Buffer reuse across forwards (and across the layers sharing a region)
+// needs no extra barrier: a source writes cnt / recv_x of forward n+1 only
+// after its own bar2 of forward n, which every rank reaches only after its
+// layout reads of forward n; GEMM2 of forward n+1 pushes into a source's
+// y_local only after bar1 of n+1, i.e. after every rank finished its combine
+// of forward n.  The epoch is per region, so consecutive layers' barriers
+// never alias.
+#include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "capi_util.h"
@@ -44,6 +61,11 @@ namespace emoe {
 namespace {
 
 constexpr int kPhases = 3;
+constexpr int kMaxE = 128;
+constexpr int kShareBits = 24;  // cum shares are fixed point with 24 fraction bits
+// stats: rows computed (padded), real rows sent to peers, real rows received
+// from peers, real rows routed (this rank's tokens), real rows computed
+constexpr int kStats = 5;
 
 struct PeerSym {
   uint64_t* flags[kMaxPeers];
@@ -89,36 +111,84 @@ __device__ void barrier(const PeerSym& sym, int W, int rank, int phase, uint64_t
 }
 
 struct LayoutArgs {
+  const int32_t* counts;       // [E] this rank's real rows per expert
   const int64_t* seg_offsets;  // [E+1] this rank's padded local segments
-  const int32_t* dest;         // [W][E]
+  const int64_t* cum;          // [E][W] cumulative shares (-1: not resident)
   const int32_t* owned;        // [n_owned] experts this rank computes (ascending)
   int n_owned;
+  int pad;
   int64_t recv_cap;
-  int64_t* recv_segs;  // [W * n_owned + 1]
-  int64_t* row_shift;  // [E]
-  int64_t* out_shift;  // [W * n_owned] receive row -> row in the source's layout
-  int64_t* recv_rows;  // [1]
+  int64_t* piece_end;    // [E][W] local row end of this rank's piece of e computed on rank q
+  int64_t* piece_shift;  // [E][W] receive row on q = local row + shift
+  int64_t* recv_segs;    // [W * n_owned + 1]
+  int64_t* out_shift;    // [W * n_owned] receive row -> row in the source's layout
+  int64_t* stats;        // [kStats]
 };
 
-// bar0: publish counts, barrier, then the receive segments and the send shifts
+// bar0: publish counts, barrier, then the split, the receive segments and the send pieces
 __global__ void __launch_bounds__(256) ep_bar0_kernel(PeerSym sym, int W, int rank, int E, uint64_t epoch,
                                                       uint64_t timeout_ns, int* status, LayoutArgs a) {
+  __shared__ int32_t cr[kMaxPeers][kMaxE];   // real counts [source][expert]
+  __shared__ int64_t pre[kMaxPeers][kMaxE];  // rows of e held by earlier sources (padded)
+  __shared__ int64_t loc[kMaxPeers][kMaxE];  // source's padded local segment offset of e
+  __shared__ int64_t bnd[kMaxE][kMaxPeers];  // split ends B_e(q)
   __shared__ int64_t tot[kMaxPeers][kMaxPeers];  // [source][receiver] rows
+  __shared__ unsigned long long st_sent, st_recv, st_routed;
   __shared__ int overflow;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    const int32_t v = (int32_t)(a.seg_offsets[e + 1] - a.seg_offsets[e]);
+    const int32_t v = a.counts[e];
     for (int q = 0; q < W; ++q) sym.cnt[q][rank * E + e] = v;
   }
   barrier(sym, W, rank, 0, epoch, timeout_ns, status);
   const int32_t* cnt = sym.cnt[rank];  // every source's counts, now local
+  const int64_t pad = a.pad;
+  for (int i = threadIdx.x; i < W * E; i += blockDim.x) cr[i / E][i % E] = cnt[i];
+  if (threadIdx.x == 0) {
+    overflow = 0;
+    st_sent = st_recv = st_routed = 0;
+  }
+  __syncthreads();
+  auto padded = [&](int s, int e) -> int64_t { return ((int64_t)cr[s][e] + pad - 1) / pad * pad; };
+  // per expert: source prefixes and the split ends
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int64_t n = 0;
+    for (int s = 0; s < W; ++s) {
+      pre[s][e] = n;
+      n += padded(s, e);
+    }
+    const int64_t units = n / pad;
+    for (int q = 0; q < W; ++q) {
+      const int64_t c = a.cum[e * W + q];
+      int64_t b = q == W - 1 || c < 0 ? n : pad * ((units * c + (1ll << (kShareBits - 1))) >> kShareBits);
+      bnd[e][q] = b < n ? b : n;
+    }
+  }
+  // per source: padded local offsets (its segments in expert order)
+  for (int s = threadIdx.x; s < W; s += blockDim.x) {
+    int64_t o = 0;
+    for (int e = 0; e < E; ++e) {
+      loc[s][e] = o;
+      o += padded(s, e);
+    }
+  }
+  __syncthreads();
+  // rows of source s's segment e that rank q computes: [lo, hi) of e's global order
+  auto piece = [&](int s, int e, int q, int64_t& lo, int64_t& hi) {
+    const int64_t p0 = pre[s][e], p1 = p0 + padded(s, e);
+    lo = max(p0, q > 0 ? bnd[e][q - 1] : (int64_t)0);
+    hi = min(p1, bnd[e][q]);
+    if (hi < lo) hi = lo;
+  };
   if (threadIdx.x < W * W) {
     const int s = threadIdx.x / W, q = threadIdx.x % W;
     int64_t t = 0;
-    for (int e = 0; e < E; ++e)
-      if (a.dest[s * E + e] == q) t += cnt[s * E + e];
+    for (int e = 0; e < E; ++e) {
+      int64_t lo, hi;
+      piece(s, e, q, lo, hi);
+      t += hi - lo;
+    }
     tot[s][q] = t;
   }
-  if (threadIdx.x == 0) overflow = 0;
   __syncthreads();
   if (threadIdx.x < W) {
     int64_t t = 0;
@@ -126,45 +196,70 @@ __global__ void __launch_bounds__(256) ep_bar0_kernel(PeerSym sym, int W, int ra
     if (t > a.recv_cap) overflow = 1;
   }
   __syncthreads();
-  if (overflow) {
+  if (overflow) {  // every rank sees the same table: all drop the forward's rows and report status 2
     if (threadIdx.x == 0) atomicExch(status, 2);
-    for (int e = threadIdx.x; e < E; e += blockDim.x) a.row_shift[e] = a.recv_cap;  // every row out of range
+    for (int i = threadIdx.x; i < E * W; i += blockDim.x) {
+      a.piece_end[i] = a.seg_offsets[i / W];  // no row falls in any piece
+      a.piece_shift[i] = 0;
+    }
     for (int i = threadIdx.x; i <= W * a.n_owned; i += blockDim.x) a.recv_segs[i] = 0;
-    if (threadIdx.x == 0) *a.recv_rows = 0;
+    if (threadIdx.x < kStats) a.stats[threadIdx.x] = 0;
     return;
   }
-  // send shifts: segment e goes to q = dest[rank][e] after every earlier
-  // source's rows for q and this rank's rows of earlier experts for q
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    const int q = a.dest[rank * E + e];
-    if (q < 0) {
-      a.row_shift[e] = 0;
-      continue;
+  // send pieces of this rank, one thread per computing rank q, experts in order
+  if (threadIdx.x < W) {
+    const int q = threadIdx.x;
+    int64_t recv_off = 0;  // rows earlier sources send q, then this rank's earlier experts
+    for (int s = 0; s < rank; ++s) recv_off += tot[s][q];
+    for (int e = 0; e < E; ++e) {
+      int64_t lo, hi;
+      piece(rank, e, q, lo, hi);
+      const int64_t p0 = pre[rank][e], seg = a.seg_offsets[e];
+      const int64_t end_g = min(max(bnd[e][q], p0), p0 + padded(rank, e));
+      a.piece_end[e * W + q] = seg + (end_g - p0);
+      // local row r of the piece lands on receive row recv_off + (r - seg) - (lo - p0)
+      a.piece_shift[e * W + q] = recv_off - seg - (lo - p0);
+      recv_off += hi - lo;
+      // real (unpadded) rows of the piece, for the exchange statistics
+      const int64_t real = min(hi, p0 + (int64_t)cr[rank][e]) - lo;
+      if (real > 0) {
+        if (q != rank) atomicAdd(&st_sent, (unsigned long long)real);
+        atomicAdd(&st_routed, (unsigned long long)real);
+      }
     }
-    int64_t base = 0;
-    for (int s = 0; s < rank; ++s) base += tot[s][q];
-    for (int e2 = 0; e2 < e; ++e2)
-      if (a.dest[rank * E + e2] == q) base += cnt[rank * E + e2];
-    a.row_shift[e] = base - a.seg_offsets[e];
   }
-  // receive segments: (source, owned expert) in order; the return shift maps
-  // receive row r of segment (s, e) to row r + shift of source s's layout
-  // (its padded segment e starts at the exclusive prefix of its counts)
-  if (threadIdx.x == 0) {
+  // receive segments of this rank: (source, owned expert) in order; the
+  // return shift maps receive row r of segment (s, e) to row r + shift of
+  // source s's layout
+  if (threadIdx.x == 32) {
     int64_t off = 0;
     int i = 0;
+    unsigned long long rr = 0, rc = 0;
     for (int s = 0; s < W; ++s)
       for (int j = 0; j < a.n_owned; ++j) {
         const int e = a.owned[j];
-        int64_t src_off = 0;
-        for (int e2 = 0; e2 < e; ++e2) src_off += cnt[s * E + e2];
+        int64_t lo, hi;
+        piece(s, e, rank, lo, hi);
         a.recv_segs[i] = off;
-        a.out_shift[i] = src_off - off;
+        a.out_shift[i] = loc[s][e] + (lo - pre[s][e]) - off;
         ++i;
-        if (a.dest[s * E + e] == rank) off += cnt[s * E + e];
+        off += hi - lo;
+        const int64_t real = min(hi, pre[s][e] + (int64_t)cr[s][e]) - lo;
+        if (real > 0) {
+          if (s != rank) rr += (unsigned long long)real;
+          rc += (unsigned long long)real;
+        }
       }
     a.recv_segs[i] = off;
-    *a.recv_rows = off;
+    a.stats[0] = off;
+    a.stats[4] = (int64_t)rc;
+    st_recv = rr;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a.stats[1] = (int64_t)st_sent;
+    a.stats[2] = (int64_t)st_recv;
+    a.stats[3] = (int64_t)st_routed;
   }
 }
 
@@ -182,36 +277,17 @@ T* dmalloc(size_t count) {
 
 size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
-}  // namespace
-}  // namespace emoe
-
-using namespace emoe;
-
-struct emoe_ep {
-  emoe_layer* layer = nullptr;
-  LayerView v{};
-  int W = 1, rank = 0;
-  int64_t recv_cap = 0;
-  std::vector<int32_t> dest;  // [W][E]
-  std::vector<int32_t> owned;
-  uint64_t epoch = 0;
-  uint64_t timeout_ns = 0;
-
-  uint8_t* sym = nullptr;  // own symmetric region
-  size_t sym_bytes = 0, off_cnt = 0, off_x = 0, off_y = 0;  // off_y: y_local
-  uint8_t* peer[kMaxPeers] = {};  // symmetric regions of every rank (own = sym)
+// The per-GPU symmetric region (shared by the layers of a stack).
+struct EpRegion {
+  int W = 1, rank = 0, E = 0, d = 0, f = 0, elem = 2;
+  int64_t recv_cap = 0, rows_cap = 0;
+  uint64_t epoch = 0, timeout_ns = 0;
+  uint8_t* sym = nullptr;
+  size_t sym_bytes = 0, off_cnt = 0, off_x = 0, off_y = 0;
+  uint8_t* peer[kMaxPeers] = {};
   bool opened = false;
-
-  int32_t* dest_dev = nullptr;
-  int32_t* owned_dev = nullptr;
-  int64_t* row_shift = nullptr;
-  int64_t* recv_segs = nullptr;
-  int32_t* seg_expert = nullptr;  // [W * n_owned]
-  int32_t* seg_rank = nullptr;    // [W * n_owned] source rank of each receive segment
-  int64_t* out_shift = nullptr;   // [W * n_owned]
-  int64_t* recv_rows = nullptr;
+  void* h = nullptr;  // [recv_cap][f] GEMM1 output of the received rows
   int* status = nullptr;
-  void* h = nullptr;
 
   PeerSym peer_sym() const {
     PeerSym p{};
@@ -221,105 +297,201 @@ struct emoe_ep {
     }
     return p;
   }
-  PeerRows rows(size_t off) const {
-    PeerRows r{};
-    for (int q = 0; q < W; ++q) r.base[q] = peer[q] + off;
-    r.dest = dest_dev + (size_t)rank * v.E;
-    r.row_shift = row_shift;
-    r.cap = recv_cap;
-    return r;
+  ~EpRegion() {
+    cudaDeviceSynchronize();
+    for (int q = 0; q < W; ++q)
+      if (peer[q] && peer[q] != sym) cudaIpcCloseMemHandle(peer[q]);
+    for (void* p : {(void*)sym, h, (void*)status})
+      if (p) cudaFree(p);
+  }
+};
+
+}  // namespace
+}  // namespace emoe
+
+using namespace emoe;
+
+struct emoe_ep {
+  emoe_layer* layer = nullptr;
+  LayerView v{};
+  std::shared_ptr<EpRegion> R;
+  std::vector<int64_t> cum;  // [E][W]
+  std::vector<int32_t> owned;
+
+  int64_t* cum_dev = nullptr;
+  int32_t* owned_dev = nullptr;
+  int64_t* piece_end = nullptr;
+  int64_t* piece_shift = nullptr;
+  int64_t* recv_segs = nullptr;
+  int32_t* seg_expert = nullptr;  // [W * n_owned]
+  int32_t* seg_rank = nullptr;    // [W * n_owned] source rank of each receive segment
+  int64_t* out_shift = nullptr;   // [W * n_owned]
+  int64_t* stats = nullptr;       // [kStats]
+
+  // stage events: route, count exchange (bar0), dispatch (remote permute),
+  // dispatch wait (bar1), gemm1, gemm2 + return pushes, return wait (bar2), combine
+  static constexpr int kEv = 9;
+  bool profiling = false;
+  std::vector<std::array<cudaEvent_t, kEv>> ev_pool;
+  size_t ev_used = 0;
+  void mark(int i, cudaStream_t s) {
+    if (!profiling) return;
+    if (i == 0 && ev_used == ev_pool.size()) {
+      std::array<cudaEvent_t, kEv> set;
+      for (cudaEvent_t& e : set) EMOE_CUDA(cudaEventCreate(&e));
+      ev_pool.push_back(set);
+    }
+    EMOE_CUDA(cudaEventRecord(ev_pool[ev_used][i], s));
+    if (i == kEv - 1) ++ev_used;
   }
 
   void forward(const void* x, const float* logits_in, void* y, int64_t T, cudaStream_t s) {
-    EMOE_REQUIRE(opened, "ep_forward: peers not opened (emoe_ep_open_peers)");
-    ++epoch;
+    EpRegion& g = *R;
+    EMOE_REQUIRE(g.opened, "ep_forward: peers not opened (emoe_ep_open_peers)");
+    const int W = g.W;
+    ++g.epoch;
+    mark(0, s);
     layer_route_scan(layer, x, logits_in, T, s);
     if (T == 0) {  // nothing routed: publish zero counts so peers' layouts stay consistent
       EMOE_CUDA(cudaMemsetAsync(const_cast<int64_t*>(v.seg_offsets), 0, sizeof(int64_t) * (v.E + 1), s));
+      EMOE_CUDA(cudaMemsetAsync(const_cast<int32_t*>(v.counts), 0, sizeof(int32_t) * v.E, s));
     }
+    mark(1, s);
     const int n_owned = (int)owned.size();
-    LayoutArgs a{v.seg_offsets, dest_dev, owned_dev, n_owned, recv_cap, recv_segs, row_shift, out_shift, recv_rows};
-    const PeerSym ps = peer_sym();
-    ep_bar0_kernel<<<1, 256, 0, s>>>(ps, W, rank, v.E, epoch, timeout_ns, status, a);
+    LayoutArgs a{v.counts, v.seg_offsets, cum_dev, owned_dev, n_owned, v.seg_pad, g.recv_cap,
+                 piece_end, piece_shift, recv_segs, out_shift, stats};
+    const PeerSym ps = g.peer_sym();
+    ep_bar0_kernel<<<1, 256, 0, s>>>(ps, W, g.rank, v.E, g.epoch, g.timeout_ns, g.status, a);
     EMOE_CUDA(cudaGetLastError());
-    launch_permute_remote(x, v.elem, T, v.d, v.E, v.k, v.served_idx, v.seg_offsets, v.block_base, rows(off_x),
-                          v.pos, s);
-    ep_bar_kernel<<<1, 32, 0, s>>>(ps, W, rank, 1, epoch, timeout_ns, status);
+    mark(2, s);
+    PeerRows pr{};
+    for (int q = 0; q < W; ++q) pr.base[q] = g.peer[q] + g.off_x;
+    pr.piece_end = piece_end;
+    pr.piece_shift = piece_shift;
+    pr.W = W;
+    pr.cap = g.recv_cap;
+    launch_permute_remote(x, v.elem, T, v.d, v.E, v.k, v.served_idx, v.seg_offsets, v.block_base, pr, v.pos, s);
+    mark(3, s);
+    ep_bar_kernel<<<1, 32, 0, s>>>(ps, W, g.rank, 1, g.epoch, g.timeout_ns, g.status);
     EMOE_CUDA(cudaGetLastError());
+    mark(4, s);
+    cudaEvent_t mid = profiling ? ev_pool[ev_used][5] : nullptr;
     if (n_owned > 0) {
       PeerOut po{};
-      for (int q = 0; q < W; ++q) po.base[q] = peer[q] + off_y;
+      for (int q = 0; q < W; ++q) po.base[q] = g.peer[q] + g.off_y;
       po.seg_rank = seg_rank;
       po.seg_shift = out_shift;
-      layer_ffn_rows(layer, sym + off_x, recv_cap, recv_segs, seg_expert, W * n_owned, h, sym + off_y, s, &po);
+      layer_ffn_rows(layer, g.sym + g.off_x, g.recv_cap, recv_segs, seg_expert, W * n_owned, g.h, g.sym + g.off_y,
+                     s, &po, mid);
+    } else if (mid) {
+      EMOE_CUDA(cudaEventRecord(mid, s));
     }
-    ep_bar_kernel<<<1, 32, 0, s>>>(ps, W, rank, 2, epoch, timeout_ns, status);
+    mark(6, s);
+    ep_bar_kernel<<<1, 32, 0, s>>>(ps, W, g.rank, 2, g.epoch, g.timeout_ns, g.status);
     EMOE_CUDA(cudaGetLastError());
     count_launch(3);
-    launch_combine(sym + off_y, DT_BF16, T, v.d, v.k, v.pos, v.served_w, y, s);
+    mark(7, s);
+    launch_combine(g.sym + g.off_y, DT_BF16, T, v.d, v.k, v.pos, v.served_w, y, s);
+    mark(8, s);
   }
 
   void destroy() {
-    for (int q = 0; q < W; ++q)
-      if (peer[q] && peer[q] != sym) cudaIpcCloseMemHandle(peer[q]);
-    for (void* p : {(void*)sym, (void*)dest_dev, (void*)owned_dev, (void*)row_shift, (void*)recv_segs,
-                    (void*)seg_expert, (void*)seg_rank, (void*)out_shift, (void*)recv_rows, (void*)status, h})
+    cudaDeviceSynchronize();
+    for (void* p : {(void*)cum_dev, (void*)owned_dev, (void*)piece_end, (void*)piece_shift, (void*)recv_segs,
+                    (void*)seg_expert, (void*)seg_rank, (void*)out_shift, (void*)stats})
       if (p) cudaFree(p);
+    for (auto& set : ev_pool)
+      for (cudaEvent_t e : set) cudaEventDestroy(e);
+    R.reset();
   }
 };
 
 extern "C" {
 
-int emoe_ep_create(emoe_layer* layer, int world, int rank, const int32_t* dest, int64_t recv_rows_cap,
-                   emoe_ep** out) {
+int emoe_ep_create(emoe_layer* layer, int world, int rank, const int64_t* cum_shares, int64_t recv_rows_cap,
+                   emoe_ep* share_with, emoe_ep** out) {
   return guard([&] {
-    EMOE_REQUIRE(layer && dest && out, "ep_create: null argument");
+    EMOE_REQUIRE(layer && cum_shares && out, "ep_create: null argument");
     EMOE_REQUIRE(world >= 1 && world <= kMaxPeers, "ep_create: world must be in [1, 8]");
     EMOE_REQUIRE(rank >= 0 && rank < world, "ep_create: rank out of range");
     const LayerView v = layer_view(layer);
     EMOE_REQUIRE(v.dtype == DT_BF16, "ep_create: expert parallelism runs the bf16 path");
     const int E = v.E;
-    std::vector<int32_t> dv(dest, dest + (size_t)world * E);
+    EMOE_REQUIRE(E <= kMaxE, "ep_create: at most 128 experts");
+    const int64_t one = 1ll << kShareBits;
+    std::vector<int64_t> cum(cum_shares, cum_shares + (size_t)world * E);
     std::vector<int32_t> owned;
     for (int e = 0; e < E; ++e) {
-      bool mine = false;
-      for (int s = 0; s < world; ++s) {
-        EMOE_REQUIRE(dv[(size_t)s * E + e] >= -1 && dv[(size_t)s * E + e] < world, "ep_create: dest out of range");
-        mine |= dv[(size_t)s * E + e] == rank;
+      const int64_t* c = cum.data() + (size_t)e * world;
+      if (c[0] < 0) {  // not resident
+        for (int q = 0; q < world; ++q) EMOE_REQUIRE(c[q] < 0, "ep_create: cum_shares row mixes -1 and shares");
+        continue;
       }
-      if (mine) owned.push_back(e);
+      for (int q = 0; q < world; ++q) {
+        EMOE_REQUIRE(c[q] >= 0 && c[q] <= one, "ep_create: cum_shares must lie in [0, 2^24]");
+        EMOE_REQUIRE(q == 0 || c[q] >= c[q - 1], "ep_create: cum_shares must be non-decreasing over ranks");
+      }
+      EMOE_REQUIRE(c[world - 1] == one, "ep_create: cum_shares must end at 2^24");
+      if (c[rank] > (rank > 0 ? c[rank - 1] : 0)) owned.push_back(e);
     }
     EMOE_REQUIRE((int64_t)world * (int64_t)owned.size() <= 256, "ep_create: more than 256 receive segments");
     auto* ep = new emoe_ep();
     try {
       ep->layer = layer;
       ep->v = v;
-      ep->W = world;
-      ep->rank = rank;
-      ep->dest = dv;
+      ep->cum = cum;
       ep->owned = owned;
-      // default: the worst case (every source sends this rank all of its rows)
-      ep->recv_cap = recv_rows_cap > 0 ? ceil_div(recv_rows_cap, v.seg_pad) * v.seg_pad : (int64_t)world * v.rows_cap;
-      const char* to = getenv("EMOE_EP_TIMEOUT_S");
-      ep->timeout_ns = (uint64_t)((to ? atof(to) : 60.0) * 1e9);
-      const size_t row = (size_t)v.d * v.elem;
-      ep->off_cnt = align256(sizeof(uint64_t) * kPhases * kMaxPeers);
-      ep->off_x = align256(ep->off_cnt + sizeof(int32_t) * kMaxPeers * E);
-      ep->off_y = align256(ep->off_x + (size_t)ep->recv_cap * row);
-      ep->sym_bytes = align256(ep->off_y + (size_t)v.rows_cap * row);
-      ep->sym = dmalloc<uint8_t>(ep->sym_bytes);
-      EMOE_CUDA(cudaMemset(ep->sym, 0, ep->sym_bytes));
-      ep->dest_dev = dmalloc<int32_t>(dv.size());
-      EMOE_CUDA(cudaMemcpy(ep->dest_dev, dv.data(), dv.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+      if (share_with) {
+        const EpRegion& g = *share_with->R;
+        EMOE_REQUIRE(g.W == world && g.rank == rank, "ep_create: share_with has another world or rank");
+        EMOE_REQUIRE(g.E == E && g.d == v.d && g.f == v.f && g.elem == v.elem && v.rows_cap <= g.rows_cap,
+                     "ep_create: share_with's region does not fit this layer's shape");
+        EMOE_REQUIRE(recv_rows_cap <= 0 || recv_rows_cap <= g.recv_cap,
+                     "ep_create: recv_rows_cap exceeds the shared region's");
+        ep->R = share_with->R;
+      } else {
+        auto g = std::make_shared<EpRegion>();
+        g->W = world;
+        g->rank = rank;
+        g->E = E;
+        g->d = v.d;
+        g->f = v.f;
+        g->elem = v.elem;
+        g->rows_cap = v.rows_cap;
+        // default: the worst case (every source sends this rank all of its rows)
+        g->recv_cap = recv_rows_cap > 0 ? ceil_div(recv_rows_cap, v.seg_pad) * v.seg_pad
+                                        : (int64_t)world * v.rows_cap;
+        const char* to = getenv("EMOE_EP_TIMEOUT_S");
+        g->timeout_ns = (uint64_t)((to ? atof(to) : 60.0) * 1e9);
+        const size_t row = (size_t)v.d * v.elem;
+        g->off_cnt = align256(sizeof(uint64_t) * kPhases * kMaxPeers);
+        g->off_x = align256(g->off_cnt + sizeof(int32_t) * kMaxPeers * E);
+        g->off_y = align256(g->off_x + (size_t)g->recv_cap * row);
+        g->sym_bytes = align256(g->off_y + (size_t)v.rows_cap * row);
+        g->sym = dmalloc<uint8_t>(g->sym_bytes);
+        EMOE_CUDA(cudaMemset(g->sym, 0, g->sym_bytes));
+        g->status = dmalloc<int>(1);
+        EMOE_CUDA(cudaMemset(g->status, 0, sizeof(int)));
+        g->h = dmalloc<uint8_t>((size_t)g->recv_cap * v.f * v.elem);
+        EMOE_CUDA(cudaMemset(g->h, 0, (size_t)g->recv_cap * v.f * v.elem));
+        g->peer[rank] = g->sym;
+        if (world == 1) g->opened = true;
+        ep->R = g;
+      }
+      ep->cum_dev = dmalloc<int64_t>(cum.size());
+      EMOE_CUDA(cudaMemcpy(ep->cum_dev, cum.data(), cum.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
       ep->owned_dev = dmalloc<int32_t>(std::max<size_t>(1, owned.size()));
       if (!owned.empty())
         EMOE_CUDA(cudaMemcpy(ep->owned_dev, owned.data(), owned.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-      ep->row_shift = dmalloc<int64_t>(E);
+      ep->piece_end = dmalloc<int64_t>((size_t)E * world);
+      ep->piece_shift = dmalloc<int64_t>((size_t)E * world);
       const int n_seg = world * (int)owned.size();
       ep->recv_segs = dmalloc<int64_t>(n_seg + 1);
       ep->seg_expert = dmalloc<int32_t>(std::max(1, n_seg));
       ep->seg_rank = dmalloc<int32_t>(std::max(1, n_seg));
       ep->out_shift = dmalloc<int64_t>(std::max(1, n_seg));
+      ep->stats = dmalloc<int64_t>(kStats);
+      EMOE_CUDA(cudaMemset(ep->stats, 0, sizeof(int64_t) * kStats));
       std::vector<int32_t> se, sr;
       for (int s = 0; s < world; ++s) {
         se.insert(se.end(), owned.begin(), owned.end());
@@ -329,13 +501,6 @@ int emoe_ep_create(emoe_layer* layer, int world, int rank, const int32_t* dest, 
         EMOE_CUDA(cudaMemcpy(ep->seg_expert, se.data(), se.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
         EMOE_CUDA(cudaMemcpy(ep->seg_rank, sr.data(), sr.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
       }
-      ep->recv_rows = dmalloc<int64_t>(1);
-      ep->status = dmalloc<int>(1);
-      EMOE_CUDA(cudaMemset(ep->status, 0, sizeof(int)));
-      ep->h = dmalloc<uint8_t>((size_t)ep->recv_cap * v.f * v.elem);
-      EMOE_CUDA(cudaMemset(ep->h, 0, (size_t)ep->recv_cap * v.f * v.elem));
-      ep->peer[rank] = ep->sym;
-      if (world == 1) ep->opened = true;
       EMOE_CUDA(cudaDeviceSynchronize());
     } catch (...) {
       ep->destroy();
@@ -351,7 +516,7 @@ int emoe_ep_ipc_handle(emoe_ep* ep, void* handle_out) {
     EMOE_REQUIRE(ep && handle_out, "ep_ipc_handle: null argument");
     static_assert(sizeof(cudaIpcMemHandle_t) == EMOE_IPC_HANDLE_BYTES, "IPC handle size");
     cudaIpcMemHandle_t hdl;
-    EMOE_CUDA(cudaIpcGetMemHandle(&hdl, ep->sym));
+    EMOE_CUDA(cudaIpcGetMemHandle(&hdl, ep->R->sym));
     std::memcpy(handle_out, &hdl, sizeof(hdl));
   });
 }
@@ -359,17 +524,18 @@ int emoe_ep_ipc_handle(emoe_ep* ep, void* handle_out) {
 int emoe_ep_open_peers(emoe_ep* ep, const void* handles) {
   return guard([&] {
     EMOE_REQUIRE(ep && handles, "ep_open_peers: null argument");
-    EMOE_REQUIRE(!ep->opened || ep->W == 1, "ep_open_peers: already opened");
+    EpRegion& g = *ep->R;
+    EMOE_REQUIRE(!g.opened || g.W == 1, "ep_open_peers: already opened (a shared region opens once)");
     const uint8_t* h = static_cast<const uint8_t*>(handles);
-    for (int q = 0; q < ep->W; ++q) {
-      if (q == ep->rank) continue;
+    for (int q = 0; q < g.W; ++q) {
+      if (q == g.rank) continue;
       cudaIpcMemHandle_t hdl;
       std::memcpy(&hdl, h + (size_t)q * EMOE_IPC_HANDLE_BYTES, sizeof(hdl));
       void* p = nullptr;
       EMOE_CUDA(cudaIpcOpenMemHandle(&p, hdl, cudaIpcMemLazyEnablePeerAccess));
-      ep->peer[q] = static_cast<uint8_t*>(p);
+      g.peer[q] = static_cast<uint8_t*>(p);
     }
-    ep->opened = true;
+    g.opened = true;
   });
 }
 
@@ -387,18 +553,67 @@ int emoe_ep_status(emoe_ep* ep, void* stream, int* status, int64_t* recv_rows) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int st = 0;
     int64_t rr = 0;
-    EMOE_CUDA(cudaMemcpyAsync(&st, ep->status, sizeof(int), cudaMemcpyDeviceToHost, s));
-    EMOE_CUDA(cudaMemcpyAsync(&rr, ep->recv_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    EMOE_CUDA(cudaMemcpyAsync(&st, ep->R->status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    EMOE_CUDA(cudaMemcpyAsync(&rr, ep->stats, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     EMOE_CUDA(cudaStreamSynchronize(s));
     if (status) *status = st;
     if (recv_rows) *recv_rows = rr;
   });
 }
 
+int emoe_ep_stats(emoe_ep* ep, void* stream, int64_t* out) {
+  return guard([&] {
+    EMOE_REQUIRE(ep && out, "ep_stats: null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    EMOE_CUDA(cudaMemcpyAsync(out, ep->stats, sizeof(int64_t) * kStats, cudaMemcpyDeviceToHost, s));
+    EMOE_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int emoe_ep_layout(emoe_ep* ep, void* stream, int64_t* piece_end, int64_t* piece_shift, int64_t* recv_segs,
+                   int64_t* out_shift) {
+  return guard([&] {
+    EMOE_REQUIRE(ep, "ep_layout: null handle");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t ew = (size_t)ep->v.E * ep->R->W, ns = (size_t)ep->R->W * ep->owned.size();
+    if (piece_end) EMOE_CUDA(cudaMemcpyAsync(piece_end, ep->piece_end, ew * 8, cudaMemcpyDeviceToHost, s));
+    if (piece_shift) EMOE_CUDA(cudaMemcpyAsync(piece_shift, ep->piece_shift, ew * 8, cudaMemcpyDeviceToHost, s));
+    if (recv_segs) EMOE_CUDA(cudaMemcpyAsync(recv_segs, ep->recv_segs, (ns + 1) * 8, cudaMemcpyDeviceToHost, s));
+    if (out_shift && ns) EMOE_CUDA(cudaMemcpyAsync(out_shift, ep->out_shift, ns * 8, cudaMemcpyDeviceToHost, s));
+    EMOE_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int emoe_ep_set_profiling(emoe_ep* ep, int enable) {
+  return guard([&] {
+    EMOE_REQUIRE(ep, "ep_set_profiling: null handle");
+    ep->profiling = enable != 0;
+    ep->ev_used = 0;
+  });
+}
+
+int emoe_ep_stage_times(emoe_ep* ep, float* ms) {
+  return guard([&] {
+    EMOE_REQUIRE(ep && ms, "ep_stage_times: null argument");
+    EMOE_REQUIRE(ep->ev_used > 0, "ep_stage_times: no profiled forward since the last call");
+    constexpr int n = emoe_ep::kEv - 1;
+    for (int i = 0; i < n; ++i) ms[i] = 0.0f;
+    for (size_t u = 0; u < ep->ev_used; ++u) {
+      auto& set = ep->ev_pool[u];
+      EMOE_CUDA(cudaEventSynchronize(set[n]));
+      for (int i = 0; i < n; ++i) {
+        float t = 0;
+        EMOE_CUDA(cudaEventElapsedTime(&t, set[i], set[i + 1]));
+        ms[i] += t / (float)ep->ev_used;
+      }
+    }
+    ep->ev_used = 0;
+  });
+}
+
 int emoe_ep_destroy(emoe_ep* ep) {
   return guard([&] {
     if (!ep) return;
-    cudaDeviceSynchronize();
     ep->destroy();
     delete ep;
   });

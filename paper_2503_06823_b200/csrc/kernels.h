@@ -42,6 +42,7 @@ struct RouteArgs {
   const uint8_t* resident;  // [E] device
   const double* scores;     // [E] device or null (empty score vector)
   int* error_flag;          // device int, set to 3 when a token needs a fallback and no expert is resident
+  const float* bias = nullptr;  // [T][E] added to the gate's logits before routing (null: none)
 };
 
 // K1 from activations: logits = x . wg^T (bf16 x via mma.sync, fp32 x via FFMA) + routing
@@ -61,15 +62,16 @@ void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int 
                     const int64_t* seg_offsets, const int64_t* block_base, void* x_perm, int32_t* pos,
                     int32_t* row_token, cudaStream_t s, float* x_hi = nullptr, float* x_lo = nullptr);
 // Expert-parallel peer-memory addressing: rank q's receive (or expert-output)
-// buffer is base[q] (own buffer or a CUDA-IPC mapping); dest[e] = rank that
-// computes this rank's rows of expert e; row_shift[e] = (row of segment e in
-// that rank's buffer) - (local segment offset).  dest / row_shift are device
-// arrays [E].
+// buffer is base[q] (own buffer or a CUDA-IPC mapping).  This rank's padded
+// segment of expert e is cut into pieces, one per computing rank q: local
+// rows [piece_end[e][q-1], piece_end[e][q]) go to rank q at receive row
+// (local row + piece_shift[e][q]).  Device arrays [E][W].
 constexpr int kMaxPeers = 8;
 struct PeerRows {
   uint8_t* base[kMaxPeers];
-  const int32_t* dest;
-  const int64_t* row_shift;
+  const int64_t* piece_end;
+  const int64_t* piece_shift;
+  int W;
   int64_t cap;  // rows per buffer: a row outside [0, cap) is not written (pos = -1)
 };
 // GEMM2 return form: segment i's output rows go to rank seg_rank[i]'s buffer
@@ -159,6 +161,7 @@ struct LayerView {
   const int64_t* seg_offsets;
   const int64_t* block_base;
   int32_t* pos;
+  const int32_t* counts;  // [E] real rows per expert of the last route
 };
 }  // namespace emoe
 
@@ -167,8 +170,10 @@ namespace emoe {
 LayerView layer_view(emoe_layer* L);
 // K1 + K3a (route, per-expert counts, padded local segment offsets); no gather
 void layer_route_scan(emoe_layer* L, const void* x, const float* logits_in, int64_t T, cudaStream_t s);
-// K4 over caller rows in n_seg segments (device seg offsets / experts)
+// K4 over caller rows in n_seg segments (device seg offsets / experts);
+// after_gemm1 (optional) is recorded on s between the two GEMMs
 void layer_ffn_rows(emoe_layer* L, const void* xr, int64_t R, const int64_t* segs, const int32_t* seg_expert,
-                    int n_seg, void* hr, void* yr, cudaStream_t s, const PeerOut* peer_out = nullptr);
+                    int n_seg, void* hr, void* yr, cudaStream_t s, const PeerOut* peer_out = nullptr,
+                    cudaEvent_t after_gemm1 = nullptr);
 
 }  // namespace emoe

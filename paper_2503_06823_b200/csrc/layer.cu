@@ -223,6 +223,11 @@ struct emoe_layer {
     return cfg.dtype == EMOE_DTYPE_BF16 && cfg.num_experts >= 32 && cfg.num_experts % 32 == 0 && wg_pad;
   }
 
+  // logits_in of a forward: EMOE_LOGITS_REPLACE (the routing-driven parity
+  // mode: no gate) or EMOE_LOGITS_ADD (the gate runs on x and logits_in is
+  // added to its logits before routing)
+  int logits_mode = EMOE_LOGITS_REPLACE;
+
   // Expert parallelism: routing sees the GLOBAL resident set (the reference
   // Placement) while this GPU's slots hold only the experts it serves.
   bool route_override = false;
@@ -248,7 +253,10 @@ struct emoe_layer {
     a.scores = have_scores ? scores_dev : nullptr;
     a.error_flag = err_flag;
     RouteOut o{logits, topk, r_expert, r_rank, r_hit, served_idx, served_w, block_counts};
-    if (logits_in) {
+    const bool add = logits_in && logits_mode == EMOE_LOGITS_ADD;
+    EMOE_REQUIRE(!add || x, "route: the logits-bias mode runs the gate, so x is required");
+    a.bias = add ? logits_in : nullptr;
+    if (logits_in && !add) {
       launch_route_from_logits(logits_in, a, o, s);
     } else if (tc_gate()) {
       // many experts: the gate is a real GEMM (T x d x E); run it on tcgen05
@@ -270,6 +278,7 @@ struct emoe_layer {
   // stage events for emoe_layer_stage_times (route, scan+permute, gemm1, gemm2, combine);
   // one event set per profiled forward, averaged and recycled by stage_times()
   bool profiling = false;
+  cudaEvent_t ext_mark3 = nullptr;  // layer_ffn_rows: the caller's between-GEMMs event
   std::vector<std::array<cudaEvent_t, 6>> ev_pool;
   size_t ev_used = 0;
   void mark(int i, cudaStream_t s) {
@@ -372,6 +381,7 @@ struct emoe_layer {
       launch_grouped_gemm(swiglu() ? EPI_SWIGLU : EPI_RELU, cta_group, a1, tb1, tb3, segs, slot_dev, n_seg, d, f, f,
                           static_cast<__nv_bfloat16*>(hr), f, num_sms, s, seg_expert, &o1);
       mark(3, s);
+      if (ext_mark3) EMOE_CUDA(cudaEventRecord(ext_mark3, s));
       launch_grouped_gemm(EPI_STORE, cta_group, a2, tb2, tb2, segs, slot_dev, n_seg, f, d, d,
                           static_cast<__nv_bfloat16*>(yr), d, num_sms, s, seg_expert, &o2, scatter, peer_out);
       mark(4, s);
@@ -989,6 +999,14 @@ int emoe_layer_gate_demand(emoe_layer* L, int64_t* counts_host, void* stream) {
   });
 }
 
+int emoe_layer_set_logits_mode(emoe_layer* L, int mode) {
+  return guard([&] {
+    EMOE_REQUIRE(L, "set_logits_mode: null layer");
+    EMOE_REQUIRE(mode == EMOE_LOGITS_REPLACE || mode == EMOE_LOGITS_ADD, "set_logits_mode: unknown mode");
+    L->logits_mode = mode;
+  });
+}
+
 int emoe_layer_set_route_residency(emoe_layer* L, const uint8_t* resident, void* stream) {
   return guard([&] {
     EMOE_REQUIRE(L, "set_route_residency: null layer");
@@ -1194,6 +1212,7 @@ LayerView layer_view(emoe_layer* L) {
   v.seg_offsets = L->seg_offsets;
   v.block_base = L->block_base;
   v.pos = L->pos;
+  v.counts = L->counts;
   return v;
 }
 
@@ -1206,10 +1225,12 @@ void layer_route_scan(emoe_layer* L, const void* x, const float* logits_in, int6
 }
 
 void layer_ffn_rows(emoe_layer* L, const void* xr, int64_t R, const int64_t* segs, const int32_t* seg_expert,
-                    int n_seg, void* hr, void* yr, cudaStream_t s, const PeerOut* peer_out) {
+                    int n_seg, void* hr, void* yr, cudaStream_t s, const PeerOut* peer_out, cudaEvent_t after_gemm1) {
   const bool was = L->profiling;
   L->profiling = false;
+  L->ext_mark3 = after_gemm1;
   L->ffn(xr, R, segs, seg_expert, n_seg, hr, yr, s, false, nullptr, peer_out);
+  L->ext_mark3 = nullptr;
   L->profiling = was;
 }
 

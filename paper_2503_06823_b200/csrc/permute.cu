@@ -76,10 +76,10 @@ __global__ void __launch_bounds__(1024) seg_offsets_kernel(const int32_t* __rest
 constexpr int PERMUTE_THREADS = 256;
 constexpr int GATHER_UNROLL = 8;
 
-// REMOTE (expert-parallel dispatch over peer memory): segment e is written to
-// rank dest[e]'s receive buffer (peers.base[dest[e]], mapped through CUDA IPC)
-// at row pos = d + row_shift[e], d being the local position above; pos[t][j]
-// then holds that remote row.  The per-block tail fence makes the NVLink
+// REMOTE (expert-parallel dispatch over peer memory): local row d of segment
+// e is written to the receive buffer of the rank computing its piece
+// (peers.base[q], mapped through CUDA IPC) at row d + piece_shift[e][q];
+// pos[t][j] keeps d, the local row the pushed output returns to.  The per-block tail fence makes the NVLink
 // stores visible system-wide before the host-ordered signal kernel runs.
 // SPLIT (fp32 rows of a 3xTF32 layer): also write each row's tf32 hi / lo
 // parts to x_hi / x_lo (a separate instantiation, so the other layers' permute
@@ -144,9 +144,12 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
       if (REMOTE) {
         uint8_t* ptr = nullptr;
         if (e >= 0) {
-          const int64_t r = d + peers.row_shift[e];
-          if (r >= 0 && r < peers.cap)  // out of range only when the receiver overflowed (status 2)
-            ptr = peers.base[peers.dest[e]] + r * row_bytes;
+          for (int q = 0; q < peers.W; ++q)  // the piece of segment e holding local row d
+            if (d < peers.piece_end[e * peers.W + q]) {
+              const int64_t r = d + peers.piece_shift[e * peers.W + q];
+              if (r >= 0 && r < peers.cap) ptr = peers.base[q] + r * row_bytes;
+              break;
+            }  // no piece: the receivers overflowed (status 2), the row is dropped
         }
         dptr_s[threadIdx.x * k + j] = ptr;
         if (t < T) pos[t * k + j] = ptr ? d : -1;  // outputs return to this local row

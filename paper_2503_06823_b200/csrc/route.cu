@@ -210,6 +210,16 @@ __device__ void route_one_token(const float* lg, int64_t t, const RouteArgs& a, 
   route_tail(ti, lg, t, a, o, st);
 }
 
+// logits-bias mode: tile[r][e] += bias[t0 + r][e] (coalesced over the tile)
+__device__ void add_bias_tile(float* tile, int ld, int64_t t0, const RouteArgs& a) {
+  __syncthreads();  // every thread's logits are in the tile
+  const int64_t rows = min((int64_t)RT, a.T - t0);
+  for (int64_t i = threadIdx.x; i < rows * a.E; i += blockDim.x) {
+    const int r = (int)(i / a.E), e = (int)(i % a.E);
+    tile[r * ld + e] += __ldg(a.bias + t0 * a.E + i);
+  }
+}
+
 // block's logits tile [rows][ld] in shared memory -> global [T][E], coalesced
 __device__ void store_logits_tile(const float* tile, int ld, int64_t t0, const RouteArgs& a, const RouteOut& o) {
   if (!o.logits) return;
@@ -316,6 +326,7 @@ __global__ void __launch_bounds__(128) gate_route_bf16_kernel(const __nv_bfloat1
       logits[(r + 8) * (EP + 1) + c] = acc[mt][nt][2];
       logits[(r + 8) * (EP + 1) + c + 1] = acc[mt][nt][3];
     }
+  if (a.bias) add_bias_tile(logits, EP + 1, t0, a);
   load_route_state(st, a);  // contains __syncthreads
   store_logits_tile(logits, EP + 1, t0, a, o);
   // thread per token: with the logits tile in shared memory even E = 128 costs
@@ -380,6 +391,7 @@ __global__ void __launch_bounds__(F32_GATE_THREADS) gate_route_f32_kernel(const 
       }
     }
   }
+  if (a.bias) add_bias_tile(logits, a.E, t0, a);
   load_route_state(st, a);
   store_logits_tile(logits, a.E, t0, a, o);
   const int64_t t = t0 + threadIdx.x;
@@ -394,7 +406,8 @@ __global__ void __launch_bounds__(F32_GATE_THREADS) gate_route_f32_kernel(const 
 // in the same order whatever the slicing), so small T still spans the GPU.
 __global__ void __launch_bounds__(256) gate_logits_f32_kernel(const float* __restrict__ x,
                                                               const float* __restrict__ wg, int64_t T, int d, int E,
-                                                              float* __restrict__ logits) {
+                                                              float* __restrict__ logits,
+                                                              const float* __restrict__ bias) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t t = (int64_t)blockIdx.x * 8 + warp;
   if (t >= T) return;
@@ -431,7 +444,7 @@ __global__ void __launch_bounds__(256) gate_logits_f32_kernel(const float* __res
       float v = acc[j];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == 0 && j < ne) logits[t * E + e0 + j] = v;
+      if (lane == 0 && j < ne) logits[t * E + e0 + j] = bias ? v + bias[t * E + e0 + j] : v;
     }
   }
 }
@@ -457,7 +470,7 @@ __global__ void __launch_bounds__(RT) route_from_logits_kernel(const float* __re
   if (o.logits && o.logits != logits)
     for (int64_t i = threadIdx.x; i < (int64_t)rows * a.E; i += blockDim.x) o.logits[t0 * a.E + i] = src[i];
   const float* lg = src + (int64_t)threadIdx.x * a.E;
-  if (a.E >= 32) {
+  if (a.E >= 32 || a.bias) {
     const int ld = a.E + 1, n = rows * a.E;
     if ((a.E & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
       constexpr int U = 8;  // 16-B loads in flight per thread before the shared stores
@@ -486,6 +499,15 @@ __global__ void __launch_bounds__(RT) route_from_logits_kernel(const float* __re
       }
     }
     lg = s_rows + threadIdx.x * ld;
+    if (a.bias) {  // logits-bias mode: the staged rows get the bias, and the workspace the sum
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += RT) {
+        const int r = i / a.E, c = i - r * a.E;
+        const float v = s_rows[r * ld + c] + __ldg(a.bias + t0 * a.E + i);
+        s_rows[r * ld + c] = v;
+        if (o.logits) o.logits[t0 * a.E + i] = v;
+      }
+    }
   }
   load_route_state(st, a);  // its barriers also publish s_rows
   if (threadIdx.x < rows) route_one_token(lg, t0 + threadIdx.x, a, o, st);
@@ -529,10 +551,13 @@ void launch_gate_route(const void* x, const void* wg, int dtype, const RouteArgs
     const int nbx = (int)ceil_div(a.T, 8);
     const int ny = std::max(1, std::min((2 * 148 + nbx - 1) / nbx, (a.E + 1) / 2));  // >= 2 experts per warp
     gate_logits_f32_kernel<<<dim3(nbx, ny), 256, 0, s>>>(static_cast<const float*>(x),
-                                                          static_cast<const float*>(wg), a.T, a.d, a.E, o.logits);
+                                                          static_cast<const float*>(wg), a.T, a.d, a.E, o.logits,
+                                                          a.bias);
     EMOE_CUDA(cudaGetLastError());
     count_launch();
-    launch_route_from_logits(o.logits, a, o, s);
+    RouteArgs ra = a;
+    ra.bias = nullptr;  // already in the logits
+    launch_route_from_logits(o.logits, ra, o, s);
     return;
   } else if (dtype == DT_F32) {
     const size_t smem = (size_t)RT * a.E * sizeof(float);
@@ -571,7 +596,7 @@ void launch_route_from_logits(const float* logits, const RouteArgs& a, const Rou
   EMOE_REQUIRE(a.k >= 1 && a.k <= 8 && a.k <= a.E, "route: top_k must be in [1, min(8, E)]");
   const int nblocks = (int)ceil_div(a.T, RT);
   if (nblocks == 0) return;
-  const int smem = a.E >= 32 ? RT * (a.E + 1) * (int)sizeof(float) : 0;
+  const int smem = a.E >= 32 || a.bias ? RT * (a.E + 1) * (int)sizeof(float) : 0;
   if (smem > 48 * 1024) ensure_max_dynamic_smem(reinterpret_cast<const void*>(route_from_logits_kernel), smem);
   route_from_logits_kernel<<<nblocks, RT, smem, s>>>(logits, a, o);
   EMOE_CUDA(cudaGetLastError());

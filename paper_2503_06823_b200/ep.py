@@ -2,9 +2,10 @@
 
 Tokens are data-parallel: every rank routes its own tokens against the GLOBAL
 resident set (the reference Placement, replicated), while the resident experts'
-weights are sharded across ranks.  When there are fewer resident experts than
-ranks (e.g. 4 resident Mixtral experts on 8 GPUs) groups of L ranks each hold a
-full replica of the resident set and source ranks are spread over the groups.
+weights are spread over the ranks by plan_shares: each expert runs on a run of
+consecutive ranks with a fixed share of its rows (token-level split), so a hot
+expert occupies several GPUs and light ones share one (e.g. 4 resident
+Mixtral experts on 8 GPUs: two ranks per expert, half its rows each).
 
 One step on every rank:
   1. route + permute locally (K1 + K3): padded per-expert segments of x
@@ -12,6 +13,7 @@ One step on every rank:
   3. dispatch all-to-all(v) of the padded segments, chunks ordered by
      (source rank, expert, token)
   4. grouped FFN (K4) on the received segments, one segment per (source, expert)
+     piece
   5. return all-to-all(v) of the expert outputs into the source's layout
   6. combine at the source in slot order (K5)
 Each row's FFN is the same kernel with the same weights wherever it runs, and
@@ -40,51 +42,144 @@ import torch
 import torch.distributed as dist
 
 
-def plan_destinations(resident: Sequence[int], num_experts: int, world: int, loads=None) -> np.ndarray:
-    """dest[src, e] = rank that computes source `src`'s rows of resident expert e
-    (-1 for non-resident experts).  Monotone in e for every source, so each
-    source's permuted buffer is already grouped by destination (the NCCL
-    transport sends contiguous chunks).
+SHARE_ONE = 1 << 24  # fixed-point unit of the cumulative shares (emoe_ep_create)
 
-    loads None: resident experts in contiguous equal-count blocks (L >= W), or
-    W // L full replicas of the resident set with sources spread over them
-    (L < W).  loads[e] (e.g. the ranks' summed Eq. 2 expected tokens): the
-    busiest rank is what an FFN-bound EP step waits for, so the resident
-    experts' loads are laid end to end on [0, W) in expert order and cut into
-    W unit intervals (one per rank); source s sends its rows of e to the rank
-    under the point c_e + (s + 1/2) w_e / W of e's interval [c_e, c_e + w_e).
-    A heavy expert is thereby replicated over the ranks its interval covers
-    and light neighbours share a rank; the points are non-decreasing in e, so
-    the plan stays monotone (tools/ep_balance_model.py on the config-2
-    routing: 0.49 -> 0.79 of W GPUs' FFN throughput at W = 8)."""
+
+def plan_shares(resident: Sequence[int], num_experts: int, world: int, loads=None,
+                min_share: float = 0.05) -> np.ndarray:
+    """cum[e][q] (int64 [E][W], fixed point SHARE_ONE = 1): the cumulative
+    share of resident expert e's rows computed on ranks <= q; -1 rows for
+    experts that are not resident.
+
+    The busiest rank is what an FFN-bound EP step waits for, so the resident
+    experts' expected loads (loads[e], e.g. the predictor's Eq. 2 aggregate,
+    identical on every rank; None = equal) are laid end to end on [0, W) in
+    expert order and cut into W unit intervals, one per rank: expert e runs on
+    the ranks its interval [c_e, c_e + w_e) covers, each with the covered
+    fraction.  Every forward then splits e's rows (all sources, in source
+    order) at those fractions rounded to the segment padding (ep.cu bar0,
+    restated in p2p_layout), so a hot expert is shared token by token and a
+    light one shares a rank with its neighbours.  A rank's share of an expert
+    below `min_share` of a rank's capacity moves to the expert's neighbouring
+    rank (one expert copy fewer for at most that much imbalance).  Ranks of
+    consecutive experts are non-decreasing, so each source's permuted buffer
+    is already grouped by destination (the NCCL transport sends contiguous
+    chunks)."""
     res = sorted(int(e) for e in resident)
-    L = len(res)
-    dest = np.full((world, num_experts), -1, np.int64)
-    if L == 0:
-        return dest
-    if loads is not None:
-        w = np.array([max(float(loads[e]), 0.0) for e in res])
-        if w.sum() > 0:
-            w = w / w.sum() * world
-            c = np.concatenate([[0.0], np.cumsum(w)])
-            for src in range(world):
-                for i, e in enumerate(res):
-                    p = c[i] + (src + 0.5) * w[i] / world
-                    dest[src, e] = min(world - 1, int(np.floor(p)))
-            return dest
-    if L >= world:
-        for i, e in enumerate(res):  # contiguous blocks of resident experts per rank
-            dest[:, e] = i * world // L
-        return dest
-    groups = world // L  # full replicas of the resident set
-    for src in range(world):
-        g = src % groups
-        for i, e in enumerate(res):
-            dest[src, e] = g * L + i
-    return dest
+    cum = np.full((num_experts, world), -1, np.int64)
+    if not res:
+        return cum
+    w = np.ones(len(res)) if loads is None else np.array([max(float(loads[e]), 0.0) for e in res])
+    if w.sum() <= 0:
+        w = np.ones(len(res))
+    w = w / w.sum() * world
+    c = np.concatenate([[0.0], np.cumsum(w)])
+    for i, e in enumerate(res):
+        amt = np.array([max(0.0, min(q + 1.0, c[i] + w[i]) - max(float(q), c[i])) for q in range(world)])
+        if amt.sum() <= 0:  # zero expected load: the rank under its (point) interval takes it
+            amt[min(world - 1, int(np.floor(c[i])))] = 1.0
+        nz = np.flatnonzero(amt > 0)
+        while len(nz) > 1 and amt[nz[0]] < min_share:  # tiny head share -> next rank
+            amt[nz[1]] += amt[nz[0]]
+            amt[nz[0]] = 0.0
+            nz = nz[1:]
+        while len(nz) > 1 and amt[nz[-1]] < min_share:  # tiny tail share -> previous rank
+            amt[nz[-2]] += amt[nz[-1]]
+            amt[nz[-1]] = 0.0
+            nz = nz[:-1]
+        frac = np.cumsum(amt) / amt.sum()
+        row = np.minimum(np.round(frac * SHARE_ONE).astype(np.int64), SHARE_ONE)
+        row[nz[-1]:] = SHARE_ONE
+        cum[e] = np.maximum.accumulate(row)
+    return cum
 
-def owned_experts(dest: np.ndarray, rank: int) -> list:
-    return sorted({int(e) for e in np.flatnonzero((dest == rank).any(axis=0))})
+
+def owned_experts(cum: np.ndarray, rank: int) -> list:
+    """Experts with a non-zero share on `rank` (the weights it must hold)."""
+    out = []
+    for e in range(cum.shape[0]):
+        if cum[e, 0] < 0:
+            continue
+        prev = cum[e, rank - 1] if rank > 0 else 0
+        if cum[e, rank] > prev:
+            out.append(e)
+    return out
+
+
+def split_bounds(counts: np.ndarray, cum: np.ndarray, pad: int):
+    """The per-forward split every rank derives from the replicated count table
+    (ep.cu ep_bar0_kernel): counts[s][e] real rows of source s.
+    Returns (cp, pre, bnd): padded counts [W][E], rows of e held by earlier
+    sources [W][E], and split ends B_e(q) [E][W] (rank q computes e's rows
+    [B_e(q-1), B_e(q)) of the source-ordered sequence)."""
+    W, E = counts.shape
+    cp = (counts.astype(np.int64) + pad - 1) // pad * pad
+    pre = np.zeros((W, E), np.int64)
+    pre[1:] = np.cumsum(cp, axis=0)[:-1]
+    n = cp.sum(axis=0)
+    bnd = np.zeros((E, W), np.int64)
+    for e in range(E):
+        for q in range(W):
+            cq = int(cum[e, q])
+            if q == W - 1 or cq < 0:
+                b = int(n[e])
+            else:
+                b = pad * ((int(n[e]) // pad * cq + (SHARE_ONE >> 1)) >> 24)
+            bnd[e, q] = min(b, int(n[e]))
+    return cp, pre, bnd
+
+
+def p2p_layout(counts: np.ndarray, cum: np.ndarray, rank: int, pad: int) -> dict:
+    """Everything ep_bar0_kernel computes on rank `rank` (csrc/ep.cu), restated.
+    counts[s][e] = real rows source s routes to expert e.
+      piece_end[e][q], piece_shift[e][q]: this rank's local rows
+          [piece_end[e][q-1], piece_end[e][q]) of segment e go to rank q at
+          receive row (local row + piece_shift[e][q]);
+      recv_segs [W*n_owned+1], seg_expert, seg_src, out_shift: the receive
+          segments (source, owned expert) in order, receive row r of segment i
+          returning to row r + out_shift[i] of source seg_src[i]'s layout;
+      tot[s][q]: rows source s sends rank q; seg_offsets: this rank's padded
+          local segment starts [E+1]."""
+    W, E = counts.shape
+    cp, pre, bnd = split_bounds(counts, cum, pad)
+    loc = np.zeros((W, E + 1), np.int64)
+    loc[:, 1:] = np.cumsum(cp, axis=1)
+
+    def piece(s, e, q):
+        p0, p1 = pre[s, e], pre[s, e] + cp[s, e]
+        lo = max(p0, bnd[e, q - 1] if q > 0 else 0)
+        hi = min(p1, bnd[e, q])
+        return lo, max(hi, lo)
+
+    tot = np.zeros((W, W), np.int64)
+    for s in range(W):
+        for q in range(W):
+            tot[s, q] = sum(piece(s, e, q)[1] - piece(s, e, q)[0] for e in range(E))
+    piece_end = np.zeros((E, W), np.int64)
+    piece_shift = np.zeros((E, W), np.int64)
+    for q in range(W):
+        recv_off = int(tot[:rank, q].sum())
+        for e in range(E):
+            lo, hi = piece(rank, e, q)
+            p0, seg = pre[rank, e], loc[rank, e]
+            end_g = min(max(bnd[e, q], p0), p0 + cp[rank, e])
+            piece_end[e, q] = seg + (end_g - p0)
+            piece_shift[e, q] = recv_off - seg - (lo - p0)
+            recv_off += hi - lo
+    owned = owned_experts(cum, rank)
+    segs, exp, src, out, off = [], [], [], [], 0
+    for s in range(W):
+        for e in owned:
+            lo, hi = piece(s, e, rank)
+            segs.append(off)
+            exp.append(e)
+            src.append(s)
+            out.append(int(loc[s, e] + (lo - pre[s, e]) - off))
+            off += hi - lo
+    segs.append(off)
+    return dict(piece_end=piece_end, piece_shift=piece_shift, recv_segs=np.asarray(segs, np.int64),
+                seg_expert=np.asarray(exp, np.int32), seg_src=np.asarray(src, np.int32),
+                out_shift=np.asarray(out, np.int64), tot=tot, seg_offsets=loc[rank])
 
 
 @dataclass
@@ -94,6 +189,7 @@ class RoutedBatch:
     pos: torch.Tensor        # [T, k]
     served_w: torch.Tensor   # [T, k]
     T: int
+    counts: Optional[np.ndarray] = None  # [E] real rows per expert
 
 
 class LayerBackend:
@@ -107,14 +203,15 @@ class LayerBackend:
         self.d, self.f, self.E = layer.d, layer.f, layer.E
         self.dtype = layer.torch_dtype
         self.device = torch.device("cuda", torch.cuda.current_device())
-        self._ws = None
+        self.layer.workspace()
+        self.pad = self.layer.seg_pad
 
     def route_permute(self, x: torch.Tensor) -> RoutedBatch:
         self.layer.route_permute(x)
         ws = self.layer.workspace()
-        self.pad = self.layer.seg_pad
         seg = ws["seg_offsets"].cpu().numpy()  # host needs the split sizes (syncs the stream)
-        return RoutedBatch(seg, ws["x_perm"][: int(seg[-1])], ws["pos"], ws["served_w"], x.shape[0])
+        return RoutedBatch(seg, ws["x_perm"][: int(seg[-1])], ws["pos"], ws["served_w"], x.shape[0],
+                           ws["counts"].cpu().numpy().astype(np.int64))
 
     def ffn(self, rows: torch.Tensor, seg_offsets: np.ndarray, seg_expert: np.ndarray) -> torch.Tensor:
         R = rows.shape[0]
@@ -134,19 +231,22 @@ class LayerBackend:
 
 
 class ExpertParallelMoE:
-    """EP forward over a process group; `backend` provides the local kernels."""
+    """EP forward over a process group with all-to-all collectives (the NCCL
+    transport); `backend` provides the local kernels.  Same split and receive
+    layout as the peer-memory path (p2p_layout), so the output is
+    bit-identical to it and to EP=1."""
 
     def __init__(self, backend, global_resident: Sequence[int], group=None, loads=None):
         self.backend = backend
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.dest = plan_destinations(global_resident, backend.E, self.world, loads)
+        self.cum = plan_shares(global_resident, backend.E, self.world, loads)
         self.stage_on_host = dist.get_backend(group) != "nccl"
         self.last = {}
 
     def owned(self) -> list:
-        return owned_experts(self.dest, self.rank)
+        return owned_experts(self.cum, self.rank)
 
     def _a2a(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits) -> torch.Tensor:
         if self.stage_on_host and inp.is_cuda:
@@ -161,94 +261,46 @@ class ExpertParallelMoE:
         b = self.backend
         E, W, r = b.E, self.world, self.rank
         batch = b.route_permute(x)
-        psz = np.diff(batch.seg_offsets)  # padded rows per expert
-        # rows this rank sends each destination, per expert
-        send_meta = np.zeros((W, E), np.int64)
-        for e in np.flatnonzero(psz):
-            q = self.dest[r, e]
-            if q < 0:
-                raise RuntimeError(f"expert {e} has rows but is not in the global resident set")
-            send_meta[q, e] = psz[e]
-        meta_out = torch.empty(W * E, dtype=torch.int64)
-        meta_in = torch.from_numpy(send_meta.reshape(-1)).clone()
+        counts = torch.from_numpy(np.ascontiguousarray(batch.counts, np.int64))
+        table = [torch.empty(E, dtype=torch.int64) for _ in range(W)]
         if self.stage_on_host:
-            dist.all_to_all_single(meta_out, meta_in, group=self.group)
+            dist.all_gather(table, counts, group=self.group)
         else:  # NCCL exchanges device tensors
             dev = torch.device("cuda", torch.cuda.current_device())
-            o = meta_out.to(dev)
-            dist.all_to_all_single(o, meta_in.to(dev), group=self.group)
-            meta_out.copy_(o.cpu())
-        recv_meta = meta_out.numpy().reshape(W, E)
-        send_rows = send_meta.sum(axis=1).tolist()
-        recv_rows = recv_meta.sum(axis=1).tolist()
+            t_dev = [torch.empty(E, dtype=torch.int64, device=dev) for _ in range(W)]
+            dist.all_gather(t_dev, counts.to(dev), group=self.group)
+            table = [t.cpu() for t in t_dev]
+        cnt = torch.stack(table).numpy()
+        lay = p2p_layout(cnt, self.cum, r, b.pad)
+        send_rows = lay["tot"][r].tolist()
+        recv_rows = lay["tot"][:, r].tolist()
         R = int(sum(recv_rows))
         recv = torch.empty(R, b.d, dtype=batch.rows.dtype, device=batch.rows.device)
         self._a2a(recv, batch.rows, recv_rows, send_rows)
-        # one segment per (source, expert), sources in rank order
-        seg_off, seg_exp, off = [0], [], 0
-        for src in range(W):
-            for e in range(E):
-                n = int(recv_meta[src, e])
-                if n:
-                    off += n
-                    seg_off.append(off)
-                    seg_exp.append(e)
-        y_recv = b.ffn(recv, np.asarray(seg_off, np.int64), np.asarray(seg_exp, np.int32))
+        y_recv = b.ffn(recv, lay["recv_segs"], lay["seg_expert"])
         y_back = torch.empty_like(batch.rows)
         self._a2a(y_back, y_recv, send_rows, recv_rows)
-        self.last = dict(send_rows=send_rows, recv_rows=recv_rows, segments=len(seg_exp))
+        self.last = dict(send_rows=send_rows, recv_rows=recv_rows, segments=len(lay["seg_expert"]))
         return b.combine(y_back, batch)
 
     __call__ = forward
 
 
-def p2p_layout(counts: np.ndarray, dest: np.ndarray, rank: int, seg_offsets: np.ndarray):
-    """The receive segments and send shifts ep_bar0_kernel computes on rank
-    `rank` (csrc/ep.cu).  counts[s, e] = padded rows source s holds for expert
-    e; seg_offsets = this rank's local padded segment starts [E+1].
-    Returns (recv_segs, seg_expert, row_shift, seg_src, out_shift): rank
-    `rank` receives segment i = (seg_src[i], seg_expert[i]) at recv_segs[i]
-    in (source, expert) order and pushes its outputs back to row r +
-    out_shift[i] of the source's own permuted layout; it writes its own
-    segment e to row seg_offsets[e] + row_shift[e] of rank dest[rank, e]'s
-    receive buffer."""
-    W, E = dest.shape
-    owned = owned_experts(dest, rank)
-    tot = np.zeros((W, W), np.int64)  # [source][receiver]
-    for s in range(W):
-        for e in range(E):
-            if dest[s, e] >= 0:
-                tot[s, dest[s, e]] += counts[s, e]
-    shift = np.zeros(E, np.int64)
-    for e in range(E):
-        q = dest[rank, e]
-        if q < 0:
-            continue
-        base = tot[:rank, q].sum() + sum(counts[rank, e2] for e2 in range(e) if dest[rank, e2] == q)
-        shift[e] = base - seg_offsets[e]
-    segs, exp, src, out, off = [], [], [], [], 0
-    for s in range(W):
-        for e in owned:
-            segs.append(off)
-            exp.append(e)
-            src.append(s)
-            out.append(int(counts[s, :e].sum()) - off)  # source s's padded segment e starts at its count prefix
-            if dest[s, e] == rank:
-                off += counts[s, e]
-    segs.append(off)
-    return (np.asarray(segs, np.int64), np.asarray(exp, np.int32), shift, np.asarray(src, np.int32),
-            np.asarray(out, np.int64))
+STAGES = ["route", "count_exchange", "dispatch", "dispatch_wait", "gemm1", "gemm2_return", "return_wait", "combine"]
 
 
 class PeerExpertParallelMoE:
     """Expert parallelism over peer memory through the C ABI (emoe_ep_*).
 
-    `layer` is this rank's MoELayer holding the experts it computes; the
-    group only carries the IPC-handle exchange at construction (gloo or
-    NCCL) -- the forward itself uses no collective.  `loads` (identical on
-    every rank) selects the load-aware placement of plan_destinations."""
+    `layer` is this rank's MoELayer holding the experts it computes
+    (owned_experts of plan_shares(...)); the group only carries the
+    IPC-handle exchange at construction (gloo or NCCL) -- the forward itself
+    uses no collective.  `loads` (identical on every rank) weights the
+    placement.  `share_with`: another PeerExpertParallelMoE of this rank
+    (a stack's first layer) whose symmetric region this one reuses."""
 
-    def __init__(self, layer, global_resident: Sequence[int], group=None, recv_rows_cap: int = 0, loads=None):
+    def __init__(self, layer, global_resident: Sequence[int], group=None, recv_rows_cap: int = 0, loads=None,
+                 share_with: Optional["PeerExpertParallelMoE"] = None, min_share: float = 0.05):
         import ctypes as C
 
         from ._lib import IPC_HANDLE_BYTES, lib
@@ -260,46 +312,82 @@ class PeerExpertParallelMoE:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.E = layer.E
-        self.dest = plan_destinations(global_resident, layer.E, self.world, loads)
+        self.cum = plan_shares(global_resident, layer.E, self.world, loads, min_share)
         res = np.zeros(layer.E, np.uint8)
         res[list(global_resident)] = 1
         layer.set_route_residency(res)
-        dest32 = np.ascontiguousarray(self.dest, np.int32)
+        cum = np.ascontiguousarray(self.cum, np.int64)
         h = C.c_void_p()
-        check(lib.emoe_ep_create(layer.h, self.world, self.rank, dest32.ctypes.data_as(C.c_void_p),
-                                 int(recv_rows_cap), C.byref(h)))
+        check(lib.emoe_ep_create(layer.h, self.world, self.rank, cum.ctypes.data_as(C.c_void_p), int(recv_rows_cap),
+                                 share_with.h if share_with is not None else None, C.byref(h)))
         self.h = h
-        buf = (C.c_uint8 * IPC_HANDLE_BYTES)()
-        check(lib.emoe_ep_ipc_handle(h, buf))
-        handles = [None] * self.world
-        dist.all_gather_object(handles, bytes(buf), group=group)
-        allh = np.frombuffer(b"".join(handles), np.uint8).copy()
-        check(lib.emoe_ep_open_peers(h, allh.ctypes.data_as(C.c_void_p)))
-        dist.barrier(group=group)  # every rank mapped every peer before the first forward
+        self._share = share_with  # keeps the region owner alive
+        if share_with is None:
+            buf = (C.c_uint8 * IPC_HANDLE_BYTES)()
+            check(lib.emoe_ep_ipc_handle(h, buf))
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(buf), group=group)
+            allh = np.frombuffer(b"".join(handles), np.uint8).copy()
+            check(lib.emoe_ep_open_peers(h, allh.ctypes.data_as(C.c_void_p)))
+            dist.barrier(group=group)  # every rank mapped every peer before the first forward
 
     def owned(self) -> list:
-        return owned_experts(self.dest, self.rank)
+        return owned_experts(self.cum, self.rank)
 
-    def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, logits: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                stream=None) -> torch.Tensor:
         C = self._C
-        assert x.is_cuda and x.dtype == torch.bfloat16 and x.shape[1] == self.layer.d
-        x = x.contiguous()
-        y = torch.empty_like(x)
+        assert x.is_cuda and x.dtype == torch.bfloat16 and x.shape[1] == self.layer.d and x.is_contiguous()
+        y = torch.empty_like(x) if out is None else out
+        lp = None
+        if logits is not None:
+            assert logits.is_cuda and logits.dtype == torch.float32 and logits.shape == (x.shape[0], self.E)
+            lp = C.c_void_p(logits.contiguous().data_ptr())
         s = stream if stream is not None else torch.cuda.current_stream()
-        self._check(self._lib.emoe_ep_forward(self.h, C.c_void_p(x.data_ptr()), None, C.c_void_p(y.data_ptr()),
+        self._check(self._lib.emoe_ep_forward(self.h, C.c_void_p(x.data_ptr()), lp, C.c_void_p(y.data_ptr()),
                                               x.shape[0], C.c_void_p(s.cuda_stream)))
         return y
 
     __call__ = forward
 
     def status(self, stream=None):
-        """(status, rows received last forward); synchronises the stream.
+        """(status, rows computed last forward); synchronises the stream.
         status 1 = a peer barrier timed out, 2 = a receive buffer overflowed."""
         C = self._C
         s = stream if stream is not None else torch.cuda.current_stream()
         st, rr = C.c_int(), C.c_int64()
         self._check(self._lib.emoe_ep_status(self.h, C.c_void_p(s.cuda_stream), C.byref(st), C.byref(rr)))
         return st.value, rr.value
+
+    def stats(self, stream=None) -> dict:
+        """Exchange volume of the last forward (synchronises the stream)."""
+        C = self._C
+        s = stream if stream is not None else torch.cuda.current_stream()
+        out = np.zeros(5, np.int64)
+        self._check(self._lib.emoe_ep_stats(self.h, C.c_void_p(s.cuda_stream), out.ctypes.data_as(C.c_void_p)))
+        row = self.layer.d * 2
+        return dict(rows_computed=int(out[0]), rows_sent_to_peers=int(out[1]), rows_recv_from_peers=int(out[2]),
+                    rows_routed=int(out[3]), rows_computed_real=int(out[4]), dispatch_bytes_to_peers=int(out[1]) * row,
+                    return_bytes_to_peers=int(out[2]) * row)
+
+    def layout(self, stream=None) -> dict:
+        """The last forward's send pieces and receive layout (tests)."""
+        C = self._C
+        s = stream if stream is not None else torch.cuda.current_stream()
+        W, E, n = self.world, self.E, len(self.owned())
+        pe, ps = np.zeros((E, W), np.int64), np.zeros((E, W), np.int64)
+        rs, osh = np.zeros(W * n + 1, np.int64), np.zeros(max(1, W * n), np.int64)
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._check(self._lib.emoe_ep_layout(self.h, C.c_void_p(s.cuda_stream), p(pe), p(ps), p(rs), p(osh)))
+        return dict(piece_end=pe, piece_shift=ps, recv_segs=rs, out_shift=osh[: W * n])
+
+    def set_profiling(self, enable: bool = True) -> None:
+        self._check(self._lib.emoe_ep_set_profiling(self.h, int(enable)))
+
+    def stage_times(self) -> dict:
+        ms = (self._C.c_float * 8)()
+        self._check(self._lib.emoe_ep_stage_times(self.h, ms))
+        return dict(zip(STAGES, [float(v) for v in ms]))
 
     def close(self):
         if getattr(self, "h", None):

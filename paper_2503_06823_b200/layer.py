@@ -110,6 +110,12 @@ class MoELayer:
         assert s.shape == (self.E,), f"scores must have {self.E} entries"
         check(lib.emoe_layer_set_scores(self.h, s.ctypes.data_as(C.c_void_p), _stream_ptr(stream)))
 
+    def set_logits_mode(self, mode: str) -> None:
+        """"replace": caller logits replace the gate (routing-driven parity mode,
+        default); "add": the gate runs on x and the caller logits are added
+        to its logits before top-k."""
+        check(lib.emoe_layer_set_logits_mode(self.h, {"replace": 0, "add": 1}[mode]))
+
     # -- residency (two-phase, engine.cpp:431-464) ------------------------
     def begin_load(self, evictions: Sequence[int], loads: Sequence[int], stream=None) -> None:
         ev = np.ascontiguousarray(np.asarray(list(evictions) or [0], np.int32))

@@ -38,6 +38,21 @@ def test_reference_arm_contract():
     assert d["config"]["tokens_per_step"] <= 512 and "of the 1x512 = 512 tokens" in cb["sample"]
 
 
+def test_multi_gpu_default_is_expert_parallel():
+    """bench.py --gpus N under torchrun measures the north star's EP split by
+    default (the driver's SCALE run passes no --parallel)."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    for argv in ([], ["--config", "stack"]):
+        a = bench.build_parser().parse_args(argv)
+        assert a.parallel == "ep" and a.ep_transport == "p2p"
+        for n in (2, 4, 8):
+            assert bench.parallelism_label(n, a.parallel, a.ep_transport) == f"ep{n}-p2p"
+    assert bench.parallelism_label(1, "ep", "p2p") == "single"
+    assert bench.parallelism_label(4, "replicas", "p2p") == "replicas4"
+
+
 def test_reference_arm_is_independent_of_the_product():
     """--impl reference runs the reference's code and the oracle only: the
     product package is never imported and libemoe.so never mapped."""

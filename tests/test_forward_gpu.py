@@ -29,13 +29,16 @@ CASES = {
     "config1_fp32_phi05": (8, 1024, 3584, 2, "fp32", "swiglu", "topk_softmax", 4, [0, 2, 5, 7], 512, 0),
     "config1_fp32_phi1": (8, 1024, 3584, 2, "fp32", "swiglu", "topk_softmax", 8, None, 512, 0),
     "fp32_relu_top1": (16, 256, 512, 1, "fp32", "relu", "full_softmax", 8, [0, 2, 5, 7, 9, 11, 13, 15], 500, 0),
+    # T >= 74 route blocks: the fused fp32 gate+route kernel (smaller T computes logits first)
+    "fp32_many_tokens": (8, 256, 512, 2, "fp32", "swiglu", "topk_softmax", 4, [0, 2, 5, 7], 9600, 0),
 }
 
 
-def run_case(name, port, use_trace_logits=False, scores=None):
+def run_case(name, port, use_trace_logits=False, scores=None, logits_mode="replace"):
     E, d, f, k, dtype, act, wm, slots, resident, T, cg = CASES[name]
     layer, wg, experts = build_layer(E, d, f, k, dtype, act, wm, slots, resident, max_tokens=max(T, 128),
                                      gemm_cta_group=cg)
+    layer.set_logits_mode(logits_mode)
     if scores is not None:
         layer.set_scores(scores)
     g = torch.Generator().manual_seed(7)
@@ -47,12 +50,14 @@ def run_case(name, port, use_trace_logits=False, scores=None):
         crng = np.random.default_rng(3)
         choices = np.stack([crng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
         logits_in = torch.from_numpy(trace_logits(choices, E)).cuda()
+        if logits_mode == "add":  # a bias that dominates the gate's own logits (~N(0, 1))
+            logits_in = logits_in * 16
     y = layer.forward(xd, logits=logits_in)
     torch.cuda.synchronize()
     ws = {key: (None if v is None else v.clone()) for key, v in layer.workspace().items()}
     res = layer.residency()
     return dict(layer=layer, wg=wg, experts=experts, x=x, y=y, ws=ws, resident=res, T=T, E=E, d=d, f=f, k=k,
-                dtype=dtype, act=act, wm=wm, logits_in=logits_in)
+                dtype=dtype, act=act, wm=wm, logits_in=logits_in, logits_mode=logits_mode)
 
 
 def check_case(c, port, scores=None):
@@ -61,8 +66,10 @@ def check_case(c, port, scores=None):
     x32 = to_f32(c["x"])
     lg = to_f32(ws["logits"])
     # A1 logits
-    if c["logits_in"] is None:
+    if c["logits_in"] is None or c.get("logits_mode") == "add":
         ref_lg = port.gate_logits(x32, to_f32(c["wg"]))
+        if c["logits_in"] is not None:  # logits-bias mode: the gate's logits + the caller's
+            ref_lg = (ref_lg + to_f32(c["logits_in"])).astype(np.float32)
         err = np.abs(lg - ref_lg).max() / max(np.abs(ref_lg).max(), 1e-30)
         assert err < 1e-4, f"gate logits rel err {err:.3e}"
     else:
@@ -147,6 +154,22 @@ def test_forward_trace_logits_and_fallback_scores(port):
     c = run_case("mixtral_small", port, use_trace_logits=True, scores=scores)
     check_case(c, port, scores=scores)
     assert (c["ws"]["route_rank"].cpu().numpy() == -1).any(), "case should exercise the fallback path"
+    c["layer"].close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["mixtral_small", "switch_small", "config1_fp32_phi05", "fp32_relu_top1",
+                                  "fp32_many_tokens"])
+def test_forward_logits_bias_mode(name, port):
+    """EMOE_LOGITS_ADD: the gate runs on x (every gate kernel: mma.sync E < 32,
+    tcgen05 GEMM + route E >= 32, fp32 fused and logits-first) and the caller's
+    logits are added before top-k; the trace bias dominates, so routing follows
+    it while the gate's arithmetic is real."""
+    c = run_case(name, port, use_trace_logits=True, logits_mode="add")
+    check_case(c, port)
+    E, k = c["E"], c["k"]
+    choices = np.argsort(-to_f32(c["logits_in"]), axis=1, kind="stable")[:, :k]
+    assert np.array_equal(c["ws"]["topk_idx"].cpu().numpy(), choices), "the bias should decide the routing"
     c["layer"].close()
 
 
