@@ -251,6 +251,10 @@ def build_workload(cfg, device, cta_group=0, rank=0, world=1, parallel="replicas
     layer = MoELayer(d, f, E, k, activation=cfg["act"], dtype=cfg.get("dtype", "bf16"), weight_mode=cfg["wm"],
                      num_slots=max(1, len(loads)), max_tokens=T, gemm_cta_group=cta_group)
     layer.set_gate(wg64.to(td))
+    # the fused tcgen05 gate (E >= 32) routes from its accumulators; the fp32
+    # logits are a parity/debug output, not consumed downstream
+    # (tests/test_forward_gpu.py::test_fused_gate_route_bit_identical: identical routing)
+    layer.set_keep_logits(False)
     experts = {}
     for e in range(E):
         w1, w3, w2 = input_expert(cfg, e)

@@ -108,6 +108,12 @@ int emoe_layer_set_copy_stream(emoe_layer* layer, void* stream);
  *   EMOE_LOGITS_ADD  the gate runs on x and logits_in [T][E] fp32 is added to
  *       its fp32 logits before top-k (a serving trace imposed as a bias on a
  *       real gate computation); the workspace logits hold the sum. */
+/* keep != 0 (default): a forward that computes the gate also stores the fp32
+ * logits [T][E] in the workspace (emoe_layer_workspace().logits).  0: the
+ * fused tcgen05 gate (E >= 32) routes from its accumulators and skips that
+ * store (33.5 MB at the Switch shape); routing outputs are identical. */
+int emoe_layer_set_keep_logits(emoe_layer* layer, int keep);
+
 #define EMOE_LOGITS_REPLACE 0
 #define EMOE_LOGITS_ADD 1
 int emoe_layer_set_logits_mode(emoe_layer* layer, int mode);

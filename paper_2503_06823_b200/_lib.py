@@ -56,7 +56,8 @@ _decl("emoe_layer_set_gate_host", vp, vp)
 _decl("emoe_layer_register_expert_host", vp, C.c_int, vp, vp, vp)
 _decl("emoe_layer_set_scores_host", vp, vp)
 _decl("emoe_layer_set_scores", vp, vp, vp)
-_decl("emoe_layer_set_logits_mode", vp, C.c_int)
+_decl("emoe_layer_set_logits_mode", "emoe_layer_set_keep_logits", vp, C.c_int)
+_decl("emoe_layer_set_keep_logits", vp, C.c_int)
 _decl("emoe_layer_register_expert_pinned", vp, C.c_int, vp, vp, vp)
 _decl("emoe_layer_set_copy_stream", vp, vp)
 _decl("emoe_layer_begin_load", vp, vp, C.c_int, vp, C.c_int, vp)
@@ -116,7 +117,7 @@ _decl("emoe_gen_routing_trace", C.c_int, C.c_int, C.c_int, dbl, dbl, C.c_int, C.
 EXPORTED = [
     "emoe_last_error", "emoe_version", "emoe_route_tokens_host", "emoe_layer_create", "emoe_layer_destroy",
     "emoe_layer_set_gate_host", "emoe_layer_register_expert_host", "emoe_layer_register_expert_pinned",
-    "emoe_layer_set_copy_stream", "emoe_layer_set_scores_host", "emoe_layer_set_scores", "emoe_layer_set_logits_mode",
+    "emoe_layer_set_copy_stream", "emoe_layer_set_scores_host", "emoe_layer_set_scores", "emoe_layer_set_logits_mode", "emoe_layer_set_keep_logits",
     "emoe_layer_begin_load", "emoe_layer_poll_loads", "emoe_layer_residency", "emoe_layer_last_load_stats",
     "emoe_moe_forward", "emoe_moe_forward_host", "emoe_moe_forward_host_async", "emoe_layer_wait_host", "emoe_route", "emoe_layer_gate_demand", "emoe_route_permute", "emoe_layer_set_route_residency",
     "emoe_ffn_segments", "emoe_combine", "emoe_ep_create", "emoe_ep_ipc_handle", "emoe_ep_open_peers",

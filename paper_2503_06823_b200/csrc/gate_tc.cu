@@ -1,0 +1,466 @@
+// K1 for many experts (E in {32, 64, 96, 128}, bf16): the gate GEMM on
+// tcgen05 with the routing fused into its epilogue, so x is read once and
+// the fp32 logits never round-trip through HBM.
+//
+// Tile = 128 tokens x all E experts (UMMA M=128, N=E, K=16 per instruction,
+// fp32 accumulators in TMEM).  TMEM lane = token: after the accumulator is
+// read (tcgen05.ld 32x32b), every epilogue thread holds its token's whole
+// logits row in registers and routes it exactly as the per-thread reference
+// restatement does (route.cu route_one_token + route_tail: top-k descending
+// with ascending index on ties, route_token remap, served set and weights,
+// with the same operation order, so results are bit-identical to routing the
+// stored logits).
+//
+// Hardware mapping (persistent, one CTA per SM, clusters of CN CTAs):
+//   warp 0      TMA producer: its own 128 x 64 x-tile per k-block, plus a
+//               1/CN slice of the gate's k-block multicast to every CTA of
+//               the cluster (the gate is the same for every tile, so a
+//               cluster shares each B k-block: L2 -> SM traffic for W_g drops
+//               CN-fold; at E = 128 the gate's reads would otherwise equal x's)
+//   warp 1      MMA issuer: tcgen05.mma.cta_group::1 per k-block, commit
+//               multicast to the stage's empty barrier of every cluster CTA
+//               (a stage is refilled only when all CN CTAs consumed it)
+//   warps 2..5  epilogue: TMEM double-buffered (2 x E columns) so tile i is
+//               routed while tile i+1's loads and MMAs run; per-tile expert
+//               counts in shared memory for the permutation (block_counts)
+// Every CTA of a cluster walks the same number of tiles (a CTA past the end
+// computes a zero-filled tile and stores nothing) so the multicast ring stays
+// in lockstep.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace emoe {
+namespace gatetc {
+
+constexpr int BK = 64;  // one 128-byte swizzle row of bf16
+constexpr int STAGES = 4;
+constexpr int NUM_THREADS = 192;
+constexpr int A_BYTES = 128 * BK * 2;
+
+struct Params {
+  RouteArgs a;
+  RouteOut o;
+  int64_t ntiles;
+  int k_blocks;
+  int store_logits;
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mcast(const CUtensorMap* desc, uint64_t* bar, void* smem_dst, int32_t c0,
+                                                  int32_t c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_mcast(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void epi_sync() {  // the 4 epilogue warps only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+struct RouteState {
+  uint8_t resident[128];
+  int counts[128];
+  int n_res;
+  int fallback;
+};
+
+template <int NE>
+__device__ __forceinline__ float pick(const float (&v)[NE], int idx) {
+  float r = 0.0f;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) r = e == idx ? v[e] : r;
+  return r;
+}
+
+// One token from its logits row in registers: the operations of
+// route_one_token + route_tail (route.cu) in the same order.
+template <int NE>
+__device__ __forceinline__ void route_row(const float (&v)[NE], int64_t t, const Params& p, RouteState& st) {
+  const RouteArgs& a = p.a;
+  const RouteOut& o = p.o;
+  const int k = a.k;
+  int ti[8];
+  uint32_t used[NE / 32];
+#pragma unroll
+  for (int c = 0; c < NE / 32; ++c) used[c] = 0;
+  {
+    int best = 0;
+    float bv = v[0];
+#pragma unroll
+    for (int e = 1; e < NE; ++e)
+      if (v[e] > bv) {
+        best = e;
+        bv = v[e];
+      }
+    ti[0] = best;
+#pragma unroll
+    for (int c = 0; c < NE / 32; ++c)
+      if ((best >> 5) == c) used[c] |= 1u << (best & 31);
+  }
+  for (int r = 1; r < k; ++r) {
+    int best = -1;
+    float bv = 0.0f;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      if (used[e >> 5] & (1u << (e & 31))) continue;
+      if (best < 0 || v[e] > bv) {
+        best = e;
+        bv = v[e];
+      }
+    }
+    ti[r] = best;
+#pragma unroll
+    for (int c = 0; c < NE / 32; ++c)
+      if ((best >> 5) == c) used[c] |= 1u << (best & 31);
+  }
+  if (o.topk_idx)
+    for (int r = 0; r < k; ++r) o.topk_idx[t * k + r] = ti[r];
+  // route_token remap (expert_store.cpp:206-220, engine.cpp:533-537)
+  int ex = -1, rk = -1, hit = 0;
+  if (st.n_res == 0) {
+    ex = ti[0];
+    if (!a.forced_miss) atomicExch(a.error_flag, 3);
+  } else {
+    for (int r = 0; r < k; ++r)
+      if (st.resident[ti[r]]) {
+        ex = ti[r];
+        rk = r;
+        hit = r == 0;
+        break;
+      }
+    if (rk < 0) ex = st.fallback;
+  }
+  if (o.route_expert) o.route_expert[t] = ex;
+  if (o.route_rank) o.route_rank[t] = rk;
+  if (o.route_hit) o.route_hit[t] = (uint8_t)hit;
+  int si[8];
+  int ns = 0;
+  if (st.n_res > 0) {
+    if (rk >= 0) {
+      for (int r = 0; r < k; ++r)
+        if (st.resident[ti[r]]) si[ns++] = ti[r];
+    } else {
+      si[ns++] = ex;
+    }
+  }
+  float w[8];
+  if (a.weight_mode == 0) {
+    if (ns > 0) {
+      const float mx = pick(v, si[0]);
+      float den = 0.0f;
+      for (int j = 0; j < ns; ++j) {
+        w[j] = expf(pick(v, si[j]) - mx);
+        den += w[j];
+      }
+      for (int j = 0; j < ns; ++j) w[j] = w[j] / den;
+    }
+  } else {
+    const float mx = pick(v, ti[0]);
+    float den = 0.0f;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) den += expf(v[e] - mx);
+    for (int j = 0; j < ns; ++j) w[j] = expf(pick(v, si[j]) - mx) / den;
+  }
+  for (int j = 0; j < k; ++j) {
+    o.served_idx[t * k + j] = j < ns ? si[j] : -1;
+    o.served_w[t * k + j] = j < ns ? w[j] : 0.0f;
+  }
+  for (int j = 0; j < ns; ++j) atomicAdd(&st.counts[si[j]], 1);
+}
+
+template <int NE, int CN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gate_route_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_g,
+                         Params p) {
+  constexpr int B_BYTES = NE * BK * 2;
+  constexpr int SLICE_ROWS = NE / CN;
+  constexpr int SLICE_BYTES = SLICE_ROWS * BK * 2;
+  constexpr int TMEM_COLS = 2 * NE <= 64 ? 64 : (2 * NE <= 128 ? 128 : 256);
+  constexpr uint16_t MASK = (uint16_t)((1u << CN) - 1u);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + STAGES * A_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_b + STAGES * B_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;  // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  __shared__ RouteState st;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = CN > 1 ? cluster_ctarank() : 0;
+  const int64_t cluster_id = blockIdx.x / CN, n_clusters = gridDim.x / CN;
+  // every CTA of a cluster walks the same number of tile slots
+  const int64_t n_iter = (ceil_div(p.ntiles, CN) + n_clusters - 1 - cluster_id) / n_clusters;
+
+  const RouteArgs& a = p.a;
+  const int E = a.E;
+  for (int e = threadIdx.x; e < E; e += NUM_THREADS) {
+    st.resident[e] = a.resident[e];
+    st.counts[e] = 0;
+  }
+  __syncthreads();
+  if (warp == 2) {  // resident count and the token-independent fallback (route.cu load_route_state)
+    int n = 0, first = -1, be = -1;
+    double bs = 0.0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      const bool r = e < E && st.resident[e];
+      const unsigned m = __ballot_sync(0xffffffffu, r);
+      n += __popc(m);
+      if (first < 0 && m) first = e0 + __ffs(m) - 1;
+      const double sc = r && a.scores ? a.scores[e] : 0.0;
+      if (r && (be < 0 || sc > bs)) {
+        bs = sc;
+        be = e;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double os = __shfl_xor_sync(0xffffffffu, bs, off);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+      if (oe >= 0 && (be < 0 || os > bs || (os == bs && oe < be))) {
+        bs = os;
+        be = oe;
+      }
+    }
+    if (lane == 0) {
+      st.n_res = n;
+      st.fallback = a.scores ? be : first;
+    }
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_x);
+    tma_prefetch_desc(&tmap_g);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], CN);  // one MMA commit from every CTA of the cluster
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  if (CN > 1)
+    cluster_sync_all();
+  else
+    __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t it = 0; it < n_iter; ++it) {
+        const int64_t tile = (cluster_id + it * n_clusters) * CN + rank;  // >= ntiles: zero-filled rows
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], A_BYTES + B_BYTES);
+          tma_load_2d(&tmap_x, &full_bar[stage], smem_a + stage * A_BYTES, kb * BK, (int32_t)(tile * 128),
+                      kCacheEvictFirst);
+          uint8_t* bdst = smem_b + stage * B_BYTES + rank * SLICE_BYTES;
+          if (CN > 1)
+            tma_load_2d_mcast(&tmap_g, &full_bar[stage], bdst, kb * BK, (int32_t)(rank * SLICE_ROWS), MASK);
+          else
+            tma_load_2d(&tmap_g, &full_bar[stage], bdst, kb * BK, 0, kCacheEvictLast);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      // tail: every peer's last commits to this CTA's empty barriers have landed
+      for (int i = 0; i < STAGES; ++i) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(128, NE);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t it = 0; it < n_iter; ++it) {
+        const int buf = (int)(it & 1);
+        mbar_wait(&tempty_bar[buf], (uint32_t)((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + buf * NE;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint64_t a_desc = umma_desc_sw128(smem_a + stage * A_BYTES);
+          const uint64_t b_desc = umma_desc_sw128(smem_b + stage * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16(tmem_d, a_desc + (uint64_t)(kk * 2), b_desc + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+          if (CN > 1)
+            umma_commit_mcast(&empty_bar[stage], MASK);
+          else
+            umma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull_bar[buf]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const RouteOut& o = p.o;
+    for (int64_t it = 0; it < n_iter; ++it) {
+      const int buf = (int)(it & 1);
+      const int64_t tile = (cluster_id + it * n_clusters) * CN + rank;
+      mbar_wait(&tfull_bar[buf], (uint32_t)((it >> 1) & 1));
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + buf * NE;
+      float v[NE];
+#pragma unroll
+      for (int c = 0; c < NE / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[c * 32 + j] = __uint_as_float(r[j]);
+      }
+      tc_fence_before();
+      if (lane == 0) mbar_arrive_relaxed(&tempty_bar[buf]);  // the MMAs of tile i+2 may start
+      if (tile < p.ntiles) {
+        const int64_t t = tile * 128 + quarter * 32 + lane;
+        if (t < a.T) {
+          if (a.bias) {
+            const float4* b4 = reinterpret_cast<const float4*>(a.bias + t * NE);
+#pragma unroll
+            for (int e = 0; e < NE; e += 4) {
+              const float4 bb = __ldg(b4 + e / 4);
+              v[e] += bb.x;
+              v[e + 1] += bb.y;
+              v[e + 2] += bb.z;
+              v[e + 3] += bb.w;
+            }
+          }
+          if (p.store_logits && o.logits) {
+            float4* dst = reinterpret_cast<float4*>(o.logits + t * NE);
+#pragma unroll
+            for (int e = 0; e < NE; e += 4) dst[e / 4] = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+          }
+          route_row<NE>(v, t, p, st);
+        }
+        epi_sync();  // every token of the tile counted
+        if (o.block_counts)
+          for (int e = threadIdx.x - 64; e < E; e += 128) {
+            o.block_counts[tile * E + e] = st.counts[e];
+            st.counts[e] = 0;
+          }
+        epi_sync();
+      }
+    }
+  }
+
+  if (CN > 1)
+    cluster_sync_all();
+  else
+    __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+template <int NE, int CN>
+void launch_one(const CUtensorMap& tx, const CUtensorMap& tg, const Params& p, int num_sms, cudaStream_t s) {
+  auto kernel = gate_route_tc_kernel<NE, CN>;
+  const int smem = 1024 + STAGES * (A_BYTES + NE * BK * 2) + 256;
+  ensure_max_dynamic_smem(reinterpret_cast<const void*>(kernel), smem);
+  const int grid = (int)std::min<int64_t>(num_sms / CN * CN, ceil_div(p.ntiles, CN) * CN);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CN;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  EMOE_CUDA(cudaLaunchKernelEx(&cfg, kernel, tx, tg, p));
+  EMOE_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+}  // namespace gatetc
+
+int gate_tc_cluster() {
+  static const int cn = [] {  // EMOE_GATE_CLUSTER: 1, 2 or 4 CTAs sharing the gate k-blocks (A/B runs)
+    const char* v = getenv("EMOE_GATE_CLUSTER");
+    const int c = v ? atoi(v) : 2;
+    return c == 1 || c == 4 ? c : 2;
+  }();
+  return cn;
+}
+
+void launch_gate_route_tc(const CUtensorMap& tmap_x, const CUtensorMap& tmap_gate_slice, const RouteArgs& a,
+                          const RouteOut& o, bool store_logits, int num_sms, cudaStream_t s) {
+  EMOE_REQUIRE(a.E >= 32 && a.E <= 128 && a.E % 32 == 0, "gate_tc: E must be 32, 64, 96 or 128");
+  EMOE_REQUIRE(a.d % gatetc::BK == 0, "gate_tc: d_model must be a multiple of 64");
+  EMOE_REQUIRE(a.k >= 1 && a.k <= 8 && a.k <= a.E, "gate_tc: top_k must be in [1, min(8, E)]");
+  gatetc::Params p;
+  p.a = a;
+  p.o = o;
+  p.ntiles = ceil_div(a.T, 128);
+  p.k_blocks = a.d / gatetc::BK;
+  p.store_logits = store_logits ? 1 : 0;
+  if (p.ntiles == 0) return;
+  const int cn = gate_tc_cluster();
+  switch (a.E) {
+#define EMOE_GATE_CASE(NEV)                                                    \
+  case NEV:                                                                    \
+    if (cn == 1)                                                               \
+      gatetc::launch_one<NEV, 1>(tmap_x, tmap_gate_slice, p, num_sms, s);      \
+    else if (cn == 2)                                                          \
+      gatetc::launch_one<NEV, 2>(tmap_x, tmap_gate_slice, p, num_sms, s);      \
+    else                                                                       \
+      gatetc::launch_one<NEV, 4>(tmap_x, tmap_gate_slice, p, num_sms, s);      \
+    break;
+    EMOE_GATE_CASE(32)
+    EMOE_GATE_CASE(64)
+    EMOE_GATE_CASE(96)
+    EMOE_GATE_CASE(128)
+#undef EMOE_GATE_CASE
+  }
+}
+
+}  // namespace emoe

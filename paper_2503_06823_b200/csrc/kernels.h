@@ -114,6 +114,14 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
                          const CUtensorMap* tmap_out = nullptr,  // null: direct st.global epilogue
                          const ScatterCombine* scatter = nullptr, const PeerOut* peer_out = nullptr);
 
+// K1 for many experts (E in {32, 64, 96, 128}, bf16): gate GEMM on tcgen05
+// with the routing fused into its epilogue (gate_tc.cu).  tmap_gate: W_g [E][d]
+// with box rows E / gate_tc_cluster() (each CTA of a cluster multicasts one
+// slice of every gate k-block).  store_logits: also write o.logits.
+int gate_tc_cluster();
+void launch_gate_route_tc(const CUtensorMap& tmap_x, const CUtensorMap& tmap_gate, const RouteArgs& a,
+                          const RouteOut& o, bool store_logits, int num_sms, cudaStream_t s);
+
 // K1 for many experts: the gate as one dense tcgen05 GEMM with fp32 output,
 // out[M][ldo] = A[M][K] . B[N_out][K]^T, columns >= col_limit (multiple of 32) not stored
 void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int K, int N_out, float* out,

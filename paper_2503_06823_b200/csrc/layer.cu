@@ -218,7 +218,16 @@ struct emoe_layer {
 
   // Gate on tcgen05 for E in {32, 64, 96, 128} (bf16): W_g zero-padded to 256 rows.
   void* wg_pad = nullptr;
-  CUtensorMap t_gate{}, t_gate2{};  // box 256 rows (1 CTA per MMA) / 128 rows (CTA pair)
+  CUtensorMap t_gate{}, t_gate2{};  // split path: box 256 rows (1 CTA per MMA) / 128 rows (CTA pair)
+  CUtensorMap t_gate_tc{};          // fused gate + route: box E / cluster rows
+  bool keep_logits = true;          // fused gate: also store the fp32 logits in the workspace
+  static bool split_gate() {
+    static const bool split = [] {
+      const char* v = getenv("EMOE_GATE_ROUTE");
+      return v && std::strcmp(v, "split") == 0;
+    }();
+    return split;
+  }
   bool tc_gate() const {
     return cfg.dtype == EMOE_DTYPE_BF16 && cfg.num_experts >= 32 && cfg.num_experts % 32 == 0 && wg_pad;
   }
@@ -258,9 +267,14 @@ struct emoe_layer {
     a.bias = add ? logits_in : nullptr;
     if (logits_in && !add) {
       launch_route_from_logits(logits_in, a, o, s);
+    } else if (tc_gate() && !split_gate()) {
+      // many experts: the gate is a real GEMM (T x d x E) on tcgen05 with the
+      // routing in its epilogue (x read once, no logits round trip)
+      const CUtensorMap tx = make_tmap_bf16_2d(x, (uint64_t)T, cfg.d_model, 128);
+      launch_gate_route_tc(tx, t_gate_tc, a, o, keep_logits, num_sms, s);
     } else if (tc_gate()) {
-      // many experts: the gate is a real GEMM (T x d x E); run it on tcgen05
-      // into the fp32 logits buffer, then route from the logits
+      // EMOE_GATE_ROUTE=split (A/B runs): the dense gate GEMM into the fp32
+      // logits buffer, then route from the logits
       const CUtensorMap tx = make_tmap_bf16_2d(x, (uint64_t)T, cfg.d_model, 128);
       static const int gate_cg = [] {  // EMOE_GATE_CG=2: the gate GEMM on CTA pairs (A/B runs)
         const char* v = getenv("EMOE_GATE_CG");
@@ -838,6 +852,7 @@ int emoe_layer_set_gate_host(emoe_layer* L, const void* wg) {
         // all 256 padded rows doubled the gate's operand bytes at E = 128)
         L->t_gate = make_tmap_bf16_2d(L->wg_pad, E, L->cfg.d_model, 256);
         L->t_gate2 = make_tmap_bf16_2d(L->wg_pad, E, L->cfg.d_model, 128);
+        if (E <= 128) L->t_gate_tc = make_tmap_bf16_2d(L->wg_pad, E, L->cfg.d_model, E / gate_tc_cluster());
       }
       EMOE_CUDA(cudaMemcpy(L->wg_pad, wg, bytes, cudaMemcpyHostToDevice));
     }
@@ -996,6 +1011,13 @@ int emoe_layer_gate_demand(emoe_layer* L, int64_t* counts_host, void* stream) {
     EMOE_CUDA(cudaMemcpyAsync(h.data(), L->demand_dev, sizeof(unsigned long long) * E, cudaMemcpyDeviceToHost, s));
     EMOE_CUDA(cudaStreamSynchronize(s));
     for (int e = 0; e < E; ++e) counts_host[e] = (int64_t)h[e];
+  });
+}
+
+int emoe_layer_set_keep_logits(emoe_layer* L, int keep) {
+  return guard([&] {
+    EMOE_REQUIRE(L, "set_keep_logits: null layer");
+    L->keep_logits = keep != 0;
   });
 }
 

@@ -116,6 +116,11 @@ class MoELayer:
         to its logits before top-k."""
         check(lib.emoe_layer_set_logits_mode(self.h, {"replace": 0, "add": 1}[mode]))
 
+    def set_keep_logits(self, keep: bool) -> None:
+        """Store the gate's fp32 logits in the workspace (default); False lets the
+        fused tcgen05 gate (E >= 32) skip that store."""
+        check(lib.emoe_layer_set_keep_logits(self.h, int(keep)))
+
     # -- residency (two-phase, engine.cpp:431-464) ------------------------
     def begin_load(self, evictions: Sequence[int], loads: Sequence[int], stream=None) -> None:
         ev = np.ascontiguousarray(np.asarray(list(evictions) or [0], np.int32))

@@ -132,8 +132,9 @@ class MoEStack:
         """The engine keeps the invocation's aggregate as every layer's route_token
         fallback scores (last_aggregate_, engine.cpp:424, :529-531); applied
         stream-ordered, so forwards already enqueued keep the previous scores."""
+        self.scores = np.array(aggregate, np.float64)  # host copy (tests, reports)
         for l, layer in enumerate(self.layers):
-            layer.set_scores(np.asarray(aggregate[l], np.float64), stream)
+            layer.set_scores(self.scores[l], stream)
 
     def apply(self, ops, stream=None) -> int:
         """Start the plan: per layer, evictions now, loads on the shared copy stream."""

@@ -232,7 +232,7 @@ def _gpu_worker(rank, world, port_no, resident, out_dir):
 def test_ep_two_ranks_one_gpu_bit_identical(resident, tmp_path):
     mp.spawn(_gpu_worker, args=(2, free_port(), resident, str(tmp_path)), nprocs=2, join=True)
     for r in range(2):
-        d = torch.load(tmp_path / f"g{r}.pt")
+        d = torch.load(tmp_path / f"g{r}.pt", weights_only=False)
         assert torch.equal(d["y_ep"], d["y_1"]), f"rank {r}: EP output differs from the single-GPU forward"
 
 
@@ -400,7 +400,7 @@ def test_ep_p2p_two_ranks_one_gpu_bit_identical(resident, loads, tmp_path):
     0, 2 and 5 live on rank 0; [3]: one expert split in half."""
     mp.spawn(_gpu_p2p_worker, args=(2, free_port(), resident, str(tmp_path), loads), nprocs=2, join=True)
     for r in range(2):
-        for i, d in enumerate(torch.load(tmp_path / f"p{r}.pt")):
+        for i, d in enumerate(torch.load(tmp_path / f"p{r}.pt", weights_only=False)):
             assert d["status"] == 0, f"rank {r} forward {i}: status {d['status']}"
             assert d["rows"] > 0 and d["rows"] == d["tot"][:, r].sum()
             assert d["layout_same"], f"rank {r} forward {i}: device layout differs from p2p_layout"
@@ -440,9 +440,9 @@ def test_ep_p2p_fault_status(case, tmp_path):
     never arrives makes the barrier give up after EMOE_EP_TIMEOUT_S with
     status 1 instead of hanging the GPU."""
     mp.spawn(_gpu_p2p_fault_worker, args=(2, free_port(), case, str(tmp_path)), nprocs=2, join=True)
-    r0 = torch.load(tmp_path / "f0.pt")
+    r0 = torch.load(tmp_path / "f0.pt", weights_only=False)
     if case == "overflow":
-        r1 = torch.load(tmp_path / "f1.pt")
+        r1 = torch.load(tmp_path / "f1.pt", weights_only=False)
         assert r0["status"] == 2 and r1["status"] == 2
         assert r0["finite"] and r1["finite"]
     else:
@@ -475,7 +475,7 @@ def test_ep_p2p_single_rank(tmp_path):
     """World size 1: the peer-memory path degenerates to local stores and a
     self-barrier and still equals the plain forward."""
     mp.spawn(_gpu_p2p_single_worker, args=(1, free_port(), str(tmp_path)), nprocs=1, join=True)
-    d = torch.load(tmp_path / "s.pt")
+    d = torch.load(tmp_path / "s.pt", weights_only=False)
     assert d["status"] == 0
     assert torch.equal(d["y_ep"], d["y_1"])
 
@@ -531,6 +531,6 @@ def test_ep_stack_two_ranks_one_gpu_bit_identical(tmp_path):
     rank equals the single-GPU stack's, over forwards of different sizes."""
     mp.spawn(_gpu_stack_worker, args=(2, free_port(), str(tmp_path)), nprocs=2, join=True)
     for r in range(2):
-        for i, d in enumerate(torch.load(tmp_path / f"st{r}.pt")):
+        for i, d in enumerate(torch.load(tmp_path / f"st{r}.pt", weights_only=False)):
             assert d["status"] == 0, f"rank {r} forward {i}: status {d['status']}"
             assert all(d["same"]), f"rank {r} forward {i}: per-layer EP == EP=1: {d['same']}"

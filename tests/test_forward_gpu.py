@@ -383,3 +383,55 @@ def test_column_panel_raster_bit_identical(cg, tmp_path):
         subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, **env), timeout=300)
         outs.append(torch.load(out))
     assert torch.equal(outs[0], outs[1])
+
+
+_GATE_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+from helpers import build_layer, to_f32
+E, d, k, T, keep = {args!r}
+res = list(range(0, E, 3))[: max(1, E // 5)]
+layer, _, _ = build_layer(E, d, 512, k, "bf16", "relu" if k == 1 else "swiglu",
+                          "full_softmax" if k == 1 else "topk_softmax", len(res), res, max_tokens=T)
+layer.set_keep_logits(keep)
+layer.set_scores([float((e * 37) % 11) for e in range(E)])
+x = torch.randn(T, d, generator=torch.Generator().manual_seed(5)).to(torch.bfloat16).cuda()
+y = layer.forward(x)
+ws = layer.workspace()
+out = {{key: ws[key].cpu() for key in ("topk_idx", "route_expert", "route_rank", "route_hit", "served_idx",
+                                       "served_w", "pos", "counts")}}
+out["y"] = y.cpu()
+out["logits"] = ws["logits"].cpu() if keep else None
+torch.save(out, {out_path!r})
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [(128, 768, 1, 65536), (128, 768, 1, 1000), (64, 512, 2, 3000), (32, 256, 1, 777),
+                                  (96, 512, 2, 2500)])
+def test_fused_gate_route_bit_identical(args, tmp_path):
+    """E >= 32: the fused tcgen05 gate + route (default; logits stored or not)
+    gives bit-identical routing, weights, permutation and outputs to the
+    split path (dense gate GEMM -> logits -> route_from_logits_kernel,
+    EMOE_GATE_ROUTE=split), and both store the same logits."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    E, d, k, T = args
+    runs = {}
+    for name, env, keep in (("split", "split", True), ("fused", "fused", True), ("fused_nolog", "fused", False)):
+        out = tmp_path / f"{name}.pt"
+        code = _GATE_SCRIPT.format(root=str(root), tests=str(root / "tests"), args=(E, d, k, T, keep),
+                                   out_path=str(out))
+        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, EMOE_GATE_ROUTE=env),
+                       timeout=300)
+        runs[name] = torch.load(out)
+    assert torch.equal(runs["split"]["logits"], runs["fused"]["logits"])
+    for name in ("fused", "fused_nolog"):
+        for key, v in runs["split"].items():
+            if key != "logits":
+                assert torch.equal(v, runs[name][key]), f"{name}: {key} differs from the split path"
+    assert (runs["split"]["route_rank"] == -1).any(), "the case should exercise the fallback"
