@@ -56,7 +56,7 @@ _decl("emoe_layer_set_gate_host", vp, vp)
 _decl("emoe_layer_register_expert_host", vp, C.c_int, vp, vp, vp)
 _decl("emoe_layer_set_scores_host", vp, vp)
 _decl("emoe_layer_set_scores", vp, vp, vp)
-_decl("emoe_layer_set_logits_mode", "emoe_layer_set_keep_logits", vp, C.c_int)
+_decl("emoe_layer_set_logits_mode", vp, C.c_int)
 _decl("emoe_layer_set_keep_logits", vp, C.c_int)
 _decl("emoe_layer_register_expert_pinned", vp, C.c_int, vp, vp, vp)
 _decl("emoe_layer_set_copy_stream", vp, vp)
