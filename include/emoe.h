@@ -356,6 +356,10 @@ int emoe_predictor_set_counts_dev(emoe_predictor* pred, const int64_t* src_dev, 
  * of a device trace [P][m][T][k]: dominant [m], sets [m][k] (-1 padded), sizes [m]. */
 int emoe_prompt_expert_sets(const int32_t* trace_dev, int P, int m, int T, int k, int prompt, int32_t* dominant_host,
                             int32_t* sets_host, int32_t* sizes_host, void* stream);
+/* Same for one prompt in host memory [m][T][k] (T = 0 allowed: dominant 0,
+ * empty sets, as the reference); expert indices must be < 1024. */
+int emoe_prompt_expert_sets_host(const int32_t* trace_prompt_host, int m, int T, int k, int32_t* dominant_host,
+                                 int32_t* sets_host, int32_t* sizes_host);
 
 /* predict_all_layers (mode 0) / predict_chained (mode 1) / predict_layerwise
  * (mode 2, `layer`) (predictor.cpp:187-220).  prev_sets [m][k] + sizes [m].

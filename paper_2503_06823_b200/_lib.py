@@ -103,6 +103,7 @@ _decl("emoe_predictor_count_size", vp, C.POINTER(C.c_int64))
 _decl("emoe_predictor_counts_dev", vp, vp, vp)
 _decl("emoe_predictor_set_counts_dev", vp, vp, vp)
 _decl("emoe_prompt_expert_sets", vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp)
+_decl("emoe_prompt_expert_sets_host", vp, C.c_int, C.c_int, C.c_int, vp, vp, vp)
 _decl("emoe_predict_host", vp, C.c_int, vp, vp, C.c_int, vp, vp, vp)
 _decl("emoe_predicted_frequencies_host", vp, C.c_int, vp)
 _decl("emoe_expected_tokens_host", C.c_int, C.c_int, C.c_int, vp, vp, vp, C.c_int, vp, vp, vp, vp, C.c_int, vp)
@@ -126,7 +127,7 @@ EXPORTED = [
     "emoe_layer_stage_times", "emoe_kernel_launches", "emoe_predictor_create",
     "emoe_predictor_destroy", "emoe_predictor_reset", "emoe_predictor_break_chain", "emoe_hist_update", "emoe_hist_update_host", "emoe_predictor_counts_host",
     "emoe_predictor_set_counts_host", "emoe_predictor_count_size", "emoe_predictor_counts_dev",
-    "emoe_predictor_set_counts_dev", "emoe_prompt_expert_sets", "emoe_predict_host",
+    "emoe_predictor_set_counts_dev", "emoe_prompt_expert_sets", "emoe_prompt_expert_sets_host", "emoe_predict_host",
     "emoe_predicted_frequencies_host", "emoe_expected_tokens_host", "emoe_select_experts_host",
     "emoe_loading_targets_host", "emoe_plan_loading_host", "emoe_invocation_host", "emoe_gen_routing_trace",
 ]

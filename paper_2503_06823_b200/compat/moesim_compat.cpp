@@ -12,7 +12,19 @@
 // Only bookkeeping stays on the host, as in the reference: the Placement
 // bitmap, value-type conversions, and the per-task grid of ExpectedTokens
 // (one product per element, computed exactly as expert_store.cpp:78-90 does).
+//
+// It also replaces workload.cpp's dominant_expert / prompt_expert_sets
+// (:350-377): the drop-in links a copy of the reference's workload.o whose
+// two symbols are made weak (oracle/Makefile, objcopy --weaken-symbol), so
+// callers outside workload.cpp (the engine's invocation, engine.cpp:388-390,
+// and the reference's test_workload suite) get the GPU versions below.
+//
+// Code that must match the reference byte for byte restates it: Placement's
+// bookkeeping (expert_store.cpp:9-57), TransitionModel::validate /
+// layer_row / prompt_row (predictor.cpp:90-136), save_model / load_model
+// (predictor.cpp:240-274) -- same messages, same JSON schema.
 #include <algorithm>
+#include <cmath>
 #include <fstream>
 #include <map>
 #include <numeric>
@@ -25,6 +37,7 @@
 #include "json.hpp"
 #include "moesim/expert_store.hpp"
 #include "moesim/predictor.hpp"
+#include "moesim/workload.hpp"
 
 namespace moesim {
 
@@ -393,6 +406,12 @@ void TransitionModel::validate() const {
         if (v < 0.0) throw ValidationError("predictor.per_task_frequency." + task + ": negative count");
     }
   }
+  // smoothed rows must be proper distributions (predictor.cpp:127-135)
+  for (int l = 0; l + 1 < num_layers; ++l) {
+    std::vector<double> row = layer_row(l, 0);
+    double s = std::accumulate(row.begin(), row.end(), 0.0);
+    if (std::abs(s - 1.0) > 1e-9) throw ValidationError("predictor.layer_counts: smoothed row does not sum to 1");
+  }
 }
 
 TransitionModel fit(const RoutingTrace& trace, const std::vector<std::string>& task_ids, double smoothing,
@@ -538,6 +557,69 @@ TransitionModel load_model(const std::string& path) {
   }
   model.validate();
   return model;
+}
+
+// ---------------------------------------------------------------------------
+// workload.cpp:350-377 on the GPU (emoe_prompt_expert_sets_host)
+// ---------------------------------------------------------------------------
+namespace {
+
+// one prompt's dominant experts and expert sets, cached while the same
+// prompt content is asked for again (dominant_expert is called per layer)
+struct PromptSets {
+  std::vector<int32_t> key;  // [layer sizes..., flattened rank-0 choices]
+  std::vector<int32_t> dom;
+  std::vector<std::vector<int>> sets;
+};
+
+const PromptSets& gpu_prompt_sets(const RoutingTrace& trace, int prompt) {
+  static thread_local PromptSets cache;
+  const auto& layers = trace.experts.at(static_cast<size_t>(prompt));
+  const int m = static_cast<int>(layers.size());
+  std::vector<int32_t> key;
+  key.reserve(m + 1);
+  for (const auto& lay : layers) key.push_back(static_cast<int32_t>(lay.size()));
+  for (const auto& lay : layers)
+    for (const auto& choice : lay) key.push_back(choice.at(0));
+  if (key == cache.key && !cache.key.empty()) return cache;
+  const int k = std::max(trace.top_k, 1);
+  PromptSets out;
+  out.dom.assign(m, 0);
+  out.sets.assign(m, {});
+  // layers of equal token count go to the GPU together ([m][T][1]: rank-0 choices)
+  int l0 = 0;
+  while (l0 < m) {
+    const int T = static_cast<int>(layers[l0].size());
+    int l1 = l0;
+    while (l1 < m && static_cast<int>(layers[l1].size()) == T) ++l1;
+    const int n = l1 - l0;
+    // [n][T][k] with the rank-0 choices (the only rank counted); sets hold up to top_k
+    std::vector<int32_t> flat(static_cast<size_t>(n) * T * k, 0);
+    for (int l = l0; l < l1; ++l)
+      for (int t = 0; t < T; ++t) flat[(static_cast<size_t>(l - l0) * T + t) * k] = layers[l][t][0];
+    std::vector<int32_t> dom(n), sets(static_cast<size_t>(n) * k), sizes(n);
+    emoe_check(emoe_prompt_expert_sets_host(flat.data(), n, T, k, dom.data(), sets.data(), sizes.data()));
+    for (int l = l0; l < l1; ++l) {
+      out.dom[l] = dom[l - l0];
+      for (int i = 0; i < sizes[l - l0]; ++i) out.sets[l].push_back(sets[static_cast<size_t>(l - l0) * k + i]);
+    }
+    l0 = l1;
+  }
+  out.key = std::move(key);
+  cache = std::move(out);
+  return cache;
+}
+
+}  // namespace
+
+int dominant_expert(const RoutingTrace& trace, int prompt, int layer) {
+  return gpu_prompt_sets(trace, prompt).dom.at(static_cast<size_t>(layer));
+}
+
+std::vector<std::vector<int>> prompt_expert_sets(const RoutingTrace& trace, int prompt) {
+  std::vector<std::vector<int>> sets = gpu_prompt_sets(trace, prompt).sets;
+  sets.resize(static_cast<size_t>(trace.num_layers));  // one (possibly empty) set per layer, as the reference
+  return sets;
 }
 
 }  // namespace moesim

@@ -788,6 +788,37 @@ int emoe_prompt_expert_sets(const int32_t* trace, int nP, int m, int T, int k, i
   });
 }
 
+int emoe_prompt_expert_sets_host(const int32_t* trace_prompt, int m, int T, int k, int32_t* dominant, int32_t* sets,
+                                 int32_t* sizes) {
+  return guard([&] {
+    EMOE_REQUIRE(m >= 1 && T >= 0 && k >= 1 && dominant && sets && sizes, "prompt_expert_sets: bad args");
+    EMOE_REQUIRE(T == 0 || trace_prompt, "prompt_expert_sets: null trace");
+    if (T == 0) {  // no tokens: the reference's empty count vector gives expert 0 and empty sets
+      for (int l = 0; l < m; ++l) {
+        dominant[l] = 0;
+        sizes[l] = 0;
+        for (int r = 0; r < k; ++r) sets[(size_t)l * k + r] = -1;
+      }
+      return;
+    }
+    // the count vector spans the largest rank-0 index seen (workload.cpp:351-356)
+    int E = 1;
+    for (size_t i = 0; i < (size_t)m * T; ++i) {
+      const int32_t e = trace_prompt[i * k];
+      EMOE_REQUIRE(e >= 0 && e < MAXE, "prompt_expert_sets: expert index out of range [0, 1024)");
+      E = std::max(E, e + 1);
+    }
+    DevBuf<int32_t> dt(trace_prompt, (size_t)m * T * k), dd(m), ds((size_t)m * k), dz(m);
+    prompt_sets_kernel<<<m, 256, E * sizeof(int)>>>(dt.p, m, T, k, E, 0, dd.p, ds.p, dz.p);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+    EMOE_CUDA(cudaDeviceSynchronize());
+    dd.to_host(dominant);
+    ds.to_host(sets);
+    dz.to_host(sizes);
+  });
+}
+
 int emoe_predict_host(emoe_predictor* P, int mode, const int32_t* sets, const int32_t* sizes, int layer,
                       double* scores, int32_t* experts, int32_t* n_experts) {
   return guard([&] {

@@ -183,7 +183,7 @@ def run_stream(stack: MoEStack, trace: np.ndarray, trace_dev: torch.Tensor, prom
     hits = torch.zeros(cfg.m, dtype=torch.int64, device=x.device)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stats = dict(invocations=0, skipped_invocations=0, planned_loads=0, invocation_host_ms=0.0, fired_at=[],
-                 skipped_at=[])
+                 skipped_at=[], delta_e_planned_s=[])
     load_events = []
     torch.cuda.synchronize()
     ev0.record()
@@ -202,8 +202,9 @@ def run_stream(stack: MoEStack, trace: np.ndarray, trace_dev: torch.Tensor, prom
             else:
                 t0 = time.perf_counter()
                 _, prev_sets = moesim_prompt_sets(trace_dev, p - 1)
-                ops, agg, _ = stack.invocation(prev_sets, requests)
+                ops, agg, delta_e = stack.invocation(prev_sets, requests)
                 stack.set_scores(agg)
+                stats["delta_e_planned_s"].append(delta_e)  # plan_loading's estimate (expert_store.cpp:189-195)
                 ls, le = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 ls.record(stack.copy_stream)
                 stats["planned_loads"] += stack.apply(ops)
@@ -219,6 +220,9 @@ def run_stream(stack: MoEStack, trace: np.ndarray, trace_dev: torch.Tensor, prom
         layer.poll_loads(blocking=True)
     ms = ev0.elapsed_time(ev1)
     load_ms = sum(a.elapsed_time(b) for a, b in load_events)
+    # the measured copy time of each invocation's loads: the live delta_e the
+    # engine's scheduler consumes (engine.cpp:333-334)
+    stats["delta_e_measured_s"] = [a.elapsed_time(b) / 1e3 for a, b in load_events]
     expert_bytes = (3 if cfg.activation == "swiglu" else 2) * cfg.d * cfg.f * 2
     load_bytes = stats["planned_loads"] * expert_bytes
     stats.update(residency="predicted", ms=ms, tokens=n_prompts * T, tokens_per_s=n_prompts * T / (ms / 1e3),

@@ -92,3 +92,40 @@ def test_reference_des_on_b200_costs(tmp_path):
         assert p50[m] < p50["dynamic"]
     # invoking the predictor every prompt pays its reloads
     assert p50["emoe_e"] > p50["emoe_a"]
+
+
+DROPIN_RUNNER = ROOT / "oracle" / "_ref" / "dropin_run_scenario"
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not (RUNNER.exists() and DROPIN_RUNNER.exists()), reason="drop-in DES runner not built")
+def test_scheduler_consumes_gpu_plans(tmp_path):
+    """the reference engine's scheduler (Eq. 3 / Alg. 1,
+    scheduler.cpp:23-35, :42-103) consumes the B200-measured per-token cost c
+    and, per invocation, the GPU plan's delta_e (engine.cpp:333-334): the
+    reference DES driver relinked on the drop-in (fit, prediction, Eq. 2,
+    loading targets, plan_loading, route_token, prompt_expert_sets on the GPU)
+    runs every mode of the B200-cost scenario, and every output file -- the
+    events log with each plan's delta_e and each admission's Eq. 3 estimate,
+    per-request latencies, memory, placement snapshots, summary -- is
+    byte-identical to the all-CPU reference run."""
+    cfg = tmp_path / "scenario.json"
+    cfg.write_text(json.dumps(b200_scenario(), indent=1))
+    outs = {}
+    for name, exe in (("ref", RUNNER), ("dropin", DROPIN_RUNNER)):
+        out = tmp_path / name
+        r = subprocess.run([str(exe), str(cfg), str(out)], capture_output=True, text=True, timeout=1800)
+        assert r.returncode == 0, r.stdout + r.stderr
+        outs[name] = {p.relative_to(out): p.read_bytes() for p in sorted(out.rglob("*")) if p.is_file()}
+    assert outs["ref"].keys() == outs["dropin"].keys()
+    for f in outs["ref"]:
+        assert outs["ref"][f] == outs["dropin"][f], f"{f} differs between the reference and the drop-in DES"
+    # the scheduler saw the plans: admissions carry Eq. 3 estimates, plans a positive delta_e
+    events = [p for p in outs["ref"] if str(p).endswith(".events.csv")]
+    assert events
+    n_plans = n_admit = 0
+    for f in events:
+        rows = list(csv.DictReader(outs["ref"][f].decode().splitlines()))
+        n_plans += sum(1 for r in rows if r["event"] == "plan" and float(r["a"]) > 0)
+        n_admit += sum(1 for r in rows if r["event"] == "admit" and float(r["a"]) > 0)
+    assert n_plans > 0 and n_admit > 0
