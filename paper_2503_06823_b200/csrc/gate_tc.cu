@@ -30,6 +30,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "route_tail.cuh"
 
 namespace emoe {
 namespace gatetc {
@@ -38,6 +39,7 @@ constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 constexpr int STAGES = 4;
 constexpr int NUM_THREADS = 192;
 constexpr int A_BYTES = 128 * BK * 2;
+constexpr int BAR_BYTES = 1024;  // mbarriers and the TMEM slot, before the epilogue rows
 
 struct Params {
   RouteArgs a;
@@ -77,117 +79,6 @@ __device__ __forceinline__ void epi_sync() {  // the 4 epilogue warps only
   asm volatile("bar.sync 1, 128;" ::: "memory");
 }
 
-struct RouteState {
-  uint8_t resident[128];
-  int counts[128];
-  int n_res;
-  int fallback;
-};
-
-template <int NE>
-__device__ __forceinline__ float pick(const float (&v)[NE], int idx) {
-  float r = 0.0f;
-#pragma unroll
-  for (int e = 0; e < NE; ++e) r = e == idx ? v[e] : r;
-  return r;
-}
-
-// One token from its logits row in registers: the operations of
-// route_one_token + route_tail (route.cu) in the same order.
-template <int NE>
-__device__ __forceinline__ void route_row(const float (&v)[NE], int64_t t, const Params& p, RouteState& st) {
-  const RouteArgs& a = p.a;
-  const RouteOut& o = p.o;
-  const int k = a.k;
-  int ti[8];
-  uint32_t used[NE / 32];
-#pragma unroll
-  for (int c = 0; c < NE / 32; ++c) used[c] = 0;
-  {
-    int best = 0;
-    float bv = v[0];
-#pragma unroll
-    for (int e = 1; e < NE; ++e)
-      if (v[e] > bv) {
-        best = e;
-        bv = v[e];
-      }
-    ti[0] = best;
-#pragma unroll
-    for (int c = 0; c < NE / 32; ++c)
-      if ((best >> 5) == c) used[c] |= 1u << (best & 31);
-  }
-  for (int r = 1; r < k; ++r) {
-    int best = -1;
-    float bv = 0.0f;
-#pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      if (used[e >> 5] & (1u << (e & 31))) continue;
-      if (best < 0 || v[e] > bv) {
-        best = e;
-        bv = v[e];
-      }
-    }
-    ti[r] = best;
-#pragma unroll
-    for (int c = 0; c < NE / 32; ++c)
-      if ((best >> 5) == c) used[c] |= 1u << (best & 31);
-  }
-  if (o.topk_idx)
-    for (int r = 0; r < k; ++r) o.topk_idx[t * k + r] = ti[r];
-  // route_token remap (expert_store.cpp:206-220, engine.cpp:533-537)
-  int ex = -1, rk = -1, hit = 0;
-  if (st.n_res == 0) {
-    ex = ti[0];
-    if (!a.forced_miss) atomicExch(a.error_flag, 3);
-  } else {
-    for (int r = 0; r < k; ++r)
-      if (st.resident[ti[r]]) {
-        ex = ti[r];
-        rk = r;
-        hit = r == 0;
-        break;
-      }
-    if (rk < 0) ex = st.fallback;
-  }
-  if (o.route_expert) o.route_expert[t] = ex;
-  if (o.route_rank) o.route_rank[t] = rk;
-  if (o.route_hit) o.route_hit[t] = (uint8_t)hit;
-  int si[8];
-  int ns = 0;
-  if (st.n_res > 0) {
-    if (rk >= 0) {
-      for (int r = 0; r < k; ++r)
-        if (st.resident[ti[r]]) si[ns++] = ti[r];
-    } else {
-      si[ns++] = ex;
-    }
-  }
-  float w[8];
-  if (a.weight_mode == 0) {
-    if (ns > 0) {
-      const float mx = pick(v, si[0]);
-      float den = 0.0f;
-      for (int j = 0; j < ns; ++j) {
-        w[j] = expf(pick(v, si[j]) - mx);
-        den += w[j];
-      }
-      for (int j = 0; j < ns; ++j) w[j] = w[j] / den;
-    }
-  } else {
-    const float mx = pick(v, ti[0]);
-    float den = 0.0f;
-#pragma unroll
-    for (int e = 0; e < NE; ++e) den += expf(v[e] - mx);
-    for (int j = 0; j < ns; ++j) w[j] = expf(pick(v, si[j]) - mx) / den;
-  }
-  for (int j = 0; j < k; ++j) {
-    o.served_idx[t * k + j] = j < ns ? si[j] : -1;
-    o.served_w[t * k + j] = j < ns ? w[j] : 0.0f;
-  }
-  for (int j = 0; j < ns; ++j) atomicAdd(&st.counts[si[j]], 1);
-}
-
 template <int NE, int CN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gate_route_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_g,
@@ -206,50 +97,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull_bar = empty_bar + STAGES;  // [2]
   uint64_t* tempty_bar = tfull_bar + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  __shared__ RouteState st;
+  // the epilogue's logits rows, one per token: [128][NE + 1] fp32 (the pitch
+  // puts a warp's per-thread row accesses on 32 distinct banks)
+  float* s_rows = reinterpret_cast<float*>(smem_b + STAGES * B_BYTES + BAR_BYTES);
+  __shared__ routing::SharedRouteState st;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = CN > 1 ? cluster_ctarank() : 0;
   const int64_t cluster_id = blockIdx.x / CN, n_clusters = gridDim.x / CN;
   // every CTA of a cluster walks the same number of tile slots
   const int64_t n_iter = (ceil_div(p.ntiles, CN) + n_clusters - 1 - cluster_id) / n_clusters;
-
   const RouteArgs& a = p.a;
   const int E = a.E;
-  for (int e = threadIdx.x; e < E; e += NUM_THREADS) {
-    st.resident[e] = a.resident[e];
-    st.counts[e] = 0;
-  }
-  __syncthreads();
-  if (warp == 2) {  // resident count and the token-independent fallback (route.cu load_route_state)
-    int n = 0, first = -1, be = -1;
-    double bs = 0.0;
-    for (int e0 = 0; e0 < E; e0 += 32) {
-      const int e = e0 + lane;
-      const bool r = e < E && st.resident[e];
-      const unsigned m = __ballot_sync(0xffffffffu, r);
-      n += __popc(m);
-      if (first < 0 && m) first = e0 + __ffs(m) - 1;
-      const double sc = r && a.scores ? a.scores[e] : 0.0;
-      if (r && (be < 0 || sc > bs)) {
-        bs = sc;
-        be = e;
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double os = __shfl_xor_sync(0xffffffffu, bs, off);
-      const int oe = __shfl_xor_sync(0xffffffffu, be, off);
-      if (oe >= 0 && (be < 0 || os > bs || (os == bs && oe < be))) {
-        bs = os;
-        be = oe;
-      }
-    }
-    if (lane == 0) {
-      st.n_res = n;
-      st.fallback = a.scores ? be : first;
-    }
-  }
+
+  routing::load_route_state(st, a);  // residency, scores, the token-independent fallback (all threads)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_x);
     tma_prefetch_desc(&tmap_g);
@@ -337,46 +198,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
+    // epilogue: TMEM lane = token; each thread moves its row to shared memory
+    // (adding the bias / storing the logits on the way) and routes it
     const int quarter = warp & 3;
     const RouteOut& o = p.o;
+    float* row = s_rows + (quarter * 32 + lane) * (NE + 1);
     for (int64_t it = 0; it < n_iter; ++it) {
       const int buf = (int)(it & 1);
       const int64_t tile = (cluster_id + it * n_clusters) * CN + rank;
+      const int64_t t = tile * 128 + quarter * 32 + lane;
+      const bool live = tile < p.ntiles && t < a.T;
       mbar_wait(&tfull_bar[buf], (uint32_t)((it >> 1) & 1));
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + buf * NE;
-      float v[NE];
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < NE / 32; ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c * 32, r);
         tmem_ld_wait();
+        float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[c * 32 + j] = __uint_as_float(r[j]);
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (live && a.bias) {
+          const float4* b4 = reinterpret_cast<const float4*>(a.bias + t * NE + c * 32);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 bb = __ldg(b4 + j / 4);
+            v[j] += bb.x;
+            v[j + 1] += bb.y;
+            v[j + 2] += bb.z;
+            v[j + 3] += bb.w;
+          }
+        }
+        if (live && p.store_logits && o.logits) {
+          float4* dst = reinterpret_cast<float4*>(o.logits + t * NE + c * 32);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) dst[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) row[c * 32 + j] = v[j];
       }
       tc_fence_before();
       if (lane == 0) mbar_arrive_relaxed(&tempty_bar[buf]);  // the MMAs of tile i+2 may start
       if (tile < p.ntiles) {
-        const int64_t t = tile * 128 + quarter * 32 + lane;
-        if (t < a.T) {
-          if (a.bias) {
-            const float4* b4 = reinterpret_cast<const float4*>(a.bias + t * NE);
-#pragma unroll
-            for (int e = 0; e < NE; e += 4) {
-              const float4 bb = __ldg(b4 + e / 4);
-              v[e] += bb.x;
-              v[e + 1] += bb.y;
-              v[e + 2] += bb.z;
-              v[e + 3] += bb.w;
-            }
-          }
-          if (p.store_logits && o.logits) {
-            float4* dst = reinterpret_cast<float4*>(o.logits + t * NE);
-#pragma unroll
-            for (int e = 0; e < NE; e += 4) dst[e / 4] = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
-          }
-          route_row<NE>(v, t, p, st);
-        }
+        if (live) routing::route_one_token(row, t, a, o, st);
         epi_sync();  // every token of the tile counted
         if (o.block_counts)
           for (int e = threadIdx.x - 64; e < E; e += 128) {
@@ -401,7 +266,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 template <int NE, int CN>
 void launch_one(const CUtensorMap& tx, const CUtensorMap& tg, const Params& p, int num_sms, cudaStream_t s) {
   auto kernel = gate_route_tc_kernel<NE, CN>;
-  const int smem = 1024 + STAGES * (A_BYTES + NE * BK * 2) + 256;
+  const int smem = 1024 + STAGES * (A_BYTES + NE * BK * 2) + BAR_BYTES + 128 * (NE + 1) * 4;
   ensure_max_dynamic_smem(reinterpret_cast<const void*>(kernel), smem);
   const int grid = (int)std::min<int64_t>(num_sms / CN * CN, ceil_div(p.ntiles, CN) * CN);
   cudaLaunchConfig_t cfg = {};

@@ -10,6 +10,7 @@
 // written to each of its <= k destinations; the combine reads each served row
 // of Y once and writes y once, accumulating in fp32 in slot order.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -203,6 +204,177 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
   if (REMOTE) __threadfence_system();
 }
 
+// K3b on the TMA engine (large batches, local rows, no tf32 split): the
+// same ranking as permute_kernel (one thread per token, warp ballots), then
+// lane 0 of every warp moves its 32 tokens' rows with bulk copies: one
+// cp.async.bulk global -> shared per row into a 3-slot ring (two loads in
+// flight while a third row is being stored), one cp.async.bulk shared ->
+// global per destination.  Rows move as whole 16-B-aligned byte ranges, so
+// the SMs issue 1 + k instructions per row instead of row_bytes / 16 loads
+// and stores per copy.
+constexpr int PB_WARPS = 4;
+constexpr int PB_SLOTS = 3;
+
+__global__ void __launch_bounds__(PB_WARPS * 32) permute_bulk_kernel(
+    const uint8_t* __restrict__ x, int row_bytes, int64_t T, int E, int k, const int32_t* __restrict__ served_idx,
+    const int64_t* __restrict__ seg_offsets, const int64_t* __restrict__ block_base, uint8_t* __restrict__ x_perm,
+    int32_t* __restrict__ pos, int32_t* __restrict__ row_token) {
+  extern __shared__ __align__(128) uint8_t smb[];
+  uint8_t* ring = smb;                                                            // [warps][slots][row_bytes]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smb + PB_WARPS * PB_SLOTS * row_bytes);  // [warps][slots]
+  int32_t* warp_counts = reinterpret_cast<int32_t*>(bars + PB_WARPS * PB_SLOTS);      // [4][E]
+  int32_t* dst_s = warp_counts + 4 * E;                                              // [RT][k]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t t0 = (int64_t)blockIdx.x * RT;
+  const int64_t t = t0 + threadIdx.x;
+  const bool valid = t < T;
+  int my[8], rank[8];
+  for (int j = 0; j < k; ++j) {
+    my[j] = valid ? served_idx[t * k + j] : -1;
+    rank[j] = 0;
+  }
+  if (lane < PB_SLOTS) mbar_init(&bars[warp * PB_SLOTS + lane], 1);
+  const uint32_t lt = (1u << lane) - 1u;
+  if (k == 1) {
+    for (int e = lane; e < E; e += 32) warp_counts[warp * E + e] = 0;
+    __syncwarp();
+    const uint32_t m = __match_any_sync(0xffffffffu, my[0]);
+    if (my[0] >= 0) {
+      rank[0] = __popc(m & lt);
+      if (rank[0] == 0) warp_counts[warp * E + my[0]] = __popc(m);
+    }
+  } else {
+    for (int e = 0; e < E; ++e) {
+      bool has = false;
+      for (int j = 0; j < k; ++j) has |= (my[j] == e);
+      const uint32_t m = __ballot_sync(0xffffffffu, has);
+      if (lane == 0) warp_counts[warp * E + e] = __popc(m);
+      if (has)
+        for (int j = 0; j < k; ++j)
+          if (my[j] == e) rank[j] = __popc(m & lt);
+    }
+  }
+  fence_barrier_init();
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    const int e = my[j];
+    int32_t d = -1;
+    if (e >= 0) {
+      int64_t base = seg_offsets[e] + block_base[(int64_t)blockIdx.x * E + e];
+      for (int w = 0; w < warp; ++w) base += warp_counts[w * E + e];
+      d = (int32_t)(base + rank[j]);
+    }
+    dst_s[threadIdx.x * k + j] = d;
+    if (valid) {
+      pos[t * k + j] = d;
+      if (row_token && d >= 0) row_token[d] = (int32_t)t;
+    }
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  // this warp's served tokens, in order
+  int list[32];
+  int n = 0;
+  for (int i = 0; i < 32; ++i) {
+    const int r = warp * 32 + i;
+    if (t0 + r < T && dst_s[r * k] >= 0) list[n++] = r;
+  }
+  uint8_t* slots = ring + (size_t)warp * PB_SLOTS * row_bytes;
+  uint64_t* bar = bars + warp * PB_SLOTS;
+  auto issue = [&](int q) {
+    const int sl = q % PB_SLOTS;
+    mbar_arrive_expect_tx(&bar[sl], (uint32_t)row_bytes);
+    bulk_load_g2s(slots + (size_t)sl * row_bytes, x + (t0 + list[q]) * (int64_t)row_bytes, (uint32_t)row_bytes,
+                  &bar[sl]);
+  };
+  for (int q = 0; q < PB_SLOTS - 1 && q < n; ++q) issue(q);
+  for (int i = 0; i < n; ++i) {
+    const int sl = i % PB_SLOTS;
+    mbar_wait(&bar[sl], (uint32_t)((i / PB_SLOTS) & 1));
+    const int r = list[i];
+    for (int j = 0; j < k; ++j) {
+      const int32_t d = dst_s[r * k + j];
+      if (d < 0) break;  // served slots are compacted to the front
+      bulk_store_s2g(x_perm + (int64_t)d * row_bytes, slots + (size_t)sl * row_bytes, (uint32_t)row_bytes);
+    }
+    bulk_commit_group();
+    const int q = i + PB_SLOTS - 1;  // its slot last held row i - 1
+    if (q < n) {
+      bulk_wait_group_read<1>();  // row i - 1's stores have read their slot
+      issue(q);
+    }
+  }
+  bulk_wait_group_all();
+}
+
+// K5 on the TMA engine (bf16, large batches): each warp walks tokens; lane 0
+// bulk-loads the next token's k output rows into the warp's other slot while
+// the warp combines the current one from shared memory (lanes own 16-B
+// column chunks, fp32 fma in slot order -- the operations of
+// combine_bf16_kernel, so bit-identical) and stores y with coalesced 16-B
+// stores.
+constexpr int CB_WARPS = 4;
+
+__global__ void __launch_bounds__(CB_WARPS * 32) combine_bulk_kernel(const __nv_bfloat16* __restrict__ Y, int64_t T,
+                                                                     int d, int k, const int32_t* __restrict__ pos,
+                                                                     const float* __restrict__ served_w,
+                                                                     __nv_bfloat16* __restrict__ y) {
+  extern __shared__ __align__(128) uint8_t smb[];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int row_bytes = d * 2;
+  uint8_t* slots = smb + (size_t)warp * 2 * k * row_bytes;                              // [2][k][row_bytes]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smb + (size_t)CB_WARPS * 2 * k * row_bytes) + warp * 2;
+  if (lane < 2) mbar_init(&bar[lane], 1);
+  fence_barrier_init();
+  __syncwarp();
+  const int64_t stride = (int64_t)gridDim.x * CB_WARPS;
+  const int64_t first = (int64_t)blockIdx.x * CB_WARPS + warp;
+  auto issue = [&](int64_t tok, int sl) {
+    uint32_t bytes = 0;
+    for (int j = 0; j < k; ++j) bytes += pos[tok * k + j] >= 0 ? (uint32_t)row_bytes : 0u;
+    mbar_arrive_expect_tx(&bar[sl], bytes);
+    for (int j = 0; j < k; ++j) {
+      const int32_t p = pos[tok * k + j];
+      if (p >= 0)
+        bulk_load_g2s(slots + ((size_t)sl * k + j) * row_bytes, Y + (int64_t)p * d, (uint32_t)row_bytes, &bar[sl]);
+    }
+  };
+  if (lane == 0 && first < T) issue(first, 0);
+  int it = 0;
+  for (int64_t tok = first; tok < T; tok += stride, ++it) {
+    const int sl = it & 1;
+    if (lane == 0 && tok + stride < T) issue(tok + stride, sl ^ 1);  // its slot was drained last iteration
+    int32_t p[8];
+    float w[8];
+    for (int j = 0; j < k; ++j) {
+      p[j] = pos[tok * k + j];
+      w[j] = served_w[tok * k + j];
+    }
+    mbar_wait(&bar[sl], (uint32_t)((it >> 1) & 1));
+    const uint8_t* rows = slots + (size_t)sl * k * row_bytes;
+    for (int v = lane; v < d / 8; v += 32) {
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int j = 0; j < k; ++j) {
+        if (p[j] < 0) continue;
+        const uint4 r = *reinterpret_cast<const uint4*>(rows + (size_t)j * row_bytes + (size_t)v * 16);
+        const uint32_t u[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[2 * q] = fmaf(w[j], bf16_lo(u[q]), acc[2 * q]);
+          acc[2 * q + 1] = fmaf(w[j], bf16_hi(u[q]), acc[2 * q + 1]);
+        }
+      }
+      uint4 o;
+      o.x = pack_bf16x2(acc[0], acc[1]);
+      o.y = pack_bf16x2(acc[2], acc[3]);
+      o.z = pack_bf16x2(acc[4], acc[5]);
+      o.w = pack_bf16x2(acc[6], acc[7]);
+      reinterpret_cast<uint4*>(y + tok * d)[v] = o;
+    }
+    __syncwarp();  // every lane is done reading this slot before lane 0 refills it
+  }
+}
+
 // One warp per token; lanes own 16-byte column chunks.
 __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* __restrict__ Y, int64_t T, int d,
                                                            int k, const int32_t* __restrict__ pos,
@@ -268,6 +440,16 @@ __global__ void __launch_bounds__(256) combine_f32_kernel(const float* __restric
   }
 }
 
+// EMOE_BULK_COPY=0 keeps the LDG/STG permute and combine (A/B runs); the
+// bulk kernels need enough token blocks to fill the GPU
+int bulk_min_blocks() {
+  static const int v = [] {
+    const char* e = getenv("EMOE_BULK_COPY");
+    return e && e[0] == '0' ? (1 << 30) : 2 * 148;
+  }();
+  return v;
+}
+
 }  // namespace
 
 void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32_t* counts, int64_t* seg_offsets,
@@ -299,6 +481,19 @@ void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int 
     return n;
   }();
   const int ny = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * sms, nblocks), row_bytes / 16 / 8));
+  if (!x_hi && nblocks >= bulk_min_blocks()) {  // large batches: rows moved by the TMA engine
+    const size_t bsmem = (size_t)PB_WARPS * PB_SLOTS * row_bytes + (size_t)PB_WARPS * PB_SLOTS * 8 +
+                         (4 * (size_t)E + (size_t)RT * k) * sizeof(int32_t);
+    if (bsmem <= 200 * 1024) {
+      if (bsmem > 48 * 1024) ensure_max_dynamic_smem(reinterpret_cast<const void*>(permute_bulk_kernel), (int)bsmem);
+      permute_bulk_kernel<<<nblocks, PB_WARPS * 32, bsmem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
+                                                                 served_idx, seg_offsets, block_base,
+                                                                 static_cast<uint8_t*>(x_perm), pos, row_token);
+      EMOE_CUDA(cudaGetLastError());
+      count_launch();
+      return;
+    }
+  }
   auto kernel = x_hi ? permute_kernel<false, true> : permute_kernel<false, false>;
   kernel<<<dim3(nblocks, ny), PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
                                                           served_idx, seg_offsets, block_base,
@@ -340,6 +535,15 @@ void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int
     EMOE_REQUIRE(d % 4 == 0, "combine: d must be a multiple of 4");
     combine_f32_kernel<<<dim3(nblocks, ny), 256, 0, s>>>(static_cast<const float*>(Y), T, d, k, pos, served_w,
                                                          static_cast<float*>(y));
+  } else if (nblocks >= bulk_min_blocks() && (size_t)CB_WARPS * 2 * k * d * 2 + CB_WARPS * 16 <= 200 * 1024) {
+    EMOE_REQUIRE(d % 8 == 0, "combine: d must be a multiple of 8");
+    const int csmem = CB_WARPS * 2 * k * d * 2 + CB_WARPS * 16;
+    if (csmem > 48 * 1024) ensure_max_dynamic_smem(reinterpret_cast<const void*>(combine_bulk_kernel), csmem);
+    int per_sm = 1;
+    EMOE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, combine_bulk_kernel, CB_WARPS * 32, csmem));
+    const int grid = (int)std::min<int64_t>(ceil_div(T, CB_WARPS), (int64_t)sms * std::max(per_sm, 1));
+    combine_bulk_kernel<<<grid, CB_WARPS * 32, csmem, s>>>(static_cast<const __nv_bfloat16*>(Y), T, d, k, pos,
+                                                           served_w, static_cast<__nv_bfloat16*>(y));
   } else {
     EMOE_REQUIRE(d % 8 == 0, "combine: d must be a multiple of 8");
     combine_bf16_kernel<<<dim3(nblocks, ny), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Y), T, d, k, pos,

@@ -435,3 +435,46 @@ def test_fused_gate_route_bit_identical(args, tmp_path):
             if key != "logits":
                 assert torch.equal(v, runs[name][key]), f"{name}: {key} differs from the split path"
     assert (runs["split"]["route_rank"] == -1).any(), "the case should exercise the fallback"
+
+
+_BULK_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+from helpers import build_layer
+E, d, f, k, T, res, act = {args!r}
+layer, _, _ = build_layer(E, d, f, k, "bf16", act, "topk_softmax" if k > 1 else "full_softmax", len(res), res,
+                          max_tokens=T)
+x = torch.randn(T, d, generator=torch.Generator().manual_seed(9)).to(torch.bfloat16).cuda()
+y = layer.forward(x)
+ws = layer.workspace()
+R = int(ws["seg_offsets"][-1].item())
+rt = ws["row_token"][:R].cpu()
+xp = ws["x_perm"][:R].cpu()
+torch.save(dict(y=y.cpu(), pos=ws["pos"].cpu(), row_token=rt, x_perm=xp[rt >= 0]), {out!r})
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [(8, 1024, 1024, 2, 40000, [0, 2, 5, 7], "swiglu"),
+                                  (8, 4096, 1024, 2, 40000, [1, 3, 4, 6], "swiglu"),
+                                  (32, 768, 1024, 1, 50000, [0, 3, 9, 17, 21, 30], "relu"),
+                                  (8, 512, 512, 2, 38000, [3], "swiglu")])
+def test_bulk_copy_permute_combine_bit_identical(args, tmp_path):
+    """Large batches move rows with cp.async.bulk (permute_bulk_kernel,
+    combine_bulk_kernel): positions, row sources, permuted rows and outputs
+    bit-identical to the LDG/STG kernels (EMOE_BULK_COPY=0)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    outs = []
+    for flag in ("1", "0"):
+        out = tmp_path / f"b{flag}.pt"
+        code = _BULK_SCRIPT.format(root=str(root), tests=str(root / "tests"), args=args, out=str(out))
+        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, EMOE_BULK_COPY=flag),
+                       timeout=300)
+        outs.append(torch.load(out))
+    for key in outs[0]:
+        assert torch.equal(outs[0][key], outs[1][key]), f"{key} differs between the bulk and LDG/STG paths"
