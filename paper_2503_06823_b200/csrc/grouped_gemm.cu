@@ -55,9 +55,9 @@ constexpr int BAR_AREA_BYTES = 2048;  // mbarriers, TMEM slot, segment offsets (
 // CG = CTAs per MMA (1 or 2), EW = epilogue warps (4: one per TMEM lane
 // quarter; 8: two per quarter, each draining half of the accumulator columns,
 // for short-K tiles whose MMAs finish faster than 4 warps can drain TMEM)
-template <int CG, int EW>
+template <int CG, int EW, int MC = 1>
 struct Cfg {
-  static constexpr int TILE_M = 128 * CG;
+  static constexpr int TILE_M = 128 * CG * MC;  // rows one tile (a CTA pair's or a multicast cluster's) covers
   static constexpr int B_ROWS = BN / CG;  // B rows held by one CTA
 #ifndef EMOE_CG1_STAGES
 #define EMOE_CG1_STAGES 4
@@ -182,6 +182,24 @@ __device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t a_desc,
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// MC > 1: the weight tile is shared by MC CTAs on adjacent row blocks; each
+// loads 1/MC of it and multicasts it to the cluster (L2 -> SM traffic for B
+// drops MC-fold), and every CTA's MMA commit releases the stage in all of them
+__device__ __forceinline__ void tma_load_2d_mcast(const CUtensorMap* desc, uint64_t* bar, void* smem_dst, int32_t c0,
+                                                  int32_t c1, uint16_t mask, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(hint)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_mcast(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {  // arrive on this offset in both CTAs
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -254,12 +272,15 @@ __device__ __forceinline__ void store_box(const Params& p, const CUtensorMap* tm
   }
 }
 
-template <int EPI, int CG, int EW>
-__global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
+template <int EPI, int CG, int EW, int MC>
+__global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                         const __grid_constant__ CUtensorMap tmap_b2, const __grid_constant__ CUtensorMap tmap_out,
                         Params p) {
-  using C = Cfg<CG, EW>;
+  using C = Cfg<CG, EW, MC>;
+  static_assert(MC == 1 || CG == 1, "multicast clusters pair with the 1-CTA MMA");
+  constexpr bool CLUSTER = CG * MC > 1;
+  constexpr uint16_t MC_MASK = (uint16_t)((1u << MC) - 1u);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -277,10 +298,11 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int E = p.num_experts;
-  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const uint32_t rank = CLUSTER ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
-  const int cluster_id = blockIdx.x / CG;
-  const int num_clusters = gridDim.x / CG;
+  const bool own_mma = MC > 1 || leader;  // CTAs that issue (and expect bytes for) their own MMAs
+  const int cluster_id = blockIdx.x / (CG * MC);
+  const int num_clusters = gridDim.x / (CG * MC);
 
   for (int i = threadIdx.x; i <= E; i += C::NUM_THREADS)
     s_offs[i] = (int32_t)(p.single_rows > 0 ? (i == 0 ? 0 : p.single_rows) : p.seg_offsets[i]);
@@ -292,7 +314,7 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
     if (EPI == EPI_SWIGLU) tma_prefetch_desc(&tmap_b2);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], MC);  // MC > 1: one commit from the MMA of every cluster CTA
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
@@ -312,7 +334,7 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
     }
   }
   tc_fence_before();
-  if (CG == 2)
+  if (CLUSTER)
     cluster_sync_all();
   else
     __syncthreads();
@@ -338,15 +360,25 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
           b_row = slot * p.b_rows_per_slot + c.nb * (BN / 2);
           if (CG == 2 && rank == 1) tb = &tmap_b2;  // pair: CTA0 holds the W1 half, CTA1 the W3 half
         } else {
-          b_row = slot * p.b_rows_per_slot + c.nb * BN + (int)rank * C::B_ROWS;
+          b_row = slot * p.b_rows_per_slot + c.nb * BN + (CG == 2 ? (int)rank * C::B_ROWS : 0);
         }
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * C::STAGE_BYTES);
+          if (own_mma) mbar_arrive_expect_tx(&full_bar[stage], CG * C::STAGE_BYTES);
           const int kc = kb * BK;
           uint8_t* adst = smem_a + stage * C::A_BYTES;
           uint8_t* bdst = smem_b + stage * C::B_BYTES;
-          if (CG == 1) {
+          if (MC > 1) {
+            // own A rows; this CTA's half of the weight tile to both CTAs
+            // (SwiGLU: CTA0 the W1 rows, CTA1 the W3 rows; else 128 rows each)
+            tma_load_2d(&tmap_a, &full_bar[stage], adst, kc, a_row, p.hint_a);
+            if (EPI == EPI_SWIGLU)
+              tma_load_2d_mcast(rank == 0 ? &tmap_b : &tmap_b2, &full_bar[stage], bdst + rank * (C::B_BYTES / 2), kc,
+                                b_row, MC_MASK, p.hint_b);
+            else
+              tma_load_2d_mcast(&tmap_b, &full_bar[stage], bdst + rank * (C::B_BYTES / MC), kc,
+                                b_row + (int)rank * (BN / MC), MC_MASK, p.hint_b);
+          } else if (CG == 1) {
             tma_load_2d(&tmap_a, &full_bar[stage], adst, kc, a_row, p.hint_a);
             if (EPI == EPI_SWIGLU) {
               tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, p.hint_b);
@@ -364,9 +396,9 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
           }
         }
       }
-      if (CG == 2) {
-        // producer tail: every stage released, i.e. the leader's last
-        // multicast commits to this CTA's barriers have landed before exit
+      if (CLUSTER) {
+        // producer tail: every stage released, i.e. the last multicast
+        // commits to this CTA's barriers have landed before exit
         for (int i = 0; i < C::STAGES; ++i) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           if (++stage == C::STAGES) {
@@ -378,8 +410,8 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA) =====================
-    if (lane == 0 && leader) {
-      constexpr uint32_t idesc = umma_idesc_bf16(C::TILE_M, BN);
+    if (lane == 0 && own_mma) {
+      constexpr uint32_t idesc = umma_idesc_bf16(128 * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -403,7 +435,9 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
             else
               umma_bf16_pair(tmem_d, a_desc + (uint64_t)(kk * 2), b_desc + (uint64_t)(kk * 2), idesc, acc);
           }
-          if (CG == 1)
+          if (MC > 1)
+            umma_commit_mcast(&empty_bar[stage], MC_MASK);
+          else if (CG == 1)
             umma_commit(&empty_bar[stage]);
           else
             umma_commit_pair(&empty_bar[stage]);
@@ -649,8 +683,8 @@ __global__ void __launch_bounds__(Cfg<CG, EW>::NUM_THREADS, 1)
     if (EPI == EPI_STORE && p.seg_out_rank != nullptr) __threadfence_system();  // pushes visible to the peers
   }
 
-  if (CG == 2)
-    cluster_sync_all();  // the leader's commits to our barriers and TMEM are done
+  if (CLUSTER)
+    cluster_sync_all();  // the cluster's commits to our barriers and TMEM are done
   else
     __syncthreads();
   if (warp == 1) {
@@ -720,8 +754,8 @@ static bool tma_store_enabled() {
   return on;
 }
 
-int gemm_tile_m(int cta_group) { return 128 * cta_group; }
-int gemm_b_box_rows(int epi, int cta_group) { return epi == EPI_SWIGLU ? 128 : 256 / cta_group; }
+int gemm_tile_m(int cta_group, int mc) { return 128 * cta_group * mc; }
+int gemm_b_box_rows(int epi, int cta_group, int mc) { return epi == EPI_SWIGLU ? 128 : 256 / (cta_group * mc); }
 
 // raster group: keep the A panel (group x tile_m rows x K) near `panel` MB of
 // L2: 24 MB for long reductions (Mixtral shape, K >= 2048: best of
@@ -780,11 +814,11 @@ static int group_rows(int K, int tile_m) {
   return g < 2 ? 2 : (g > 64 ? 64 : g);
 }
 
-static void launch_params(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
+static void launch_params(int epi, int cta_group, int mc, const CUtensorMap& ta, const CUtensorMap& tb,
                           const CUtensorMap& tb2, const CUtensorMap& to, const gemm::Params& p, int num_sms,
                           cudaStream_t stream);
 
-void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
+void launch_grouped_gemm(int epi, int cta_group, int mc, const CUtensorMap& ta, const CUtensorMap& tb,
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
                          int num_sms, cudaStream_t stream, const int32_t* seg_expert, const CUtensorMap* tmap_out,
@@ -793,6 +827,8 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
   EMOE_REQUIRE(!scatter || epi == EPI_STORE, "grouped_gemm: the fused combine needs the GEMM2 epilogue");
   EMOE_REQUIRE(K % gemm::BK == 0, "grouped_gemm: K must be a multiple of 64");
   EMOE_REQUIRE(cta_group == 1 || cta_group == 2, "grouped_gemm: cta_group must be 1 or 2");
+  EMOE_REQUIRE(mc == 1 || (mc == 2 && cta_group == 1 && epi != EPI_F32),
+               "grouped_gemm: weight multicast pairs (mc = 2) run with cta_group 1");
   gemm::Params p;
   p.seg_offsets = seg_offsets;
   p.slot_of_expert = slot_of_expert;
@@ -803,7 +839,7 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
   EMOE_REQUIRE(N_out % p.out_block_cols == 0, "grouped_gemm: N must be a multiple of the column block");
   p.n_blocks = N_out / p.out_block_cols;
   p.b_rows_per_slot = b_rows_per_slot;
-  p.group_m = group_rows(K, 128 * cta_group);
+  p.group_m = group_rows(K, 128 * cta_group * mc);
   l2_hints(p.hint_a, p.hint_b);
   p.group_n = p.n_blocks;
   {  // EMOE_GEMM_STORE_HINT: 0 none (default), 1 evict-first, 2 evict-last (A/B runs)
@@ -842,7 +878,7 @@ void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CU
   p.scatter_arrive = scatter ? scatter->arrive : nullptr;
   EMOE_REQUIRE(!scatter || scatter->k == 1 || (scatter->k == 2 && scatter->pos && scatter->arrive),
                "grouped_gemm: the fused top-2 combine needs positions and arrival counters");
-  launch_params(epi, cta_group, ta, tb, tb2, p.tma_store ? *tmap_out : ta, p, num_sms, stream);
+  launch_params(epi, cta_group, mc, ta, tb, tb2, p.tma_store ? *tmap_out : ta, p, num_sms, stream);
 }
 
 __device__ int32_t g_slot_zero = 0;
@@ -882,7 +918,7 @@ void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t
   p.scatter_arrive = nullptr;
   p.seg_out_rank = nullptr;
   p.seg_out_shift = nullptr;
-  launch_params(EPI_F32, cta_group, ta, tb, tb, ta, p, num_sms, stream);
+  launch_params(EPI_F32, cta_group, 1, ta, tb, tb, ta, p, num_sms, stream);
 }
 
 // epilogue warps per CTA: 4 (one per TMEM lane quarter).  8 (two per quarter)
@@ -897,14 +933,15 @@ static int epilogue_warps(int /*K*/) {
   return forced == 8 ? 8 : 4;
 }
 
-template <int EPI, int CG, int EW>
+template <int EPI, int CG, int EW, int MC>
 static void launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const CUtensorMap& to,
                        const gemm::Params& p, int num_sms, cudaStream_t stream) {
-  using C = gemm::Cfg<CG, EW>;
-  auto kernel = gemm::grouped_gemm_kernel<EPI, CG, EW>;
+  using C = gemm::Cfg<CG, EW, MC>;
+  auto kernel = gemm::grouped_gemm_kernel<EPI, CG, EW, MC>;
   ensure_max_dynamic_smem(reinterpret_cast<const void*>(kernel), C::SMEM_BYTES);
-  const int grid = CG == 2 ? (num_sms / 2) * 2 : num_sms;
-  if (CG == 1) {
+  constexpr int CS = CG * MC;  // CTAs per cluster
+  const int grid = (num_sms / CS) * CS;
+  if (CS == 1) {
     kernel<<<grid, C::NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, tb2, to, p);
   } else {
     cudaLaunchConfig_t cfg = {};
@@ -914,7 +951,7 @@ static void launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = CS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -929,15 +966,22 @@ template <int EPI, int CG>
 static void launch_ew(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const CUtensorMap& to,
                       const gemm::Params& p, int num_sms, cudaStream_t stream) {
   if (epilogue_warps(p.K) == 8)
-    launch_one<EPI, CG, 8>(ta, tb, tb2, to, p, num_sms, stream);
+    launch_one<EPI, CG, 8, 1>(ta, tb, tb2, to, p, num_sms, stream);
   else
-    launch_one<EPI, CG, 4>(ta, tb, tb2, to, p, num_sms, stream);
+    launch_one<EPI, CG, 4, 1>(ta, tb, tb2, to, p, num_sms, stream);
 }
 
-static void launch_params(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
+static void launch_params(int epi, int cta_group, int mc, const CUtensorMap& ta, const CUtensorMap& tb,
                           const CUtensorMap& tb2, const CUtensorMap& to, const gemm::Params& p, int num_sms,
                           cudaStream_t stream) {
-  if (cta_group == 1) {
+  if (mc == 2) {  // 1-CTA MMAs, weight tile multicast over a cluster of 2 (4 epilogue warps)
+    if (epi == EPI_SWIGLU)
+      launch_one<EPI_SWIGLU, 1, 4, 2>(ta, tb, tb2, to, p, num_sms, stream);
+    else if (epi == EPI_RELU)
+      launch_one<EPI_RELU, 1, 4, 2>(ta, tb, tb2, to, p, num_sms, stream);
+    else
+      launch_one<EPI_STORE, 1, 4, 2>(ta, tb, tb2, to, p, num_sms, stream);
+  } else if (cta_group == 1) {
     if (epi == EPI_SWIGLU)
       launch_ew<EPI_SWIGLU, 1>(ta, tb, tb2, to, p, num_sms, stream);
     else if (epi == EPI_RELU)

@@ -95,8 +95,10 @@ void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int
 // K4: tcgen05 grouped GEMM (bf16); cta_group 1 (tile 128x256) or 2 (CTA pair, tile 256x256)
 CUtensorMap make_tmap_bf16_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 CUtensorMap make_tmap_bf16_store(const void* base, uint64_t rows, uint64_t cols);  // epilogue store target
-int gemm_tile_m(int cta_group);                 // segment padding the kernel needs
-int gemm_b_box_rows(int epi, int cta_group);    // TMA box rows of the weight operand
+// mc = 2: 1-CTA MMAs whose weight tile is multicast over a cluster of 2 CTAs
+// on adjacent row blocks (segments padded to 256 rows)
+int gemm_tile_m(int cta_group, int mc = 1);             // segment padding the kernel needs
+int gemm_b_box_rows(int epi, int cta_group, int mc = 1);  // TMA box rows of the weight operand
 struct PeerOut;  // expert parallelism: GEMM2 rows pushed to their source ranks (below)
 // top-1 combine fused into GEMM2's epilogue: y[row_token[r]] = weight[token] * Y[r]
 struct ScatterCombine {
@@ -107,7 +109,7 @@ struct ScatterCombine {
   const int32_t* pos = nullptr;  // k = 2: [T][2] rows of the served slots (-1 = not served)
   int32_t* arrive = nullptr;     // k = 2: [T][n_blocks][2] zeroed counters (left zeroed)
 };
-void launch_grouped_gemm(int epi, int cta_group, const CUtensorMap& ta, const CUtensorMap& tb,
+void launch_grouped_gemm(int epi, int cta_group, int mc, const CUtensorMap& ta, const CUtensorMap& tb,
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
                          int num_sms, cudaStream_t stream, const int32_t* seg_expert = nullptr,

@@ -94,6 +94,7 @@ struct emoe_layer {
   int num_sms = 148;
   int64_t rows_cap = 0;
   int cta_group = 1;  // FFN GEMM CTA group
+  int gemm_mc = 1;    // 2: weight tiles multicast over CTA pairs (1-CTA MMAs)
   int seg_pad = kSegPad;
   int route_blocks = 0;
   cudaStream_t copy_stream = nullptr;
@@ -392,11 +393,11 @@ struct emoe_layer {
         o1 = make_tmap_bf16_store(hr, (uint64_t)R, f);
         o2 = make_tmap_bf16_store(yr, (uint64_t)R, d);
       }
-      launch_grouped_gemm(swiglu() ? EPI_SWIGLU : EPI_RELU, cta_group, a1, tb1, tb3, segs, slot_dev, n_seg, d, f, f,
+      launch_grouped_gemm(swiglu() ? EPI_SWIGLU : EPI_RELU, cta_group, gemm_mc, a1, tb1, tb3, segs, slot_dev, n_seg, d, f, f,
                           static_cast<__nv_bfloat16*>(hr), f, num_sms, s, seg_expert, &o1);
       mark(3, s);
       if (ext_mark3) EMOE_CUDA(cudaEventRecord(ext_mark3, s));
-      launch_grouped_gemm(EPI_STORE, cta_group, a2, tb2, tb2, segs, slot_dev, n_seg, f, d, d,
+      launch_grouped_gemm(EPI_STORE, cta_group, gemm_mc, a2, tb2, tb2, segs, slot_dev, n_seg, f, d, d,
                           static_cast<__nv_bfloat16*>(yr), d, num_sms, s, seg_expert, &o2, scatter, peer_out);
       mark(4, s);
     } else if (tf32) {
@@ -670,7 +671,12 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
       // shape) — profiles/r01_cta_group_ab.jsonl
       const int auto_cg = c.d_model <= 2048 ? 2 : 1;
       L->cta_group = c.dtype == EMOE_DTYPE_BF16 ? (c.gemm_cta_group ? c.gemm_cta_group : auto_cg) : 1;
-      L->seg_pad = c.dtype == EMOE_DTYPE_BF16 ? gemm_tile_m(L->cta_group) : kSegPad;
+      // EMOE_GEMM_MC=2: 1-CTA GEMMs with the weight tile multicast over CTA pairs (A/B runs)
+      L->gemm_mc = c.dtype == EMOE_DTYPE_BF16 && L->cta_group == 1 && getenv("EMOE_GEMM_MC") &&
+                           atoi(getenv("EMOE_GEMM_MC")) == 2
+                       ? 2
+                       : 1;
+      L->seg_pad = c.dtype == EMOE_DTYPE_BF16 ? gemm_tile_m(L->cta_group, L->gemm_mc) : kSegPad;
       L->rows_cap = T * k + (int64_t)E * L->seg_pad;
       L->route_blocks = (int)ceil_div(T, kRouteBlockTokens);
       EMOE_CUDA(cudaStreamCreateWithFlags(&L->copy_stream, cudaStreamNonBlocking));
@@ -720,12 +726,12 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
       if (c.dtype == EMOE_DTYPE_BF16) {
         const uint64_t d = c.d_model, f = c.d_ff;
         const int epi1 = L->swiglu() ? EPI_SWIGLU : EPI_RELU;
-        const uint32_t b1_box = gemm_b_box_rows(epi1, L->cta_group);
+        const uint32_t b1_box = gemm_b_box_rows(epi1, L->cta_group, L->gemm_mc);
         L->ta1 = make_tmap_bf16_2d(L->x_perm, L->rows_cap, d, 128);
         L->tb1 = make_tmap_bf16_2d(L->w1_pool, (uint64_t)c.num_slots * f, d, b1_box);
         L->tb3 = L->swiglu() ? make_tmap_bf16_2d(L->w3_pool, (uint64_t)c.num_slots * f, d, b1_box) : L->tb1;
         L->ta2 = make_tmap_bf16_2d(L->h, L->rows_cap, f, 128);
-        L->tb2 = make_tmap_bf16_2d(L->w2_pool, (uint64_t)c.num_slots * d, f, gemm_b_box_rows(EPI_STORE, L->cta_group));
+        L->tb2 = make_tmap_bf16_2d(L->w2_pool, (uint64_t)c.num_slots * d, f, gemm_b_box_rows(EPI_STORE, L->cta_group, L->gemm_mc));
         L->to1 = make_tmap_bf16_store(L->h, L->rows_cap, f);
         L->to2 = make_tmap_bf16_store(L->y_perm, L->rows_cap, d);
       } else {

@@ -478,3 +478,30 @@ def test_bulk_copy_permute_combine_bit_identical(args, tmp_path):
         outs.append(torch.load(out))
     for key in outs[0]:
         assert torch.equal(outs[0][key], outs[1][key]), f"{key} differs between the bulk and LDG/STG paths"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [(8, 1024, 1024, 2, 5000, [0, 2, 5, 7], "swiglu"),
+                                  (32, 768, 1024, 1, 6000, [0, 3, 9, 17, 21, 30], "relu"),
+                                  (8, 2304, 2304, 2, 3000, [1, 3, 4, 6], "swiglu"),
+                                  (8, 512, 512, 2, 777, [3], "swiglu")])
+def test_gemm_weight_multicast_bit_identical(args, tmp_path):
+    """EMOE_GEMM_MC=2 (1-CTA MMAs, each weight tile multicast over a 2-CTA
+    cluster on adjacent row blocks, segments padded to 256 rows): positions
+    change with the padding, but every token's output is bit-identical."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    outs = []
+    for flag in ("2", "1"):
+        out = tmp_path / f"mc{flag}.pt"
+        code = _BULK_SCRIPT.replace("max_tokens=T)", "max_tokens=T, gemm_cta_group=1)").format(
+            root=str(root), tests=str(root / "tests"), args=args, out=str(out))
+        env = dict(os.environ, EMOE_GEMM_MC=flag)
+        subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
+        outs.append(torch.load(out))
+    assert torch.equal(outs[0]["y"], outs[1]["y"]), "outputs differ with the weight multicast"
+    assert torch.equal(outs[0]["x_perm"], outs[1]["x_perm"])  # the same rows, in the same order
