@@ -307,74 +307,6 @@ __global__ void __launch_bounds__(PB_WARPS * 32) permute_bulk_kernel(
   bulk_wait_group_all();
 }
 
-// K5 on the TMA engine (bf16, large batches): each warp walks tokens; lane 0
-// bulk-loads the next token's k output rows into the warp's other slot while
-// the warp combines the current one from shared memory (lanes own 16-B
-// column chunks, fp32 fma in slot order -- the operations of
-// combine_bf16_kernel, so bit-identical) and stores y with coalesced 16-B
-// stores.
-constexpr int CB_WARPS = 4;
-
-__global__ void __launch_bounds__(CB_WARPS * 32) combine_bulk_kernel(const __nv_bfloat16* __restrict__ Y, int64_t T,
-                                                                     int d, int k, const int32_t* __restrict__ pos,
-                                                                     const float* __restrict__ served_w,
-                                                                     __nv_bfloat16* __restrict__ y) {
-  extern __shared__ __align__(128) uint8_t smb[];
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int row_bytes = d * 2;
-  uint8_t* slots = smb + (size_t)warp * 2 * k * row_bytes;                              // [2][k][row_bytes]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smb + (size_t)CB_WARPS * 2 * k * row_bytes) + warp * 2;
-  if (lane < 2) mbar_init(&bar[lane], 1);
-  fence_barrier_init();
-  __syncwarp();
-  const int64_t stride = (int64_t)gridDim.x * CB_WARPS;
-  const int64_t first = (int64_t)blockIdx.x * CB_WARPS + warp;
-  auto issue = [&](int64_t tok, int sl) {
-    uint32_t bytes = 0;
-    for (int j = 0; j < k; ++j) bytes += pos[tok * k + j] >= 0 ? (uint32_t)row_bytes : 0u;
-    mbar_arrive_expect_tx(&bar[sl], bytes);
-    for (int j = 0; j < k; ++j) {
-      const int32_t p = pos[tok * k + j];
-      if (p >= 0)
-        bulk_load_g2s(slots + ((size_t)sl * k + j) * row_bytes, Y + (int64_t)p * d, (uint32_t)row_bytes, &bar[sl]);
-    }
-  };
-  if (lane == 0 && first < T) issue(first, 0);
-  int it = 0;
-  for (int64_t tok = first; tok < T; tok += stride, ++it) {
-    const int sl = it & 1;
-    if (lane == 0 && tok + stride < T) issue(tok + stride, sl ^ 1);  // its slot was drained last iteration
-    int32_t p[8];
-    float w[8];
-    for (int j = 0; j < k; ++j) {
-      p[j] = pos[tok * k + j];
-      w[j] = served_w[tok * k + j];
-    }
-    mbar_wait(&bar[sl], (uint32_t)((it >> 1) & 1));
-    const uint8_t* rows = slots + (size_t)sl * k * row_bytes;
-    for (int v = lane; v < d / 8; v += 32) {
-      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int j = 0; j < k; ++j) {
-        if (p[j] < 0) continue;
-        const uint4 r = *reinterpret_cast<const uint4*>(rows + (size_t)j * row_bytes + (size_t)v * 16);
-        const uint32_t u[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          acc[2 * q] = fmaf(w[j], bf16_lo(u[q]), acc[2 * q]);
-          acc[2 * q + 1] = fmaf(w[j], bf16_hi(u[q]), acc[2 * q + 1]);
-        }
-      }
-      uint4 o;
-      o.x = pack_bf16x2(acc[0], acc[1]);
-      o.y = pack_bf16x2(acc[2], acc[3]);
-      o.z = pack_bf16x2(acc[4], acc[5]);
-      o.w = pack_bf16x2(acc[6], acc[7]);
-      reinterpret_cast<uint4*>(y + tok * d)[v] = o;
-    }
-    __syncwarp();  // every lane is done reading this slot before lane 0 refills it
-  }
-}
-
 // One warp per token; lanes own 16-byte column chunks.
 __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* __restrict__ Y, int64_t T, int d,
                                                            int k, const int32_t* __restrict__ pos,
@@ -440,8 +372,8 @@ __global__ void __launch_bounds__(256) combine_f32_kernel(const float* __restric
   }
 }
 
-// EMOE_BULK_COPY=0 keeps the LDG/STG permute and combine (A/B runs); the
-// bulk kernels need enough token blocks to fill the GPU
+// EMOE_BULK_COPY=0 keeps the LDG/STG permute (A/B runs); the bulk kernel
+// needs enough token blocks to fill the GPU
 int bulk_min_blocks() {
   static const int v = [] {
     const char* e = getenv("EMOE_BULK_COPY");
@@ -481,7 +413,11 @@ void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int 
     return n;
   }();
   const int ny = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * sms, nblocks), row_bytes / 16 / 8));
-  if (!x_hi && nblocks >= bulk_min_blocks()) {  // large batches: rows moved by the TMA engine
+  // large batches of long rows (>= 4 KB): rows moved by the TMA engine.
+  // Shorter rows (Switch shape, 1.5 KB) stay on LDG/STG: 44 vs 35 us at
+  // T = 65,536 -- one bulk copy in flight per 1.5 KB row is too little
+  // parallelism (profiles/r02_bulk_copy_ab.txt)
+  if (!x_hi && nblocks >= bulk_min_blocks() && row_bytes >= 4096) {
     const size_t bsmem = (size_t)PB_WARPS * PB_SLOTS * row_bytes + (size_t)PB_WARPS * PB_SLOTS * 8 +
                          (4 * (size_t)E + (size_t)RT * k) * sizeof(int32_t);
     if (bsmem <= 200 * 1024) {
@@ -535,15 +471,6 @@ void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int
     EMOE_REQUIRE(d % 4 == 0, "combine: d must be a multiple of 4");
     combine_f32_kernel<<<dim3(nblocks, ny), 256, 0, s>>>(static_cast<const float*>(Y), T, d, k, pos, served_w,
                                                          static_cast<float*>(y));
-  } else if (nblocks >= bulk_min_blocks() && (size_t)CB_WARPS * 2 * k * d * 2 + CB_WARPS * 16 <= 200 * 1024) {
-    EMOE_REQUIRE(d % 8 == 0, "combine: d must be a multiple of 8");
-    const int csmem = CB_WARPS * 2 * k * d * 2 + CB_WARPS * 16;
-    if (csmem > 48 * 1024) ensure_max_dynamic_smem(reinterpret_cast<const void*>(combine_bulk_kernel), csmem);
-    int per_sm = 1;
-    EMOE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, combine_bulk_kernel, CB_WARPS * 32, csmem));
-    const int grid = (int)std::min<int64_t>(ceil_div(T, CB_WARPS), (int64_t)sms * std::max(per_sm, 1));
-    combine_bulk_kernel<<<grid, CB_WARPS * 32, csmem, s>>>(static_cast<const __nv_bfloat16*>(Y), T, d, k, pos,
-                                                           served_w, static_cast<__nv_bfloat16*>(y));
   } else {
     EMOE_REQUIRE(d % 8 == 0, "combine: d must be a multiple of 8");
     combine_bf16_kernel<<<dim3(nblocks, ny), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Y), T, d, k, pos,

@@ -460,9 +460,9 @@ torch.save(dict(y=y.cpu(), pos=ws["pos"].cpu(), row_token=rt, x_perm=xp[rt >= 0]
                                   (32, 768, 1024, 1, 50000, [0, 3, 9, 17, 21, 30], "relu"),
                                   (8, 512, 512, 2, 38000, [3], "swiglu")])
 def test_bulk_copy_permute_combine_bit_identical(args, tmp_path):
-    """Large batches move rows with cp.async.bulk (permute_bulk_kernel,
-    combine_bulk_kernel): positions, row sources, permuted rows and outputs
-    bit-identical to the LDG/STG kernels (EMOE_BULK_COPY=0)."""
+    """Large batches of long rows move them with cp.async.bulk
+    (permute_bulk_kernel): positions, row sources, permuted rows and outputs
+    bit-identical to the LDG/STG kernel (EMOE_BULK_COPY=0)."""
     import os
     import subprocess
     import sys
