@@ -153,61 +153,6 @@ __device__ __forceinline__ TileCoord decode_tile(int t, int total_mb, int n_bloc
   return c;
 }
 
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-// ---- cta_group::2 flavours of the PTX wrappers ----
-__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* desc, uint64_t* leader_bar, void* smem_dst,
-                                                 int32_t c0, int32_t c1, uint64_t hint) {
-  // completion bytes go to the leader CTA's barrier (peer bit cleared)
-  const uint32_t bar = smem_u32(leader_bar) & 0xFEFFFFFFu;
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar), "r"(c0), "r"(c1), "l"(hint)
-      : "memory");
-}
-__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                               uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// MC > 1: the weight tile is shared by MC CTAs on adjacent row blocks; each
-// loads 1/MC of it and multicasts it to the cluster (L2 -> SM traffic for B
-// drops MC-fold), and every CTA's MMA commit releases the stage in all of them
-__device__ __forceinline__ void tma_load_2d_mcast(const CUtensorMap* desc, uint64_t* bar, void* smem_dst, int32_t c0,
-                                                  int32_t c1, uint16_t mask, uint64_t hint) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
-      " [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(hint)
-      : "memory");
-}
-__device__ __forceinline__ void umma_commit_mcast(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {  // arrive on this offset in both CTAs
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"((uint16_t)0x3)
-      : "memory");
-}
-
 // ---- TMA bulk store of the epilogue boxes ----
 __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* desc, const void* smem_src, int32_t c0,
                                                   int32_t c1, uint64_t hint) {
@@ -225,18 +170,6 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* desc, const void
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
-// TMEM-empty signal: the accumulator reads are complete (tcgen05.wait::ld),
-// nothing else needs ordering, so the arrive is relaxed (a release arrive
-// costs a full memory barrier per tile)
-__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_leader_relaxed(uint64_t* bar) {  // CTA 0's copy of `bar`
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
-  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
-}
 
 // One warp's 32 rows x 64 bf16 columns (lane = row, packed[32] = its 128 B)
 // to global.  TMA path: the warp's staging box (128-B rows, SWIZZLE_128B:

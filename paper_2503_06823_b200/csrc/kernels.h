@@ -118,9 +118,9 @@ void launch_grouped_gemm(int epi, int cta_group, int mc, const CUtensorMap& ta, 
 
 // K1 for many experts (E in {32, 64, 96, 128}, bf16): gate GEMM on tcgen05
 // with the routing fused into its epilogue (gate_tc.cu).  tmap_gate: W_g [E][d]
-// with box rows E / gate_tc_cluster() (each CTA of a cluster multicasts one
-// slice of every gate k-block).  store_logits: also write o.logits.
-int gate_tc_cluster();
+// with box rows gate_tc_box_rows(E, d) (the slice of the gate one CTA
+// loads).  store_logits: also write o.logits.
+int gate_tc_box_rows(int E, int d);
 void launch_gate_route_tc(const CUtensorMap& tmap_x, const CUtensorMap& tmap_gate, const RouteArgs& a,
                           const RouteOut& o, bool store_logits, int num_sms, cudaStream_t s);
 

@@ -858,7 +858,7 @@ int emoe_layer_set_gate_host(emoe_layer* L, const void* wg) {
         // all 256 padded rows doubled the gate's operand bytes at E = 128)
         L->t_gate = make_tmap_bf16_2d(L->wg_pad, E, L->cfg.d_model, 256);
         L->t_gate2 = make_tmap_bf16_2d(L->wg_pad, E, L->cfg.d_model, 128);
-        if (E <= 128) L->t_gate_tc = make_tmap_bf16_2d(L->wg_pad, E, L->cfg.d_model, E / gate_tc_cluster());
+        if (E <= 128) L->t_gate_tc = make_tmap_bf16_2d(L->wg_pad, E, L->cfg.d_model, gate_tc_box_rows(E, L->cfg.d_model));
       }
       EMOE_CUDA(cudaMemcpy(L->wg_pad, wg, bytes, cudaMemcpyHostToDevice));
     }

@@ -408,12 +408,14 @@ torch.save(out, {out_path!r})
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("args", [(128, 768, 1, 65536), (128, 768, 1, 1000), (64, 512, 2, 3000), (32, 256, 1, 777),
-                                  (96, 512, 2, 2500)])
+                                  (96, 512, 2, 2500), (128, 1024, 1, 3000), (64, 2048, 2, 1300)])
 def test_fused_gate_route_bit_identical(args, tmp_path):
-    """E >= 32: the fused tcgen05 gate + route (default; logits stored or not)
-    gives bit-identical routing, weights, permutation and outputs to the
-    split path (dense gate GEMM -> logits -> route_from_logits_kernel,
-    EMOE_GATE_ROUTE=split), and both store the same logits."""
+    """E >= 32: the fused tcgen05 gate + route -- the CTA-pair form with the
+    gate resident in shared memory (default where it fits) and the streaming
+    form (EMOE_GATE_TC=stream), logits stored or not -- gives bit-identical
+    routing, weights, permutation and outputs to the split path (dense gate
+    GEMM -> logits -> route_from_logits_kernel, EMOE_GATE_ROUTE=split), and
+    all store the same logits."""
     import os
     import subprocess
     import sys
@@ -422,15 +424,17 @@ def test_fused_gate_route_bit_identical(args, tmp_path):
     root = Path(__file__).resolve().parent.parent
     E, d, k, T = args
     runs = {}
-    for name, env, keep in (("split", "split", True), ("fused", "fused", True), ("fused_nolog", "fused", False)):
+    for name, env, form, keep in (("split", "split", "", True), ("fused", "fused", "", True),
+                                  ("fused_nolog", "fused", "", False), ("stream", "fused", "stream", True)):
         out = tmp_path / f"{name}.pt"
         code = _GATE_SCRIPT.format(root=str(root), tests=str(root / "tests"), args=(E, d, k, T, keep),
                                    out_path=str(out))
-        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, EMOE_GATE_ROUTE=env),
-                       timeout=300)
+        subprocess.run([sys.executable, "-c", code], check=True,
+                       env=dict(os.environ, EMOE_GATE_ROUTE=env, EMOE_GATE_TC=form), timeout=300)
         runs[name] = torch.load(out)
     assert torch.equal(runs["split"]["logits"], runs["fused"]["logits"])
-    for name in ("fused", "fused_nolog"):
+    assert torch.equal(runs["split"]["logits"], runs["stream"]["logits"])
+    for name in ("fused", "fused_nolog", "stream"):
         for key, v in runs["split"].items():
             if key != "logits":
                 assert torch.equal(v, runs[name][key]), f"{name}: {key} differs from the split path"
