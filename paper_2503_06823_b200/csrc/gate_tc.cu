@@ -2,30 +2,32 @@
 // tcgen05 with the routing fused into its epilogue, so x is read once and
 // the fp32 logits never round-trip through HBM.
 //
-// Tile = 128 tokens x all E experts (UMMA M=128, N=E, K=16 per instruction,
-// fp32 accumulators in TMEM).  TMEM lane = token: after the accumulator is
-// read (tcgen05.ld 32x32b), every epilogue thread holds its token's whole
-// logits row in registers and routes it exactly as the per-thread reference
-// restatement does (route.cu route_one_token + route_tail: top-k descending
-// with ascending index on ties, route_token remap, served set and weights,
-// with the same operation order, so results are bit-identical to routing the
-// stored logits).
+// Tile = 128 tokens x all E experts (UMMA N = E, K = 16 per instruction,
+// fp32 accumulators in TMEM).  TMEM lane = token: every epilogue thread reads
+// its own token's logits row from TMEM in 32-column chunks and routes it in
+// registers -- a running top-k in one pass, and for the full-softmax weight
+// mode a second pass for the denominator -- with the operations, and the
+// order, of routing::route_one_token + route_tail (route_tail.cuh), so the
+// results are bit-identical to routing the stored logits.
 //
-// Hardware mapping (persistent, one CTA per SM, clusters of CN CTAs):
-//   warp 0      TMA producer: its own 128 x 64 x-tile per k-block, plus a
-//               1/CN slice of the gate's k-block multicast to every CTA of
-//               the cluster (the gate is the same for every tile, so a
-//               cluster shares each B k-block: L2 -> SM traffic for W_g drops
-//               CN-fold; at E = 128 the gate's reads would otherwise equal x's)
-//   warp 1      MMA issuer: tcgen05.mma.cta_group::1 per k-block, commit
-//               multicast to the stage's empty barrier of every cluster CTA
-//               (a stage is refilled only when all CN CTAs consumed it)
-//   warps 2..5  epilogue: TMEM double-buffered (2 x E columns) so tile i is
-//               routed while tile i+1's loads and MMAs run; per-tile expert
-//               counts in shared memory for the permutation (block_counts)
-// Every CTA of a cluster walks the same number of tiles (a CTA past the end
-// computes a zero-filled tile and stores nothing) so the multicast ring stays
-// in lockstep.
+// Two forms, both persistent with NG = 4 epilogue warp groups (TMEM holds
+// four accumulator buffers; group g routes the tiles with it % 4 == g, so four
+// tiles are routed concurrently while the next ones load -- the per-token
+// routing is a long dependent chain and one warp per SM sub-partition could
+// not hide it):
+//   pair    (default where it fits) CTA pairs, tcgen05.mma.cta_group::2,
+//           M = 256 tokens: each CTA keeps its half of W_g resident in shared
+//           memory for the whole kernel (E/2 x d x 2 bytes, 96 KB at E = 128,
+//           d = 768), so only x streams from HBM, through a ring of up to 8
+//           16-KB stages
+//   stream  each CTA streams its x tile and the gate k-blocks; a cluster of
+//           CN CTAs shares every gate k-block by TMA multicast (CN = 2
+//           default), and every CTA's MMA commit releases the stage in all of
+//           them (the rings run in lockstep; a CTA past the end computes a
+//           zero-filled tile and stores nothing)
+// warp 0 = TMA producer, warp 1 = MMA issuer (one thread), warps 2.. = the
+// epilogue groups.  Per-tile expert counts (block_counts, the permutation's
+// input) are tallied per group in shared memory.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -38,23 +40,225 @@ namespace emoe {
 namespace gatetc {
 
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
-constexpr int STAGES = 4;
-constexpr int NUM_THREADS = 192;
+constexpr int NG = 4;   // epilogue warp groups = TMEM accumulator buffers
+constexpr int NUM_THREADS = 64 + 128 * NG;
 constexpr int A_BYTES = 128 * BK * 2;
-constexpr int BAR_BYTES = 1024;  // mbarriers and the TMEM slot, before the epilogue rows
+constexpr int MAX_STAGES = 8;
+constexpr int BAR_BYTES = 1024;  // mbarriers and the TMEM slot
+constexpr int SMEM_LIMIT = 227 * 1024;
 
 struct Params {
   RouteArgs a;
   RouteOut o;
   int64_t ntiles;
   int k_blocks;
+  int stages;
   int store_logits;
 };
 
-__device__ __forceinline__ void epi_sync() {  // the 4 epilogue warps only
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+__device__ __forceinline__ void group_sync(int g) {  // the 4 warps of epilogue group g
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
 }
 
+// One 32-column chunk of this thread's logits row (+ the caller's bias).
+__device__ __forceinline__ void load_chunk(uint32_t taddr, int c, int64_t t, bool live, const RouteArgs& a, int NE,
+                                           float (&v)[32]) {
+  uint32_t r[32];
+  tmem_ld_32x32b_x32(taddr + c * 32, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if (live && a.bias) {
+    const float4* b4 = reinterpret_cast<const float4*>(a.bias + t * NE + c * 32);
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      const float4 bb = __ldg(b4 + j / 4);
+      v[j] += bb.x;
+      v[j + 1] += bb.y;
+      v[j + 2] += bb.z;
+      v[j + 3] += bb.w;
+    }
+  }
+}
+
+// Route this thread's token (TMEM lane) of the tile at taddr.  Top-k by a
+// running insertion with strict comparisons in index order (a value displaces
+// an entry only when larger, so ties keep the lower index: the order of
+// route_one_token's repeated argmax); then route_tail's remap, served set
+// and weights.  Every TMEM read is done when it returns.
+template <int NE>
+__device__ __forceinline__ void route_from_tmem(uint32_t taddr, int64_t t, bool live, const Params& p,
+                                                const routing::SharedRouteState& st, int* counts) {
+  const RouteArgs& a = p.a;
+  const RouteOut& o = p.o;
+  const int k = a.k;
+  float tv[8];
+  int ti[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    tv[r] = 0.0f;
+    ti[r] = -1;
+  }
+  int n = 0;
+#pragma unroll 1
+  for (int c = 0; c < NE / 32; ++c) {
+    float v[32];
+    load_chunk(taddr, c, t, live, a, NE, v);
+    if (live && p.store_logits && o.logits) {
+      float4* dst = reinterpret_cast<float4*>(o.logits + t * NE + c * 32);
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) dst[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+    if (k == 1) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (ti[0] < 0 || v[j] > tv[0]) {
+          tv[0] = v[j];
+          ti[0] = c * 32 + j;
+        }
+    } else if (k == 2) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int e = c * 32 + j;
+        if (ti[0] < 0 || v[j] > tv[0]) {
+          tv[1] = tv[0];
+          ti[1] = ti[0];
+          tv[0] = v[j];
+          ti[0] = e;
+        } else if (ti[1] < 0 || v[j] > tv[1]) {
+          tv[1] = v[j];
+          ti[1] = e;
+        }
+      }
+    } else {
+#pragma unroll 1
+      for (int j = 0; j < 32; ++j) {
+        const float x = v[j];
+        if (n == k && !(x > tv[k - 1])) continue;
+        int pos = n < k ? n : k - 1;
+        while (pos > 0 && x > tv[pos - 1]) {
+          tv[pos] = tv[pos - 1];
+          ti[pos] = ti[pos - 1];
+          --pos;
+        }
+        tv[pos] = x;
+        ti[pos] = c * 32 + j;
+        if (n < k) ++n;
+      }
+    }
+  }
+  // route_token remap (expert_store.cpp:206-220, engine.cpp:533-537)
+  int ex = -1, rk = -1, hit = 0;
+  if (live) {
+    if (st.n_res == 0) {
+      ex = ti[0];
+      if (!a.forced_miss) atomicExch(a.error_flag, 3);
+    } else {
+      for (int r = 0; r < k; ++r)
+        if (st.resident[ti[r]]) {
+          ex = ti[r];
+          rk = r;
+          hit = r == 0;
+          break;
+        }
+      if (rk < 0) ex = st.fallback;
+    }
+  }
+  // full-softmax weights: the denominator over every logit in index order
+  // (route_tail's serial sum), and the fallback expert's logit
+  float den1 = 0.0f, vex = 0.0f;
+  if (a.weight_mode != 0) {
+    const float mx = tv[0];
+#pragma unroll 1
+    for (int c = 0; c < NE / 32; ++c) {
+      float v[32];
+      load_chunk(taddr, c, t, live, a, NE, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        den1 += expf(v[j] - mx);
+        if (c * 32 + j == ex) vex = v[j];
+      }
+    }
+  }
+  if (!live) return;
+  if (o.topk_idx)
+    for (int r = 0; r < k; ++r) o.topk_idx[t * k + r] = ti[r];
+  if (o.route_expert) o.route_expert[t] = ex;
+  if (o.route_rank) o.route_rank[t] = rk;
+  if (o.route_hit) o.route_hit[t] = (uint8_t)hit;
+  int si[8];
+  float sv[8];  // the served experts' logits
+  int ns = 0;
+  if (st.n_res > 0) {
+    if (rk >= 0) {
+      for (int r = 0; r < k; ++r)
+        if (st.resident[ti[r]]) {
+          sv[ns] = tv[r];
+          si[ns++] = ti[r];
+        }
+    } else {
+      sv[ns] = a.weight_mode == 0 ? 0.0f : vex;  // mode 0: a lone served expert's weight is expf(0) / expf(0)
+      si[ns++] = ex;
+    }
+  }
+  float w[8];
+  if (a.weight_mode == 0) {
+    if (ns > 0) {
+      const float mx = sv[0];
+      float den = 0.0f;
+      for (int j = 0; j < ns; ++j) {
+        w[j] = expf(sv[j] - mx);
+        den += w[j];
+      }
+      for (int j = 0; j < ns; ++j) w[j] = w[j] / den;
+    }
+  } else {
+    const float mx = tv[0];
+    for (int j = 0; j < ns; ++j) w[j] = expf(sv[j] - mx) / den1;
+  }
+  for (int j = 0; j < k; ++j) {
+    o.served_idx[t * k + j] = j < ns ? si[j] : -1;
+    o.served_w[t * k + j] = j < ns ? w[j] : 0.0f;
+  }
+  for (int j = 0; j < ns; ++j) atomicAdd(&counts[si[j]], 1);
+}
+
+// The epilogue of one tile for epilogue group g: route, release the TMEM
+// buffer, flush the tile's expert counts.
+template <int NE>
+__device__ __forceinline__ void epilogue_tile(uint32_t taddr, int64_t tile, int quarter, int lane, int g,
+                                              const Params& p, const routing::SharedRouteState& st, int* counts,
+                                              uint64_t* tempty, bool to_leader) {
+  const int64_t t = tile * 128 + quarter * 32 + lane;
+  const bool live = tile < p.ntiles && t < p.a.T;
+  route_from_tmem<NE>(taddr, t, live, p, st, counts);
+  tc_fence_before();
+  if (lane == 0) {
+    if (to_leader)
+      mbar_arrive_leader_relaxed(tempty);
+    else
+      mbar_arrive_relaxed(tempty);
+  }
+  if (tile < p.ntiles) {
+    group_sync(g);  // every token of the tile counted
+    const int tg = (threadIdx.x - 64) % 128;
+    if (p.o.block_counts)
+      for (int e = tg; e < p.a.E; e += 128) {
+        p.o.block_counts[tile * p.a.E + e] = counts[e];
+        counts[e] = 0;
+      }
+    group_sync(g);
+  }
+}
+
+template <int NE>
+constexpr int tmem_cols() {
+  return NG * NE <= 128 ? 128 : (NG * NE <= 256 ? 256 : 512);
+}
+
+// ---------------------------------------------------------------------------
+// stream form
+// ---------------------------------------------------------------------------
 template <int NE, int CN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gate_route_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_g,
@@ -62,20 +266,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr int B_BYTES = NE * BK * 2;
   constexpr int SLICE_ROWS = NE / CN;
   constexpr int SLICE_BYTES = SLICE_ROWS * BK * 2;
-  constexpr int TMEM_COLS = 2 * NE <= 64 ? 64 : (2 * NE <= 128 ? 128 : 256);
+  constexpr int TMEM_COLS = tmem_cols<NE>();
   constexpr uint16_t MASK = (uint16_t)((1u << CN) - 1u);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = p.stages;
   uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + STAGES * A_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_b + STAGES * B_BYTES);
-  uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* tfull_bar = empty_bar + STAGES;  // [2]
-  uint64_t* tempty_bar = tfull_bar + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  // the epilogue's logits rows, one per token: [128][NE + 1] fp32 (the pitch
-  // puts a warp's per-thread row accesses on 32 distinct banks)
-  float* s_rows = reinterpret_cast<float*>(smem_b + STAGES * B_BYTES + BAR_BYTES);
+  uint8_t* smem_b = smem + S * A_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_b + S * B_BYTES);
+  uint64_t* empty_bar = full_bar + MAX_STAGES;
+  uint64_t* tfull_bar = empty_bar + MAX_STAGES;  // [NG]
+  uint64_t* tempty_bar = tfull_bar + NG;         // [NG]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + NG);
+  int* g_counts = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(full_bar) + BAR_BYTES);  // [NG][NE]
   __shared__ routing::SharedRouteState st;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -83,18 +286,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int64_t cluster_id = blockIdx.x / CN, n_clusters = gridDim.x / CN;
   // every CTA of a cluster walks the same number of tile slots
   const int64_t n_iter = (ceil_div(p.ntiles, CN) + n_clusters - 1 - cluster_id) / n_clusters;
-  const RouteArgs& a = p.a;
-  const int E = a.E;
 
-  routing::load_route_state(st, a);  // residency, scores, the token-independent fallback (all threads)
+  routing::load_route_state(st, p.a);
+  for (int i = threadIdx.x; i < NG * NE; i += NUM_THREADS) g_counts[i] = 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_x);
     tma_prefetch_desc(&tmap_g);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], CN);  // one MMA commit from every CTA of the cluster
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NG; ++b) {
       mbar_init(&tfull_bar[b], 1);
       mbar_init(&tempty_bar[b], 4);
     }
@@ -129,16 +331,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                               kCacheEvictLast);
           else
             tma_load_2d(&tmap_g, &full_bar[stage], bdst, kb * BK, 0, kCacheEvictLast);
-          if (++stage == STAGES) {
+          if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
       // tail: every peer's last commits to this CTA's empty barriers have landed
-      for (int i = 0; i < STAGES; ++i) {
+      for (int i = 0; i < S; ++i) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
-        if (++stage == STAGES) {
+        if (++stage == S) {
           stage = 0;
           phase ^= 1;
         }
@@ -150,8 +352,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t it = 0; it < n_iter; ++it) {
-        const int buf = (int)(it & 1);
-        mbar_wait(&tempty_bar[buf], (uint32_t)((it >> 1) & 1) ^ 1);
+        const int buf = (int)(it % NG);
+        mbar_wait(&tempty_bar[buf], (uint32_t)((it / NG) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + buf * NE;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
@@ -166,7 +368,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             umma_commit_mcast(&empty_bar[stage], MASK);
           else
             umma_commit(&empty_bar[stage]);
-          if (++stage == STAGES) {
+          if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
@@ -175,58 +377,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
-    // epilogue: TMEM lane = token; each thread moves its row to shared memory
-    // (adding the bias / storing the logits on the way) and routes it
-    const int quarter = warp & 3;
-    const RouteOut& o = p.o;
-    float* row = s_rows + (quarter * 32 + lane) * (NE + 1);
-    for (int64_t it = 0; it < n_iter; ++it) {
-      const int buf = (int)(it & 1);
+    const int g = (warp - 2) / 4, quarter = warp & 3;
+    for (int64_t it = g; it < n_iter; it += NG) {
       const int64_t tile = (cluster_id + it * n_clusters) * CN + rank;
-      const int64_t t = tile * 128 + quarter * 32 + lane;
-      const bool live = tile < p.ntiles && t < a.T;
-      mbar_wait(&tfull_bar[buf], (uint32_t)((it >> 1) & 1));
+      mbar_wait(&tfull_bar[g], (uint32_t)((it / NG) & 1));
       tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + buf * NE;
-#pragma unroll 1
-      for (int c = 0; c < NE / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr + c * 32, r);
-        tmem_ld_wait();
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (live && a.bias) {
-          const float4* b4 = reinterpret_cast<const float4*>(a.bias + t * NE + c * 32);
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float4 bb = __ldg(b4 + j / 4);
-            v[j] += bb.x;
-            v[j + 1] += bb.y;
-            v[j + 2] += bb.z;
-            v[j + 3] += bb.w;
-          }
-        }
-        if (live && p.store_logits && o.logits) {
-          float4* dst = reinterpret_cast<float4*>(o.logits + t * NE + c * 32);
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) dst[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) row[c * 32 + j] = v[j];
-      }
-      tc_fence_before();
-      if (lane == 0) mbar_arrive_relaxed(&tempty_bar[buf]);  // the MMAs of tile i+2 may start
-      if (tile < p.ntiles) {
-        if (live) routing::route_one_token(row, t, a, o, st);
-        epi_sync();  // every token of the tile counted
-        if (o.block_counts)
-          for (int e = threadIdx.x - 64; e < E; e += 128) {
-            o.block_counts[tile * E + e] = st.counts[e];
-            st.counts[e] = 0;
-          }
-        epi_sync();
-      }
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + g * NE;
+      epilogue_tile<NE>(taddr, tile, quarter, lane, g, p, st, g_counts + g * NE, &tempty_bar[g], false);
     }
   }
 
@@ -240,37 +397,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-
 // ---------------------------------------------------------------------------
-// CTA-pair form with the gate resident in shared memory (E/2 x d x 2 bytes
-// per CTA fits next to the x ring, e.g. 96 KB at E = 128, d = 768): each pair
-// computes 256 tokens x E per tile with tcgen05.mma.cta_group::2 (M = 256; A =
-// each CTA's own 128 token rows, B = each CTA's resident half of W_g), so only
-// x streams from HBM -- no per-tile reload of W_g into shared memory, half the
-// L2 -> SM bytes of the streaming form.  Each CTA's TMEM holds its own 128
-// tokens x all E experts, so the epilogue is the streaming form's.
+// pair form: the gate resident in shared memory, cta_group::2
 // ---------------------------------------------------------------------------
-constexpr int PAIR_STAGES = 3;
-
 template <int NE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gate_route_tc2_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_g,
                           Params p) {
   constexpr int BH = NE / 2;             // gate rows this CTA holds
   constexpr int KB_BYTES = BH * BK * 2;  // one resident k-block
-  constexpr int TMEM_COLS = 2 * NE <= 64 ? 64 : (2 * NE <= 128 ? 128 : 256);
+  constexpr int TMEM_COLS = tmem_cols<NE>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* smem_a = smem;                                        // [PAIR_STAGES][A_BYTES]
-  uint8_t* b_res = smem + PAIR_STAGES * A_BYTES;                 // [k_blocks][KB_BYTES]
+  const int S = p.stages;
+  uint8_t* smem_a = smem;               // [S][A_BYTES]
+  uint8_t* b_res = smem + S * A_BYTES;  // [k_blocks][KB_BYTES]
   uint8_t* bar_area = b_res + (size_t)p.k_blocks * KB_BYTES;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(bar_area);
-  uint64_t* empty_bar = full_bar + PAIR_STAGES;
-  uint64_t* tfull_bar = empty_bar + PAIR_STAGES;  // [2]
-  uint64_t* tempty_bar = tfull_bar + 2;           // [2]
-  uint64_t* bres_bar = tempty_bar + 2;
+  uint64_t* empty_bar = full_bar + MAX_STAGES;
+  uint64_t* tfull_bar = empty_bar + MAX_STAGES;  // [NG]
+  uint64_t* tempty_bar = tfull_bar + NG;         // [NG]
+  uint64_t* bres_bar = tempty_bar + NG;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_bar + 1);
-  float* s_rows = reinterpret_cast<float*>(bar_area + BAR_BYTES);  // [128][NE + 1]
+  int* g_counts = reinterpret_cast<int*>(bar_area + BAR_BYTES);  // [NG][NE]
   __shared__ routing::SharedRouteState st;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -279,18 +428,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int64_t pair_id = blockIdx.x / 2, n_pairs = gridDim.x / 2;
   const int64_t ntiles2 = ceil_div(p.ntiles, 2);  // 256-token pair tiles
   const int64_t n_iter = (ntiles2 + n_pairs - 1 - pair_id) / n_pairs;
-  const RouteArgs& a = p.a;
-  const int E = a.E;
 
-  routing::load_route_state(st, a);
+  routing::load_route_state(st, p.a);
+  for (int i = threadIdx.x; i < NG * NE; i += NUM_THREADS) g_counts[i] = 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_x);
     tma_prefetch_desc(&tmap_g);
-    for (int s = 0; s < PAIR_STAGES; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NG; ++b) {
       mbar_init(&tfull_bar[b], 1);
       mbar_init(&tempty_bar[b], 8);  // 4 epilogue warps x 2 CTAs (the leader's copy counts)
     }
@@ -323,15 +471,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * A_BYTES);
           tma_load_2d_pair(&tmap_x, &full_bar[stage], smem_a + stage * A_BYTES, kb * BK,
                            (int32_t)(tile2 * 256 + rank * 128), kCacheEvictFirst);
-          if (++stage == PAIR_STAGES) {
+          if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
-      for (int i = 0; i < PAIR_STAGES; ++i) {  // the leader's last commits to this CTA have landed
+      for (int i = 0; i < S; ++i) {  // the leader's last commits to this CTA have landed
         mbar_wait(&empty_bar[stage], phase ^ 1);
-        if (++stage == PAIR_STAGES) {
+        if (++stage == S) {
           stage = 0;
           phase ^= 1;
         }
@@ -345,8 +493,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t it = 0; it < n_iter; ++it) {
-        const int buf = (int)(it & 1);
-        mbar_wait(&tempty_bar[buf], (uint32_t)((it >> 1) & 1) ^ 1);
+        const int buf = (int)(it % NG);
+        mbar_wait(&tempty_bar[buf], (uint32_t)((it / NG) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + buf * NE;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
@@ -358,7 +506,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int kk = 0; kk < BK / 16; ++kk)
             umma_bf16_pair(tmem_d, a_desc + (uint64_t)(kk * 2), b_desc + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
           umma_commit_pair(&empty_bar[stage]);
-          if (++stage == PAIR_STAGES) {
+          if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
@@ -367,61 +515,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
-    const int quarter = warp & 3;
-    const RouteOut& o = p.o;
-    float* row = s_rows + (quarter * 32 + lane) * (NE + 1);
-    for (int64_t it = 0; it < n_iter; ++it) {
-      const int buf = (int)(it & 1);
+    const int g = (warp - 2) / 4, quarter = warp & 3;
+    for (int64_t it = g; it < n_iter; it += NG) {
       const int64_t tile = (pair_id + it * n_pairs) * 2 + rank;  // this CTA's 128-token block
-      const int64_t t = tile * 128 + quarter * 32 + lane;
-      const bool live = tile < p.ntiles && t < a.T;
-      mbar_wait(&tfull_bar[buf], (uint32_t)((it >> 1) & 1));
+      mbar_wait(&tfull_bar[g], (uint32_t)((it / NG) & 1));
       tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + buf * NE;
-#pragma unroll 1
-      for (int c = 0; c < NE / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr + c * 32, r);
-        tmem_ld_wait();
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (live && a.bias) {
-          const float4* b4 = reinterpret_cast<const float4*>(a.bias + t * NE + c * 32);
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float4 bb = __ldg(b4 + j / 4);
-            v[j] += bb.x;
-            v[j + 1] += bb.y;
-            v[j + 2] += bb.z;
-            v[j + 3] += bb.w;
-          }
-        }
-        if (live && p.store_logits && o.logits) {
-          float4* dst = reinterpret_cast<float4*>(o.logits + t * NE + c * 32);
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) dst[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) row[c * 32 + j] = v[j];
-      }
-      tc_fence_before();
-      if (lane == 0) {
-        if (leader)
-          mbar_arrive_relaxed(&tempty_bar[buf]);
-        else
-          mbar_arrive_leader_relaxed(&tempty_bar[buf]);
-      }
-      if (tile < p.ntiles) {
-        if (live) routing::route_one_token(row, t, a, o, st);
-        epi_sync();
-        if (o.block_counts)
-          for (int e = threadIdx.x - 64; e < E; e += 128) {
-            o.block_counts[tile * E + e] = st.counts[e];
-            st.counts[e] = 0;
-          }
-        epi_sync();
-      }
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + g * NE;
+      epilogue_tile<NE>(taddr, tile, quarter, lane, g, p, st, g_counts + g * NE, &tempty_bar[g], !leader);
     }
   }
 
@@ -432,17 +532,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-template <int NE>
-int pair_smem_bytes(int k_blocks) {
-  return 1024 + PAIR_STAGES * A_BYTES + k_blocks * (NE / 2) * BK * 2 + BAR_BYTES + 128 * (NE + 1) * 4;
+// shared memory of the two forms at `stages` ring stages
+int smem_bytes(bool pair, int E, int k_blocks, int stages) {
+  const int fixed = 1024 + BAR_BYTES + NG * E * 4;
+  return pair ? fixed + stages * A_BYTES + k_blocks * (E / 2) * BK * 2 : fixed + stages * (A_BYTES + E * BK * 2);
+}
+int max_stages(bool pair, int E, int k_blocks) {
+  int s = MAX_STAGES;
+  while (s > 2 && smem_bytes(pair, E, k_blocks, s) > SMEM_LIMIT) --s;
+  return s;
 }
 
-template <int NE>
-void launch_pair(const CUtensorMap& tx, const CUtensorMap& tg, const Params& p, int num_sms, cudaStream_t s) {
-  auto kernel = gate_route_tc2_kernel<NE>;
-  const int smem = pair_smem_bytes<NE>(p.k_blocks);
+template <typename K>
+void launch(K kernel, int cluster, int grid, int smem, const CUtensorMap& tx, const CUtensorMap& tg, const Params& p,
+            cudaStream_t s) {
   ensure_max_dynamic_smem(reinterpret_cast<const void*>(kernel), smem);
-  const int grid = (int)std::min<int64_t>(num_sms / 2 * 2, ceil_div(p.ntiles, 2) * 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NUM_THREADS);
@@ -450,7 +554,7 @@ void launch_pair(const CUtensorMap& tx, const CUtensorMap& tg, const Params& p, 
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = cluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -458,47 +562,36 @@ void launch_pair(const CUtensorMap& tx, const CUtensorMap& tg, const Params& p, 
   EMOE_CUDA(cudaLaunchKernelEx(&cfg, kernel, tx, tg, p));
   EMOE_CUDA(cudaGetLastError());
   count_launch();
+}
+
+template <int NE>
+void launch_pair(const CUtensorMap& tx, const CUtensorMap& tg, Params p, int num_sms, cudaStream_t s) {
+  p.stages = max_stages(true, NE, p.k_blocks);
+  const int grid = (int)std::min<int64_t>(num_sms / 2 * 2, ceil_div(p.ntiles, 2) * 2);
+  launch(gate_route_tc2_kernel<NE>, 2, grid, smem_bytes(true, NE, p.k_blocks, p.stages), tx, tg, p, s);
 }
 
 template <int NE, int CN>
-void launch_one(const CUtensorMap& tx, const CUtensorMap& tg, const Params& p, int num_sms, cudaStream_t s) {
-  auto kernel = gate_route_tc_kernel<NE, CN>;
-  const int smem = 1024 + STAGES * (A_BYTES + NE * BK * 2) + BAR_BYTES + 128 * (NE + 1) * 4;
-  ensure_max_dynamic_smem(reinterpret_cast<const void*>(kernel), smem);
+void launch_stream(const CUtensorMap& tx, const CUtensorMap& tg, Params p, int num_sms, cudaStream_t s) {
+  p.stages = max_stages(false, NE, p.k_blocks);
   const int grid = (int)std::min<int64_t>(num_sms / CN * CN, ceil_div(p.ntiles, CN) * CN);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CN;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  EMOE_CUDA(cudaLaunchKernelEx(&cfg, kernel, tx, tg, p));
-  EMOE_CUDA(cudaGetLastError());
-  count_launch();
+  launch(gate_route_tc_kernel<NE, CN>, CN, grid, smem_bytes(false, NE, p.k_blocks, p.stages), tx, tg, p, s);
 }
 
 }  // namespace gatetc
 
 // Which form runs (EMOE_GATE_TC=pair|stream overrides for A/B runs): the
-// CTA-pair form whenever the gate half fits in shared memory next to the x
-// ring, else the streaming form with the gate k-blocks multicast over a
-// cluster of EMOE_GATE_CLUSTER (default 2) CTAs.
+// pair form whenever the gate half fits in shared memory next to a ring of
+// at least 4 stages, else the stream form with the gate k-blocks multicast
+// over a cluster of EMOE_GATE_CLUSTER (default 2) CTAs.
 static bool gate_tc_pair(int E, int d) {
   static const int force = [] {
     const char* v = getenv("EMOE_GATE_TC");
     return v ? (std::strcmp(v, "pair") == 0 ? 1 : std::strcmp(v, "stream") == 0 ? 0 : -1) : -1;
   }();
-  const int k_blocks = d / gatetc::BK;
-  const int smem = 1024 + gatetc::PAIR_STAGES * gatetc::A_BYTES + k_blocks * (E / 2) * gatetc::BK * 2 +
-                   gatetc::BAR_BYTES + 128 * (E + 1) * 4;
-  const bool fits = smem <= 227 * 1024;
-  return force == 1 ? fits : (force == 0 ? false : fits);
+  const int kb = d / gatetc::BK;
+  const bool fits = gatetc::smem_bytes(true, E, kb, 4) <= gatetc::SMEM_LIMIT;
+  return force == 0 ? false : fits;
 }
 
 static int gate_tc_cluster() {
@@ -522,6 +615,7 @@ void launch_gate_route_tc(const CUtensorMap& tmap_x, const CUtensorMap& tmap_gat
   p.o = o;
   p.ntiles = ceil_div(a.T, 128);
   p.k_blocks = a.d / gatetc::BK;
+  p.stages = 0;
   p.store_logits = store_logits ? 1 : 0;
   if (p.ntiles == 0) return;
   if (gate_tc_pair(a.E, a.d)) {
@@ -534,15 +628,16 @@ void launch_gate_route_tc(const CUtensorMap& tmap_x, const CUtensorMap& tmap_gat
     return;
   }
   const int cn = gate_tc_cluster();
+  EMOE_REQUIRE(gatetc::smem_bytes(false, a.E, p.k_blocks, 2) <= gatetc::SMEM_LIMIT, "gate_tc: tile too large");
   switch (a.E) {
-#define EMOE_GATE_CASE(NEV)                                                    \
-  case NEV:                                                                    \
-    if (cn == 1)                                                               \
-      gatetc::launch_one<NEV, 1>(tmap_x, tmap_gate_slice, p, num_sms, s);      \
-    else if (cn == 2)                                                          \
-      gatetc::launch_one<NEV, 2>(tmap_x, tmap_gate_slice, p, num_sms, s);      \
-    else                                                                       \
-      gatetc::launch_one<NEV, 4>(tmap_x, tmap_gate_slice, p, num_sms, s);      \
+#define EMOE_GATE_CASE(NEV)                                                        \
+  case NEV:                                                                        \
+    if (cn == 1)                                                                   \
+      gatetc::launch_stream<NEV, 1>(tmap_x, tmap_gate_slice, p, num_sms, s);       \
+    else if (cn == 2)                                                              \
+      gatetc::launch_stream<NEV, 2>(tmap_x, tmap_gate_slice, p, num_sms, s);       \
+    else                                                                           \
+      gatetc::launch_stream<NEV, 4>(tmap_x, tmap_gate_slice, p, num_sms, s);       \
     break;
     EMOE_GATE_CASE(32)
     EMOE_GATE_CASE(64)
