@@ -45,7 +45,7 @@ constexpr int NUM_THREADS = 64 + 128 * NG;
 constexpr int A_BYTES = 128 * BK * 2;
 constexpr int MAX_STAGES = 8;
 constexpr int BAR_BYTES = 1024;  // mbarriers and the TMEM slot
-constexpr int SMEM_LIMIT = 227 * 1024;
+constexpr int SMEM_LIMIT = 227 * 1024 - 4096;  // dynamic bytes: static shared state and alignment slack stay free
 
 struct Params {
   RouteArgs a;
