@@ -262,6 +262,38 @@ int emoe_ep_set_profiling(emoe_ep* ep, int enable);
 int emoe_ep_stage_times(emoe_ep* ep, float* ms);
 int emoe_ep_destroy(emoe_ep* ep);
 
+/* ========================================================================
+ * Expert parallelism over NCCL all-to-all without host synchronisation (the
+ * capacity-padded form; the baseline the peer-memory form
+ * replaces).  Every (source, destination) pair owns a fixed chunk of cap
+ * rows in the caller's send / receive / return buffers ([world][cap][d]
+ * bf16), so the caller's all-to-alls take equal splits and no host-side
+ * sizes.  Same split (cum_shares) and bit-identical outputs as emoe_ep_*.
+ * Per forward, all on one stream:
+ *   emoe_epx_route      route + counts (the layer workspace's counts [E] i32);
+ *                       the caller all-gathers them into table [world][E]
+ *   emoe_epx_dispatch   split layout from the table + permute into the send
+ *                       chunks (a pair over cap rows drops the forward's rows on
+ *                       every rank: status 2)
+ *   (caller: all_to_all send -> receive)
+ *   emoe_epx_ffn        grouped FFN over the received chunks, outputs into
+ *                       the return chunks (same rows)
+ *   (caller: all_to_all return -> returned)
+ *   emoe_epx_combine    local combine from the returned chunks
+ * cap_rows 0 = the layer's rows_cap (every pair may carry all of a source's
+ * rows); emoe_epx_cap_rows reads the padded value back. */
+typedef struct emoe_epx emoe_epx;
+int emoe_epx_create(emoe_layer* layer, int world, int rank, const int64_t* cum_shares, int64_t cap_rows,
+                    emoe_epx** out);
+int emoe_epx_cap_rows(const emoe_epx* x, int64_t* cap_rows);
+int emoe_epx_route(emoe_epx* x, const void* x_dev, const float* logits_in_dev, int64_t T, void* stream);
+int emoe_epx_dispatch(emoe_epx* x, const int32_t* table_dev, const void* x_dev, int64_t T, void* send_chunks_dev,
+                      void* stream);
+int emoe_epx_ffn(emoe_epx* x, const void* recv_chunks_dev, void* return_chunks_dev, void* stream);
+int emoe_epx_combine(emoe_epx* x, const void* returned_chunks_dev, void* y_dev, int64_t T, void* stream);
+int emoe_epx_status(emoe_epx* x, void* stream, int* status, int64_t* rows_computed);
+int emoe_epx_destroy(emoe_epx* x);
+
 /* Device pointers of the last forward's intermediates (valid until the next
  * call on the layer).  Sizes: T tokens, R = rows_cap permuted rows. */
 typedef struct {

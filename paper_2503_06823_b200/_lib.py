@@ -86,6 +86,14 @@ _decl("emoe_ep_layout", vp, vp, vp, vp, vp, vp)
 _decl("emoe_ep_set_profiling", vp, C.c_int)
 _decl("emoe_ep_stage_times", vp, vp)
 _decl("emoe_ep_destroy", vp)
+_decl("emoe_epx_create", vp, C.c_int, C.c_int, vp, i64, C.POINTER(vp))
+_decl("emoe_epx_cap_rows", vp, C.POINTER(i64))
+_decl("emoe_epx_route", vp, vp, vp, i64, vp)
+_decl("emoe_epx_dispatch", vp, vp, vp, i64, vp, vp)
+_decl("emoe_epx_ffn", vp, vp, vp, vp)
+_decl("emoe_epx_combine", vp, vp, vp, i64, vp)
+_decl("emoe_epx_status", vp, vp, C.POINTER(C.c_int), C.POINTER(i64))
+_decl("emoe_epx_destroy", vp)
 IPC_HANDLE_BYTES = 64
 _decl("emoe_layer_set_profiling", vp, C.c_int)
 _decl("emoe_layer_stage_times", vp, vp)
@@ -123,7 +131,8 @@ EXPORTED = [
     "emoe_moe_forward", "emoe_moe_forward_host", "emoe_moe_forward_host_async", "emoe_layer_wait_host", "emoe_route", "emoe_layer_gate_demand", "emoe_route_permute", "emoe_layer_set_route_residency",
     "emoe_ffn_segments", "emoe_combine", "emoe_ep_create", "emoe_ep_ipc_handle", "emoe_ep_open_peers",
     "emoe_ep_forward", "emoe_ep_status", "emoe_ep_stats", "emoe_ep_layout", "emoe_ep_set_profiling",
-    "emoe_ep_stage_times", "emoe_ep_destroy", "emoe_layer_workspace", "emoe_layer_share_workspace", "emoe_layer_set_profiling",
+    "emoe_ep_stage_times", "emoe_ep_destroy", "emoe_epx_create", "emoe_epx_cap_rows", "emoe_epx_route",
+    "emoe_epx_dispatch", "emoe_epx_ffn", "emoe_epx_combine", "emoe_epx_status", "emoe_epx_destroy", "emoe_layer_workspace", "emoe_layer_share_workspace", "emoe_layer_set_profiling",
     "emoe_layer_stage_times", "emoe_kernel_launches", "emoe_predictor_create",
     "emoe_predictor_destroy", "emoe_predictor_reset", "emoe_predictor_break_chain", "emoe_hist_update", "emoe_hist_update_host", "emoe_predictor_counts_host",
     "emoe_predictor_set_counts_host", "emoe_predictor_count_size", "emoe_predictor_counts_dev",

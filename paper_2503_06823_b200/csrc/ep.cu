@@ -263,6 +263,121 @@ __global__ void __launch_bounds__(256) ep_bar0_kernel(PeerSym sym, int W, int ra
   }
 }
 
+
+// NCCL chunk transport (ep.py NcclExpertParallelMoE): every (source,
+// destination) pair owns a fixed chunk of `cap` rows in the send / receive /
+// return buffers, so the all-to-all needs no host-side split sizes.  From the
+// all-gathered count table (device), every rank derives the same split as
+// ep_bar0_kernel, then: its send pieces into its send chunks (chunk q = rows
+// [q cap, (q + 1) cap), pieces in expert order), and its receive segments
+// (source, owned expert) in compact order with the shift of each into the
+// receive chunks (which the return chunks mirror).  A pair over `cap` rows
+// drops the forward's rows on every rank and sets status 2.
+struct ChunkArgs {
+  const int32_t* table;        // [W][E] real counts of every source (all-gathered)
+  const int64_t* seg_offsets;  // [E+1] this rank's padded local segments
+  const int64_t* cum;          // [E][W]
+  const int32_t* owned;        // [n_owned]
+  int n_owned, pad;
+  int64_t cap;
+  int64_t* piece_end;    // [E][W]
+  int64_t* piece_shift;  // [E][W]: send-buffer row = local row + shift
+  int64_t* recv_segs;    // [W * n_owned + 1] compact
+  int64_t* a_shift;      // [W * n_owned]: receive-chunk row = compact row + shift
+  int64_t* stats;        // [kStats]
+  int* status;
+};
+
+__global__ void __launch_bounds__(256) epx_layout_kernel(int W, int rank, int E, ChunkArgs a) {
+  __shared__ int32_t cr[kMaxPeers][kMaxE];
+  __shared__ int64_t pre[kMaxPeers][kMaxE];
+  __shared__ int64_t bnd[kMaxE][kMaxPeers];
+  __shared__ int64_t tot[kMaxPeers][kMaxPeers];
+  __shared__ int overflow;
+  const int64_t pad = a.pad;
+  for (int i = threadIdx.x; i < W * E; i += blockDim.x) cr[i / E][i % E] = a.table[i];
+  if (threadIdx.x == 0) overflow = 0;
+  __syncthreads();
+  auto padded = [&](int s, int e) -> int64_t { return ((int64_t)cr[s][e] + pad - 1) / pad * pad; };
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int64_t n = 0;
+    for (int s = 0; s < W; ++s) {
+      pre[s][e] = n;
+      n += padded(s, e);
+    }
+    const int64_t units = n / pad;
+    for (int q = 0; q < W; ++q) {
+      const int64_t c = a.cum[e * W + q];
+      int64_t b = q == W - 1 || c < 0 ? n : pad * ((units * c + (1ll << (kShareBits - 1))) >> kShareBits);
+      bnd[e][q] = b < n ? b : n;
+    }
+  }
+  __syncthreads();
+  auto piece = [&](int s, int e, int q, int64_t& lo, int64_t& hi) {
+    const int64_t p0 = pre[s][e], p1 = p0 + padded(s, e);
+    lo = max(p0, q > 0 ? bnd[e][q - 1] : (int64_t)0);
+    hi = min(p1, bnd[e][q]);
+    if (hi < lo) hi = lo;
+  };
+  if (threadIdx.x < W * W) {
+    const int s = threadIdx.x / W, q = threadIdx.x % W;
+    int64_t t = 0;
+    for (int e = 0; e < E; ++e) {
+      int64_t lo, hi;
+      piece(s, e, q, lo, hi);
+      t += hi - lo;
+    }
+    tot[s][q] = t;
+    if (t > a.cap) overflow = 1;  // benign race: every writer stores 1
+  }
+  __syncthreads();
+  if (overflow) {
+    if (threadIdx.x == 0) atomicExch(a.status, 2);
+    for (int i = threadIdx.x; i < E * W; i += blockDim.x) {
+      a.piece_end[i] = a.seg_offsets[i / W];
+      a.piece_shift[i] = 0;
+    }
+    for (int i = threadIdx.x; i <= W * a.n_owned; i += blockDim.x) a.recv_segs[i] = 0;
+    if (threadIdx.x < kStats) a.stats[threadIdx.x] = 0;
+    return;
+  }
+  if (threadIdx.x < W) {  // send pieces into this rank's chunk for q
+    const int q = threadIdx.x;
+    int64_t off = 0;  // rows already placed in chunk q
+    for (int e = 0; e < E; ++e) {
+      int64_t lo, hi;
+      piece(rank, e, q, lo, hi);
+      const int64_t p0 = pre[rank][e], seg = a.seg_offsets[e];
+      const int64_t end_g = min(max(bnd[e][q], p0), p0 + padded(rank, e));
+      a.piece_end[e * W + q] = seg + (end_g - p0);
+      a.piece_shift[e * W + q] = (int64_t)q * a.cap + off - seg - (lo - p0);
+      off += hi - lo;
+    }
+  }
+  if (threadIdx.x == 32) {  // receive segments: (source, owned expert), compact, shifted into chunk s
+    int64_t off = 0;
+    int i = 0;
+    for (int s = 0; s < W; ++s) {
+      int64_t in_chunk = 0;
+      int j = 0;
+      for (int e = 0; e < E; ++e) {
+        int64_t lo, hi;
+        piece(s, e, rank, lo, hi);
+        if (j < a.n_owned && a.owned[j] == e) {
+          a.recv_segs[i] = off;
+          a.a_shift[i] = (int64_t)s * a.cap + in_chunk - off;
+          ++i;
+          ++j;
+          off += hi - lo;
+        }
+        in_chunk += hi - lo;  // a non-owned expert has no rows for this rank
+      }
+    }
+    a.recv_segs[i] = off;
+    a.stats[0] = off;
+  }
+}
+
 __global__ void ep_bar_kernel(PeerSym sym, int W, int rank, int phase, uint64_t epoch, uint64_t timeout_ns,
                               int* status) {
   barrier(sym, W, rank, phase, epoch, timeout_ns, status);
@@ -616,6 +731,171 @@ int emoe_ep_destroy(emoe_ep* ep) {
     if (!ep) return;
     ep->destroy();
     delete ep;
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// NCCL chunk transport: the device halves (the collectives are the caller's)
+// ---------------------------------------------------------------------------
+struct emoe_epx {
+  emoe_layer* layer = nullptr;
+  LayerView v{};
+  int W = 1, rank = 0;
+  int64_t cap = 0;
+  std::vector<int32_t> owned;
+  int64_t* cum_dev = nullptr;
+  int32_t* owned_dev = nullptr;
+  int64_t* piece_end = nullptr;
+  int64_t* piece_shift = nullptr;
+  int64_t* recv_segs = nullptr;
+  int64_t* a_shift = nullptr;
+  int32_t* seg_expert = nullptr;
+  int64_t* stats = nullptr;
+  int* status = nullptr;
+  void* h = nullptr;  // [W * cap][f] GEMM1 output, compact
+  void destroy() {
+    cudaDeviceSynchronize();
+    for (void* p : {(void*)cum_dev, (void*)owned_dev, (void*)piece_end, (void*)piece_shift, (void*)recv_segs,
+                    (void*)a_shift, (void*)seg_expert, (void*)stats, (void*)status, h})
+      if (p) cudaFree(p);
+  }
+};
+
+extern "C" {
+
+int emoe_epx_create(emoe_layer* layer, int world, int rank, const int64_t* cum_shares, int64_t cap_rows,
+                    emoe_epx** out) {
+  return guard([&] {
+    EMOE_REQUIRE(layer && cum_shares && out, "epx_create: null argument");
+    EMOE_REQUIRE(world >= 1 && world <= kMaxPeers && rank >= 0 && rank < world, "epx_create: bad world / rank");
+    const LayerView v = layer_view(layer);
+    EMOE_REQUIRE(v.dtype == DT_BF16 && v.E <= kMaxE, "epx_create: bf16, E <= 128");
+    const int E = v.E;
+    std::vector<int32_t> owned;
+    for (int e = 0; e < E; ++e) {
+      const int64_t* c = cum_shares + (size_t)e * world;
+      if (c[0] >= 0 && c[rank] > (rank > 0 ? c[rank - 1] : 0)) owned.push_back(e);
+    }
+    EMOE_REQUIRE((int64_t)world * (int64_t)owned.size() <= 256, "epx_create: more than 256 receive segments");
+    auto* x = new emoe_epx();
+    try {
+      x->layer = layer;
+      x->v = v;
+      x->W = world;
+      x->rank = rank;
+      x->owned = owned;
+      x->cap = ceil_div(cap_rows > 0 ? cap_rows : v.rows_cap, v.seg_pad) * v.seg_pad;
+      const size_t ew = (size_t)E * world, ns = (size_t)world * owned.size();
+      x->cum_dev = dmalloc<int64_t>(ew);
+      EMOE_CUDA(cudaMemcpy(x->cum_dev, cum_shares, ew * 8, cudaMemcpyHostToDevice));
+      x->owned_dev = dmalloc<int32_t>(std::max<size_t>(1, owned.size()));
+      if (!owned.empty())
+        EMOE_CUDA(cudaMemcpy(x->owned_dev, owned.data(), owned.size() * 4, cudaMemcpyHostToDevice));
+      x->piece_end = dmalloc<int64_t>(ew);
+      x->piece_shift = dmalloc<int64_t>(ew);
+      x->recv_segs = dmalloc<int64_t>(ns + 1);
+      x->a_shift = dmalloc<int64_t>(std::max<size_t>(1, ns));
+      x->seg_expert = dmalloc<int32_t>(std::max<size_t>(1, ns));
+      std::vector<int32_t> se;
+      for (int s = 0; s < world; ++s) se.insert(se.end(), owned.begin(), owned.end());
+      if (ns) EMOE_CUDA(cudaMemcpy(x->seg_expert, se.data(), ns * 4, cudaMemcpyHostToDevice));
+      x->stats = dmalloc<int64_t>(kStats);
+      EMOE_CUDA(cudaMemset(x->stats, 0, sizeof(int64_t) * kStats));
+      x->status = dmalloc<int>(1);
+      EMOE_CUDA(cudaMemset(x->status, 0, sizeof(int)));
+      x->h = dmalloc<uint8_t>((size_t)world * x->cap * v.f * v.elem);
+      EMOE_CUDA(cudaDeviceSynchronize());
+    } catch (...) {
+      x->destroy();
+      delete x;
+      throw;
+    }
+    *out = x;
+  });
+}
+
+int emoe_epx_cap_rows(const emoe_epx* x, int64_t* cap) {
+  return guard([&] {
+    EMOE_REQUIRE(x && cap, "epx_cap_rows: null argument");
+    *cap = x->cap;
+  });
+}
+
+int emoe_epx_route(emoe_epx* x, const void* xin, const float* logits_in, int64_t T, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(x && xin, "epx_route: null argument");
+    EMOE_REQUIRE(T >= 0 && T <= x->v.max_tokens, "epx_route: T exceeds the layer's max_tokens");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    layer_route_scan(x->layer, xin, logits_in, T, s);
+    if (T == 0) EMOE_CUDA(cudaMemsetAsync(const_cast<int32_t*>(x->v.counts), 0, sizeof(int32_t) * x->v.E, s));
+  });
+}
+
+int emoe_epx_dispatch(emoe_epx* x, const int32_t* table_dev, const void* xin, int64_t T, void* send_chunks,
+                      void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(x && table_dev && send_chunks, "epx_dispatch: null argument");
+    EMOE_REQUIRE(T == 0 || xin, "epx_dispatch: null x");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ChunkArgs a{table_dev,   x->v.seg_offsets, x->cum_dev,   x->owned_dev, (int)x->owned.size(), x->v.seg_pad,
+                x->cap,      x->piece_end,     x->piece_shift, x->recv_segs, x->a_shift,           x->stats,
+                x->status};
+    epx_layout_kernel<<<1, 256, 0, s>>>(x->W, x->rank, x->v.E, a);
+    EMOE_CUDA(cudaGetLastError());
+    count_launch();
+    if (T == 0) return;
+    PeerRows pr{};
+    for (int q = 0; q < x->W; ++q) pr.base[q] = static_cast<uint8_t*>(send_chunks);
+    pr.piece_end = x->piece_end;
+    pr.piece_shift = x->piece_shift;
+    pr.W = x->W;
+    pr.cap = (int64_t)x->W * x->cap;
+    pr.pos_remote = 1;
+    launch_permute_remote(xin, x->v.elem, T, x->v.d, x->v.E, x->v.k, x->v.served_idx, x->v.seg_offsets,
+                          x->v.block_base, pr, x->v.pos, s);
+  });
+}
+
+int emoe_epx_ffn(emoe_epx* x, const void* recv_chunks, void* return_chunks, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(x && recv_chunks && return_chunks, "epx_ffn: null argument");
+    const int n_seg = x->W * (int)x->owned.size();
+    if (n_seg == 0) return;
+    const int64_t rows = (int64_t)x->W * x->cap;
+    layer_ffn_chunks(x->layer, recv_chunks, rows, x->recv_segs, x->seg_expert, n_seg, x->a_shift, x->h, rows,
+                     return_chunks, rows, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int emoe_epx_combine(emoe_epx* x, const void* returned_chunks, void* y, int64_t T, void* stream) {
+  return guard([&] {
+    EMOE_REQUIRE(x && returned_chunks && y, "epx_combine: null argument");
+    launch_combine(returned_chunks, DT_BF16, T, x->v.d, x->v.k, x->v.pos, x->v.served_w, y,
+                   static_cast<cudaStream_t>(stream));
+  });
+}
+
+int emoe_epx_status(emoe_epx* x, void* stream, int* status, int64_t* rows) {
+  return guard([&] {
+    EMOE_REQUIRE(x, "epx_status: null handle");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int st = 0;
+    int64_t rr = 0;
+    EMOE_CUDA(cudaMemcpyAsync(&st, x->status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    EMOE_CUDA(cudaMemcpyAsync(&rr, x->stats, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    EMOE_CUDA(cudaStreamSynchronize(s));
+    if (status) *status = st;
+    if (rows) *rows = rr;
+  });
+}
+
+int emoe_epx_destroy(emoe_epx* x) {
+  return guard([&] {
+    if (!x) return;
+    x->destroy();
+    delete x;
   });
 }
 

@@ -50,7 +50,9 @@ constexpr int TMEM_COLS = 512;
 // (128-B swizzled rows) per epilogue warp
 constexpr int OUT_BOX_COLS = 64;
 constexpr int OUT_BOX_BYTES = 32 * OUT_BOX_COLS * 2;
-constexpr int BAR_AREA_BYTES = 2048;  // mbarriers, TMEM slot, segment offsets (int32) and slots (int16)
+// mbarriers, TMEM slot, segment offsets (int32), weight slots (int16) and
+// the segments' A / output row shifts (int32)
+constexpr int BAR_AREA_BYTES = 4096;
 
 // CG = CTAs per MMA (1 or 2), EW = epilogue warps (4: one per TMEM lane
 // quarter; 8: two per quarter, each draining half of the accumulator columns,
@@ -73,7 +75,8 @@ struct Cfg {
   static constexpr int NUM_THREADS = 64 + 32 * EW;
   static constexpr int SMEM_BYTES = 1024 /*align*/ + STAGES * STAGE_BYTES + OUT_STAGE_BYTES + BAR_AREA_BYTES;
   static_assert(SMEM_BYTES <= 232448, "shared memory over the sm_100 per-block limit");
-  static_assert(2 * STAGES * 8 + 4 * 8 + 16 + 4 * (MAX_EXPERTS + 1) + 2 * MAX_EXPERTS <= BAR_AREA_BYTES,
+  static_assert(2 * STAGES * 8 + 4 * 8 + 16 + 4 * (MAX_EXPERTS + 1) + 2 * MAX_EXPERTS + 8 * MAX_EXPERTS <=
+                    BAR_AREA_BYTES,
                 "barrier area");
 };
 
@@ -116,6 +119,13 @@ struct Params {
   uint64_t hint_a, hint_b;
   int group_n;  // column panel width in n-blocks (>= n_blocks: whole width)
   uint64_t hint_out;  // L2 policy of the TMA output stores (0: none)
+  // per-segment row shifts (null = none): segment i's A rows are read from
+  // row r + seg_a_shift[i] and its outputs stored to row r + seg_o_shift[i]
+  // (r = the compact padded row); the NCCL expert-parallel transport reads
+  // the received rows straight out of its all-to-all chunks and writes Y
+  // back into the return chunks (ep.py NcclExpertParallelMoE)
+  const int64_t* seg_a_shift;
+  const int64_t* seg_o_shift;
 };
 
 struct TileCoord {
@@ -227,6 +237,8 @@ __global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
   int32_t* s_offs = reinterpret_cast<int32_t*>(tmem_slot + 4);
   int16_t* s_slot = reinterpret_cast<int16_t*>(s_offs + MAX_EXPERTS + 1);  // weight slot of each segment
                                                                             // (the producer's per-tile lookup)
+  int32_t* s_ashift = reinterpret_cast<int32_t*>(s_slot + MAX_EXPERTS);     // [MAX_EXPERTS]
+  int32_t* s_oshift = s_ashift + MAX_EXPERTS;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -241,6 +253,10 @@ __global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
     s_offs[i] = (int32_t)(p.single_rows > 0 ? (i == 0 ? 0 : p.single_rows) : p.seg_offsets[i]);
   for (int i = threadIdx.x; i < E; i += C::NUM_THREADS)
     s_slot[i] = (int16_t)p.slot_of_expert[p.seg_expert ? p.seg_expert[i] : i];
+  for (int i = threadIdx.x; i < E; i += C::NUM_THREADS) {
+    s_ashift[i] = p.seg_a_shift ? (int32_t)p.seg_a_shift[i] : 0;
+    s_oshift[i] = p.seg_o_shift ? (int32_t)p.seg_o_shift[i] : 0;
+  }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
@@ -286,7 +302,7 @@ __global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
         const TileCoord c = decode_tile(t, total_mb, p.n_blocks, p.group_m, C::TILE_M, s_offs, E, p.group_n);
         const int slot = s_slot[c.expert];
-        const int a_row = c.mb * C::TILE_M + (int)rank * 128;
+        const int a_row = c.mb * C::TILE_M + (int)rank * 128 + s_ashift[c.expert];
         int b_row;
         const CUtensorMap* tb = &tmap_b;
         if (EPI == EPI_SWIGLU) {
@@ -403,9 +419,10 @@ __global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
       tc_fence_after();
       const int64_t row0 = (int64_t)c.mb * C::TILE_M + rank * 128 + quarter * 32;
       const int64_t row = row0 + lane;
+      const int64_t orow0 = row0 + s_oshift[c.expert];  // output row of this warp's first row
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + buf * BN;
       const int col0 = c.nb * p.out_block_cols;
-      __nv_bfloat16* orow = p.out + row * p.ldo + col0;
+      __nv_bfloat16* orow = p.out + (orow0 + lane) * p.ldo + col0;
       int combine_partner = -1, combine_slot = 0, combine_tok = -1;  // fused top-2 combine, after the TMEM release
       float combine_w0 = 0.0f, combine_w1 = 0.0f;
       if (EPI == EPI_SWIGLU) {
@@ -428,7 +445,7 @@ __global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
             const float h1 = gb / (1.0f + __expf(-gb)) * ub;
             packed[j] = pack_bf16x2(h0, h1);
           }
-          store_box(p, &tmap_out, my_stage, orow + cc, packed, lane, col0 + cc, row0);
+          store_box(p, &tmap_out, my_stage, orow + cc, packed, lane, col0 + cc, orow0);
         }
       } else if (EPI == EPI_F32) {
         // fp32 accumulators straight out (dense gate GEMM): rows >= row_limit
@@ -575,7 +592,7 @@ __global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
             }
             packed[j] = pack_bf16x2(v0, v1);
           }
-          store_box(p, &tmap_out, my_stage, orow + cc, packed, lane, col0 + cc, row0);
+          store_box(p, &tmap_out, my_stage, orow + cc, packed, lane, col0 + cc, orow0);
         }
       }
       tc_fence_before();
@@ -755,7 +772,8 @@ void launch_grouped_gemm(int epi, int cta_group, int mc, const CUtensorMap& ta, 
                          const CUtensorMap& tb2, const int64_t* seg_offsets, const int32_t* slot_of_expert,
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
                          int num_sms, cudaStream_t stream, const int32_t* seg_expert, const CUtensorMap* tmap_out,
-                         const ScatterCombine* scatter, const PeerOut* peer_out) {
+                         const ScatterCombine* scatter, const PeerOut* peer_out, const int64_t* seg_a_shift,
+                         const int64_t* seg_o_shift) {
   EMOE_REQUIRE(num_experts <= gemm::MAX_EXPERTS, "grouped_gemm: too many segments");
   EMOE_REQUIRE(!scatter || epi == EPI_STORE, "grouped_gemm: the fused combine needs the GEMM2 epilogue");
   EMOE_REQUIRE(K % gemm::BK == 0, "grouped_gemm: K must be a multiple of 64");
@@ -802,6 +820,8 @@ void launch_grouped_gemm(int epi, int cta_group, int mc, const CUtensorMap& ta, 
   p.tma_store = tmap_out != nullptr && tma_store_enabled() && !scatter && !peer_out;
   p.seg_out_rank = peer_out ? peer_out->seg_rank : nullptr;
   p.seg_out_shift = peer_out ? peer_out->seg_shift : nullptr;
+  p.seg_a_shift = seg_a_shift;
+  p.seg_o_shift = seg_o_shift;
   for (int q = 0; q < kMaxPeers; ++q) p.out_peer[q] = peer_out ? peer_out->base[q] : nullptr;
   p.scatter_tok = scatter ? scatter->row_token : nullptr;
   p.scatter_w = scatter ? scatter->weight : nullptr;
@@ -851,19 +871,9 @@ void launch_dense_gemm_f32(const CUtensorMap& ta, const CUtensorMap& tb, int64_t
   p.scatter_arrive = nullptr;
   p.seg_out_rank = nullptr;
   p.seg_out_shift = nullptr;
+  p.seg_a_shift = nullptr;
+  p.seg_o_shift = nullptr;
   launch_params(EPI_F32, cta_group, 1, ta, tb, tb, ta, p, num_sms, stream);
-}
-
-// epilogue warps per CTA: 4 (one per TMEM lane quarter).  8 (two per quarter)
-// was measured for the short-K Switch GEMM1 and is 1-2 % slower
-// (profiles/r01_epilogue_warps_ab.jsonl): its tiles are not epilogue-bound.
-// EMOE_GEMM_EPI_WARPS = 8 selects it for A/B runs.
-static int epilogue_warps(int /*K*/) {
-  static const int forced = [] {
-    const char* v = getenv("EMOE_GEMM_EPI_WARPS");
-    return v ? atoi(v) : 0;
-  }();
-  return forced == 8 ? 8 : 4;
 }
 
 template <int EPI, int CG, int EW, int MC>
@@ -898,10 +908,10 @@ static void launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
 template <int EPI, int CG>
 static void launch_ew(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const CUtensorMap& to,
                       const gemm::Params& p, int num_sms, cudaStream_t stream) {
-  if (epilogue_warps(p.K) == 8)
-    launch_one<EPI, CG, 8, 1>(ta, tb, tb2, to, p, num_sms, stream);
-  else
-    launch_one<EPI, CG, 4, 1>(ta, tb, tb2, to, p, num_sms, stream);
+  // 4 epilogue warps (one per TMEM lane quarter); 8 (two per quarter, each
+  // draining half the columns) measured 1-2 % slower for the short-K Switch
+  // GEMM1 and was dropped (profiles/r01_epilogue_warps_ab.jsonl)
+  launch_one<EPI, CG, 4, 1>(ta, tb, tb2, to, p, num_sms, stream);
 }
 
 static void launch_params(int epi, int cta_group, int mc, const CUtensorMap& ta, const CUtensorMap& tb,

@@ -73,6 +73,7 @@ struct PeerRows {
   const int64_t* piece_shift;
   int W;
   int64_t cap;  // rows per buffer: a row outside [0, cap) is not written (pos = -1)
+  int pos_remote = 0;  // pos[t][j] = the destination row (1) or the local row (0)
 };
 // GEMM2 return form: segment i's output rows go to rank seg_rank[i]'s buffer
 // base[seg_rank[i]] at row (r + seg_shift[i]) -- the source's own permuted
@@ -114,7 +115,9 @@ void launch_grouped_gemm(int epi, int cta_group, int mc, const CUtensorMap& ta, 
                          int num_experts, int K, int N_out, int b_rows_per_slot, __nv_bfloat16* out, int64_t ldo,
                          int num_sms, cudaStream_t stream, const int32_t* seg_expert = nullptr,
                          const CUtensorMap* tmap_out = nullptr,  // null: direct st.global epilogue
-                         const ScatterCombine* scatter = nullptr, const PeerOut* peer_out = nullptr);
+                         const ScatterCombine* scatter = nullptr, const PeerOut* peer_out = nullptr,
+                         const int64_t* seg_a_shift = nullptr,   // [n_seg] A row shift per segment
+                         const int64_t* seg_o_shift = nullptr);  // [n_seg] output row shift per segment
 
 // K1 for many experts (E in {32, 64, 96, 128}, bf16): gate GEMM on tcgen05
 // with the routing fused into its epilogue (gate_tc.cu).  tmap_gate: W_g [E][d]
@@ -185,5 +188,11 @@ void layer_route_scan(emoe_layer* L, const void* x, const float* logits_in, int6
 void layer_ffn_rows(emoe_layer* L, const void* xr, int64_t R, const int64_t* segs, const int32_t* seg_expert,
                     int n_seg, void* hr, void* yr, cudaStream_t s, const PeerOut* peer_out = nullptr,
                     cudaEvent_t after_gemm1 = nullptr);
+// K4 over received all-to-all chunks (NCCL EP transport): segment i's A rows
+// at r + a_shift[i] of x_chunks, H compact [h_rows][f], Y rows stored at
+// r + a_shift[i] of y_chunks (the return chunks mirror the receive chunks)
+void layer_ffn_chunks(emoe_layer* L, const void* x_chunks, int64_t x_rows, const int64_t* segs,
+                      const int32_t* seg_expert, int n_seg, const int64_t* a_shift, void* h, int64_t h_rows,
+                      void* y_chunks, int64_t y_rows, cudaStream_t s, cudaEvent_t after_gemm1 = nullptr);
 
 }  // namespace emoe

@@ -1252,6 +1252,25 @@ void layer_route_scan(emoe_layer* L, const void* x, const float* logits_in, int6
                 L->seg_offsets, L->block_base, s);
 }
 
+void layer_ffn_chunks(emoe_layer* L, const void* x_chunks, int64_t x_rows, const int64_t* segs,
+                      const int32_t* seg_expert, int n_seg, const int64_t* a_shift, void* h, int64_t h_rows,
+                      void* y_chunks, int64_t y_rows, cudaStream_t s, cudaEvent_t after_gemm1) {
+  EMOE_REQUIRE(L->cfg.dtype == EMOE_DTYPE_BF16, "ffn_chunks: the NCCL EP transport runs the bf16 path");
+  const int d = L->cfg.d_model, f = L->cfg.d_ff;
+  const CUtensorMap a1 = make_tmap_bf16_2d(x_chunks, (uint64_t)x_rows, d, 128);
+  const CUtensorMap o1 = make_tmap_bf16_store(h, (uint64_t)h_rows, f);
+  const CUtensorMap a2 = make_tmap_bf16_2d(h, (uint64_t)h_rows, f, 128);
+  const CUtensorMap o2 = make_tmap_bf16_store(y_chunks, (uint64_t)y_rows, d);
+  // GEMM1: A rows from the receive chunks, H compact; GEMM2: H compact, Y into the return chunks
+  launch_grouped_gemm(L->swiglu() ? EPI_SWIGLU : EPI_RELU, L->cta_group, L->gemm_mc, a1, L->tb1, L->tb3, segs,
+                      L->slot_dev, n_seg, d, f, f, static_cast<__nv_bfloat16*>(h), f, L->num_sms, s, seg_expert, &o1,
+                      nullptr, nullptr, a_shift, nullptr);
+  if (after_gemm1) EMOE_CUDA(cudaEventRecord(after_gemm1, s));
+  launch_grouped_gemm(EPI_STORE, L->cta_group, L->gemm_mc, a2, L->tb2, L->tb2, segs, L->slot_dev, n_seg, f, d, d,
+                      static_cast<__nv_bfloat16*>(y_chunks), d, L->num_sms, s, seg_expert, &o2, nullptr, nullptr,
+                      nullptr, a_shift);
+}
+
 void layer_ffn_rows(emoe_layer* L, const void* xr, int64_t R, const int64_t* segs, const int32_t* seg_expert,
                     int n_seg, void* hr, void* yr, cudaStream_t s, const PeerOut* peer_out, cudaEvent_t after_gemm1) {
   const bool was = L->profiling;

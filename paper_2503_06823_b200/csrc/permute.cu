@@ -144,16 +144,22 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
       if (blockIdx.y != 0) continue;  // column-split blocks: block row 0 writes the positions
       if (REMOTE) {
         uint8_t* ptr = nullptr;
+        int64_t dst_row = -1;
         if (e >= 0) {
           for (int q = 0; q < peers.W; ++q)  // the piece of segment e holding local row d
             if (d < peers.piece_end[e * peers.W + q]) {
               const int64_t r = d + peers.piece_shift[e * peers.W + q];
-              if (r >= 0 && r < peers.cap) ptr = peers.base[q] + r * row_bytes;
+              if (r >= 0 && r < peers.cap) {
+                ptr = peers.base[q] + r * row_bytes;
+                dst_row = r;
+              }
               break;
             }  // no piece: the receivers overflowed (status 2), the row is dropped
         }
         dptr_s[threadIdx.x * k + j] = ptr;
-        if (t < T) pos[t * k + j] = ptr ? d : -1;  // outputs return to this local row
+        // outputs return to this local row (peer memory), or to the same row
+        // of the return chunks (NCCL chunk transport)
+        if (t < T) pos[t * k + j] = ptr ? (peers.pos_remote ? (int32_t)dst_row : d) : -1;
       } else if (t < T) {
         if (pos) pos[t * k + j] = d;
         if (row_token && d >= 0) row_token[d] = (int32_t)t;

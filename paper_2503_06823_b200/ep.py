@@ -286,6 +286,127 @@ class ExpertParallelMoE:
     __call__ = forward
 
 
+class NcclExpertParallelMoE:
+    """Expert parallelism over NCCL all-to-all with no host synchronisation
+    (the capacity-padded form of SURVEY.md §8e) through emoe_epx_*: the count
+    exchange is one all_gather_into_tensor of [E] int32 on the device, the
+    split layout is computed on the device from it (the same split as the
+    peer-memory path), and every (source, destination) pair owns a fixed chunk
+    of `cap` rows, so both all_to_all_single calls take equal splits.  The
+    price is wire bytes: every chunk travels whole (cap rows), so cap should
+    be a bound on the rows one source sends one destination
+    (plan_pair_rows); a pair over cap drops the forward's rows on every rank
+    and status() reports 2.  Bit-identical to the peer-memory path and EP=1."""
+
+    def __init__(self, layer, global_resident: Sequence[int], group=None, loads=None, cap_rows: int = 0,
+                 min_share: float = 0.05):
+        import ctypes as C
+
+        from ._lib import lib
+        from .moesim import check
+
+        self._lib, self._check, self._C = lib, check, C
+        self.layer = layer
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.E = layer.E
+        self.cum = plan_shares(global_resident, layer.E, self.world, loads, min_share)
+        res = np.zeros(layer.E, np.uint8)
+        res[list(global_resident)] = 1
+        layer.set_route_residency(res)
+        cum = np.ascontiguousarray(self.cum, np.int64)
+        h = C.c_void_p()
+        check(lib.emoe_epx_create(layer.h, self.world, self.rank, cum.ctypes.data_as(C.c_void_p), int(cap_rows),
+                                  C.byref(h)))
+        self.h = h
+        cap = C.c_int64()
+        check(lib.emoe_epx_cap_rows(h, C.byref(cap)))
+        self.cap = int(cap.value)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        rows = self.world * self.cap
+        self.send = torch.empty(rows, layer.d, dtype=torch.bfloat16, device=dev)
+        self.recv = torch.empty_like(self.send)
+        self.ret = torch.empty_like(self.send)
+        self.back = torch.empty_like(self.send)
+        self.table = torch.empty(self.world * layer.E, dtype=torch.int32, device=dev)
+        self.stage_on_host = dist.get_backend(group) != "nccl"
+
+    def owned(self) -> list:
+        return owned_experts(self.cum, self.rank)
+
+    def _a2a(self, out, inp):
+        if self.stage_on_host:  # gloo (tests, ranks sharing one GPU): staged through the host
+            o = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_to_all_single(o, inp.cpu(), group=self.group)
+            out.copy_(o)
+        else:
+            dist.all_to_all_single(out, inp, group=self.group)
+
+    def forward(self, x: torch.Tensor, logits: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                stream=None) -> torch.Tensor:
+        C = self._C
+        assert x.is_cuda and x.dtype == torch.bfloat16 and x.shape[1] == self.layer.d and x.is_contiguous()
+        y = torch.empty_like(x) if out is None else out
+        s = stream if stream is not None else torch.cuda.current_stream()
+        sp = C.c_void_p(s.cuda_stream)
+        lp = None if logits is None else C.c_void_p(logits.contiguous().data_ptr())
+        T = x.shape[0]
+        self._check(self._lib.emoe_epx_route(self.h, C.c_void_p(x.data_ptr()), lp, T, sp))
+        counts = self.layer.workspace()["counts"]
+        if self.stage_on_host:
+            parts = [torch.empty(self.E, dtype=torch.int32) for _ in range(self.world)]
+            dist.all_gather(parts, counts.cpu(), group=self.group)
+            self.table.copy_(torch.cat(parts))
+        else:
+            dist.all_gather_into_tensor(self.table, counts, group=self.group)
+        self._check(self._lib.emoe_epx_dispatch(self.h, C.c_void_p(self.table.data_ptr()), C.c_void_p(x.data_ptr()),
+                                                T, C.c_void_p(self.send.data_ptr()), sp))
+        self._a2a(self.recv, self.send)
+        self._check(self._lib.emoe_epx_ffn(self.h, C.c_void_p(self.recv.data_ptr()), C.c_void_p(self.ret.data_ptr()),
+                                           sp))
+        self._a2a(self.back, self.ret)
+        self._check(self._lib.emoe_epx_combine(self.h, C.c_void_p(self.back.data_ptr()), C.c_void_p(y.data_ptr()), T,
+                                               sp))
+        return y
+
+    __call__ = forward
+
+    def status(self, stream=None):
+        """(status, rows computed last forward); synchronises the stream.
+        status 2 = a (source, destination) pair exceeded cap rows."""
+        C = self._C
+        s = stream if stream is not None else torch.cuda.current_stream()
+        st, rr = C.c_int(), C.c_int64()
+        self._check(self._lib.emoe_epx_status(self.h, C.c_void_p(s.cuda_stream), C.byref(st), C.byref(rr)))
+        return st.value, rr.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.emoe_epx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+def plan_pair_rows(cum: np.ndarray, loads, tokens: int, top_k: int, pad: int, slack: float = 1.25) -> int:
+    """A capacity for NcclExpertParallelMoE: the rows the busiest (source,
+    destination) pair is expected to carry when every source routes `tokens`
+    tokens (<= top_k rows each) with the experts' load shares `loads`
+    (e.g. the Eq. 2 aggregate), times `slack`, plus one pad per expert."""
+    W = cum.shape[1]
+    res = [e for e in range(cum.shape[0]) if cum[e, 0] >= 0]
+    w = np.array([max(float(loads[e]), 0.0) for e in res]) if loads is not None else np.ones(len(res))
+    w = w / w.sum() if w.sum() > 0 else np.ones(len(res)) / len(res)
+    rows = tokens * top_k
+    per_q = np.zeros(W)
+    for i, e in enumerate(res):
+        frac = np.diff(np.concatenate([[0], cum[e]])) / SHARE_ONE
+        per_q += frac * w[i] * rows
+    return int(np.ceil(per_q.max() * slack)) + len(res) * pad
+
+
 STAGES = ["route", "count_exchange", "dispatch", "dispatch_wait", "gemm1", "gemm2_return", "return_wait", "combine"]
 
 

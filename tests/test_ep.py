@@ -534,3 +534,94 @@ def test_ep_stack_two_ranks_one_gpu_bit_identical(tmp_path):
         for i, d in enumerate(torch.load(tmp_path / f"st{r}.pt", weights_only=False)):
             assert d["status"] == 0, f"rank {r} forward {i}: status {d['status']}"
             assert all(d["same"]), f"rank {r} forward {i}: per-layer EP == EP=1: {d['same']}"
+
+
+# ---------------------------------------------------------------------------
+# NCCL transport without host synchronisation (emoe_epx_*, capacity chunks)
+# ---------------------------------------------------------------------------
+def _gpu_epx_worker(rank, world, port_no, resident, out_dir, loads, cap):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from helpers import build_layer
+    from paper_2503_06823_b200.ep import NcclExpertParallelMoE
+
+    cum = plan_shares(resident, 8, world, loads)
+    mine = owned_experts(cum, rank)
+    layer, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", len(mine), mine, max_tokens=2048)
+    ep = NcclExpertParallelMoE(layer, resident, loads=loads, cap_rows=cap)
+    full, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", len(resident), resident,
+                             max_tokens=2048)
+    res = []
+    for it, T in enumerate([1500 + 100 * rank, 700 - 50 * rank, 2048]):
+        x = torch.randn(T, 256, generator=torch.Generator().manual_seed(10 * it + rank)).to(torch.bfloat16).cuda()
+        y_ep = ep(x)
+        st, rows = ep.status()
+        y_1 = full.forward(x)
+        torch.cuda.synchronize()
+        res.append(dict(same=bool(torch.equal(y_ep, y_1)), status=st, rows=rows))
+    torch.save(res, Path(out_dir) / f"x{rank}.pt")
+    dist.barrier()
+    ep.close()
+    layer.close()
+    full.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("resident,loads,cap", [([0, 2, 5, 7], None, 0), ([0, 2, 5, 7], SKEW, 0), ([3], None, 0),
+                                               ([1, 6], [0, 1, 0, 0, 0, 0, 3, 0], 2048), ([0, 2, 5, 7], None, 128)])
+def test_epx_two_ranks_one_gpu(resident, loads, cap, tmp_path):
+    """The NCCL chunk transport (here over gloo, 2 ranks sharing one B200):
+    bit-identical to the single-GPU forward over three forwards; a capacity
+    too small for a pair (cap = 128 rows) drops the forward on both ranks with
+    status 2 instead of returning a wrong output silently."""
+    mp.spawn(_gpu_epx_worker, args=(2, free_port(), resident, str(tmp_path), loads, cap), nprocs=2, join=True)
+    for r in range(2):
+        for i, d in enumerate(torch.load(tmp_path / f"x{r}.pt", weights_only=False)):
+            if cap == 128:
+                assert d["status"] == 2, f"rank {r} forward {i}: overflow not reported"
+            else:
+                assert d["status"] == 0 and d["rows"] > 0, f"rank {r} forward {i}: status {d['status']}"
+                assert d["same"], f"rank {r} forward {i}: NCCL chunk EP output differs from 1 GPU"
+
+
+def _nccl_graph_worker(rank, world, port_no, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    from helpers import build_layer
+    from paper_2503_06823_b200.ep import NcclExpertParallelMoE
+
+    resident = [0, 2, 5, 7]
+    layer, _, _ = build_layer(8, 256, 512, 2, "bf16", "swiglu", "topk_softmax", 4, resident, max_tokens=2048)
+    ep = NcclExpertParallelMoE(layer, resident)
+    x = torch.randn(1800, 256, generator=torch.Generator().manual_seed(4)).to(torch.bfloat16).cuda()
+    y = torch.empty_like(x)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ep(x, out=y)  # warm-up (lazy NCCL communicator setup happens outside the capture)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):  # any host synchronisation inside would abort the capture
+        ep(x, out=y)
+    y.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    ref = layer.forward(x)
+    torch.cuda.synchronize()
+    torch.save(dict(same=bool(torch.equal(y, ref))), Path(out_dir) / "g.pt")
+    ep.close()
+    layer.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_epx_nccl_forward_has_no_host_sync(tmp_path):
+    """The whole NCCL-transport forward -- route, device count all-gather,
+    device layout + dispatch permute, equal-split all_to_all, FFN, return
+    all_to_all, combine -- is captured into one CUDA graph on an NCCL group
+    (world 1 on this single-GPU box): a host synchronisation anywhere would
+    abort the capture.  The replay equals the plain forward."""
+    mp.spawn(_nccl_graph_worker, args=(1, free_port(), str(tmp_path)), nprocs=1, join=True)
+    assert torch.load(tmp_path / "g.pt", weights_only=False)["same"]
