@@ -570,7 +570,7 @@ def _gpu_epx_worker(rank, world, port_no, resident, out_dir, loads, cap):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("resident,loads,cap", [([0, 2, 5, 7], None, 0), ([0, 2, 5, 7], SKEW, 0), ([3], None, 0),
-                                               ([1, 6], [0, 1, 0, 0, 0, 0, 3, 0], 2048), ([0, 2, 5, 7], None, 128)])
+                                               ([1, 6], [0, 1, 0, 0, 0, 0, 3, 0], 4352), ([0, 2, 5, 7], None, 128)])
 def test_epx_two_ranks_one_gpu(resident, loads, cap, tmp_path):
     """The NCCL chunk transport (here over gloo, 2 ranks sharing one B200):
     bit-identical to the single-GPU forward over three forwards; a capacity
