@@ -46,6 +46,11 @@ CONFIGS = {
                                "(predicted), d_model=1024, d_ff=3584, 512 tokens",
                       E=8, k=2, L=4, d=1024, f=3584, act="swiglu", wm="topk_softmax", prompts=1, tokens=512,
                       train=200, layer_lambda=0.6, prompt_lambda=0.8, seed=17, dtype="fp32"),
+    # a small bf16 layer for the bench-path tests (not a BASELINE config)
+    "tiny": dict(workload="test layer: bf16, 8 experts top-2, 4 resident (predicted), d_model=512, d_ff=1024, "
+                          "4 x 512 tokens",
+                 E=8, k=2, L=4, d=512, f=1024, act="swiglu", wm="topk_softmax", prompts=4, tokens=512,
+                 train=40, layer_lambda=0.6, prompt_lambda=0.8, seed=17),
     "switch": dict(workload="BASELINE config 3: Switch-base-128-shaped layer bf16, 128 experts top-1, 20% resident "
                             "(L=26, predicted), 32 x 2048 tokens",
                    E=128, k=1, L=26, d=768, f=3072, act="relu", wm="full_softmax", prompts=32, tokens=2048,
@@ -387,11 +392,15 @@ def build_parser():
                     help="N>1: expert parallelism (default; the north star's split: each GPU computes its share "
                          "of the resident experts' rows, tokens exchanged over NVLink) or replicas of the "
                          "predicted resident set (no exchange)")
+    ap.add_argument("--ep-at-1", action="store_true",
+                    help="run the expert-parallel code path even with one process (a world-1 group; tests)")
     ap.add_argument("--ep-recv-cap", type=int, default=0,
-                    help="--parallel ep: receive-buffer rows per GPU (0 = the worst case, world x rows_cap)")
+                    help="--parallel ep: p2p receive-buffer rows per GPU (0 = the worst case, world x rows_cap); "
+                         "nccl: rows per (source, destination) chunk (0 = the plan's bound, ep.plan_pair_rows)")
     ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"],
                     help="--parallel ep: dispatch/combine fused into the permute/combine kernels over "
-                         "IPC-mapped peer memory (p2p), or NCCL all-to-all between the stage kernels")
+                         "IPC-mapped peer memory (p2p), or NCCL all-to-alls over fixed capacity chunks between "
+                         "the stage kernels (no host synchronisation)")
     return ap
 
 
@@ -421,7 +430,8 @@ def main():
     import paper_2503_06823_b200 as emoe
     from paper_2503_06823_b200 import _lib
 
-    use_ep = args.parallel == "ep" and world > 1
+    use_ep = args.parallel == "ep" and (world > 1 or args.ep_at_1)
+    ensure_group_for_ep_at_1(args, world)
     strong = args.scaling == "strong" and world > 1
     if strong and cfg["prompts"] % world:
         raise SystemExit(f"--scaling strong: {world} GPUs do not divide the {cfg['prompts']} prompts")
@@ -441,15 +451,16 @@ def main():
 
         ep_model = PeerExpertParallelMoE(layer, info["global_resident"], loads=info["aggregate"],
                                          recv_rows_cap=args.ep_recv_cap)
-    elif use_ep:
-        from paper_2503_06823_b200.ep import ExpertParallelMoE, LayerBackend
+    elif use_ep:  # NCCL all-to-alls over capacity chunks, no host synchronisation
+        from paper_2503_06823_b200.ep import NcclExpertParallelMoE, plan_pair_rows, plan_shares
 
-        ep_model = ExpertParallelMoE(LayerBackend(layer, info["global_resident"]), info["global_resident"],
-                                    loads=info["aggregate"])
+        cum = plan_shares(info["global_resident"], cfg["E"], world, info["aggregate"])
+        cap = args.ep_recv_cap or plan_pair_rows(cum, info["aggregate"], T, cfg["k"], layer.seg_pad)
+        ep_model = NcclExpertParallelMoE(layer, info["global_resident"], loads=info["aggregate"], cap_rows=cap)
 
     def eager_step():
         if ep_model is not None:
-            ep_model(x, out=y) if args.ep_transport == "p2p" else ep_model(x)
+            ep_model(x, out=y)
         else:
             layer.forward(x, out=y)
         ws_topk = layer_ws_topk(layer)
@@ -528,8 +539,12 @@ def main():
         ep_stats = ep_model.stats()
         stages = dict(route=ep_stages["route"], permute=ep_stages["dispatch"], gemm1=ep_stages["gemm1"],
                       gemm2=ep_stages["gemm2_return"], combine=ep_stages["combine"])
-    else:  # NCCL transport: stage boundaries are host-synchronous collectives; the whole step as FFN (a bound)
+    else:  # NCCL transport: the collectives run on NCCL's streams; the whole step as FFN (a bound)
         stages = dict(route=0.0, permute=0.0, gemm1=ms, gemm2=0.0, combine=0.0)
+        ep_status, _ = ep_model.status()
+        if ep_status != 0:
+            raise SystemExit(f"--ep-transport nccl: a (source, destination) pair overflowed the {ep_model.cap}-row "
+                             "chunk (status 2); raise --ep-recv-cap")
     layer.set_profiling(False)
     if world > 1:
         t = torch.tensor([ms], device=device)
@@ -668,6 +683,19 @@ def main():
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def ensure_group_for_ep_at_1(args, world):
+    """--ep-at-1 without torchrun: a world-1 NCCL group, so the expert-parallel
+    code path (handle exchange, device barriers, stage events, report) runs on
+    one GPU."""
+    import torch
+    import torch.distributed as dist
+
+    if args.ep_at_1 and world == 1 and args.parallel == "ep" and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
 
 
 def nccl_log_to_stderr():
@@ -905,7 +933,8 @@ def main_stack(args):
     device = torch.device("cuda", local)
     m, E, k, L, d, f, P, Tp = args.stream_layers, 8, 2, 4, 4096, 14336, 32, 2048
     strong = args.scaling == "strong" and world > 1
-    use_ep = args.parallel == "ep" and world > 1
+    use_ep = args.parallel == "ep" and (world > 1 or args.ep_at_1)
+    ensure_group_for_ep_at_1(args, world)
     if use_ep and args.ep_transport != "p2p":
         raise SystemExit("--config stack: expert parallelism runs the p2p transport")
     if strong and P % world:

@@ -96,3 +96,27 @@ def test_gpu_arm_contract(graph):
     assert cb["value"] > 0 and cb["cores"] >= 1 and cb["kind"] in ("port", "reference")
     assert " of 512 tokens" in cb["sample"]  # the sample never exceeds the batch
     assert d["config"]["step_launch"].startswith("one CUDA graph" if graph == "on" else "eager")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_gpu_arm_expert_parallel_path(transport):
+    """The bench's expert-parallel path (a world-1 group on this one-GPU box):
+    the EP forward runs in the timed steps, and for the peer-memory transport
+    the line carries the EP stage times, exchange volume and placement."""
+    d = run_bench("--config", "tiny", "--steps", "4", "--warmup", "3", "--e2e-steps", "3", "--ep-at-1",
+                  "--ep-transport", transport, "--no-cpu-baseline")
+    assert d["value"] > 0 and d["gpu_launches"] > 0
+    if transport == "p2p":
+        ep = d["ep"]
+        assert set(ep["stages_ms"]) == {"route", "count_exchange", "dispatch", "dispatch_wait", "gemm1",
+                                        "gemm2_return", "return_wait", "combine"}
+        assert ep["rows_computed_per_rank"][0] > 0 and ep["placement"]
+
+
+@pytest.mark.gpu
+def test_stack_expert_parallel_path():
+    """--config stack on the EP path (world-1 group, 3 layers): every layer's
+    EP handle on one shared region, the gate computed per layer."""
+    d = run_bench("--config", "stack", "--stream-layers", "3", "--steps", "2", "--warmup", "3", "--ep-at-1")
+    assert d["value"] > 0 and d["ep"]["layers"] == 3 and d["config"]["routing_follows_trace"]
