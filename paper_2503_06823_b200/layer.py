@@ -54,6 +54,11 @@ class MoELayer:
         h = C.c_void_p()
         check(lib.emoe_layer_create(C.byref(cfg), C.byref(h)))
         self.h = h
+        w = Workspace()  # the layout constants are fixed at creation
+        check(lib.emoe_layer_workspace(self.h, C.byref(w)))
+        self.seg_pad = int(w.seg_pad)
+        self.gemm_cta_group = int(w.gemm_cta_group)
+        self.fp32_tensor_core = bool(w.fp32_tensor_core)
 
     def close(self):
         if getattr(self, "h", None):
