@@ -492,7 +492,7 @@ def main():
         launches_per_step = int(_lib.lib.emoe_kernel_launches() - l0)
         graph.replay()  # warm replay
         torch.cuda.synchronize()
-    elif ep_model is not None and args.ep_transport == "p2p":
+    elif ep_model is not None:
         ep_model.set_profiling(True)
     else:
         layer.set_profiling(True)
@@ -539,8 +539,11 @@ def main():
         ep_stats = ep_model.stats()
         stages = dict(route=ep_stages["route"], permute=ep_stages["dispatch"], gemm1=ep_stages["gemm1"],
                       gemm2=ep_stages["gemm2_return"], combine=ep_stages["combine"])
-    else:  # NCCL transport: the collectives run on NCCL's streams; the whole step as FFN (a bound)
-        stages = dict(route=0.0, permute=0.0, gemm1=ms, gemm2=0.0, combine=0.0)
+    else:  # NCCL transport: events on the compute stream, which waits on each collective
+        ep_stages = ep_model.stage_times()
+        ep_model.set_profiling(False)
+        stages = dict(route=ep_stages["route"], permute=ep_stages["dispatch"], gemm1=ep_stages["ffn"], gemm2=0.0,
+                      combine=ep_stages["combine"])
         ep_status, _ = ep_model.status()
         if ep_status != 0:
             raise SystemExit(f"--ep-transport nccl: a (source, destination) pair overflowed the {ep_model.cap}-row "
@@ -677,6 +680,17 @@ def main():
                                 experts=info["loads"]))
     if ep_stats:
         out["ep"] = ep_report(ep_model, ep_stages, ep_stats, world, rank, device)
+    elif ep_model is not None:  # NCCL transport
+        a2a_bytes = ep_model.send.numel() * ep_model.send.element_size()
+        out["ep"] = dict(transport="nccl: count all_gather_into_tensor, dispatch and return all_to_all_single over "
+                                   f"equal {ep_model.cap}-row chunks per (source, destination) pair, no host sync",
+                         stages_ms={kk: round(v, 4) for kk, v in ep_stages.items()},
+                         exchange=dict(a2a_bytes_per_call=a2a_bytes,
+                                       dispatch_a2a_gbs=round(a2a_bytes / max(ep_stages["dispatch_a2a"], 1e-9) / 1e6, 1),
+                                       return_a2a_gbs=round(a2a_bytes / max(ep_stages["return_a2a"], 1e-9) / 1e6, 1),
+                                       note="bytes each rank's all_to_all_single moves (whole chunks, incl. its own); "
+                                            "GB/s over the stage's events on the compute stream"),
+                         placement=ep_model.owned())
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = run_cpu_baseline(cfg, info["x_host"], info["wg"], info["experts"], info)
     if rank == 0:

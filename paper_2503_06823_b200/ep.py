@@ -331,6 +331,32 @@ class NcclExpertParallelMoE:
         self.back = torch.empty_like(self.send)
         self.table = torch.empty(self.world * layer.E, dtype=torch.int32, device=dev)
         self.stage_on_host = dist.get_backend(group) != "nccl"
+        self._prof = False
+        self._ev_sets = []  # one list of len(NCCL_STAGES) + 1 events per profiled forward
+
+    def set_profiling(self, enable: bool = True) -> None:
+        """Record CUDA events between the forward's stages (on the compute
+        stream, which waits on each collective, so a stage's time includes its
+        all-to-all); read them with stage_times()."""
+        self._prof = bool(enable)
+        self._ev_sets = []
+
+    def _mark(self, evs, s):
+        if evs is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(s)
+            evs.append(e)
+
+    def stage_times(self) -> dict:
+        """ms per stage (NCCL_STAGES), averaged over the profiled forwards;
+        synchronises the device."""
+        torch.cuda.synchronize()
+        tot = dict.fromkeys(NCCL_STAGES, 0.0)
+        for evs in self._ev_sets:
+            for i, name in enumerate(NCCL_STAGES):
+                tot[name] += evs[i].elapsed_time(evs[i + 1])
+        n = max(1, len(self._ev_sets))
+        return {k: v / n for k, v in tot.items()}
 
     def owned(self) -> list:
         return owned_experts(self.cum, self.rank)
@@ -352,7 +378,10 @@ class NcclExpertParallelMoE:
         sp = C.c_void_p(s.cuda_stream)
         lp = None if logits is None else C.c_void_p(logits.contiguous().data_ptr())
         T = x.shape[0]
+        evs = [] if self._prof else None
+        self._mark(evs, s)
         self._check(self._lib.emoe_epx_route(self.h, C.c_void_p(x.data_ptr()), lp, T, sp))
+        self._mark(evs, s)
         counts = self.layer.workspace()["counts"]
         if self.stage_on_host:
             parts = [torch.empty(self.E, dtype=torch.int32) for _ in range(self.world)]
@@ -360,14 +389,22 @@ class NcclExpertParallelMoE:
             self.table.copy_(torch.cat(parts))
         else:
             dist.all_gather_into_tensor(self.table, counts, group=self.group)
+        self._mark(evs, s)
         self._check(self._lib.emoe_epx_dispatch(self.h, C.c_void_p(self.table.data_ptr()), C.c_void_p(x.data_ptr()),
                                                 T, C.c_void_p(self.send.data_ptr()), sp))
+        self._mark(evs, s)
         self._a2a(self.recv, self.send)
+        self._mark(evs, s)
         self._check(self._lib.emoe_epx_ffn(self.h, C.c_void_p(self.recv.data_ptr()), C.c_void_p(self.ret.data_ptr()),
                                            sp))
+        self._mark(evs, s)
         self._a2a(self.back, self.ret)
+        self._mark(evs, s)
         self._check(self._lib.emoe_epx_combine(self.h, C.c_void_p(self.back.data_ptr()), C.c_void_p(y.data_ptr()), T,
                                                sp))
+        self._mark(evs, s)
+        if evs is not None:
+            self._ev_sets.append(evs)
         return y
 
     __call__ = forward
@@ -408,6 +445,9 @@ def plan_pair_rows(cum: np.ndarray, loads, tokens: int, top_k: int, pad: int, sl
 
 
 STAGES = ["route", "count_exchange", "dispatch", "dispatch_wait", "gemm1", "gemm2_return", "return_wait", "combine"]
+# NcclExpertParallelMoE: route + permute, count all-gather, dispatch packing,
+# dispatch all-to-all, both GEMMs, return all-to-all, combine
+NCCL_STAGES = ["route", "count_exchange", "dispatch", "dispatch_a2a", "ffn", "return_a2a", "combine"]
 
 
 class PeerExpertParallelMoE:

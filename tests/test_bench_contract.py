@@ -103,7 +103,8 @@ def test_gpu_arm_contract(graph):
 def test_gpu_arm_expert_parallel_path(transport):
     """The bench's expert-parallel path (a world-1 group on this one-GPU box):
     the EP forward runs in the timed steps, and for the peer-memory transport
-    the line carries the EP stage times, exchange volume and placement."""
+    the line carries the EP stage times, exchange volume and placement (both
+    transports: the NCCL one from events on the compute stream)."""
     d = run_bench("--config", "tiny", "--steps", "4", "--warmup", "3", "--e2e-steps", "3", "--ep-at-1",
                   "--ep-transport", transport, "--no-cpu-baseline")
     assert d["value"] > 0 and d["gpu_launches"] > 0
@@ -112,6 +113,11 @@ def test_gpu_arm_expert_parallel_path(transport):
         assert set(ep["stages_ms"]) == {"route", "count_exchange", "dispatch", "dispatch_wait", "gemm1",
                                         "gemm2_return", "return_wait", "combine"}
         assert ep["rows_computed_per_rank"][0] > 0 and ep["placement"]
+    else:
+        ep = d["ep"]
+        assert set(ep["stages_ms"]) == {"route", "count_exchange", "dispatch", "dispatch_a2a", "ffn", "return_a2a",
+                                        "combine"}
+        assert ep["stages_ms"]["ffn"] > 0 and ep["exchange"]["a2a_bytes_per_call"] > 0 and ep["placement"]
 
 
 @pytest.mark.gpu
