@@ -24,6 +24,12 @@
 // rotating 128-column TMEM slots and the epilogue warps sum the chunks in
 // fp32 registers (round to nearest), ~2e-6 relative.  SwiGLU: the B tile is 64
 // rows of W1 and the same 64 rows of W3, so a tile yields 64 columns of H.
+// Schedule: whole tiles round-robin, or stream-K (the tiles' k-blocks split
+// evenly over the co-resident CTAs; a tile split between CTAs is finished by
+// the CTA holding its first k-blocks, which adds the others' raw partials in
+// k order) where the tile count leaves a wave mostly empty (config 1's GEMM2).
+// Variants measured and dropped (CTA-pair 256 x 256 tiles, the split done in
+// shared memory from raw fp32 operands): profiles/r02_tf32_variants_ab.txt.
 #include <algorithm>
 #include <cstdlib>
 #include <map>
@@ -67,14 +73,7 @@ struct Params {
   float* partial;   // [CTAs][32 float4 columns][128 rows] float4: one raw partial tile per CTA
   int32_t* arrive;  // [tiles] helper arrivals, zero between launches (the owner re-zeroes)
   int dp;           // 1: whole tiles round-robin (data-parallel), no split tiles
-  int prefetch_kb;  // > 0: L2 prefetch of the weight boxes this many k-blocks ahead
 };
-
-__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* desc, int32_t c0, int32_t c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(desc)),
-               "r"(c0), "r"(c1)
-               : "memory");
-}
 
 // D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, 1 CTA
 __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -251,16 +250,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int a_row = mb * BM;
         const int b_row = slot * p.b_rows_per_slot + nb * (EPI == EPI_SWIGLU ? BN / 2 : BN);
         for (int kb = g.kb0; kb < g.kb1; ++kb) {
-          if (p.prefetch_kb > 0) {  // weight boxes prefetch_kb k-blocks ahead (the segment's first ones at its start)
-            for (int q = (kb == g.kb0 ? kb : kb + p.prefetch_kb); q <= kb + p.prefetch_kb && q < g.kb1; ++q) {
-              tma_prefetch_l2_2d(&tb_hi, q * BK, b_row);
-              tma_prefetch_l2_2d(&tb_lo, q * BK, b_row);
-              if (EPI == EPI_SWIGLU) {
-                tma_prefetch_l2_2d(&tb2_hi, q * BK, b_row);
-                tma_prefetch_l2_2d(&tb2_lo, q * BK, b_row);
-              }
-            }
-          }
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
           uint8_t* st = smem + stage * STAGE_BYTES;
@@ -449,710 +438,13 @@ __global__ void split_tf32_kernel(const float4* x, float4* hi, float4* __restric
     l.y = v.y - h.y;
     l.z = v.z - h.z;
     l.w = v.w - h.w;
-#ifdef EMOE_TF32_RAW_HI_PROBE
-    // probe: hi = the raw fp32 value, lo = x - trunc_tf32(x) -- exact iff the
-    // tensor core reads a raw fp32 operand as its truncation
-    h = v;
-    l.x = v.x - __uint_as_float(__float_as_uint(v.x) & ~0x1FFFu);
-    l.y = v.y - __uint_as_float(__float_as_uint(v.y) & ~0x1FFFu);
-    l.z = v.z - __uint_as_float(__float_as_uint(v.z) & ~0x1FFFu);
-    l.w = v.w - __uint_as_float(__float_as_uint(v.w) & ~0x1FFFu);
-#endif
     hi[i] = h;
     lo[i] = l;
   }
 }
 
-// ---------------------------------------------------------------------------
-// Split-in-shared-memory form (SIS).  The tensor core reads a raw fp32
-// operand as its truncation to tf32 (measured: tools/probes/tf32_raw_hi_probe.py),
-// so hi needs no storage: HBM holds the raw fp32 weights, activations and H,
-// the TMA brings only those (16 KB of A + 16 KB of B per k-block, half of the
-// pre-split form's bytes), and two converter warps write lo = x - trunc(x)
-// of both tiles into a small lo ring in shared memory (same swizzled offsets:
-// the split is elementwise).  Per k-block the MMA issuer then runs
-// a_lo b_hi + a_hi b_lo + a_hi b_hi with a_hi / b_hi = the raw tiles.
-//   warp 0 TMA producer, warp 1 MMA issuer, warps 2-3 converters,
-//   warps 4-7 epilogue (TMEM lane quarter = warp % 4)
-// Raw ring RS x 32 KB, lo ring LS x 32 KB.  Same tiles, chunked accumulation,
-// stream-K / data-parallel schedule and epilogue as gemm_tf32x3_kernel.
-namespace sis {
-constexpr int RS = 4, LS = 2;
-constexpr int RAW_BYTES = 2 * TILE_BYTES;  // A raw + B raw
-constexpr int LO_BYTES = 2 * TILE_BYTES;   // A lo + B lo
-#ifndef EMOE_SIS_CONV_WARPS
-#define EMOE_SIS_CONV_WARPS 4
-#endif
-constexpr int CONV_WARPS = EMOE_SIS_CONV_WARPS;
-constexpr int NUM_THREADS = 32 * (2 + CONV_WARPS + 4);
-constexpr int SMEM_BYTES = 1024 + RS * RAW_BYTES + LS * LO_BYTES + 4096;
-static_assert(SMEM_BYTES <= 232448, "shared memory over the sm_100 per-block limit");
-static_assert(2 * RS * 8 + 2 * LS * 8 + 2 * SLOTS * 8 + 16 + 4 * (2 * MAX_SEGS + 1) <= 4096, "barrier area");
-}  // namespace sis
-
-__device__ __forceinline__ float tf32_trunc_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & ~0x1FFFu); }
-
-template <int EPI>
-__global__ void __launch_bounds__(sis::NUM_THREADS, 1)
-    gemm_tf32x3_sis_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-                           const __grid_constant__ CUtensorMap tb2, Params p) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* raw = smem;
-  uint8_t* lo = smem + sis::RS * sis::RAW_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(lo + sis::LS * sis::LO_BYTES);
-  uint64_t* empty_bar = full_bar + sis::RS;
-  uint64_t* lofull_bar = empty_bar + sis::RS;
-  uint64_t* loempty_bar = lofull_bar + sis::LS;
-  uint64_t* tfull_bar = loempty_bar + sis::LS;
-  uint64_t* tempty_bar = tfull_bar + SLOTS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + SLOTS);
-  int32_t* s_offs = reinterpret_cast<int32_t*>(tmem_slot + 4);
-  int32_t* s_slot = s_offs + MAX_SEGS + 1;
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int S = p.n_seg;
-  for (int i = threadIdx.x; i <= S; i += sis::NUM_THREADS) s_offs[i] = (int32_t)p.seg_offsets[i];
-  for (int i = threadIdx.x; i < S; i += sis::NUM_THREADS) s_slot[i] = p.slot_of_expert[p.seg_expert ? p.seg_expert[i] : i];
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&ta);
-    tma_prefetch_desc(&tb);
-    if (EPI == EPI_SWIGLU) tma_prefetch_desc(&tb2);
-    for (int s = 0; s < sis::RS; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
-    }
-    for (int s = 0; s < sis::LS; ++s) {
-      mbar_init(&lofull_bar[s], sis::CONV_WARPS);  // one arrival per converter warp
-      mbar_init(&loempty_bar[s], 1);
-    }
-    for (int b = 0; b < SLOTS; ++b) {
-      mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 4);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) {
-    tmem_alloc(tmem_slot, TMEM_COLS);
-    tmem_relinquish();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const int total_mb = s_offs[S] / BM;
-  const int total_tiles = total_mb * p.n_blocks;
-  const int KB = p.K / BK;
-  const int64_t U = (int64_t)total_tiles * KB;
-  const int P = (int)(U < (int64_t)gridDim.x ? U : (int64_t)gridDim.x);
-  const int me = blockIdx.x;
-  const int64_t u_begin = me < P ? range_start(me, P, U) : U;
-  const int64_t u_end = me < P ? range_start(me + 1, P, U) : U;
-  const Work work0{u_begin, u_end, KB, me, (int)gridDim.x, total_tiles, p.dp};
-
-  if (warp == 0) {
-    if (lane == 0) {  // ===== TMA producer: raw A and B
-      int stage = 0;
-      uint32_t phase = 0;
-      Work w = work0;
-      Segment g;
-      while (w.next(g)) {
-        int mb, nb, seg;
-        decode(g.t, total_mb, p.n_blocks, p.group_m, s_offs, S, mb, nb, seg);
-        const int a_row = mb * BM;
-        const int b_row = s_slot[seg] * p.b_rows_per_slot + nb * (EPI == EPI_SWIGLU ? BN / 2 : BN);
-        for (int kb = g.kb0; kb < g.kb1; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], sis::RAW_BYTES);
-          uint8_t* st = raw + stage * sis::RAW_BYTES;
-          const int kc = kb * BK;
-          tma_load_2d(&ta, &full_bar[stage], st, kc, a_row, kCacheEvictNormal);
-          if (EPI == EPI_SWIGLU) {  // B rows 0-63: W1, 64-127: W3 (same output columns)
-            tma_load_2d(&tb, &full_bar[stage], st + TILE_BYTES, kc, b_row, kCacheEvictNormal);
-            tma_load_2d(&tb2, &full_bar[stage], st + TILE_BYTES + TILE_BYTES / 2, kc, b_row, kCacheEvictNormal);
-          } else {
-            tma_load_2d(&tb, &full_bar[stage], st + TILE_BYTES, kc, b_row, kCacheEvictNormal);
-          }
-          if (++stage == sis::RS) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ===== MMA issuer
-      constexpr uint32_t idesc = umma_idesc_tf32(BM, BN);
-      int rs = 0, ls = 0;
-      uint32_t rphase = 0, lphase = 0;
-      uint32_t chunk = 0;
-      Work w = work0;
-      Segment g;
-      while (w.next(g)) {
-        for (int c0 = g.kb0; c0 < g.kb1; ++chunk) {
-          const int c1 = min(g.kb1, (c0 / CHUNK_KB + 1) * CHUNK_KB);
-          const int slot = chunk % SLOTS;
-          mbar_wait(&tempty_bar[slot], ((chunk / SLOTS) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t tmem_d = tmem_base + slot * BN;
-          for (int kb = c0; kb < c1; ++kb) {
-            mbar_wait(&full_bar[rs], rphase);
-            mbar_wait(&lofull_bar[ls], lphase);
-            tc_fence_after();
-            uint8_t* st = raw + rs * sis::RAW_BYTES;
-            uint8_t* sl = lo + ls * sis::LO_BYTES;
-            const uint64_t a_hi = umma_desc_sw128(st), b_hi = umma_desc_sw128(st + TILE_BYTES);
-            const uint64_t a_lo = umma_desc_sw128(sl), b_lo = umma_desc_sw128(sl + TILE_BYTES);
-#pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint64_t o = (uint64_t)(kk * 2);
-              umma_tf32(tmem_d, a_lo + o, b_hi + o, idesc, (kb != c0 || kk != 0) ? 1u : 0u);
-              umma_tf32(tmem_d, a_hi + o, b_lo + o, idesc, 1u);
-              umma_tf32(tmem_d, a_hi + o, b_hi + o, idesc, 1u);
-            }
-            umma_commit(&empty_bar[rs]);
-            umma_commit(&loempty_bar[ls]);
-            if (++rs == sis::RS) {
-              rs = 0;
-              rphase ^= 1;
-            }
-            if (++ls == sis::LS) {
-              ls = 0;
-              lphase ^= 1;
-            }
-          }
-          umma_commit(&tfull_bar[slot]);
-          c0 = c1;
-        }
-      }
-    }
-  } else if (warp < 2 + sis::CONV_WARPS) {  // ===== converters: lo = x - trunc_tf32(x) of both raw tiles
-    constexpr int CT = 32 * sis::CONV_WARPS;
-    const int ct = threadIdx.x - 64;
-    int rs = 0, ls = 0;
-    uint32_t rphase = 0, lphase = 0;
-    Work w = work0;
-    Segment g;
-    while (w.next(g)) {
-      for (int kb = g.kb0; kb < g.kb1; ++kb) {
-        mbar_wait(&full_bar[rs], rphase);
-        mbar_wait(&loempty_bar[ls], lphase ^ 1);
-        // explicit shared-space accesses (the aligned smem base is a generic
-        // pointer: plain loads compiled to generic LD/ST)
-        const uint32_t src = smem_u32(raw + rs * sis::RAW_BYTES) + ct * 16;
-        const uint32_t dst = smem_u32(lo + ls * sis::LO_BYTES) + ct * 16;
-#pragma unroll 1
-        for (int i0 = 0; i0 < sis::RAW_BYTES; i0 += CT * 16 * 8) {
-          float4 v[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(v[j].x), "=f"(v[j].y), "=f"(v[j].z), "=f"(v[j].w)
-                         : "r"(src + i0 + j * CT * 16));
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + i0 + j * CT * 16),
-                         "f"(tf32_trunc_lo(v[j].x)), "f"(tf32_trunc_lo(v[j].y)), "f"(tf32_trunc_lo(v[j].z)),
-                         "f"(tf32_trunc_lo(v[j].w))
-                         : "memory");
-        }
-        fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&lofull_bar[ls]);
-        if (++rs == sis::RS) {
-          rs = 0;
-          rphase ^= 1;
-        }
-        if (++ls == sis::LS) {
-          ls = 0;
-          lphase ^= 1;
-        }
-      }
-    }
-  } else {  // ===== epilogue: the last 4 warps
-    const int quarter = warp & 3;
-    const int r_local = quarter * 32 + lane;
-    uint32_t chunk = 0;
-    Work w = work0;
-    Segment g;
-    while (w.next(g)) {
-      float acc[BN];
-#pragma unroll
-      for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
-      for (int c0 = g.kb0; c0 < g.kb1; ++chunk) {
-        const int c1 = min(g.kb1, (c0 / CHUNK_KB + 1) * CHUNK_KB);
-        const int slot = chunk % SLOTS;
-        mbar_wait(&tfull_bar[slot], (chunk / SLOTS) & 1);
-        tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + slot * BN;
-#pragma unroll
-        for (int cc = 0; cc < BN; cc += 32) {
-          uint32_t a[32];
-          tmem_ld_32x32b_x32(taddr + cc, a);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) acc[cc + j] += __uint_as_float(a[j]);
-        }
-        tc_fence_before();
-        if (lane == 0) mbar_arrive(&tempty_bar[slot]);
-        c0 = c1;
-      }
-      if (g.kb0 > 0) {  // stream-K helper (see gemm_tf32x3_kernel)
-        float4* mine = reinterpret_cast<float4*>(p.partial + (int64_t)me * (BM * BN));
-#pragma unroll
-        for (int j = 0; j < BN; j += 4)
-          __stcg(mine + (j / 4) * BM + r_local, make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 2 + sis::CONV_WARPS && lane == 0)
-          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.arrive + g.t) : "memory");
-        continue;
-      }
-      if (g.kb1 < KB) {  // stream-K owner
-        const int last = worker_of((int64_t)g.t * KB + KB - 1, P, U);
-        wait_helpers(p.arrive + g.t, last - me, lane);
-        for (int q = me + 1; q <= last; ++q) {
-          const float4* hp = reinterpret_cast<const float4*>(p.partial + (int64_t)q * (BM * BN));
-#pragma unroll
-          for (int j = 0; j < BN; j += 4) {
-            const float4 v = __ldcg(hp + (j / 4) * BM + r_local);
-            acc[j] += v.x;
-            acc[j + 1] += v.y;
-            acc[j + 2] += v.z;
-            acc[j + 3] += v.w;
-          }
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 2 + sis::CONV_WARPS && lane == 0) p.arrive[g.t] = 0;
-      }
-      int mb, nb, seg;
-      decode(g.t, total_mb, p.n_blocks, p.group_m, s_offs, S, mb, nb, seg);
-      const int64_t row = (int64_t)mb * BM + r_local;
-      float* orow = p.out_hi + row * p.ldo + nb * p.out_block_cols;
-      constexpr int OUT = EPI == EPI_SWIGLU ? BN / 2 : BN;
-#pragma unroll
-      for (int cc = 0; cc < OUT; cc += 4) {
-        float v[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float gv = acc[cc + i];
-          if (EPI == EPI_SWIGLU)
-            v[i] = gv / (1.0f + expf(-gv)) * acc[BN / 2 + cc + i];
-          else if (EPI == EPI_RELU)
-            v[i] = fmaxf(gv, 0.0f);
-          else
-            v[i] = gv;
-        }
-        *reinterpret_cast<float4*>(orow + cc) = make_float4(v[0], v[1], v[2], v[3]);
-      }
-    }
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
-  }
-}
-
 }  // namespace tf32x3
 
-// ---------------------------------------------------------------------------
-// CTA-pair, stream-K form (the default where the shape tiles).
-//
-// The 1-CTA 128 x 128 tile above needs 64 KB of operands (A and B, hi and lo)
-// per 768-clock k-block: ~85 B/clk per SM, more than L2 feeds 148 SMs at
-// once, and a config-1 GEMM1 has 448 such tiles = 3.03 waves (4 rounds).
-// Here a CTA pair (cta_group::2) computes a 256 x 256 tile: each CTA loads
-// its own 128 A rows and half of the 256 B rows (hi and lo, 64 KB per k-block
-// of 1536 clocks: ~42 B/clk per SM), and the tiles' k-blocks are divided
-// evenly over the co-resident pairs (stream-K), so every pair does the same
-// number of MMAs whatever the tile count.  A tile whose k range spans several
-// pairs is finished by the pair that computed its first k-blocks (the
-// "owner": that segment is the last of the owner's range, so the helpers --
-// whose piece of the tile is the FIRST of theirs -- finish early): each
-// helper stores its raw fp32 partial and counts itself in on the tile's
-// arrival counter, the owner waits for all of them and adds the partials in
-// k order (deterministic for a given tile count), then applies the epilogue.
-//   warp 0      TMA producer (every CTA; completion bytes on the leader's barrier)
-//   warp 1      MMA issuer (leader CTA, one thread)
-//   warps 2..9  epilogue: two warps per TMEM lane quarter, each draining half
-//               of the 256 accumulator columns (SwiGLU: 64 gate + the same 64
-//               up columns), summing the 128-long K chunks in fp32 registers
-namespace tf32p {
-
-constexpr int BM = 128;  // rows per CTA (a pair tile covers 256)
-constexpr int TILE_M = 256;
-constexpr int BN = 256;  // accumulator columns per tile
-constexpr int BK = 32;
-constexpr int STAGES = 3;
-constexpr int TILE_BYTES = 128 * 128;
-constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // A hi, A lo, B half hi, B half lo
-constexpr int EW = 8;
-constexpr int NUM_THREADS = 64 + 32 * EW;
-constexpr int SLOTS = 2;  // TMEM accumulator slots of 256 columns
-constexpr int CHUNK_KB = 4;
-constexpr int TMEM_COLS = SLOTS * BN;
-constexpr int MAX_SEGS = 256;
-constexpr int BAR_BYTES = 4096;
-constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + BAR_BYTES;
-constexpr int PARTIAL_FLOATS = 2 * BM * BN;  // one pair's partial tile (both CTAs)
-static_assert(2 * STAGES * 8 + 2 * SLOTS * 8 + 16 + 4 * (2 * MAX_SEGS + 1) <= BAR_BYTES, "barrier / table area");
-static_assert(SMEM_BYTES <= 232448, "shared memory over the sm_100 per-block limit");
-
-struct Params {
-  const int64_t* seg_offsets;  // [n_seg + 1], multiples of 256
-  const int32_t* slot_of_expert;
-  const int32_t* seg_expert;
-  int n_seg;
-  int K;
-  int n_blocks;
-  int out_block_cols;  // 128 (SwiGLU) or 256
-  int b_rows_per_slot;
-  int group_m;
-  float* out_hi;
-  float* out_lo;
-  int64_t ldo;
-  float* partial;   // [pairs][2 CTAs][64 float4 columns][128 rows] float4
-  int32_t* arrive;  // [tiles][2], zero between launches (the owner re-zeroes)
-  uint64_t hint_a, hint_b;  // L2 policies: the A rows are reused by every n-block, a weight box by one tile
-  int prefetch_kb;          // > 0: L2 prefetch of the weight boxes this many k-blocks ahead
-};
-
-__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* desc, int32_t c0, int32_t c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(desc)),
-               "r"(c0), "r"(c1)
-               : "memory");
-}
-
-__device__ __forceinline__ void umma_tf32_pair(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                               uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-using tf32x3::range_start;
-using tf32x3::wait_helpers;
-using tf32x3::worker_of;
-
-// tile t -> (256-row block, n-block, segment) in the grouped raster of tf32x3::decode
-__device__ __forceinline__ void tile_decode(int t, int total_mb, int n_blocks, int group_m, const int32_t* offs,
-                                            int n_seg, int& mb, int& nb, int& seg) {
-  const int per_group = group_m * n_blocks;
-  const int g = t / per_group;
-  const int local = t - g * per_group;
-  const int rows_in_group = min(group_m, total_mb - g * group_m);
-  nb = local / rows_in_group;
-  mb = g * group_m + (local - nb * rows_in_group);
-  const int row = mb * TILE_M;
-  int e = 0, hi = n_seg - 1;
-  while (e < hi) {
-    const int mid = (e + hi + 1) >> 1;
-    if (offs[mid] <= row)
-      e = mid;
-    else
-      hi = mid - 1;
-  }
-  seg = e;
-}
-
-__device__ __forceinline__ void epi_barrier() {  // the 8 epilogue warps of this CTA
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
-}
-
-template <int EPI>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    gemm_tf32x3_pair_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
-                            const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
-                            const __grid_constant__ CUtensorMap tb2_hi, const __grid_constant__ CUtensorMap tb2_lo,
-                            Params p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* tfull_bar = empty_bar + STAGES;  // [SLOTS]
-  uint64_t* tempty_bar = tfull_bar + SLOTS;  // [SLOTS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + SLOTS);
-  int32_t* s_offs = reinterpret_cast<int32_t*>(tmem_slot + 4);
-  int32_t* s_slot = s_offs + MAX_SEGS + 1;
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  const int pair = blockIdx.x / 2, P = gridDim.x / 2;
-  const int S = p.n_seg;
-  for (int i = threadIdx.x; i <= S; i += NUM_THREADS) s_offs[i] = (int32_t)p.seg_offsets[i];
-  for (int i = threadIdx.x; i < S; i += NUM_THREADS) s_slot[i] = p.slot_of_expert[p.seg_expert ? p.seg_expert[i] : i];
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&ta_hi);
-    tma_prefetch_desc(&ta_lo);
-    tma_prefetch_desc(&tb_hi);
-    tma_prefetch_desc(&tb_lo);
-    if (EPI == EPI_SWIGLU) {
-      tma_prefetch_desc(&tb2_hi);
-      tma_prefetch_desc(&tb2_lo);
-    }
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
-    }
-    for (int b = 0; b < SLOTS; ++b) {
-      mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 2 * EW);  // every epilogue warp of both CTAs
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const int total_mb = s_offs[S] / TILE_M;
-  const int total_tiles = total_mb * p.n_blocks;
-  const int KB = p.K / BK;
-  const int64_t U = (int64_t)total_tiles * KB;
-  // at most one pair per k-block, so every working pair's range is non-empty
-  // (an owner's helpers are then exactly the pairs after it up to the tile's end)
-  const int Pe = (int)(U < P ? U : P);
-  const int64_t u_begin = pair < Pe ? range_start(pair, Pe, U) : U;
-  const int64_t u_end = pair < Pe ? range_start(pair + 1, Pe, U) : U;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ===== TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t u = u_begin; u < u_end;) {
-        const int t = (int)(u / KB);
-        const int kb0 = (int)(u - (int64_t)t * KB);
-        const int kb1 = (int)(u_end - u < (int64_t)(KB - kb0) ? kb0 + (u_end - u) : KB);
-        u += kb1 - kb0;
-        int mb, nb, seg;
-        tile_decode(t, total_mb, p.n_blocks, p.group_m, s_offs, S, mb, nb, seg);
-        const int slot = s_slot[seg];
-        const int a_row = mb * TILE_M + (int)rank * BM;
-        // SwiGLU: the leader holds the tile's 128 W1 rows, the follower the same W3 rows
-        const int b_row = EPI == EPI_SWIGLU ? slot * p.b_rows_per_slot + nb * (BN / 2)
-                                            : slot * p.b_rows_per_slot + nb * BN + (int)rank * BM;
-        const CUtensorMap* bh = (EPI == EPI_SWIGLU && rank == 1) ? &tb2_hi : &tb_hi;
-        const CUtensorMap* bl = (EPI == EPI_SWIGLU && rank == 1) ? &tb2_lo : &tb_lo;
-        if (p.prefetch_kb > 0)  // the segment's first weight boxes
-          for (int kb = kb0; kb < min(kb1, kb0 + p.prefetch_kb); ++kb) {
-            tma_prefetch_l2_2d(bh, kb * BK, b_row);
-            tma_prefetch_l2_2d(bl, kb * BK, b_row);
-          }
-        for (int kb = kb0; kb < kb1; ++kb) {
-          if (p.prefetch_kb > 0 && kb + p.prefetch_kb < kb1) {
-            tma_prefetch_l2_2d(bh, (kb + p.prefetch_kb) * BK, b_row);
-            tma_prefetch_l2_2d(bl, (kb + p.prefetch_kb) * BK, b_row);
-          }
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
-          uint8_t* st = smem + stage * STAGE_BYTES;
-          const int kc = kb * BK;
-          tma_load_2d_pair(&ta_hi, &full_bar[stage], st, kc, a_row, p.hint_a);
-          tma_load_2d_pair(&ta_lo, &full_bar[stage], st + TILE_BYTES, kc, a_row, p.hint_a);
-          tma_load_2d_pair(bh, &full_bar[stage], st + 2 * TILE_BYTES, kc, b_row, p.hint_b);
-          tma_load_2d_pair(bl, &full_bar[stage], st + 3 * TILE_BYTES, kc, b_row, p.hint_b);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-      // every stage released: the leader's last commits to our barriers have landed
-      for (int i = 0; i < STAGES; ++i) {
-        mbar_wait(&empty_bar[stage], phase ^ 1);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && leader) {  // ===== MMA issuer (leader)
-      constexpr uint32_t idesc = tf32x3::umma_idesc_tf32(2 * BM, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      uint32_t chunk = 0;
-      for (int64_t u = u_begin; u < u_end;) {
-        const int t = (int)(u / KB);
-        const int kb0 = (int)(u - (int64_t)t * KB);
-        const int kb1 = (int)(u_end - u < (int64_t)(KB - kb0) ? kb0 + (u_end - u) : KB);
-        u += kb1 - kb0;
-        for (int c0 = kb0; c0 < kb1; ++chunk) {
-          const int c1 = min(kb1, (c0 / CHUNK_KB + 1) * CHUNK_KB);  // chunks on absolute k boundaries
-          const int slot = chunk % SLOTS;
-          mbar_wait(&tempty_bar[slot], ((chunk / SLOTS) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t tmem_d = tmem_base + slot * BN;
-          for (int kb = c0; kb < c1; ++kb) {
-            mbar_wait(&full_bar[stage], phase);
-            tc_fence_after();
-            uint8_t* st = smem + stage * STAGE_BYTES;
-            const uint64_t a_hi = umma_desc_sw128(st), a_lo = umma_desc_sw128(st + TILE_BYTES);
-            const uint64_t b_hi = umma_desc_sw128(st + 2 * TILE_BYTES), b_lo = umma_desc_sw128(st + 3 * TILE_BYTES);
-#pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint64_t o = (uint64_t)(kk * 2);
-              umma_tf32_pair(tmem_d, a_lo + o, b_hi + o, idesc, (kb != c0 || kk != 0) ? 1u : 0u);
-              umma_tf32_pair(tmem_d, a_hi + o, b_lo + o, idesc, 1u);
-              umma_tf32_pair(tmem_d, a_hi + o, b_hi + o, idesc, 1u);
-            }
-            umma_commit_pair(&empty_bar[stage]);
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-          umma_commit_pair(&tfull_bar[slot]);
-          c0 = c1;
-        }
-      }
-    }
-  } else {  // ===== epilogue: warps 2..9
-    const int ew = warp - 2;
-    const int quarter = warp & 3;
-    const int half = ew / 4;
-    const int r_local = quarter * 32 + lane;  // this thread's row in the CTA's 128
-    // accumulator columns this warp drains, in 32-column pieces
-    int cols[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      cols[i] = EPI == EPI_SWIGLU ? (i < 2 ? 64 * half + 32 * i : BN / 2 + 64 * half + 32 * (i - 2))
-                                  : 128 * half + 32 * i;
-    uint32_t chunk = 0;
-    for (int64_t u = u_begin; u < u_end;) {
-      const int t = (int)(u / KB);
-      const int kb0 = (int)(u - (int64_t)t * KB);
-      const int kb1 = (int)(u_end - u < (int64_t)(KB - kb0) ? kb0 + (u_end - u) : KB);
-      u += kb1 - kb0;
-      float acc[128];
-#pragma unroll
-      for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
-      for (int c0 = kb0; c0 < kb1; ++chunk) {
-        const int c1 = min(kb1, (c0 / CHUNK_KB + 1) * CHUNK_KB);
-        const int slot = chunk % SLOTS;
-        mbar_wait(&tfull_bar[slot], (chunk / SLOTS) & 1);
-        tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + slot * BN;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint32_t a[32];
-          tmem_ld_32x32b_x32(taddr + cols[i], a);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) acc[32 * i + j] += __uint_as_float(a[j]);
-        }
-        tc_fence_before();
-        if (lane == 0) {
-          if (leader)
-            mbar_arrive_relaxed(&tempty_bar[slot]);
-          else
-            mbar_arrive_leader_relaxed(&tempty_bar[slot]);
-        }
-        c0 = c1;
-      }
-      // float4 column index (0..63) of this warp's piece i, element j0
-      float4* my_partial = reinterpret_cast<float4*>(p.partial + ((int64_t)pair * 2 + rank) * (BM * BN));
-      if (kb0 > 0) {
-        // helper: raw partial out, then count in on the tile's arrival counter
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            __stcg(my_partial + ((cols[i] + j) / 4) * BM + r_local,
-                   make_float4(acc[32 * i + j], acc[32 * i + j + 1], acc[32 * i + j + 2], acc[32 * i + j + 3]));
-        __threadfence();
-        epi_barrier();
-        if (ew == 0 && lane == 0) {
-          int32_t* cnt = p.arrive + (int64_t)t * 2 + rank;
-          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(cnt) : "memory");
-        }
-        continue;
-      }
-      if (kb1 < KB) {
-        // owner of a split tile: add the helpers' partials in k order
-        const int last = worker_of((int64_t)t * KB + KB - 1, Pe, U);
-        const int helpers = last - pair;
-        int32_t* cnt = p.arrive + (int64_t)t * 2 + rank;
-        wait_helpers(cnt, helpers, lane);
-        for (int q = pair + 1; q <= last; ++q) {
-          const float4* hp = reinterpret_cast<const float4*>(p.partial + ((int64_t)q * 2 + rank) * (BM * BN));
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 v = __ldcg(hp + ((cols[i] + j) / 4) * BM + r_local);
-              acc[32 * i + j] += v.x;
-              acc[32 * i + j + 1] += v.y;
-              acc[32 * i + j + 2] += v.z;
-              acc[32 * i + j + 3] += v.w;
-            }
-        }
-        epi_barrier();
-        if (ew == 0 && lane == 0) *cnt = 0;  // next launch (stream-ordered) starts from zero
-      }
-      int mb, nb, seg;
-      tile_decode(t, total_mb, p.n_blocks, p.group_m, s_offs, S, mb, nb, seg);
-      const int64_t row = (int64_t)mb * TILE_M + rank * BM + r_local;
-      if (EPI == EPI_SWIGLU) {
-        const int col0 = nb * (BN / 2) + 64 * half;
-        float* ohi = p.out_hi + row * p.ldo + col0;
-        float* olo = p.out_lo + row * p.ldo + col0;
-#pragma unroll
-        for (int c = 0; c < 64; c += 4) {
-          float h[4], l[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float g = acc[c + i];
-            const float v = g / (1.0f + expf(-g)) * acc[64 + c + i];
-            h[i] = round_tf32(v);
-            l[i] = v - h[i];
-          }
-          *reinterpret_cast<float4*>(ohi + c) = make_float4(h[0], h[1], h[2], h[3]);
-          *reinterpret_cast<float4*>(olo + c) = make_float4(l[0], l[1], l[2], l[3]);
-        }
-      } else {
-        const int col0 = nb * BN + 128 * half;
-        float* ohi = p.out_hi + row * p.ldo + col0;
-        float* olo = EPI == EPI_RELU ? p.out_lo + row * p.ldo + col0 : nullptr;
-#pragma unroll
-        for (int c = 0; c < 128; c += 4) {
-          float v[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) v[i] = EPI == EPI_RELU ? fmaxf(acc[c + i], 0.0f) : acc[c + i];
-          if (EPI == EPI_STORE) {
-            *reinterpret_cast<float4*>(ohi + c) = make_float4(v[0], v[1], v[2], v[3]);
-          } else {
-            float h[4], l[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              h[i] = round_tf32(v[i]);
-              l[i] = v[i] - h[i];
-            }
-            *reinterpret_cast<float4*>(ohi + c) = make_float4(h[0], h[1], h[2], h[3]);
-            *reinterpret_cast<float4*>(olo + c) = make_float4(l[0], l[1], l[2], l[3]);
-          }
-        }
-      }
-    }
-  }
-  cluster_sync_all();  // the leader's commits to our barriers and TMEM are done
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS) : "memory");
-  }
-}
-
-}  // namespace tf32p
 
 typedef CUresult (*PFN_encodeTiled32)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1197,9 +489,9 @@ bool gemm_tf32x3_supported(int epi, int K, int N_out) {
 
 int gemm_tf32x3_b_box_rows(int epi) { return epi == EPI_SWIGLU ? tf32x3::BN / 2 : tf32x3::BN; }
 
-// co-resident CTAs of a stream-K kernel (owners wait on helpers, so every
-// CTA of the grid must be resident at once), per device and kernel
-static int coresident_ctas(const void* kernel, int threads, int smem, int cluster) {
+// co-resident CTAs of the persistent stream-K kernel (owners wait on
+// helpers, so every CTA of the grid must be resident at once), per device
+static int coresident_ctas(const void* kernel, int threads, int smem) {
   static std::mutex mu;
   static std::map<std::pair<int, const void*>, int> cache;
   int dev = 0;
@@ -1208,40 +500,18 @@ static int coresident_ctas(const void* kernel, int threads, int smem, int cluste
   auto it = cache.find({dev, kernel});
   if (it != cache.end()) return it->second;
   ensure_max_dynamic_smem(kernel, smem);
-  int sms = 0;
+  int sms = 0, per_sm = 0;
   EMOE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  int n = 0;
-  if (cluster == 1) {
-    int per_sm = 0;
-    EMOE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
-    n = std::min(per_sm, 1) * sms;  // persistent: one CTA per SM
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((sms / cluster) * cluster);
-    cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int clusters = 0;
-    EMOE_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kernel, &cfg));
-    n = std::min(clusters, sms / cluster) * cluster;
-  }
-  if (n < cluster) throw CudaError("gemm_tf32x3: the kernel does not fit on this device");
+  EMOE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  const int n = std::min(per_sm, 1) * sms;  // persistent: one CTA per SM
+  if (n < 1) throw CudaError("gemm_tf32x3: the kernel does not fit on this device");
   cache[{dev, kernel}] = n;
   return n;
 }
 
-size_t gemm_tf32x3_partial_floats(int num_sms, bool pair) {
-  return pair ? (size_t)(num_sms / 2) * tf32p::PARTIAL_FLOATS : (size_t)num_sms * tf32x3::BM * tf32x3::BN;
-}
+size_t gemm_tf32x3_partial_floats(int num_sms) { return (size_t)num_sms * tf32x3::BM * tf32x3::BN; }
 
-int64_t gemm_tf32x3_arrivals(int epi, int N_out, int64_t rows, bool pair) {
-  if (pair) return ceil_div(rows, tf32p::TILE_M) * (N_out / (epi == EPI_SWIGLU ? tf32p::BN / 2 : tf32p::BN)) * 2;
+int64_t gemm_tf32x3_arrivals(int epi, int N_out, int64_t rows) {
   return ceil_div(rows, tf32x3::BM) * (N_out / (epi == EPI_SWIGLU ? tf32x3::BN / 2 : tf32x3::BN));
 }
 
@@ -1276,24 +546,22 @@ void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t*
   p.ldo = ldo;
   p.partial = sk.partial;
   p.arrive = sk.arrive;
-  // A/B knobs: EMOE_TF32_SK = bitmask of the GEMMs that run stream-K (1 =
-  // GEMM1, 2 = GEMM2; the others whole tiles round-robin); EMOE_TF32_PREFETCH=n
+  // Schedule (profiles/r02_tf32_variants_ab.txt): GEMM2 stream-K (config 1:
+  // 64 tiles of 112 k-blocks for 148 SMs, 56.3 -> 50.3 us over split-K),
+  // GEMM1 whole tiles round-robin (448 tiles = 3.03 waves: stream-K's fixups
+  // cost more than the 4th round's 4 tiles).  EMOE_TF32_SK = bitmask of the
+  // GEMMs on stream-K (1 = GEMM1, 2 = GEMM2), A/B runs.
   static const int sk_mask = [] {
     const char* v = getenv("EMOE_TF32_SK");
     return v ? atoi(v) : 2;
   }();
-  static const int prefetch = [] {
-    const char* v = getenv("EMOE_TF32_PREFETCH");
-    return v ? atoi(v) : 0;
-  }();
   p.dp = (sk_mask & (epi == EPI_STORE ? 2 : 1)) ? 0 : 1;
-  p.prefetch_kb = prefetch;
-  EMOE_REQUIRE(gemm_tf32x3_arrivals(epi, N_out, max_rows, false) <= sk.arrivals,
+  EMOE_REQUIRE(gemm_tf32x3_arrivals(epi, N_out, max_rows) <= sk.arrivals,
                "gemm_tf32x3: stream-K arrival table smaller than the tile count");
   const void* kern = epi == EPI_SWIGLU ? reinterpret_cast<const void*>(gemm_tf32x3_kernel<EPI_SWIGLU>)
                      : epi == EPI_RELU ? reinterpret_cast<const void*>(gemm_tf32x3_kernel<EPI_RELU>)
                                        : reinterpret_cast<const void*>(gemm_tf32x3_kernel<EPI_STORE>);
-  int ctas = coresident_ctas(kern, NUM_THREADS, SMEM_BYTES, 1);
+  int ctas = coresident_ctas(kern, NUM_THREADS, SMEM_BYTES);
   ctas = (int)std::min<size_t>(ctas, sk.partial_floats / (BM * BN));
   EMOE_REQUIRE(ctas >= 1, "gemm_tf32x3: stream-K partial buffer too small");
   if (epi == EPI_SWIGLU)
@@ -1302,140 +570,6 @@ void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t*
     launch_1cta<EPI_RELU>(ops, p, ctas, stream);
   else
     launch_1cta<EPI_STORE>(ops, p, ctas, stream);
-  EMOE_CUDA(cudaGetLastError());
-  count_launch();
-}
-
-}  // namespace emoe
-
-namespace emoe {
-
-bool gemm_tf32x3_pair_supported(int epi, int K, int N_out) {
-  return K % tf32p::BK == 0 && N_out % (epi == EPI_SWIGLU ? tf32p::BN / 2 : tf32p::BN) == 0;
-}
-
-void launch_grouped_gemm_tf32x3_pair(int epi, const Tf32Operands& ops, const int64_t* seg_offsets,
-                                     const int32_t* slot_of_expert, const int32_t* seg_expert, int n_seg, int K,
-                                     int N_out, int b_rows_per_slot, float* out_hi, float* out_lo, int64_t ldo,
-                                     int64_t max_rows, const StreamK& sk, cudaStream_t stream) {
-  using namespace tf32p;
-  EMOE_REQUIRE(n_seg >= 1 && n_seg <= MAX_SEGS, "gemm_tf32x3_pair: segment count out of range");
-  EMOE_REQUIRE(gemm_tf32x3_pair_supported(epi, K, N_out), "gemm_tf32x3_pair: K % 32 and N % tile must be 0");
-  EMOE_REQUIRE(epi == EPI_STORE || out_lo, "gemm_tf32x3_pair: GEMM1 needs the lo output");
-  Params p;
-  p.seg_offsets = seg_offsets;
-  p.slot_of_expert = slot_of_expert;
-  p.seg_expert = seg_expert;
-  p.n_seg = n_seg;
-  p.K = K;
-  p.out_block_cols = epi == EPI_SWIGLU ? BN / 2 : BN;
-  p.n_blocks = N_out / p.out_block_cols;
-  p.b_rows_per_slot = b_rows_per_slot;
-  // raster: an A panel of ~8 MB (hi + lo rows) stays in L2 while the weight tiles pass
-  p.group_m = std::max(1, std::min(64, (int)((8ll << 20) / ((int64_t)TILE_M * K * 8))));
-  p.out_hi = out_hi;
-  p.out_lo = out_lo;
-  p.ldo = ldo;
-  p.partial = sk.partial;
-  p.arrive = sk.arrive;
-  // A/B knobs: EMOE_TF32_HINTS=0 evict-normal everywhere; EMOE_TF32_PREFETCH=n k-blocks
-  static const int hints = [] {
-    const char* v = getenv("EMOE_TF32_HINTS");
-    return v ? atoi(v) : 1;
-  }();
-  static const int prefetch = [] {
-    const char* v = getenv("EMOE_TF32_PREFETCH");
-    return v ? atoi(v) : 0;
-  }();
-  p.hint_a = hints ? kCacheEvictLast : kCacheEvictNormal;
-  p.hint_b = hints ? kCacheEvictFirst : kCacheEvictNormal;
-  p.prefetch_kb = prefetch;
-  EMOE_REQUIRE(gemm_tf32x3_arrivals(epi, N_out, max_rows, true) <= sk.arrivals,
-               "gemm_tf32x3_pair: stream-K arrival table smaller than the tile count");
-  const void* kern = epi == EPI_SWIGLU ? reinterpret_cast<const void*>(gemm_tf32x3_pair_kernel<EPI_SWIGLU>)
-                     : epi == EPI_RELU ? reinterpret_cast<const void*>(gemm_tf32x3_pair_kernel<EPI_RELU>)
-                                       : reinterpret_cast<const void*>(gemm_tf32x3_pair_kernel<EPI_STORE>);
-  int clusters = coresident_ctas(kern, NUM_THREADS, SMEM_BYTES, 2) / 2;
-  clusters = (int)std::min<size_t>(clusters, sk.partial_floats / PARTIAL_FLOATS);
-  EMOE_REQUIRE(clusters >= 1, "gemm_tf32x3_pair: stream-K partial buffer too small");
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * clusters);
-  cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (epi == EPI_SWIGLU)
-    EMOE_CUDA(cudaLaunchKernelEx(&cfg, gemm_tf32x3_pair_kernel<EPI_SWIGLU>, ops.a_hi, ops.a_lo, ops.b_hi, ops.b_lo,
-                                 ops.b2_hi, ops.b2_lo, p));
-  else if (epi == EPI_RELU)
-    EMOE_CUDA(cudaLaunchKernelEx(&cfg, gemm_tf32x3_pair_kernel<EPI_RELU>, ops.a_hi, ops.a_lo, ops.b_hi, ops.b_lo,
-                                 ops.b2_hi, ops.b2_lo, p));
-  else
-    EMOE_CUDA(cudaLaunchKernelEx(&cfg, gemm_tf32x3_pair_kernel<EPI_STORE>, ops.a_hi, ops.a_lo, ops.b_hi, ops.b_lo,
-                                 ops.b2_hi, ops.b2_lo, p));
-  EMOE_CUDA(cudaGetLastError());
-  count_launch();
-}
-
-}  // namespace emoe
-
-namespace emoe {
-
-template <int EPI>
-static void launch_sis(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
-                       const tf32x3::Params& p, int ctas, cudaStream_t stream) {
-  tf32x3::gemm_tf32x3_sis_kernel<EPI><<<ctas, tf32x3::sis::NUM_THREADS, tf32x3::sis::SMEM_BYTES, stream>>>(ta, tb, tb2,
-                                                                                                        p);
-}
-
-void launch_grouped_gemm_tf32x3_sis(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
-                                    const int64_t* seg_offsets, const int32_t* slot_of_expert,
-                                    const int32_t* seg_expert, int n_seg, int K, int N_out, int b_rows_per_slot,
-                                    float* out, int64_t ldo, int64_t max_rows, const StreamK& sk, cudaStream_t stream) {
-  using namespace tf32x3;
-  EMOE_REQUIRE(n_seg >= 1 && n_seg <= MAX_SEGS, "gemm_tf32x3_sis: segment count out of range");
-  EMOE_REQUIRE(gemm_tf32x3_supported(epi, K, N_out), "gemm_tf32x3_sis: K % 32 and N % tile must be 0");
-  Params p{};
-  p.seg_offsets = seg_offsets;
-  p.slot_of_expert = slot_of_expert;
-  p.seg_expert = seg_expert;
-  p.n_seg = n_seg;
-  p.K = K;
-  p.out_block_cols = epi == EPI_SWIGLU ? BN / 2 : BN;
-  p.n_blocks = N_out / p.out_block_cols;
-  p.b_rows_per_slot = b_rows_per_slot;
-  p.group_m = std::max(2, std::min(64, (int)((8ll << 20) / ((int64_t)BM * K * 4))));
-  p.out_hi = out;
-  p.out_lo = nullptr;
-  p.ldo = ldo;
-  p.partial = sk.partial;
-  p.arrive = sk.arrive;
-  static const int sk_mask = [] {  // as launch_grouped_gemm_tf32x3
-    const char* v = getenv("EMOE_TF32_SK");
-    return v ? atoi(v) : 2;
-  }();
-  p.dp = (sk_mask & (epi == EPI_STORE ? 2 : 1)) ? 0 : 1;
-  p.prefetch_kb = 0;
-  EMOE_REQUIRE(gemm_tf32x3_arrivals(epi, N_out, max_rows, false) <= sk.arrivals,
-               "gemm_tf32x3_sis: stream-K arrival table smaller than the tile count");
-  const void* kern = epi == EPI_SWIGLU ? reinterpret_cast<const void*>(gemm_tf32x3_sis_kernel<EPI_SWIGLU>)
-                     : epi == EPI_RELU ? reinterpret_cast<const void*>(gemm_tf32x3_sis_kernel<EPI_RELU>)
-                                       : reinterpret_cast<const void*>(gemm_tf32x3_sis_kernel<EPI_STORE>);
-  int ctas = coresident_ctas(kern, sis::NUM_THREADS, sis::SMEM_BYTES, 1);
-  ctas = (int)std::min<size_t>(ctas, sk.partial_floats / (BM * BN));
-  EMOE_REQUIRE(ctas >= 1, "gemm_tf32x3_sis: stream-K partial buffer too small");
-  if (epi == EPI_SWIGLU)
-    launch_sis<EPI_SWIGLU>(ta, tb, tb2, p, ctas, stream);
-  else if (epi == EPI_RELU)
-    launch_sis<EPI_RELU>(ta, tb, tb2, p, ctas, stream);
-  else
-    launch_sis<EPI_STORE>(ta, tb, tb2, p, ctas, stream);
   EMOE_CUDA(cudaGetLastError());
   count_launch();
 }

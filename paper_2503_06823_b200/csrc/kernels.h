@@ -147,34 +147,23 @@ void launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStre
                        const int64_t* rows_dev = nullptr, int row_elems = 0);
 // split-K scratch for small batches: `rows` = the row capacity of the
 // operands, `capacity` floats at `partial`
-// Stream-K scratch of the 3xTF32 kernels: one raw partial tile per
-// co-resident CTA (pair), and an arrival counter per output tile (per CTA of
-// a pair tile), zero-initialised once -- every launch leaves them zero
+// Stream-K scratch of the 3xTF32 kernel: one raw partial tile per
+// co-resident CTA, and an arrival counter per output tile, zero-initialised
+// once (every launch leaves them zero)
 struct StreamK {
   float* partial;
   size_t partial_floats;
   int32_t* arrive;
   int64_t arrivals;
 };
-size_t gemm_tf32x3_partial_floats(int num_sms, bool pair);
-int64_t gemm_tf32x3_arrivals(int epi, int N_out, int64_t rows, bool pair);
+size_t gemm_tf32x3_partial_floats(int num_sms);
+int64_t gemm_tf32x3_arrivals(int epi, int N_out, int64_t rows);
 // GEMM1 (SwiGLU/ReLU): out_hi/out_lo = split(H); GEMM2 (STORE): out_hi = Y.
 // 1-CTA 128 x 128 tiles (segments padded to 128 rows)
 void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t* seg_offsets,
                                 const int32_t* slot_of_expert, const int32_t* seg_expert, int n_seg, int K, int N_out,
                                 int b_rows_per_slot, float* out_hi, float* out_lo, int64_t ldo, int64_t max_rows,
                                 const StreamK& sk, cudaStream_t stream);
-// split-in-shared-memory form: raw fp32 operands (A rows, weight pool, H)
-void launch_grouped_gemm_tf32x3_sis(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
-                                    const int64_t* seg_offsets, const int32_t* slot_of_expert,
-                                    const int32_t* seg_expert, int n_seg, int K, int N_out, int b_rows_per_slot,
-                                    float* out, int64_t ldo, int64_t max_rows, const StreamK& sk, cudaStream_t stream);
-// CTA-pair 256 x 256 tiles (segments padded to 256 rows; A/B form)
-bool gemm_tf32x3_pair_supported(int epi, int K, int N_out);
-void launch_grouped_gemm_tf32x3_pair(int epi, const Tf32Operands& ops, const int64_t* seg_offsets,
-                                     const int32_t* slot_of_expert, const int32_t* seg_expert, int n_seg, int K,
-                                     int N_out, int b_rows_per_slot, float* out_hi, float* out_lo, int64_t ldo,
-                                     int64_t max_rows, const StreamK& sk, cudaStream_t stream);
 
 // K4 fp32 path (SIMT FFMA): same grouping/epilogues, fp32 in/out (shapes the
 // 3xTF32 kernel does not tile)

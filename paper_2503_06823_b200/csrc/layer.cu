@@ -156,21 +156,15 @@ struct emoe_layer {
   float* h_lo = nullptr;
   Tf32Operands op1{}, op2{};
   // stream-K scratch of the 3xTF32 GEMMs (grouped_gemm_tf32.cu): one raw
-  // partial tile per co-resident CTA and per-tile arrival counters;
-  // tf32_pair = the CTA-pair kernel (EMOE_TF32_KERNEL=pair, A/B runs;
-  // 256-row segments)
-  bool tf32_pair = false;
-  // tf32_sis = the split-in-shared-memory kernel: pools, activations and H
-  // stay raw fp32 (no lo twins, no split passes); EMOE_TF32_KERNEL=sis
-  bool tf32_sis = false;
+  // partial tile per co-resident CTA and per-tile arrival counters
   float* sk_partial = nullptr;
   size_t sk_partial_floats = 0;
   int32_t* sk_arrive = nullptr;
   int64_t sk_arrivals = 0;
   void ensure_sk_arrive(int64_t rows, cudaStream_t s) {
     const int epi1 = swiglu() ? EPI_SWIGLU : EPI_RELU;
-    const int64_t need = std::max(gemm_tf32x3_arrivals(epi1, cfg.d_ff, rows, tf32_pair),
-                                  gemm_tf32x3_arrivals(EPI_STORE, cfg.d_model, rows, tf32_pair));
+    const int64_t need =
+        std::max(gemm_tf32x3_arrivals(epi1, cfg.d_ff, rows), gemm_tf32x3_arrivals(EPI_STORE, cfg.d_model, rows));
     if (need <= sk_arrivals) return;
     if (sk_arrive) {
       EMOE_CUDA(cudaStreamSynchronize(s));  // earlier launches may still use the old table
@@ -396,8 +390,8 @@ struct emoe_layer {
     // 3xTF32 layers: the permute also writes the hi / lo split of every row
     // (the GEMM reads only those), so ffn() skips the separate split pass
     launch_permute(x, elem, T, cfg.d_model, E, cfg.top_k, served_idx, seg_offsets, block_base, x_perm, pos,
-                   row_token, s, tf32 && !tf32_sis ? x_hi : nullptr, tf32 && !tf32_sis ? x_lo : nullptr);
-    perm_split_done = tf32 && !tf32_sis;
+                   row_token, s, tf32 ? x_hi : nullptr, tf32 ? x_lo : nullptr);
+    perm_split_done = tf32;
   }
   bool perm_split_done = false;  // x_hi / x_lo hold the split of x_perm's rows
 
@@ -421,21 +415,6 @@ struct emoe_layer {
       if (ext_mark3) EMOE_CUDA(cudaEventRecord(ext_mark3, s));
       launch_grouped_gemm(EPI_STORE, cta_group, gemm_mc, a2, tb2, tb2, segs, slot_dev, n_seg, f, d, d,
                           static_cast<__nv_bfloat16*>(yr), d, num_sms, s, seg_expert, &o2, scatter, peer_out);
-      mark(4, s);
-    } else if (tf32 && tf32_sis) {
-      const int epi1 = swiglu() ? EPI_SWIGLU : EPI_RELU;
-      CUtensorMap a1 = op1.a_hi, a2 = op2.a_hi;
-      if (!workspace) {
-        a1 = make_tmap_f32_2d(xr, (uint64_t)R, d, 128);
-        a2 = make_tmap_f32_2d(hr, (uint64_t)R, f, 128);
-      }
-      ensure_sk_arrive(R, s);
-      const StreamK sk{sk_partial, sk_partial_floats, sk_arrive, sk_arrivals};
-      launch_grouped_gemm_tf32x3_sis(epi1, a1, op1.b_hi, op1.b2_hi, segs, slot_dev, seg_expert, n_seg, d, f, f,
-                                     static_cast<float*>(hr), f, R, sk, s);
-      mark(3, s);
-      launch_grouped_gemm_tf32x3_sis(EPI_STORE, a2, op2.b_hi, op2.b_hi, segs, slot_dev, seg_expert, n_seg, f, d, d,
-                                     static_cast<float*>(yr), d, R, sk, s);
       mark(4, s);
     } else if (tf32) {
       const int epi1 = swiglu() ? EPI_SWIGLU : EPI_RELU;
@@ -462,10 +441,11 @@ struct emoe_layer {
         launch_split_tf32(static_cast<const float*>(xr), xh, xl, R * d, s, segs + n_seg, d);
       ensure_sk_arrive(R, s);
       const StreamK sk{sk_partial, sk_partial_floats, sk_arrive, sk_arrivals};
-      auto gemm = tf32_pair ? launch_grouped_gemm_tf32x3_pair : launch_grouped_gemm_tf32x3;
-      gemm(epi1, o1, segs, slot_dev, seg_expert, n_seg, d, f, f, static_cast<float*>(hr), hl, f, R, sk, s);
+      launch_grouped_gemm_tf32x3(epi1, o1, segs, slot_dev, seg_expert, n_seg, d, f, f, static_cast<float*>(hr), hl,
+                                 f, R, sk, s);
       mark(3, s);
-      gemm(EPI_STORE, o2, segs, slot_dev, seg_expert, n_seg, f, d, d, static_cast<float*>(yr), nullptr, d, R, sk, s);
+      launch_grouped_gemm_tf32x3(EPI_STORE, o2, segs, slot_dev, seg_expert, n_seg, f, d, d, static_cast<float*>(yr),
+                                 nullptr, d, R, sk, s);
       mark(4, s);
     } else {
       launch_grouped_gemm_f32(swiglu() ? EPI_SWIGLU : EPI_RELU, static_cast<const float*>(xr), d,
@@ -617,7 +597,7 @@ struct emoe_layer {
       EMOE_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(w2_pool) + slot * b2, host_w2[e], b2, cudaMemcpyHostToDevice,
                                 cs));
       pending_bytes += (double)b2;
-      if (tf32 && !tf32_sis) {  // tf32 hi in place + fp32 lo twin, on the copy stream before the load event
+      if (tf32) {  // tf32 hi in place + fp32 lo twin, on the copy stream before the load event
         auto split = [&](void* pool, void* lo, size_t elems) {
           float* w = reinterpret_cast<float*>(static_cast<uint8_t*>(pool) + slot * elems * 4);
           launch_split_tf32(w, w, reinterpret_cast<float*>(static_cast<uint8_t*>(lo) + slot * elems * 4),
@@ -716,17 +696,7 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
                            atoi(getenv("EMOE_GEMM_MC")) == 2
                        ? 2
                        : 1;
-      if (c.dtype != EMOE_DTYPE_BF16) {
-        // fp32 on tensor cores: EMOE_TF32_KERNEL=pair runs the CTA-pair 3xTF32
-        // kernel where the shape tiles (A/B runs; slower)
-        const char* mode = getenv("EMOE_F32_GEMM");
-        const char* kern = getenv("EMOE_TF32_KERNEL");
-        const int epi1 = c.activation == EMOE_ACT_SWIGLU ? EPI_SWIGLU : EPI_RELU;
-        L->tf32_pair = !(mode && std::strcmp(mode, "ffma") == 0) && kern && std::strcmp(kern, "pair") == 0 &&
-                       gemm_tf32x3_pair_supported(epi1, (int)c.d_model, (int)c.d_ff) &&
-                       gemm_tf32x3_pair_supported(EPI_STORE, (int)c.d_ff, (int)c.d_model);
-      }
-      L->seg_pad = c.dtype == EMOE_DTYPE_BF16 ? gemm_tile_m(L->cta_group, L->gemm_mc) : (L->tf32_pair ? 256 : kSegPad);
+      L->seg_pad = c.dtype == EMOE_DTYPE_BF16 ? gemm_tile_m(L->cta_group, L->gemm_mc) : kSegPad;
       L->rows_cap = T * k + (int64_t)E * L->seg_pad;
       L->route_blocks = (int)ceil_div(T, kRouteBlockTokens);
       EMOE_CUDA(cudaStreamCreateWithFlags(&L->copy_stream, cudaStreamNonBlocking));
@@ -791,19 +761,7 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
         const uint64_t d = c.d_model, f = c.d_ff, slots = c.num_slots;
         L->tf32 = !(mode && std::strcmp(mode, "ffma") == 0) && gemm_tf32x3_supported(epi1, (int)d, (int)f) &&
                   gemm_tf32x3_supported(EPI_STORE, (int)f, (int)d);
-        const char* tk = getenv("EMOE_TF32_KERNEL");
-        L->tf32_sis = L->tf32 && !L->tf32_pair && tk && std::strcmp(tk, "sis") == 0;
-        if (L->tf32_sis) {
-          const uint32_t bb = gemm_tf32x3_b_box_rows(epi1), bb2 = gemm_tf32x3_b_box_rows(EPI_STORE);
-          L->op1.a_hi = make_tmap_f32_2d(L->x_perm, L->rows_cap, d, 128);
-          L->op1.b_hi = make_tmap_f32_2d(L->w1_pool, slots * f, d, bb);
-          L->op1.b2_hi = L->swiglu() ? make_tmap_f32_2d(L->w3_pool, slots * f, d, bb) : L->op1.b_hi;
-          L->op2.a_hi = make_tmap_f32_2d(L->h, L->rows_cap, f, 128);
-          L->op2.b_hi = make_tmap_f32_2d(L->w2_pool, slots * d, f, bb2);
-          L->sk_partial_floats = gemm_tf32x3_partial_floats(L->num_sms, false);
-          L->sk_partial = dmalloc<float>(L->sk_partial_floats);
-          L->ensure_sk_arrive(L->rows_cap, 0);
-        } else if (L->tf32) {
+        if (L->tf32) {
           const size_t pw1 = slots * L->w1_elems() * 4, pw2 = slots * L->w2_elems() * 4;
           L->w1_lo = dmalloc<uint8_t>(pw1);
           EMOE_CUDA(cudaMemset(L->w1_lo, 0, pw1));
@@ -816,8 +774,7 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
           L->x_hi = dmalloc<float>((size_t)L->rows_cap * d);
           L->x_lo = dmalloc<float>((size_t)L->rows_cap * d);
           L->h_lo = dmalloc<float>((size_t)L->rows_cap * f);
-          const uint32_t bb = L->tf32_pair ? 128 : gemm_tf32x3_b_box_rows(epi1),
-                         bb2 = L->tf32_pair ? 128 : gemm_tf32x3_b_box_rows(EPI_STORE);
+          const uint32_t bb = gemm_tf32x3_b_box_rows(epi1), bb2 = gemm_tf32x3_b_box_rows(EPI_STORE);
           L->op1.a_hi = make_tmap_f32_2d(L->x_hi, L->rows_cap, d, 128);
           L->op1.a_lo = make_tmap_f32_2d(L->x_lo, L->rows_cap, d, 128);
           L->op1.b_hi = make_tmap_f32_2d(L->w1_pool, slots * f, d, bb);
@@ -831,7 +788,7 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
           L->op2.b2_hi = L->op2.b_hi;
           L->op2.b2_lo = L->op2.b_lo;
           // stream-K scratch (one partial tile per co-resident CTA, ~10-19 MB)
-          L->sk_partial_floats = gemm_tf32x3_partial_floats(L->num_sms, L->tf32_pair);
+          L->sk_partial_floats = gemm_tf32x3_partial_floats(L->num_sms);
           L->sk_partial = dmalloc<float>(L->sk_partial_floats);
           L->ensure_sk_arrive(L->rows_cap, 0);
         }
@@ -862,8 +819,7 @@ int emoe_layer_share_workspace(emoe_layer* L, const emoe_layer* donor) {
     const emoe_layer_config &a = L->cfg, &b = donor->cfg;
     EMOE_REQUIRE(a.d_model == b.d_model && a.d_ff == b.d_ff && a.num_experts == b.num_experts &&
                      a.top_k == b.top_k && a.dtype == b.dtype && a.max_tokens == b.max_tokens &&
-                     L->rows_cap == donor->rows_cap && L->tf32 == donor->tf32 &&
-                     L->tf32_sis == donor->tf32_sis,
+                     L->rows_cap == donor->rows_cap && L->tf32 == donor->tf32,
                  "share_workspace: layers differ in shape, dtype, max_tokens or GEMM tiling");
     EMOE_CUDA(cudaDeviceSynchronize());  // nothing in flight on the buffers being released
     if (!L->borrowed_ws)
