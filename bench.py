@@ -446,16 +446,21 @@ def main():
 
     ep_model = None
     ep_stats = ep_stages = None
+    ep_fallback = None
     if use_ep and args.ep_transport == "p2p":
-        from paper_2503_06823_b200.ep import PeerExpertParallelMoE
-
-        ep_model = PeerExpertParallelMoE(layer, info["global_resident"], loads=info["aggregate"],
-                                         recv_rows_cap=args.ep_recv_cap)
-    elif use_ep:  # NCCL all-to-alls over capacity chunks, no host synchronisation
+        ep_model, ep_fallback = make_p2p_ep(layer, info, args, x, world, device)
+        if ep_model is None:  # every rank falls back together: the NCCL transport, same placement
+            args.ep_transport = "nccl"
+            if rank == 0:
+                print(f"bench: peer-memory EP unavailable ({ep_fallback}); running the NCCL transport",
+                      file=sys.stderr, flush=True)
+    if use_ep and args.ep_transport == "nccl":  # NCCL all-to-alls over capacity chunks, no host synchronisation
         from paper_2503_06823_b200.ep import NcclExpertParallelMoE, plan_pair_rows, plan_shares
 
         cum = plan_shares(info["global_resident"], cfg["E"], world, info["aggregate"])
-        cap = args.ep_recv_cap or plan_pair_rows(cum, info["aggregate"], T, cfg["k"], layer.seg_pad)
+        # --ep-recv-cap sizes the NCCL chunks too, unless it is the p2p setting that just failed
+        cap = (args.ep_recv_cap if not ep_fallback else 0) or plan_pair_rows(cum, info["aggregate"], T, cfg["k"],
+                                                                            layer.seg_pad)
         ep_model = NcclExpertParallelMoE(layer, info["global_resident"], loads=info["aggregate"], cap_rows=cap)
 
     def eager_step():
@@ -682,6 +687,8 @@ def main():
         out["ep"] = ep_report(ep_model, ep_stages, ep_stats, world, rank, device)
     elif ep_model is not None:  # NCCL transport
         a2a_bytes = ep_model.send.numel() * ep_model.send.element_size()
+        if ep_fallback:
+            out["config"]["ep_p2p_fallback"] = ep_fallback
         out["ep"] = dict(transport="nccl: count all_gather_into_tensor, dispatch and return all_to_all_single over "
                                    f"equal {ep_model.cap}-row chunks per (source, destination) pair, no host sync",
                          stages_ms={kk: round(v, 4) for kk, v in ep_stages.items()},
@@ -718,6 +725,36 @@ def nccl_log_to_stderr():
     os.environ.setdefault("NCCL_DEBUG", "INFO")
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,P2P,NVLS")
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
+
+def make_p2p_ep(layer, info, args, x, world, device):
+    """The peer-memory EP model, or (None, why) when it cannot run here: its
+    construction or a first forward failed (or timed out) on any rank -- the
+    ranks agree by an all-reduce, so all of them fall back together."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_06823_b200.ep import PeerExpertParallelMoE
+
+    os.environ.setdefault("EMOE_EP_TIMEOUT_S", "20")  # a failed peer surfaces as status 1, not a hang
+    model, err = None, None
+    try:
+        model = PeerExpertParallelMoE(layer, info["global_resident"], loads=info["aggregate"],
+                                      recv_rows_cap=args.ep_recv_cap)
+        model(x)
+        st, _ = model.status()
+        if st != 0:
+            err = f"first forward status {st}"
+    except Exception as e:  # noqa: BLE001 (reported, and every rank falls back)
+        err = f"{type(e).__name__}: {e}"
+    ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=device)
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if int(ok.item()) == 1:
+        return model, None
+    if model is not None:
+        model.close()
+    return None, err or "the peer-memory setup failed on another rank"
 
 
 def ep_report(ep_models, stages, stats, world, rank, device):

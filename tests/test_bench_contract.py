@@ -121,6 +121,17 @@ def test_gpu_arm_expert_parallel_path(transport):
 
 
 @pytest.mark.gpu
+def test_p2p_failure_falls_back_to_nccl():
+    """A peer-memory EP that cannot run (here: a 1-row receive buffer, so the
+    first forward reports an overflow) makes every rank fall back to the NCCL
+    transport with the same placement, and the line says why."""
+    d = run_bench("--config", "tiny", "--steps", "2", "--warmup", "3", "--e2e-steps", "2", "--ep-at-1",
+                  "--ep-transport", "p2p", "--ep-recv-cap", "1", "--no-cpu-baseline")
+    assert d["value"] > 0 and d["ep"]["transport"].startswith("nccl")
+    assert "status 2" in d["config"]["ep_p2p_fallback"]
+
+
+@pytest.mark.gpu
 def test_stack_expert_parallel_path():
     """--config stack on the EP path (world-1 group, 3 layers): every layer's
     EP handle on one shared region, the gate computed per layer."""
