@@ -287,7 +287,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // every CTA of a cluster walks the same number of tile slots
   const int64_t n_iter = (ceil_div(p.ntiles, CN) + n_clusters - 1 - cluster_id) / n_clusters;
 
-  routing::load_route_state(st, p.a);
   for (int i = threadIdx.x; i < NG * NE; i += NUM_THREADS) g_counts[i] = 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_x);
@@ -306,6 +305,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tmem_alloc(tmem_slot, TMEM_COLS);
     tmem_relinquish();
   }
+  // barriers, TMEM and descriptors are set up: from here on the kernel reads
+  // what preceding kernels wrote (x, the residency tables)
+  pdl_wait();
+  pdl_trigger();
+  routing::load_route_state(st, p.a);
   tc_fence_before();
   if (CN > 1)
     cluster_sync_all();
@@ -429,7 +433,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int64_t ntiles2 = ceil_div(p.ntiles, 2);  // 256-token pair tiles
   const int64_t n_iter = (ntiles2 + n_pairs - 1 - pair_id) / n_pairs;
 
-  routing::load_route_state(st, p.a);
   for (int i = threadIdx.x; i < NG * NE; i += NUM_THREADS) g_counts[i] = 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_x);
@@ -451,6 +454,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
+  pdl_wait();
+  pdl_trigger();
+  routing::load_route_state(st, p.a);
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
@@ -547,20 +553,7 @@ template <typename K>
 void launch(K kernel, int cluster, int grid, int smem, const CUtensorMap& tx, const CUtensorMap& tg, const Params& p,
             cudaStream_t s) {
   ensure_max_dynamic_smem(reinterpret_cast<const void*>(kernel), smem);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  EMOE_CUDA(cudaLaunchKernelEx(&cfg, kernel, tx, tg, p));
-  EMOE_CUDA(cudaGetLastError());
+  EMOE_CUDA(launch_pdl(kernel, dim3(grid), dim3(NUM_THREADS), (size_t)smem, s, cluster, tx, tg, p));
   count_launch();
 }
 

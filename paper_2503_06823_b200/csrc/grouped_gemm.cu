@@ -249,14 +249,6 @@ __global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
   const int cluster_id = blockIdx.x / (CG * MC);
   const int num_clusters = gridDim.x / (CG * MC);
 
-  for (int i = threadIdx.x; i <= E; i += C::NUM_THREADS)
-    s_offs[i] = (int32_t)(p.single_rows > 0 ? (i == 0 ? 0 : p.single_rows) : p.seg_offsets[i]);
-  for (int i = threadIdx.x; i < E; i += C::NUM_THREADS)
-    s_slot[i] = (int16_t)p.slot_of_expert[p.seg_expert ? p.seg_expert[i] : i];
-  for (int i = threadIdx.x; i < E; i += C::NUM_THREADS) {
-    s_ashift[i] = p.seg_a_shift ? (int32_t)p.seg_a_shift[i] : 0;
-    s_oshift[i] = p.seg_o_shift ? (int32_t)p.seg_o_shift[i] : 0;
-  }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
@@ -281,6 +273,17 @@ __global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
                    : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
+  }
+  // set-up done: the segment table and rows come from preceding kernels
+  pdl_wait();
+  pdl_trigger();
+  for (int i = threadIdx.x; i <= E; i += C::NUM_THREADS)
+    s_offs[i] = (int32_t)(p.single_rows > 0 ? (i == 0 ? 0 : p.single_rows) : p.seg_offsets[i]);
+  for (int i = threadIdx.x; i < E; i += C::NUM_THREADS)
+    s_slot[i] = (int16_t)p.slot_of_expert[p.seg_expert ? p.seg_expert[i] : i];
+  for (int i = threadIdx.x; i < E; i += C::NUM_THREADS) {
+    s_ashift[i] = p.seg_a_shift ? (int32_t)p.seg_a_shift[i] : 0;
+    s_oshift[i] = p.seg_o_shift ? (int32_t)p.seg_o_shift[i] : 0;
   }
   tc_fence_before();
   if (CLUSTER)
@@ -884,23 +887,8 @@ static void launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
   ensure_max_dynamic_smem(reinterpret_cast<const void*>(kernel), C::SMEM_BYTES);
   constexpr int CS = CG * MC;  // CTAs per cluster
   const int grid = (num_sms / CS) * CS;
-  if (CS == 1) {
-    kernel<<<grid, C::NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, tb2, to, p);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(C::NUM_THREADS);
-    cfg.dynamicSmemBytes = C::SMEM_BYTES;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CS;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    EMOE_CUDA(cudaLaunchKernelEx(&cfg, kernel, ta, tb, tb2, to, p));
-  }
+  EMOE_CUDA(launch_pdl(kernel, dim3(grid), dim3(C::NUM_THREADS), (size_t)C::SMEM_BYTES, stream, CS, ta, tb, tb2, to, p));
+
   EMOE_CUDA(cudaGetLastError());
   count_launch();
 }

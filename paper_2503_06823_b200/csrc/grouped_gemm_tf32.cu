@@ -41,18 +41,28 @@
 namespace emoe {
 namespace tf32x3 {
 
-constexpr int BM = 128, BN = 128;
+constexpr int BM = 128, BN = 128;  // per CTA: 128 rows (TMEM lanes) x 128 accumulator columns
 constexpr int BK = 32;  // fp32 elements per 128-B swizzle row
-constexpr int STAGES = 3;
 constexpr int TILE_BYTES = 128 * 128;  // 128 rows x 128 B
-constexpr int STAGE_BYTES = 4 * TILE_BYTES;
 constexpr int NUM_THREADS = 192;
 constexpr int SLOTS = 4;     // rotating TMEM accumulator slots (4 x 128 columns)
 constexpr int CHUNK_KB = 4;  // k-blocks (128 of K) per accumulator chunk
 constexpr int TMEM_COLS = SLOTS * BN;
 constexpr int MAX_SEGS = 256;
-constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 4096;
-static_assert(2 * STAGES * 8 + 2 * SLOTS * 8 + 16 + 4 * (2 * MAX_SEGS + 1) <= 4096, "barrier / table area");
+// CG = 1: one CTA per 128 x 128 tile, stage {A_hi, A_lo, B_hi, B_lo} = 64 KB, 3 stages.
+// CG = 2: a CTA pair per 256 x 128 tile (tcgen05 cta_group::2, M = 256): each
+// CTA holds its 128 A rows and half of the 128 B rows, stage = 48 KB, 4 stages
+// -- a quarter fewer bytes per MAC and a deeper ring in the same shared memory.
+template <int CG>
+struct TCfg {
+  static constexpr int B_ROWS = BN / CG;  // B rows this CTA loads per stage
+  static constexpr int B_BYTES = B_ROWS * 128;
+  static constexpr int STAGE_BYTES = 2 * TILE_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES = CG == 1 ? 3 : 4;
+  static constexpr int TILE_M = BM * CG;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 4096;
+  static_assert(2 * STAGES * 8 + 2 * SLOTS * 8 + 16 + 4 * (2 * MAX_SEGS + 1) <= 4096, "barrier / table area");
+};
 
 struct Params {
   const int64_t* seg_offsets;     // [n_seg + 1], multiples of 128
@@ -75,15 +85,24 @@ struct Params {
   int dp;           // 1: whole tiles round-robin (data-parallel), no split tiles
 };
 
-// D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, 1 CTA
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, 1 CTA or a CTA pair
+template <int CG>
 __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
+  if (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
 }
 
 // A/B = TF32 (format 2), D = f32, both K-major
@@ -97,14 +116,14 @@ __host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N) {
 using emoe::round_tf32;
 
 __device__ __forceinline__ void decode(int t, int total_mb, int n_blocks, int group_m, const int32_t* offs, int n_seg,
-                                       int& mb, int& nb, int& seg) {
+                                       int tile_m, int& mb, int& nb, int& seg) {
   const int per_group = group_m * n_blocks;
   const int g = t / per_group;
   const int local = t - g * per_group;
   const int rows_in_group = min(group_m, total_mb - g * group_m);
   nb = local / rows_in_group;
   mb = g * group_m + (local - nb * rows_in_group);
-  const int row = mb * BM;
+  const int row = mb * tile_m;
   // last segment starting at or before `row` (binary search: E = 128 made the
   // linear scan a ~2K-cycle per-tile stall of the producer warp)
   int e = 0, hi = n_seg - 1;
@@ -178,15 +197,17 @@ __device__ __forceinline__ void wait_helpers(const int32_t* cnt, int helpers, in
   __syncwarp();
 }
 
-template <int EPI>
+template <int EPI, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                        const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                        const __grid_constant__ CUtensorMap tb2_hi, const __grid_constant__ CUtensorMap tb2_lo,
                        Params p) {
+  using C = TCfg<CG>;
+  constexpr int STAGES = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;  // [SLOTS]
   uint64_t* tempty_bar = tfull_bar + SLOTS;  // [SLOTS]
@@ -196,8 +217,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int S = p.n_seg;
-  for (int i = threadIdx.x; i <= S; i += NUM_THREADS) s_offs[i] = (int32_t)p.seg_offsets[i];
-  for (int i = threadIdx.x; i < S; i += NUM_THREADS) s_slot[i] = p.slot_of_expert[p.seg_expert ? p.seg_expert[i] : i];
+  // CTA pair: rank 0 (the leader) issues the M = 256 MMAs for both CTAs; the
+  // pair walks one work list (worker = pair) and each CTA owns its 128 rows
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&ta_hi);
     tma_prefetch_desc(&ta_lo);
@@ -213,60 +236,99 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int b = 0; b < SLOTS; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 4);
+      mbar_init(&tempty_bar[b], 4 * CG);  // every epilogue warp of every CTA (the leader's copy counts)
     }
     fence_barrier_init();
   }
   if (warp == 1) {
-    tmem_alloc(tmem_slot, TMEM_COLS);
-    tmem_relinquish();
+    if (CG == 1) {
+      tmem_alloc(tmem_slot, TMEM_COLS);
+      tmem_relinquish();
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
+  pdl_wait();  // set-up done: the segment table and rows come from preceding kernels
+  pdl_trigger();
+  for (int i = threadIdx.x; i <= S; i += NUM_THREADS) s_offs[i] = (int32_t)p.seg_offsets[i];
+  for (int i = threadIdx.x; i < S; i += NUM_THREADS) s_slot[i] = p.slot_of_expert[p.seg_expert ? p.seg_expert[i] : i];
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync_all();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int total_mb = s_offs[S] / BM;
+  const int total_mb = s_offs[S] / C::TILE_M;
   const int total_tiles = total_mb * p.n_blocks;
   const int KB = p.K / BK;
   const int64_t U = (int64_t)total_tiles * KB;
-  // at most one CTA per k-block, so every working CTA's range is non-empty
-  // (an owner's helpers are then exactly the CTAs after it up to the tile's end)
-  const int P = (int)(U < (int64_t)gridDim.x ? U : (int64_t)gridDim.x);
-  const int me = blockIdx.x;
+  const int workers = (int)gridDim.x / CG;
+  // at most one worker per k-block, so every working worker's range is non-empty
+  // (an owner's helpers are then exactly the workers after it up to the tile's end)
+  const int P = (int)(U < (int64_t)workers ? U : (int64_t)workers);
+  const int me = (int)blockIdx.x / CG;
   const int64_t u_begin = me < P ? range_start(me, P, U) : U;
   const int64_t u_end = me < P ? range_start(me + 1, P, U) : U;
-  const Work work0{u_begin, u_end, KB, me, (int)gridDim.x, total_tiles, p.dp};
+  const Work work0{u_begin, u_end, KB, me, workers, total_tiles, p.dp};
 
   if (warp == 0) {
-    if (lane == 0) {  // ===== TMA producer
+    if (lane == 0) {  // ===== TMA producer (every CTA: its A rows and its half of the B rows)
       int stage = 0;
       uint32_t phase = 0;
       Work w = work0;
       Segment g;
       while (w.next(g)) {
         int mb, nb, seg;
-        decode(g.t, total_mb, p.n_blocks, p.group_m, s_offs, S, mb, nb, seg);
+        decode(g.t, total_mb, p.n_blocks, p.group_m, s_offs, S, C::TILE_M, mb, nb, seg);
         const int slot = s_slot[seg];
-        const int a_row = mb * BM;
-        const int b_row = slot * p.b_rows_per_slot + nb * (EPI == EPI_SWIGLU ? BN / 2 : BN);
+        const int a_row = mb * C::TILE_M + (int)rank * BM;
+        // SwiGLU: B rows 0-63 = W1, 64-127 = W3 of the same 64 output columns
+        // (pair: CTA 0 the W1 half, CTA 1 the W3 half); else 128 rows (pair: 64 each)
+        const int b_row = EPI == EPI_SWIGLU ? slot * p.b_rows_per_slot + nb * (BN / 2)
+                                            : slot * p.b_rows_per_slot + nb * BN + (int)rank * C::B_ROWS;
         for (int kb = g.kb0; kb < g.kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
-          uint8_t* st = smem + stage * STAGE_BYTES;
+          uint8_t* st = smem + stage * C::STAGE_BYTES;
+          uint8_t* bh = st + 2 * TILE_BYTES;
+          uint8_t* bl = bh + C::B_BYTES;
           const int kc = kb * BK;
-          tma_load_2d(&ta_hi, &full_bar[stage], st, kc, a_row, kCacheEvictNormal);
-          tma_load_2d(&ta_lo, &full_bar[stage], st + TILE_BYTES, kc, a_row, kCacheEvictNormal);
-          if (EPI == EPI_SWIGLU) {  // B tile rows 0-63: W1, 64-127: W3 (same output columns)
-            tma_load_2d(&tb_hi, &full_bar[stage], st + 2 * TILE_BYTES, kc, b_row, kCacheEvictNormal);
-            tma_load_2d(&tb2_hi, &full_bar[stage], st + 2 * TILE_BYTES + TILE_BYTES / 2, kc, b_row,
-                        kCacheEvictNormal);
-            tma_load_2d(&tb_lo, &full_bar[stage], st + 3 * TILE_BYTES, kc, b_row, kCacheEvictNormal);
-            tma_load_2d(&tb2_lo, &full_bar[stage], st + 3 * TILE_BYTES + TILE_BYTES / 2, kc, b_row,
-                        kCacheEvictNormal);
-          } else {
-            tma_load_2d(&tb_hi, &full_bar[stage], st + 2 * TILE_BYTES, kc, b_row, kCacheEvictNormal);
-            tma_load_2d(&tb_lo, &full_bar[stage], st + 3 * TILE_BYTES, kc, b_row, kCacheEvictNormal);
+          if (CG == 1) {
+            mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+            tma_load_2d(&ta_hi, &full_bar[stage], st, kc, a_row, kCacheEvictNormal);
+            tma_load_2d(&ta_lo, &full_bar[stage], st + TILE_BYTES, kc, a_row, kCacheEvictNormal);
+            if (EPI == EPI_SWIGLU) {
+              tma_load_2d(&tb_hi, &full_bar[stage], bh, kc, b_row, kCacheEvictNormal);
+              tma_load_2d(&tb2_hi, &full_bar[stage], bh + C::B_BYTES / 2, kc, b_row, kCacheEvictNormal);
+              tma_load_2d(&tb_lo, &full_bar[stage], bl, kc, b_row, kCacheEvictNormal);
+              tma_load_2d(&tb2_lo, &full_bar[stage], bl + C::B_BYTES / 2, kc, b_row, kCacheEvictNormal);
+            } else {
+              tma_load_2d(&tb_hi, &full_bar[stage], bh, kc, b_row, kCacheEvictNormal);
+              tma_load_2d(&tb_lo, &full_bar[stage], bl, kc, b_row, kCacheEvictNormal);
+            }
+          } else {  // completion bytes of both CTAs go to the leader's barrier
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
+            const CUtensorMap* bhi = EPI == EPI_SWIGLU && rank == 1 ? &tb2_hi : &tb_hi;
+            const CUtensorMap* blo = EPI == EPI_SWIGLU && rank == 1 ? &tb2_lo : &tb_lo;
+            tma_load_2d_pair(&ta_hi, &full_bar[stage], st, kc, a_row, kCacheEvictNormal);
+            tma_load_2d_pair(&ta_lo, &full_bar[stage], st + TILE_BYTES, kc, a_row, kCacheEvictNormal);
+            tma_load_2d_pair(bhi, &full_bar[stage], bh, kc, b_row, kCacheEvictNormal);
+            tma_load_2d_pair(blo, &full_bar[stage], bl, kc, b_row, kCacheEvictNormal);
           }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (CG == 2) {
+        // producer tail: every stage released, i.e. the leader's last
+        // multicast commits to this CTA's barriers have landed before exit
+        for (int i = 0; i < STAGES; ++i) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -275,17 +337,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ===== MMA issuer
+    if (lane == 0 && leader) {  // ===== MMA issuer
       // The tensor core adds each MMA into its fp32 accumulator with a
       // truncating (biased) rounding, so a tile's K range is accumulated in
       // chunks of CHUNK_KB k-blocks (on absolute k boundaries) into rotating
       // TMEM slots and the epilogue sums the chunks in registers (fp32, round
       // to nearest): the bias stays at ~CHUNK_KB * 12 roundings per chunk
       // instead of K * 3 / 8 per output.
-      constexpr uint32_t idesc = umma_idesc_tf32(BM, BN);
+      constexpr uint32_t idesc = umma_idesc_tf32(C::TILE_M, BN);
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t chunk = 0;  // chunks issued by this CTA (slot = chunk % SLOTS)
+      uint32_t chunk = 0;  // chunks issued by this worker (slot = chunk % SLOTS)
       Work w = work0;
       Segment g;
       while (w.next(g)) {
@@ -298,23 +360,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int kb = c0; kb < c1; ++kb) {
             mbar_wait(&full_bar[stage], phase);
             tc_fence_after();
-            uint8_t* st = smem + stage * STAGE_BYTES;
+            uint8_t* st = smem + stage * C::STAGE_BYTES;
             const uint64_t a_hi = umma_desc_sw128(st), a_lo = umma_desc_sw128(st + TILE_BYTES);
-            const uint64_t b_hi = umma_desc_sw128(st + 2 * TILE_BYTES), b_lo = umma_desc_sw128(st + 3 * TILE_BYTES);
+            const uint64_t b_hi = umma_desc_sw128(st + 2 * TILE_BYTES);
+            const uint64_t b_lo = umma_desc_sw128(st + 2 * TILE_BYTES + C::B_BYTES);
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 = 32 B per MMA
               const uint64_t o = (uint64_t)(kk * 2);
-              umma_tf32(tmem_d, a_lo + o, b_hi + o, idesc, (kb != c0 || kk != 0) ? 1u : 0u);
-              umma_tf32(tmem_d, a_hi + o, b_lo + o, idesc, 1u);
-              umma_tf32(tmem_d, a_hi + o, b_hi + o, idesc, 1u);
+              umma_tf32<CG>(tmem_d, a_lo + o, b_hi + o, idesc, (kb != c0 || kk != 0) ? 1u : 0u);
+              umma_tf32<CG>(tmem_d, a_hi + o, b_lo + o, idesc, 1u);
+              umma_tf32<CG>(tmem_d, a_hi + o, b_hi + o, idesc, 1u);
             }
-            umma_commit(&empty_bar[stage]);
+            if (CG == 1)
+              umma_commit(&empty_bar[stage]);
+            else
+              umma_commit_pair(&empty_bar[stage]);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
-          umma_commit(&tfull_bar[slot]);
+          if (CG == 1)
+            umma_commit(&tfull_bar[slot]);
+          else
+            umma_commit_pair(&tfull_bar[slot]);
           c0 = c1;
         }
       }
@@ -322,6 +391,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else {  // ===== epilogue: warps 2..5, TMEM lane quarter = warp % 4
     const int quarter = warp & 3;
     const int r_local = quarter * 32 + lane;
+    const int cta = (int)blockIdx.x;  // partial-tile slot of this CTA
     uint32_t chunk = 0;
     Work w = work0;
     Segment g;
@@ -344,7 +414,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int j = 0; j < 32; ++j) acc[cc + j] += __uint_as_float(a[j]);
         }
         tc_fence_before();
-        if (lane == 0) mbar_arrive(&tempty_bar[slot]);
+        if (lane == 0) {
+          if (CG == 1)
+            mbar_arrive(&tempty_bar[slot]);
+          else
+            mbar_arrive_leader_relaxed(&tempty_bar[slot]);
+        }
         c0 = c1;
       }
       // stream-K: a segment not starting at k = 0 is a helper's share of the
@@ -352,21 +427,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // count in.  The segment starting at k = 0 is the owner's (the last of
       // its range when the tile continues): it adds the helpers' partials in
       // k order -- deterministic for a given tile count -- then the epilogue.
+      // Pairs: each CTA exchanges its own 128 rows (counter per tile and rank).
       if (g.kb0 > 0) {
-        float4* mine = reinterpret_cast<float4*>(p.partial + (int64_t)me * (BM * BN));
+        float4* mine = reinterpret_cast<float4*>(p.partial + (int64_t)cta * (BM * BN));
 #pragma unroll
         for (int j = 0; j < BN; j += 4)
           __stcg(mine + (j / 4) * BM + r_local, make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
-        if (warp == 2 && lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.arrive + g.t) : "memory");
+        if (warp == 2 && lane == 0)
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.arrive + (int64_t)g.t * CG + rank)
+                       : "memory");
         continue;
       }
       if (g.kb1 < KB) {
         const int last = worker_of((int64_t)g.t * KB + KB - 1, P, U);
-        wait_helpers(p.arrive + g.t, last - me, lane);
+        int32_t* cnt = p.arrive + (int64_t)g.t * CG + rank;
+        wait_helpers(cnt, last - me, lane);
         for (int q = me + 1; q <= last; ++q) {
-          const float4* hp = reinterpret_cast<const float4*>(p.partial + (int64_t)q * (BM * BN));
+          const float4* hp = reinterpret_cast<const float4*>(p.partial + ((int64_t)q * CG + rank) * (BM * BN));
 #pragma unroll
           for (int j = 0; j < BN; j += 4) {
             const float4 v = __ldcg(hp + (j / 4) * BM + r_local);
@@ -377,11 +456,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 2 && lane == 0) p.arrive[g.t] = 0;  // the next launch (stream-ordered) starts from zero
+        if (warp == 2 && lane == 0) *cnt = 0;  // the next launch (stream-ordered) starts from zero
       }
       int mb, nb, seg;
-      decode(g.t, total_mb, p.n_blocks, p.group_m, s_offs, S, mb, nb, seg);
-      const int64_t row = (int64_t)mb * BM + r_local;
+      decode(g.t, total_mb, p.n_blocks, p.group_m, s_offs, S, C::TILE_M, mb, nb, seg);
+      const int64_t row = (int64_t)mb * C::TILE_M + (int)rank * BM + r_local;
       const int col0 = nb * p.out_block_cols;
       float* ohi = p.out_hi + row * p.ldo + col0;
       float* olo = p.out_lo ? p.out_lo + row * p.ldo + col0 : nullptr;
@@ -414,10 +493,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  if (CG == 2)
+    cluster_sync_all();  // the peer's MMAs and TMEM reads are done before the pair frees TMEM
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    if (CG == 1)
+      tmem_dealloc(tmem_base, TMEM_COLS);
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -487,7 +574,21 @@ bool gemm_tf32x3_supported(int epi, int K, int N_out) {
   return K % tf32x3::BK == 0 && N_out % (epi == EPI_SWIGLU ? tf32x3::BN / 2 : tf32x3::BN) == 0;
 }
 
-int gemm_tf32x3_b_box_rows(int epi) { return epi == EPI_SWIGLU ? tf32x3::BN / 2 : tf32x3::BN; }
+// CTA pair (M = 256 tiles) or single CTA (M = 128); EMOE_TF32_CG=1|2 (A/B runs)
+int gemm_tf32x3_cta_group() {
+  static const int cg = [] {
+    const char* v = getenv("EMOE_TF32_CG");
+    return v && v[0] == '1' ? 1 : v && v[0] == '2' ? 2 : 1;
+  }();
+  return cg;
+}
+
+int gemm_tf32x3_tile_m() { return tf32x3::BM * gemm_tf32x3_cta_group(); }
+
+int gemm_tf32x3_b_box_rows(int epi) {
+  if (gemm_tf32x3_cta_group() == 2) return tf32x3::BN / 2;  // each CTA of the pair loads half the B rows
+  return epi == EPI_SWIGLU ? tf32x3::BN / 2 : tf32x3::BN;
+}
 
 // co-resident CTAs of the persistent stream-K kernel (owners wait on
 // helpers, so every CTA of the grid must be resident at once), per device
@@ -515,11 +616,30 @@ int64_t gemm_tf32x3_arrivals(int epi, int N_out, int64_t rows) {
   return ceil_div(rows, tf32x3::BM) * (N_out / (epi == EPI_SWIGLU ? tf32x3::BN / 2 : tf32x3::BN));
 }
 
-template <int EPI>
-static void launch_1cta(const Tf32Operands& ops, const tf32x3::Params& p, int ctas, cudaStream_t stream) {
+template <int EPI, int CG>
+static void launch_tf32(const Tf32Operands& ops, const tf32x3::Params& p, int ctas, cudaStream_t stream) {
   using namespace tf32x3;
-  gemm_tf32x3_kernel<EPI><<<ctas, NUM_THREADS, SMEM_BYTES, stream>>>(ops.a_hi, ops.a_lo, ops.b_hi, ops.b_lo, ops.b2_hi,
-                                                                    ops.b2_lo, p);
+  EMOE_CUDA(launch_pdl(gemm_tf32x3_kernel<EPI, CG>, dim3(ctas), dim3(NUM_THREADS), (size_t)TCfg<CG>::SMEM_BYTES, stream,
+                       CG, ops.a_hi, ops.a_lo, ops.b_hi, ops.b_lo, ops.b2_hi, ops.b2_lo, p));
+}
+
+template <int CG>
+static void launch_cg(int epi, const Tf32Operands& ops, const tf32x3::Params& p, const StreamK& sk,
+                      cudaStream_t stream) {
+  using namespace tf32x3;
+  const void* kern = epi == EPI_SWIGLU ? reinterpret_cast<const void*>(gemm_tf32x3_kernel<EPI_SWIGLU, CG>)
+                     : epi == EPI_RELU ? reinterpret_cast<const void*>(gemm_tf32x3_kernel<EPI_RELU, CG>)
+                                       : reinterpret_cast<const void*>(gemm_tf32x3_kernel<EPI_STORE, CG>);
+  int ctas = coresident_ctas(kern, NUM_THREADS, TCfg<CG>::SMEM_BYTES);
+  ctas = (int)std::min<size_t>(ctas, sk.partial_floats / (BM * BN));
+  ctas = ctas / CG * CG;
+  EMOE_REQUIRE(ctas >= CG, "gemm_tf32x3: stream-K partial buffer too small");
+  if (epi == EPI_SWIGLU)
+    launch_tf32<EPI_SWIGLU, CG>(ops, p, ctas, stream);
+  else if (epi == EPI_RELU)
+    launch_tf32<EPI_RELU, CG>(ops, p, ctas, stream);
+  else
+    launch_tf32<EPI_STORE, CG>(ops, p, ctas, stream);
 }
 
 void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t* seg_offsets,
@@ -540,7 +660,7 @@ void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t*
   p.n_blocks = N_out / p.out_block_cols;
   p.b_rows_per_slot = b_rows_per_slot;
   // raster: A panel of ~8 MB (the fp32 hi + lo rows of the group) stays in L2
-  p.group_m = std::max(2, std::min(64, (int)((8ll << 20) / ((int64_t)BM * K * 8))));
+  p.group_m = std::max(2, std::min(64, (int)((8ll << 20) / ((int64_t)gemm_tf32x3_tile_m() * K * 8))));
   p.out_hi = out_hi;
   p.out_lo = out_lo;
   p.ldo = ldo;
@@ -558,18 +678,10 @@ void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t*
   p.dp = (sk_mask & (epi == EPI_STORE ? 2 : 1)) ? 0 : 1;
   EMOE_REQUIRE(gemm_tf32x3_arrivals(epi, N_out, max_rows) <= sk.arrivals,
                "gemm_tf32x3: stream-K arrival table smaller than the tile count");
-  const void* kern = epi == EPI_SWIGLU ? reinterpret_cast<const void*>(gemm_tf32x3_kernel<EPI_SWIGLU>)
-                     : epi == EPI_RELU ? reinterpret_cast<const void*>(gemm_tf32x3_kernel<EPI_RELU>)
-                                       : reinterpret_cast<const void*>(gemm_tf32x3_kernel<EPI_STORE>);
-  int ctas = coresident_ctas(kern, NUM_THREADS, SMEM_BYTES);
-  ctas = (int)std::min<size_t>(ctas, sk.partial_floats / (BM * BN));
-  EMOE_REQUIRE(ctas >= 1, "gemm_tf32x3: stream-K partial buffer too small");
-  if (epi == EPI_SWIGLU)
-    launch_1cta<EPI_SWIGLU>(ops, p, ctas, stream);
-  else if (epi == EPI_RELU)
-    launch_1cta<EPI_RELU>(ops, p, ctas, stream);
+  if (gemm_tf32x3_cta_group() == 2)
+    launch_cg<2>(epi, ops, p, sk, stream);
   else
-    launch_1cta<EPI_STORE>(ops, p, ctas, stream);
+    launch_cg<1>(epi, ops, p, sk, stream);
   EMOE_CUDA(cudaGetLastError());
   count_launch();
 }

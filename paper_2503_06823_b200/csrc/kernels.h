@@ -16,6 +16,38 @@ long long launch_count();
 // (device, kernel) before a launch needing more than 48 KB (thread-safe)
 void ensure_max_dynamic_smem(const void* func, int bytes);
 
+// Programmatic dependent launch for the kernels of one forward (gate -> scan
+// -> permute -> GEMM1 -> GEMM2 -> combine): each is launched with
+// programmatic stream serialisation, calls pdl_wait() (common.cuh) before its
+// first read of anything a preceding kernel wrote, and pdl_trigger() once it
+// is running, so the next kernel's launch and prologue (barrier init, TMEM
+// allocation, descriptor prefetch) overlap this one's tail.  Every kernel
+// launched this way waits unconditionally, so the ordering stays transitive
+// along the chain.  EMOE_PDL=0 launches them fully serialised (A/B runs).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              int cluster, Args&&... args) {
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[n++].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = (unsigned)cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n++].val.clusterDim.z = 1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = (unsigned)n;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
+
 enum EpiKind { EPI_SWIGLU = 0, EPI_RELU = 1, EPI_STORE = 2, EPI_F32 = 3 };
 enum DType { DT_BF16 = 0, DT_F32 = 1 };
 
@@ -54,9 +86,10 @@ void launch_route_from_logits(const float* logits, const RouteArgs& a, const Rou
 // A2 route_token over ranked gate choices [T][k] (no logits; served weights uniform)
 void launch_route_from_choices(const int32_t* choices, const RouteArgs& a, const RouteOut& o, cudaStream_t s);
 
-// K3a: per-expert totals, padded segment offsets, per-block bases
+// K3a: per-expert totals, padded segment offsets, per-block bases, -1 in the
+// padding rows of row_token (nullable); done = a zeroed device counter
 void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32_t* counts,
-                 int64_t* seg_offsets, int64_t* block_base, cudaStream_t s);
+                 int64_t* seg_offsets, int64_t* block_base, int32_t* row_token, int32_t* done, cudaStream_t s);
 // K3b: stable permutation + row gather into the padded segments
 void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
                     const int64_t* seg_offsets, const int64_t* block_base, void* x_perm, int32_t* pos,
@@ -141,6 +174,8 @@ struct Tf32Operands {
 CUtensorMap make_tmap_f32_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 bool gemm_tf32x3_supported(int epi, int K, int N_out);
 int gemm_tf32x3_b_box_rows(int epi);
+int gemm_tf32x3_cta_group();  // 1: 128 x 128 tiles on one CTA; 2: 256 x 128 tiles on a CTA pair
+int gemm_tf32x3_tile_m();     // the segment padding the kernel needs (128 or 256)
 // x -> tf32(x) in hi (hi may alias x), x - tf32(x) in lo; n % 4 == 0
 // rows_dev (optional): device row count bounding the split to rows * row_elems
 void launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t s,
@@ -159,7 +194,7 @@ struct StreamK {
 size_t gemm_tf32x3_partial_floats(int num_sms);
 int64_t gemm_tf32x3_arrivals(int epi, int N_out, int64_t rows);
 // GEMM1 (SwiGLU/ReLU): out_hi/out_lo = split(H); GEMM2 (STORE): out_hi = Y.
-// 1-CTA 128 x 128 tiles (segments padded to 128 rows)
+// 1-CTA 128 x 128 tiles or CTA-pair 256 x 128 tiles (segments padded to gemm_tf32x3_tile_m())
 void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t* seg_offsets,
                                 const int32_t* slot_of_expert, const int32_t* seg_expert, int n_seg, int K, int N_out,
                                 int b_rows_per_slot, float* out_hi, float* out_lo, int64_t ldo, int64_t max_rows,

@@ -24,6 +24,14 @@ static std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("EMOE_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 void ensure_max_dynamic_smem(const void* func, int bytes) {
   int dev = 0;
   EMOE_CUDA(cudaGetDevice(&dev));
@@ -385,8 +393,7 @@ struct emoe_layer {
   void permute(const void* x, int64_t T, cudaStream_t s) {
     const int nb = (int)ceil_div(T, kRouteBlockTokens);
     const int E = cfg.num_experts;
-    launch_scan(block_counts, nb, E, seg_pad, counts, seg_offsets, block_base, s);
-    EMOE_CUDA(cudaMemsetAsync(row_token, 0xff, sizeof(int32_t) * rows_cap, s));
+    launch_scan(block_counts, nb, E, seg_pad, counts, seg_offsets, block_base, row_token, counts + E, s);
     // 3xTF32 layers: the permute also writes the hi / lo split of every row
     // (the GEMM reads only those), so ffn() skips the separate split pass
     launch_permute(x, elem, T, cfg.d_model, E, cfg.top_k, served_idx, seg_offsets, block_base, x_perm, pos,
@@ -696,7 +703,7 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
                            atoi(getenv("EMOE_GEMM_MC")) == 2
                        ? 2
                        : 1;
-      L->seg_pad = c.dtype == EMOE_DTYPE_BF16 ? gemm_tile_m(L->cta_group, L->gemm_mc) : kSegPad;
+      L->seg_pad = c.dtype == EMOE_DTYPE_BF16 ? gemm_tile_m(L->cta_group, L->gemm_mc) : gemm_tf32x3_tile_m();
       L->rows_cap = T * k + (int64_t)E * L->seg_pad;
       L->route_blocks = (int)ceil_div(T, kRouteBlockTokens);
       EMOE_CUDA(cudaStreamCreateWithFlags(&L->copy_stream, cudaStreamNonBlocking));
@@ -719,7 +726,8 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
       L->served_idx = dmalloc<int32_t>((size_t)T * k);
       L->served_w = dmalloc<float>((size_t)T * k);
       L->block_counts = dmalloc<int32_t>((size_t)L->route_blocks * E);
-      L->counts = dmalloc<int32_t>(E);
+      L->counts = dmalloc<int32_t>(E + 1);  // [E] = the scan kernel's last-block counter
+      EMOE_CUDA(cudaMemset(L->counts, 0, (E + 1) * sizeof(int32_t)));
       L->seg_offsets = dmalloc<int64_t>(E + 1);
       L->block_base = dmalloc<int64_t>((size_t)L->route_blocks * E);
       L->pos = dmalloc<int32_t>((size_t)T * k);
@@ -1263,7 +1271,7 @@ void layer_route_scan(emoe_layer* L, const void* x, const float* logits_in, int6
   L->route(x, logits_in, T, s);
   if (T > 0)
     launch_scan(L->block_counts, (int)ceil_div(T, kRouteBlockTokens), L->cfg.num_experts, L->seg_pad, L->counts,
-                L->seg_offsets, L->block_base, s);
+                L->seg_offsets, L->block_base, nullptr, L->counts + L->cfg.num_experts, s);
 }
 
 void layer_ffn_chunks(emoe_layer* L, const void* x_chunks, int64_t x_rows, const int64_t* segs,

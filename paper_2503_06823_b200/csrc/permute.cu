@@ -21,15 +21,23 @@ namespace {
 
 constexpr int RT = kRouteBlockTokens;
 
-// K3a, pass 1: one block per expert scans its per-block counts (block order)
-// into per-block bases and the expert total.
-__global__ void __launch_bounds__(256) scan_blocks_kernel(const int32_t* __restrict__ block_counts, int nblocks,
-                                                          int E, int64_t* __restrict__ block_base,
-                                                          int32_t* __restrict__ counts) {
+// K3a: one block per expert scans its per-block counts (block order) into
+// per-block bases and the expert total; the last block to finish (a device
+// counter, reset by that block for the next launch) turns the totals into the
+// padded segment offsets and marks the padding rows of every segment as
+// sourceless (row_token = -1; rows past seg_offsets[E] are never read).  One
+// launch instead of scan + offsets kernels and a row_token memset.
+__global__ void __launch_bounds__(256) scan_kernel(const int32_t* __restrict__ block_counts, int nblocks, int E,
+                                                   int pad, int64_t* __restrict__ block_base,
+                                                   int32_t* __restrict__ counts, int64_t* __restrict__ seg_offsets,
+                                                   int32_t* __restrict__ row_token, int32_t* __restrict__ done) {
   __shared__ int64_t warp_tot[8];
   __shared__ int64_t carry;
+  __shared__ int is_last;
   const int e = blockIdx.x, lane = threadIdx.x % 32, warp = threadIdx.x / 32;
   if (threadIdx.x == 0) carry = 0;
+  pdl_wait();
+  pdl_trigger();
   __syncthreads();
   for (int b0 = 0; b0 < nblocks; b0 += 256) {
     const int b = b0 + threadIdx.x;
@@ -49,26 +57,43 @@ __global__ void __launch_bounds__(256) scan_blocks_kernel(const int32_t* __restr
     if (threadIdx.x == 255) carry = before + incl;
     __syncthreads();
   }
-  if (threadIdx.x == 0) counts[e] = (int32_t)carry;
-}
-
-// K3a, pass 2: padded segment offsets (a running sum over E experts)
-// (one block of the next power of two >= E threads, Hillis-Steele scan in shared memory)
-__global__ void __launch_bounds__(1024) seg_offsets_kernel(const int32_t* __restrict__ counts, int E, int pad,
-                                                           int64_t* __restrict__ seg_offsets) {
-  __shared__ int64_t buf[2][1024];
-  const int i = threadIdx.x;
-  const int64_t v = i < E ? ((int64_t)counts[i] + pad - 1) / pad * pad : 0;
-  int cur = 0;
-  buf[cur][i] = v;
+  if (threadIdx.x == 0) {
+    counts[e] = (int32_t)carry;
+    __threadfence();
+    is_last = atomicAdd(done, 1) == E - 1;
+  }
   __syncthreads();
-  for (int off = 1; off < (int)blockDim.x; off <<= 1) {
-    buf[cur ^ 1][i] = buf[cur][i] + (i >= off ? buf[cur][i - off] : 0);
-    cur ^= 1;
+  if (!is_last) return;
+  __threadfence();
+  // the padded segment offsets: exclusive scan over E in chunks of 256
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int e0 = 0; e0 < E; e0 += 256) {
+    const int i = e0 + threadIdx.x;
+    const int64_t n = i < E ? (int64_t)__ldcg(counts + i) : 0;
+    const int64_t v = (n + pad - 1) / pad * pad;
+    int64_t incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += u;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    int64_t before = carry;
+    for (int w = 0; w < warp; ++w) before += warp_tot[w];
+    const int64_t off_i = before + incl - v;
+    if (i < E) {
+      seg_offsets[i] = off_i;
+      if (i == E - 1) seg_offsets[E] = off_i + v;
+      if (row_token)  // this segment's padding rows
+        for (int64_t r = off_i + n; r < off_i + v; ++r) row_token[r] = -1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 255) carry = before + incl;
     __syncthreads();
   }
-  if (i < E) seg_offsets[i] = buf[cur][i] - v;  // exclusive
-  if (i == E - 1) seg_offsets[E] = buf[cur][i];
+  if (threadIdx.x == 0) *done = 0;
 }
 
 // K3b.  Block = 128 tokens (the route kernel's blocks).  Warps 0-3 rank their
@@ -98,6 +123,8 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
   uint8_t** dptr_s = reinterpret_cast<uint8_t**>(sh + 4 * E + ((RT * k + 1) & ~1));
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t t0 = (int64_t)blockIdx.x * RT;
+  pdl_wait();
+  pdl_trigger();
   int my[8];
   int rank[8];
   if (warp < 4) {
@@ -234,6 +261,8 @@ __global__ void __launch_bounds__(PB_WARPS * 32) permute_bulk_kernel(
   const int64_t t0 = (int64_t)blockIdx.x * RT;
   const int64_t t = t0 + threadIdx.x;
   const bool valid = t < T;
+  pdl_wait();
+  pdl_trigger();
   int my[8], rank[8];
   for (int j = 0; j < k; ++j) {
     my[j] = valid ? served_idx[t * k + j] : -1;
@@ -318,6 +347,8 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
                                                            int k, const int32_t* __restrict__ pos,
                                                            const float* __restrict__ served_w,
                                                            __nv_bfloat16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t t = (int64_t)blockIdx.x * 8 + warp;
   if (t >= T) return;
@@ -353,6 +384,8 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
 __global__ void __launch_bounds__(256) combine_f32_kernel(const float* __restrict__ Y, int64_t T, int d, int k,
                                                           const int32_t* __restrict__ pos,
                                                           const float* __restrict__ served_w, float* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t t = (int64_t)blockIdx.x * 8 + warp;
   if (t >= T) return;
@@ -391,15 +424,11 @@ int bulk_min_blocks() {
 }  // namespace
 
 void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32_t* counts, int64_t* seg_offsets,
-                 int64_t* block_base, cudaStream_t s) {
-  EMOE_REQUIRE(E <= 1024, "scan: too many experts");
-  scan_blocks_kernel<<<E, 256, 0, s>>>(block_counts, nblocks, E, block_base, counts);
-  EMOE_CUDA(cudaGetLastError());
-  int threads = 32;  // a power of two >= E: the scan's rounds are log2(threads)
-  while (threads < E) threads *= 2;
-  seg_offsets_kernel<<<1, threads, 0, s>>>(counts, E, pad, seg_offsets);
-  EMOE_CUDA(cudaGetLastError());
-  count_launch(2);
+                 int64_t* block_base, int32_t* row_token, int32_t* done, cudaStream_t s) {
+  EMOE_REQUIRE(E >= 1 && E <= 1024, "scan: expert count out of range");
+  EMOE_CUDA(launch_pdl(scan_kernel, dim3(E), dim3(256), 0, s, 1, block_counts, nblocks, E, pad, block_base, counts,
+                       seg_offsets, row_token, done));
+  count_launch();
 }
 
 void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
@@ -428,20 +457,17 @@ void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int 
                          (4 * (size_t)E + (size_t)RT * k) * sizeof(int32_t);
     if (bsmem <= 200 * 1024) {
       if (bsmem > 48 * 1024) ensure_max_dynamic_smem(reinterpret_cast<const void*>(permute_bulk_kernel), (int)bsmem);
-      permute_bulk_kernel<<<nblocks, PB_WARPS * 32, bsmem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
-                                                                 served_idx, seg_offsets, block_base,
-                                                                 static_cast<uint8_t*>(x_perm), pos, row_token);
-      EMOE_CUDA(cudaGetLastError());
+      EMOE_CUDA(launch_pdl(permute_bulk_kernel, dim3(nblocks), dim3(PB_WARPS * 32), bsmem, s, 1,
+                           static_cast<const uint8_t*>(x), row_bytes, T, E, k, served_idx, seg_offsets, block_base,
+                           static_cast<uint8_t*>(x_perm), pos, row_token));
       count_launch();
       return;
     }
   }
   auto kernel = x_hi ? permute_kernel<false, true> : permute_kernel<false, false>;
-  kernel<<<dim3(nblocks, ny), PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
-                                                          served_idx, seg_offsets, block_base,
-                                                          static_cast<uint8_t*>(x_perm), pos, row_token, PeerRows{},
-                                                          x_hi, x_lo);
-  EMOE_CUDA(cudaGetLastError());
+  EMOE_CUDA(launch_pdl(kernel, dim3(nblocks, ny), dim3(PERMUTE_THREADS), smem, s, 1,
+                       static_cast<const uint8_t*>(x), row_bytes, T, E, k, served_idx, seg_offsets, block_base,
+                       static_cast<uint8_t*>(x_perm), pos, row_token, PeerRows{}, x_hi, x_lo));
   count_launch();
 }
 
@@ -475,12 +501,12 @@ void launch_combine(const void* Y, int dtype, int64_t T, int d, int k, const int
   const int ny = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * sms, nblocks), nvec / 32));
   if (dtype == DT_F32) {
     EMOE_REQUIRE(d % 4 == 0, "combine: d must be a multiple of 4");
-    combine_f32_kernel<<<dim3(nblocks, ny), 256, 0, s>>>(static_cast<const float*>(Y), T, d, k, pos, served_w,
-                                                         static_cast<float*>(y));
+    EMOE_CUDA(launch_pdl(combine_f32_kernel, dim3(nblocks, ny), dim3(256), 0, s, 1, static_cast<const float*>(Y), T,
+                         d, k, pos, served_w, static_cast<float*>(y)));
   } else {
     EMOE_REQUIRE(d % 8 == 0, "combine: d must be a multiple of 8");
-    combine_bf16_kernel<<<dim3(nblocks, ny), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Y), T, d, k, pos,
-                                                          served_w, static_cast<__nv_bfloat16*>(y));
+    EMOE_CUDA(launch_pdl(combine_bf16_kernel, dim3(nblocks, ny), dim3(256), 0, s, 1,
+                         static_cast<const __nv_bfloat16*>(Y), T, d, k, pos, served_w, static_cast<__nv_bfloat16*>(y)));
   }
   EMOE_CUDA(cudaGetLastError());
   count_launch();

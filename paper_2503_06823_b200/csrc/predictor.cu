@@ -64,11 +64,22 @@ __global__ void hist_kernel(const int32_t* __restrict__ trace, int P, int m, int
     for (int i = threadIdx.x; i < E * E; i += blockDim.x)
       if (htr[i]) atomicAdd(&dst[i], (u64)htr[i]);
   }
-  if (threadIdx.x == 0) {  // dominant_expert: modal rank-0, smallest index on ties (workload.cpp:350-361)
-    int best = 0;
-    for (int e = 1; e < E; ++e)
-      if (h0[e] > h0[best]) best = e;
-    dom[(int64_t)p * m + l] = best;
+  if (threadIdx.x < 32) {  // dominant_expert: modal rank-0, smallest index on ties (workload.cpp:350-361)
+    int bc = -1, be = 0;     // this lane's best over e = lane, lane + 32, ... (ascending: first max kept)
+    for (int e = threadIdx.x; e < E; e += 32)
+      if (h0[e] > bc) {
+        bc = h0[e];
+        be = e;
+      }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {  // (count desc, index asc) is a total order: the reduction is exact
+      const int oc = __shfl_down_sync(0xffffffffu, bc, off), oe = __shfl_down_sync(0xffffffffu, be, off);
+      if (oc > bc || (oc == bc && oe < be)) {
+        bc = oc;
+        be = oe;
+      }
+    }
+    if (threadIdx.x == 0) dom[(int64_t)p * m + l] = be;
   }
 }
 
@@ -654,7 +665,7 @@ int emoe_hist_update(emoe_predictor* P, const int32_t* trace, int nP, int T, con
     const size_t smem = (size_t)(2 * E + (P->m > 1 ? E * E : 0)) * sizeof(int);
     EMOE_REQUIRE(smem <= 200 * 1024, "hist_update: E too large for the shared-memory histogram");
     ensure_max_dynamic_smem(reinterpret_cast<const void*>(hist_kernel), (int)smem);
-    hist_kernel<<<nP * P->m, 256, smem, s>>>(trace, nP, P->m, T, P->k, E, task_ids, P->layer_counts, P->task_counts,
+    hist_kernel<<<nP * P->m, 512, smem, s>>>(trace, nP, P->m, T, P->k, E, task_ids, P->layer_counts, P->task_counts,
                                              P->dom);
     EMOE_CUDA(cudaGetLastError());
     count_launch();

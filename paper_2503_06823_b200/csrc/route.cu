@@ -97,6 +97,8 @@ template <int NT>
 __global__ void __launch_bounds__(128) gate_route_bf16_kernel(const __nv_bfloat16* __restrict__ x,
                                                               const __nv_bfloat16* __restrict__ wg, RouteArgs a,
                                                               RouteOut o) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int EP = NT * 8;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* xs = smem;                      // [2][RT][64] bf16
@@ -200,6 +202,8 @@ constexpr int F32_GATE_THREADS = 512;
 __global__ void __launch_bounds__(F32_GATE_THREADS) gate_route_f32_kernel(const float* __restrict__ x,
                                                                           const float* __restrict__ wg, RouteArgs a,
                                                                           RouteOut o) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(128) uint8_t smem[];
   float* logits = reinterpret_cast<float*>(smem);  // [RT][E]
   __shared__ SharedRouteState st;
@@ -262,6 +266,8 @@ __global__ void __launch_bounds__(256) gate_logits_f32_kernel(const float* __res
                                                               const float* __restrict__ wg, int64_t T, int d, int E,
                                                               float* __restrict__ logits,
                                                               const float* __restrict__ bias) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t t = (int64_t)blockIdx.x * 8 + warp;
   if (t >= T) return;
@@ -316,6 +322,8 @@ __global__ void __launch_bounds__(256) gate_logits_f32_kernel(const float* __res
 // quad-parallel argmax / expf were both slower).
 __global__ void __launch_bounds__(RT) route_from_logits_kernel(const float* __restrict__ logits, RouteArgs a,
                                                                RouteOut o) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ SharedRouteState st;
   extern __shared__ float s_rows[];  // [RT][E + 1] when E >= 32
   const int64_t t0 = (int64_t)blockIdx.x * RT;
@@ -404,9 +412,8 @@ void launch_gate_route(const void* x, const void* wg, int dtype, const RouteArgs
     // small T: logits with one warp per token over the whole GPU, then routing
     const int nbx = (int)ceil_div(a.T, 8);
     const int ny = std::max(1, std::min((2 * 148 + nbx - 1) / nbx, (a.E + 1) / 2));  // >= 2 experts per warp
-    gate_logits_f32_kernel<<<dim3(nbx, ny), 256, 0, s>>>(static_cast<const float*>(x),
-                                                          static_cast<const float*>(wg), a.T, a.d, a.E, o.logits,
-                                                          a.bias);
+    EMOE_CUDA(launch_pdl(gate_logits_f32_kernel, dim3(nbx, ny), dim3(256), 0, s, 1, static_cast<const float*>(x),
+                         static_cast<const float*>(wg), a.T, a.d, a.E, o.logits, a.bias));
     EMOE_CUDA(cudaGetLastError());
     count_launch();
     RouteArgs ra = a;
@@ -416,8 +423,8 @@ void launch_gate_route(const void* x, const void* wg, int dtype, const RouteArgs
   } else if (dtype == DT_F32) {
     const size_t smem = (size_t)RT * a.E * sizeof(float);
     EMOE_REQUIRE(smem <= 48 * 1024, "route: fp32 logits tile exceeds 48 KB");
-    gate_route_f32_kernel<<<nblocks, F32_GATE_THREADS, smem, s>>>(static_cast<const float*>(x), static_cast<const float*>(wg), a,
-                                                     o);
+    EMOE_CUDA(launch_pdl(gate_route_f32_kernel, dim3(nblocks), dim3(F32_GATE_THREADS), smem, s, 1,
+                         static_cast<const float*>(x), static_cast<const float*>(wg), a, o));
   } else {
     EMOE_REQUIRE(a.d % KC == 0, "route: d_model must be a multiple of 64 for bf16");
     const int nt = (a.E + 7) / 8;
@@ -427,8 +434,8 @@ void launch_gate_route(const void* x, const void* wg, int dtype, const RouteArgs
       const size_t lsm = (size_t)RT * (EP + 1) * sizeof(float);
       if (lsm > smem) smem = lsm;
       ensure_max_dynamic_smem(reinterpret_cast<const void*>(kernel), (int)smem);
-      kernel<<<nblocks, 128, smem, s>>>(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg),
-                                        a, o);
+      EMOE_CUDA(launch_pdl(kernel, dim3(nblocks), dim3(128), smem, s, 1, static_cast<const __nv_bfloat16*>(x),
+                           static_cast<const __nv_bfloat16*>(wg), a, o));
     };
     if (nt <= 1)
       go(gate_route_bf16_kernel<1>, 1);
@@ -452,7 +459,7 @@ void launch_route_from_logits(const float* logits, const RouteArgs& a, const Rou
   if (nblocks == 0) return;
   const int smem = a.E >= 32 || a.bias ? RT * (a.E + 1) * (int)sizeof(float) : 0;
   if (smem > 48 * 1024) ensure_max_dynamic_smem(reinterpret_cast<const void*>(route_from_logits_kernel), smem);
-  route_from_logits_kernel<<<nblocks, RT, smem, s>>>(logits, a, o);
+  EMOE_CUDA(launch_pdl(route_from_logits_kernel, dim3(nblocks), dim3(RT), (size_t)smem, s, 1, logits, a, o));
   EMOE_CUDA(cudaGetLastError());
   count_launch();
 }

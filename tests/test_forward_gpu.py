@@ -509,3 +509,22 @@ def test_gemm_weight_multicast_bit_identical(args, tmp_path):
         outs.append(torch.load(out))
     assert torch.equal(outs[0]["y"], outs[1]["y"]), "outputs differ with the weight multicast"
     assert torch.equal(outs[0]["x_perm"], outs[1]["x_perm"])  # the same rows, in the same order
+
+
+@pytest.mark.gpu
+def test_tf32_both_cta_groups_parity():
+    """3xTF32 in both forms: the fp32 parity cases with each
+    EMOE_TF32_CG (CTA-pair 256 x 128 tiles with segments padded to 256 rows,
+    or single-CTA 128 x 128 tiles) -- every fp32 stage within the 1e-5
+    tolerance of the oracle, permutation bit-exact for that padding."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    here = Path(__file__).resolve()
+    for cg in ("1", "2"):
+        r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", "-m", "gpu",
+                            str(here), "-k", "test_forward_parity and fp32"], cwd=str(here.parent.parent),
+                           env=dict(os.environ, EMOE_TF32_CG=cg), capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0 and " passed" in r.stdout, f"EMOE_TF32_CG={cg}\n" + r.stdout[-3000:] + r.stderr[-2000:]
