@@ -117,3 +117,82 @@ def test_stage_api_equals_forward(dtype, port):
     torch.cuda.synchronize()
     assert torch.equal(y, y_ref)
     layer.close()
+
+
+def _near_tie_logits(T, E, seed):
+    """Rows built to stress top-k tie-breaking (ascending index on equal
+    logits): all equal, a tie at the top, a tie straddling the k-th place,
+    neighbours one ulp apart, quantised values with many ties, +0 / -0."""
+    rng = np.random.default_rng(seed)
+    L = np.empty((T, E), np.float32)
+    for t in range(T):
+        kind = t % 6
+        if kind == 0:
+            L[t] = np.float32(rng.normal())
+        elif kind == 1:
+            L[t] = rng.normal(size=E).astype(np.float32) - 4
+            a, b = rng.choice(E, 2, replace=False)
+            L[t, a] = L[t, b] = np.float32(2.5)
+        elif kind == 2:
+            L[t] = np.float32(-1)
+            top = rng.choice(E, 3, replace=False)
+            L[t, top[0]] = 3
+            L[t, top[1:]] = 1  # two equal candidates for the next place
+        elif kind == 3:
+            base = np.float32(rng.normal())
+            L[t] = base
+            for j, e in enumerate(rng.permutation(E)[:4]):  # 1-ulp ladder above the rest
+                v = base
+                for _ in range(j + 1):
+                    v = np.nextafter(v, np.float32(np.inf), dtype=np.float32)
+                L[t, e] = v
+        elif kind == 4:
+            L[t] = (np.round(rng.normal(size=E) * 2) / 2).astype(np.float32)
+        else:
+            L[t] = np.where(rng.random(E) < 0.5, np.float32(0.0), np.float32(-0.0))
+    return L
+
+
+@pytest.mark.parametrize("E,k,wm", [(8, 2, 0), (8, 1, 1), (32, 2, 0)])
+def test_near_tie_logits_given(E, k, wm, port):
+    """Routing-driven logits with exact ties and one-ulp gaps: top-k and the
+    served set bit-exact against the oracle, weights to the expf tolerance."""
+    T = 600
+    res = list(range(0, E, 2))
+    layer, _, experts = build_layer(E, 256, 256, k, act="swiglu" if k > 1 else "relu",
+                                    weight_mode="topk_softmax" if wm == 0 else "full_softmax", slots=len(res),
+                                    resident=res, max_tokens=T)
+    L = _near_tie_logits(T, E, 17 + E + k)
+    x = torch.randn(T, 256, generator=torch.Generator().manual_seed(6)).to(torch.bfloat16)
+    layer.forward(x.cuda(), logits=torch.from_numpy(L).cuda())
+    torch.cuda.synchronize()
+    ws = layer.workspace()
+    o = port.gate_route(L, k, wm, layer.residency(), None)
+    assert np.array_equal(ws["topk_idx"].cpu().numpy(), o["topk_idx"])
+    assert np.array_equal(ws["served_idx"].cpu().numpy(), o["served_idx"])
+    # weights: device expf vs the C library's (a few ulp), as in test_forward_gpu
+    np.testing.assert_allclose(ws["served_w"].cpu().numpy(), o["served_w"], rtol=2e-6, atol=1e-7)
+    layer.close()
+
+
+def test_near_tie_logits_fused_tc_gate(port):
+    """The fused tcgen05 gate + route (E = 128, top-1, full-softmax weights):
+    x = 0 makes the gate's logits exactly 0, so in logits-bias mode the
+    routed logits are exactly the near-tie bias rows -- routing bit-exact
+    against the oracle on them, weights to the expf tolerance."""
+    E, T = 128, 1536
+    res = list(range(0, 128, 5))
+    layer, _, _ = build_layer(E, 256, 512, 1, act="relu", weight_mode="full_softmax", slots=len(res), resident=res,
+                              max_tokens=T)
+    layer.set_logits_mode("add")
+    L = _near_tie_logits(T, E, 99)
+    x = torch.zeros(T, 256, dtype=torch.bfloat16)
+    layer.forward(x.cuda(), logits=torch.from_numpy(L).cuda())
+    torch.cuda.synchronize()
+    ws = layer.workspace()
+    o = port.gate_route(L + np.float32(0.0), 1, 1, layer.residency(), None)
+    assert np.array_equal(ws["topk_idx"].cpu().numpy(), o["topk_idx"])
+    assert np.array_equal(ws["served_idx"].cpu().numpy(), o["served_idx"])
+    # weights: device expf vs the C library's (a few ulp), as in test_forward_gpu
+    np.testing.assert_allclose(ws["served_w"].cpu().numpy(), o["served_w"], rtol=2e-6, atol=1e-7)
+    layer.close()
