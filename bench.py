@@ -593,8 +593,26 @@ def main():
         t = torch.tensor([e2e_s], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+    # the copy floor of the e2e path: the same H2D and D2H bytes per step with
+    # no compute (one stream each way, concurrent, back to back)
+    xd_f = torch.empty(x_host.shape, dtype=x_host.dtype, device=device)
+    yd_f = torch.empty_like(xd_f)
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    n_floor = 20
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n_floor):
+        with torch.cuda.stream(s_in):
+            xd_f.copy_(x_host, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            y_host.copy_(yd_f, non_blocking=True)
+    torch.cuda.synchronize()
+    floor_s = (time.perf_counter() - t0) / n_floor
+    del xd_f, yd_f
     e2e = dict(value=world * T / e2e_s, unit="tokens/s", h2d_bytes_per_step=x_host.numel() * x_host.element_size(),
                d2h_bytes_per_step=y_host.numel() * y_host.element_size(), ms_per_step=e2e_s * 1e3,
+               copy_floor_ms=floor_s * 1e3, frac_of_copy_floor=floor_s / e2e_s,
+               copy_floor_gbs=(x_host.numel() + y_host.numel()) * x_host.element_size() / floor_s / 1e9,
                calls=args.e2e_steps,
                note="emoe_moe_forward_host_async per call (H2D x, K1-K5, D2H y), wall clock over the calls; "
                     "the device-timed step also runs the A6 histogram update and per-stage events, which "

@@ -299,7 +299,8 @@ __global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
 
   if (warp == 0) {
     // ===================== TMA producer (every CTA) =====================
-    if (lane == 0) {
+    // warp-uniform walk (as the MMA issuer), one elected lane issues the copies
+    {
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
@@ -316,32 +317,37 @@ __global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
         }
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          if (own_mma) mbar_arrive_expect_tx(&full_bar[stage], CG * C::STAGE_BYTES);
           const int kc = kb * BK;
           uint8_t* adst = smem_a + stage * C::A_BYTES;
           uint8_t* bdst = smem_b + stage * C::B_BYTES;
-          if (MC > 1) {
-            // own A rows; this CTA's half of the weight tile to both CTAs
-            // (SwiGLU: CTA0 the W1 rows, CTA1 the W3 rows; else 128 rows each)
-            tma_load_2d(&tmap_a, &full_bar[stage], adst, kc, a_row, p.hint_a);
-            if (EPI == EPI_SWIGLU)
-              tma_load_2d_mcast(rank == 0 ? &tmap_b : &tmap_b2, &full_bar[stage], bdst + rank * (C::B_BYTES / 2), kc,
-                                b_row, MC_MASK, p.hint_b);
-            else
-              tma_load_2d_mcast(&tmap_b, &full_bar[stage], bdst + rank * (C::B_BYTES / MC), kc,
-                                b_row + (int)rank * (BN / MC), MC_MASK, p.hint_b);
-          } else if (CG == 1) {
-            tma_load_2d(&tmap_a, &full_bar[stage], adst, kc, a_row, p.hint_a);
-            if (EPI == EPI_SWIGLU) {
-              tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, p.hint_b);
-              tma_load_2d(&tmap_b2, &full_bar[stage], bdst + C::B_BYTES / 2, kc, b_row, p.hint_b);
+          if (elect_one()) {
+            if (MC > 1) {
+              if (own_mma) mbar_arrive_expect_tx(&full_bar[stage], CG * C::STAGE_BYTES);
+              // own A rows; this CTA's half of the weight tile to both CTAs
+              // (SwiGLU: CTA0 the W1 rows, CTA1 the W3 rows; else 128 rows each)
+              tma_load_2d(&tmap_a, &full_bar[stage], adst, kc, a_row, p.hint_a);
+              if (EPI == EPI_SWIGLU)
+                tma_load_2d_mcast(rank == 0 ? &tmap_b : &tmap_b2, &full_bar[stage], bdst + rank * (C::B_BYTES / 2), kc,
+                                  b_row, MC_MASK, p.hint_b);
+              else
+                tma_load_2d_mcast(&tmap_b, &full_bar[stage], bdst + rank * (C::B_BYTES / MC), kc,
+                                  b_row + (int)rank * (BN / MC), MC_MASK, p.hint_b);
+            } else if (CG == 1) {
+              mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+              tma_load_2d(&tmap_a, &full_bar[stage], adst, kc, a_row, p.hint_a);
+              if (EPI == EPI_SWIGLU) {
+                tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, p.hint_b);
+                tma_load_2d(&tmap_b2, &full_bar[stage], bdst + C::B_BYTES / 2, kc, b_row, p.hint_b);
+              } else {
+                tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, p.hint_b);
+              }
             } else {
-              tma_load_2d(&tmap_b, &full_bar[stage], bdst, kc, b_row, p.hint_b);
+              if (own_mma) mbar_arrive_expect_tx(&full_bar[stage], CG * C::STAGE_BYTES);
+              tma_load_2d_pair(&tmap_a, &full_bar[stage], adst, kc, a_row, p.hint_a);
+              tma_load_2d_pair(tb, &full_bar[stage], bdst, kc, b_row, p.hint_b);
             }
-          } else {
-            tma_load_2d_pair(&tmap_a, &full_bar[stage], adst, kc, a_row, p.hint_a);
-            tma_load_2d_pair(tb, &full_bar[stage], bdst, kc, b_row, p.hint_b);
           }
+          __syncwarp();
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -362,7 +368,11 @@ __global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA) =====================
-    if (lane == 0 && own_mma) {
+    // The whole warp walks the tile schedule (barrier waits and descriptors
+    // stay warp-uniform, in uniform registers) and one elected lane issues
+    // the MMAs and commits; from a single-lane branch every tcgen05.mma
+    // needed a waterfall loop to move its operands to uniform registers.
+    if (own_mma) {
       constexpr uint32_t idesc = umma_idesc_bf16(128 * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -378,30 +388,36 @@ __global__ void __launch_bounds__(Cfg<CG, EW, MC>::NUM_THREADS, 1)
           tc_fence_after();
           const uint64_t a_desc = umma_desc_sw128(smem_a + stage * C::A_BYTES);
           const uint64_t b_desc = umma_desc_sw128(smem_b + stage * C::B_BYTES);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            // advance 16 bf16 = 32 B inside the 128-B swizzle row
-            const uint32_t acc = (kb | kk) != 0 ? 1u : 0u;
-            if (CG == 1)
-              umma_bf16(tmem_d, a_desc + (uint64_t)(kk * 2), b_desc + (uint64_t)(kk * 2), idesc, acc);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              // advance 16 bf16 = 32 B inside the 128-B swizzle row
+              const uint32_t acc = (kb | kk) != 0 ? 1u : 0u;
+              if (CG == 1)
+                umma_bf16(tmem_d, a_desc + (uint64_t)(kk * 2), b_desc + (uint64_t)(kk * 2), idesc, acc);
+              else
+                umma_bf16_pair(tmem_d, a_desc + (uint64_t)(kk * 2), b_desc + (uint64_t)(kk * 2), idesc, acc);
+            }
+            if (MC > 1)
+              umma_commit_mcast(&empty_bar[stage], MC_MASK);
+            else if (CG == 1)
+              umma_commit(&empty_bar[stage]);
             else
-              umma_bf16_pair(tmem_d, a_desc + (uint64_t)(kk * 2), b_desc + (uint64_t)(kk * 2), idesc, acc);
+              umma_commit_pair(&empty_bar[stage]);
           }
-          if (MC > 1)
-            umma_commit_mcast(&empty_bar[stage], MC_MASK);
-          else if (CG == 1)
-            umma_commit(&empty_bar[stage]);
-          else
-            umma_commit_pair(&empty_bar[stage]);
+          __syncwarp();
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (CG == 1)
-          umma_commit(&tfull_bar[buf]);
-        else
-          umma_commit_pair(&tfull_bar[buf]);
+        if (elect_one()) {
+          if (CG == 1)
+            umma_commit(&tfull_bar[buf]);
+          else
+            umma_commit_pair(&tfull_bar[buf]);
+        }
+        __syncwarp();
       }
     }
   } else {

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const Work work0{u_begin, u_end, KB, me, workers, total_tiles, p.dp};
 
   if (warp == 0) {
-    if (lane == 0) {  // ===== TMA producer (every CTA: its A rows and its half of the B rows)
+    {  // ===== TMA producer (every CTA: its A rows and its half of the B rows; warp-uniform, one lane issues)
       int stage = 0;
       uint32_t phase = 0;
       Work w = work0;
@@ -296,28 +296,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t* bh = st + 2 * TILE_BYTES;
           uint8_t* bl = bh + C::B_BYTES;
           const int kc = kb * BK;
-          if (CG == 1) {
-            mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
-            tma_load_2d(&ta_hi, &full_bar[stage], st, kc, a_row, kCacheEvictNormal);
-            tma_load_2d(&ta_lo, &full_bar[stage], st + TILE_BYTES, kc, a_row, kCacheEvictNormal);
-            if (EPI == EPI_SWIGLU) {
-              tma_load_2d(&tb_hi, &full_bar[stage], bh, kc, b_row, kCacheEvictNormal);
-              tma_load_2d(&tb2_hi, &full_bar[stage], bh + C::B_BYTES / 2, kc, b_row, kCacheEvictNormal);
-              tma_load_2d(&tb_lo, &full_bar[stage], bl, kc, b_row, kCacheEvictNormal);
-              tma_load_2d(&tb2_lo, &full_bar[stage], bl + C::B_BYTES / 2, kc, b_row, kCacheEvictNormal);
-            } else {
-              tma_load_2d(&tb_hi, &full_bar[stage], bh, kc, b_row, kCacheEvictNormal);
-              tma_load_2d(&tb_lo, &full_bar[stage], bl, kc, b_row, kCacheEvictNormal);
+          if (elect_one()) {
+            if (CG == 1) {
+              mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+              tma_load_2d(&ta_hi, &full_bar[stage], st, kc, a_row, kCacheEvictNormal);
+              tma_load_2d(&ta_lo, &full_bar[stage], st + TILE_BYTES, kc, a_row, kCacheEvictNormal);
+              if (EPI == EPI_SWIGLU) {
+                tma_load_2d(&tb_hi, &full_bar[stage], bh, kc, b_row, kCacheEvictNormal);
+                tma_load_2d(&tb2_hi, &full_bar[stage], bh + C::B_BYTES / 2, kc, b_row, kCacheEvictNormal);
+                tma_load_2d(&tb_lo, &full_bar[stage], bl, kc, b_row, kCacheEvictNormal);
+                tma_load_2d(&tb2_lo, &full_bar[stage], bl + C::B_BYTES / 2, kc, b_row, kCacheEvictNormal);
+              } else {
+                tma_load_2d(&tb_hi, &full_bar[stage], bh, kc, b_row, kCacheEvictNormal);
+                tma_load_2d(&tb_lo, &full_bar[stage], bl, kc, b_row, kCacheEvictNormal);
+              }
+            } else {  // completion bytes of both CTAs go to the leader's barrier
+              if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
+              const CUtensorMap* bhi = EPI == EPI_SWIGLU && rank == 1 ? &tb2_hi : &tb_hi;
+              const CUtensorMap* blo = EPI == EPI_SWIGLU && rank == 1 ? &tb2_lo : &tb_lo;
+              tma_load_2d_pair(&ta_hi, &full_bar[stage], st, kc, a_row, kCacheEvictNormal);
+              tma_load_2d_pair(&ta_lo, &full_bar[stage], st + TILE_BYTES, kc, a_row, kCacheEvictNormal);
+              tma_load_2d_pair(bhi, &full_bar[stage], bh, kc, b_row, kCacheEvictNormal);
+              tma_load_2d_pair(blo, &full_bar[stage], bl, kc, b_row, kCacheEvictNormal);
             }
-          } else {  // completion bytes of both CTAs go to the leader's barrier
-            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
-            const CUtensorMap* bhi = EPI == EPI_SWIGLU && rank == 1 ? &tb2_hi : &tb_hi;
-            const CUtensorMap* blo = EPI == EPI_SWIGLU && rank == 1 ? &tb2_lo : &tb_lo;
-            tma_load_2d_pair(&ta_hi, &full_bar[stage], st, kc, a_row, kCacheEvictNormal);
-            tma_load_2d_pair(&ta_lo, &full_bar[stage], st + TILE_BYTES, kc, a_row, kCacheEvictNormal);
-            tma_load_2d_pair(bhi, &full_bar[stage], bh, kc, b_row, kCacheEvictNormal);
-            tma_load_2d_pair(blo, &full_bar[stage], bl, kc, b_row, kCacheEvictNormal);
           }
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -337,7 +340,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {  // ===== MMA issuer
+    if (leader) {  // ===== MMA issuer
+      // The whole warp walks the schedule (barrier waits, descriptors: warp-
+      // uniform values the compiler keeps in uniform registers) and one
+      // elected lane issues the MMAs and their commits.  Issued from a
+      // single-lane branch instead, every tcgen05.mma needed a waterfall loop
+      // moving its operands to uniform registers (~200 instructions per
+      // k-block for its 12 MMAs: the issue rate, not the tensor core, bounded
+      // the k-loop -- profiles/r02_tf32_variants_ab.txt).
       // The tensor core adds each MMA into its fp32 accumulator with a
       // truncating (biased) rounding, so a tile's K range is accumulated in
       // chunks of CHUNK_KB k-blocks (on absolute k boundaries) into rotating
@@ -364,26 +374,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t a_hi = umma_desc_sw128(st), a_lo = umma_desc_sw128(st + TILE_BYTES);
             const uint64_t b_hi = umma_desc_sw128(st + 2 * TILE_BYTES);
             const uint64_t b_lo = umma_desc_sw128(st + 2 * TILE_BYTES + C::B_BYTES);
+            if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 = 32 B per MMA
-              const uint64_t o = (uint64_t)(kk * 2);
-              umma_tf32<CG>(tmem_d, a_lo + o, b_hi + o, idesc, (kb != c0 || kk != 0) ? 1u : 0u);
-              umma_tf32<CG>(tmem_d, a_hi + o, b_lo + o, idesc, 1u);
-              umma_tf32<CG>(tmem_d, a_hi + o, b_hi + o, idesc, 1u);
+              for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 = 32 B per MMA
+                const uint64_t o = (uint64_t)(kk * 2);
+                umma_tf32<CG>(tmem_d, a_lo + o, b_hi + o, idesc, (kb != c0 || kk != 0) ? 1u : 0u);
+                umma_tf32<CG>(tmem_d, a_hi + o, b_lo + o, idesc, 1u);
+                umma_tf32<CG>(tmem_d, a_hi + o, b_hi + o, idesc, 1u);
+              }
+              if (CG == 1)
+                umma_commit(&empty_bar[stage]);
+              else
+                umma_commit_pair(&empty_bar[stage]);
             }
-            if (CG == 1)
-              umma_commit(&empty_bar[stage]);
-            else
-              umma_commit_pair(&empty_bar[stage]);
+            __syncwarp();
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
-          if (CG == 1)
-            umma_commit(&tfull_bar[slot]);
-          else
-            umma_commit_pair(&tfull_bar[slot]);
+          if (elect_one()) {
+            if (CG == 1)
+              umma_commit(&tfull_bar[slot]);
+            else
+              umma_commit_pair(&tfull_bar[slot]);
+          }
+          __syncwarp();
           c0 = c1;
         }
       }
