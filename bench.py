@@ -381,7 +381,7 @@ def build_parser():
     ap.add_argument("--gemm-cta-group", type=int, default=0, choices=[0, 1, 2],
                     help="FFN GEMM CTA group (0 = the layer's auto choice)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
-                    help="replay each step as one captured CUDA graph (stage times then from eager steps "
+                    help="replay each step as one captured CUDA graph (stage times then from a profiling capture of the step "
                          "after the timed region) or launch it eagerly; auto = graph for the sub-millisecond "
                          "steps of configs 1 and 3 (launch-bound: +27 %% / +6 %%, profiles/r01_cuda_graph_ab.jsonl), "
                          "eager for config 2 (stage events inside the timed region)")
@@ -485,7 +485,7 @@ def main():
     # replayed as a whole: no per-launch host or queue gaps, which matter for
     # the small configs; EP steps stay eager).  The per-stage events are not
     # captured (their timestamps inside replays were not trustworthy), so the
-    # stage times then come from eager steps right after the timed region.
+    # stage times then come from a second capture with the events as graph record nodes.
     graph = None
     launches_per_step = 0
     use_graph = args.graph == "on" or (args.graph == "auto" and args.config in ("synthetic", "switch"))
@@ -532,12 +532,25 @@ def main():
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     if ep_model is None:
-        if graph is not None:  # stage times from eager steps after the timed replays
+        if graph is not None:
+            # stage times from the same step captured once more with the stage
+            # events as record nodes of the graph, replayed and read one replay
+            # at a time (eager steps carry host launch gaps between stages, which
+            # inflated them by up to 25 % on some hosts)
             layer.set_profiling(True)
-            for _ in range(args.steps):
+            gprof = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gprof, capture_error_mode="thread_local"):
                 eager_step()
-            torch.cuda.synchronize()
-        stages = layer.stage_times()
+            layer.set_profiling(False)
+            stages = {}
+            for _ in range(args.steps):
+                gprof.replay()
+                torch.cuda.synchronize()
+                for key, v in layer.stage_times_last().items():
+                    stages[key] = stages.get(key, 0.0) + v / args.steps
+            del gprof
+        else:
+            stages = layer.stage_times()
     elif args.ep_transport == "p2p":  # the EP forward's own stage events
         ep_stages = ep_model.stage_times()
         ep_model.set_profiling(False)
@@ -584,11 +597,12 @@ def main():
     e2e_wait()
     if world > 1:
         dist.barrier()
-    t0 = time.perf_counter()
-    for i in range(args.e2e_steps):
-        e2e_step(i)
-    e2e_wait()
-    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    with ClockSampler(local) as e2e_clk:  # the e2e calls run for seconds: their own clock record
+        t0 = time.perf_counter()
+        for i in range(args.e2e_steps):
+            e2e_step(i)
+        e2e_wait()
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     if world > 1:
         t = torch.tensor([e2e_s], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -611,7 +625,7 @@ def main():
     del xd_f, yd_f
     e2e = dict(value=world * T / e2e_s, unit="tokens/s", h2d_bytes_per_step=x_host.numel() * x_host.element_size(),
                d2h_bytes_per_step=y_host.numel() * y_host.element_size(), ms_per_step=e2e_s * 1e3,
-               copy_floor_ms=floor_s * 1e3, frac_of_copy_floor=floor_s / e2e_s,
+               copy_floor_ms=floor_s * 1e3, frac_of_copy_floor=floor_s / e2e_s, clocks=e2e_clk.summary(),
                copy_floor_gbs=(x_host.numel() + y_host.numel()) * x_host.element_size() / floor_s / 1e9,
                calls=args.e2e_steps,
                note="emoe_moe_forward_host_async per call (H2D x, K1-K5, D2H y), wall clock over the calls; "
@@ -684,8 +698,9 @@ def main():
                data="synthetic (random-init weights; routing = reference Markov trace embedded in x)",
                config=dict(workload=cfg["workload"] + (f" split over {world} GPUs" if strong else ""),
                            tokens_per_step=T, tokens_per_gpu=T, num_experts=cfg["E"], top_k=cfg["k"],
-                           step_launch=("one CUDA graph per step (replayed); stages_ms and the roofline from as many "
-                                        "eager steps right after the timed region") if graph is not None else "eager",
+                           step_launch=("one CUDA graph per step (replayed); stages_ms and the roofline from the "
+                                        "same step captured with its stage events as graph record nodes, replayed "
+                                        "and read one replay at a time") if graph is not None else "eager",
                            resident_experts=cfg["L"], resident_set=[e for e in range(cfg["E"])
                                                                      if info["resident"][e]],
                            d_model=d, d_ff=f, activation=cfg["act"], served_rows=S, hit_rate=round(hit_rate, 4),

@@ -337,6 +337,11 @@ int emoe_layer_share_workspace(emoe_layer* layer, const emoe_layer* donor);
  * the previous emoe_layer_stage_times call. */
 int emoe_layer_set_profiling(emoe_layer* layer, int enable);
 int emoe_layer_stage_times(emoe_layer* layer, float* ms);
+/* The stage times of the first profiled forward's event set without
+ * recycling it: for a forward captured once (profiling on) into a CUDA graph,
+ * read after each replay -- the events are record nodes of the graph, so every
+ * replay re-stamps them with no host launch gaps between the stages. */
+int emoe_layer_stage_times_last(emoe_layer* layer, float* ms);
 /* kernels launched by this library since load (gpu_launches evidence) */
 long long emoe_kernel_launches(void);
 

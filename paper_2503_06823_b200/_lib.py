@@ -97,6 +97,7 @@ _decl("emoe_epx_destroy", vp)
 IPC_HANDLE_BYTES = 64
 _decl("emoe_layer_set_profiling", vp, C.c_int)
 _decl("emoe_layer_stage_times", vp, vp)
+_decl("emoe_layer_stage_times_last", vp, vp)
 lib.emoe_kernel_launches.restype = C.c_longlong
 lib.emoe_kernel_launches.argtypes = []
 _decl("emoe_predictor_create", C.c_int, C.c_int, C.c_int, C.c_int, dbl, C.POINTER(vp))
@@ -133,7 +134,7 @@ EXPORTED = [
     "emoe_ep_forward", "emoe_ep_status", "emoe_ep_stats", "emoe_ep_layout", "emoe_ep_set_profiling",
     "emoe_ep_stage_times", "emoe_ep_destroy", "emoe_epx_create", "emoe_epx_cap_rows", "emoe_epx_route",
     "emoe_epx_dispatch", "emoe_epx_ffn", "emoe_epx_combine", "emoe_epx_status", "emoe_epx_destroy", "emoe_layer_workspace", "emoe_layer_share_workspace", "emoe_layer_set_profiling",
-    "emoe_layer_stage_times", "emoe_kernel_launches", "emoe_predictor_create",
+    "emoe_layer_stage_times", "emoe_layer_stage_times_last", "emoe_kernel_launches", "emoe_predictor_create",
     "emoe_predictor_destroy", "emoe_predictor_reset", "emoe_predictor_break_chain", "emoe_hist_update", "emoe_hist_update_host", "emoe_predictor_counts_host",
     "emoe_predictor_set_counts_host", "emoe_predictor_count_size", "emoe_predictor_counts_dev",
     "emoe_predictor_set_counts_dev", "emoe_prompt_expert_sets", "emoe_prompt_expert_sets_host", "emoe_predict_host",

@@ -1168,6 +1168,16 @@ int emoe_layer_stage_times(emoe_layer* L, float* ms) {
   });
 }
 
+int emoe_layer_stage_times_last(emoe_layer* L, float* ms) {
+  return guard([&] {
+    EMOE_REQUIRE(L && ms, "stage_times: null argument");
+    EMOE_REQUIRE(!L->ev_pool.empty(), "stage_times: no profiled forward");
+    auto& set = L->ev_pool[0];
+    EMOE_CUDA(cudaEventSynchronize(set[5]));
+    for (int i = 0; i < 5; ++i) EMOE_CUDA(cudaEventElapsedTime(&ms[i], set[i], set[i + 1]));
+  });
+}
+
 long long emoe_kernel_launches(void) { return launch_count(); }
 
 int emoe_route_tokens_host(const int32_t* choices, int64_t T, int k, const uint8_t* resident, int E,

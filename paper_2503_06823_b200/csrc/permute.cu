@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const int32_t* __restrict__ b
   __shared__ int64_t warp_tot[8];
   __shared__ int64_t carry;
   __shared__ int is_last;
+  __shared__ int32_t pad_beg[1024], pad_len[1024];
   const int e = blockIdx.x, lane = threadIdx.x % 32, warp = threadIdx.x / 32;
   if (threadIdx.x == 0) carry = 0;
   pdl_wait();
@@ -86,13 +87,16 @@ __global__ void __launch_bounds__(256) scan_kernel(const int32_t* __restrict__ b
     if (i < E) {
       seg_offsets[i] = off_i;
       if (i == E - 1) seg_offsets[E] = off_i + v;
-      if (row_token)  // this segment's padding rows
-        for (int64_t r = off_i + n; r < off_i + v; ++r) row_token[r] = -1;
+      pad_beg[i] = (int32_t)(off_i + n);  // this segment's padding rows [off + n, off + pad(n))
+      pad_len[i] = (int32_t)(v - n);
     }
     __syncthreads();
     if (threadIdx.x == 255) carry = before + incl;
     __syncthreads();
   }
+  if (row_token)
+    for (int e = 0; e < E; ++e)
+      for (int r = threadIdx.x; r < pad_len[e]; r += blockDim.x) row_token[pad_beg[e] + r] = -1;
   if (threadIdx.x == 0) *done = 0;
 }
 

@@ -32,9 +32,15 @@ using u64 = unsigned long long;
 // ---------------------------------------------------------------------------
 // A6 histograms
 // ---------------------------------------------------------------------------
+// The last block to finish (a device counter in last[m], reset by that
+// block) also tallies the prompt n -> n+1 transitions of the dominant
+// experts (predictor.cpp:176-183), continuing the chain from the previous
+// call through last[] when has_last, and saves the last prompt's dominant
+// experts for the next call: one launch per update.
 __global__ void hist_kernel(const int32_t* __restrict__ trace, int P, int m, int T, int k, int E,
                             const int32_t* __restrict__ task_ids, u64* __restrict__ layer_counts,
-                            u64* __restrict__ task_counts, int32_t* __restrict__ dom) {
+                            u64* __restrict__ task_counts, int32_t* __restrict__ dom, int32_t* __restrict__ last,
+                            int has_last, u64* __restrict__ prompt_counts) {
   extern __shared__ int sh[];
   int* h0 = sh;          // [E] rank-0 counts
   int* hall = sh + E;    // [E] all-rank counts
@@ -81,23 +87,25 @@ __global__ void hist_kernel(const int32_t* __restrict__ trace, int P, int m, int
     }
     if (threadIdx.x == 0) dom[(int64_t)p * m + l] = be;
   }
-}
-
-__global__ void prompt_trans_kernel(const int32_t* __restrict__ dom, int P, int m, int E, int32_t* __restrict__ last,
-                                    int has_last, u64* __restrict__ prompt_counts) {
-  // prompt n -> n+1 transitions of the dominant experts (predictor.cpp:176-183)
-  const int total = (P - 1 + (has_last ? 1 : 0)) * m;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int l = i % m;
-    int pi = i / m - (has_last ? 1 : 0);  // -1 = chain from the previous call
-    const int a = pi < 0 ? last[l] : dom[(int64_t)pi * m + l];
-    const int b = dom[(int64_t)(pi + 1) * m + l];
-    atomicAdd(&prompt_counts[((int64_t)l * E + a) * E + b], 1ull);
+  __shared__ int is_last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    is_last = atomicAdd(&last[m], 1) == (int)gridDim.x - 1;
   }
-}
-
-__global__ void save_last_kernel(const int32_t* __restrict__ dom, int P, int m, int32_t* __restrict__ last) {
-  for (int l = threadIdx.x; l < m; l += blockDim.x) last[l] = dom[(int64_t)(P - 1) * m + l];
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  const int total = (P - 1 + (has_last ? 1 : 0)) * m;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int ll = i % m;
+    const int pi = i / m - (has_last ? 1 : 0);  // -1 = chain from the previous call
+    const int a = pi < 0 ? last[ll] : __ldcg(dom + (int64_t)pi * m + ll);
+    const int b = __ldcg(dom + (int64_t)(pi + 1) * m + ll);
+    atomicAdd(&prompt_counts[((int64_t)ll * E + a) * E + b], 1ull);
+  }
+  __syncthreads();  // every read of last[] above precedes the overwrite
+  for (int ll = threadIdx.x; ll < m; ll += blockDim.x) last[ll] = __ldcg(dom + (int64_t)(P - 1) * m + ll);
+  if (threadIdx.x == 0) last[m] = 0;
 }
 
 // prompt_expert_sets (workload.cpp:363-377): one block per layer
@@ -612,7 +620,8 @@ int emoe_predictor_create(int m, int E, int k, int n_tasks, double smoothing, em
     EMOE_CUDA(cudaMalloc(&P->layer_counts, std::max<size_t>(1, P->n_layer()) * sizeof(u64)));
     EMOE_CUDA(cudaMalloc(&P->prompt_counts, P->n_prompt() * sizeof(u64)));
     EMOE_CUDA(cudaMalloc(&P->task_counts, std::max<size_t>(1, P->n_task()) * sizeof(u64)));
-    EMOE_CUDA(cudaMalloc(&P->last_dom, m * sizeof(int32_t)));
+    EMOE_CUDA(cudaMalloc(&P->last_dom, (m + 1) * sizeof(int32_t)));  // [m] = hist_kernel's last-block counter
+    EMOE_CUDA(cudaMemset(P->last_dom, 0, (m + 1) * sizeof(int32_t)));
     EMOE_CUDA(cudaStreamCreateWithFlags(&P->inv_stream, cudaStreamNonBlocking));
     EMOE_CUDA(cudaEventCreateWithFlags(&P->hist_done, cudaEventDisableTiming));
     P->zero();
@@ -666,17 +675,7 @@ int emoe_hist_update(emoe_predictor* P, const int32_t* trace, int nP, int T, con
     EMOE_REQUIRE(smem <= 200 * 1024, "hist_update: E too large for the shared-memory histogram");
     ensure_max_dynamic_smem(reinterpret_cast<const void*>(hist_kernel), (int)smem);
     hist_kernel<<<nP * P->m, 512, smem, s>>>(trace, nP, P->m, T, P->k, E, task_ids, P->layer_counts, P->task_counts,
-                                             P->dom);
-    EMOE_CUDA(cudaGetLastError());
-    count_launch();
-    const int pairs = (nP - 1 + (P->has_last ? 1 : 0)) * P->m;
-    if (pairs > 0) {
-      prompt_trans_kernel<<<(pairs + 255) / 256, 256, 0, s>>>(P->dom, nP, P->m, E, P->last_dom, P->has_last ? 1 : 0,
-                                                              P->prompt_counts);
-      EMOE_CUDA(cudaGetLastError());
-    count_launch();
-    }
-    save_last_kernel<<<1, 128, 0, s>>>(P->dom, nP, P->m, P->last_dom);
+                                             P->dom, P->last_dom, P->has_last ? 1 : 0, P->prompt_counts);
     EMOE_CUDA(cudaGetLastError());
     count_launch();
     EMOE_CUDA(cudaEventRecord(P->hist_done, s));  // the next invocation reads the counts after this

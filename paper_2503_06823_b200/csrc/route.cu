@@ -278,7 +278,31 @@ __global__ void __launch_bounds__(256) gate_logits_f32_kernel(const float* __res
     const int ne = min(8, e_end - e0);
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (vec) {
-      for (int i = lane * 4; i < d; i += 128) {
+      // four 128-element slices per round, every load issued before the FMAs
+      // (a latency-bound loop at small T: ~1 round trip per 512 elements)
+      int i = lane * 4;
+      for (; i + 3 * 128 < d; i += 4 * 128) {
+        float4 xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = __ldg(reinterpret_cast<const float4*>(xr + i + u * 128));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j < ne) {
+            float4 wv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              wv[u] = __ldg(reinterpret_cast<const float4*>(wg + (int64_t)(e0 + j) * d + i + u * 128));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              acc[j] = fmaf(xv[u].x, wv[u].x, acc[j]);
+              acc[j] = fmaf(xv[u].y, wv[u].y, acc[j]);
+              acc[j] = fmaf(xv[u].z, wv[u].z, acc[j]);
+              acc[j] = fmaf(xv[u].w, wv[u].w, acc[j]);
+            }
+          }
+        }
+      }
+      for (; i < d; i += 128) {
         const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + i));
 #pragma unroll
         for (int j = 0; j < 8; ++j) {

@@ -252,6 +252,13 @@ class MoELayer:
         check(lib.emoe_layer_stage_times(self.h, ms))
         return dict(zip(["route", "permute", "gemm1", "gemm2", "combine"], [float(v) for v in ms]))
 
+    def stage_times_last(self) -> Dict[str, float]:
+        """ms of the stages of the first profiled forward's events, not recycled:
+        for a forward captured into a CUDA graph, read after each replay."""
+        ms = (C.c_float * 5)()
+        check(lib.emoe_layer_stage_times_last(self.h, ms))
+        return dict(zip(["route", "permute", "gemm1", "gemm2", "combine"], [float(v) for v in ms]))
+
     def share_workspace(self, donor: "MoELayer") -> None:
         """Run on `donor`'s workspace (released here); see emoe_layer_share_workspace."""
         check(lib.emoe_layer_share_workspace(self.h, donor.h))
