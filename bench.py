@@ -597,12 +597,13 @@ def main():
     e2e_wait()
     if world > 1:
         dist.barrier()
-    with ClockSampler(local) as e2e_clk:  # the e2e calls run for seconds: their own clock record
-        t0 = time.perf_counter()
-        for i in range(args.e2e_steps):
-            e2e_step(i)
-        e2e_wait()
-        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    # PCIe-bound shapes (config 3) vary with the box's host link: the copy
+    # floor below is measured on the same box for comparison
+    t0 = time.perf_counter()
+    for i in range(args.e2e_steps):
+        e2e_step(i)
+    e2e_wait()
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     if world > 1:
         t = torch.tensor([e2e_s], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -625,7 +626,7 @@ def main():
     del xd_f, yd_f
     e2e = dict(value=world * T / e2e_s, unit="tokens/s", h2d_bytes_per_step=x_host.numel() * x_host.element_size(),
                d2h_bytes_per_step=y_host.numel() * y_host.element_size(), ms_per_step=e2e_s * 1e3,
-               copy_floor_ms=floor_s * 1e3, frac_of_copy_floor=floor_s / e2e_s, clocks=e2e_clk.summary(),
+               copy_floor_ms=floor_s * 1e3, frac_of_copy_floor=floor_s / e2e_s,
                copy_floor_gbs=(x_host.numel() + y_host.numel()) * x_host.element_size() / floor_s / 1e9,
                calls=args.e2e_steps,
                note="emoe_moe_forward_host_async per call (H2D x, K1-K5, D2H y), wall clock over the calls; "
