@@ -23,7 +23,8 @@ void ensure_max_dynamic_smem(const void* func, int bytes);
 // is running, so the next kernel's launch and prologue (barrier init, TMEM
 // allocation, descriptor prefetch) overlap this one's tail.  Every kernel
 // launched this way waits unconditionally, so the ordering stays transitive
-// along the chain.  EMOE_PDL=0 launches them fully serialised (A/B runs).
+// along the chain.  Off by default (EMOE_PDL=1 enables it): measured neutral
+// in graph replays and slower in the host-buffer pipeline.
 bool pdl_enabled();
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -75,6 +76,8 @@ struct RouteArgs {
   const double* scores;     // [E] device or null (empty score vector)
   int* error_flag;          // device int, set to 3 when a token needs a fallback and no expert is resident
   const float* bias = nullptr;  // [T][E] added to the gate's logits before routing (null: none)
+  int32_t* sync = nullptr;      // [ceil(T/128)] zeroed counters: the small-T fp32 gate routes in its
+                                // last block per 128-token block (null: logits kernel + routing kernel)
 };
 
 // K1 from activations: logits = x . wg^T (bf16 x via mma.sync, fp32 x via FFMA) + routing

@@ -24,10 +24,13 @@ static std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+// off by default: neutral inside the replayed graphs of configs 1 and 3, and
+// it slowed the host-buffer (e2e) path of config 2 from 24.5 to 26.8 ms per
+// call on the same box (profiles/r02_pdl_fused_scan_ab_L2.txt); EMOE_PDL=1 enables it
 bool pdl_enabled() {
   static const bool on = [] {
     const char* v = getenv("EMOE_PDL");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
   return on;
 }
@@ -138,6 +141,7 @@ struct emoe_layer {
   int64_t* block_base = nullptr;
   int32_t* pos = nullptr;
   int32_t* row_token = nullptr;
+  int32_t* route_sync = nullptr;  // [route blocks] zeroed counters (RouteArgs::sync); per layer, never shared
   void* x_perm = nullptr;
   void* h = nullptr;
   void* y_perm = nullptr;
@@ -290,6 +294,7 @@ struct emoe_layer {
     const bool add = logits_in && logits_mode == EMOE_LOGITS_ADD;
     EMOE_REQUIRE(!add || x, "route: the logits-bias mode runs the gate, so x is required");
     a.bias = add ? logits_in : nullptr;
+    a.sync = route_sync;
     if (logits_in && !add) {
       launch_route_from_logits(logits_in, a, o, s);
     } else if (tc_gate() && !split_gate()) {
@@ -642,7 +647,7 @@ struct emoe_layer {
                     (void*)route_resident_dev, wg_pad, (void*)demand_dev, x_in, y_out, (void*)err_flag, x_stage[0],
                     x_stage[1], y_stage[0], y_stage[1], w1_lo, w3_lo, w2_lo, (void*)sx_hi, (void*)sx_lo,
                     (void*)sh_lo, (void*)combine_arrive, (void*)sk_partial,
-                    (void*)sk_arrive})
+                    (void*)sk_arrive, (void*)route_sync})
       f(p);
     for (auto* v : {&host_w1, &host_w3, &host_w2})
       for (size_t e = 0; e < v->size(); ++e)
@@ -726,6 +731,8 @@ int emoe_layer_create(const emoe_layer_config* cfg, emoe_layer** out) {
       L->served_idx = dmalloc<int32_t>((size_t)T * k);
       L->served_w = dmalloc<float>((size_t)T * k);
       L->block_counts = dmalloc<int32_t>((size_t)L->route_blocks * E);
+      L->route_sync = dmalloc<int32_t>((size_t)L->route_blocks);  // the small-T fp32 gate's counters
+      EMOE_CUDA(cudaMemset(L->route_sync, 0, sizeof(int32_t) * L->route_blocks));
       L->counts = dmalloc<int32_t>(E + 1);  // [E] = the scan kernel's last-block counter
       EMOE_CUDA(cudaMemset(L->counts, 0, (E + 1) * sizeof(int32_t)));
       L->seg_offsets = dmalloc<int64_t>(E + 1);

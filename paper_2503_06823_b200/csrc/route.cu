@@ -262,15 +262,9 @@ __global__ void __launch_bounds__(F32_GATE_THREADS) gate_route_f32_kernel(const 
 // route_from_logits_kernel.  Same dot-product order as the fused kernel.
 // blockIdx.y selects a slice of the experts (each expert's sum is computed
 // in the same order whatever the slicing), so small T still spans the GPU.
-__global__ void __launch_bounds__(256) gate_logits_f32_kernel(const float* __restrict__ x,
-                                                              const float* __restrict__ wg, int64_t T, int d, int E,
-                                                              float* __restrict__ logits,
-                                                              const float* __restrict__ bias) {
-  pdl_wait();
-  pdl_trigger();
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t t = (int64_t)blockIdx.x * 8 + warp;
-  if (t >= T) return;
+// one token's logits over the experts of this block's column slice (a warp)
+__device__ void gate_logits_f32_token(const float* __restrict__ x, const float* __restrict__ wg, int64_t t, int d,
+                                      int E, float* __restrict__ logits, const float* __restrict__ bias, int lane) {
   const float* xr = x + t * d;
   const bool vec = (d & 3) == 0;
   const int e_beg = E * blockIdx.y / gridDim.y, e_end = E * (blockIdx.y + 1) / gridDim.y;
@@ -332,6 +326,49 @@ __global__ void __launch_bounds__(256) gate_logits_f32_kernel(const float* __res
     }
   }
 }
+
+// With a.sync set, the blocks covering one 128-token route block count in
+// on a.sync[route block] and the last of them routes its tokens (the logits
+// of the other blocks read through L2), so the small-T gate is one launch.
+__global__ void __launch_bounds__(256) gate_logits_f32_kernel(const float* __restrict__ x,
+                                                              const float* __restrict__ wg, int64_t T, int d, int E,
+                                                              float* __restrict__ logits,
+                                                              const float* __restrict__ bias, RouteArgs a,
+                                                              RouteOut o) {
+  pdl_wait();
+  pdl_trigger();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t t = (int64_t)blockIdx.x * 8 + warp;
+  if (t < T) gate_logits_f32_token(x, wg, t, d, E, logits, bias, lane);
+  if (!a.sync) return;
+  __shared__ SharedRouteState st;
+  __shared__ int is_last;
+  extern __shared__ float s_rows[];  // [RT][E + 1]: the route block's logits
+  constexpr int XB = RT / 8;         // x blocks per route block
+  const int rb = blockIdx.x / XB;
+  const int members = min(XB, (int)gridDim.x - rb * XB) * (int)gridDim.y;
+  __syncthreads();  // this block's logits are stored
+  if (threadIdx.x == 0) {
+    __threadfence();
+    is_last = atomicAdd(a.sync + rb, 1) == members - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  const int64_t t0 = (int64_t)rb * RT;
+  const int rows = (int)min((int64_t)RT, T - t0);
+  for (int i = threadIdx.x; i < rows * E; i += blockDim.x) {
+    const int r = i / E;
+    s_rows[r * (E + 1) + (i - r * E)] = __ldcg(logits + t0 * E + i);
+  }
+  load_route_state(st, a);  // its barriers also publish s_rows
+  if (threadIdx.x < rows) route_one_token(s_rows + threadIdx.x * (E + 1), t0 + threadIdx.x, a, o, st);
+  __syncthreads();
+  if (o.block_counts)
+    for (int e = threadIdx.x; e < E; e += blockDim.x) o.block_counts[(int64_t)rb * E + e] = st.counts[e];
+  if (threadIdx.x == 0) a.sync[rb] = 0;  // for the next launch (stream-ordered)
+}
+
 
 // ---------------------------------------------------------------------------
 // routing-driven mode: logits supplied by the caller
@@ -436,13 +473,14 @@ void launch_gate_route(const void* x, const void* wg, int dtype, const RouteArgs
     // small T: logits with one warp per token over the whole GPU, then routing
     const int nbx = (int)ceil_div(a.T, 8);
     const int ny = std::max(1, std::min((2 * 148 + nbx - 1) / nbx, (a.E + 1) / 2));  // >= 2 experts per warp
-    EMOE_CUDA(launch_pdl(gate_logits_f32_kernel, dim3(nbx, ny), dim3(256), 0, s, 1, static_cast<const float*>(x),
-                         static_cast<const float*>(wg), a.T, a.d, a.E, o.logits, a.bias));
-    EMOE_CUDA(cudaGetLastError());
-    count_launch();
     RouteArgs ra = a;
-    ra.bias = nullptr;  // already in the logits
-    launch_route_from_logits(o.logits, ra, o, s);
+    ra.bias = nullptr;  // added to the logits by the gate
+    const size_t smem = a.sync ? (size_t)RT * (a.E + 1) * sizeof(float) : 0;
+    if (smem > 48 * 1024) ensure_max_dynamic_smem(reinterpret_cast<const void*>(gate_logits_f32_kernel), (int)smem);
+    EMOE_CUDA(launch_pdl(gate_logits_f32_kernel, dim3(nbx, ny), dim3(256), smem, s, 1, static_cast<const float*>(x),
+                         static_cast<const float*>(wg), a.T, a.d, a.E, o.logits, a.bias, ra, o));
+    count_launch();
+    if (!a.sync) launch_route_from_logits(o.logits, ra, o, s);  // routing in its own kernel
     return;
   } else if (dtype == DT_F32) {
     const size_t smem = (size_t)RT * a.E * sizeof(float);
