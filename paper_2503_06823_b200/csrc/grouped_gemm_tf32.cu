@@ -83,6 +83,7 @@ struct Params {
   float* partial;   // [CTAs][32 float4 columns][128 rows] float4: one raw partial tile per CTA
   int32_t* arrive;  // [tiles] helper arrivals, zero between launches (the owner re-zeroes)
   int dp;           // 1: whole tiles round-robin (data-parallel), no split tiles
+  int chunk_kb;     // k-blocks per TMEM accumulator chunk (CHUNK_KB; EMOE_TF32_CHUNK for A/B runs)
 };
 
 // D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, 1 CTA or a CTA pair
@@ -362,7 +363,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       Segment g;
       while (w.next(g)) {
         for (int c0 = g.kb0; c0 < g.kb1; ++chunk) {
-          const int c1 = min(g.kb1, (c0 / CHUNK_KB + 1) * CHUNK_KB);
+          const int c1 = min(g.kb1, (c0 / p.chunk_kb + 1) * p.chunk_kb);
           const int slot = chunk % SLOTS;
           mbar_wait(&tempty_bar[slot], ((chunk / SLOTS) & 1) ^ 1);
           tc_fence_after();
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
       for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
       for (int c0 = g.kb0; c0 < g.kb1; ++chunk) {
-        const int c1 = min(g.kb1, (c0 / CHUNK_KB + 1) * CHUNK_KB);
+        const int c1 = min(g.kb1, (c0 / p.chunk_kb + 1) * p.chunk_kb);
         const int slot = chunk % SLOTS;
         mbar_wait(&tfull_bar[slot], (chunk / SLOTS) & 1);
         tc_fence_after();
@@ -692,6 +693,11 @@ void launch_grouped_gemm_tf32x3(int epi, const Tf32Operands& ops, const int64_t*
     return v ? atoi(v) : 2;
   }();
   p.dp = (sk_mask & (epi == EPI_STORE ? 2 : 1)) ? 0 : 1;
+  static const int chunk_kb = [] {
+    const char* v = getenv("EMOE_TF32_CHUNK");
+    return v ? std::max(1, atoi(v)) : CHUNK_KB;
+  }();
+  p.chunk_kb = chunk_kb;
   EMOE_REQUIRE(gemm_tf32x3_arrivals(epi, N_out, max_rows) <= sk.arrivals,
                "gemm_tf32x3: stream-K arrival table smaller than the tile count");
   if (gemm_tf32x3_cta_group() == 2)
