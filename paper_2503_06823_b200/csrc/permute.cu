@@ -27,11 +27,12 @@ constexpr int RT = kRouteBlockTokens;
 // padded segment offsets and marks the padding rows of every segment as
 // sourceless (row_token = -1; rows past seg_offsets[E] are never read).  One
 // launch instead of scan + offsets kernels and a row_token memset.
-__global__ void __launch_bounds__(256) scan_kernel(const int32_t* __restrict__ block_counts, int nblocks, int E,
+constexpr int SCAN_T = 512;
+__global__ void __launch_bounds__(SCAN_T) scan_kernel(const int32_t* __restrict__ block_counts, int nblocks, int E,
                                                    int pad, int64_t* __restrict__ block_base,
                                                    int32_t* __restrict__ counts, int64_t* __restrict__ seg_offsets,
                                                    int32_t* __restrict__ row_token, int32_t* __restrict__ done) {
-  __shared__ int64_t warp_tot[8];
+  __shared__ int64_t warp_tot[SCAN_T / 32];
   __shared__ int64_t carry;
   __shared__ int is_last;
   __shared__ int32_t pad_beg[1024], pad_len[1024];
@@ -40,7 +41,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const int32_t* __restrict__ b
   pdl_wait();
   pdl_trigger();
   __syncthreads();
-  for (int b0 = 0; b0 < nblocks; b0 += 256) {
+  for (int b0 = 0; b0 < nblocks; b0 += SCAN_T) {  // one round for up to 65,536 tokens
     const int b = b0 + threadIdx.x;
     const int64_t v = b < nblocks ? block_counts[(int64_t)b * E + e] : 0;
     int64_t incl = v;  // inclusive warp scan
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const int32_t* __restrict__ b
     for (int w = 0; w < warp; ++w) before += warp_tot[w];
     if (b < nblocks) block_base[(int64_t)b * E + e] = before + incl - v;
     __syncthreads();
-    if (threadIdx.x == 255) carry = before + incl;
+    if (threadIdx.x == SCAN_T - 1) carry = before + incl;
     __syncthreads();
   }
   if (threadIdx.x == 0) {
@@ -66,10 +67,10 @@ __global__ void __launch_bounds__(256) scan_kernel(const int32_t* __restrict__ b
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  // the padded segment offsets: exclusive scan over E in chunks of 256
+  // the padded segment offsets: exclusive scan over E in chunks of SCAN_T
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int e0 = 0; e0 < E; e0 += 256) {
+  for (int e0 = 0; e0 < E; e0 += SCAN_T) {
     const int i = e0 + threadIdx.x;
     const int64_t n = i < E ? (int64_t)__ldcg(counts + i) : 0;
     const int64_t v = (n + pad - 1) / pad * pad;
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const int32_t* __restrict__ b
       pad_len[i] = (int32_t)(v - n);
     }
     __syncthreads();
-    if (threadIdx.x == 255) carry = before + incl;
+    if (threadIdx.x == SCAN_T - 1) carry = before + incl;
     __syncthreads();
   }
   if (row_token)
@@ -430,7 +431,7 @@ int bulk_min_blocks() {
 void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32_t* counts, int64_t* seg_offsets,
                  int64_t* block_base, int32_t* row_token, int32_t* done, cudaStream_t s) {
   EMOE_REQUIRE(E >= 1 && E <= 1024, "scan: expert count out of range");
-  EMOE_CUDA(launch_pdl(scan_kernel, dim3(E), dim3(256), 0, s, 1, block_counts, nblocks, E, pad, block_base, counts,
+  EMOE_CUDA(launch_pdl(scan_kernel, dim3(E), dim3(SCAN_T), 0, s, 1, block_counts, nblocks, E, pad, block_base, counts,
                        seg_offsets, row_token, done));
   count_launch();
 }
