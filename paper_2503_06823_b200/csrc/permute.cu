@@ -27,7 +27,7 @@ constexpr int RT = kRouteBlockTokens;
 // padded segment offsets and marks the padding rows of every segment as
 // sourceless (row_token = -1; rows past seg_offsets[E] are never read).  One
 // launch instead of scan + offsets kernels and a row_token memset.
-constexpr int SCAN_T = 512;
+constexpr int SCAN_T = 256;
 __global__ void __launch_bounds__(SCAN_T) scan_kernel(const int32_t* __restrict__ block_counts, int nblocks, int E,
                                                    int pad, int64_t* __restrict__ block_base,
                                                    int32_t* __restrict__ counts, int64_t* __restrict__ seg_offsets,
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(SCAN_T) scan_kernel(const int32_t* __restrict_
   pdl_wait();
   pdl_trigger();
   __syncthreads();
-  for (int b0 = 0; b0 < nblocks; b0 += SCAN_T) {  // one round for up to 65,536 tokens
+  for (int b0 = 0; b0 < nblocks; b0 += SCAN_T) {
     const int b = b0 + threadIdx.x;
     const int64_t v = b < nblocks ? block_counts[(int64_t)b * E + e] : 0;
     int64_t incl = v;  // inclusive warp scan
