@@ -93,6 +93,12 @@ void launch_route_from_choices(const int32_t* choices, const RouteArgs& a, const
 // padding rows of row_token (nullable); done = a zeroed device counter
 void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32_t* counts,
                  int64_t* seg_offsets, int64_t* block_base, int32_t* row_token, int32_t* done, cudaStream_t s);
+// K3a + K3b as one call: for small batches (<= 32 token blocks, E <= 128) the
+// scan is folded into the permute kernel (one launch), else scan + permute
+void launch_scan_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
+                         const int32_t* block_counts, int pad, int32_t* counts, int64_t* seg_offsets,
+                         int64_t* block_base, void* x_perm, int32_t* pos, int32_t* row_token, int32_t* done,
+                         cudaStream_t s, float* x_hi = nullptr, float* x_lo = nullptr);
 // K3b: stable permutation + row gather into the padded segments
 void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
                     const int64_t* seg_offsets, const int64_t* block_base, void* x_perm, int32_t* pos,

@@ -396,13 +396,12 @@ struct emoe_layer {
 
   // A3 after route(): per-expert offsets, positions, gathered rows in x_perm
   void permute(const void* x, int64_t T, cudaStream_t s) {
-    const int nb = (int)ceil_div(T, kRouteBlockTokens);
     const int E = cfg.num_experts;
-    launch_scan(block_counts, nb, E, seg_pad, counts, seg_offsets, block_base, row_token, counts + E, s);
     // 3xTF32 layers: the permute also writes the hi / lo split of every row
     // (the GEMM reads only those), so ffn() skips the separate split pass
-    launch_permute(x, elem, T, cfg.d_model, E, cfg.top_k, served_idx, seg_offsets, block_base, x_perm, pos,
-                   row_token, s, tf32 ? x_hi : nullptr, tf32 ? x_lo : nullptr);
+    launch_scan_permute(x, elem, T, cfg.d_model, E, cfg.top_k, served_idx, block_counts, seg_pad, counts,
+                        seg_offsets, block_base, x_perm, pos, row_token, counts + E, s, tf32 ? x_hi : nullptr,
+                        tf32 ? x_lo : nullptr);
     perm_split_done = tf32;
   }
   bool perm_split_done = false;  // x_hi / x_lo hold the split of x_perm's rows

@@ -118,13 +118,29 @@ constexpr int GATHER_UNROLL = 8;
 // SPLIT (fp32 rows of a 3xTF32 layer): also write each row's tf32 hi / lo
 // parts to x_hi / x_lo (a separate instantiation, so the other layers' permute
 // carries none of it)
+// Small batches (few token blocks): K3a folded into K3b.  Every block derives
+// the segment offsets and its own per-expert bases from the block counts
+// (nblocks x E values, read through L2), and block (0, 0) stores the counts,
+// the padded offsets (read by the GEMMs) and the padding rows of row_token --
+// one launch instead of two where the scan's latency is most of its cost.
+struct SmallScan {
+  const int32_t* block_counts = nullptr;  // null: offsets / bases come from scan_kernel
+  int nblocks = 0;
+  int pad = 0;
+  int32_t* counts = nullptr;
+  int64_t* seg_offsets = nullptr;
+};
+constexpr int SMALL_SCAN_BLOCKS = 32;  // token blocks (4,096 tokens) up to which the scan is folded in
+constexpr int SMALL_SCAN_E = 128;
+
 template <bool REMOTE, bool SPLIT = false>
 __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
     const uint8_t* __restrict__ x, int row_bytes, int64_t T, int E, int k, const int32_t* __restrict__ served_idx,
     const int64_t* __restrict__ seg_offsets, const int64_t* __restrict__ block_base, uint8_t* __restrict__ x_perm,
     int32_t* __restrict__ pos, int32_t* __restrict__ row_token, PeerRows peers, float* __restrict__ x_hi,
-    float* __restrict__ x_lo) {
+    float* __restrict__ x_lo, SmallScan ss) {
   extern __shared__ int32_t sh[];
+  __shared__ int64_t s_off[SMALL_SCAN_E + 1], s_base[SMALL_SCAN_E];
   int32_t* warp_counts = sh;          // [4][E]
   int32_t* dst_s = sh + 4 * E;        // [RT][k]
   // REMOTE: destination row pointer per (token, slot), 8-B aligned after dst_s
@@ -133,6 +149,39 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
   const int64_t t0 = (int64_t)blockIdx.x * RT;
   pdl_wait();
   pdl_trigger();
+  const bool small_scan = !REMOTE && ss.block_counts != nullptr;
+  if (small_scan) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      int64_t tot = 0, base = 0;
+      for (int b = 0; b < ss.nblocks; ++b) {
+        if (b == (int)blockIdx.x) base = tot;
+        tot += __ldcg(ss.block_counts + (int64_t)b * E + e);
+      }
+      s_base[e] = base;
+      s_off[e] = tot;  // the total, until the scan below
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // padded exclusive scan over the experts (E <= 128)
+      int64_t run = 0;
+      for (int e = 0; e < E; ++e) {
+        const int64_t n = s_off[e];
+        s_off[e] = run;
+        run += (n + ss.pad - 1) / ss.pad * ss.pad;
+      }
+      s_off[E] = run;
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && blockIdx.y == 0) {
+      for (int e = threadIdx.x; e <= E; e += blockDim.x) ss.seg_offsets[e] = s_off[e];
+      for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        int64_t tot = 0;
+        for (int b = 0; b < ss.nblocks; ++b) tot += __ldcg(ss.block_counts + (int64_t)b * E + e);
+        ss.counts[e] = (int32_t)tot;
+        if (row_token)  // this segment's padding rows
+          for (int64_t r = s_off[e] + tot; r < s_off[e + 1]; ++r) row_token[r] = -1;
+      }
+    }
+  }
   int my[8];
   int rank[8];
   if (warp < 4) {
@@ -171,7 +220,7 @@ __global__ void __launch_bounds__(PERMUTE_THREADS) permute_kernel(
       const int e = my[j];
       int32_t d = -1;
       if (e >= 0) {
-        int64_t base = seg_offsets[e] + block_base[(int64_t)blockIdx.x * E + e];
+        int64_t base = small_scan ? s_off[e] + s_base[e] : seg_offsets[e] + block_base[(int64_t)blockIdx.x * E + e];
         for (int w = 0; w < warp; ++w) base += warp_counts[w * E + e];
         d = (int32_t)(base + rank[j]);
       }
@@ -439,9 +488,47 @@ void launch_scan(const int32_t* block_counts, int nblocks, int E, int pad, int32
   count_launch();
 }
 
+static void launch_permute_ss(const void* x, int elem_bytes, int64_t T, int d, int E, int k,
+                              const int32_t* served_idx, const int64_t* seg_offsets, const int64_t* block_base,
+                              void* x_perm, int32_t* pos, int32_t* row_token, cudaStream_t s, float* x_hi,
+                              float* x_lo, const SmallScan& ss);
+
 void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
                     const int64_t* seg_offsets, const int64_t* block_base, void* x_perm, int32_t* pos,
                     int32_t* row_token, cudaStream_t s, float* x_hi, float* x_lo) {
+  launch_permute_ss(x, elem_bytes, T, d, E, k, served_idx, seg_offsets, block_base, x_perm, pos, row_token, s, x_hi,
+                    x_lo, SmallScan{});
+}
+
+void launch_scan_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int k, const int32_t* served_idx,
+                         const int32_t* block_counts, int pad, int32_t* counts, int64_t* seg_offsets,
+                         int64_t* block_base, void* x_perm, int32_t* pos, int32_t* row_token, int32_t* done,
+                         cudaStream_t s, float* x_hi, float* x_lo) {
+  static const bool fold = [] {  // EMOE_SMALL_SCAN=0 keeps the separate scan launch (A/B runs)
+    const char* v = getenv("EMOE_SMALL_SCAN");
+    return !(v && v[0] == '0');
+  }();
+  const int nblocks = (int)ceil_div(T, RT);
+  if (fold && nblocks >= 1 && nblocks <= SMALL_SCAN_BLOCKS && E <= SMALL_SCAN_E) {
+    SmallScan ss;
+    ss.block_counts = block_counts;
+    ss.nblocks = nblocks;
+    ss.pad = pad;
+    ss.counts = counts;
+    ss.seg_offsets = seg_offsets;
+    launch_permute_ss(x, elem_bytes, T, d, E, k, served_idx, seg_offsets, block_base, x_perm, pos, row_token, s, x_hi,
+                      x_lo, ss);
+    return;
+  }
+  launch_scan(block_counts, nblocks, E, pad, counts, seg_offsets, block_base, row_token, done, s);
+  launch_permute(x, elem_bytes, T, d, E, k, served_idx, seg_offsets, block_base, x_perm, pos, row_token, s, x_hi,
+                 x_lo);
+}
+
+static void launch_permute_ss(const void* x, int elem_bytes, int64_t T, int d, int E, int k,
+                              const int32_t* served_idx, const int64_t* seg_offsets, const int64_t* block_base,
+                              void* x_perm, int32_t* pos, int32_t* row_token, cudaStream_t s, float* x_hi,
+                              float* x_lo, const SmallScan& ss) {
   EMOE_REQUIRE(!x_hi || (elem_bytes == 4 && x_lo), "permute: the tf32 split needs fp32 rows and both outputs");
   const int row_bytes = d * elem_bytes;
   EMOE_REQUIRE(row_bytes % 16 == 0, "permute: row bytes must be a multiple of 16");
@@ -475,7 +562,7 @@ void launch_permute(const void* x, int elem_bytes, int64_t T, int d, int E, int 
   auto kernel = x_hi ? permute_kernel<false, true> : permute_kernel<false, false>;
   EMOE_CUDA(launch_pdl(kernel, dim3(nblocks, ny), dim3(PERMUTE_THREADS), smem, s, 1,
                        static_cast<const uint8_t*>(x), row_bytes, T, E, k, served_idx, seg_offsets, block_base,
-                       static_cast<uint8_t*>(x_perm), pos, row_token, PeerRows{}, x_hi, x_lo));
+                       static_cast<uint8_t*>(x_perm), pos, row_token, PeerRows{}, x_hi, x_lo, ss));
   count_launch();
 }
 
@@ -489,7 +576,7 @@ void launch_permute_remote(const void* x, int elem_bytes, int64_t T, int d, int 
   const size_t smem = (4 * (size_t)E + (size_t)((RT * k + 1) & ~1)) * sizeof(int32_t) + (size_t)RT * k * 8;
   permute_kernel<true><<<nblocks, PERMUTE_THREADS, smem, s>>>(static_cast<const uint8_t*>(x), row_bytes, T, E, k,
                                                               served_idx, seg_offsets, block_base, nullptr, pos,
-                                                              nullptr, peers, nullptr, nullptr);
+                                                              nullptr, peers, nullptr, nullptr, SmallScan{});
   EMOE_CUDA(cudaGetLastError());
   count_launch();
 }
