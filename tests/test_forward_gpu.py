@@ -528,3 +528,46 @@ def test_tf32_both_cta_groups_parity():
                             str(here), "-k", "test_forward_parity and fp32"], cwd=str(here.parent.parent),
                            env=dict(os.environ, EMOE_TF32_CG=cg), capture_output=True, text=True, timeout=900)
         assert r.returncode == 0 and " passed" in r.stdout, f"EMOE_TF32_CG={cg}\n" + r.stdout[-3000:] + r.stderr[-2000:]
+
+
+_SCAN_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+from helpers import build_layer
+E, d, f, k, T, res, act, dtype = {args!r}
+layer, _, _ = build_layer(E, d, f, k, dtype, act, "topk_softmax" if k > 1 else "full_softmax", len(res), res,
+                          max_tokens=T)
+td = torch.bfloat16 if dtype == "bf16" else torch.float32
+x = torch.randn(T, d, generator=torch.Generator().manual_seed(5)).to(td).cuda()
+y = layer.forward(x)
+ws = layer.workspace()
+R = int(ws["seg_offsets"][-1].item())
+torch.save(dict(y=y.cpu(), pos=ws["pos"].cpu(), counts=ws["counts"].cpu(), offs=ws["seg_offsets"].cpu(),
+                row_token=ws["row_token"][:R].cpu()), {out!r})
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [(8, 256, 512, 2, 4096, [0, 2, 5, 7], "swiglu", "bf16"),
+                                  (128, 256, 512, 1, 3000, list(range(0, 128, 5)), "relu", "bf16"),
+                                  (8, 256, 512, 2, 700, [1, 2, 3, 4], "swiglu", "fp32"),
+                                  (32, 512, 512, 3, 1, [4, 9], "swiglu", "bf16")])
+def test_small_batch_scan_fold_bit_identical(args, tmp_path):
+    """Up to 32 token blocks the K3a scan runs inside the permute kernel
+    (EMOE_SMALL_SCAN=1, default): counts, padded offsets, positions, row
+    sources and outputs bit-identical to scan_kernel + permute (=0)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    outs = []
+    for flag in ("1", "0"):
+        out = tmp_path / f"s{flag}.pt"
+        code = _SCAN_SCRIPT.format(root=str(root), tests=str(root / "tests"), args=args, out=str(out))
+        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, EMOE_SMALL_SCAN=flag),
+                       timeout=300)
+        outs.append(torch.load(out))
+    for key in outs[0]:
+        assert torch.equal(outs[0][key], outs[1][key]), f"{key} differs between the folded and separate scan"
