@@ -6,8 +6,9 @@
 // that slice in shared memory and folds them into exact 64-bit global tallies
 // (the reference stores the same integers as doubles, predictor.cpp:164-183;
 // counts commute, so block order does not matter).  Dominant experts per
-// (prompt, layer) are reduced on the fly and the prompt-transition tally is a
-// second tiny kernel that also continues the chain across calls.
+// (prompt, layer) are reduced on the fly, and the last block to finish
+// tallies the prompt transitions, continuing the chain across calls (one
+// launch per update).
 //
 // A7/A8 are latency-bound fp64 control logic over m x E numbers.  They run as
 // single-block kernels whose every floating-point expression and summation
